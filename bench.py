@@ -1,0 +1,390 @@
+#!/usr/bin/env python
+"""Benchmark of the sketch hot path (BASELINE.json metric) -- one JSON line.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+Workload (BASELINE.json configs[1], "C2"): A = n x n Gaussian-kernel matrix,
+n = 16384, x_i ~ U[0,1]^8 (seed = rank), h = 0.5, +1e-2 on the diagonal,
+generated in HBM (2.15 GB, far larger than the 126 MB L2, so no flush is
+needed between steps).  One STEP = the SJLT sketch S = A R^T with d = 512,
+alpha = 4 (block construction, R drawn by the reference's generator with
+SeedSequence((0, 0))), i.e. one full pass over A.  `value` is the A-streamed
+GB/s of the whole job (sum over ranks / max-over-ranks time).  The Gaussian
+d = 512 product on the same A (the config's comparison) is reported under
+"gaussian" in FP64 TFLOP/s, next to cuBLAS DGEMM on the same operands.
+
+Multi-GPU (torchrun, one rank per GPU): every rank sketches its own C2
+matrix with the same R -- row-block sharding needs no collective for
+S = A R^T, so this is weak scaling.
+
+--impl reference times the reference algorithm on the host CPU: the C
+restatement in oracle/ (bit-exact with hsskit's SjltBlock.apply_right; the
+reference itself is pure Python/numpy and is not shipped to the GPU box),
+on all host cores, one bounded row slab of the same workload per step.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+N = 16384
+D = 512
+ALPHA = 4
+DIM = 8
+H = 0.5
+METRIC = "sketch S=A·R^T: A-streamed GB/s (SJLT) and FP64 TFLOP/s (Gaussian) vs roofline"
+
+
+def _peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(path) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured"
+    except Exception:  # noqa: BLE001
+        return 6650.0, "fallback"
+
+
+def _traffic_from_profiles(kernel_key: str):
+    """Per-launch DRAM bytes of the kernel from the committed ncu summary."""
+    path = os.path.join(ROOT, "profiles", "ncu_summary.json")
+    try:
+        with open(path) as f:
+            prof = json.load(f)
+        ent = prof["kernels"][kernel_key]
+        return ent["dram_bytes_per_launch"]
+    except Exception:  # noqa: BLE001
+        return None
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled in the background."""
+
+    QUERY = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int, period_ms: int = 50):
+        self.samples = []
+        self.proc = None
+        self.gpu = gpu_index
+        self.period = period_ms
+        self.thread = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.gpu}", f"--query-gpu={self.QUERY}",
+                 "--format=csv,noheader,nounits", f"-lms={self.period}"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:  # noqa: BLE001
+            self.proc = None
+            return self
+        self.thread = threading.Thread(target=self._read, daemon=True)
+        self.thread.start()
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) >= 9:
+                self.samples.append((time.perf_counter(), parts))
+
+    def stop(self):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:  # noqa: BLE001
+                self.proc.kill()
+
+    def summary(self, t0: float, t1: float):
+        win = [p for t, p in self.samples if t0 <= t <= t1]
+        src = "timed_region"
+        if not win:  # timed region shorter than the sampling period
+            near = sorted(self.samples, key=lambda s: min(abs(s[0] - t0), abs(s[0] - t1)))[:3]
+            win = [p for _, p in near]
+            src = "nearest_samples"
+        if not win:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0,
+                    "source": "unavailable"}
+
+        def num(x):
+            try:
+                return float(x)
+            except ValueError:
+                return None
+        sm = [num(p[1]) for p in win if num(p[1]) is not None]
+        reasons = set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for p in win:
+            for name, v in zip(names, p[5:9]):
+                if v.lower().startswith("active"):
+                    reasons.add(name)
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": num(win[0][2]), "reasons": sorted(reasons),
+                "samples": len(win), "source": src}
+
+
+# --------------------------------------------------------------- reference
+
+def host_kernel_slab(rows: int, seed: int = 0) -> np.ndarray:
+    """Rows [0, rows) of the C2 Gaussian-kernel matrix computed on the host."""
+    x = np.random.default_rng(seed).uniform(0.0, 1.0, (N, DIM))
+    out = np.empty((rows, N), order="F")
+    sq = np.sum(x * x, axis=1)
+    for c0 in range(0, N, 2048):
+        c1 = min(N, c0 + 2048)
+        g = x[:rows] @ x[c0:c1].T
+        d2 = np.maximum(sq[:rows, None] + sq[None, c0:c1] - 2.0 * g, 0.0)
+        out[:, c0:c1] = np.exp(-d2 / (2 * H * H))
+    idx = np.arange(rows)
+    out[idx, idx] += 1e-2
+    return out
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    from oracle import oracle as O
+    from paper_2302_01977_b200 import draws
+    threads = os.cpu_count() or 1
+    pos, sg = draws.sjlt_draw(N, D, np.random.SeedSequence((0, 0)), ALPHA, "block")
+    scale = 1.0 / np.sqrt(ALPHA)
+    rows = int(os.environ.get("HSK_REF_ROWS", "2048"))
+    slab = host_kernel_slab(rows)
+    for _ in range(max(args.warmup, 1)):
+        O.sjlt_right(slab, pos, sg, D, scale, nthreads=threads)
+    times = []
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        O.sjlt_right(slab, pos, sg, D, scale, nthreads=threads)
+        times.append(time.perf_counter() - t0)
+    t = statistics.median(times)
+    gbs = slab.nbytes / t / 1e9
+    sample = f"row slab {rows} x {N} of the C2 matrix per step (S rows are independent)"
+    line = {
+        "impl": "reference", "metric": METRIC, "value": gbs, "unit": "GB/s",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": t * 1e3, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": "c2_sjlt_S", "n": N, "d": D, "alpha": ALPHA,
+                   "construction": "block", "rows_per_step": rows},
+        "cpu_baseline": {"value": gbs, "unit": "GB/s", "cores": threads, "kind": "port",
+                         "sample": sample},
+        "e2e": {"value": gbs, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# --------------------------------------------------------------------- ours
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=400)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline leg")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+    if args.impl == "reference":
+        run_reference(args)
+        return
+
+    import torch
+    import torch.distributed as dist
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    from paper_2302_01977_b200 import _lib, device, matgen
+    from paper_2302_01977_b200 import sketching as sk
+    _lib.load()
+
+    stream = torch.cuda.current_stream()
+    sptr = stream.cuda_stream
+    op = sk.new_operator(sk.SJLT, N, D, np.random.SeedSequence((0, 0)), alpha=ALPHA,
+                         construction=sk.BLOCK)
+    blk = op.blocks[0]
+    A = matgen.gaussian_kernel(N, DIM, H, 1e-2, seed=rank)
+    S = device.DeviceMatrix.empty(N, D)
+    device.block_state(blk)
+    torch.cuda.synchronize()
+
+    def sjlt(trans=False, out=S):
+        device.apply_block(blk, A, trans, out, 0, sptr)
+
+    for _ in range(args.warmup):
+        sjlt()
+    torch.cuda.synchronize()
+
+    sampler = ClockSampler(torch.cuda.current_device()).start()
+    time.sleep(0.3)
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+           for _ in range(args.steps)]
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    t_wall0 = time.perf_counter()
+    g0 = torch.cuda.Event(enable_timing=True)
+    g1 = torch.cuda.Event(enable_timing=True)
+    g0.record(stream)
+    for e0, e1 in evs:
+        e0.record(stream)
+        sjlt()
+        e1.record(stream)
+    g1.record(stream)
+    torch.cuda.synchronize()
+    t_wall1 = time.perf_counter()
+    if world > 1:
+        dist.barrier()
+    total_ms = g0.elapsed_time(g1)
+    launch_ms = [a.elapsed_time(b) for a, b in evs]
+    if world > 1:
+        t = torch.tensor([total_ms], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total_ms = float(t.item())
+    time.sleep(0.25)
+    sampler.stop()
+    clocks = sampler.summary(t_wall0, t_wall1)
+
+    ms_per_step = total_ms / args.steps
+    a_bytes = N * N * 8
+    s_bytes = N * D * 8
+    value = world * a_bytes / (ms_per_step * 1e-3) / 1e9
+    avg_launch = statistics.mean(launch_ms)
+    peak, peak_src = _peaks()
+    achieved = (a_bytes + s_bytes) / (avg_launch * 1e-3) / 1e9
+
+    # S' = A^T R^T on the same A (secondary, same algorithmic bytes)
+    St = device.DeviceMatrix.empty(N, D)
+    for _ in range(3):
+        sjlt(True, St)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    reps = max(10, min(args.steps, 100))
+    e0.record(stream)
+    for _ in range(reps):
+        sjlt(True, St)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    st_ms = e0.elapsed_time(e1) / reps
+
+    # Gaussian d=512 on the same A (config's comparison) + cuBLAS DGEMM
+    gop = sk.new_operator(sk.GAUSSIAN, N, D, np.random.SeedSequence((0, 0)))
+    gblk = gop.blocks[0]
+    gst = device.block_state(gblk)
+    SG = device.DeviceMatrix.empty(N, D)
+    for _ in range(2):
+        device.apply_block(gblk, A, False, SG, 0, sptr)
+    greps = 5
+    e0.record(stream)
+    for _ in range(greps):
+        device.apply_block(gblk, A, False, SG, 0, sptr)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    g_ms = e0.elapsed_time(e1) / greps
+    flops = 2.0 * N * N * D
+    At = A.t[:, :N]               # (cols, rows) = A^T as a row-major tensor
+    for _ in range(2):
+        ref_c = torch.matmul(gst.R, At)   # R A^T = (A R^T)^T, cuBLAS DGEMM
+    e0.record(stream)
+    for _ in range(greps):
+        ref_c = torch.matmul(gst.R, At)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    cublas_ms = e0.elapsed_time(e1) / greps
+    del ref_c
+
+    # end to end through the public API: pinned host A -> H2D -> kernel -> D2H S
+    e2e = None
+    if rank == 0 or world > 1:
+        host = torch.empty((N, N), dtype=torch.float64, pin_memory=True)
+        host.copy_(A.t[:, :N])
+        A_host = host.numpy().T           # F-ordered view of the pinned buffer
+        e2e_steps = max(3, min(args.steps, 10))
+        sk.apply_right(A_host, op)
+        torch.cuda.synchronize()
+        e0.record(stream)
+        for _ in range(e2e_steps):
+            S_host = sk.apply_right(A_host, op)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        e2e_ms = e0.elapsed_time(e1) / e2e_steps
+        if world > 1:
+            t = torch.tensor([e2e_ms], device="cuda")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            e2e_ms = float(t.item())
+        e2e = {"value": world * a_bytes / (e2e_ms * 1e-3) / 1e9, "unit": "GB/s",
+               "h2d_bytes_per_step": a_bytes, "d2h_bytes_per_step": int(S_host.nbytes),
+               "ms_per_step": e2e_ms, "path": "sketching.apply_right(pinned host array)"}
+        del host, A_host
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        from oracle import oracle as O
+        threads = os.cpu_count() or 1
+        rows = 2048
+        slab = A.row_view(0, rows).to_host()
+        slab = np.asfortranarray(slab)
+        O.sjlt_right(slab, blk._pos, blk._signs, D, blk._scale, nthreads=threads)
+        ts = []
+        t_start = time.perf_counter()
+        while len(ts) < 3 or (time.perf_counter() - t_start < 10.0 and len(ts) < 50):
+            t0 = time.perf_counter()
+            O.sjlt_right(slab, blk._pos, blk._signs, D, blk._scale, nthreads=threads)
+            ts.append(time.perf_counter() - t0)
+        cpu = {"value": slab.nbytes / statistics.median(ts) / 1e9, "unit": "GB/s",
+               "cores": threads, "kind": "port",
+               "sample": f"oracle SjltBlock.apply_right restatement on a {rows} x {N} row slab "
+                         f"of the same A, median of {len(ts)}"}
+
+    line = {
+        "metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic",
+        "config": {"workload": "c2_sjlt_S", "n": N, "d": D, "alpha": ALPHA,
+                   "construction": "block", "matrix": "gaussian kernel 8-D h=0.5",
+                   "parallelism": f"rowshard{world}", "l2": "inputs larger than L2 (2.15 GB A)"},
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": achieved / peak, "peak_source": peak_src,
+                     "traffic": _traffic_from_profiles("sjlt_apply_S"),
+                     "algorithmic_bytes_per_launch": a_bytes + s_bytes,
+                     "avg_launch_ms": avg_launch},
+        "gpu_launches": args.steps,
+        "clocks": clocks,
+        "e2e": e2e,
+        "cpu_baseline": cpu,
+        "transposed": {"metric": "S'=A^T R^T A-streamed GB/s", "ms": st_ms,
+                       "value": a_bytes / (st_ms * 1e-3) / 1e9,
+                       "frac": (a_bytes + s_bytes) / (st_ms * 1e-3) / 1e9 / peak},
+        "gaussian": {"metric": "FP64 TFLOP/s, S=A R^T d=512 (DMMA)", "ms": g_ms,
+                     "value": flops / (g_ms * 1e-3) / 1e12, "unit": "TFLOP/s",
+                     "cublas_dgemm_ms": cublas_ms,
+                     "cublas_dgemm_tflops": flops / (cublas_ms * 1e-3) / 1e12},
+    }
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,66 @@
+"""Adaptive sketching with append-in-place device buffers.
+
+The reference grows its sketch by drawing a fresh block
+(`append_columns`), sketching only that block against A, and concatenating
+on the host (hss_compress.py:168-182; append-only, earlier
+columns are never recomputed).  DeviceSketch keeps S = A R^T and
+S' = A^T R^T in HBM with capacity d_max columns; each increment launches the
+kernels once for the new block, writing straight into columns
+[d, d + dd) (hsk_*_apply `col0`).  Old columns are neither re-read nor moved.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+
+from . import device as _dev
+from . import sketching as _sk
+
+
+class DeviceSketch:
+    def __init__(self, A, n_cols_max: int, *, right: bool = True, transposed: bool = True):
+        self.A = _sk.device_matrix_of(A)
+        self.capacity = int(n_cols_max)
+        self.d = 0
+        self.op = None
+        self.S = _dev.DeviceMatrix.empty(self.A.rows, self.capacity) if right else None
+        self.St = _dev.DeviceMatrix.empty(self.A.cols, self.capacity) if transposed else None
+
+    def _sketch_block(self, blk):
+        if self.d + blk.rows > self.capacity:
+            raise ValueError(f"sketch capacity {self.capacity} exceeded "
+                             f"(d={self.d}, block rows={blk.rows})")
+        if self.S is not None:
+            _dev.apply_block(blk, self.A, False, self.S, self.d)
+        if self.St is not None:
+            _dev.apply_block(blk, self.A, True, self.St, self.d)
+        self.d += blk.rows
+
+    def start(self, op) -> "DeviceSketch":
+        """Sketch every block of a fresh operator (init_sketch)."""
+        if self.S is not None and op.n != self.A.cols:
+            raise ValueError("operator dimension does not match A's columns")
+        if self.St is not None and op.n != self.A.rows:
+            raise ValueError("operator dimension does not match A's rows")
+        self.d = 0
+        for blk in op.blocks:
+            self._sketch_block(blk)
+        self.op = op
+        return self
+
+    def extend(self, op) -> "DeviceSketch":
+        """Sketch only the blocks op has beyond the current operator
+        (extend_sketch after append_columns)."""
+        known = 0 if self.op is None else len(self.op.blocks)
+        if self.op is not None and tuple(op.blocks[:known]) != tuple(self.op.blocks):
+            raise ValueError("operator is not an extension of the sketched one")
+        for blk in op.blocks[known:]:
+            self._sketch_block(blk)
+        self.op = op
+        return self
+
+    def right(self) -> np.ndarray:
+        return self.S.to_host(0, self.d)
+
+    def transposed(self) -> np.ndarray:
+        return self.St.to_host(0, self.d)

@@ -1,0 +1,212 @@
+// hsk_gauss.cu -- Gaussian sketch S = A R^T / S' = A^T R^T as an FP64
+// tensor-core contraction on sm_100a.
+//
+// Replaces GaussianBlock.apply_right (buf @ matrix.T) and
+// apply_right_transposed ((matrix @ buf).T), sketching.py:134-138.
+//
+// tcgen05.mma has no f64 kind, so the FP64 tensor path on sm_100a is the
+// warp-level mma.sync.m8n8k4.f64 (SASS DMMA.8x8x4).  CTA tile BM x BN with
+// BK = 16 k-steps staged by a STAGES-deep cp.async ring; 8 warps, each a
+// (BM/2) x (BN/4) register tile of 8x8 DMMA fragments.  Shared-memory pitches
+// are chosen so every fragment load is two conflict-free wavefronts
+// (DESIGN.md §Gaussian).  R is the reference's d x n row-major `matrix`,
+// i.e. R^T column-major with leading dimension n.
+#include <algorithm>
+
+#include "hsk_common.cuh"
+
+namespace hsk {
+namespace gauss {
+
+constexpr int BK = 16;
+constexpr int STAGES = 3;
+constexpr int PKK = BK + 4;  // pitch of k-contiguous tiles (== 4 mod 16)
+
+struct Args {
+    const double *A;
+    int64_t lda;
+    const double *R;
+    int64_t M, N, K;
+    double *S;
+    int64_t lds, col0;
+    int a16, b16;  // 16-byte cp.async allowed
+    int ntiles_n;
+};
+
+__device__ __forceinline__ void dmma(double (&c)[2], double a, double b) {
+    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+                 : "+d"(c[0]), "+d"(c[1])
+                 : "d"(a), "d"(b));
+}
+
+// copy the two doubles src[0..1] (valid0/valid1) to dst, 16B if allowed
+__device__ __forceinline__ void copy2(double *dst, const double *src, bool v0, bool v1,
+                                      bool vec16) {
+    if (vec16 && v0 && v1) {
+        cp_async16(dst, src, true);
+    } else {
+        cp_async8(dst, v0 ? src : dst, v0);
+        cp_async8(dst + 1, v1 ? src + 1 : dst, v1);
+    }
+}
+
+template <int BM, int BN, int TRANS>
+struct Smem {
+    static constexpr int PA = TRANS ? PKK : BM + 8;  // trans0: [BK][BM+8], BM+8 == 8 mod 16
+    static constexpr int A_ELEMS = TRANS ? BM * PKK : BK * (BM + 8);
+    static constexpr int B_ELEMS = BN * PKK;
+    static constexpr int STAGE = A_ELEMS + B_ELEMS;
+    static constexpr int BYTES = STAGES * STAGE * 8;
+};
+
+template <int BM, int BN, int TRANS>
+__global__ void __launch_bounds__(256) gauss_kernel(const Args p) {
+    using SM = Smem<BM, BN, TRANS>;
+    constexpr int WM = BM / 2, WN = BN / 4;
+    constexpr int MF = WM / 8, NF = WN / 8;
+    extern __shared__ __align__(128) double sm[];
+
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int64_t nt = blockIdx.x % p.ntiles_n, mt = blockIdx.x / p.ntiles_n;
+    const int64_t m0 = mt * BM, n0 = nt * BN;
+    const int wm0 = (warp >> 2) * WM, wn0 = (warp & 3) * WN;
+    const int64_t ktiles = (p.K + BK - 1) / BK;
+
+    auto load_stage = [&](int64_t kt, int s) {
+        double *sA = sm + s * SM::STAGE;
+        double *sB = sA + SM::A_ELEMS;
+        const int64_t k0 = kt * BK;
+        if (!TRANS) {
+            // A(m,k) = A[k*lda + m]: BK columns of BM contiguous rows
+            for (int q = tid; q < BK * (BM / 2); q += 256) {
+                const int kk = q / (BM / 2), mm = (q % (BM / 2)) * 2;
+                const int64_t gm = m0 + mm, gk = k0 + kk;
+                const bool vk = gk < p.K;
+                const double *src = p.A + gk * p.lda + gm;
+                copy2(sA + kk * SM::PA + mm, src, vk && gm < p.M, vk && gm + 1 < p.M, p.a16);
+            }
+        } else {
+            // A^T(m,k) = A[m*lda + k]: BM rows of BK contiguous k
+            for (int q = tid; q < BM * (BK / 2); q += 256) {
+                const int mm = q / (BK / 2), kk = (q % (BK / 2)) * 2;
+                const int64_t gm = m0 + mm, gk = k0 + kk;
+                const bool vm = gm < p.M;
+                const double *src = p.A + gm * p.lda + gk;
+                copy2(sA + mm * PKK + kk, src, vm && gk < p.K, vm && gk + 1 < p.K, p.a16);
+            }
+        }
+        // B(k,j) = R[j*K + k]
+        for (int q = tid; q < BN * (BK / 2); q += 256) {
+            const int jj = q / (BK / 2), kk = (q % (BK / 2)) * 2;
+            const int64_t gj = n0 + jj, gk = k0 + kk;
+            const bool vj = gj < p.N;
+            const double *src = p.R + gj * p.K + gk;
+            copy2(sB + jj * PKK + kk, src, vj && gk < p.K, vj && gk + 1 < p.K, p.b16);
+        }
+    };
+
+    double acc[MF][NF][2];
+#pragma unroll
+    for (int i = 0; i < MF; ++i)
+#pragma unroll
+        for (int j = 0; j < NF; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+
+#pragma unroll
+    for (int s = 0; s < STAGES - 1; ++s) {
+        if (s < ktiles) load_stage(s, s);
+        cp_async_commit();
+    }
+    for (int64_t kt = 0; kt < ktiles; ++kt) {
+        cp_async_wait<STAGES - 2>();
+        __syncthreads();
+        {
+            const int64_t nk = kt + STAGES - 1;
+            if (nk < ktiles) load_stage(nk, (int)(nk % STAGES));
+            cp_async_commit();
+        }
+        const double *sA = sm + (kt % STAGES) * SM::STAGE;
+        const double *sB = sA + SM::A_ELEMS;
+        const int fr = lane >> 2, fc = lane & 3;
+#pragma unroll
+        for (int k4 = 0; k4 < BK; k4 += 4) {
+            double a[MF], b[NF];
+#pragma unroll
+            for (int i = 0; i < MF; ++i) {
+                const int m = wm0 + i * 8 + fr;
+                a[i] = TRANS ? sA[m * PKK + k4 + fc] : sA[(k4 + fc) * SM::PA + m];
+            }
+#pragma unroll
+            for (int j = 0; j < NF; ++j) b[j] = sB[(wn0 + j * 8 + fr) * PKK + k4 + fc];
+#pragma unroll
+            for (int i = 0; i < MF; ++i)
+#pragma unroll
+                for (int j = 0; j < NF; ++j) dmma(acc[i][j], a[i], b[j]);
+        }
+    }
+    cp_async_wait<0>();
+
+    const int fr = lane >> 2, fc = lane & 3;
+#pragma unroll
+    for (int i = 0; i < MF; ++i) {
+        const int64_t m = m0 + wm0 + i * 8 + fr;
+        if (m >= p.M) continue;
+#pragma unroll
+        for (int j = 0; j < NF; ++j) {
+            const int64_t c = n0 + wn0 + j * 8 + 2 * fc;
+            if (c < p.N) p.S[(p.col0 + c) * p.lds + m] = acc[i][j][0];
+            if (c + 1 < p.N) p.S[(p.col0 + c + 1) * p.lds + m] = acc[i][j][1];
+        }
+    }
+}
+
+template <int BM, int BN, int TRANS>
+static int launch(Args a, cudaStream_t st) {
+    using SM = Smem<BM, BN, TRANS>;
+    auto kern = gauss_kernel<BM, BN, TRANS>;
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SM::BYTES);
+    if (e != cudaSuccess) return cuda_status(e, "gauss: set smem attribute");
+    a.ntiles_n = (int)((a.N + BN - 1) / BN);
+    const int64_t grid = ((a.M + BM - 1) / BM) * a.ntiles_n;
+    HSK_REQUIRE(grid < (1ll << 31), HSK_EINVAL, "gauss: grid too large");
+    kern<<<(unsigned)grid, 256, SM::BYTES, st>>>(a);
+    HSK_CHECK_LAUNCH("gauss_kernel");
+    return HSK_OK;
+}
+
+}  // namespace gauss
+}  // namespace hsk
+
+using namespace hsk;
+
+extern "C" int hsk_gauss_apply(const double *A, int64_t rows, int64_t cols, int64_t lda,
+                               int32_t trans, const double *R, int64_t n, int32_t d, double *S,
+                               int64_t lds, int64_t col0, void *stream) {
+    HSK_REQUIRE(trans == 0 || trans == 1, HSK_EINVAL, "gauss apply: trans must be 0 or 1");
+    HSK_REQUIRE(rows >= 0 && cols >= 0 && lda >= std::max<int64_t>(rows, 1), HSK_EINVAL,
+                "gauss apply: bad A shape");
+    HSK_REQUIRE(d >= 1, HSK_EINVAL, "gauss apply: d must be >= 1");
+    const int64_t kdim = trans ? rows : cols;
+    const int64_t m_out = trans ? cols : rows;
+    if (kdim != n) {
+        return set_error(HSK_EINVAL, "operator is over dimension %lld, matrix has %lld %s",
+                         (long long)n, (long long)kdim, trans ? "rows" : "columns");
+    }
+    HSK_REQUIRE(lds >= std::max<int64_t>(m_out, 1) && col0 >= 0, HSK_EINVAL,
+                "gauss apply: bad output lds/col0");
+    if (m_out == 0) return HSK_OK;
+    HSK_REQUIRE(S && R && (A || n == 0), HSK_EINVAL, "gauss apply: null pointer");
+    gauss::Args a{};
+    a.A = A;
+    a.lda = lda;
+    a.R = R;
+    a.M = m_out;
+    a.N = d;
+    a.K = n;
+    a.S = S;
+    a.lds = lds;
+    a.col0 = col0;
+    a.a16 = ((reinterpret_cast<uintptr_t>(A) & 15) == 0) && (lda % 2 == 0);
+    a.b16 = ((reinterpret_cast<uintptr_t>(R) & 15) == 0) && (n % 2 == 0);
+    cudaStream_t st = as_stream(stream);
+    return trans ? gauss::launch<128, 128, 1>(a, st) : gauss::launch<128, 128, 0>(a, st);
+}

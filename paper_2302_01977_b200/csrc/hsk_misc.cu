@@ -1,0 +1,169 @@
+// hsk_misc.cu -- C-ABI plumbing (errors, device info), synthetic matrix
+// generators for the BASELINE.json configs, and the L2 flush used between
+// timed launches.
+#include <math.h>
+#include <stdarg.h>
+#include <string.h>
+
+#include <algorithm>
+
+#include "hsk_common.cuh"
+
+namespace hsk {
+
+static thread_local char g_err[512] = "";
+
+int set_error(int code, const char *fmt, ...) {
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(g_err, sizeof(g_err), fmt, ap);
+    va_end(ap);
+    return code;
+}
+
+int cuda_status(cudaError_t e, const char *what) {
+    return set_error(e == cudaErrorNoDevice || e == cudaErrorInsufficientDriver ? HSK_ENODEV
+                                                                                 : HSK_ECUDA,
+                     "%s: %s", what, cudaGetErrorString(e));
+}
+
+int sm_count() {
+    static int cached = 0;
+    if (!cached) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&cached, cudaDevAttrMultiProcessorCount, dev);
+        if (cached <= 0) cached = 148;
+    }
+    return cached;
+}
+
+// A_ij = exp(-|x_i - x_j|^2 / (2 h^2)) + diag*(i==j); thread per element,
+// consecutive threads along the column (contiguous) dimension.
+__global__ void gen_gauss_kernel(const double *__restrict__ pts, int64_t n, int dim,
+                                 double inv2h2, double diag, int64_t row0, int64_t nrows,
+                                 int64_t col0, int64_t ncols, double *__restrict__ A,
+                                 int64_t lda) {
+    const int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    const int64_t c = blockIdx.y;
+    if (r >= nrows) return;
+    for (int64_t cc = c; cc < ncols; cc += gridDim.y) {
+        const int64_t i = row0 + r, j = col0 + cc;
+        const double *xi = pts + i * dim, *xj = pts + j * dim;
+        double s = 0.0;
+        for (int q = 0; q < dim; ++q) {
+            const double t = xi[q] - xj[q];
+            s += t * t;
+        }
+        double v = exp(-s * inv2h2);
+        if (i == j) v += diag;
+        A[cc * lda + r] = v;
+    }
+}
+
+// A_ij = 1/(1+|i-j|) + 0.1 sin(i+2j)/n
+__global__ void gen_toeplitz_sin_kernel(int64_t n, int64_t row0, int64_t nrows, int64_t col0,
+                                        int64_t ncols, double *__restrict__ A, int64_t lda) {
+    const int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (r >= nrows) return;
+    for (int64_t cc = blockIdx.y; cc < ncols; cc += gridDim.y) {
+        const int64_t i = row0 + r, j = col0 + cc;
+        const int64_t dd = i > j ? i - j : j - i;
+        A[cc * lda + r] = 1.0 / (1.0 + (double)dd) + 0.1 * sin((double)(i + 2 * j)) / (double)n;
+    }
+}
+
+__global__ void l2_flush_kernel(double4 *p, int64_t n4, double v) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n4;
+         i += (int64_t)gridDim.x * blockDim.x)
+        p[i] = make_double4(v, v, v, v);
+}
+
+}  // namespace hsk
+
+using namespace hsk;
+
+extern "C" int hsk_abi_version(void) { return HSK_ABI_VERSION; }
+
+extern "C" int hsk_last_error(char *buf, size_t len) {
+    const int n = (int)strlen(g_err);
+    if (buf && len) {
+        strncpy(buf, g_err, len - 1);
+        buf[len - 1] = '\0';
+    }
+    return n;
+}
+
+extern "C" int hsk_device_info(int *sms, int *major, int *minor, int64_t *l2) {
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return cuda_status(e, "cudaGetDevice");
+    int v = 0;
+    if (sms) {
+        cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+        *sms = v;
+    }
+    if (major) {
+        cudaDeviceGetAttribute(&v, cudaDevAttrComputeCapabilityMajor, dev);
+        *major = v;
+    }
+    if (minor) {
+        cudaDeviceGetAttribute(&v, cudaDevAttrComputeCapabilityMinor, dev);
+        *minor = v;
+    }
+    if (l2) {
+        cudaDeviceGetAttribute(&v, cudaDevAttrL2CacheSize, dev);
+        *l2 = v;
+    }
+    return HSK_OK;
+}
+
+static int gen_grid(int64_t nrows, int64_t ncols, dim3 &grid) {
+    const int64_t bx = (nrows + 255) / 256;
+    HSK_REQUIRE(bx < (1ll << 31), HSK_EINVAL, "generator: too many rows");
+    grid = dim3((unsigned)bx, (unsigned)std::min<int64_t>(std::max<int64_t>(ncols, 1), 65535), 1);
+    return HSK_OK;
+}
+
+extern "C" int hsk_gen_gauss_kernel(const double *pts, int64_t n, int32_t dim, double h,
+                                    double diag, int64_t row0, int64_t nrows, int64_t col0,
+                                    int64_t ncols, double *A, int64_t lda, void *stream) {
+    HSK_REQUIRE(n >= 0 && dim >= 1 && h > 0, HSK_EINVAL, "gen_gauss_kernel: bad n/dim/h");
+    HSK_REQUIRE(row0 >= 0 && nrows >= 0 && row0 + nrows <= n && col0 >= 0 && ncols >= 0 &&
+                    col0 + ncols <= n && lda >= std::max<int64_t>(nrows, 1),
+                HSK_EINVAL, "gen_gauss_kernel: bad block");
+    if (nrows == 0 || ncols == 0) return HSK_OK;
+    dim3 grid;
+    int rc = gen_grid(nrows, ncols, grid);
+    if (rc) return rc;
+    gen_gauss_kernel<<<grid, 256, 0, as_stream(stream)>>>(pts, n, dim, 1.0 / (2.0 * h * h), diag,
+                                                          row0, nrows, col0, ncols, A, lda);
+    HSK_CHECK_LAUNCH("gen_gauss_kernel");
+    return HSK_OK;
+}
+
+extern "C" int hsk_gen_toeplitz_sin(int64_t n, int64_t row0, int64_t nrows, int64_t col0,
+                                    int64_t ncols, double *A, int64_t lda, void *stream) {
+    HSK_REQUIRE(n >= 0 && row0 >= 0 && nrows >= 0 && row0 + nrows <= n && col0 >= 0 &&
+                    ncols >= 0 && col0 + ncols <= n && lda >= std::max<int64_t>(nrows, 1),
+                HSK_EINVAL, "gen_toeplitz_sin: bad block");
+    if (nrows == 0 || ncols == 0) return HSK_OK;
+    dim3 grid;
+    int rc = gen_grid(nrows, ncols, grid);
+    if (rc) return rc;
+    gen_toeplitz_sin_kernel<<<grid, 256, 0, as_stream(stream)>>>(n, row0, nrows, col0, ncols, A,
+                                                                 lda);
+    HSK_CHECK_LAUNCH("gen_toeplitz_sin_kernel");
+    return HSK_OK;
+}
+
+extern "C" int hsk_l2_flush(void *scratch, int64_t bytes, void *stream) {
+    HSK_REQUIRE(scratch && bytes >= 32 && (reinterpret_cast<uintptr_t>(scratch) & 31) == 0,
+                HSK_EINVAL, "l2_flush: need a 32-byte aligned scratch buffer");
+    static double v = 0.0;
+    v += 1.0;
+    l2_flush_kernel<<<sm_count() * 4, 256, 0, as_stream(stream)>>>(
+        static_cast<double4 *>(scratch), bytes / 32, v);
+    HSK_CHECK_LAUNCH("l2_flush_kernel");
+    return HSK_OK;
+}

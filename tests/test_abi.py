@@ -1,0 +1,81 @@
+"""The C-ABI library loads and exports every symbol include/hsk.h declares.
+
+CPU-only: no compute calls that need a device.  The entry points validate
+their arguments on the host before touching CUDA, so the reference's error
+behaviour (ValueError on shape mismatch) is checked here too.
+"""
+
+import ctypes
+import os
+import re
+
+import pytest
+
+from paper_2302_01977_b200 import _lib
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _declared():
+    with open(os.path.join(ROOT, "include", "hsk.h")) as f:
+        text = f.read()
+    return sorted(set(re.findall(r"\b(hsk_[a-z0-9_]+)\s*\(", text)))
+
+
+def test_header_and_binding_agree():
+    assert _declared() == sorted(_lib.exported_symbols())
+
+
+def test_library_exports_every_declared_symbol():
+    lib = _lib.load()
+    for name in _declared():
+        assert hasattr(lib, name), name
+    assert lib.hsk_abi_version() == 1
+
+
+def test_library_is_sm100a():
+    import subprocess
+    out = subprocess.run(["cuobjdump", "--list-elf", _lib.LIB_PATH], capture_output=True, text=True)
+    if out.returncode != 0:
+        pytest.skip("cuobjdump unavailable")
+    assert "sm_100a" in out.stdout
+
+
+def test_plan_bytes_is_host_only_and_validates():
+    lib = _lib.load()
+    b1 = lib.hsk_sjlt_plan_bytes(4096, 256, 4)
+    b2 = lib.hsk_sjlt_plan_bytes(8192, 256, 4)
+    assert 0 < b1 < b2
+    assert lib.hsk_sjlt_plan_bytes(4096, 0, 4) == _lib.HSK_EINVAL
+    assert lib.hsk_sjlt_plan_bytes(4096, 256, 0) == _lib.HSK_EINVAL
+
+
+def test_apply_dimension_mismatch_is_einval():
+    lib = _lib.load()
+    # S = A R^T needs cols == n: 10 columns vs an operator over 12
+    rc = lib.hsk_sjlt_apply(None, 5, 10, 5, 0, None, 12, 4, 2, 0.5, None, 5, 0, None)
+    assert rc == _lib.HSK_EINVAL
+    assert "operator is over dimension 12" in _lib.last_error()
+    with pytest.raises(ValueError):
+        _lib.check(rc)
+    rc = lib.hsk_gauss_apply(None, 9, 3, 9, 1, None, 8, 4, None, 3, 0, None)
+    assert rc == _lib.HSK_EINVAL
+    rc = lib.hsk_srht_apply(None, 4, 6, 4, 0, None, 6, 6, None, 2, 1.0, None, 4, 0, None)
+    assert rc == _lib.HSK_EINVAL  # n_pad not a power of two
+    rc = lib.hsk_fwht(None, 1, 6, 1, None)
+    assert rc == _lib.HSK_EINVAL
+
+
+def test_bad_trans_and_lda_rejected():
+    lib = _lib.load()
+    assert lib.hsk_sjlt_apply(None, 4, 4, 4, 2, None, 4, 4, 2, 0.5, None, 4, 0, None) == _lib.HSK_EINVAL
+    assert lib.hsk_gauss_apply(None, 4, 4, 3, 0, None, 4, 4, None, 4, 0, None) == _lib.HSK_EINVAL
+
+
+def test_oracle_library_exports():
+    from oracle import oracle as O
+    lib = O.lib()
+    for name in ("oracle_sjlt_right", "oracle_sjlt_right_t", "oracle_srht", "oracle_gauss",
+                 "oracle_fwht", "oracle_reduceat_segment"):
+        assert hasattr(lib, name)
+    assert isinstance(lib, ctypes.CDLL)

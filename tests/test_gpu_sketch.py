@@ -1,0 +1,233 @@
+"""GPU parity: libhsk kernels through the public API vs reference + oracle.
+
+Tolerances (BASELINE.json north_star): the sketch must match the reference's
+on the same inputs and the same R within 1e-12 relative Frobenius (fp64);
+the reference's own kernel tests use max|diff| <= 1e-12..1e-14 * ||A||_F
+(test_sketching.py:53-131, test_acceptance.py:66-93), asserted here too.
+R is bit-exact by construction (tests/test_operator_draws.py).
+"""
+
+import math
+
+import numpy as np
+import pytest
+
+from conftest import case_inputs, seed_of
+from oracle import oracle as O
+from paper_2302_01977_b200 import adaptive, device
+from paper_2302_01977_b200 import sketching as sk
+
+pytestmark = pytest.mark.gpu
+
+REL = 1e-12
+
+
+def _op(case):
+    kw = dict(alpha=case["alpha"], construction=case["construction"]) if case["kind"] == "sjlt" else {}
+    (r0, s0), *rest = case["blocks"]
+    op = sk.new_operator(case["kind"], case["n"], r0, seed_of(s0), **kw)
+    for rows, s in rest:
+        op = sk.append_columns(op, rows, seed_of(s))
+    return op
+
+
+def _close(x, ref, scale_norm, rel=REL):
+    assert x.shape == ref.shape
+    assert O.rel_frobenius(x, ref) <= rel
+    assert np.max(np.abs(x - ref), initial=0.0) <= 1e-12 * scale_norm
+
+
+def test_golden_cases(golden, cuda):
+    arrays, man = golden
+    for case in man["cases"]:
+        op = _op(case)
+        A, B = case_inputs(case)
+        S = sk.apply_right(A, op)
+        St = sk.apply_right_transposed(B, op)
+        assert S.flags.f_contiguous and St.flags.f_contiguous
+        _close(S, arrays[case["name"] + "/S"], np.linalg.norm(A))
+        _close(St, arrays[case["name"] + "/St"], np.linalg.norm(B))
+
+
+def test_worked_pattern_and_trailing_empty(golden, cuda):
+    arrays, man = golden
+    w = man["patterns"][0]
+    blk = sk.SjltBlock.from_pattern(4, 3, 2, w["pos"], w["signs"])
+    A = np.random.default_rng(w["data_seed"]).standard_normal((5, 4))
+    np.testing.assert_allclose(blk.apply_right(np.asfortranarray(A)),
+                               arrays["worked_pattern/S"], atol=1e-14)
+    np.testing.assert_allclose(blk.apply_right_transposed(np.asfortranarray(A.T)),
+                               arrays["worked_pattern/St"], atol=1e-14)
+    e = man["patterns"][1]
+    blk = sk.SjltBlock.from_pattern(2, 3, 1, e["pos"], e["signs"])
+    Ae = np.arange(6.0).reshape(2, 3)
+    np.testing.assert_array_equal(blk.apply_right_transposed(np.asfortranarray(Ae)),
+                                  arrays["trailing_empty/St"])
+
+
+def test_acceptance_criterion_2(cuda):
+    """Reference acceptance 2 (test_acceptance.py:66-93) through the GPU."""
+    rng = np.random.default_rng(2024)
+    for trial in range(100):
+        m = int(rng.integers(8, 65))
+        n = int(rng.integers(8, 65))
+        A = rng.standard_normal((m, n))
+        tol = 1e-12 * np.linalg.norm(A)
+        alpha = (1, 2, 4)[trial % 3]
+        for cons in (sk.BLOCK, sk.GRAPH):
+            if cons == sk.BLOCK:
+                d_r = alpha * int(rng.integers(1, min(32, n) // alpha + 1))
+                d_l = alpha * int(rng.integers(1, min(32, m) // alpha + 1))
+            else:
+                d_r = int(rng.integers(alpha, min(32, n) + 1))
+                d_l = int(rng.integers(alpha, min(32, m) + 1))
+            op_r = sk.new_operator(sk.SJLT, n, d_r, seed=(2, trial), alpha=alpha, construction=cons)
+            Rt = sk.dense_rows(op_r, np.arange(n), np.arange(d_r))
+            assert np.max(np.abs(sk.apply_right(A, op_r) - A @ Rt)) <= tol
+            op_l = sk.new_operator(sk.SJLT, m, d_l, seed=(3, trial), alpha=alpha, construction=cons)
+            Lt = sk.dense_rows(op_l, np.arange(m), np.arange(d_l))
+            assert np.max(np.abs(sk.apply_right_transposed(A, op_l) - A.T @ Lt)) <= tol
+
+
+@pytest.mark.parametrize("m,n,d,alpha,cons", [
+    (1, 64, 8, 2, "graph"), (31, 100, 3, 1, "graph"), (33, 129, 63, 3, "graph"),
+    (64, 64, 64, 8, "block"), (65, 300, 65, 5, "graph"), (127, 1000, 128, 4, "block"),
+    (129, 517, 200, 8, "graph"), (200, 2048, 256, 4, "graph"), (333, 1500, 300, 4, "block"),
+    (96, 4096, 512, 8, "block"), (70, 3000, 513, 3, "graph"), (40, 5000, 2048, 8, "block"),
+    (50, 700, 600, 33, "graph"), (20, 400, 300, 100, "graph"),
+])
+def test_sjlt_shapes_vs_oracle(cuda, m, n, d, alpha, cons):
+    rng = np.random.default_rng(m * 1000 + d)
+    op = sk.new_operator(sk.SJLT, n, d, seed=(m, n, d), alpha=alpha, construction=cons)
+    b = op.blocks[0]
+    A = rng.standard_normal((m, n))
+    ref = O.sjlt_right(A, b._pos, b._signs, d, b._scale)
+    _close(sk.apply_right(A, op), ref, np.linalg.norm(A))
+    B = rng.standard_normal((n, m))
+    ref_t = O.sjlt_right_t(B, b._pos, b._signs, d, b._scale)
+    _close(sk.apply_right_transposed(B, op), ref_t, np.linalg.norm(B))
+
+
+def test_odd_leading_dimension_and_column_offset(cuda):
+    rng = np.random.default_rng(5)
+    m, n, d = 77, 333, 96
+    A = rng.standard_normal((m, n))
+    for kind, kw in ((sk.SJLT, dict(alpha=4, construction=sk.GRAPH)), (sk.GAUSSIAN, {}),
+                     (sk.SRHT, {})):
+        op = sk.new_operator(kind, n, d, seed=7, **kw)
+        ref = O.apply_right(A, op)
+        dA = device.DeviceMatrix(m, n, ld=m)          # odd ld: unaligned columns
+        dA.upload(A)
+        out = device.DeviceMatrix.zeros(m, d + 10, ld=m + 3)
+        sk.apply_right_device(dA, op, out=out, col0=5)
+        got = out.to_host()
+        _close(got[:, 5:5 + d], ref, np.linalg.norm(A))
+        assert np.all(got[:, :5] == 0) and np.all(got[:, 5 + d:] == 0)
+        B = rng.standard_normal((n, m))
+        dB = device.DeviceMatrix(n, m, ld=n + 1)
+        dB.upload(B)
+        ref_t = O.apply_right_transposed(B, op)
+        _close(sk.apply_right_transposed_device(dB, op).to_host(), ref_t, np.linalg.norm(B))
+
+
+def test_results_are_deterministic(cuda):
+    rng = np.random.default_rng(9)
+    A = rng.standard_normal((1000, 2000))
+    for kind, kw in ((sk.SJLT, dict(alpha=8, construction=sk.BLOCK)), (sk.GAUSSIAN, {}),
+                     (sk.SRHT, {})):
+        op = sk.new_operator(kind, 2000, 256, seed=1, **kw)
+        acc = sk.DenseAccessor(A)
+        s1 = sk.apply_right(acc, op)
+        s2 = sk.apply_right(acc, op)
+        np.testing.assert_array_equal(s1, s2)
+        t1 = sk.apply_right_transposed(acc, sk.new_operator(kind, 1000, 128, seed=2, **kw))
+        t2 = sk.apply_right_transposed(acc, sk.new_operator(kind, 1000, 128, seed=2, **kw))
+        np.testing.assert_array_equal(t1, t2)
+
+
+def test_symmetric_sides_and_zero_matrix(cuda):
+    rng = np.random.default_rng(6)
+    Bm = rng.standard_normal((300, 300))
+    A = Bm + Bm.T
+    op = sk.new_operator(sk.SJLT, 300, 40, seed=3, alpha=2, construction=sk.GRAPH)
+    np.testing.assert_allclose(sk.apply_right(A, op), sk.apply_right_transposed(A, op), atol=1e-12)
+    for kind, kw in ((sk.SRHT, {}), (sk.SJLT, dict(alpha=3)), (sk.GAUSSIAN, {})):
+        op = sk.new_operator(kind, 12, 4, seed=0, **kw) if kind != sk.SJLT else \
+            sk.new_operator(kind, 12, 6, seed=0, **kw)
+        np.testing.assert_array_equal(sk.apply_right(np.zeros((5, 12)), op), 0.0)
+
+
+def test_accessor_equivalence_and_device_cache(cuda):
+    rng = np.random.default_rng(7)
+    A = rng.standard_normal((60, 180))
+    op = sk.new_operator(sk.GAUSSIAN, 180, 16, seed=8)
+    acc = sk.DenseAccessor(A)
+    np.testing.assert_array_equal(sk.apply_right(acc, op), sk.apply_right(A, op))
+    d1 = sk.device_matrix_of(acc)
+    d2 = sk.device_matrix_of(acc)
+    assert d1 is d2  # uploaded once (dense() contract)
+
+
+def test_gaussian_vs_oracle(cuda):
+    rng = np.random.default_rng(12)
+    for m, n, d in ((1, 7, 1), (130, 257, 129), (300, 2048, 512), (513, 1000, 64)):
+        A = rng.standard_normal((m, n))
+        op = sk.new_operator(sk.GAUSSIAN, n, d, seed=m)
+        _close(sk.apply_right(A, op), O.apply_right(A, op), np.linalg.norm(A))
+        B = rng.standard_normal((n, m))
+        _close(sk.apply_right_transposed(B, op), O.apply_right_transposed(B, op),
+               np.linalg.norm(B))
+
+
+def test_srht_vs_oracle(cuda):
+    rng = np.random.default_rng(13)
+    for m, n, d in ((3, 1, 1), (40, 100, 24), (33, 256, 64), (65, 1000, 100), (64, 4096, 512),
+                    (17, 5000, 300), (32, 70000, 64)):
+        A = rng.standard_normal((m, n))
+        op = sk.new_operator(sk.SRHT, n, d, seed=n)
+        _close(sk.apply_right(A, op), O.apply_right(A, op), np.linalg.norm(A))
+        if n <= 5000:
+            B = rng.standard_normal((n, m))
+            _close(sk.apply_right_transposed(B, op), O.apply_right_transposed(B, op),
+                   np.linalg.norm(B))
+
+
+def test_srht_duplicate_samples(cuda):
+    op = sk.new_operator(sk.SRHT, 64, 60, seed=4)
+    sample = op.blocks[0].sample
+    assert len(np.unique(sample)) < len(sample)  # drawn with replacement
+    A = np.random.default_rng(1).standard_normal((10, 64))
+    S = sk.apply_right(A, op)
+    for t in range(60):
+        for u in range(60):
+            if sample[t] == sample[u]:
+                np.testing.assert_array_equal(S[:, t], S[:, u])
+
+
+def test_fwht_gpu_known_answers(golden, cuda):
+    arrays, _ = golden
+    np.testing.assert_allclose(sk.fwht([1.0, 1.0, 1.0, 1.0]), arrays["fwht/const4"], atol=0)
+    X = np.random.default_rng(1).standard_normal((3, 16))
+    np.testing.assert_allclose(sk.fwht(X), arrays["fwht/rows16"], atol=1e-14)
+    H = sk.fwht(np.eye(64))
+    np.testing.assert_allclose(H.T @ H, np.eye(64), atol=1e-12)
+    with pytest.raises(ValueError):
+        sk.fwht(np.ones(6))
+
+
+def test_adaptive_append_matches_one_shot(cuda):
+    rng = np.random.default_rng(21)
+    n = 1500
+    A = rng.standard_normal((n, n))
+    for kind, kw in ((sk.SJLT, dict(alpha=8, construction=sk.BLOCK)), (sk.GAUSSIAN, {}),
+                     (sk.SRHT, {})):
+        op = sk.new_operator(kind, n, 128, seed=(0, 0), **kw)
+        ds = adaptive.DeviceSketch(sk.DenseAccessor(A), 128 + 5 * 64).start(op)
+        for r in range(1, 6):
+            op = sk.append_columns(op, 64, seed=(0, r))
+            ds.extend(op)
+        assert ds.d == op.d
+        _close(ds.right(), O.apply_right(A, op), np.linalg.norm(A))
+        _close(ds.transposed(), O.apply_right_transposed(A, op), np.linalg.norm(A))
+        # the one-shot API gives the identical bytes (same kernels, same order)
+        np.testing.assert_array_equal(ds.right(), sk.apply_right(A, op))
