@@ -3,6 +3,7 @@
 // cp.async.bulk (TMA bulk copy engine) and cp.async.
 #pragma once
 
+#include <cuda.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 #include <stdio.h>
@@ -29,6 +30,12 @@ int cuda_status(cudaError_t e, const char *what);
 int sm_count();
 
 inline cudaStream_t as_stream(void *s) { return reinterpret_cast<cudaStream_t>(s); }
+
+// 2-D float64 TMA descriptor over a column-major matrix: inner dimension =
+// rows (contiguous), outer = columns, row stride lda*8 bytes (multiple of 16).
+// Out-of-bounds box elements are zero-filled by the TMA unit.
+int make_tmap_f64_2d(CUtensorMap *map, const void *base, uint64_t rows, uint64_t cols,
+                     uint64_t lda, uint32_t box_rows, uint32_t box_cols);
 
 // ------------------------------------------------------------ PTX helpers
 __device__ __forceinline__ uint32_t smem_u32(const void *p) {
@@ -80,6 +87,21 @@ __device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t by
             "r"(smem_u32(dst)),
         "l"(src), "r"(bytes), "r"(smem_u32(bar))
         : "memory");
+}
+
+// TMA 2-D tile load (SASS: UTMALDG) into shared memory, completion counted
+// on an mbarrier.  x = inner (row) coordinate, y = outer (column) coordinate.
+__device__ __forceinline__ void tma_load_2d(void *dst, const CUtensorMap *map, int x, int y,
+                                            uint64_t *bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes "
+        "[%0], [%1, {%2, %3}], [%4];" ::"r"(smem_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(smem_u32(bar))
+        : "memory");
+}
+
+__device__ __forceinline__ void prefetch_tmap(const CUtensorMap *map) {
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(map)) : "memory");
 }
 
 // 8-byte cp.async with zero fill when !valid (src-size 0).

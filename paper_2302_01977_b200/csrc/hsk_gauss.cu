@@ -11,6 +11,8 @@
 // are chosen so every fragment load is two conflict-free wavefronts
 // (DESIGN.md §Gaussian).  R is the reference's d x n row-major `matrix`,
 // i.e. R^T column-major with leading dimension n.
+#include <stdlib.h>
+
 #include <algorithm>
 
 #include "hsk_common.cuh"
@@ -40,13 +42,14 @@ __device__ __forceinline__ void dmma(double (&c)[2], double a, double b) {
 }
 
 // copy the two doubles src[0..1] (valid0/valid1) to dst, 16B if allowed
+// (`safe` is any valid global address used when a half is out of range)
 __device__ __forceinline__ void copy2(double *dst, const double *src, bool v0, bool v1,
-                                      bool vec16) {
+                                      bool vec16, const double *safe) {
     if (vec16 && v0 && v1) {
         cp_async16(dst, src, true);
     } else {
-        cp_async8(dst, v0 ? src : dst, v0);
-        cp_async8(dst + 1, v1 ? src + 1 : dst, v1);
+        cp_async8(dst, v0 ? src : safe, v0);
+        cp_async8(dst + 1, v1 ? src + 1 : safe, v1);
     }
 }
 
@@ -83,7 +86,7 @@ __global__ void __launch_bounds__(256) gauss_kernel(const Args p) {
                 const int64_t gm = m0 + mm, gk = k0 + kk;
                 const bool vk = gk < p.K;
                 const double *src = p.A + gk * p.lda + gm;
-                copy2(sA + kk * SM::PA + mm, src, vk && gm < p.M, vk && gm + 1 < p.M, p.a16);
+                copy2(sA + kk * SM::PA + mm, src, vk && gm < p.M, vk && gm + 1 < p.M, p.a16, p.R);
             }
         } else {
             // A^T(m,k) = A[m*lda + k]: BM rows of BK contiguous k
@@ -92,7 +95,7 @@ __global__ void __launch_bounds__(256) gauss_kernel(const Args p) {
                 const int64_t gm = m0 + mm, gk = k0 + kk;
                 const bool vm = gm < p.M;
                 const double *src = p.A + gm * p.lda + gk;
-                copy2(sA + mm * PKK + kk, src, vm && gk < p.K, vm && gk + 1 < p.K, p.a16);
+                copy2(sA + mm * PKK + kk, src, vm && gk < p.K, vm && gk + 1 < p.K, p.a16, p.R);
             }
         }
         // B(k,j) = R[j*K + k]
@@ -101,7 +104,7 @@ __global__ void __launch_bounds__(256) gauss_kernel(const Args p) {
             const int64_t gj = n0 + jj, gk = k0 + kk;
             const bool vj = gj < p.N;
             const double *src = p.R + gj * p.K + gk;
-            copy2(sB + jj * PKK + kk, src, vj && gk < p.K, vj && gk + 1 < p.K, p.b16);
+            copy2(sB + jj * PKK + kk, src, vj && gk < p.K, vj && gk + 1 < p.K, p.b16, p.R);
         }
     };
 
@@ -208,5 +211,8 @@ extern "C" int hsk_gauss_apply(const double *A, int64_t rows, int64_t cols, int6
     a.a16 = ((reinterpret_cast<uintptr_t>(A) & 15) == 0) && (lda % 2 == 0);
     a.b16 = ((reinterpret_cast<uintptr_t>(R) & 15) == 0) && (n % 2 == 0);
     cudaStream_t st = as_stream(stream);
+    const char *cfg = getenv("HSK_GAUSS_CFG");  // tuning override: "64" -> 64 x 128 tiles
+    if (cfg && cfg[0] == '6')
+        return trans ? gauss::launch<64, 128, 1>(a, st) : gauss::launch<64, 128, 0>(a, st);
     return trans ? gauss::launch<128, 128, 1>(a, st) : gauss::launch<128, 128, 0>(a, st);
 }

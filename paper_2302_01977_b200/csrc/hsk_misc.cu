@@ -7,6 +7,8 @@
 
 #include <algorithm>
 
+#include <cudaTypedefs.h>
+
 #include "hsk_common.cuh"
 
 namespace hsk {
@@ -25,6 +27,29 @@ int cuda_status(cudaError_t e, const char *what) {
     return set_error(e == cudaErrorNoDevice || e == cudaErrorInsufficientDriver ? HSK_ENODEV
                                                                                  : HSK_ECUDA,
                      "%s: %s", what, cudaGetErrorString(e));
+}
+
+int make_tmap_f64_2d(CUtensorMap *map, const void *base, uint64_t rows, uint64_t cols,
+                     uint64_t lda, uint32_t box_rows, uint32_t box_cols) {
+    static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
+    if (!encode) {
+        void *fn = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        cudaError_t e = cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q);
+        if (e != cudaSuccess || q != cudaDriverEntryPointSuccess || !fn)
+            return set_error(HSK_ECUDA, "cuTensorMapEncodeTiled unavailable");
+        encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+    }
+    cuuint64_t dims[2] = {rows, cols};
+    cuuint64_t strides[1] = {lda * 8};
+    cuuint32_t box[2] = {box_rows, box_cols};
+    cuuint32_t estr[2] = {1, 1};
+    CUresult r = encode(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<void *>(base), dims,
+                        strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                        CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                        CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) return set_error(HSK_ECUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
+    return HSK_OK;
 }
 
 int sm_count() {

@@ -3,26 +3,29 @@
 // Replaces SjltBlock._build_storage / apply_right / apply_right_transposed
 // (/root/reference/pkg/src/hsskit/sketching.py:292-351; PAPER.md §6).
 //
-// Design (see DESIGN.md §SJLT):
-//  * The reference keeps R^T = s (B+ - B-) as index-only CSR/CSC.  The GPU
-//    plan re-blocks the same pattern by k-chunks of TK input indices: per
-//    chunk, the TK*alpha entries sorted by bucket (stable in (k, t)), each a
-//    16-bit word (k - k0) | (sign < 0) << 15, plus per-chunk bucket offsets.
-//    Built on device by a per-chunk bitonic sort (sjlt_plan_kernel).
-//  * Apply: a CTA owns TM = 32*RPT output rows and a slab of NW*DB buckets.
-//    Consumer warp w owns buckets [j0 + w*DB, +DB); every lane owns RPT
-//    output rows, so each warp keeps an RPT x DB register accumulator block
-//    (owner-computes: no atomics, fixed summation order -> deterministic).
-//  * A producer warp streams TK x TM tiles of A (each input element read
-//    once from HBM) plus the chunk's plan slice into a STAGES-deep shared
-//    memory ring: TMA bulk copies (cp.async.bulk, one per 512-byte column
-//    segment) when A's columns are 16-byte aligned, else 8-byte cp.async
-//    (which also performs the transpose for S' = A^T R^T).  mbarrier
-//    full/empty pairs decouple producer and consumers, so per-chunk load
-//    imbalance between warps is absorbed across stages.
-//  * Consumer inner loop per entry: LDS entry word, LDS.64/LDS.128 of the
-//    A tile, DFMA with +-1 (exactly the reference's add/subtract: one
-//    rounding), no multiplies by data values.
+// Design (DESIGN.md §SJLT):
+//  * Plan.  The reference keeps R^T = s (B+ - B-) as index-only CSR/CSC.  The
+//    GPU plan re-blocks the same pattern by k-chunks of TK input indices: per
+//    chunk, its TK*alpha entries sorted by bucket (stable in (k, t)), each a
+//    32-bit word  kk | sign << 31  (kk = k - k0), plus per-chunk bucket
+//    offsets.  Built on device by a per-chunk bitonic sort.
+//  * Apply.  A CTA owns TM = 32*RPT output rows and a slab of NW*DB buckets.
+//    Consumer warp w owns buckets [j0 + w*DB, +DB); lane l owns rows
+//    l*RPT .. l*RPT+RPT-1, so each warp holds an RPT x DB register
+//    accumulator block: owner-computes, no atomics, a fixed summation order
+//    (deterministic).  Per entry: one broadcast LDS of the entry word, one
+//    LDS.128 (RPT = 2) of the staged A tile, RPT DFMAs with +-1 (exactly the
+//    reference's add/subtract, one rounding each; no data multiplies).
+//  * Streaming.  A producer warp moves TK x TM tiles of A (every element
+//    read once from HBM) plus the chunk's plan slice into a STAGES-deep
+//    shared-memory ring: one TMA 2-D tile load (UTMALDG, OOB zero-filled)
+//    per chunk when A's columns are 16-byte aligned, otherwise 8-byte
+//    cp.async (which also transposes the tile for S' = A^T R^T).  mbarrier
+//    full/empty pairs decouple producer and consumer warps, so per-chunk
+//    load imbalance between warps is absorbed across stages.
+#include <stdlib.h>
+#include <string.h>
+
 #include <algorithm>
 
 #include "hsk_common.cuh"
@@ -31,15 +34,15 @@ namespace hsk {
 namespace sjlt {
 
 constexpr int kHeaderBytes = 128;
-constexpr int kMaxChunkEntries = 2048;  // TK * alpha bound (11-bit local index)
-constexpr int64_t kMaxD = (1 << 20);    // bucket index must fit 21 bits of the sort key
+constexpr int kMaxChunkEntries = 4096;  // TK * alpha bound (12-bit local index)
+constexpr int kPlanSlab = 512;          // bucket-offset rows padded for slabs | 512
+constexpr int64_t kMaxD = (1 << 19);    // bucket index fits 19 bits of the sort key
 
 struct Geom {
     int tk;
-    int slab;
     int64_t nchunks;
     int64_t bstride;   // uint16 per bucket-offset row
-    int64_t estride;   // uint16 per chunk entry row (tk*alpha rounded to 8)
+    int64_t estride;   // uint32 per chunk entry row (tk*alpha rounded to 4)
     int64_t bptr_off;  // bytes
     int64_t ent_off;   // bytes
     int64_t bytes;
@@ -47,10 +50,8 @@ struct Geom {
 
 static inline int64_t roundup(int64_t x, int64_t m) { return (x + m - 1) / m * m; }
 
-static inline int slab_for(int d) { return d <= 64 ? 64 : d <= 128 ? 128 : d <= 256 ? 256 : 512; }
-
 static inline int tk_for(int alpha) {
-    int tk = 64;
+    int tk = 128;
     while (tk > 1 && tk * alpha > kMaxChunkEntries) tk >>= 1;
     return tk;
 }
@@ -58,22 +59,22 @@ static inline int tk_for(int alpha) {
 static Geom geom(int64_t n, int d, int alpha) {
     Geom g;
     g.tk = tk_for(alpha);
-    g.slab = slab_for(d);
     g.nchunks = (n + g.tk - 1) / g.tk;
-    g.bstride = roundup(d, g.slab) + 8;
-    g.estride = roundup((int64_t)g.tk * alpha, 8);
+    g.bstride = roundup(d, kPlanSlab) + 8;
+    g.estride = roundup((int64_t)g.tk * alpha, 4);
     g.bptr_off = kHeaderBytes;
     g.ent_off = roundup(g.bptr_off + (g.nchunks + 1) * g.bstride * 2, 128);
-    g.bytes = g.ent_off + roundup((g.nchunks + 1) * g.estride * 2, 128);
+    g.bytes = g.ent_off + roundup((g.nchunks + 1) * g.estride * 4, 128);
     return g;
 }
 
 // ------------------------------------------------------------ plan build
+// One CTA per chunk: sort the chunk's (bucket, local index) keys, emit
+// entry words in that order and per-bucket lower bounds.
 __global__ void sjlt_plan_kernel(const int32_t *__restrict__ pos, const int8_t *__restrict__ sgn,
                                  int64_t n, int d, int alpha, int tk, int p2, int64_t bstride,
-                                 int64_t estride,
-                                 uint16_t *__restrict__ bptr, uint16_t *__restrict__ ent,
-                                 int *err) {
+                                 int64_t estride, uint16_t *__restrict__ bptr,
+                                 uint32_t *__restrict__ ent, int *err) {
     extern __shared__ uint32_t keys[];
     const int64_t c = blockIdx.x;
     const int64_t k0 = c * tk;
@@ -88,7 +89,7 @@ __global__ void sjlt_plan_kernel(const int32_t *__restrict__ pos, const int8_t *
                 atomicOr(err, 1);
                 p = p < 0 ? 0 : d - 1;
             }
-            key = ((uint32_t)p << 11) | (uint32_t)i;
+            key = ((uint32_t)p << 12) | (uint32_t)i;
         }
         keys[i] = key;
     }
@@ -96,11 +97,10 @@ __global__ void sjlt_plan_kernel(const int32_t *__restrict__ pos, const int8_t *
     for (int k = 2; k <= p2; k <<= 1) {
         for (int j = k >> 1; j > 0; j >>= 1) {
             for (int i = threadIdx.x; i < p2; i += blockDim.x) {
-                int ixj = i ^ j;
+                const int ixj = i ^ j;
                 if (ixj > i) {
-                    uint32_t a = keys[i], b = keys[ixj];
-                    bool up = (i & k) == 0;
-                    if ((a > b) == up) {
+                    const uint32_t a = keys[i], b = keys[ixj];
+                    if ((a > b) == ((i & k) == 0)) {
                         keys[i] = b;
                         keys[ixj] = a;
                     }
@@ -109,26 +109,23 @@ __global__ void sjlt_plan_kernel(const int32_t *__restrict__ pos, const int8_t *
             __syncthreads();
         }
     }
-    uint16_t *e_out = ent + c * estride;
+    uint32_t *e_out = ent + c * estride;
     for (int e = threadIdx.x; e < estride; e += blockDim.x) {
-        uint16_t w = 0;
+        uint32_t w = 0;
         if (e < cnt) {
-            int local = keys[e] & 2047;
-            int kk = local / alpha;
-            w = (uint16_t)(kk | (sgn[q0 + local] < 0 ? 0x8000 : 0));
+            const int local = keys[e] & 4095;
+            w = (uint32_t)(local / alpha) | (sgn[q0 + local] < 0 ? 0x80000000u : 0u);
         }
         e_out[e] = w;
     }
     uint16_t *b_out = bptr + c * bstride;
     for (int64_t j = threadIdx.x; j < bstride; j += blockDim.x) {
-        int lb;
-        if (j >= d) {
-            lb = cnt;
-        } else {  // number of keys with bucket < j
-            uint32_t target = (uint32_t)j << 11;
+        int lb = cnt;
+        if (j < d) {  // number of keys with bucket < j
+            const uint32_t target = (uint32_t)j << 12;
             int lo = 0, hi = cnt;
             while (lo < hi) {
-                int mid = (lo + hi) >> 1;
+                const int mid = (lo + hi) >> 1;
                 if (keys[mid] < target) lo = mid + 1; else hi = mid;
             }
             lb = lo;
@@ -142,13 +139,13 @@ struct ApplyArgs {
     const double *A;
     int64_t lda;
     int trans;
-    int bulk_ok;
+    int use_tma;
     int64_t m_out;  // output rows (rows of A for trans 0, cols of A for trans 1)
     int64_t n;      // input index extent (= op.n)
     int d, alpha, tk;
     int64_t nchunks, bstride, estride;
     const uint16_t *bptr;
-    const uint16_t *ent;
+    const uint32_t *ent;
     double scale;
     double *S;
     int64_t lds, col0;
@@ -157,7 +154,8 @@ struct ApplyArgs {
 };
 
 template <int RPT, int DB, int NW>
-__global__ void __launch_bounds__((NW + 1) * 32, 1) sjlt_apply_kernel(const ApplyArgs p) {
+__global__ void __launch_bounds__((NW + 1) * 32, 1)
+    sjlt_apply_kernel(const ApplyArgs p, const __grid_constant__ CUtensorMap tmap) {
     constexpr int TM = 32 * RPT;
     constexpr int SLAB = NW * DB;
     extern __shared__ __align__(128) unsigned char smem[];
@@ -170,14 +168,15 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) sjlt_apply_kernel(const Appl
     const int64_t tile = blockIdx.x / p.nslabs;
     const int64_t r0 = tile * TM;
     const int j0 = slab * SLAB;
-    const bool bulk = p.bulk_ok && !p.trans && (r0 + TM <= p.m_out);
+    const bool tma = p.use_tma != 0;
 
     if (threadIdx.x == 0) {
         for (int s = 0; s < p.stages; ++s) {
-            mbar_init(&full[s], bulk ? 1 : 32);
+            mbar_init(&full[s], tma ? 1 : 32);
             mbar_init(&empty[s], NW);
         }
         fence_mbar_init();
+        if (tma) prefetch_tmap(&tmap);
     }
     __syncthreads();
 
@@ -185,30 +184,32 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) sjlt_apply_kernel(const Appl
     if (warp == NW) {
         // ---------------------------------------------------- producer
         const uint32_t bp_bytes = (SLAB + 8) * 2;
-        const uint32_t en_bytes = (uint32_t)p.estride * 2;
+        const uint32_t en_bytes = (uint32_t)p.estride * 4;
+        const uint32_t tile_bytes = (uint32_t)p.tk * TM * 8;
         for (int64_t c = 0; c < p.nchunks; ++c) {
             const int s = (int)(c % stages);
             if (c >= stages) mbar_wait(&empty[s], (uint32_t)((c / stages) - 1) & 1u);
             unsigned char *st = stage0 + (size_t)s * p.stage_bytes;
             double *sx = reinterpret_cast<double *>(st);
             uint16_t *sbp = reinterpret_cast<uint16_t *>(st + p.bp_off);
-            uint16_t *sen = reinterpret_cast<uint16_t *>(st + p.en_off);
+            uint32_t *sen = reinterpret_cast<uint32_t *>(st + p.en_off);
             const int64_t k0 = c * p.tk;
             const int kc = (int)(p.n - k0 < p.tk ? p.n - k0 : p.tk);
             const uint16_t *gbp = p.bptr + c * p.bstride + j0;
-            const uint16_t *gen = p.ent + c * p.estride;
-            if (bulk) {
+            const uint32_t *gen = p.ent + c * p.estride;
+            if (tma) {
                 if (lane == 0) {
-                    mbar_arrive_expect_tx(&full[s], (uint32_t)kc * TM * 8 + bp_bytes + en_bytes);
+                    mbar_arrive_expect_tx(&full[s], tile_bytes + bp_bytes + en_bytes);
+                    tma_load_2d(sx, &tmap, (int)r0, (int)k0, &full[s]);
                     bulk_g2s(sbp, gbp, bp_bytes, &full[s]);
                     bulk_g2s(sen, gen, en_bytes, &full[s]);
                 }
                 __syncwarp();
-                for (int kk = lane; kk < kc; kk += 32)
-                    bulk_g2s(sx + kk * p.pitch, p.A + (k0 + kk) * p.lda + r0, TM * 8, &full[s]);
             } else {
-                for (uint32_t i = lane; i < bp_bytes / 16; i += 32) cp_async16(sbp + i * 8, gbp + i * 8, true);
-                for (uint32_t i = lane; i < en_bytes / 16; i += 32) cp_async16(sen + i * 8, gen + i * 8, true);
+                for (uint32_t i = lane; i < bp_bytes / 16; i += 32)
+                    cp_async16(sbp + i * 8, gbp + i * 8, true);
+                for (uint32_t i = lane; i < en_bytes / 16; i += 32)
+                    cp_async16(sen + i * 4, gen + i * 4, true);
                 if (!p.trans) {
                     // lanes along rows: coalesced global, consecutive smem
                     for (int idx = lane; idx < p.tk * TM; idx += 32) {
@@ -219,8 +220,9 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) sjlt_apply_kernel(const Appl
                     }
                 } else {
                     // S' tile: element (out row r0+rr, k0+kk) = A[k0+kk, r0+rr].
-                    // Lanes: 16 consecutive k (coalesced 128 B) x 2 rows, so
-                    // the transposing smem writes hit 16 distinct bank pairs.
+                    // 16 consecutive k per half-warp (coalesced 128 B reads);
+                    // pitch == 2 mod 16 doubles keeps the transposing stores at
+                    // two wavefronts per warp.
                     const int kl = lane & 15, rl = lane >> 4;
                     for (int rb = 0; rb < TM; rb += 2) {
                         const int rr = rb + rl;
@@ -243,64 +245,51 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) sjlt_apply_kernel(const Appl
 #pragma unroll
             for (int jj = 0; jj < DB; ++jj) acc[r][jj] = 0.0;
 
-        const int pitch = p.pitch;
+        const uint32_t pitch8 = (uint32_t)p.pitch * 8;
         for (int64_t c = 0; c < p.nchunks; ++c) {
             const int s = (int)(c % stages);
             mbar_wait(&full[s], (uint32_t)(c / stages) & 1u);
             const unsigned char *st = stage0 + (size_t)s * p.stage_bytes;
-            const double *sx = reinterpret_cast<const double *>(st) + lane * RPT;
+            const unsigned char *sxl = st + lane * RPT * 8;
             const uint16_t *sbp = reinterpret_cast<const uint16_t *>(st + p.bp_off) + warp * DB;
-            const uint16_t *sen = reinterpret_cast<const uint16_t *>(st + p.en_off);
+            const uint32_t *sen = reinterpret_cast<const uint32_t *>(st + p.en_off);
             int e = sbp[0];
 #pragma unroll
             for (int jj = 0; jj < DB; ++jj) {
                 const int e1 = sbp[jj + 1];
-                for (; e + 1 < e1; e += 2) {
-                    const uint32_t w0 = sen[e], w1 = sen[e + 1];
-                    const double g0 = (w0 & 0x8000u) ? -1.0 : 1.0;
-                    const double g1 = (w1 & 0x8000u) ? -1.0 : 1.0;
-                    const double *x0 = sx + (w0 & 0x7fffu) * pitch;
-                    const double *x1 = sx + (w1 & 0x7fffu) * pitch;
+                for (; e < e1; ++e) {
+                    const uint32_t w = sen[e];
+                    const unsigned char *src = sxl + (w & 0xffffu) * pitch8;
+                    // +-1.0 from the sign bit: exact, so fma(v, g, acc) == acc +- v
+                    const double g = __hiloint2double((int)((w & 0x80000000u) | 0x3ff00000u), 0);
                     if (RPT == 2) {
-                        const double2 v0 = *reinterpret_cast<const double2 *>(x0);
-                        const double2 v1 = *reinterpret_cast<const double2 *>(x1);
-                        acc[0][jj] = fma(v0.x, g0, acc[0][jj]);
-                        acc[RPT - 1][jj] = fma(v0.y, g0, acc[RPT - 1][jj]);
-                        acc[0][jj] = fma(v1.x, g1, acc[0][jj]);
-                        acc[RPT - 1][jj] = fma(v1.y, g1, acc[RPT - 1][jj]);
+                        const double2 v = *reinterpret_cast<const double2 *>(src);
+                        acc[0][jj] = fma(v.x, g, acc[0][jj]);
+                        acc[RPT - 1][jj] = fma(v.y, g, acc[RPT - 1][jj]);
                     } else {
-                        const double v0 = *x0, v1 = *x1;
-                        acc[0][jj] = fma(v0, g0, acc[0][jj]);
-                        acc[0][jj] = fma(v1, g1, acc[0][jj]);
+                        acc[0][jj] = fma(*reinterpret_cast<const double *>(src), g, acc[0][jj]);
                     }
                 }
-                if (e < e1) {
-                    const uint32_t w0 = sen[e];
-                    const double g0 = (w0 & 0x8000u) ? -1.0 : 1.0;
-                    const double *x0 = sx + (w0 & 0x7fffu) * pitch;
-                    if (RPT == 2) {
-                        const double2 v0 = *reinterpret_cast<const double2 *>(x0);
-                        acc[0][jj] = fma(v0.x, g0, acc[0][jj]);
-                        acc[RPT - 1][jj] = fma(v0.y, g0, acc[RPT - 1][jj]);
-                    } else {
-                        acc[0][jj] = fma(*x0, g0, acc[0][jj]);
-                    }
-                }
-                e = e1;
             }
             __syncwarp();
             if (lane == 0) mbar_arrive(&empty[s]);
         }
         // epilogue: one final scaling, as the reference (`out *= scale`)
+        const bool vec_ok = RPT == 2 && ((p.lds & 1) == 0) &&
+                            ((reinterpret_cast<uintptr_t>(p.S) & 15) == 0);
 #pragma unroll
         for (int jj = 0; jj < DB; ++jj) {
             const int j = j0 + warp * DB + jj;
             if (j < p.d) {
                 double *col = p.S + (p.col0 + j) * p.lds;
+                const int64_t row = r0 + lane * RPT;
+                if (vec_ok && row + 1 < p.m_out) {
+                    *reinterpret_cast<double2 *>(col + row) =
+                        make_double2(acc[0][jj] * p.scale, acc[RPT - 1][jj] * p.scale);
+                } else {
 #pragma unroll
-                for (int r = 0; r < RPT; ++r) {
-                    const int64_t row = r0 + lane * RPT + r;
-                    if (row < p.m_out) col[row] = acc[r][jj] * p.scale;
+                    for (int r = 0; r < RPT; ++r)
+                        if (row + r < p.m_out) col[row + r] = acc[r][jj] * p.scale;
                 }
             }
         }
@@ -312,24 +301,32 @@ static int launch(ApplyArgs a, cudaStream_t st) {
     constexpr int TM = 32 * RPT;
     constexpr int SLAB = NW * DB;
     a.pitch = a.trans ? TM + (RPT == 2 ? 2 : 1) : TM;
+    a.use_tma = a.use_tma && !a.trans;
+    CUtensorMap tmap;
+    memset(&tmap, 0, sizeof(tmap));
+    if (a.use_tma) {
+        int rc = make_tmap_f64_2d(&tmap, a.A, (uint64_t)a.m_out, (uint64_t)a.n, (uint64_t)a.lda,
+                                  TM, (uint32_t)a.tk);
+        if (rc) return rc;
+    }
     const int a_bytes = (int)roundup((int64_t)a.tk * a.pitch * 8, 128);
     const int bp_bytes = (int)roundup((SLAB + 8) * 2, 128);
-    const int en_bytes = (int)roundup(a.estride * 2, 128);
+    const int en_bytes = (int)roundup(a.estride * 4, 128);
     a.bp_off = a_bytes;
     a.en_off = a_bytes + bp_bytes;
     a.stage_bytes = a_bytes + bp_bytes + en_bytes;
-    const int budget = 200 * 1024;
+    const int budget = 220 * 1024;
     a.stages = std::max(2, std::min(8, (budget - 128) / a.stage_bytes));
     if (a.nchunks > 0 && a.stages > a.nchunks) a.stages = (int)std::max<int64_t>(2, a.nchunks);
     const int smem = 128 + a.stages * a.stage_bytes;
     auto kern = sjlt_apply_kernel<RPT, DB, NW>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e != cudaSuccess) return cuda_status(e, "sjlt: set smem attribute");
-    a.nslabs = (int)((a.d + SLAB - 1) / SLAB);
+    a.nslabs = (a.d + SLAB - 1) / SLAB;
     const int64_t tiles = (a.m_out + TM - 1) / TM;
     const int64_t grid = tiles * a.nslabs;
     HSK_REQUIRE(grid < (1ll << 31), HSK_EINVAL, "sjlt: grid too large");
-    kern<<<(unsigned)grid, (NW + 1) * 32, smem, st>>>(a);
+    kern<<<(unsigned)grid, (NW + 1) * 32, smem, st>>>(a, tmap);
     HSK_CHECK_LAUNCH("sjlt_apply_kernel");
     return HSK_OK;
 }
@@ -340,7 +337,8 @@ static int launch(ApplyArgs a, cudaStream_t st) {
 using namespace hsk;
 
 extern "C" int64_t hsk_sjlt_plan_bytes(int64_t n, int32_t d, int32_t alpha) {
-    if (n < 0 || d < 1 || alpha < 1 || d > sjlt::kMaxD) return HSK_EINVAL;
+    if (n < 0 || d < 1 || alpha < 1 || d > sjlt::kMaxD || alpha > sjlt::kMaxChunkEntries)
+        return HSK_EINVAL;
     return sjlt::geom(n, d, alpha).bytes;
 }
 
@@ -352,6 +350,7 @@ extern "C" int hsk_sjlt_plan_build(const int32_t *pos, const int8_t *sgn, int64_
     HSK_REQUIRE(d <= sjlt::kMaxD, HSK_EINVAL, "sjlt plan: d=%d exceeds %lld", d,
                 (long long)sjlt::kMaxD);
     HSK_REQUIRE(alpha <= sjlt::kMaxChunkEntries, HSK_EINVAL, "sjlt plan: alpha=%d too large", alpha);
+    HSK_REQUIRE(n < (1ll << 31), HSK_EINVAL, "sjlt plan: n too large");
     const sjlt::Geom g = sjlt::geom(n, d, alpha);
     HSK_REQUIRE(plan != nullptr && plan_bytes >= g.bytes, HSK_EINVAL,
                 "sjlt plan: buffer of %lld bytes, need %lld", (long long)plan_bytes,
@@ -361,17 +360,13 @@ extern "C" int hsk_sjlt_plan_build(const int32_t *pos, const int8_t *sgn, int64_
     unsigned char *base = static_cast<unsigned char *>(plan);
     cudaError_t e = cudaMemsetAsync(base, 0, g.bytes, st);
     if (e != cudaSuccess) return cuda_status(e, "sjlt plan: memset");
-    int32_t header[8] = {0x4B534A50, (int32_t)n, d, alpha, g.tk, (int32_t)g.nchunks,
-                         (int32_t)g.bstride, 0};
-    (void)header;  // header words are informational; err flag lives at byte 28
     if (n > 0) {
         int p2 = 1;
         while (p2 < g.tk * alpha) p2 <<= 1;
-        const int threads = 256;
-        sjlt::sjlt_plan_kernel<<<(unsigned)g.nchunks, threads, p2 * sizeof(uint32_t), st>>>(
+        sjlt::sjlt_plan_kernel<<<(unsigned)g.nchunks, 256, p2 * sizeof(uint32_t), st>>>(
             pos, sgn, n, d, alpha, g.tk, p2, g.bstride, g.estride,
             reinterpret_cast<uint16_t *>(base + g.bptr_off),
-            reinterpret_cast<uint16_t *>(base + g.ent_off), reinterpret_cast<int *>(base + 28));
+            reinterpret_cast<uint32_t *>(base + g.ent_off), reinterpret_cast<int *>(base + 28));
         HSK_CHECK_LAUNCH("sjlt_plan_kernel");
     }
     return HSK_OK;
@@ -398,13 +393,14 @@ extern "C" int hsk_sjlt_apply(const double *A, int64_t rows, int64_t cols, int64
     if (m_out == 0) return HSK_OK;
     HSK_REQUIRE(plan != nullptr && S != nullptr && (A != nullptr || n == 0), HSK_EINVAL,
                 "sjlt apply: null pointer");
+    HSK_REQUIRE(m_out < (1ll << 31) && n < (1ll << 31), HSK_EINVAL, "sjlt apply: too large");
     const sjlt::Geom g = sjlt::geom(n, d, alpha);
     const unsigned char *base = static_cast<const unsigned char *>(plan);
     sjlt::ApplyArgs a{};
     a.A = A;
     a.lda = lda;
     a.trans = trans;
-    a.bulk_ok = ((reinterpret_cast<uintptr_t>(A) & 15) == 0) && (lda % 2 == 0);
+    a.use_tma = ((reinterpret_cast<uintptr_t>(A) & 15) == 0) && (lda % 2 == 0) && n > 0;
     a.m_out = m_out;
     a.n = n;
     a.d = d;
@@ -414,16 +410,15 @@ extern "C" int hsk_sjlt_apply(const double *A, int64_t rows, int64_t cols, int64
     a.bstride = g.bstride;
     a.estride = g.estride;
     a.bptr = reinterpret_cast<const uint16_t *>(base + g.bptr_off);
-    a.ent = reinterpret_cast<const uint16_t *>(base + g.ent_off);
+    a.ent = reinterpret_cast<const uint32_t *>(base + g.ent_off);
     a.scale = scale;
     a.S = S;
     a.lds = lds;
     a.col0 = col0;
     cudaStream_t st = as_stream(stream);
-    switch (g.slab) {
-        case 64: return sjlt::launch<2, 16, 4>(a, st);
-        case 128: return sjlt::launch<2, 16, 8>(a, st);
-        case 256: return sjlt::launch<2, 16, 16>(a, st);
-        default: return sjlt::launch<1, 32, 16>(a, st);
-    }
+    const char *cfg = getenv("HSK_SJLT_CFG");  // tuning override: "512" -> RPT 1 x 512 slab
+    if (cfg && cfg[0] == '5' && d > 256) return sjlt::launch<1, 32, 16>(a, st);
+    if (d <= 64) return sjlt::launch<2, 8, 8>(a, st);
+    if (d <= 128) return sjlt::launch<2, 16, 8>(a, st);
+    return sjlt::launch<2, 16, 16>(a, st);
 }
