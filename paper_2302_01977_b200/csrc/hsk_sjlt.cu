@@ -6,9 +6,12 @@
 // Design (DESIGN.md §SJLT):
 //  * Plan.  The reference keeps R^T = s (B+ - B-) as index-only CSR/CSC.  The
 //    GPU plan re-blocks the same pattern by k-chunks of TK input indices: per
-//    chunk, its TK*alpha entries sorted by bucket (stable in (k, t)), each a
-//    32-bit word  kk | sign << 31  (kk = k - k0), plus per-chunk bucket
-//    offsets.  Built on device by a per-chunk bitonic sort.
+//    chunk, its TK*alpha entries sorted by bucket (stable in (k, t)), plus
+//    per-chunk bucket offsets.  An entry is 16 bytes, pre-decoded for the
+//    consumer: {byte offset of row kk in the staged tile, 0, (double)+-1}, so
+//    the inner loop spends no instructions on decoding.  Two entry arrays
+//    are kept, one per tile pitch (S: TMA-dense, S': padded transpose).
+//    Built on device by a per-chunk bitonic sort.
 //  * Apply.  A CTA owns TM = 32*RPT output rows and a slab of NW*DB buckets.
 //    Consumer warp w owns buckets [j0 + w*DB, +DB); lane l owns rows
 //    l*RPT .. l*RPT+RPT-1, so each warp holds an RPT x DB register
@@ -39,32 +42,45 @@ constexpr int kPlanSlab = 512;          // bucket-offset rows padded for slabs |
 constexpr int64_t kMaxD = (1 << 19);    // bucket index fits 19 bits of the sort key
 
 struct Geom {
+    int rpt;           // rows per lane: 4 for d <= 64, else 2
+    int tm;            // rows per CTA = 32 * rpt
+    int pitch_s;       // tile pitch (doubles) for S: TMA writes densely
+    int pitch_t;       // tile pitch for S': == 2 mod 16, conflict-free transposing stores
     int tk;
     int64_t nchunks;
     int64_t bstride;   // uint16 per bucket-offset row
-    int64_t estride;   // uint32 per chunk entry row (tk*alpha rounded to 4)
+    int64_t estride;   // entries per chunk row (tk*alpha)
     int64_t bptr_off;  // bytes
-    int64_t ent_off;   // bytes
+    int64_t ent_off;   // bytes: entries for S (pitch kPitchS)
+    int64_t entt_off;  // bytes: entries for S' (pitch kPitchT)
     int64_t bytes;
 };
 
 static inline int64_t roundup(int64_t x, int64_t m) { return (x + m - 1) / m * m; }
 
-static inline int tk_for(int alpha) {
+// TK: as long as a stage (TK x TM x 8 B tile + TK*alpha 16-byte entries)
+// leaves room for >= 3 stages in shared memory, capped at 128.
+static inline int tk_for(int alpha, int tm) {
     int tk = 128;
-    while (tk > 1 && tk * alpha > kMaxChunkEntries) tk >>= 1;
+    while (tk > 1 && (tk * alpha > kMaxChunkEntries || tk * ((tm + 2) * 8 + 16 * alpha) > 72 * 1024))
+        tk >>= 1;
     return tk;
 }
 
 static Geom geom(int64_t n, int d, int alpha) {
     Geom g;
-    g.tk = tk_for(alpha);
+    g.rpt = d <= 64 ? 4 : 2;
+    g.tm = 32 * g.rpt;
+    g.pitch_s = g.tm;
+    g.pitch_t = g.tm + 2;
+    g.tk = tk_for(alpha, g.tm);
     g.nchunks = (n + g.tk - 1) / g.tk;
     g.bstride = roundup(d, kPlanSlab) + 8;
-    g.estride = roundup((int64_t)g.tk * alpha, 4);
+    g.estride = (int64_t)g.tk * alpha;
     g.bptr_off = kHeaderBytes;
     g.ent_off = roundup(g.bptr_off + (g.nchunks + 1) * g.bstride * 2, 128);
-    g.bytes = g.ent_off + roundup((g.nchunks + 1) * g.estride * 4, 128);
+    g.entt_off = g.ent_off + roundup((g.nchunks + 1) * g.estride * 16, 128);
+    g.bytes = g.entt_off + roundup((g.nchunks + 1) * g.estride * 16, 128);
     return g;
 }
 
@@ -73,8 +89,9 @@ static Geom geom(int64_t n, int d, int alpha) {
 // entry words in that order and per-bucket lower bounds.
 __global__ void sjlt_plan_kernel(const int32_t *__restrict__ pos, const int8_t *__restrict__ sgn,
                                  int64_t n, int d, int alpha, int tk, int p2, int64_t bstride,
-                                 int64_t estride, uint16_t *__restrict__ bptr,
-                                 uint32_t *__restrict__ ent, int *err) {
+                                 int64_t estride, int pitch_s, int pitch_t,
+                                 uint16_t *__restrict__ bptr, uint4 *__restrict__ ent,
+                                 uint4 *__restrict__ entt, int *err) {
     extern __shared__ uint32_t keys[];
     const int64_t c = blockIdx.x;
     const int64_t k0 = c * tk;
@@ -109,14 +126,19 @@ __global__ void sjlt_plan_kernel(const int32_t *__restrict__ pos, const int8_t *
             __syncthreads();
         }
     }
-    uint32_t *e_out = ent + c * estride;
+    uint4 *e_out = ent + c * estride;
+    uint4 *t_out = entt + c * estride;
     for (int e = threadIdx.x; e < estride; e += blockDim.x) {
-        uint32_t w = 0;
+        uint4 w = make_uint4(0, 0, 0, 0), wt = w;
         if (e < cnt) {
             const int local = keys[e] & 4095;
-            w = (uint32_t)(local / alpha) | (sgn[q0 + local] < 0 ? 0x80000000u : 0u);
+            const uint32_t kk = (uint32_t)(local / alpha);
+            const uint32_t g_hi = sgn[q0 + local] < 0 ? 0xBFF00000u : 0x3FF00000u;  // -1.0 / +1.0
+            w = make_uint4(kk * pitch_s * 8, 0, 0, g_hi);
+            wt = make_uint4(kk * pitch_t * 8, 0, 0, g_hi);
         }
         e_out[e] = w;
+        t_out[e] = wt;
     }
     uint16_t *b_out = bptr + c * bstride;
     for (int64_t j = threadIdx.x; j < bstride; j += blockDim.x) {
@@ -145,7 +167,7 @@ struct ApplyArgs {
     int d, alpha, tk;
     int64_t nchunks, bstride, estride;
     const uint16_t *bptr;
-    const uint32_t *ent;
+    const uint4 *ent;
     double scale;
     double *S;
     int64_t lds, col0;
@@ -153,8 +175,10 @@ struct ApplyArgs {
     int stage_bytes, bp_off, en_off;
 };
 
-template <int RPT, int DB, int NW>
-__global__ void __launch_bounds__((NW + 1) * 32, 1)
+// Warp roles: warps [0, NW) consume (bucket owners), warps [NW, NW+PW)
+// produce.  Lane l owns rows RPT*l .. RPT*l+RPT-1 of the TM-row tile.
+template <int RPT, int DB, int NW, int PW>
+__global__ void __launch_bounds__((NW + PW) * 32, 1)
     sjlt_apply_kernel(const ApplyArgs p, const __grid_constant__ CUtensorMap tmap) {
     constexpr int TM = 32 * RPT;
     constexpr int SLAB = NW * DB;
@@ -172,7 +196,7 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1)
 
     if (threadIdx.x == 0) {
         for (int s = 0; s < p.stages; ++s) {
-            mbar_init(&full[s], tma ? 1 : 32);
+            mbar_init(&full[s], tma ? 1 : 32 * PW);
             mbar_init(&empty[s], NW);
         }
         fence_mbar_init();
@@ -181,10 +205,12 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1)
     __syncthreads();
 
     const int stages = p.stages;
-    if (warp == NW) {
-        // ---------------------------------------------------- producer
+    if (warp >= NW) {
+        // ---------------------------------------------------- producers
+        const int pw = warp - NW;
+        if (tma && pw != 0) return;
         const uint32_t bp_bytes = (SLAB + 8) * 2;
-        const uint32_t en_bytes = (uint32_t)p.estride * 4;
+        const uint32_t en_bytes = (uint32_t)p.estride * 16;
         const uint32_t tile_bytes = (uint32_t)p.tk * TM * 8;
         for (int64_t c = 0; c < p.nchunks; ++c) {
             const int s = (int)(c % stages);
@@ -192,11 +218,11 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1)
             unsigned char *st = stage0 + (size_t)s * p.stage_bytes;
             double *sx = reinterpret_cast<double *>(st);
             uint16_t *sbp = reinterpret_cast<uint16_t *>(st + p.bp_off);
-            uint32_t *sen = reinterpret_cast<uint32_t *>(st + p.en_off);
+            uint4 *sen = reinterpret_cast<uint4 *>(st + p.en_off);
             const int64_t k0 = c * p.tk;
             const int kc = (int)(p.n - k0 < p.tk ? p.n - k0 : p.tk);
             const uint16_t *gbp = p.bptr + c * p.bstride + j0;
-            const uint32_t *gen = p.ent + c * p.estride;
+            const uint4 *gen = p.ent + c * p.estride;
             if (tma) {
                 if (lane == 0) {
                     mbar_arrive_expect_tx(&full[s], tile_bytes + bp_bytes + en_bytes);
@@ -206,13 +232,14 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1)
                 }
                 __syncwarp();
             } else {
-                for (uint32_t i = lane; i < bp_bytes / 16; i += 32)
+                const int pl = pw * 32 + lane;  // producer lane id in [0, 32*PW)
+                for (uint32_t i = pl; i < bp_bytes / 16; i += 32 * PW)
                     cp_async16(sbp + i * 8, gbp + i * 8, true);
-                for (uint32_t i = lane; i < en_bytes / 16; i += 32)
-                    cp_async16(sen + i * 4, gen + i * 4, true);
+                for (uint32_t i = pl; i < en_bytes / 16; i += 32 * PW)
+                    cp_async16(sen + i, gen + i, true);
                 if (!p.trans) {
                     // lanes along rows: coalesced global, consecutive smem
-                    for (int idx = lane; idx < p.tk * TM; idx += 32) {
+                    for (int idx = pl; idx < p.tk * TM; idx += 32 * PW) {
                         const int kk = idx / TM, rr = idx % TM;
                         const bool v = (kk < kc) && (r0 + rr < p.m_out);
                         const double *src = v ? p.A + (k0 + kk) * p.lda + r0 + rr : p.A;
@@ -220,11 +247,11 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1)
                     }
                 } else {
                     // S' tile: element (out row r0+rr, k0+kk) = A[k0+kk, r0+rr].
-                    // 16 consecutive k per half-warp (coalesced 128 B reads);
-                    // pitch == 2 mod 16 doubles keeps the transposing stores at
-                    // two wavefronts per warp.
+                    // Per warp: 16 consecutive k (coalesced 128 B) x 2 rows; the
+                    // pitch (== 2 mod 16 doubles) makes the transposing stores
+                    // two conflict-free wavefronts.
                     const int kl = lane & 15, rl = lane >> 4;
-                    for (int rb = 0; rb < TM; rb += 2) {
+                    for (int rb = 2 * pw; rb < TM; rb += 2 * PW) {
                         const int rr = rb + rl;
                         const bool rv = r0 + rr < p.m_out;
                         const double *col = p.A + (r0 + rr) * p.lda + k0;
@@ -245,29 +272,29 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1)
 #pragma unroll
             for (int jj = 0; jj < DB; ++jj) acc[r][jj] = 0.0;
 
-        const uint32_t pitch8 = (uint32_t)p.pitch * 8;
         for (int64_t c = 0; c < p.nchunks; ++c) {
             const int s = (int)(c % stages);
             mbar_wait(&full[s], (uint32_t)(c / stages) & 1u);
             const unsigned char *st = stage0 + (size_t)s * p.stage_bytes;
             const unsigned char *sxl = st + lane * RPT * 8;
             const uint16_t *sbp = reinterpret_cast<const uint16_t *>(st + p.bp_off) + warp * DB;
-            const uint32_t *sen = reinterpret_cast<const uint32_t *>(st + p.en_off);
+            const uint4 *sen = reinterpret_cast<const uint4 *>(st + p.en_off);
             int e = sbp[0];
 #pragma unroll
             for (int jj = 0; jj < DB; ++jj) {
                 const int e1 = sbp[jj + 1];
+                // entry = {tile byte offset, 0, +-1.0}: acc +-= A[rows, k]
+#pragma unroll 1
                 for (; e < e1; ++e) {
-                    const uint32_t w = sen[e];
-                    const unsigned char *src = sxl + (w & 0xffffu) * pitch8;
-                    // +-1.0 from the sign bit: exact, so fma(v, g, acc) == acc +- v
-                    const double g = __hiloint2double((int)((w & 0x80000000u) | 0x3ff00000u), 0);
-                    if (RPT == 2) {
-                        const double2 v = *reinterpret_cast<const double2 *>(src);
-                        acc[0][jj] = fma(v.x, g, acc[0][jj]);
-                        acc[RPT - 1][jj] = fma(v.y, g, acc[RPT - 1][jj]);
-                    } else {
-                        acc[0][jj] = fma(*reinterpret_cast<const double *>(src), g, acc[0][jj]);
+                    const uint4 w = sen[e];
+                    const double g = __hiloint2double((int)w.w, (int)w.z);
+                    const double2 v0 = *reinterpret_cast<const double2 *>(sxl + w.x);
+                    acc[0][jj] = fma(v0.x, g, acc[0][jj]);
+                    acc[1][jj] = fma(v0.y, g, acc[1][jj]);
+                    if (RPT == 4) {
+                        const double2 v1 = *reinterpret_cast<const double2 *>(sxl + w.x + 16);
+                        acc[RPT - 2][jj] = fma(v1.x, g, acc[RPT - 2][jj]);
+                        acc[RPT - 1][jj] = fma(v1.y, g, acc[RPT - 1][jj]);
                     }
                 }
             }
@@ -275,21 +302,22 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1)
             if (lane == 0) mbar_arrive(&empty[s]);
         }
         // epilogue: one final scaling, as the reference (`out *= scale`)
-        const bool vec_ok = RPT == 2 && ((p.lds & 1) == 0) &&
-                            ((reinterpret_cast<uintptr_t>(p.S) & 15) == 0);
+        const bool vec_ok = ((p.lds & 1) == 0) && ((reinterpret_cast<uintptr_t>(p.S) & 15) == 0);
+        const int64_t row = r0 + lane * RPT;
 #pragma unroll
         for (int jj = 0; jj < DB; ++jj) {
             const int j = j0 + warp * DB + jj;
             if (j < p.d) {
                 double *col = p.S + (p.col0 + j) * p.lds;
-                const int64_t row = r0 + lane * RPT;
-                if (vec_ok && row + 1 < p.m_out) {
-                    *reinterpret_cast<double2 *>(col + row) =
-                        make_double2(acc[0][jj] * p.scale, acc[RPT - 1][jj] * p.scale);
-                } else {
 #pragma unroll
-                    for (int r = 0; r < RPT; ++r)
+                for (int r = 0; r < RPT; r += 2) {
+                    if (vec_ok && row + r + 1 < p.m_out) {
+                        *reinterpret_cast<double2 *>(col + row + r) =
+                            make_double2(acc[r][jj] * p.scale, acc[r + 1][jj] * p.scale);
+                    } else {
                         if (row + r < p.m_out) col[row + r] = acc[r][jj] * p.scale;
+                        if (row + r + 1 < p.m_out) col[row + r + 1] = acc[r + 1][jj] * p.scale;
+                    }
                 }
             }
         }
@@ -297,10 +325,12 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1)
 }
 
 template <int RPT, int DB, int NW>
-static int launch(ApplyArgs a, cudaStream_t st) {
+static int launch(ApplyArgs a, const Geom &g, cudaStream_t st) {
     constexpr int TM = 32 * RPT;
     constexpr int SLAB = NW * DB;
-    a.pitch = a.trans ? TM + (RPT == 2 ? 2 : 1) : TM;
+    constexpr int PW = 4;  // producer warps (1 active on the TMA path)
+    HSK_REQUIRE(g.tm == TM, HSK_EINVAL, "sjlt: plan/config mismatch");
+    a.pitch = a.trans ? g.pitch_t : g.pitch_s;
     a.use_tma = a.use_tma && !a.trans;
     CUtensorMap tmap;
     memset(&tmap, 0, sizeof(tmap));
@@ -311,22 +341,22 @@ static int launch(ApplyArgs a, cudaStream_t st) {
     }
     const int a_bytes = (int)roundup((int64_t)a.tk * a.pitch * 8, 128);
     const int bp_bytes = (int)roundup((SLAB + 8) * 2, 128);
-    const int en_bytes = (int)roundup(a.estride * 4, 128);
+    const int en_bytes = (int)roundup(a.estride * 16, 128);
     a.bp_off = a_bytes;
     a.en_off = a_bytes + bp_bytes;
     a.stage_bytes = a_bytes + bp_bytes + en_bytes;
-    const int budget = 220 * 1024;
+    const int budget = 224 * 1024;
     a.stages = std::max(2, std::min(8, (budget - 128) / a.stage_bytes));
     if (a.nchunks > 0 && a.stages > a.nchunks) a.stages = (int)std::max<int64_t>(2, a.nchunks);
     const int smem = 128 + a.stages * a.stage_bytes;
-    auto kern = sjlt_apply_kernel<RPT, DB, NW>;
+    auto kern = sjlt_apply_kernel<RPT, DB, NW, PW>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e != cudaSuccess) return cuda_status(e, "sjlt: set smem attribute");
     a.nslabs = (a.d + SLAB - 1) / SLAB;
     const int64_t tiles = (a.m_out + TM - 1) / TM;
     const int64_t grid = tiles * a.nslabs;
     HSK_REQUIRE(grid < (1ll << 31), HSK_EINVAL, "sjlt: grid too large");
-    kern<<<(unsigned)grid, (NW + 1) * 32, smem, st>>>(a, tmap);
+    kern<<<(unsigned)grid, (NW + PW) * 32, smem, st>>>(a, tmap);
     HSK_CHECK_LAUNCH("sjlt_apply_kernel");
     return HSK_OK;
 }
@@ -364,9 +394,10 @@ extern "C" int hsk_sjlt_plan_build(const int32_t *pos, const int8_t *sgn, int64_
         int p2 = 1;
         while (p2 < g.tk * alpha) p2 <<= 1;
         sjlt::sjlt_plan_kernel<<<(unsigned)g.nchunks, 256, p2 * sizeof(uint32_t), st>>>(
-            pos, sgn, n, d, alpha, g.tk, p2, g.bstride, g.estride,
+            pos, sgn, n, d, alpha, g.tk, p2, g.bstride, g.estride, g.pitch_s, g.pitch_t,
             reinterpret_cast<uint16_t *>(base + g.bptr_off),
-            reinterpret_cast<uint32_t *>(base + g.ent_off), reinterpret_cast<int *>(base + 28));
+            reinterpret_cast<uint4 *>(base + g.ent_off),
+            reinterpret_cast<uint4 *>(base + g.entt_off), reinterpret_cast<int *>(base + 28));
         HSK_CHECK_LAUNCH("sjlt_plan_kernel");
     }
     return HSK_OK;
@@ -410,15 +441,13 @@ extern "C" int hsk_sjlt_apply(const double *A, int64_t rows, int64_t cols, int64
     a.bstride = g.bstride;
     a.estride = g.estride;
     a.bptr = reinterpret_cast<const uint16_t *>(base + g.bptr_off);
-    a.ent = reinterpret_cast<const uint32_t *>(base + g.ent_off);
+    a.ent = reinterpret_cast<const uint4 *>(base + (trans ? g.entt_off : g.ent_off));
     a.scale = scale;
     a.S = S;
     a.lds = lds;
     a.col0 = col0;
     cudaStream_t st = as_stream(stream);
-    const char *cfg = getenv("HSK_SJLT_CFG");  // tuning override: "512" -> RPT 1 x 512 slab
-    if (cfg && cfg[0] == '5' && d > 256) return sjlt::launch<1, 32, 16>(a, st);
-    if (d <= 64) return sjlt::launch<2, 8, 8>(a, st);
-    if (d <= 128) return sjlt::launch<2, 16, 8>(a, st);
-    return sjlt::launch<2, 16, 16>(a, st);
+    if (d <= 64) return sjlt::launch<4, 8, 8>(a, g, st);
+    if (d <= 128) return sjlt::launch<2, 16, 8>(a, g, st);
+    return sjlt::launch<2, 16, 16>(a, g, st);
 }
