@@ -44,15 +44,14 @@ constexpr int64_t kMaxD = (1 << 19);    // bucket index fits 19 bits of the sort
 struct Geom {
     int rpt;           // rows per lane: 4 for d <= 64, else 2
     int tm;            // rows per CTA = 32 * rpt
-    int pitch_s;       // tile pitch (doubles) for S: TMA writes densely
-    int pitch_t;       // tile pitch for S': == 2 mod 16, conflict-free transposing stores
+    int pitch;         // tile pitch (doubles) = tm: TMA writes densely; the S'
+                       // producer orders its transposing stores conflict-free
     int tk;
     int64_t nchunks;
     int64_t bstride;   // uint16 per bucket-offset row
     int64_t estride;   // entries per chunk row (tk*alpha)
     int64_t bptr_off;  // bytes
-    int64_t ent_off;   // bytes: entries for S (pitch kPitchS)
-    int64_t entt_off;  // bytes: entries for S' (pitch kPitchT)
+    int64_t ent_off;   // bytes
     int64_t bytes;
 };
 
@@ -62,7 +61,7 @@ static inline int64_t roundup(int64_t x, int64_t m) { return (x + m - 1) / m * m
 // leaves room for >= 3 stages in shared memory, capped at 128.
 static inline int tk_for(int alpha, int tm) {
     int tk = 128;
-    while (tk > 1 && (tk * alpha > kMaxChunkEntries || tk * ((tm + 2) * 8 + 16 * alpha) > 72 * 1024))
+    while (tk > 1 && (tk * alpha > kMaxChunkEntries || tk * (tm * 8 + 16 * alpha) > 74 * 1024))
         tk >>= 1;
     return tk;
 }
@@ -71,16 +70,14 @@ static Geom geom(int64_t n, int d, int alpha) {
     Geom g;
     g.rpt = d <= 64 ? 4 : 2;
     g.tm = 32 * g.rpt;
-    g.pitch_s = g.tm;
-    g.pitch_t = g.tm + 2;
+    g.pitch = g.tm;
     g.tk = tk_for(alpha, g.tm);
     g.nchunks = (n + g.tk - 1) / g.tk;
     g.bstride = roundup(d, kPlanSlab) + 8;
     g.estride = (int64_t)g.tk * alpha;
     g.bptr_off = kHeaderBytes;
     g.ent_off = roundup(g.bptr_off + (g.nchunks + 1) * g.bstride * 2, 128);
-    g.entt_off = g.ent_off + roundup((g.nchunks + 1) * g.estride * 16, 128);
-    g.bytes = g.entt_off + roundup((g.nchunks + 1) * g.estride * 16, 128);
+    g.bytes = g.ent_off + roundup((g.nchunks + 1) * g.estride * 16, 128);
     return g;
 }
 
@@ -89,9 +86,8 @@ static Geom geom(int64_t n, int d, int alpha) {
 // entry words in that order and per-bucket lower bounds.
 __global__ void sjlt_plan_kernel(const int32_t *__restrict__ pos, const int8_t *__restrict__ sgn,
                                  int64_t n, int d, int alpha, int tk, int p2, int64_t bstride,
-                                 int64_t estride, int pitch_s, int pitch_t,
-                                 uint16_t *__restrict__ bptr, uint4 *__restrict__ ent,
-                                 uint4 *__restrict__ entt, int *err) {
+                                 int64_t estride, int pitch, uint16_t *__restrict__ bptr,
+                                 uint4 *__restrict__ ent, int *err) {
     extern __shared__ uint32_t keys[];
     const int64_t c = blockIdx.x;
     const int64_t k0 = c * tk;
@@ -127,18 +123,15 @@ __global__ void sjlt_plan_kernel(const int32_t *__restrict__ pos, const int8_t *
         }
     }
     uint4 *e_out = ent + c * estride;
-    uint4 *t_out = entt + c * estride;
     for (int e = threadIdx.x; e < estride; e += blockDim.x) {
-        uint4 w = make_uint4(0, 0, 0, 0), wt = w;
+        uint4 w = make_uint4(0, 0, 0, 0);
         if (e < cnt) {
             const int local = keys[e] & 4095;
             const uint32_t kk = (uint32_t)(local / alpha);
             const uint32_t g_hi = sgn[q0 + local] < 0 ? 0xBFF00000u : 0x3FF00000u;  // -1.0 / +1.0
-            w = make_uint4(kk * pitch_s * 8, 0, 0, g_hi);
-            wt = make_uint4(kk * pitch_t * 8, 0, 0, g_hi);
+            w = make_uint4(kk * pitch * 8, 0, 0, g_hi);
         }
         e_out[e] = w;
-        t_out[e] = wt;
     }
     uint16_t *b_out = bptr + c * bstride;
     for (int64_t j = threadIdx.x; j < bstride; j += blockDim.x) {
@@ -154,6 +147,68 @@ __global__ void sjlt_plan_kernel(const int32_t *__restrict__ pos, const int8_t *
         }
         b_out[j] = (uint16_t)lb;
     }
+}
+
+// ------------------------------------------------------- consumer inner loop
+// One bucket's entries [pe, pe_end) (shared byte addresses, 16 B each) folded
+// into the lane's RPT accumulators.  Written in PTX so the loop branches are
+// `bra.uni` (warp-uniform by construction: every lane walks the same entry
+// list), which spares the per-bucket convergence barriers the compiler
+// would otherwise emit.  Per entry: LDS.128 entry, IADD, LDS.128 tile, RPT
+// DFMA with the pre-decoded +-1.0.
+__device__ __forceinline__ void bucket_run2(uint32_t &pe, uint32_t pe_end, uint32_t sxl,
+                                            double &a0, double &a1) {
+    asm volatile(
+        "{\n\t"
+        ".reg .pred p;\n\t"
+        ".reg .b32 o, z, gl, gh, ad;\n\t"
+        ".reg .f64 x, y, g;\n\t"
+        "setp.ge.u32 p, %2, %3;\n\t"
+        "@p bra.uni DONE;\n\t"
+        "LOOP:\n\t"
+        "ld.shared.v4.b32 {o, z, gl, gh}, [%2];\n\t"
+        "add.u32 ad, o, %4;\n\t"
+        "ld.shared.v2.f64 {x, y}, [ad];\n\t"
+        "mov.b64 g, {gl, gh};\n\t"
+        "fma.rn.f64 %0, x, g, %0;\n\t"
+        "fma.rn.f64 %1, y, g, %1;\n\t"
+        "add.u32 %2, %2, 16;\n\t"
+        "setp.lt.u32 p, %2, %3;\n\t"
+        "@p bra.uni LOOP;\n\t"
+        "DONE:\n\t"
+        "}"
+        : "+d"(a0), "+d"(a1), "+r"(pe)
+        : "r"(pe_end), "r"(sxl)
+        : "memory");
+}
+
+__device__ __forceinline__ void bucket_run4(uint32_t &pe, uint32_t pe_end, uint32_t sxl,
+                                            double &a0, double &a1, double &a2, double &a3) {
+    asm volatile(
+        "{\n\t"
+        ".reg .pred p;\n\t"
+        ".reg .b32 o, z, gl, gh, ad;\n\t"
+        ".reg .f64 x, y, u, v, g;\n\t"
+        "setp.ge.u32 p, %4, %5;\n\t"
+        "@p bra.uni DONE;\n\t"
+        "LOOP:\n\t"
+        "ld.shared.v4.b32 {o, z, gl, gh}, [%4];\n\t"
+        "add.u32 ad, o, %6;\n\t"
+        "ld.shared.v2.f64 {x, y}, [ad];\n\t"
+        "ld.shared.v2.f64 {u, v}, [ad+16];\n\t"
+        "mov.b64 g, {gl, gh};\n\t"
+        "fma.rn.f64 %0, x, g, %0;\n\t"
+        "fma.rn.f64 %1, y, g, %1;\n\t"
+        "fma.rn.f64 %2, u, g, %2;\n\t"
+        "fma.rn.f64 %3, v, g, %3;\n\t"
+        "add.u32 %4, %4, 16;\n\t"
+        "setp.lt.u32 p, %4, %5;\n\t"
+        "@p bra.uni LOOP;\n\t"
+        "DONE:\n\t"
+        "}"
+        : "+d"(a0), "+d"(a1), "+d"(a2), "+d"(a3), "+r"(pe)
+        : "r"(pe_end), "r"(sxl)
+        : "memory");
 }
 
 // ----------------------------------------------------------------- apply
@@ -212,9 +267,10 @@ __global__ void __launch_bounds__((NW + PW) * 32, 1)
         const uint32_t bp_bytes = (SLAB + 8) * 2;
         const uint32_t en_bytes = (uint32_t)p.estride * 16;
         const uint32_t tile_bytes = (uint32_t)p.tk * TM * 8;
+        int s = 0;
+        uint32_t ph = 0;  // parity of the empty-barrier phase to wait for
         for (int64_t c = 0; c < p.nchunks; ++c) {
-            const int s = (int)(c % stages);
-            if (c >= stages) mbar_wait(&empty[s], (uint32_t)((c / stages) - 1) & 1u);
+            if (c >= stages) mbar_wait(&empty[s], ph ^ 1u);
             unsigned char *st = stage0 + (size_t)s * p.stage_bytes;
             double *sx = reinterpret_cast<double *>(st);
             uint16_t *sbp = reinterpret_cast<uint16_t *>(st + p.bp_off);
@@ -247,21 +303,26 @@ __global__ void __launch_bounds__((NW + PW) * 32, 1)
                     }
                 } else {
                     // S' tile: element (out row r0+rr, k0+kk) = A[k0+kk, r0+rr].
-                    // Per warp: 16 consecutive k (coalesced 128 B) x 2 rows; the
-                    // pitch (== 2 mod 16 doubles) makes the transposing stores
-                    // two conflict-free wavefronts.
-                    const int kl = lane & 15, rl = lane >> 4;
-                    for (int rb = 2 * pw; rb < TM; rb += 2 * PW) {
+                    // A warp instruction covers 16 consecutive rows x 2 adjacent
+                    // k: the 16 rows land in 16 distinct bank pairs of the
+                    // dense tile (two wavefronts), and each 32-byte sector of
+                    // A is finished by the next instruction (L1-resident).
+                    const int rl = lane & 15, kl = lane >> 4;
+                    for (int rb = 16 * pw; rb < TM; rb += 16 * PW) {
                         const int rr = rb + rl;
                         const bool rv = r0 + rr < p.m_out;
                         const double *col = p.A + (r0 + rr) * p.lda + k0;
-                        for (int kk = kl; kk < p.tk; kk += 16) {
+                        for (int kk = kl; kk < p.tk; kk += 2) {
                             const bool v = rv && (kk < kc);
                             cp_async8(sx + kk * p.pitch + rr, v ? col + kk : p.A, v);
                         }
                     }
                 }
                 cp_async_mbar_arrive(&full[s]);
+            }
+            if (++s == stages) {
+                s = 0;
+                ph ^= 1u;
             }
         }
     } else {
@@ -272,34 +333,39 @@ __global__ void __launch_bounds__((NW + PW) * 32, 1)
 #pragma unroll
             for (int jj = 0; jj < DB; ++jj) acc[r][jj] = 0.0;
 
+        const uint32_t smem_base = smem_u32(stage0);
+        int s = 0;
+        uint32_t ph = 0;
         for (int64_t c = 0; c < p.nchunks; ++c) {
-            const int s = (int)(c % stages);
-            mbar_wait(&full[s], (uint32_t)(c / stages) & 1u);
-            const unsigned char *st = stage0 + (size_t)s * p.stage_bytes;
-            const unsigned char *sxl = st + lane * RPT * 8;
-            const uint16_t *sbp = reinterpret_cast<const uint16_t *>(st + p.bp_off) + warp * DB;
-            const uint4 *sen = reinterpret_cast<const uint4 *>(st + p.en_off);
-            int e = sbp[0];
+            mbar_wait(&full[s], ph);
+            const uint32_t st = smem_base + (uint32_t)s * p.stage_bytes;
+            const uint32_t sxl = st + lane * RPT * 8;
+            const uint16_t *sbp = reinterpret_cast<const uint16_t *>(
+                                      stage0 + (size_t)s * p.stage_bytes + p.bp_off) + warp * DB;
+            const uint32_t sen = st + p.en_off;
+            // bucket bounds as packed u16 pairs (9 registers, one LDS.128 x 2 + LDS)
+            uint32_t bw[(DB + 2) / 2];
+#pragma unroll
+            for (int q = 0; q < (DB + 2) / 2; ++q)
+                bw[q] = reinterpret_cast<const uint32_t *>(sbp)[q];
+            uint32_t pe = sen + 16u * (bw[0] & 0xffffu);
 #pragma unroll
             for (int jj = 0; jj < DB; ++jj) {
-                const int e1 = sbp[jj + 1];
-                // entry = {tile byte offset, 0, +-1.0}: acc +-= A[rows, k]
-#pragma unroll 1
-                for (; e < e1; ++e) {
-                    const uint4 w = sen[e];
-                    const double g = __hiloint2double((int)w.w, (int)w.z);
-                    const double2 v0 = *reinterpret_cast<const double2 *>(sxl + w.x);
-                    acc[0][jj] = fma(v0.x, g, acc[0][jj]);
-                    acc[1][jj] = fma(v0.y, g, acc[1][jj]);
-                    if (RPT == 4) {
-                        const double2 v1 = *reinterpret_cast<const double2 *>(sxl + w.x + 16);
-                        acc[RPT - 2][jj] = fma(v1.x, g, acc[RPT - 2][jj]);
-                        acc[RPT - 1][jj] = fma(v1.y, g, acc[RPT - 1][jj]);
-                    }
-                }
+                const uint32_t b1 = ((jj + 1) & 1) ? (bw[(jj + 1) >> 1] >> 16)
+                                                   : (bw[(jj + 1) >> 1] & 0xffffu);
+                const uint32_t pe_end = sen + 16u * b1;
+                if (RPT == 2)
+                    bucket_run2(pe, pe_end, sxl, acc[0][jj], acc[1][jj]);
+                else
+                    bucket_run4(pe, pe_end, sxl, acc[0][jj], acc[1][jj], acc[RPT - 2][jj],
+                                acc[RPT - 1][jj]);
             }
             __syncwarp();
             if (lane == 0) mbar_arrive(&empty[s]);
+            if (++s == stages) {
+                s = 0;
+                ph ^= 1u;
+            }
         }
         // epilogue: one final scaling, as the reference (`out *= scale`)
         const bool vec_ok = ((p.lds & 1) == 0) && ((reinterpret_cast<uintptr_t>(p.S) & 15) == 0);
@@ -328,9 +394,9 @@ template <int RPT, int DB, int NW>
 static int launch(ApplyArgs a, const Geom &g, cudaStream_t st) {
     constexpr int TM = 32 * RPT;
     constexpr int SLAB = NW * DB;
-    constexpr int PW = 4;  // producer warps (1 active on the TMA path)
+    constexpr int PW = 2;  // producer warps (1 active on the TMA path)
     HSK_REQUIRE(g.tm == TM, HSK_EINVAL, "sjlt: plan/config mismatch");
-    a.pitch = a.trans ? g.pitch_t : g.pitch_s;
+    a.pitch = g.pitch;
     a.use_tma = a.use_tma && !a.trans;
     CUtensorMap tmap;
     memset(&tmap, 0, sizeof(tmap));
@@ -394,10 +460,9 @@ extern "C" int hsk_sjlt_plan_build(const int32_t *pos, const int8_t *sgn, int64_
         int p2 = 1;
         while (p2 < g.tk * alpha) p2 <<= 1;
         sjlt::sjlt_plan_kernel<<<(unsigned)g.nchunks, 256, p2 * sizeof(uint32_t), st>>>(
-            pos, sgn, n, d, alpha, g.tk, p2, g.bstride, g.estride, g.pitch_s, g.pitch_t,
+            pos, sgn, n, d, alpha, g.tk, p2, g.bstride, g.estride, g.pitch,
             reinterpret_cast<uint16_t *>(base + g.bptr_off),
-            reinterpret_cast<uint4 *>(base + g.ent_off),
-            reinterpret_cast<uint4 *>(base + g.entt_off), reinterpret_cast<int *>(base + 28));
+            reinterpret_cast<uint4 *>(base + g.ent_off), reinterpret_cast<int *>(base + 28));
         HSK_CHECK_LAUNCH("sjlt_plan_kernel");
     }
     return HSK_OK;
@@ -441,7 +506,7 @@ extern "C" int hsk_sjlt_apply(const double *A, int64_t rows, int64_t cols, int64
     a.bstride = g.bstride;
     a.estride = g.estride;
     a.bptr = reinterpret_cast<const uint16_t *>(base + g.bptr_off);
-    a.ent = reinterpret_cast<const uint4 *>(base + (trans ? g.entt_off : g.ent_off));
+    a.ent = reinterpret_cast<const uint4 *>(base + g.ent_off);
     a.scale = scale;
     a.S = S;
     a.lds = lds;
