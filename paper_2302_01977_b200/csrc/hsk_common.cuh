@@ -131,4 +131,21 @@ __device__ __forceinline__ void cp_async_mbar_arrive(uint64_t *bar) {
                  : "memory");
 }
 
+// Cluster-wide barrier (all threads of all CTAs in the cluster), with
+// release/acquire so shared-memory writes before it are visible after it.
+__device__ __forceinline__ void cluster_sync() {
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;"
+                 ::: "memory");
+}
+
+// Load a double from the same shared-memory offset in CTA `rank` of the
+// cluster (distributed shared memory).
+__device__ __forceinline__ double ld_dsmem_f64(const double *local, uint32_t rank) {
+    uint32_t remote;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(remote) : "r"(smem_u32(local)), "r"(rank));
+    double v;
+    asm volatile("ld.shared::cluster.f64 %0, [%1];" : "=d"(v) : "r"(remote) : "memory");
+    return v;
+}
+
 }  // namespace hsk

@@ -217,6 +217,8 @@ struct ApplyArgs {
     int64_t lda;
     int trans;
     int use_tma;
+    int mode;       // 0: TMA tile, 1: LDG.128 + transposing STS (S'), 2: 8-byte cp.async
+    int ksplit;     // CTAs of a cluster splitting the k range (DSMEM reduction)
     int64_t m_out;  // output rows (rows of A for trans 0, cols of A for trans 1)
     int64_t n;      // input index extent (= op.n)
     int d, alpha, tk;
@@ -243,19 +245,28 @@ __global__ void __launch_bounds__((NW + PW) * 32, 1)
     unsigned char *stage0 = smem + 128;
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int slab = (int)(blockIdx.x % p.nslabs);
-    const int64_t tile = blockIdx.x / p.nslabs;
+    const int ks = p.ksplit;
+    const int kr = (int)(blockIdx.x % ks);  // == %cluster_ctarank (cluster = ks consecutive CTAs)
+    const int64_t bid = blockIdx.x / ks;
+    const int slab = (int)(bid % p.nslabs);
+    const int64_t tile = bid / p.nslabs;
     const int64_t r0 = tile * TM;
     const int j0 = slab * SLAB;
-    const bool tma = p.use_tma != 0;
+    // chunk range of this CTA
+    const int64_t per = (p.nchunks + ks - 1) / ks;
+    const int64_t c_begin = (int64_t)kr * per < p.nchunks ? (int64_t)kr * per : p.nchunks;
+    const int64_t c_end = c_begin + per < p.nchunks ? c_begin + per : p.nchunks;
+    const int64_t nloc = c_end - c_begin;
+    const int mode = p.mode;
 
     if (threadIdx.x == 0) {
+        const uint32_t fcount = mode == 0 ? 1u : mode == 1 ? 1u + 32u * PW : 32u * PW;
         for (int s = 0; s < p.stages; ++s) {
-            mbar_init(&full[s], tma ? 1 : 32 * PW);
+            mbar_init(&full[s], fcount);
             mbar_init(&empty[s], NW);
         }
         fence_mbar_init();
-        if (tma) prefetch_tmap(&tmap);
+        if (mode == 0) prefetch_tmap(&tmap);
     }
     __syncthreads();
 
@@ -263,97 +274,136 @@ __global__ void __launch_bounds__((NW + PW) * 32, 1)
     if (warp >= NW) {
         // ---------------------------------------------------- producers
         const int pw = warp - NW;
-        if (tma && pw != 0) return;
         const uint32_t bp_bytes = (SLAB + 8) * 2;
         const uint32_t en_bytes = (uint32_t)p.estride * 16;
         const uint32_t tile_bytes = (uint32_t)p.tk * TM * 8;
         int s = 0;
         uint32_t ph = 0;  // parity of the empty-barrier phase to wait for
-        for (int64_t c = 0; c < p.nchunks; ++c) {
-            if (c >= stages) mbar_wait(&empty[s], ph ^ 1u);
-            unsigned char *st = stage0 + (size_t)s * p.stage_bytes;
-            double *sx = reinterpret_cast<double *>(st);
-            uint16_t *sbp = reinterpret_cast<uint16_t *>(st + p.bp_off);
-            uint4 *sen = reinterpret_cast<uint4 *>(st + p.en_off);
-            const int64_t k0 = c * p.tk;
-            const int kc = (int)(p.n - k0 < p.tk ? p.n - k0 : p.tk);
-            const uint16_t *gbp = p.bptr + c * p.bstride + j0;
-            const uint4 *gen = p.ent + c * p.estride;
-            if (tma) {
-                if (lane == 0) {
-                    mbar_arrive_expect_tx(&full[s], tile_bytes + bp_bytes + en_bytes);
-                    tma_load_2d(sx, &tmap, (int)r0, (int)k0, &full[s]);
-                    bulk_g2s(sbp, gbp, bp_bytes, &full[s]);
-                    bulk_g2s(sen, gen, en_bytes, &full[s]);
-                }
-                __syncwarp();
-            } else {
-                const int pl = pw * 32 + lane;  // producer lane id in [0, 32*PW)
-                for (uint32_t i = pl; i < bp_bytes / 16; i += 32 * PW)
-                    cp_async16(sbp + i * 8, gbp + i * 8, true);
-                for (uint32_t i = pl; i < en_bytes / 16; i += 32 * PW)
-                    cp_async16(sen + i, gen + i, true);
-                if (!p.trans) {
-                    // lanes along rows: coalesced global, consecutive smem
-                    for (int idx = pl; idx < p.tk * TM; idx += 32 * PW) {
-                        const int kk = idx / TM, rr = idx % TM;
-                        const bool v = (kk < kc) && (r0 + rr < p.m_out);
-                        const double *src = v ? p.A + (k0 + kk) * p.lda + r0 + rr : p.A;
-                        cp_async8(sx + kk * p.pitch + rr, src, v);
+        if (mode != 0 || pw == 0) {
+            for (int64_t i = 0; i < nloc; ++i) {
+                const int64_t c = c_begin + i;
+                if (i >= stages) mbar_wait(&empty[s], ph ^ 1u);
+                unsigned char *st = stage0 + (size_t)s * p.stage_bytes;
+                double *sx = reinterpret_cast<double *>(st);
+                uint16_t *sbp = reinterpret_cast<uint16_t *>(st + p.bp_off);
+                uint4 *sen = reinterpret_cast<uint4 *>(st + p.en_off);
+                const int64_t k0 = c * p.tk;
+                const int kc = (int)(p.n - k0 < p.tk ? p.n - k0 : p.tk);
+                const uint16_t *gbp = p.bptr + c * p.bstride + j0;
+                const uint4 *gen = p.ent + c * p.estride;
+                if (mode == 0) {
+                    if (lane == 0) {
+                        mbar_arrive_expect_tx(&full[s], tile_bytes + bp_bytes + en_bytes);
+                        tma_load_2d(sx, &tmap, (int)r0, (int)k0, &full[s]);
+                        bulk_g2s(sbp, gbp, bp_bytes, &full[s]);
+                        bulk_g2s(sen, gen, en_bytes, &full[s]);
                     }
-                } else {
-                    // S' tile: element (out row r0+rr, k0+kk) = A[k0+kk, r0+rr].
-                    // A warp instruction covers 16 consecutive rows x 2 adjacent
-                    // k: the 16 rows land in 16 distinct bank pairs of the
-                    // dense tile (two wavefronts), and each 32-byte sector of
-                    // A is finished by the next instruction (L1-resident).
-                    const int rl = lane & 15, kl = lane >> 4;
-                    for (int rb = 16 * pw; rb < TM; rb += 16 * PW) {
-                        const int rr = rb + rl;
-                        const bool rv = r0 + rr < p.m_out;
-                        const double *col = p.A + (r0 + rr) * p.lda + k0;
-                        for (int kk = kl; kk < p.tk; kk += 2) {
-                            const bool v = rv && (kk < kc);
-                            cp_async8(sx + kk * p.pitch + rr, v ? col + kk : p.A, v);
+                    __syncwarp();
+                } else if (mode == 1) {
+                    // S' tile X[kk][rr] = A[k0+kk, r0+rr] (A columns are contiguous
+                    // in kk).  Lanes = 32 consecutive output rows rr; each lane
+                    // reads one full 32-byte sector (4 consecutive kk, two
+                    // LDG.128) and scatters it with 4 conflict-free STS.64.
+                    if (pw == 0 && lane == 0) {
+                        mbar_arrive_expect_tx(&full[s], bp_bytes + en_bytes);
+                        bulk_g2s(sbp, gbp, bp_bytes, &full[s]);
+                        bulk_g2s(sen, gen, en_bytes, &full[s]);
+                    }
+                    constexpr int GR = TM / 32;  // 32-row groups
+                    constexpr int PU = 2;        // items in flight per lane
+                    const int items = GR * (p.tk / 4);
+                    for (int it0 = pw * PU; it0 < items; it0 += PU * PW) {
+                        double2 v[PU][2];
+#pragma unroll
+                        for (int u = 0; u < PU; ++u) {
+                            const int it = it0 + u;
+                            const int g = it % GR, q = it / GR;
+                            const int rr = g * 32 + lane, kk = 4 * q;
+                            const bool rv = (it < items) && (r0 + rr < p.m_out);
+                            const double *src = p.A + (r0 + rr) * p.lda + k0 + kk;
+                            if (rv && kk + 4 <= kc) {
+                                v[u][0] = __ldg(reinterpret_cast<const double2 *>(src));
+                                v[u][1] = __ldg(reinterpret_cast<const double2 *>(src) + 1);
+                            } else {
+                                double t[4];
+#pragma unroll
+                                for (int w = 0; w < 4; ++w) t[w] = (rv && kk + w < kc) ? src[w] : 0.0;
+                                v[u][0] = make_double2(t[0], t[1]);
+                                v[u][1] = make_double2(t[2], t[3]);
+                            }
+                        }
+#pragma unroll
+                        for (int u = 0; u < PU; ++u) {
+                            const int it = it0 + u;
+                            if (it < items) {
+                                const int g = it % GR, q = it / GR;
+                                double *dst = sx + (4 * q) * p.pitch + g * 32 + lane;
+                                dst[0] = v[u][0].x;
+                                dst[p.pitch] = v[u][0].y;
+                                dst[2 * p.pitch] = v[u][1].x;
+                                dst[3 * p.pitch] = v[u][1].y;
+                            }
                         }
                     }
+                    mbar_arrive(&full[s]);  // release: this lane's stores
+                } else {
+                    const int pl = pw * 32 + lane;  // producer lane id in [0, 32*PW)
+                    for (uint32_t q = pl; q < bp_bytes / 16; q += 32 * PW)
+                        cp_async16(sbp + q * 8, gbp + q * 8, true);
+                    for (uint32_t q = pl; q < en_bytes / 16; q += 32 * PW)
+                        cp_async16(sen + q, gen + q, true);
+                    for (int idx = pl; idx < p.tk * TM; idx += 32 * PW) {
+                        int kk, rr;
+                        const double *src;
+                        if (!p.trans) {  // lanes along rows: coalesced global
+                            kk = idx / TM;
+                            rr = idx % TM;
+                            src = p.A + (k0 + kk) * p.lda + r0 + rr;
+                        } else {         // lanes along k: coalesced global
+                            rr = idx / p.tk;
+                            kk = idx % p.tk;
+                            src = p.A + (r0 + rr) * p.lda + k0 + kk;
+                        }
+                        const bool v = (kk < kc) && (r0 + rr < p.m_out);
+                        cp_async8(sx + kk * p.pitch + rr, v ? src : p.A, v);
+                    }
+                    cp_async_mbar_arrive(&full[s]);
                 }
-                cp_async_mbar_arrive(&full[s]);
-            }
-            if (++s == stages) {
-                s = 0;
-                ph ^= 1u;
+                if (++s == stages) {
+                    s = 0;
+                    ph ^= 1u;
+                }
             }
         }
-    } else {
-        // ---------------------------------------------------- consumers
-        double acc[RPT][DB];
-#pragma unroll
-        for (int r = 0; r < RPT; ++r)
-#pragma unroll
-            for (int jj = 0; jj < DB; ++jj) acc[r][jj] = 0.0;
+        if (ks > 1) {  // match the consumers' barriers of the k-split reduction
+            __syncthreads();
+            cluster_sync();
+            cluster_sync();
+        }
+        return;
+    }
 
+    // -------------------------------------------------------- consumers
+    double acc[RPT][DB];
+#pragma unroll
+    for (int r = 0; r < RPT; ++r)
+#pragma unroll
+        for (int jj = 0; jj < DB; ++jj) acc[r][jj] = 0.0;
+    {
         const uint32_t smem_base = smem_u32(stage0);
         int s = 0;
         uint32_t ph = 0;
-        for (int64_t c = 0; c < p.nchunks; ++c) {
+        for (int64_t i = 0; i < nloc; ++i) {
             mbar_wait(&full[s], ph);
             const uint32_t st = smem_base + (uint32_t)s * p.stage_bytes;
             const uint32_t sxl = st + lane * RPT * 8;
             const uint16_t *sbp = reinterpret_cast<const uint16_t *>(
                                       stage0 + (size_t)s * p.stage_bytes + p.bp_off) + warp * DB;
             const uint32_t sen = st + p.en_off;
-            // bucket bounds as packed u16 pairs (9 registers, one LDS.128 x 2 + LDS)
-            uint32_t bw[(DB + 2) / 2];
-#pragma unroll
-            for (int q = 0; q < (DB + 2) / 2; ++q)
-                bw[q] = reinterpret_cast<const uint32_t *>(sbp)[q];
-            uint32_t pe = sen + 16u * (bw[0] & 0xffffu);
+            uint32_t pe = sen + 16u * (uint32_t)sbp[0];
 #pragma unroll
             for (int jj = 0; jj < DB; ++jj) {
-                const uint32_t b1 = ((jj + 1) & 1) ? (bw[(jj + 1) >> 1] >> 16)
-                                                   : (bw[(jj + 1) >> 1] & 0xffffu);
-                const uint32_t pe_end = sen + 16u * b1;
+                const uint32_t pe_end = sen + 16u * (uint32_t)sbp[jj + 1];
                 if (RPT == 2)
                     bucket_run2(pe, pe_end, sxl, acc[0][jj], acc[1][jj]);
                 else
@@ -367,23 +417,51 @@ __global__ void __launch_bounds__((NW + PW) * 32, 1)
                 ph ^= 1u;
             }
         }
-        // epilogue: one final scaling, as the reference (`out *= scale`)
-        const bool vec_ok = ((p.lds & 1) == 0) && ((reinterpret_cast<uintptr_t>(p.S) & 15) == 0);
-        const int64_t row = r0 + lane * RPT;
+    }
+
+    // ------------------------------------------- k-split: DSMEM reduction
+    // Partial sums of the ks CTAs of a cluster are combined by rank 0 in
+    // rank order (deterministic).  The stage ring is reused as the buffer.
+    double *red = reinterpret_cast<double *>(stage0);
+    if (ks > 1) {
+        __syncthreads();  // every stage consumed: the ring is free
+        if (kr > 0) {
 #pragma unroll
-        for (int jj = 0; jj < DB; ++jj) {
-            const int j = j0 + warp * DB + jj;
-            if (j < p.d) {
-                double *col = p.S + (p.col0 + j) * p.lds;
+            for (int jj = 0; jj < DB; ++jj)
 #pragma unroll
-                for (int r = 0; r < RPT; r += 2) {
-                    if (vec_ok && row + r + 1 < p.m_out) {
-                        *reinterpret_cast<double2 *>(col + row + r) =
-                            make_double2(acc[r][jj] * p.scale, acc[r + 1][jj] * p.scale);
-                    } else {
-                        if (row + r < p.m_out) col[row + r] = acc[r][jj] * p.scale;
-                        if (row + r + 1 < p.m_out) col[row + r + 1] = acc[r + 1][jj] * p.scale;
-                    }
+                for (int r = 0; r < RPT; ++r)
+                    red[((warp * DB + jj) * RPT + r) * 32 + lane] = acc[r][jj];
+        }
+        cluster_sync();
+        if (kr == 0) {
+            for (int q = 1; q < ks; ++q) {
+#pragma unroll
+                for (int jj = 0; jj < DB; ++jj)
+#pragma unroll
+                    for (int r = 0; r < RPT; ++r)
+                        acc[r][jj] += ld_dsmem_f64(&red[((warp * DB + jj) * RPT + r) * 32 + lane], q);
+            }
+        }
+        cluster_sync();
+        if (kr > 0) return;
+    }
+
+    // epilogue: one final scaling, as the reference (`out *= scale`)
+    const bool vec_ok = ((p.lds & 1) == 0) && ((reinterpret_cast<uintptr_t>(p.S) & 15) == 0);
+    const int64_t row = r0 + lane * RPT;
+#pragma unroll
+    for (int jj = 0; jj < DB; ++jj) {
+        const int j = j0 + warp * DB + jj;
+        if (j < p.d) {
+            double *col = p.S + (p.col0 + j) * p.lds;
+#pragma unroll
+            for (int r = 0; r < RPT; r += 2) {
+                if (vec_ok && row + r + 1 < p.m_out) {
+                    *reinterpret_cast<double2 *>(col + row + r) =
+                        make_double2(acc[r][jj] * p.scale, acc[r + 1][jj] * p.scale);
+                } else {
+                    if (row + r < p.m_out) col[row + r] = acc[r][jj] * p.scale;
+                    if (row + r + 1 < p.m_out) col[row + r + 1] = acc[r + 1][jj] * p.scale;
                 }
             }
         }
@@ -397,10 +475,11 @@ static int launch(ApplyArgs a, const Geom &g, cudaStream_t st) {
     constexpr int PW = 2;  // producer warps (1 active on the TMA path)
     HSK_REQUIRE(g.tm == TM, HSK_EINVAL, "sjlt: plan/config mismatch");
     a.pitch = g.pitch;
-    a.use_tma = a.use_tma && !a.trans;
+    const bool aligned = a.use_tma != 0;  // 16-byte aligned columns (lda even)
+    a.mode = aligned ? (a.trans ? 1 : 0) : 2;
     CUtensorMap tmap;
     memset(&tmap, 0, sizeof(tmap));
-    if (a.use_tma) {
+    if (a.mode == 0) {
         int rc = make_tmap_f64_2d(&tmap, a.A, (uint64_t)a.m_out, (uint64_t)a.n, (uint64_t)a.lda,
                                   TM, (uint32_t)a.tk);
         if (rc) return rc;
@@ -411,18 +490,42 @@ static int launch(ApplyArgs a, const Geom &g, cudaStream_t st) {
     a.bp_off = a_bytes;
     a.en_off = a_bytes + bp_bytes;
     a.stage_bytes = a_bytes + bp_bytes + en_bytes;
+    a.nslabs = (a.d + SLAB - 1) / SLAB;
+    const int64_t tiles = (a.m_out + TM - 1) / TM;
+    // k-split across a cluster when the tile grid cannot fill the GPU
+    int ks = 1;
+    const int64_t ctas = tiles * a.nslabs;
+    if (ctas < sm_count()) {
+        ks = (int)std::min<int64_t>(8, sm_count() / ctas);
+        while (ks > 1 && a.nchunks / ks < 8) --ks;
+        if (ks == 3 || ks == 5 || ks == 6 || ks == 7) ks = ks >= 4 ? 4 : 2;
+    }
+    a.ksplit = ks;
+    const int per = (int)((a.nchunks + ks - 1) / ks);
     const int budget = 224 * 1024;
     a.stages = std::max(2, std::min(8, (budget - 128) / a.stage_bytes));
-    if (a.nchunks > 0 && a.stages > a.nchunks) a.stages = (int)std::max<int64_t>(2, a.nchunks);
-    const int smem = 128 + a.stages * a.stage_bytes;
+    if (per > 0 && a.stages > per) a.stages = std::max(2, per);
+    int smem = 128 + a.stages * a.stage_bytes;
+    if (ks > 1) smem = std::max(smem, 128 + NW * DB * RPT * 32 * 8);
     auto kern = sjlt_apply_kernel<RPT, DB, NW, PW>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e != cudaSuccess) return cuda_status(e, "sjlt: set smem attribute");
-    a.nslabs = (a.d + SLAB - 1) / SLAB;
-    const int64_t tiles = (a.m_out + TM - 1) / TM;
-    const int64_t grid = tiles * a.nslabs;
+    const int64_t grid = tiles * a.nslabs * ks;
     HSK_REQUIRE(grid < (1ll << 31), HSK_EINVAL, "sjlt: grid too large");
-    kern<<<(unsigned)grid, (NW + PW) * 32, smem, st>>>(a, tmap);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)grid, 1, 1);
+    cfg.blockDim = dim3((NW + PW) * 32, 1, 1);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = ks;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    e = cudaLaunchKernelEx(&cfg, kern, a, tmap);
+    if (e != cudaSuccess) return cuda_status(e, "sjlt_apply_kernel launch");
     HSK_CHECK_LAUNCH("sjlt_apply_kernel");
     return HSK_OK;
 }
@@ -512,7 +615,7 @@ extern "C" int hsk_sjlt_apply(const double *A, int64_t rows, int64_t cols, int64
     a.lds = lds;
     a.col0 = col0;
     cudaStream_t st = as_stream(stream);
-    if (d <= 64) return sjlt::launch<4, 8, 8>(a, g, st);
+    if (d <= 64) return sjlt::launch<4, 4, 16>(a, g, st);
     if (d <= 128) return sjlt::launch<2, 16, 8>(a, g, st);
     return sjlt::launch<2, 16, 16>(a, g, st);
 }
