@@ -129,7 +129,8 @@ __global__ void sjlt_plan_kernel(const int32_t *__restrict__ pos, const int8_t *
             const int local = keys[e] & 4095;
             const uint32_t kk = (uint32_t)(local / alpha);
             const uint32_t g_hi = sgn[q0 + local] < 0 ? 0xBFF00000u : 0x3FF00000u;  // -1.0 / +1.0
-            w = make_uint4(kk * pitch * 8, 0, 0, g_hi);
+            // .y: byte XOR of the S' tile swizzle (row ^ (kk mod 32))
+            w = make_uint4(kk * pitch * 8, (kk & 31u) * 8u, 0, g_hi);
         }
         e_out[e] = w;
     }
@@ -211,13 +212,80 @@ __device__ __forceinline__ void bucket_run4(uint32_t &pe, uint32_t pe_end, uint3
         : "memory");
 }
 
+// S' tiles are stored swizzled: element (kk, row) lives at kk*TM + (row ^ (kk%32))
+// so that the transposing 8-byte cp.async writes (lanes along kk) and the
+// consumer reads (lanes along rows) are both conflict-free.  A lane owns
+// rows lane + 32*r, r < RPT; entry .y holds the XOR term (kk%32)*8.
+__device__ __forceinline__ void bucket_run_t2(uint32_t &pe, uint32_t pe_end, uint32_t st,
+                                              uint32_t lane8, double &a0, double &a1) {
+    asm volatile(
+        "{\n\t"
+        ".reg .pred p;\n\t"
+        ".reg .b32 o, x, gl, gh, ad;\n\t"
+        ".reg .f64 u, v, g;\n\t"
+        "setp.ge.u32 p, %2, %3;\n\t"
+        "@p bra.uni DONE;\n\t"
+        "LOOP:\n\t"
+        "ld.shared.v4.b32 {o, x, gl, gh}, [%2];\n\t"
+        "xor.b32 ad, x, %5;\n\t"
+        "add.u32 ad, ad, o;\n\t"
+        "add.u32 ad, ad, %4;\n\t"
+        "ld.shared.f64 u, [ad];\n\t"
+        "ld.shared.f64 v, [ad+256];\n\t"
+        "mov.b64 g, {gl, gh};\n\t"
+        "fma.rn.f64 %0, u, g, %0;\n\t"
+        "fma.rn.f64 %1, v, g, %1;\n\t"
+        "add.u32 %2, %2, 16;\n\t"
+        "setp.lt.u32 p, %2, %3;\n\t"
+        "@p bra.uni LOOP;\n\t"
+        "DONE:\n\t"
+        "}"
+        : "+d"(a0), "+d"(a1), "+r"(pe)
+        : "r"(pe_end), "r"(st), "r"(lane8)
+        : "memory");
+}
+
+__device__ __forceinline__ void bucket_run_t4(uint32_t &pe, uint32_t pe_end, uint32_t st,
+                                              uint32_t lane8, double &a0, double &a1,
+                                              double &a2, double &a3) {
+    asm volatile(
+        "{\n\t"
+        ".reg .pred p;\n\t"
+        ".reg .b32 o, x, gl, gh, ad;\n\t"
+        ".reg .f64 u, v, w, y, g;\n\t"
+        "setp.ge.u32 p, %4, %5;\n\t"
+        "@p bra.uni DONE;\n\t"
+        "LOOP:\n\t"
+        "ld.shared.v4.b32 {o, x, gl, gh}, [%4];\n\t"
+        "xor.b32 ad, x, %7;\n\t"
+        "add.u32 ad, ad, o;\n\t"
+        "add.u32 ad, ad, %6;\n\t"
+        "ld.shared.f64 u, [ad];\n\t"
+        "ld.shared.f64 v, [ad+256];\n\t"
+        "ld.shared.f64 w, [ad+512];\n\t"
+        "ld.shared.f64 y, [ad+768];\n\t"
+        "mov.b64 g, {gl, gh};\n\t"
+        "fma.rn.f64 %0, u, g, %0;\n\t"
+        "fma.rn.f64 %1, v, g, %1;\n\t"
+        "fma.rn.f64 %2, w, g, %2;\n\t"
+        "fma.rn.f64 %3, y, g, %3;\n\t"
+        "add.u32 %4, %4, 16;\n\t"
+        "setp.lt.u32 p, %4, %5;\n\t"
+        "@p bra.uni LOOP;\n\t"
+        "DONE:\n\t"
+        "}"
+        : "+d"(a0), "+d"(a1), "+d"(a2), "+d"(a3), "+r"(pe)
+        : "r"(pe_end), "r"(st), "r"(lane8)
+        : "memory");
+}
+
 // ----------------------------------------------------------------- apply
 struct ApplyArgs {
     const double *A;
     int64_t lda;
     int trans;
     int use_tma;
-    int mode;       // 0: TMA tile, 1: LDG.128 + transposing STS (S'), 2: 8-byte cp.async
+    int mode;       // 0: TMA tile (S), 1: swizzled transposing cp.async (S'), 2: cp.async (S)
     int ksplit;     // CTAs of a cluster splitting the k range (DSMEM reduction)
     int64_t m_out;  // output rows (rows of A for trans 0, cols of A for trans 1)
     int64_t n;      // input index extent (= op.n)
@@ -234,7 +302,7 @@ struct ApplyArgs {
 
 // Warp roles: warps [0, NW) consume (bucket owners), warps [NW, NW+PW)
 // produce.  Lane l owns rows RPT*l .. RPT*l+RPT-1 of the TM-row tile.
-template <int RPT, int DB, int NW, int PW>
+template <int RPT, int DB, int NW, int PW, bool TRANS>
 __global__ void __launch_bounds__((NW + PW) * 32, 1)
     sjlt_apply_kernel(const ApplyArgs p, const __grid_constant__ CUtensorMap tmap) {
     constexpr int TM = 32 * RPT;
@@ -260,7 +328,7 @@ __global__ void __launch_bounds__((NW + PW) * 32, 1)
     const int mode = p.mode;
 
     if (threadIdx.x == 0) {
-        const uint32_t fcount = mode == 0 ? 1u : mode == 1 ? 1u + 32u * PW : 32u * PW;
+        const uint32_t fcount = mode == 0 ? 1u : mode == 1 ? 1u + 32u * PW : 32u * PW;  // S': bulk + noinc
         for (int s = 0; s < p.stages; ++s) {
             mbar_init(&full[s], fcount);
             mbar_init(&empty[s], NW);
@@ -299,53 +367,24 @@ __global__ void __launch_bounds__((NW + PW) * 32, 1)
                         bulk_g2s(sen, gen, en_bytes, &full[s]);
                     }
                     __syncwarp();
-                } else if (mode == 1) {
-                    // S' tile X[kk][rr] = A[k0+kk, r0+rr] (A columns are contiguous
-                    // in kk).  Lanes = 32 consecutive output rows rr; each lane
-                    // reads one full 32-byte sector (4 consecutive kk, two
-                    // LDG.128) and scatters it with 4 conflict-free STS.64.
+                } else if (TRANS) {
+                    // S' tile: element (kk, rr) = A[k0+kk, r0+rr], stored at
+                    // kk*TM + (rr ^ (kk%32)).  Lanes run along kk (256 B of one
+                    // column of A per instruction); the swizzle spreads the
+                    // 32 stores over all bank pairs.
                     if (pw == 0 && lane == 0) {
                         mbar_arrive_expect_tx(&full[s], bp_bytes + en_bytes);
                         bulk_g2s(sbp, gbp, bp_bytes, &full[s]);
                         bulk_g2s(sen, gen, en_bytes, &full[s]);
                     }
-                    constexpr int GR = TM / 32;  // 32-row groups
-                    constexpr int PU = 2;        // items in flight per lane
-                    const int items = GR * (p.tk / 4);
-                    for (int it0 = pw * PU; it0 < items; it0 += PU * PW) {
-                        double2 v[PU][2];
-#pragma unroll
-                        for (int u = 0; u < PU; ++u) {
-                            const int it = it0 + u;
-                            const int g = it % GR, q = it / GR;
-                            const int rr = g * 32 + lane, kk = 4 * q;
-                            const bool rv = (it < items) && (r0 + rr < p.m_out);
-                            const double *src = p.A + (r0 + rr) * p.lda + k0 + kk;
-                            if (rv && kk + 4 <= kc) {
-                                v[u][0] = __ldg(reinterpret_cast<const double2 *>(src));
-                                v[u][1] = __ldg(reinterpret_cast<const double2 *>(src) + 1);
-                            } else {
-                                double t[4];
-#pragma unroll
-                                for (int w = 0; w < 4; ++w) t[w] = (rv && kk + w < kc) ? src[w] : 0.0;
-                                v[u][0] = make_double2(t[0], t[1]);
-                                v[u][1] = make_double2(t[2], t[3]);
-                            }
-                        }
-#pragma unroll
-                        for (int u = 0; u < PU; ++u) {
-                            const int it = it0 + u;
-                            if (it < items) {
-                                const int g = it % GR, q = it / GR;
-                                double *dst = sx + (4 * q) * p.pitch + g * 32 + lane;
-                                dst[0] = v[u][0].x;
-                                dst[p.pitch] = v[u][0].y;
-                                dst[2 * p.pitch] = v[u][1].x;
-                                dst[3 * p.pitch] = v[u][1].y;
-                            }
-                        }
+                    const int pl = pw * 32 + lane;
+                    for (int idx = pl; idx < p.tk * TM; idx += 32 * PW) {
+                        const int rr = idx / p.tk, kk = idx % p.tk;
+                        const bool v = (kk < kc) && (r0 + rr < p.m_out);
+                        const double *src = p.A + (r0 + rr) * p.lda + k0 + kk;
+                        cp_async8(sx + kk * TM + (rr ^ (kk & 31)), v ? src : p.A, v);
                     }
-                    mbar_arrive(&full[s]);  // release: this lane's stores
+                    cp_async_mbar_arrive(&full[s]);
                 } else {
                     const int pl = pw * 32 + lane;  // producer lane id in [0, 32*PW)
                     for (uint32_t q = pl; q < bp_bytes / 16; q += 32 * PW)
@@ -404,11 +443,18 @@ __global__ void __launch_bounds__((NW + PW) * 32, 1)
 #pragma unroll
             for (int jj = 0; jj < DB; ++jj) {
                 const uint32_t pe_end = sen + 16u * (uint32_t)sbp[jj + 1];
-                if (RPT == 2)
+                if (TRANS) {
+                    if (RPT == 2)
+                        bucket_run_t2(pe, pe_end, st, lane * 8u, acc[0][jj], acc[1][jj]);
+                    else
+                        bucket_run_t4(pe, pe_end, st, lane * 8u, acc[0][jj], acc[1][jj],
+                                      acc[RPT - 2][jj], acc[RPT - 1][jj]);
+                } else if (RPT == 2) {
                     bucket_run2(pe, pe_end, sxl, acc[0][jj], acc[1][jj]);
-                else
+                } else {
                     bucket_run4(pe, pe_end, sxl, acc[0][jj], acc[1][jj], acc[RPT - 2][jj],
                                 acc[RPT - 1][jj]);
+                }
             }
             __syncwarp();
             if (lane == 0) mbar_arrive(&empty[s]);
@@ -448,20 +494,28 @@ __global__ void __launch_bounds__((NW + PW) * 32, 1)
 
     // epilogue: one final scaling, as the reference (`out *= scale`)
     const bool vec_ok = ((p.lds & 1) == 0) && ((reinterpret_cast<uintptr_t>(p.S) & 15) == 0);
-    const int64_t row = r0 + lane * RPT;
 #pragma unroll
     for (int jj = 0; jj < DB; ++jj) {
         const int j = j0 + warp * DB + jj;
         if (j < p.d) {
             double *col = p.S + (p.col0 + j) * p.lds;
+            if (TRANS) {  // lane owns rows lane + 32 r
 #pragma unroll
-            for (int r = 0; r < RPT; r += 2) {
-                if (vec_ok && row + r + 1 < p.m_out) {
-                    *reinterpret_cast<double2 *>(col + row + r) =
-                        make_double2(acc[r][jj] * p.scale, acc[r + 1][jj] * p.scale);
-                } else {
-                    if (row + r < p.m_out) col[row + r] = acc[r][jj] * p.scale;
-                    if (row + r + 1 < p.m_out) col[row + r + 1] = acc[r + 1][jj] * p.scale;
+                for (int r = 0; r < RPT; ++r) {
+                    const int64_t row = r0 + lane + 32 * r;
+                    if (row < p.m_out) col[row] = acc[r][jj] * p.scale;
+                }
+            } else {      // lane owns rows RPT*lane + r
+                const int64_t row = r0 + lane * RPT;
+#pragma unroll
+                for (int r = 0; r < RPT; r += 2) {
+                    if (vec_ok && row + r + 1 < p.m_out) {
+                        *reinterpret_cast<double2 *>(col + row + r) =
+                            make_double2(acc[r][jj] * p.scale, acc[r + 1][jj] * p.scale);
+                    } else {
+                        if (row + r < p.m_out) col[row + r] = acc[r][jj] * p.scale;
+                        if (row + r + 1 < p.m_out) col[row + r + 1] = acc[r + 1][jj] * p.scale;
+                    }
                 }
             }
         }
@@ -476,7 +530,7 @@ static int launch(ApplyArgs a, const Geom &g, cudaStream_t st) {
     HSK_REQUIRE(g.tm == TM, HSK_EINVAL, "sjlt: plan/config mismatch");
     a.pitch = g.pitch;
     const bool aligned = a.use_tma != 0;  // 16-byte aligned columns (lda even)
-    a.mode = aligned ? (a.trans ? 1 : 0) : 2;
+    a.mode = a.trans ? 1 : (aligned ? 0 : 2);
     CUtensorMap tmap;
     memset(&tmap, 0, sizeof(tmap));
     if (a.mode == 0) {
@@ -507,7 +561,8 @@ static int launch(ApplyArgs a, const Geom &g, cudaStream_t st) {
     if (per > 0 && a.stages > per) a.stages = std::max(2, per);
     int smem = 128 + a.stages * a.stage_bytes;
     if (ks > 1) smem = std::max(smem, 128 + NW * DB * RPT * 32 * 8);
-    auto kern = sjlt_apply_kernel<RPT, DB, NW, PW>;
+    auto kern = a.trans ? sjlt_apply_kernel<RPT, DB, NW, PW, true>
+                        : sjlt_apply_kernel<RPT, DB, NW, PW, false>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e != cudaSuccess) return cuda_status(e, "sjlt: set smem attribute");
     const int64_t grid = tiles * a.nslabs * ks;
