@@ -61,7 +61,7 @@ static inline int64_t roundup(int64_t x, int64_t m) { return (x + m - 1) / m * m
 // leaves room for >= 3 stages in shared memory, capped at 128.
 static inline int tk_for(int alpha, int tm) {
     int tk = 128;
-    while (tk > 1 && (tk * alpha > kMaxChunkEntries || tk * (tm * 8 + 16 * alpha) > 74 * 1024))
+    while (tk > 1 && (tk * alpha > kMaxChunkEntries || tk * (tm * 8 + 16 * alpha) > 72 * 1024))
         tk >>= 1;
     return tk;
 }
@@ -150,136 +150,52 @@ __global__ void sjlt_plan_kernel(const int32_t *__restrict__ pos, const int8_t *
     }
 }
 
-// ------------------------------------------------------- consumer inner loop
-// One bucket's entries [pe, pe_end) (shared byte addresses, 16 B each) folded
-// into the lane's RPT accumulators.  Written in PTX so the loop branches are
-// `bra.uni` (warp-uniform by construction: every lane walks the same entry
-// list), which spares the per-bucket convergence barriers the compiler
-// would otherwise emit.  Per entry: LDS.128 entry, IADD, LDS.128 tile, RPT
-// DFMA with the pre-decoded +-1.0.
-__device__ __forceinline__ void bucket_run2(uint32_t &pe, uint32_t pe_end, uint32_t sxl,
-                                            double &a0, double &a1) {
-    asm volatile(
-        "{\n\t"
-        ".reg .pred p;\n\t"
-        ".reg .b32 o, z, gl, gh, ad;\n\t"
-        ".reg .f64 x, y, g;\n\t"
-        "setp.ge.u32 p, %2, %3;\n\t"
-        "@p bra.uni DONE;\n\t"
-        "LOOP:\n\t"
-        "ld.shared.v4.b32 {o, z, gl, gh}, [%2];\n\t"
-        "add.u32 ad, o, %4;\n\t"
-        "ld.shared.v2.f64 {x, y}, [ad];\n\t"
-        "mov.b64 g, {gl, gh};\n\t"
-        "fma.rn.f64 %0, x, g, %0;\n\t"
-        "fma.rn.f64 %1, y, g, %1;\n\t"
-        "add.u32 %2, %2, 16;\n\t"
-        "setp.lt.u32 p, %2, %3;\n\t"
-        "@p bra.uni LOOP;\n\t"
-        "DONE:\n\t"
-        "}"
-        : "+d"(a0), "+d"(a1), "+r"(pe)
-        : "r"(pe_end), "r"(sxl)
-        : "memory");
+// ------------------------------------------------------------------ apply
+//
+// Stage layout in shared memory (per ring slot):
+//   [A tile: TK rows of TM doubles][zero row: TM doubles][bucket bounds]
+//   [entries: estride + 1 words of 16 B; the last is the null entry]
+// The null entry {offset of the zero row, 0, +1.0} lets a warp fold the
+// FIRST entry of every bucket in a batch without predication: empty
+// buckets read the zero row and add +0.0.
+//
+// Lane -> tile rows.  S tiles (dense, TMA-written): RPT = 2 -> rows 2l, 2l+1
+// (one LDS.128); RPT = 4 -> rows 2l, 2l+1, 64+2l, 64+2l+1 (two LDS.128, each
+// a contiguous 512 B).  S' tiles (swizzled, element (kk,row) at
+// kk*TM + (row ^ (kk%32))): rows l + 32 r (LDS.64 each, conflict-free).
+
+// Remaining entries [pe, pend) of one bucket (shared byte addresses), two
+// per iteration.  `bra.uni`: every lane walks the same list.
+// run_s*: S tiles, rows {2l, 2l+1} at [sx + o] (and {64+2l, 64+2l+1} at +512).
+// run_t*: S' tiles, rows l + 32 r at st + o + (x ^ lane8) + 256 r.
+__device__ __forceinline__ void run_s2(uint32_t pe, uint32_t pend, uint32_t sx, double &c0, double &c1) {
+    asm volatile("{\n\t.reg .pred p;\n\t.reg .b32 o0, x0, l0, h0, o1, x1, l1, h1, a0, a1, t;\n\t.reg .f64 u0, v0, u1, v1, g0, g1;\n\tsetp.ge.u32 p, %0, %3;\n\t@p bra.uni DONE;\n\tadd.u32 t, %0, 16;\n\tsetp.ge.u32 p, t, %3;\n\t@p bra.uni ONE;\n\tPAIR:\n\tld.shared.v4.b32 {o0, x0, l0, h0}, [%0];\n\tld.shared.v4.b32 {o1, x1, l1, h1}, [%0+16];\n\tadd.u32 a0, o0, %4;\n\tld.shared.v2.f64 {u0, v0}, [a0];\n\tmov.b64 g0, {l0, h0};\n\tadd.u32 a1, o1, %4;\n\tld.shared.v2.f64 {u1, v1}, [a1];\n\tmov.b64 g1, {l1, h1};\n\tfma.rn.f64 %1, u0, g0, %1;\n\tfma.rn.f64 %2, v0, g0, %2;\n\tfma.rn.f64 %1, u1, g1, %1;\n\tfma.rn.f64 %2, v1, g1, %2;\n\tadd.u32 %0, %0, 32;\n\tadd.u32 t, %0, 16;\n\tsetp.lt.u32 p, t, %3;\n\t@p bra.uni PAIR;\n\tsetp.ge.u32 p, %0, %3;\n\t@p bra.uni DONE;\n\tONE:\n\tld.shared.v4.b32 {o0, x0, l0, h0}, [%0];\n\tadd.u32 a0, o0, %4;\n\tld.shared.v2.f64 {u0, v0}, [a0];\n\tmov.b64 g0, {l0, h0};\n\tfma.rn.f64 %1, u0, g0, %1;\n\tfma.rn.f64 %2, v0, g0, %2;\n\tDONE:\n\t}"
+                 : "+r"(pe), "+d"(c0), "+d"(c1)
+                 : "r"(pend), "r"(sx)
+                 : "memory");
 }
 
-__device__ __forceinline__ void bucket_run4(uint32_t &pe, uint32_t pe_end, uint32_t sxl,
-                                            double &a0, double &a1, double &a2, double &a3) {
-    asm volatile(
-        "{\n\t"
-        ".reg .pred p;\n\t"
-        ".reg .b32 o, z, gl, gh, ad;\n\t"
-        ".reg .f64 x, y, u, v, g;\n\t"
-        "setp.ge.u32 p, %4, %5;\n\t"
-        "@p bra.uni DONE;\n\t"
-        "LOOP:\n\t"
-        "ld.shared.v4.b32 {o, z, gl, gh}, [%4];\n\t"
-        "add.u32 ad, o, %6;\n\t"
-        "ld.shared.v2.f64 {x, y}, [ad];\n\t"
-        "ld.shared.v2.f64 {u, v}, [ad+16];\n\t"
-        "mov.b64 g, {gl, gh};\n\t"
-        "fma.rn.f64 %0, x, g, %0;\n\t"
-        "fma.rn.f64 %1, y, g, %1;\n\t"
-        "fma.rn.f64 %2, u, g, %2;\n\t"
-        "fma.rn.f64 %3, v, g, %3;\n\t"
-        "add.u32 %4, %4, 16;\n\t"
-        "setp.lt.u32 p, %4, %5;\n\t"
-        "@p bra.uni LOOP;\n\t"
-        "DONE:\n\t"
-        "}"
-        : "+d"(a0), "+d"(a1), "+d"(a2), "+d"(a3), "+r"(pe)
-        : "r"(pe_end), "r"(sxl)
-        : "memory");
+__device__ __forceinline__ void run_s4(uint32_t pe, uint32_t pend, uint32_t sx, double &c0, double &c1, double &c2, double &c3) {
+    asm volatile("{\n\t.reg .pred p;\n\t.reg .b32 o0, x0, l0, h0, o1, x1, l1, h1, a0, a1, t;\n\t.reg .f64 u0, v0, w0, y0, u1, v1, w1, y1, g0, g1;\n\tsetp.ge.u32 p, %0, %5;\n\t@p bra.uni DONE;\n\tadd.u32 t, %0, 16;\n\tsetp.ge.u32 p, t, %5;\n\t@p bra.uni ONE;\n\tPAIR:\n\tld.shared.v4.b32 {o0, x0, l0, h0}, [%0];\n\tld.shared.v4.b32 {o1, x1, l1, h1}, [%0+16];\n\tadd.u32 a0, o0, %6;\n\tld.shared.v2.f64 {u0, v0}, [a0];\n\tld.shared.v2.f64 {w0, y0}, [a0+512];\n\tmov.b64 g0, {l0, h0};\n\tadd.u32 a1, o1, %6;\n\tld.shared.v2.f64 {u1, v1}, [a1];\n\tld.shared.v2.f64 {w1, y1}, [a1+512];\n\tmov.b64 g1, {l1, h1};\n\tfma.rn.f64 %1, u0, g0, %1;\n\tfma.rn.f64 %2, v0, g0, %2;\n\tfma.rn.f64 %3, w0, g0, %3;\n\tfma.rn.f64 %4, y0, g0, %4;\n\tfma.rn.f64 %1, u1, g1, %1;\n\tfma.rn.f64 %2, v1, g1, %2;\n\tfma.rn.f64 %3, w1, g1, %3;\n\tfma.rn.f64 %4, y1, g1, %4;\n\tadd.u32 %0, %0, 32;\n\tadd.u32 t, %0, 16;\n\tsetp.lt.u32 p, t, %5;\n\t@p bra.uni PAIR;\n\tsetp.ge.u32 p, %0, %5;\n\t@p bra.uni DONE;\n\tONE:\n\tld.shared.v4.b32 {o0, x0, l0, h0}, [%0];\n\tadd.u32 a0, o0, %6;\n\tld.shared.v2.f64 {u0, v0}, [a0];\n\tld.shared.v2.f64 {w0, y0}, [a0+512];\n\tmov.b64 g0, {l0, h0};\n\tfma.rn.f64 %1, u0, g0, %1;\n\tfma.rn.f64 %2, v0, g0, %2;\n\tfma.rn.f64 %3, w0, g0, %3;\n\tfma.rn.f64 %4, y0, g0, %4;\n\tDONE:\n\t}"
+                 : "+r"(pe), "+d"(c0), "+d"(c1), "+d"(c2), "+d"(c3)
+                 : "r"(pend), "r"(sx)
+                 : "memory");
 }
 
-// S' tiles are stored swizzled: element (kk, row) lives at kk*TM + (row ^ (kk%32))
-// so that the transposing 8-byte cp.async writes (lanes along kk) and the
-// consumer reads (lanes along rows) are both conflict-free.  A lane owns
-// rows lane + 32*r, r < RPT; entry .y holds the XOR term (kk%32)*8.
-__device__ __forceinline__ void bucket_run_t2(uint32_t &pe, uint32_t pe_end, uint32_t st,
-                                              uint32_t lane8, double &a0, double &a1) {
-    asm volatile(
-        "{\n\t"
-        ".reg .pred p;\n\t"
-        ".reg .b32 o, x, gl, gh, ad;\n\t"
-        ".reg .f64 u, v, g;\n\t"
-        "setp.ge.u32 p, %2, %3;\n\t"
-        "@p bra.uni DONE;\n\t"
-        "LOOP:\n\t"
-        "ld.shared.v4.b32 {o, x, gl, gh}, [%2];\n\t"
-        "xor.b32 ad, x, %5;\n\t"
-        "add.u32 ad, ad, o;\n\t"
-        "add.u32 ad, ad, %4;\n\t"
-        "ld.shared.f64 u, [ad];\n\t"
-        "ld.shared.f64 v, [ad+256];\n\t"
-        "mov.b64 g, {gl, gh};\n\t"
-        "fma.rn.f64 %0, u, g, %0;\n\t"
-        "fma.rn.f64 %1, v, g, %1;\n\t"
-        "add.u32 %2, %2, 16;\n\t"
-        "setp.lt.u32 p, %2, %3;\n\t"
-        "@p bra.uni LOOP;\n\t"
-        "DONE:\n\t"
-        "}"
-        : "+d"(a0), "+d"(a1), "+r"(pe)
-        : "r"(pe_end), "r"(st), "r"(lane8)
-        : "memory");
+__device__ __forceinline__ void run_t2(uint32_t pe, uint32_t pend, uint32_t st, uint32_t lane8, double &c0, double &c1) {
+    asm volatile("{\n\t.reg .pred p;\n\t.reg .b32 o0, x0, l0, h0, o1, x1, l1, h1, a0, a1, t;\n\t.reg .f64 u0, v0, u1, v1, g0, g1;\n\tsetp.ge.u32 p, %0, %3;\n\t@p bra.uni DONE;\n\tadd.u32 t, %0, 16;\n\tsetp.ge.u32 p, t, %3;\n\t@p bra.uni ONE;\n\tPAIR:\n\tld.shared.v4.b32 {o0, x0, l0, h0}, [%0];\n\tld.shared.v4.b32 {o1, x1, l1, h1}, [%0+16];\n\txor.b32 a0, x0, %5;\n\tadd.u32 a0, a0, o0;\n\tadd.u32 a0, a0, %4;\n\tld.shared.f64 u0, [a0];\n\tld.shared.f64 v0, [a0+256];\n\tmov.b64 g0, {l0, h0};\n\txor.b32 a1, x1, %5;\n\tadd.u32 a1, a1, o1;\n\tadd.u32 a1, a1, %4;\n\tld.shared.f64 u1, [a1];\n\tld.shared.f64 v1, [a1+256];\n\tmov.b64 g1, {l1, h1};\n\tfma.rn.f64 %1, u0, g0, %1;\n\tfma.rn.f64 %2, v0, g0, %2;\n\tfma.rn.f64 %1, u1, g1, %1;\n\tfma.rn.f64 %2, v1, g1, %2;\n\tadd.u32 %0, %0, 32;\n\tadd.u32 t, %0, 16;\n\tsetp.lt.u32 p, t, %3;\n\t@p bra.uni PAIR;\n\tsetp.ge.u32 p, %0, %3;\n\t@p bra.uni DONE;\n\tONE:\n\tld.shared.v4.b32 {o0, x0, l0, h0}, [%0];\n\txor.b32 a0, x0, %5;\n\tadd.u32 a0, a0, o0;\n\tadd.u32 a0, a0, %4;\n\tld.shared.f64 u0, [a0];\n\tld.shared.f64 v0, [a0+256];\n\tmov.b64 g0, {l0, h0};\n\tfma.rn.f64 %1, u0, g0, %1;\n\tfma.rn.f64 %2, v0, g0, %2;\n\tDONE:\n\t}"
+                 : "+r"(pe), "+d"(c0), "+d"(c1)
+                 : "r"(pend), "r"(st), "r"(lane8)
+                 : "memory");
 }
 
-__device__ __forceinline__ void bucket_run_t4(uint32_t &pe, uint32_t pe_end, uint32_t st,
-                                              uint32_t lane8, double &a0, double &a1,
-                                              double &a2, double &a3) {
-    asm volatile(
-        "{\n\t"
-        ".reg .pred p;\n\t"
-        ".reg .b32 o, x, gl, gh, ad;\n\t"
-        ".reg .f64 u, v, w, y, g;\n\t"
-        "setp.ge.u32 p, %4, %5;\n\t"
-        "@p bra.uni DONE;\n\t"
-        "LOOP:\n\t"
-        "ld.shared.v4.b32 {o, x, gl, gh}, [%4];\n\t"
-        "xor.b32 ad, x, %7;\n\t"
-        "add.u32 ad, ad, o;\n\t"
-        "add.u32 ad, ad, %6;\n\t"
-        "ld.shared.f64 u, [ad];\n\t"
-        "ld.shared.f64 v, [ad+256];\n\t"
-        "ld.shared.f64 w, [ad+512];\n\t"
-        "ld.shared.f64 y, [ad+768];\n\t"
-        "mov.b64 g, {gl, gh};\n\t"
-        "fma.rn.f64 %0, u, g, %0;\n\t"
-        "fma.rn.f64 %1, v, g, %1;\n\t"
-        "fma.rn.f64 %2, w, g, %2;\n\t"
-        "fma.rn.f64 %3, y, g, %3;\n\t"
-        "add.u32 %4, %4, 16;\n\t"
-        "setp.lt.u32 p, %4, %5;\n\t"
-        "@p bra.uni LOOP;\n\t"
-        "DONE:\n\t"
-        "}"
-        : "+d"(a0), "+d"(a1), "+d"(a2), "+d"(a3), "+r"(pe)
-        : "r"(pe_end), "r"(st), "r"(lane8)
-        : "memory");
+__device__ __forceinline__ void run_t4(uint32_t pe, uint32_t pend, uint32_t st, uint32_t lane8, double &c0, double &c1, double &c2, double &c3) {
+    asm volatile("{\n\t.reg .pred p;\n\t.reg .b32 o0, x0, l0, h0, o1, x1, l1, h1, a0, a1, t;\n\t.reg .f64 u0, v0, w0, y0, u1, v1, w1, y1, g0, g1;\n\tsetp.ge.u32 p, %0, %5;\n\t@p bra.uni DONE;\n\tadd.u32 t, %0, 16;\n\tsetp.ge.u32 p, t, %5;\n\t@p bra.uni ONE;\n\tPAIR:\n\tld.shared.v4.b32 {o0, x0, l0, h0}, [%0];\n\tld.shared.v4.b32 {o1, x1, l1, h1}, [%0+16];\n\txor.b32 a0, x0, %7;\n\tadd.u32 a0, a0, o0;\n\tadd.u32 a0, a0, %6;\n\tld.shared.f64 u0, [a0];\n\tld.shared.f64 v0, [a0+256];\n\tld.shared.f64 w0, [a0+512];\n\tld.shared.f64 y0, [a0+768];\n\tmov.b64 g0, {l0, h0};\n\txor.b32 a1, x1, %7;\n\tadd.u32 a1, a1, o1;\n\tadd.u32 a1, a1, %6;\n\tld.shared.f64 u1, [a1];\n\tld.shared.f64 v1, [a1+256];\n\tld.shared.f64 w1, [a1+512];\n\tld.shared.f64 y1, [a1+768];\n\tmov.b64 g1, {l1, h1};\n\tfma.rn.f64 %1, u0, g0, %1;\n\tfma.rn.f64 %2, v0, g0, %2;\n\tfma.rn.f64 %3, w0, g0, %3;\n\tfma.rn.f64 %4, y0, g0, %4;\n\tfma.rn.f64 %1, u1, g1, %1;\n\tfma.rn.f64 %2, v1, g1, %2;\n\tfma.rn.f64 %3, w1, g1, %3;\n\tfma.rn.f64 %4, y1, g1, %4;\n\tadd.u32 %0, %0, 32;\n\tadd.u32 t, %0, 16;\n\tsetp.lt.u32 p, t, %5;\n\t@p bra.uni PAIR;\n\tsetp.ge.u32 p, %0, %5;\n\t@p bra.uni DONE;\n\tONE:\n\tld.shared.v4.b32 {o0, x0, l0, h0}, [%0];\n\txor.b32 a0, x0, %7;\n\tadd.u32 a0, a0, o0;\n\tadd.u32 a0, a0, %6;\n\tld.shared.f64 u0, [a0];\n\tld.shared.f64 v0, [a0+256];\n\tld.shared.f64 w0, [a0+512];\n\tld.shared.f64 y0, [a0+768];\n\tmov.b64 g0, {l0, h0};\n\tfma.rn.f64 %1, u0, g0, %1;\n\tfma.rn.f64 %2, v0, g0, %2;\n\tfma.rn.f64 %3, w0, g0, %3;\n\tfma.rn.f64 %4, y0, g0, %4;\n\tDONE:\n\t}"
+                 : "+r"(pe), "+d"(c0), "+d"(c1), "+d"(c2), "+d"(c3)
+                 : "r"(pend), "r"(st), "r"(lane8)
+                 : "memory");
 }
 
-// ----------------------------------------------------------------- apply
 struct ApplyArgs {
     const double *A;
     int64_t lda;
@@ -289,24 +205,27 @@ struct ApplyArgs {
     int ksplit;     // CTAs of a cluster splitting the k range (DSMEM reduction)
     int64_t m_out;  // output rows (rows of A for trans 0, cols of A for trans 1)
     int64_t n;      // input index extent (= op.n)
-    int d, alpha, tk;
+    int d, alpha, tk, log2tk;
     int64_t nchunks, bstride, estride;
     const uint16_t *bptr;
     const uint4 *ent;
     double scale;
     double *S;
     int64_t lds, col0;
-    int nslabs, stages, pitch;
-    int stage_bytes, bp_off, en_off;
+    int nslabs, stages;
+    int stage_bytes, zero_off, bp_off, en_off;
 };
 
-// Warp roles: warps [0, NW) consume (bucket owners), warps [NW, NW+PW)
-// produce.  Lane l owns rows RPT*l .. RPT*l+RPT-1 of the TM-row tile.
-template <int RPT, int DB, int NW, int PW, bool TRANS>
-__global__ void __launch_bounds__((NW + PW) * 32, 1)
+// All NW warps own buckets (NW*DB per CTA slab) and share the producer work:
+// warp 0 / lane 0 issues TMA + bulk copies (mode 0); in modes 1/2 every lane
+// issues its share of 8-byte cp.async for the chunk STAGES-1 ahead.
+template <int RPT, int DB, int NW, bool TRANS>
+__global__ void __launch_bounds__(NW * 32, 1)
     sjlt_apply_kernel(const ApplyArgs p, const __grid_constant__ CUtensorMap tmap) {
     constexpr int TM = 32 * RPT;
     constexpr int SLAB = NW * DB;
+    constexpr int G = 4;  // buckets whose first entries are folded as one batch
+    static_assert(DB % G == 0, "DB must be a multiple of the batch");
     extern __shared__ __align__(128) unsigned char smem[];
     uint64_t *full = reinterpret_cast<uint64_t *>(smem);
     uint64_t *empty = full + 8;
@@ -320,16 +239,28 @@ __global__ void __launch_bounds__((NW + PW) * 32, 1)
     const int64_t tile = bid / p.nslabs;
     const int64_t r0 = tile * TM;
     const int j0 = slab * SLAB;
-    // chunk range of this CTA
     const int64_t per = (p.nchunks + ks - 1) / ks;
     const int64_t c_begin = (int64_t)kr * per < p.nchunks ? (int64_t)kr * per : p.nchunks;
     const int64_t c_end = c_begin + per < p.nchunks ? c_begin + per : p.nchunks;
-    const int64_t nloc = c_end - c_begin;
+    const int nloc = (int)(c_end - c_begin);
     const int mode = p.mode;
+    const int stages = p.stages;
+    const uint32_t bp_bytes = (SLAB + 8) * 2;
+    const uint32_t en_bytes = (uint32_t)p.estride * 16;
+    const uint32_t tile_bytes = (uint32_t)p.tk * TM * 8;
 
+    // zero rows + null entries, barriers
+    for (int s = 0; s < stages; ++s) {
+        unsigned char *st = stage0 + (size_t)s * p.stage_bytes;
+        double *zr = reinterpret_cast<double *>(st + p.zero_off);
+        for (int q = threadIdx.x; q < TM; q += NW * 32) zr[q] = 0.0;
+        if (threadIdx.x == 0)
+            reinterpret_cast<uint4 *>(st + p.en_off)[p.estride] =
+                make_uint4((uint32_t)p.zero_off, 0u, 0u, 0x3FF00000u);
+    }
     if (threadIdx.x == 0) {
-        const uint32_t fcount = mode == 0 ? 1u : mode == 1 ? 1u + 32u * PW : 32u * PW;  // S': bulk + noinc
-        for (int s = 0; s < p.stages; ++s) {
+        const uint32_t fcount = mode == 0 ? 1u : 1u + 32u * NW;
+        for (int s = 0; s < stages; ++s) {
             mbar_init(&full[s], fcount);
             mbar_init(&empty[s], NW);
         }
@@ -338,138 +269,163 @@ __global__ void __launch_bounds__((NW + PW) * 32, 1)
     }
     __syncthreads();
 
-    const int stages = p.stages;
-    if (warp >= NW) {
-        // ---------------------------------------------------- producers
-        const int pw = warp - NW;
-        const uint32_t bp_bytes = (SLAB + 8) * 2;
-        const uint32_t en_bytes = (uint32_t)p.estride * 16;
-        const uint32_t tile_bytes = (uint32_t)p.tk * TM * 8;
-        int s = 0;
-        uint32_t ph = 0;  // parity of the empty-barrier phase to wait for
-        if (mode != 0 || pw == 0) {
-            for (int64_t i = 0; i < nloc; ++i) {
-                const int64_t c = c_begin + i;
-                if (i >= stages) mbar_wait(&empty[s], ph ^ 1u);
-                unsigned char *st = stage0 + (size_t)s * p.stage_bytes;
-                double *sx = reinterpret_cast<double *>(st);
-                uint16_t *sbp = reinterpret_cast<uint16_t *>(st + p.bp_off);
-                uint4 *sen = reinterpret_cast<uint4 *>(st + p.en_off);
-                const int64_t k0 = c * p.tk;
-                const int kc = (int)(p.n - k0 < p.tk ? p.n - k0 : p.tk);
-                const uint16_t *gbp = p.bptr + c * p.bstride + j0;
-                const uint4 *gen = p.ent + c * p.estride;
-                if (mode == 0) {
-                    if (lane == 0) {
-                        mbar_arrive_expect_tx(&full[s], tile_bytes + bp_bytes + en_bytes);
-                        tma_load_2d(sx, &tmap, (int)r0, (int)k0, &full[s]);
-                        bulk_g2s(sbp, gbp, bp_bytes, &full[s]);
-                        bulk_g2s(sen, gen, en_bytes, &full[s]);
-                    }
-                    __syncwarp();
-                } else if (TRANS) {
-                    // S' tile: element (kk, rr) = A[k0+kk, r0+rr], stored at
-                    // kk*TM + (rr ^ (kk%32)).  Lanes run along kk (256 B of one
-                    // column of A per instruction); the swizzle spreads the
-                    // 32 stores over all bank pairs.
-                    if (pw == 0 && lane == 0) {
-                        mbar_arrive_expect_tx(&full[s], bp_bytes + en_bytes);
-                        bulk_g2s(sbp, gbp, bp_bytes, &full[s]);
-                        bulk_g2s(sen, gen, en_bytes, &full[s]);
-                    }
-                    const int pl = pw * 32 + lane;
-                    for (int idx = pl; idx < p.tk * TM; idx += 32 * PW) {
-                        const int rr = idx / p.tk, kk = idx % p.tk;
-                        const bool v = (kk < kc) && (r0 + rr < p.m_out);
-                        const double *src = p.A + (r0 + rr) * p.lda + k0 + kk;
-                        cp_async8(sx + kk * TM + (rr ^ (kk & 31)), v ? src : p.A, v);
-                    }
-                    cp_async_mbar_arrive(&full[s]);
-                } else {
-                    const int pl = pw * 32 + lane;  // producer lane id in [0, 32*PW)
-                    for (uint32_t q = pl; q < bp_bytes / 16; q += 32 * PW)
-                        cp_async16(sbp + q * 8, gbp + q * 8, true);
-                    for (uint32_t q = pl; q < en_bytes / 16; q += 32 * PW)
-                        cp_async16(sen + q, gen + q, true);
-                    for (int idx = pl; idx < p.tk * TM; idx += 32 * PW) {
-                        int kk, rr;
-                        const double *src;
-                        if (!p.trans) {  // lanes along rows: coalesced global
-                            kk = idx / TM;
-                            rr = idx % TM;
-                            src = p.A + (k0 + kk) * p.lda + r0 + rr;
-                        } else {         // lanes along k: coalesced global
-                            rr = idx / p.tk;
-                            kk = idx % p.tk;
-                            src = p.A + (r0 + rr) * p.lda + k0 + kk;
-                        }
-                        const bool v = (kk < kc) && (r0 + rr < p.m_out);
-                        cp_async8(sx + kk * p.pitch + rr, v ? src : p.A, v);
-                    }
-                    cp_async_mbar_arrive(&full[s]);
-                }
-                if (++s == stages) {
-                    s = 0;
-                    ph ^= 1u;
-                }
+    // ---- producer helpers
+    auto stage_of = [&](int j) { return stage0 + (size_t)(j % stages) * p.stage_bytes; };
+    auto issue_tma = [&](int j) {  // warp 0, lane 0
+        unsigned char *st = stage_of(j);
+        uint64_t *bar = &full[j % stages];
+        const int64_t c = c_begin + j;
+        mbar_arrive_expect_tx(bar, tile_bytes + bp_bytes + en_bytes);
+        tma_load_2d(st, &tmap, (int)r0, (int)(c * p.tk), bar);
+        bulk_g2s(st + p.bp_off, p.bptr + c * p.bstride + j0, bp_bytes, bar);
+        bulk_g2s(st + p.en_off, p.ent + c * p.estride, en_bytes, bar);
+    };
+    auto issue_coop = [&](int j) {  // every lane
+        unsigned char *st = stage_of(j);
+        uint64_t *bar = &full[j % stages];
+        const int64_t c = c_begin + j;
+        const int64_t k0 = c * p.tk;
+        const int kc = (int)(p.n - k0 < p.tk ? p.n - k0 : p.tk);
+        if (threadIdx.x == 0) {
+            mbar_arrive_expect_tx(bar, bp_bytes + en_bytes);
+            bulk_g2s(st + p.bp_off, p.bptr + c * p.bstride + j0, bp_bytes, bar);
+            bulk_g2s(st + p.en_off, p.ent + c * p.estride, en_bytes, bar);
+        }
+        double *sx = reinterpret_cast<double *>(st);
+        const int nel = p.tk * TM;
+        if (TRANS) {
+            // element (kk, rr) = A[k0+kk, r0+rr] -> sx[kk*TM + (rr ^ (kk%32))];
+            // lanes along kk: coalesced reads, conflict-free swizzled writes
+            const int tkm = p.tk - 1, lg = p.log2tk;
+            for (int idx = threadIdx.x; idx < nel; idx += NW * 32) {
+                const int rr = idx >> lg, kk = idx & tkm;
+                const bool v = (kk < kc) && (r0 + rr < p.m_out);
+                const double *src = p.A + (r0 + rr) * p.lda + k0 + kk;
+                cp_async8(sx + kk * TM + (rr ^ (kk & 31)), v ? src : p.A, v);
+            }
+        } else {
+            for (int idx = threadIdx.x; idx < nel; idx += NW * 32) {
+                const int kk = idx / TM, rr = idx % TM;
+                const bool v = (kk < kc) && (r0 + rr < p.m_out);
+                const double *src = p.A + (k0 + kk) * p.lda + r0 + rr;
+                cp_async8(sx + kk * TM + rr, v ? src : p.A, v);
             }
         }
-        if (ks > 1) {  // match the consumers' barriers of the k-split reduction
-            __syncthreads();
-            cluster_sync();
-            cluster_sync();
-        }
-        return;
+        cp_async_mbar_arrive(bar);
+    };
+
+    int issued = 0;
+    if (mode == 0) {
+        if (warp == 0 && lane == 0)
+            for (; issued < nloc && issued < stages; ++issued) issue_tma(issued);
+    } else {
+        for (; issued < nloc && issued < stages - 1; ++issued) issue_coop(issued);
     }
 
-    // -------------------------------------------------------- consumers
     double acc[RPT][DB];
 #pragma unroll
     for (int r = 0; r < RPT; ++r)
 #pragma unroll
         for (int jj = 0; jj < DB; ++jj) acc[r][jj] = 0.0;
-    {
-        const uint32_t smem_base = smem_u32(stage0);
-        int s = 0;
-        uint32_t ph = 0;
-        for (int64_t i = 0; i < nloc; ++i) {
-            mbar_wait(&full[s], ph);
-            const uint32_t st = smem_base + (uint32_t)s * p.stage_bytes;
-            const uint32_t sxl = st + lane * RPT * 8;
-            const uint16_t *sbp = reinterpret_cast<const uint16_t *>(
-                                      stage0 + (size_t)s * p.stage_bytes + p.bp_off) + warp * DB;
-            const uint32_t sen = st + p.en_off;
-            uint32_t pe = sen + 16u * (uint32_t)sbp[0];
+
+    const uint32_t smem_base = smem_u32(stage0);
+    const uint32_t lane8 = lane * 8u;
+    const uint32_t lane_off = TRANS ? 0u : lane * 16u;  // S tiles: rows 2l, 2l+1 (+64)
+    for (int i = 0; i < nloc; ++i) {
+        // ---- producer duty for chunk i + stages - 1 (its slot held chunk i - 1)
+        if (mode == 0) {
+            if (warp == 0) {
+                if (lane == 0) {
+                    while (issued < nloc && issued < i + stages) {
+                        const int j = issued;
+                        const uint32_t par = (uint32_t)((j / stages) - 1) & 1u;
+                        if (issued == i) mbar_wait(&empty[j % stages], par);
+                        else if (!mbar_test_wait(&empty[j % stages], par)) break;
+                        issue_tma(j);
+                        ++issued;
+                    }
+                }
+                __syncwarp();
+            }
+        } else if (issued < nloc) {
+            const int j = issued;  // == i + stages - 1
+            if (j >= stages) mbar_wait(&empty[j % stages], (uint32_t)((j / stages) - 1) & 1u);
+            issue_coop(j);
+            ++issued;
+        }
+
+        // ---- consume chunk i
+        const int s = i % stages;
+        mbar_wait(&full[s], (uint32_t)(i / stages) & 1u);
+        const uint32_t st = smem_base + (uint32_t)s * p.stage_bytes;
+        const uint32_t sx = st + lane_off;
+        const uint32_t sen = st + p.en_off;
+        const uint16_t *sbp = reinterpret_cast<const uint16_t *>(
+                                  stage0 + (size_t)s * p.stage_bytes + p.bp_off) + warp * DB;
+        const uint32_t nul = (uint32_t)p.estride;
 #pragma unroll
-            for (int jj = 0; jj < DB; ++jj) {
-                const uint32_t pe_end = sen + 16u * (uint32_t)sbp[jj + 1];
+        for (int g0 = 0; g0 < DB; g0 += G) {
+            uint32_t b[G + 1];
+#pragma unroll
+            for (int t = 0; t <= G; ++t) b[t] = sbp[g0 + t];
+            // batch: first entry of each of the G buckets (null if empty)
+            uint4 w[G];
+#pragma unroll
+            for (int t = 0; t < G; ++t) {
+                const uint32_t idx = b[t + 1] > b[t] ? b[t] : nul;
+                asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];"
+                             : "=r"(w[t].x), "=r"(w[t].y), "=r"(w[t].z), "=r"(w[t].w)
+                             : "r"(sen + 16u * idx) : "memory");
+            }
+#pragma unroll
+            for (int t = 0; t < G; ++t) {
+                const double g = __hiloint2double((int)w[t].w, (int)w[t].z);
+                const int jj = g0 + t;
                 if (TRANS) {
-                    if (RPT == 2)
-                        bucket_run_t2(pe, pe_end, st, lane * 8u, acc[0][jj], acc[1][jj]);
-                    else
-                        bucket_run_t4(pe, pe_end, st, lane * 8u, acc[0][jj], acc[1][jj],
-                                      acc[RPT - 2][jj], acc[RPT - 1][jj]);
-                } else if (RPT == 2) {
-                    bucket_run2(pe, pe_end, sxl, acc[0][jj], acc[1][jj]);
+                    const uint32_t ad = st + w[t].x + (w[t].y ^ lane8);
+#pragma unroll
+                    for (int r = 0; r < RPT; ++r) {
+                        double u;
+                        asm volatile("ld.shared.f64 %0, [%1];" : "=d"(u) : "r"(ad + 256u * r) : "memory");
+                        acc[r][jj] = fma(u, g, acc[r][jj]);
+                    }
                 } else {
-                    bucket_run4(pe, pe_end, sxl, acc[0][jj], acc[1][jj], acc[RPT - 2][jj],
+                    const uint32_t ad = sx + w[t].x;
+#pragma unroll
+                    for (int h = 0; h < RPT / 2; ++h) {
+                        double u, v;
+                        asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(u), "=d"(v)
+                                     : "r"(ad + 512u * h) : "memory");
+                        acc[2 * h][jj] = fma(u, g, acc[2 * h][jj]);
+                        acc[2 * h + 1][jj] = fma(v, g, acc[2 * h + 1][jj]);
+                    }
+                }
+            }
+            // remaining entries of each bucket
+#pragma unroll
+            for (int t = 0; t < G; ++t) {
+                const int jj = g0 + t;
+                const uint32_t pe = sen + 16u * (b[t] + 1), pend = sen + 16u * b[t + 1];
+                if (TRANS) {
+                    if (RPT == 2) run_t2(pe, pend, st, lane8, acc[0][jj], acc[1][jj]);
+                    else run_t4(pe, pend, st, lane8, acc[0][jj], acc[1][jj], acc[RPT - 2][jj],
+                                acc[RPT - 1][jj]);
+                } else {
+                    if (RPT == 2) run_s2(pe, pend, sx, acc[0][jj], acc[1][jj]);
+                    else run_s4(pe, pend, sx, acc[0][jj], acc[1][jj], acc[RPT - 2][jj],
                                 acc[RPT - 1][jj]);
                 }
             }
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&empty[s]);
-            if (++s == stages) {
-                s = 0;
-                ph ^= 1u;
-            }
         }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[s]);
     }
 
     // ------------------------------------------- k-split: DSMEM reduction
     // Partial sums of the ks CTAs of a cluster are combined by rank 0 in
     // rank order (deterministic).  The stage ring is reused as the buffer.
-    double *red = reinterpret_cast<double *>(stage0);
     if (ks > 1) {
+        double *red = reinterpret_cast<double *>(stage0);
         __syncthreads();  // every stage consumed: the ring is free
         if (kr > 0) {
 #pragma unroll
@@ -505,16 +461,16 @@ __global__ void __launch_bounds__((NW + PW) * 32, 1)
                     const int64_t row = r0 + lane + 32 * r;
                     if (row < p.m_out) col[row] = acc[r][jj] * p.scale;
                 }
-            } else {      // lane owns rows RPT*lane + r
-                const int64_t row = r0 + lane * RPT;
+            } else {      // lane owns rows 2l, 2l+1 (+64 for RPT 4)
 #pragma unroll
-                for (int r = 0; r < RPT; r += 2) {
-                    if (vec_ok && row + r + 1 < p.m_out) {
-                        *reinterpret_cast<double2 *>(col + row + r) =
-                            make_double2(acc[r][jj] * p.scale, acc[r + 1][jj] * p.scale);
+                for (int h = 0; h < RPT / 2; ++h) {
+                    const int64_t row = r0 + 64 * h + 2 * lane;
+                    const double x0 = acc[2 * h][jj] * p.scale, x1 = acc[2 * h + 1][jj] * p.scale;
+                    if (vec_ok && row + 1 < p.m_out) {
+                        *reinterpret_cast<double2 *>(col + row) = make_double2(x0, x1);
                     } else {
-                        if (row + r < p.m_out) col[row + r] = acc[r][jj] * p.scale;
-                        if (row + r + 1 < p.m_out) col[row + r + 1] = acc[r + 1][jj] * p.scale;
+                        if (row < p.m_out) col[row] = x0;
+                        if (row + 1 < p.m_out) col[row + 1] = x1;
                     }
                 }
             }
@@ -526,11 +482,11 @@ template <int RPT, int DB, int NW>
 static int launch(ApplyArgs a, const Geom &g, cudaStream_t st) {
     constexpr int TM = 32 * RPT;
     constexpr int SLAB = NW * DB;
-    constexpr int PW = 2;  // producer warps (1 active on the TMA path)
     HSK_REQUIRE(g.tm == TM, HSK_EINVAL, "sjlt: plan/config mismatch");
-    a.pitch = g.pitch;
     const bool aligned = a.use_tma != 0;  // 16-byte aligned columns (lda even)
     a.mode = a.trans ? 1 : (aligned ? 0 : 2);
+    a.log2tk = 0;
+    while ((1 << a.log2tk) < a.tk) ++a.log2tk;
     CUtensorMap tmap;
     memset(&tmap, 0, sizeof(tmap));
     if (a.mode == 0) {
@@ -538,12 +494,11 @@ static int launch(ApplyArgs a, const Geom &g, cudaStream_t st) {
                                   TM, (uint32_t)a.tk);
         if (rc) return rc;
     }
-    const int a_bytes = (int)roundup((int64_t)a.tk * a.pitch * 8, 128);
-    const int bp_bytes = (int)roundup((SLAB + 8) * 2, 128);
-    const int en_bytes = (int)roundup(a.estride * 16, 128);
-    a.bp_off = a_bytes;
-    a.en_off = a_bytes + bp_bytes;
-    a.stage_bytes = a_bytes + bp_bytes + en_bytes;
+    const int a_bytes = a.tk * TM * 8;
+    a.zero_off = a_bytes;
+    a.bp_off = (int)roundup(a_bytes + TM * 8, 128);
+    a.en_off = (int)roundup(a.bp_off + (SLAB + 8) * 2, 128);
+    a.stage_bytes = (int)roundup(a.en_off + (a.estride + 1) * 16, 128);
     a.nslabs = (a.d + SLAB - 1) / SLAB;
     const int64_t tiles = (a.m_out + TM - 1) / TM;
     // k-split across a cluster when the tile grid cannot fill the GPU
@@ -556,20 +511,20 @@ static int launch(ApplyArgs a, const Geom &g, cudaStream_t st) {
     }
     a.ksplit = ks;
     const int per = (int)((a.nchunks + ks - 1) / ks);
-    const int budget = 224 * 1024;
+    const int budget = 226 * 1024;
     a.stages = std::max(2, std::min(8, (budget - 128) / a.stage_bytes));
-    if (per > 0 && a.stages > per) a.stages = std::max(2, per);
+    if (per > 0 && a.stages > per + 1) a.stages = std::max(2, per + 1);
     int smem = 128 + a.stages * a.stage_bytes;
     if (ks > 1) smem = std::max(smem, 128 + NW * DB * RPT * 32 * 8);
-    auto kern = a.trans ? sjlt_apply_kernel<RPT, DB, NW, PW, true>
-                        : sjlt_apply_kernel<RPT, DB, NW, PW, false>;
+    auto kern = a.trans ? sjlt_apply_kernel<RPT, DB, NW, true>
+                        : sjlt_apply_kernel<RPT, DB, NW, false>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e != cudaSuccess) return cuda_status(e, "sjlt: set smem attribute");
     const int64_t grid = tiles * a.nslabs * ks;
     HSK_REQUIRE(grid < (1ll << 31), HSK_EINVAL, "sjlt: grid too large");
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3((unsigned)grid, 1, 1);
-    cfg.blockDim = dim3((NW + PW) * 32, 1, 1);
+    cfg.blockDim = dim3(NW * 32, 1, 1);
     cfg.dynamicSmemBytes = smem;
     cfg.stream = st;
     cudaLaunchAttribute attr[1];
@@ -671,6 +626,6 @@ extern "C" int hsk_sjlt_apply(const double *A, int64_t rows, int64_t cols, int64
     a.col0 = col0;
     cudaStream_t st = as_stream(stream);
     if (d <= 64) return sjlt::launch<4, 4, 16>(a, g, st);
-    if (d <= 128) return sjlt::launch<2, 16, 8>(a, g, st);
+    if (d <= 128) return sjlt::launch<2, 8, 16>(a, g, st);
     return sjlt::launch<2, 16, 16>(a, g, st);
 }
