@@ -219,7 +219,7 @@ struct ApplyArgs {
 // All NW warps own buckets (NW*DB per CTA slab) and share the producer work:
 // warp 0 / lane 0 issues TMA + bulk copies (mode 0); in modes 1/2 every lane
 // issues its share of 8-byte cp.async for the chunk STAGES-1 ahead.
-template <int RPT, int DB, int NW, bool TRANS>
+template <int RPT, int DB, int NW, bool TRANS, bool BATCH>
 __global__ void __launch_bounds__(NW * 32, 1)
     sjlt_apply_kernel(const ApplyArgs p, const __grid_constant__ CUtensorMap tmap) {
     constexpr int TM = 32 * RPT;
@@ -229,7 +229,8 @@ __global__ void __launch_bounds__(NW * 32, 1)
     extern __shared__ __align__(128) unsigned char smem[];
     uint64_t *full = reinterpret_cast<uint64_t *>(smem);
     uint64_t *empty = full + 8;
-    unsigned char *stage0 = smem + 128;
+    unsigned *done = reinterpret_cast<unsigned *>(full + 16);  // per-slot finished-warp counters
+    unsigned char *stage0 = smem + 256;
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int ks = p.ksplit;
@@ -263,6 +264,7 @@ __global__ void __launch_bounds__(NW * 32, 1)
         for (int s = 0; s < stages; ++s) {
             mbar_init(&full[s], fcount);
             mbar_init(&empty[s], NW);
+            done[s] = 0;
         }
         fence_mbar_init();
         if (mode == 0) prefetch_tmap(&tmap);
@@ -332,23 +334,10 @@ __global__ void __launch_bounds__(NW * 32, 1)
     const uint32_t lane8 = lane * 8u;
     const uint32_t lane_off = TRANS ? 0u : lane * 16u;  // S tiles: rows 2l, 2l+1 (+64)
     for (int i = 0; i < nloc; ++i) {
-        // ---- producer duty for chunk i + stages - 1 (its slot held chunk i - 1)
-        if (mode == 0) {
-            if (warp == 0) {
-                if (lane == 0) {
-                    while (issued < nloc && issued < i + stages) {
-                        const int j = issued;
-                        const uint32_t par = (uint32_t)((j / stages) - 1) & 1u;
-                        if (issued == i) mbar_wait(&empty[j % stages], par);
-                        else if (!mbar_test_wait(&empty[j % stages], par)) break;
-                        issue_tma(j);
-                        ++issued;
-                    }
-                }
-                __syncwarp();
-            }
-        } else if (issued < nloc) {
-            const int j = issued;  // == i + stages - 1
+        // ---- producer duty (modes 1/2): chunk i + stages - 1 into the slot of
+        // chunk i - 1, once every warp has finished chunk i - 1
+        if (mode != 0 && issued < nloc) {
+            const int j = issued;
             if (j >= stages) mbar_wait(&empty[j % stages], (uint32_t)((j / stages) - 1) & 1u);
             issue_coop(j);
             ++issued;
@@ -363,8 +352,26 @@ __global__ void __launch_bounds__(NW * 32, 1)
         const uint16_t *sbp = reinterpret_cast<const uint16_t *>(
                                   stage0 + (size_t)s * p.stage_bytes + p.bp_off) + warp * DB;
         const uint32_t nul = (uint32_t)p.estride;
+        if (!BATCH) {
+            // plain per-bucket loops over all entries
+            uint32_t pe = sen + 16u * sbp[0];
 #pragma unroll
-        for (int g0 = 0; g0 < DB; g0 += G) {
+            for (int jj = 0; jj < DB; ++jj) {
+                const uint32_t pend = sen + 16u * sbp[jj + 1];
+                if (TRANS) {
+                    if (RPT == 2) run_t2(pe, pend, st, lane8, acc[0][jj], acc[1][jj]);
+                    else run_t4(pe, pend, st, lane8, acc[0][jj], acc[1][jj], acc[RPT - 2][jj],
+                                acc[RPT - 1][jj]);
+                } else {
+                    if (RPT == 2) run_s2(pe, pend, sx, acc[0][jj], acc[1][jj]);
+                    else run_s4(pe, pend, sx, acc[0][jj], acc[1][jj], acc[RPT - 2][jj],
+                                acc[RPT - 1][jj]);
+                }
+                pe = pend;
+            }
+        }
+#pragma unroll
+        for (int g0 = 0; g0 < (BATCH ? DB : 0); g0 += G) {
             uint32_t b[G + 1];
 #pragma unroll
             for (int t = 0; t <= G; ++t) b[t] = sbp[g0 + t];
@@ -418,7 +425,17 @@ __global__ void __launch_bounds__(NW * 32, 1)
             }
         }
         __syncwarp();
-        if (lane == 0) mbar_arrive(&empty[s]);
+        if (lane == 0) {
+            if (mode == 0) {
+                // the last warp to finish chunk i refills its slot with chunk i + stages
+                if (atomicAdd(&done[s], 1u) == NW - 1) {
+                    done[s] = 0;
+                    if (i + stages < nloc) issue_tma(i + stages);
+                }
+            } else {
+                mbar_arrive(&empty[s]);
+            }
+        }
     }
 
     // ------------------------------------------- k-split: DSMEM reduction
@@ -512,12 +529,18 @@ static int launch(ApplyArgs a, const Geom &g, cudaStream_t st) {
     a.ksplit = ks;
     const int per = (int)((a.nchunks + ks - 1) / ks);
     const int budget = 226 * 1024;
-    a.stages = std::max(2, std::min(8, (budget - 128) / a.stage_bytes));
+    a.stages = std::max(2, std::min(8, (budget - 256) / a.stage_bytes));
     if (per > 0 && a.stages > per + 1) a.stages = std::max(2, per + 1);
-    int smem = 128 + a.stages * a.stage_bytes;
-    if (ks > 1) smem = std::max(smem, 128 + NW * DB * RPT * 32 * 8);
-    auto kern = a.trans ? sjlt_apply_kernel<RPT, DB, NW, true>
-                        : sjlt_apply_kernel<RPT, DB, NW, false>;
+    int smem = 256 + a.stages * a.stage_bytes;
+    if (ks > 1) smem = std::max(smem, 256 + NW * DB * RPT * 32 * 8);
+    // batched first-entry folding pays off when buckets hold several entries
+    // per chunk (lambda = tk*alpha/d); HSK_SJLT_BATCH=0/1 overrides
+    bool batch = (int64_t)a.tk * a.alpha >= 4 * (int64_t)a.d;
+    if (const char *env = getenv("HSK_SJLT_BATCH")) batch = env[0] == '1';
+    auto kern = a.trans ? (batch ? sjlt_apply_kernel<RPT, DB, NW, true, true>
+                                 : sjlt_apply_kernel<RPT, DB, NW, true, false>)
+                        : (batch ? sjlt_apply_kernel<RPT, DB, NW, false, true>
+                                 : sjlt_apply_kernel<RPT, DB, NW, false, false>);
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e != cudaSuccess) return cuda_status(e, "sjlt: set smem attribute");
     const int64_t grid = tiles * a.nslabs * ks;
