@@ -61,6 +61,7 @@ static inline int64_t roundup(int64_t x, int64_t m) { return (x + m - 1) / m * m
 // leaves room for >= 3 stages in shared memory, capped at 128.
 static inline int tk_for(int alpha, int tm) {
     int tk = 128;
+    if (const char *env = getenv("HSK_SJLT_TK")) tk = atoi(env);  // tuning override (power of 2)
     while (tk > 1 && (tk * alpha > kMaxChunkEntries || tk * (tm * 8 + 16 * alpha) > 72 * 1024))
         tk >>= 1;
     return tk;
@@ -219,8 +220,8 @@ struct ApplyArgs {
 // All NW warps own buckets (NW*DB per CTA slab) and share the producer work:
 // warp 0 / lane 0 issues TMA + bulk copies (mode 0); in modes 1/2 every lane
 // issues its share of 8-byte cp.async for the chunk STAGES-1 ahead.
-template <int RPT, int DB, int NW, bool TRANS, bool BATCH>
-__global__ void __launch_bounds__(NW * 32, 1)
+template <int RPT, int DB, int NW, bool TRANS, bool BATCH, bool PROD>
+__global__ void __launch_bounds__((NW + (PROD ? 1 : 0)) * 32, 1)
     sjlt_apply_kernel(const ApplyArgs p, const __grid_constant__ CUtensorMap tmap) {
     constexpr int TM = 32 * RPT;
     constexpr int SLAB = NW * DB;
@@ -254,7 +255,7 @@ __global__ void __launch_bounds__(NW * 32, 1)
     for (int s = 0; s < stages; ++s) {
         unsigned char *st = stage0 + (size_t)s * p.stage_bytes;
         double *zr = reinterpret_cast<double *>(st + p.zero_off);
-        for (int q = threadIdx.x; q < TM; q += NW * 32) zr[q] = 0.0;
+        for (int q = threadIdx.x; q < TM; q += blockDim.x) zr[q] = 0.0;
         if (threadIdx.x == 0)
             reinterpret_cast<uint4 *>(st + p.en_off)[p.estride] =
                 make_uint4((uint32_t)p.zero_off, 0u, 0u, 0x3FF00000u);
@@ -317,7 +318,25 @@ __global__ void __launch_bounds__(NW * 32, 1)
     };
 
     int issued = 0;
-    if (mode == 0) {
+    if (PROD) {
+        // dedicated producer warp (mode 0): refill a slot as soon as every
+        // consumer warp has released it
+        if (warp == NW) {
+            if (lane == 0) {
+                for (int j = 0; j < nloc; ++j) {
+                    if (j >= stages) mbar_wait(&empty[j % stages], (uint32_t)((j / stages) - 1) & 1u);
+                    issue_tma(j);
+                }
+            }
+            __syncwarp();
+            if (ks > 1) {  // match the consumers' barriers of the k-split reduction
+                __syncthreads();
+                cluster_sync();
+                cluster_sync();
+            }
+            return;
+        }
+    } else if (mode == 0) {
         if (warp == 0 && lane == 0)
             for (; issued < nloc && issued < stages; ++issued) issue_tma(issued);
     } else {
@@ -333,6 +352,8 @@ __global__ void __launch_bounds__(NW * 32, 1)
     const uint32_t smem_base = smem_u32(stage0);
     const uint32_t lane8 = lane * 8u;
     const uint32_t lane_off = TRANS ? 0u : lane * 16u;  // S tiles: rows 2l, 2l+1 (+64)
+    int cs = 0;
+    uint32_t cph = 0;
     for (int i = 0; i < nloc; ++i) {
         // ---- producer duty (modes 1/2): chunk i + stages - 1 into the slot of
         // chunk i - 1, once every warp has finished chunk i - 1
@@ -344,8 +365,8 @@ __global__ void __launch_bounds__(NW * 32, 1)
         }
 
         // ---- consume chunk i
-        const int s = i % stages;
-        mbar_wait(&full[s], (uint32_t)(i / stages) & 1u);
+        const int s = cs;
+        mbar_wait(&full[s], cph);
         const uint32_t st = smem_base + (uint32_t)s * p.stage_bytes;
         const uint32_t sx = st + lane_off;
         const uint32_t sen = st + p.en_off;
@@ -426,7 +447,7 @@ __global__ void __launch_bounds__(NW * 32, 1)
         }
         __syncwarp();
         if (lane == 0) {
-            if (mode == 0) {
+            if (mode == 0 && !PROD) {
                 // the last warp to finish chunk i refills its slot with chunk i + stages
                 if (atomicAdd(&done[s], 1u) == NW - 1) {
                     done[s] = 0;
@@ -435,6 +456,10 @@ __global__ void __launch_bounds__(NW * 32, 1)
             } else {
                 mbar_arrive(&empty[s]);
             }
+        }
+        if (++cs == stages) {
+            cs = 0;
+            cph ^= 1u;
         }
     }
 
@@ -530,6 +555,7 @@ static int launch(ApplyArgs a, const Geom &g, cudaStream_t st) {
     const int per = (int)((a.nchunks + ks - 1) / ks);
     const int budget = 226 * 1024;
     a.stages = std::max(2, std::min(8, (budget - 256) / a.stage_bytes));
+    if (const char *env = getenv("HSK_SJLT_STAGES")) a.stages = std::max(2, std::min(a.stages, atoi(env)));
     if (per > 0 && a.stages > per + 1) a.stages = std::max(2, per + 1);
     int smem = 256 + a.stages * a.stage_bytes;
     if (ks > 1) smem = std::max(smem, 256 + NW * DB * RPT * 32 * 8);
@@ -537,17 +563,25 @@ static int launch(ApplyArgs a, const Geom &g, cudaStream_t st) {
     // per chunk (lambda = tk*alpha/d); HSK_SJLT_BATCH=0/1 overrides
     bool batch = (int64_t)a.tk * a.alpha >= 4 * (int64_t)a.d;
     if (const char *env = getenv("HSK_SJLT_BATCH")) batch = env[0] == '1';
-    auto kern = a.trans ? (batch ? sjlt_apply_kernel<RPT, DB, NW, true, true>
-                                 : sjlt_apply_kernel<RPT, DB, NW, true, false>)
-                        : (batch ? sjlt_apply_kernel<RPT, DB, NW, false, true>
-                                 : sjlt_apply_kernel<RPT, DB, NW, false, false>);
+    // dedicated producer warp (TMA path only; 17 warps -> 96-register budget,
+    // so it pairs with the unbatched consumer loops)
+    bool prod = false;
+    if (const char *env = getenv("HSK_SJLT_PROD")) prod = env[0] == '1';
+    prod = prod && a.mode == 0;
+    if (prod) batch = false;
+    auto kern = a.trans ? (batch ? sjlt_apply_kernel<RPT, DB, NW, true, true, false>
+                                 : sjlt_apply_kernel<RPT, DB, NW, true, false, false>)
+                        : (prod ? sjlt_apply_kernel<RPT, DB, NW, false, false, true>
+                                : batch ? sjlt_apply_kernel<RPT, DB, NW, false, true, false>
+                                        : sjlt_apply_kernel<RPT, DB, NW, false, false, false>);
+    const int nthreads = (NW + (prod ? 1 : 0)) * 32;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e != cudaSuccess) return cuda_status(e, "sjlt: set smem attribute");
     const int64_t grid = tiles * a.nslabs * ks;
     HSK_REQUIRE(grid < (1ll << 31), HSK_EINVAL, "sjlt: grid too large");
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3((unsigned)grid, 1, 1);
-    cfg.blockDim = dim3(NW * 32, 1, 1);
+    cfg.blockDim = dim3(nthreads, 1, 1);
     cfg.dynamicSmemBytes = smem;
     cfg.stream = st;
     cudaLaunchAttribute attr[1];
