@@ -590,7 +590,8 @@ static int launch(ApplyArgs a, const Geom &g, cudaStream_t st) {
     attr[0].val.clusterDim.y = 1;
     attr[0].val.clusterDim.z = 1;
     cfg.attrs = attr;
-    cfg.numAttrs = 1;
+    cfg.numAttrs = ks > 1 ? 1 : 0;  // plain launch unless the k-split needs a cluster
+    if (const char *env = getenv("HSK_SJLT_FORCE_CLUSTER")) cfg.numAttrs = env[0] == '1' ? 1 : cfg.numAttrs;
     e = cudaLaunchKernelEx(&cfg, kern, a, tmap);
     if (e != cudaSuccess) return cuda_status(e, "sjlt_apply_kernel launch");
     HSK_CHECK_LAUNCH("sjlt_apply_kernel");
