@@ -373,12 +373,24 @@ __global__ void __launch_bounds__((NW + (PROD ? 1 : 0)) * 32, 1)
         const uint16_t *sbp = reinterpret_cast<const uint16_t *>(
                                   stage0 + (size_t)s * p.stage_bytes + p.bp_off) + warp * DB;
         const uint32_t nul = (uint32_t)p.estride;
+        // the warp's DB+1 bucket bounds, preloaded (packed u16 pairs) so no
+        // bucket waits on a shared-memory load of its own bound
+        constexpr int NBW = DB / 2 + 1;
+        uint32_t bw[NBW];
+        {
+            const uint32_t *src = reinterpret_cast<const uint32_t *>(sbp);
+#pragma unroll
+            for (int q = 0; q < NBW; ++q) bw[q] = src[q];
+        }
+        auto bound = [&](int jj) -> uint32_t {
+            return (jj & 1) ? (bw[jj >> 1] >> 16) : (bw[jj >> 1] & 0xffffu);
+        };
         if (!BATCH) {
             // plain per-bucket loops over all entries
-            uint32_t pe = sen + 16u * sbp[0];
+            uint32_t pe = sen + 16u * bound(0);
 #pragma unroll
             for (int jj = 0; jj < DB; ++jj) {
-                const uint32_t pend = sen + 16u * sbp[jj + 1];
+                const uint32_t pend = sen + 16u * bound(jj + 1);
                 if (TRANS) {
                     if (RPT == 2) run_t2(pe, pend, st, lane8, acc[0][jj], acc[1][jj]);
                     else run_t4(pe, pend, st, lane8, acc[0][jj], acc[1][jj], acc[RPT - 2][jj],
@@ -395,7 +407,7 @@ __global__ void __launch_bounds__((NW + (PROD ? 1 : 0)) * 32, 1)
         for (int g0 = 0; g0 < (BATCH ? DB : 0); g0 += G) {
             uint32_t b[G + 1];
 #pragma unroll
-            for (int t = 0; t <= G; ++t) b[t] = sbp[g0 + t];
+            for (int t = 0; t <= G; ++t) b[t] = bound(g0 + t);
             // batch: first entry of each of the G buckets (null if empty)
             uint4 w[G];
 #pragma unroll
