@@ -165,33 +165,35 @@ __global__ void sjlt_plan_kernel(const int32_t *__restrict__ pos, const int8_t *
 // a contiguous 512 B).  S' tiles (swizzled, element (kk,row) at
 // kk*TM + (row ^ (kk%32))): rows l + 32 r (LDS.64 each, conflict-free).
 
-// Remaining entries [pe, pend) of one bucket (shared byte addresses), two
-// per iteration.  `bra.uni`: every lane walks the same list.
+// Remaining entries [pe, pend) of one bucket (shared byte addresses), one
+// per iteration: consecutive DFMAs on an accumulator are a full iteration
+// (two shared loads) apart, so they never wait on each other.  `bra.uni`:
+// every lane walks the same list.
 // run_s*: S tiles, rows {2l, 2l+1} at [sx + o] (and {64+2l, 64+2l+1} at +512).
 // run_t*: S' tiles, rows l + 32 r at st + o + (x ^ lane8) + 256 r.
 __device__ __forceinline__ void run_s2(uint32_t pe, uint32_t pend, uint32_t sx, double &c0, double &c1) {
-    asm volatile("{\n\t.reg .pred p;\n\t.reg .b32 o0, x0, l0, h0, o1, x1, l1, h1, a0, a1, t;\n\t.reg .f64 u0, v0, u1, v1, g0, g1;\n\tsetp.ge.u32 p, %0, %3;\n\t@p bra.uni DONE;\n\tadd.u32 t, %0, 16;\n\tsetp.ge.u32 p, t, %3;\n\t@p bra.uni ONE;\n\tPAIR:\n\tld.shared.v4.b32 {o0, x0, l0, h0}, [%0];\n\tld.shared.v4.b32 {o1, x1, l1, h1}, [%0+16];\n\tadd.u32 a0, o0, %4;\n\tld.shared.v2.f64 {u0, v0}, [a0];\n\tmov.b64 g0, {l0, h0};\n\tadd.u32 a1, o1, %4;\n\tld.shared.v2.f64 {u1, v1}, [a1];\n\tmov.b64 g1, {l1, h1};\n\tfma.rn.f64 %1, u0, g0, %1;\n\tfma.rn.f64 %2, v0, g0, %2;\n\tfma.rn.f64 %1, u1, g1, %1;\n\tfma.rn.f64 %2, v1, g1, %2;\n\tadd.u32 %0, %0, 32;\n\tadd.u32 t, %0, 16;\n\tsetp.lt.u32 p, t, %3;\n\t@p bra.uni PAIR;\n\tsetp.ge.u32 p, %0, %3;\n\t@p bra.uni DONE;\n\tONE:\n\tld.shared.v4.b32 {o0, x0, l0, h0}, [%0];\n\tadd.u32 a0, o0, %4;\n\tld.shared.v2.f64 {u0, v0}, [a0];\n\tmov.b64 g0, {l0, h0};\n\tfma.rn.f64 %1, u0, g0, %1;\n\tfma.rn.f64 %2, v0, g0, %2;\n\tDONE:\n\t}"
+    asm volatile("{\n\t.reg .pred p;\n\t.reg .b32 o0, x0, l0, h0, a0;\n\t.reg .f64 u0, v0, g0;\n\tsetp.ge.u32 p, %0, %3;\n\t@p bra.uni DONE;\n\tLOOP:\n\tld.shared.v4.b32 {o0, x0, l0, h0}, [%0];\n\tadd.u32 a0, o0, %4;\n\tld.shared.v2.f64 {u0, v0}, [a0];\n\tmov.b64 g0, {l0, h0};\n\tfma.rn.f64 %1, u0, g0, %1;\n\tfma.rn.f64 %2, v0, g0, %2;\n\tadd.u32 %0, %0, 16;\n\tsetp.lt.u32 p, %0, %3;\n\t@p bra.uni LOOP;\n\tDONE:\n\t}"
                  : "+r"(pe), "+d"(c0), "+d"(c1)
                  : "r"(pend), "r"(sx)
                  : "memory");
 }
 
 __device__ __forceinline__ void run_s4(uint32_t pe, uint32_t pend, uint32_t sx, double &c0, double &c1, double &c2, double &c3) {
-    asm volatile("{\n\t.reg .pred p;\n\t.reg .b32 o0, x0, l0, h0, o1, x1, l1, h1, a0, a1, t;\n\t.reg .f64 u0, v0, w0, y0, u1, v1, w1, y1, g0, g1;\n\tsetp.ge.u32 p, %0, %5;\n\t@p bra.uni DONE;\n\tadd.u32 t, %0, 16;\n\tsetp.ge.u32 p, t, %5;\n\t@p bra.uni ONE;\n\tPAIR:\n\tld.shared.v4.b32 {o0, x0, l0, h0}, [%0];\n\tld.shared.v4.b32 {o1, x1, l1, h1}, [%0+16];\n\tadd.u32 a0, o0, %6;\n\tld.shared.v2.f64 {u0, v0}, [a0];\n\tld.shared.v2.f64 {w0, y0}, [a0+512];\n\tmov.b64 g0, {l0, h0};\n\tadd.u32 a1, o1, %6;\n\tld.shared.v2.f64 {u1, v1}, [a1];\n\tld.shared.v2.f64 {w1, y1}, [a1+512];\n\tmov.b64 g1, {l1, h1};\n\tfma.rn.f64 %1, u0, g0, %1;\n\tfma.rn.f64 %2, v0, g0, %2;\n\tfma.rn.f64 %3, w0, g0, %3;\n\tfma.rn.f64 %4, y0, g0, %4;\n\tfma.rn.f64 %1, u1, g1, %1;\n\tfma.rn.f64 %2, v1, g1, %2;\n\tfma.rn.f64 %3, w1, g1, %3;\n\tfma.rn.f64 %4, y1, g1, %4;\n\tadd.u32 %0, %0, 32;\n\tadd.u32 t, %0, 16;\n\tsetp.lt.u32 p, t, %5;\n\t@p bra.uni PAIR;\n\tsetp.ge.u32 p, %0, %5;\n\t@p bra.uni DONE;\n\tONE:\n\tld.shared.v4.b32 {o0, x0, l0, h0}, [%0];\n\tadd.u32 a0, o0, %6;\n\tld.shared.v2.f64 {u0, v0}, [a0];\n\tld.shared.v2.f64 {w0, y0}, [a0+512];\n\tmov.b64 g0, {l0, h0};\n\tfma.rn.f64 %1, u0, g0, %1;\n\tfma.rn.f64 %2, v0, g0, %2;\n\tfma.rn.f64 %3, w0, g0, %3;\n\tfma.rn.f64 %4, y0, g0, %4;\n\tDONE:\n\t}"
+    asm volatile("{\n\t.reg .pred p;\n\t.reg .b32 o0, x0, l0, h0, a0;\n\t.reg .f64 u0, v0, w0, y0, g0;\n\tsetp.ge.u32 p, %0, %5;\n\t@p bra.uni DONE;\n\tLOOP:\n\tld.shared.v4.b32 {o0, x0, l0, h0}, [%0];\n\tadd.u32 a0, o0, %6;\n\tld.shared.v2.f64 {u0, v0}, [a0];\n\tld.shared.v2.f64 {w0, y0}, [a0+512];\n\tmov.b64 g0, {l0, h0};\n\tfma.rn.f64 %1, u0, g0, %1;\n\tfma.rn.f64 %2, v0, g0, %2;\n\tfma.rn.f64 %3, w0, g0, %3;\n\tfma.rn.f64 %4, y0, g0, %4;\n\tadd.u32 %0, %0, 16;\n\tsetp.lt.u32 p, %0, %5;\n\t@p bra.uni LOOP;\n\tDONE:\n\t}"
                  : "+r"(pe), "+d"(c0), "+d"(c1), "+d"(c2), "+d"(c3)
                  : "r"(pend), "r"(sx)
                  : "memory");
 }
 
 __device__ __forceinline__ void run_t2(uint32_t pe, uint32_t pend, uint32_t st, uint32_t lane8, double &c0, double &c1) {
-    asm volatile("{\n\t.reg .pred p;\n\t.reg .b32 o0, x0, l0, h0, o1, x1, l1, h1, a0, a1, t;\n\t.reg .f64 u0, v0, u1, v1, g0, g1;\n\tsetp.ge.u32 p, %0, %3;\n\t@p bra.uni DONE;\n\tadd.u32 t, %0, 16;\n\tsetp.ge.u32 p, t, %3;\n\t@p bra.uni ONE;\n\tPAIR:\n\tld.shared.v4.b32 {o0, x0, l0, h0}, [%0];\n\tld.shared.v4.b32 {o1, x1, l1, h1}, [%0+16];\n\txor.b32 a0, x0, %5;\n\tadd.u32 a0, a0, o0;\n\tadd.u32 a0, a0, %4;\n\tld.shared.f64 u0, [a0];\n\tld.shared.f64 v0, [a0+256];\n\tmov.b64 g0, {l0, h0};\n\txor.b32 a1, x1, %5;\n\tadd.u32 a1, a1, o1;\n\tadd.u32 a1, a1, %4;\n\tld.shared.f64 u1, [a1];\n\tld.shared.f64 v1, [a1+256];\n\tmov.b64 g1, {l1, h1};\n\tfma.rn.f64 %1, u0, g0, %1;\n\tfma.rn.f64 %2, v0, g0, %2;\n\tfma.rn.f64 %1, u1, g1, %1;\n\tfma.rn.f64 %2, v1, g1, %2;\n\tadd.u32 %0, %0, 32;\n\tadd.u32 t, %0, 16;\n\tsetp.lt.u32 p, t, %3;\n\t@p bra.uni PAIR;\n\tsetp.ge.u32 p, %0, %3;\n\t@p bra.uni DONE;\n\tONE:\n\tld.shared.v4.b32 {o0, x0, l0, h0}, [%0];\n\txor.b32 a0, x0, %5;\n\tadd.u32 a0, a0, o0;\n\tadd.u32 a0, a0, %4;\n\tld.shared.f64 u0, [a0];\n\tld.shared.f64 v0, [a0+256];\n\tmov.b64 g0, {l0, h0};\n\tfma.rn.f64 %1, u0, g0, %1;\n\tfma.rn.f64 %2, v0, g0, %2;\n\tDONE:\n\t}"
+    asm volatile("{\n\t.reg .pred p;\n\t.reg .b32 o0, x0, l0, h0, a0;\n\t.reg .f64 u0, v0, g0;\n\tsetp.ge.u32 p, %0, %3;\n\t@p bra.uni DONE;\n\tLOOP:\n\tld.shared.v4.b32 {o0, x0, l0, h0}, [%0];\n\txor.b32 a0, x0, %5;\n\tadd.u32 a0, a0, o0;\n\tadd.u32 a0, a0, %4;\n\tld.shared.f64 u0, [a0];\n\tld.shared.f64 v0, [a0+256];\n\tmov.b64 g0, {l0, h0};\n\tfma.rn.f64 %1, u0, g0, %1;\n\tfma.rn.f64 %2, v0, g0, %2;\n\tadd.u32 %0, %0, 16;\n\tsetp.lt.u32 p, %0, %3;\n\t@p bra.uni LOOP;\n\tDONE:\n\t}"
                  : "+r"(pe), "+d"(c0), "+d"(c1)
                  : "r"(pend), "r"(st), "r"(lane8)
                  : "memory");
 }
 
 __device__ __forceinline__ void run_t4(uint32_t pe, uint32_t pend, uint32_t st, uint32_t lane8, double &c0, double &c1, double &c2, double &c3) {
-    asm volatile("{\n\t.reg .pred p;\n\t.reg .b32 o0, x0, l0, h0, o1, x1, l1, h1, a0, a1, t;\n\t.reg .f64 u0, v0, w0, y0, u1, v1, w1, y1, g0, g1;\n\tsetp.ge.u32 p, %0, %5;\n\t@p bra.uni DONE;\n\tadd.u32 t, %0, 16;\n\tsetp.ge.u32 p, t, %5;\n\t@p bra.uni ONE;\n\tPAIR:\n\tld.shared.v4.b32 {o0, x0, l0, h0}, [%0];\n\tld.shared.v4.b32 {o1, x1, l1, h1}, [%0+16];\n\txor.b32 a0, x0, %7;\n\tadd.u32 a0, a0, o0;\n\tadd.u32 a0, a0, %6;\n\tld.shared.f64 u0, [a0];\n\tld.shared.f64 v0, [a0+256];\n\tld.shared.f64 w0, [a0+512];\n\tld.shared.f64 y0, [a0+768];\n\tmov.b64 g0, {l0, h0};\n\txor.b32 a1, x1, %7;\n\tadd.u32 a1, a1, o1;\n\tadd.u32 a1, a1, %6;\n\tld.shared.f64 u1, [a1];\n\tld.shared.f64 v1, [a1+256];\n\tld.shared.f64 w1, [a1+512];\n\tld.shared.f64 y1, [a1+768];\n\tmov.b64 g1, {l1, h1};\n\tfma.rn.f64 %1, u0, g0, %1;\n\tfma.rn.f64 %2, v0, g0, %2;\n\tfma.rn.f64 %3, w0, g0, %3;\n\tfma.rn.f64 %4, y0, g0, %4;\n\tfma.rn.f64 %1, u1, g1, %1;\n\tfma.rn.f64 %2, v1, g1, %2;\n\tfma.rn.f64 %3, w1, g1, %3;\n\tfma.rn.f64 %4, y1, g1, %4;\n\tadd.u32 %0, %0, 32;\n\tadd.u32 t, %0, 16;\n\tsetp.lt.u32 p, t, %5;\n\t@p bra.uni PAIR;\n\tsetp.ge.u32 p, %0, %5;\n\t@p bra.uni DONE;\n\tONE:\n\tld.shared.v4.b32 {o0, x0, l0, h0}, [%0];\n\txor.b32 a0, x0, %7;\n\tadd.u32 a0, a0, o0;\n\tadd.u32 a0, a0, %6;\n\tld.shared.f64 u0, [a0];\n\tld.shared.f64 v0, [a0+256];\n\tld.shared.f64 w0, [a0+512];\n\tld.shared.f64 y0, [a0+768];\n\tmov.b64 g0, {l0, h0};\n\tfma.rn.f64 %1, u0, g0, %1;\n\tfma.rn.f64 %2, v0, g0, %2;\n\tfma.rn.f64 %3, w0, g0, %3;\n\tfma.rn.f64 %4, y0, g0, %4;\n\tDONE:\n\t}"
+    asm volatile("{\n\t.reg .pred p;\n\t.reg .b32 o0, x0, l0, h0, a0;\n\t.reg .f64 u0, v0, w0, y0, g0;\n\tsetp.ge.u32 p, %0, %5;\n\t@p bra.uni DONE;\n\tLOOP:\n\tld.shared.v4.b32 {o0, x0, l0, h0}, [%0];\n\txor.b32 a0, x0, %7;\n\tadd.u32 a0, a0, o0;\n\tadd.u32 a0, a0, %6;\n\tld.shared.f64 u0, [a0];\n\tld.shared.f64 v0, [a0+256];\n\tld.shared.f64 w0, [a0+512];\n\tld.shared.f64 y0, [a0+768];\n\tmov.b64 g0, {l0, h0};\n\tfma.rn.f64 %1, u0, g0, %1;\n\tfma.rn.f64 %2, v0, g0, %2;\n\tfma.rn.f64 %3, w0, g0, %3;\n\tfma.rn.f64 %4, y0, g0, %4;\n\tadd.u32 %0, %0, 16;\n\tsetp.lt.u32 p, %0, %5;\n\t@p bra.uni LOOP;\n\tDONE:\n\t}"
                  : "+r"(pe), "+d"(c0), "+d"(c1), "+d"(c2), "+d"(c3)
                  : "r"(pend), "r"(st), "r"(lane8)
                  : "memory");
