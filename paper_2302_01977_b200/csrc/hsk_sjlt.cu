@@ -579,7 +579,7 @@ static int launch(ApplyArgs a, const Geom &g, cudaStream_t st) {
     if (const char *env = getenv("HSK_SJLT_BATCH")) batch = env[0] == '1';
     // dedicated producer warp (TMA path only; 17 warps -> 96-register budget,
     // so it pairs with the unbatched consumer loops)
-    bool prod = false;
+    bool prod = true;
     if (const char *env = getenv("HSK_SJLT_PROD")) prod = env[0] == '1';
     prod = prod && a.mode == 0;
     if (prod) batch = false;
