@@ -1,0 +1,164 @@
+"""Row-block sharded sketching across GPUs (one process per GPU).
+
+BASELINE.json C5 / SURVEY.md §8(e).  GPU g holds rows [r0_g, r1_g) of A (all n
+columns) and the full operator R (tiny for SJLT; d x n for Gaussian):
+
+  S  = A R^T      rows are local:  S[r0:r1] = A_g R^T           -- no communication
+  S' = A^T R^T  = sum_g A_g^T R_g^T,  R_g = R restricted to input indices [r0, r1)
+                   every GPU forms partials for all n output rows, blocked by
+                   destination rank, and a reduce-scatter leaves GPU g with
+                   S'[r0:r1] (the same row sharding as S).
+
+The destination blocks are produced by separate launches over column
+slices of A_g (contiguous in the column-major layout), so each block is a
+contiguous (m_q x d) buffer and the reduce-scatter needs no repacking.
+
+Determinism: NCCL's reduce-scatter is deterministic for a fixed algorithm and
+topology; `deterministic=True` instead gathers every partial of block q on
+rank q and sums them in rank order (bitwise reproducible across runs and
+NCCL algorithms; also used for uneven shards).
+
+SRHT mixes all input indices in its FWHT, so only S = A R^T row-shards; its
+S' is formed on column shards (`sketch_columns_local`).
+"""
+
+from __future__ import annotations
+
+import numpy as np
+
+from . import operators as ops
+
+try:
+    import torch
+    import torch.distributed as dist
+except ImportError:  # pragma: no cover
+    torch = None
+    dist = None
+
+
+def shard_bounds(n: int, world: int) -> list[tuple[int, int]]:
+    """Contiguous near-equal row blocks [r0, r1) per rank."""
+    base, extra = divmod(n, world)
+    out, r = [], 0
+    for g in range(world):
+        m = base + (1 if g < extra else 0)
+        out.append((r, r + m))
+        r += m
+    return out
+
+
+def restrict_block(block, r0: int, r1: int):
+    """The block's operator restricted to input indices [r0, r1)."""
+    if block.kind == ops.SJLT:
+        sub = ops.SjltBlock.from_pattern(r1 - r0, block.rows, block.alpha,
+                                         block._pos[r0:r1], block._signs[r0:r1])
+        sub._scale = block._scale
+        return sub
+    if block.kind == ops.GAUSSIAN:
+        sub = ops.GaussianBlock.__new__(ops.GaussianBlock)
+        sub.n, sub.rows = r1 - r0, block.rows
+        sub.matrix = np.ascontiguousarray(block.matrix[:, r0:r1])
+        return sub
+    raise ValueError("SRHT does not decompose over input-index shards")
+
+
+def restrict_operator(op, r0: int, r1: int):
+    blocks = tuple(restrict_block(b, r0, r1) for b in op.blocks)
+    return ops.SketchOperator(op.kind, r1 - r0, blocks, op.alpha, op.construction)
+
+
+# --------------------------------------------------------------- local math
+
+def _gpu_local_right(A_shard, op):
+    from . import sketching as sk
+    return sk.apply_right_device(A_shard, op)
+
+
+def _gpu_local_transposed_blocks(A_shard, sub_op, bounds):
+    """Partials of S' for each destination row block, as torch tensors of
+    shape (d, m_q) (column-major m_q x d)."""
+    from . import device
+    from . import sketching as sk
+    outs = []
+    for (c0, c1) in bounds:
+        view = A_shard.column_view(c0, c1 - c0)
+        part = device.DeviceMatrix.empty(c1 - c0, sub_op.d, ld=max(1, c1 - c0))
+        sk.apply_right_transposed_device(view, sub_op, out=part)
+        outs.append(part.t[:, :c1 - c0] if part.t.shape[1] != c1 - c0 else part.t)
+    return outs
+
+
+def sketch_row_sharded(A_shard, op, *, rank: int, world: int, n_rows: int,
+                       transposed: bool = True, group=None, deterministic: bool = False,
+                       local_right=None, local_transposed=None):
+    """S rows and (optionally) S' rows of this rank's shard.
+
+    A_shard: rows [r0, r1) of the global n_rows x op.n matrix (DeviceMatrix on
+    GPU ranks).  Returns (S_local, St_local) as torch tensors of shape
+    (d, m_local) -- column-major (m_local x d) -- St_local None unless
+    `transposed`.  `local_right` / `local_transposed` replace the GPU kernels
+    (test hook for CPU process groups).
+    """
+    bounds = shard_bounds(n_rows, world)
+    r0, r1 = bounds[rank]
+    local_right = local_right or (lambda A, o: _gpu_local_right(A, o).t[:, :A.rows])
+    S_local = local_right(A_shard, op)
+    if not transposed:
+        return S_local, None
+    if op.n != n_rows:
+        raise ValueError("S' = A^T R^T needs a square operator over the row space")
+    sub = restrict_operator(op, r0, r1)
+    local_transposed = local_transposed or _gpu_local_transposed_blocks
+    parts = local_transposed(A_shard, sub, bounds)  # list of (d, m_q) tensors
+    m_loc = r1 - r0
+    d = op.d
+    if deterministic or any(b[1] - b[0] != m_loc for b in bounds):
+        # fixed rank-order summation (bitwise reproducible; uneven shards OK)
+        return S_local, _ordered_reduce_scatter(parts, rank, world, group)
+    flat = torch.cat([p.contiguous().reshape(-1) for p in parts])
+    out = torch.empty(d * m_loc, dtype=torch.float64, device=flat.device)
+    dist.reduce_scatter_tensor(out, flat, op=dist.ReduceOp.SUM, group=group)
+    return S_local, out.view(d, m_loc)
+
+
+def _ordered_reduce_scatter(parts, rank: int, world: int, group):
+    """out = sum over source ranks g = 0..world-1 (in that order) of the
+    partial that rank g computed for this rank's block."""
+    mine = None
+    for q in range(world):
+        # rank q collects everyone's partial for block q
+        buf = parts[q].contiguous()
+        gathered = [torch.empty_like(buf) for _ in range(world)] if q == rank else None
+        if world == 1:
+            gathered = [buf]
+        else:
+            dist.gather(buf, gather_list=gathered, dst=q, group=group)
+        if q == rank:
+            acc = gathered[0].clone()
+            for g in range(1, world):
+                acc += gathered[g]
+            mine = acc
+    return mine
+
+
+def sketch_columns_local(A_cols, op):
+    """S' rows for this rank's column block of A: columns are independent in
+    A^T R^T, so column sharding needs no communication (any operator,
+    including SRHT)."""
+    from . import sketching as sk
+    return sk.apply_right_transposed_device(A_cols, op)
+
+
+def scaling_model(n: int, d: int, world: int, hbm_gbs: float, link_gbs: float = 770.0):
+    """Roofline model of the C5 S' step: per-GPU A stream + reduce-scatter."""
+    a_bytes = n * n * 8 / world
+    t_compute = a_bytes / (hbm_gbs * 1e9)
+    rs_bytes = n * d * 8 * (world - 1) / world
+    t_comm = rs_bytes / (link_gbs * 1e9) if world > 1 else 0.0
+    return {"t_compute_s": t_compute, "t_comm_s": t_comm,
+            "serial_eff": t_compute / (t_compute + t_comm) if world > 1 else 1.0,
+            "overlap_eff": min(1.0, t_compute / max(t_compute, t_comm)) if world > 1 else 1.0}
+
+
+__all__ = ["shard_bounds", "restrict_block", "restrict_operator", "sketch_row_sharded",
+           "sketch_columns_local", "scaling_model"]

@@ -1,0 +1,92 @@
+"""Drop-in through the reference's own compressor (hsskit).
+
+The reference package is installed into baseline/_ref (git-ignored; it
+travels to the GPU box).  plugin.install() rebinds hsskit.sketching.apply_right
+/ apply_right_transposed; the compressor, operator draws and dense_rows stay
+the reference's.  Skipped when hsskit is not importable.
+"""
+
+import os
+import sys
+
+import numpy as np
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+REF = os.path.join(ROOT, "baseline", "_ref")
+if os.path.isdir(REF) and REF not in sys.path:
+    sys.path.append(REF)
+hsskit = pytest.importorskip("hsskit")
+
+from oracle import oracle as O  # noqa: E402
+from paper_2302_01977_b200 import matgen, plugin  # noqa: E402
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture
+def installed(cuda):
+    import hsskit.sketching as hs
+    plugin.install(hs)
+    yield hs
+    plugin.uninstall(hs)
+
+
+def test_reference_sketching_suite_through_gpu(installed):
+    hs = installed
+    rng = np.random.default_rng(5)
+    A = rng.standard_normal((16, 12))
+    for cons in (hs.BLOCK, hs.GRAPH):
+        op = hs.new_operator(hs.SJLT, 12, 6, seed=9, alpha=3, construction=cons)
+        Rt = hs.dense_rows(op, np.arange(12), np.arange(6))
+        np.testing.assert_allclose(hs.apply_right(A, op), A @ Rt, atol=1e-13 * np.linalg.norm(A))
+    for kind in (hs.GAUSSIAN, hs.SRHT):
+        op = hs.new_operator(kind, 21, 5, seed=1)
+        Rt = hs.dense_rows(op, np.arange(21), np.arange(5))
+        B = rng.standard_normal((8, 21))
+        np.testing.assert_allclose(hs.apply_right(B, op), B @ Rt, atol=1e-12 * np.linalg.norm(B))
+        np.testing.assert_allclose(hs.apply_right_transposed(B.T, op), B @ Rt,
+                                   atol=1e-12 * np.linalg.norm(B))
+    with pytest.raises(ValueError):
+        hs.apply_right(np.zeros((3, 9)), hs.new_operator(hs.GAUSSIAN, 8, 4, seed=0))
+
+
+def test_compress_bit_reproducible_through_gpu(installed):
+    from hsskit import compress, matvec, reconstruct_dense, synthetic_hss
+    from hsskit.hss_compress import CompressOptions
+    acc, tree, _ = synthetic_hss(256, 64, 8, seed=8)
+    opts = CompressOptions(d0=16, dd=8, eps_rel=1e-6, eps_abs=1e-10, kind="sjlt", alpha=4,
+                           seed=9, leaf_size=64)
+    H1 = compress(acc, tree, opts)
+    H2 = compress(acc, tree, opts)
+    np.testing.assert_array_equal(reconstruct_dense(H1), reconstruct_dense(H2))
+    x = np.random.default_rng(10).standard_normal(256)
+    np.testing.assert_array_equal(matvec(H1, x), matvec(H2, x))
+
+
+@pytest.mark.slow
+def test_c1_hss_error_matches_reference(cuda):
+    """C1: HSS compression of the n=4096 Gaussian-kernel matrix with the GPU
+    sketch; the relative error must be within 1% of the CPU reference's on
+    the same A bytes (BASELINE.json north_star)."""
+    import hsskit.sketching as hs
+    from hsskit import build_uniform, compress, relative_error, stats
+    from hsskit.hss_compress import CompressOptions
+    from hsskit.sketching import DenseAccessor
+    n = 4096
+    Ah = matgen.gaussian_kernel(n, 8, 0.5).to_host()
+    opts = CompressOptions(d0=192, dd=64, eps_rel=1e-6, eps_abs=1e-8, leaf_size=128,
+                           kind="sjlt", alpha=4, construction="graph", seed=0)
+    tree = build_uniform(n, 128)
+    H_ref = compress(DenseAccessor(Ah), tree, opts)
+    err_ref = relative_error(Ah, H_ref)
+    plugin.install(hs)
+    try:
+        H_gpu = compress(DenseAccessor(Ah), tree, opts)
+    finally:
+        plugin.uninstall(hs)
+    err_gpu = relative_error(Ah, H_gpu)
+    assert abs(err_gpu - err_ref) <= 0.01 * err_ref, (err_gpu, err_ref)
+    assert stats(H_gpu).final_d == stats(H_ref).final_d
+    print(f"C1 HSS relative error: reference {err_ref:.6e}, GPU sketch {err_gpu:.6e}, "
+          f"final_d {stats(H_gpu).final_d}")
