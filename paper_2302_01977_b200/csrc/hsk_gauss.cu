@@ -8,7 +8,7 @@
 // warp-level mma.sync.m8n8k4.f64 (SASS DMMA.8x8x4).  CTA tile BM x BN with
 // BK = 16 k-steps staged by a STAGES-deep cp.async ring; 8 warps, each a
 // (BM/2) x (BN/4) register tile of 8x8 DMMA fragments.  Shared-memory pitches
-// are chosen so every fragment load is two conflict-free wavefronts
+// are chosen so every fragment load is conflict-free
 // (DESIGN.md §Gaussian).  R is the reference's d x n row-major `matrix`,
 // i.e. R^T column-major with leading dimension n.
 #include <stdlib.h>
@@ -55,8 +55,10 @@ __device__ __forceinline__ void copy2(double *dst, const double *src, bool v0, b
 
 template <int BM, int BN, int TRANS>
 struct Smem {
-    static constexpr int PA = TRANS ? PKK : BM + 8;  // trans0: [BK][BM+8], BM+8 == 8 mod 16
-    static constexpr int A_ELEMS = TRANS ? BM * PKK : BK * (BM + 8);
+    // 8-byte fragment loads are serviced per half-warp (4 k x 4 rows): a pitch
+    // == 4 (mod 16) doubles puts the 4 k-rows on disjoint 8-bank groups.
+    static constexpr int PA = TRANS ? PKK : BM + 4;  // trans0: [BK][BM+4]
+    static constexpr int A_ELEMS = TRANS ? BM * PKK : BK * (BM + 4);
     static constexpr int B_ELEMS = BN * PKK;
     static constexpr int STAGE = A_ELEMS + B_ELEMS;
     static constexpr int BYTES = STAGES * STAGE * 8;
