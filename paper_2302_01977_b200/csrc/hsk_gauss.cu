@@ -12,6 +12,7 @@
 // (DESIGN.md §Gaussian).  R is the reference's d x n row-major `matrix`,
 // i.e. R^T column-major with leading dimension n.
 #include <stdlib.h>
+#include <string.h>
 
 #include <algorithm>
 
@@ -21,7 +22,6 @@ namespace hsk {
 namespace gauss {
 
 constexpr int BK = 16;
-constexpr int STAGES = 3;
 constexpr int PKK = BK + 4;  // pitch of k-contiguous tiles (== 4 mod 16)
 
 struct Args {
@@ -53,7 +53,7 @@ __device__ __forceinline__ void copy2(double *dst, const double *src, bool v0, b
     }
 }
 
-template <int BM, int BN, int TRANS>
+template <int BM, int BN, int TRANS, int STAGES>
 struct Smem {
     // 8-byte fragment loads are serviced per half-warp (4 k x 4 rows): a pitch
     // == 4 (mod 16) doubles puts the 4 k-rows on disjoint 8-bank groups.
@@ -64,26 +64,52 @@ struct Smem {
     static constexpr int BYTES = STAGES * STAGE * 8;
 };
 
-template <int BM, int BN, int TRANS>
-__global__ void __launch_bounds__(256) gauss_kernel(const Args p) {
-    using SM = Smem<BM, BN, TRANS>;
-    constexpr int WM = BM / 2, WN = BN / 4;
+// WGM x WGN warps, each a (BM/WGM) x (BN/WGN) tile of 8x8 DMMA fragments.
+template <int BM, int BN, int TRANS, int WGM, int WGN, int STAGES>
+__global__ void __launch_bounds__(WGM * WGN * 32) gauss_kernel(const Args p) {
+    using SM = Smem<BM, BN, TRANS, STAGES>;
+    constexpr int NT = WGM * WGN * 32;
+    constexpr int WM = BM / WGM, WN = BN / WGN;
     constexpr int MF = WM / 8, NF = WN / 8;
     extern __shared__ __align__(128) double sm[];
 
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int64_t nt = blockIdx.x % p.ntiles_n, mt = blockIdx.x / p.ntiles_n;
     const int64_t m0 = mt * BM, n0 = nt * BN;
-    const int wm0 = (warp >> 2) * WM, wn0 = (warp & 3) * WN;
+    const int wm0 = (warp / WGN) * WM, wn0 = (warp % WGN) * WN;
     const int64_t ktiles = (p.K + BK - 1) / BK;
 
+    // interior tiles (all rows/columns/k in range, 16-byte aligned operands)
+    // take an unpredicated copy path
+    const bool full_mn = (m0 + BM <= p.M) && (n0 + BN <= p.N) && p.a16 && p.b16;
     auto load_stage = [&](int64_t kt, int s) {
         double *sA = sm + s * SM::STAGE;
         double *sB = sA + SM::A_ELEMS;
         const int64_t k0 = kt * BK;
+        if (full_mn && k0 + BK <= p.K) {
+            if (!TRANS) {
+#pragma unroll
+                for (int q = tid; q < BK * (BM / 2); q += NT) {
+                    const int kk = q / (BM / 2), mm = (q % (BM / 2)) * 2;
+                    cp_async16(sA + kk * SM::PA + mm, p.A + (k0 + kk) * p.lda + m0 + mm, true);
+                }
+            } else {
+#pragma unroll
+                for (int q = tid; q < BM * (BK / 2); q += NT) {
+                    const int mm = q / (BK / 2), kk = (q % (BK / 2)) * 2;
+                    cp_async16(sA + mm * PKK + kk, p.A + (m0 + mm) * p.lda + k0 + kk, true);
+                }
+            }
+#pragma unroll
+            for (int q = tid; q < BN * (BK / 2); q += NT) {
+                const int jj = q / (BK / 2), kk = (q % (BK / 2)) * 2;
+                cp_async16(sB + jj * PKK + kk, p.R + (n0 + jj) * p.K + k0 + kk, true);
+            }
+            return;
+        }
         if (!TRANS) {
             // A(m,k) = A[k*lda + m]: BK columns of BM contiguous rows
-            for (int q = tid; q < BK * (BM / 2); q += 256) {
+            for (int q = tid; q < BK * (BM / 2); q += NT) {
                 const int kk = q / (BM / 2), mm = (q % (BM / 2)) * 2;
                 const int64_t gm = m0 + mm, gk = k0 + kk;
                 const bool vk = gk < p.K;
@@ -92,7 +118,7 @@ __global__ void __launch_bounds__(256) gauss_kernel(const Args p) {
             }
         } else {
             // A^T(m,k) = A[m*lda + k]: BM rows of BK contiguous k
-            for (int q = tid; q < BM * (BK / 2); q += 256) {
+            for (int q = tid; q < BM * (BK / 2); q += NT) {
                 const int mm = q / (BK / 2), kk = (q % (BK / 2)) * 2;
                 const int64_t gm = m0 + mm, gk = k0 + kk;
                 const bool vm = gm < p.M;
@@ -101,7 +127,7 @@ __global__ void __launch_bounds__(256) gauss_kernel(const Args p) {
             }
         }
         // B(k,j) = R[j*K + k]
-        for (int q = tid; q < BN * (BK / 2); q += 256) {
+        for (int q = tid; q < BN * (BK / 2); q += NT) {
             const int jj = q / (BK / 2), kk = (q % (BK / 2)) * 2;
             const int64_t gj = n0 + jj, gk = k0 + kk;
             const bool vj = gj < p.N;
@@ -121,15 +147,18 @@ __global__ void __launch_bounds__(256) gauss_kernel(const Args p) {
         if (s < ktiles) load_stage(s, s);
         cp_async_commit();
     }
+    int rs = 0, ws = STAGES - 1;  // read / write stage (incremental, no division)
     for (int64_t kt = 0; kt < ktiles; ++kt) {
         cp_async_wait<STAGES - 2>();
         __syncthreads();
         {
             const int64_t nk = kt + STAGES - 1;
-            if (nk < ktiles) load_stage(nk, (int)(nk % STAGES));
+            if (nk < ktiles) load_stage(nk, ws);
             cp_async_commit();
+            if (++ws == STAGES) ws = 0;
         }
-        const double *sA = sm + (kt % STAGES) * SM::STAGE;
+        const double *sA = sm + rs * SM::STAGE;
+        if (++rs == STAGES) rs = 0;
         const double *sB = sA + SM::A_ELEMS;
         const int fr = lane >> 2, fc = lane & 3;
 #pragma unroll
@@ -164,16 +193,16 @@ __global__ void __launch_bounds__(256) gauss_kernel(const Args p) {
     }
 }
 
-template <int BM, int BN, int TRANS>
+template <int BM, int BN, int TRANS, int WGM, int WGN, int STAGES>
 static int launch(Args a, cudaStream_t st) {
-    using SM = Smem<BM, BN, TRANS>;
-    auto kern = gauss_kernel<BM, BN, TRANS>;
+    using SM = Smem<BM, BN, TRANS, STAGES>;
+    auto kern = gauss_kernel<BM, BN, TRANS, WGM, WGN, STAGES>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SM::BYTES);
     if (e != cudaSuccess) return cuda_status(e, "gauss: set smem attribute");
     a.ntiles_n = (int)((a.N + BN - 1) / BN);
     const int64_t grid = ((a.M + BM - 1) / BM) * a.ntiles_n;
     HSK_REQUIRE(grid < (1ll << 31), HSK_EINVAL, "gauss: grid too large");
-    kern<<<(unsigned)grid, 256, SM::BYTES, st>>>(a);
+    kern<<<(unsigned)grid, WGM * WGN * 32, SM::BYTES, st>>>(a);
     HSK_CHECK_LAUNCH("gauss_kernel");
     return HSK_OK;
 }
@@ -213,8 +242,18 @@ extern "C" int hsk_gauss_apply(const double *A, int64_t rows, int64_t cols, int6
     a.a16 = ((reinterpret_cast<uintptr_t>(A) & 15) == 0) && (lda % 2 == 0);
     a.b16 = ((reinterpret_cast<uintptr_t>(R) & 15) == 0) && (n % 2 == 0);
     cudaStream_t st = as_stream(stream);
-    const char *cfg = getenv("HSK_GAUSS_CFG");  // tuning override: "64" -> 64 x 128 tiles
-    if (cfg && cfg[0] == '6')
-        return trans ? gauss::launch<64, 128, 1>(a, st) : gauss::launch<64, 128, 0>(a, st);
-    return trans ? gauss::launch<128, 128, 1>(a, st) : gauss::launch<128, 128, 0>(a, st);
+    // 64 x 64 tiles, 2 x 2 warps, 4 stages: many resident CTAs keep the FP64
+    // tensor pipe fed.  HSK_GAUSS_CFG overrides: "128" (128x128, 2x4 warps),
+    // "64x128" (2x4 warps).
+    const char *cfg = getenv("HSK_GAUSS_CFG");
+    if (cfg && !strcmp(cfg, "128"))
+        return trans ? gauss::launch<128, 128, 1, 2, 4, 3>(a, st)
+                     : gauss::launch<128, 128, 0, 2, 4, 3>(a, st);
+    if (cfg && !strcmp(cfg, "64x128"))
+        return trans ? gauss::launch<64, 128, 1, 2, 4, 3>(a, st)
+                     : gauss::launch<64, 128, 0, 2, 4, 3>(a, st);
+    if (cfg && !strcmp(cfg, "64x64x8"))
+        return trans ? gauss::launch<64, 64, 1, 2, 4, 4>(a, st)
+                     : gauss::launch<64, 64, 0, 2, 4, 4>(a, st);
+    return trans ? gauss::launch<64, 64, 1, 2, 2, 4>(a, st) : gauss::launch<64, 64, 0, 2, 2, 4>(a, st);
 }

@@ -165,38 +165,74 @@ __global__ void sjlt_plan_kernel(const int32_t *__restrict__ pos, const int8_t *
 // a contiguous 512 B).  S' tiles (swizzled, element (kk,row) at
 // kk*TM + (row ^ (kk%32))): rows l + 32 r (LDS.64 each, conflict-free).
 
-// Remaining entries [pe, pend) of one bucket (shared byte addresses), one
-// per iteration: consecutive DFMAs on an accumulator are a full iteration
-// (two shared loads) apart, so they never wait on each other.  `bra.uni`:
-// every lane walks the same list.
+// Entries [pe, pend) of one bucket (shared byte addresses), one per
+// iteration: consecutive DFMAs on an accumulator are a full iteration (two
+// shared loads) apart.  `bra.uni`: every lane walks the same list.
+// run_*f: the bucket's first entry is passed in registers (prefetched while
+// the previous bucket ran), so a bucket's chain starts at its tile load.
 // run_s*: S tiles, rows {2l, 2l+1} at [sx + o] (and {64+2l, 64+2l+1} at +512).
 // run_t*: S' tiles, rows l + 32 r at st + o + (x ^ lane8) + 256 r.
-__device__ __forceinline__ void run_s2(uint32_t pe, uint32_t pend, uint32_t sx, double &c0, double &c1) {
+__device__ __forceinline__ void run_s2(uint32_t &pe, uint32_t pend, uint32_t sx, double &c0, double &c1) {
     asm volatile("{\n\t.reg .pred p;\n\t.reg .b32 o0, x0, l0, h0, a0;\n\t.reg .f64 u0, v0, g0;\n\tsetp.ge.u32 p, %0, %3;\n\t@p bra.uni DONE;\n\tLOOP:\n\tld.shared.v4.b32 {o0, x0, l0, h0}, [%0];\n\tadd.u32 a0, o0, %4;\n\tld.shared.v2.f64 {u0, v0}, [a0];\n\tmov.b64 g0, {l0, h0};\n\tfma.rn.f64 %1, u0, g0, %1;\n\tfma.rn.f64 %2, v0, g0, %2;\n\tadd.u32 %0, %0, 16;\n\tsetp.lt.u32 p, %0, %3;\n\t@p bra.uni LOOP;\n\tDONE:\n\t}"
                  : "+r"(pe), "+d"(c0), "+d"(c1)
                  : "r"(pend), "r"(sx)
                  : "memory");
 }
 
-__device__ __forceinline__ void run_s4(uint32_t pe, uint32_t pend, uint32_t sx, double &c0, double &c1, double &c2, double &c3) {
-    asm volatile("{\n\t.reg .pred p;\n\t.reg .b32 o0, x0, l0, h0, a0;\n\t.reg .f64 u0, v0, w0, y0, g0;\n\tsetp.ge.u32 p, %0, %5;\n\t@p bra.uni DONE;\n\tLOOP:\n\tld.shared.v4.b32 {o0, x0, l0, h0}, [%0];\n\tadd.u32 a0, o0, %6;\n\tld.shared.v2.f64 {u0, v0}, [a0];\n\tld.shared.v2.f64 {w0, y0}, [a0+512];\n\tmov.b64 g0, {l0, h0};\n\tfma.rn.f64 %1, u0, g0, %1;\n\tfma.rn.f64 %2, v0, g0, %2;\n\tfma.rn.f64 %3, w0, g0, %3;\n\tfma.rn.f64 %4, y0, g0, %4;\n\tadd.u32 %0, %0, 16;\n\tsetp.lt.u32 p, %0, %5;\n\t@p bra.uni LOOP;\n\tDONE:\n\t}"
-                 : "+r"(pe), "+d"(c0), "+d"(c1), "+d"(c2), "+d"(c3)
-                 : "r"(pend), "r"(sx)
+__device__ __forceinline__ void run_s2f(uint32_t &pe, uint32_t pend, uint32_t sx, uint4 f, double &c0, double &c1) {
+    asm volatile("{\n\t.reg .pred p;\n\t.reg .b32 o0, x0, l0, h0, a0;\n\t.reg .f64 u0, v0, g0;\n\tsetp.ge.u32 p, %0, %3;\n\t@p bra.uni DONE;\n\tadd.u32 a0, %5, %4;\n\tld.shared.v2.f64 {u0, v0}, [a0];\n\tmov.b64 g0, {%7, %8};\n\tfma.rn.f64 %1, u0, g0, %1;\n\tfma.rn.f64 %2, v0, g0, %2;\n\tadd.u32 %0, %0, 16;\n\tsetp.ge.u32 p, %0, %3;\n\t@p bra.uni DONE;\n\tLOOP:\n\tld.shared.v4.b32 {o0, x0, l0, h0}, [%0];\n\tadd.u32 a0, o0, %4;\n\tld.shared.v2.f64 {u0, v0}, [a0];\n\tmov.b64 g0, {l0, h0};\n\tfma.rn.f64 %1, u0, g0, %1;\n\tfma.rn.f64 %2, v0, g0, %2;\n\tadd.u32 %0, %0, 16;\n\tsetp.lt.u32 p, %0, %3;\n\t@p bra.uni LOOP;\n\tDONE:\n\t}"
+                 : "+r"(pe), "+d"(c0), "+d"(c1)
+                 : "r"(pend), "r"(sx), "r"(f.x), "r"(f.y), "r"(f.z), "r"(f.w)
                  : "memory");
 }
 
-__device__ __forceinline__ void run_t2(uint32_t pe, uint32_t pend, uint32_t st, uint32_t lane8, double &c0, double &c1) {
+__device__ __forceinline__ void run_t2(uint32_t &pe, uint32_t pend, uint32_t st, uint32_t lane8, double &c0, double &c1) {
     asm volatile("{\n\t.reg .pred p;\n\t.reg .b32 o0, x0, l0, h0, a0;\n\t.reg .f64 u0, v0, g0;\n\tsetp.ge.u32 p, %0, %3;\n\t@p bra.uni DONE;\n\tLOOP:\n\tld.shared.v4.b32 {o0, x0, l0, h0}, [%0];\n\txor.b32 a0, x0, %5;\n\tadd.u32 a0, a0, o0;\n\tadd.u32 a0, a0, %4;\n\tld.shared.f64 u0, [a0];\n\tld.shared.f64 v0, [a0+256];\n\tmov.b64 g0, {l0, h0};\n\tfma.rn.f64 %1, u0, g0, %1;\n\tfma.rn.f64 %2, v0, g0, %2;\n\tadd.u32 %0, %0, 16;\n\tsetp.lt.u32 p, %0, %3;\n\t@p bra.uni LOOP;\n\tDONE:\n\t}"
                  : "+r"(pe), "+d"(c0), "+d"(c1)
                  : "r"(pend), "r"(st), "r"(lane8)
                  : "memory");
 }
 
-__device__ __forceinline__ void run_t4(uint32_t pe, uint32_t pend, uint32_t st, uint32_t lane8, double &c0, double &c1, double &c2, double &c3) {
+__device__ __forceinline__ void run_t2f(uint32_t &pe, uint32_t pend, uint32_t st, uint32_t lane8, uint4 f, double &c0, double &c1) {
+    asm volatile("{\n\t.reg .pred p;\n\t.reg .b32 o0, x0, l0, h0, a0;\n\t.reg .f64 u0, v0, g0;\n\tsetp.ge.u32 p, %0, %3;\n\t@p bra.uni DONE;\n\txor.b32 a0, %7, %5;\n\tadd.u32 a0, a0, %6;\n\tadd.u32 a0, a0, %4;\n\tld.shared.f64 u0, [a0];\n\tld.shared.f64 v0, [a0+256];\n\tmov.b64 g0, {%8, %9};\n\tfma.rn.f64 %1, u0, g0, %1;\n\tfma.rn.f64 %2, v0, g0, %2;\n\tadd.u32 %0, %0, 16;\n\tsetp.ge.u32 p, %0, %3;\n\t@p bra.uni DONE;\n\tLOOP:\n\tld.shared.v4.b32 {o0, x0, l0, h0}, [%0];\n\txor.b32 a0, x0, %5;\n\tadd.u32 a0, a0, o0;\n\tadd.u32 a0, a0, %4;\n\tld.shared.f64 u0, [a0];\n\tld.shared.f64 v0, [a0+256];\n\tmov.b64 g0, {l0, h0};\n\tfma.rn.f64 %1, u0, g0, %1;\n\tfma.rn.f64 %2, v0, g0, %2;\n\tadd.u32 %0, %0, 16;\n\tsetp.lt.u32 p, %0, %3;\n\t@p bra.uni LOOP;\n\tDONE:\n\t}"
+                 : "+r"(pe), "+d"(c0), "+d"(c1)
+                 : "r"(pend), "r"(st), "r"(lane8), "r"(f.x), "r"(f.y), "r"(f.z), "r"(f.w)
+                 : "memory");
+}
+
+__device__ __forceinline__ void run_s4(uint32_t &pe, uint32_t pend, uint32_t sx, double &c0, double &c1, double &c2, double &c3) {
+    asm volatile("{\n\t.reg .pred p;\n\t.reg .b32 o0, x0, l0, h0, a0;\n\t.reg .f64 u0, v0, w0, y0, g0;\n\tsetp.ge.u32 p, %0, %5;\n\t@p bra.uni DONE;\n\tLOOP:\n\tld.shared.v4.b32 {o0, x0, l0, h0}, [%0];\n\tadd.u32 a0, o0, %6;\n\tld.shared.v2.f64 {u0, v0}, [a0];\n\tld.shared.v2.f64 {w0, y0}, [a0+512];\n\tmov.b64 g0, {l0, h0};\n\tfma.rn.f64 %1, u0, g0, %1;\n\tfma.rn.f64 %2, v0, g0, %2;\n\tfma.rn.f64 %3, w0, g0, %3;\n\tfma.rn.f64 %4, y0, g0, %4;\n\tadd.u32 %0, %0, 16;\n\tsetp.lt.u32 p, %0, %5;\n\t@p bra.uni LOOP;\n\tDONE:\n\t}"
+                 : "+r"(pe), "+d"(c0), "+d"(c1), "+d"(c2), "+d"(c3)
+                 : "r"(pend), "r"(sx)
+                 : "memory");
+}
+
+__device__ __forceinline__ void run_s4f(uint32_t &pe, uint32_t pend, uint32_t sx, uint4 f, double &c0, double &c1, double &c2, double &c3) {
+    asm volatile("{\n\t.reg .pred p;\n\t.reg .b32 o0, x0, l0, h0, a0;\n\t.reg .f64 u0, v0, w0, y0, g0;\n\tsetp.ge.u32 p, %0, %5;\n\t@p bra.uni DONE;\n\tadd.u32 a0, %7, %6;\n\tld.shared.v2.f64 {u0, v0}, [a0];\n\tld.shared.v2.f64 {w0, y0}, [a0+512];\n\tmov.b64 g0, {%9, %10};\n\tfma.rn.f64 %1, u0, g0, %1;\n\tfma.rn.f64 %2, v0, g0, %2;\n\tfma.rn.f64 %3, w0, g0, %3;\n\tfma.rn.f64 %4, y0, g0, %4;\n\tadd.u32 %0, %0, 16;\n\tsetp.ge.u32 p, %0, %5;\n\t@p bra.uni DONE;\n\tLOOP:\n\tld.shared.v4.b32 {o0, x0, l0, h0}, [%0];\n\tadd.u32 a0, o0, %6;\n\tld.shared.v2.f64 {u0, v0}, [a0];\n\tld.shared.v2.f64 {w0, y0}, [a0+512];\n\tmov.b64 g0, {l0, h0};\n\tfma.rn.f64 %1, u0, g0, %1;\n\tfma.rn.f64 %2, v0, g0, %2;\n\tfma.rn.f64 %3, w0, g0, %3;\n\tfma.rn.f64 %4, y0, g0, %4;\n\tadd.u32 %0, %0, 16;\n\tsetp.lt.u32 p, %0, %5;\n\t@p bra.uni LOOP;\n\tDONE:\n\t}"
+                 : "+r"(pe), "+d"(c0), "+d"(c1), "+d"(c2), "+d"(c3)
+                 : "r"(pend), "r"(sx), "r"(f.x), "r"(f.y), "r"(f.z), "r"(f.w)
+                 : "memory");
+}
+
+__device__ __forceinline__ void run_t4(uint32_t &pe, uint32_t pend, uint32_t st, uint32_t lane8, double &c0, double &c1, double &c2, double &c3) {
     asm volatile("{\n\t.reg .pred p;\n\t.reg .b32 o0, x0, l0, h0, a0;\n\t.reg .f64 u0, v0, w0, y0, g0;\n\tsetp.ge.u32 p, %0, %5;\n\t@p bra.uni DONE;\n\tLOOP:\n\tld.shared.v4.b32 {o0, x0, l0, h0}, [%0];\n\txor.b32 a0, x0, %7;\n\tadd.u32 a0, a0, o0;\n\tadd.u32 a0, a0, %6;\n\tld.shared.f64 u0, [a0];\n\tld.shared.f64 v0, [a0+256];\n\tld.shared.f64 w0, [a0+512];\n\tld.shared.f64 y0, [a0+768];\n\tmov.b64 g0, {l0, h0};\n\tfma.rn.f64 %1, u0, g0, %1;\n\tfma.rn.f64 %2, v0, g0, %2;\n\tfma.rn.f64 %3, w0, g0, %3;\n\tfma.rn.f64 %4, y0, g0, %4;\n\tadd.u32 %0, %0, 16;\n\tsetp.lt.u32 p, %0, %5;\n\t@p bra.uni LOOP;\n\tDONE:\n\t}"
                  : "+r"(pe), "+d"(c0), "+d"(c1), "+d"(c2), "+d"(c3)
                  : "r"(pend), "r"(st), "r"(lane8)
                  : "memory");
+}
+
+__device__ __forceinline__ void run_t4f(uint32_t &pe, uint32_t pend, uint32_t st, uint32_t lane8, uint4 f, double &c0, double &c1, double &c2, double &c3) {
+    asm volatile("{\n\t.reg .pred p;\n\t.reg .b32 o0, x0, l0, h0, a0;\n\t.reg .f64 u0, v0, w0, y0, g0;\n\tsetp.ge.u32 p, %0, %5;\n\t@p bra.uni DONE;\n\txor.b32 a0, %9, %7;\n\tadd.u32 a0, a0, %8;\n\tadd.u32 a0, a0, %6;\n\tld.shared.f64 u0, [a0];\n\tld.shared.f64 v0, [a0+256];\n\tld.shared.f64 w0, [a0+512];\n\tld.shared.f64 y0, [a0+768];\n\tmov.b64 g0, {%10, %11};\n\tfma.rn.f64 %1, u0, g0, %1;\n\tfma.rn.f64 %2, v0, g0, %2;\n\tfma.rn.f64 %3, w0, g0, %3;\n\tfma.rn.f64 %4, y0, g0, %4;\n\tadd.u32 %0, %0, 16;\n\tsetp.ge.u32 p, %0, %5;\n\t@p bra.uni DONE;\n\tLOOP:\n\tld.shared.v4.b32 {o0, x0, l0, h0}, [%0];\n\txor.b32 a0, x0, %7;\n\tadd.u32 a0, a0, o0;\n\tadd.u32 a0, a0, %6;\n\tld.shared.f64 u0, [a0];\n\tld.shared.f64 v0, [a0+256];\n\tld.shared.f64 w0, [a0+512];\n\tld.shared.f64 y0, [a0+768];\n\tmov.b64 g0, {l0, h0};\n\tfma.rn.f64 %1, u0, g0, %1;\n\tfma.rn.f64 %2, v0, g0, %2;\n\tfma.rn.f64 %3, w0, g0, %3;\n\tfma.rn.f64 %4, y0, g0, %4;\n\tadd.u32 %0, %0, 16;\n\tsetp.lt.u32 p, %0, %5;\n\t@p bra.uni LOOP;\n\tDONE:\n\t}"
+                 : "+r"(pe), "+d"(c0), "+d"(c1), "+d"(c2), "+d"(c3)
+                 : "r"(pend), "r"(st), "r"(lane8), "r"(f.x), "r"(f.y), "r"(f.z), "r"(f.w)
+                 : "memory");
+}
+
+__device__ __forceinline__ uint4 lds_u4(uint32_t addr) {
+    uint4 w;
+    asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];"
+                 : "=r"(w.x), "=r"(w.y), "=r"(w.z), "=r"(w.w) : "r"(addr) : "memory");
+    return w;
 }
 
 struct ApplyArgs {
@@ -388,19 +424,23 @@ __global__ void __launch_bounds__((NW + (PROD ? 1 : 0)) * 32, 1)
             return (jj & 1) ? (bw[jj >> 1] >> 16) : (bw[jj >> 1] & 0xffffu);
         };
         if (!BATCH) {
-            // plain per-bucket loops over all entries
+            // per-bucket loops; the first entry of bucket jj+1 is loaded while
+            // bucket jj runs (index <= estride: the null entry keeps it in range)
             uint32_t pe = sen + 16u * bound(0);
+            uint4 wn = lds_u4(pe);
 #pragma unroll
             for (int jj = 0; jj < DB; ++jj) {
                 const uint32_t pend = sen + 16u * bound(jj + 1);
+                const uint4 w = wn;
+                if (jj + 1 < DB) wn = lds_u4(pend);
                 if (TRANS) {
-                    if (RPT == 2) run_t2(pe, pend, st, lane8, acc[0][jj], acc[1][jj]);
-                    else run_t4(pe, pend, st, lane8, acc[0][jj], acc[1][jj], acc[RPT - 2][jj],
-                                acc[RPT - 1][jj]);
+                    if (RPT == 2) run_t2f(pe, pend, st, lane8, w, acc[0][jj], acc[1][jj]);
+                    else run_t4f(pe, pend, st, lane8, w, acc[0][jj], acc[1][jj], acc[RPT - 2][jj],
+                                 acc[RPT - 1][jj]);
                 } else {
-                    if (RPT == 2) run_s2(pe, pend, sx, acc[0][jj], acc[1][jj]);
-                    else run_s4(pe, pend, sx, acc[0][jj], acc[1][jj], acc[RPT - 2][jj],
-                                acc[RPT - 1][jj]);
+                    if (RPT == 2) run_s2f(pe, pend, sx, w, acc[0][jj], acc[1][jj]);
+                    else run_s4f(pe, pend, sx, w, acc[0][jj], acc[1][jj], acc[RPT - 2][jj],
+                                 acc[RPT - 1][jj]);
                 }
                 pe = pend;
             }
@@ -447,7 +487,8 @@ __global__ void __launch_bounds__((NW + (PROD ? 1 : 0)) * 32, 1)
 #pragma unroll
             for (int t = 0; t < G; ++t) {
                 const int jj = g0 + t;
-                const uint32_t pe = sen + 16u * (b[t] + 1), pend = sen + 16u * b[t + 1];
+                uint32_t pe = sen + 16u * (b[t] + 1);
+                const uint32_t pend = sen + 16u * b[t + 1];
                 if (TRANS) {
                     if (RPT == 2) run_t2(pe, pend, st, lane8, acc[0][jj], acc[1][jj]);
                     else run_t4(pe, pend, st, lane8, acc[0][jj], acc[1][jj], acc[RPT - 2][jj],
