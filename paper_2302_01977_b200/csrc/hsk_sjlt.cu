@@ -263,7 +263,7 @@ __global__ void __launch_bounds__((NW + (PROD ? 1 : 0)) * 32, 1)
     sjlt_apply_kernel(const ApplyArgs p, const __grid_constant__ CUtensorMap tmap) {
     constexpr int TM = 32 * RPT;
     constexpr int SLAB = NW * DB;
-    constexpr int G = 4;  // buckets whose first entries are folded as one batch
+    constexpr int G = DB < 4 ? DB : 4;  // buckets whose first entries are folded as one batch
     static_assert(DB % G == 0, "DB must be a multiple of the batch");
     extern __shared__ __align__(128) unsigned char smem[];
     uint64_t *full = reinterpret_cast<uint64_t *>(smem);
@@ -738,6 +738,12 @@ extern "C" int hsk_sjlt_apply(const double *A, int64_t rows, int64_t cols, int64
     a.lds = lds;
     a.col0 = col0;
     cudaStream_t st = as_stream(stream);
+    const char *w32 = getenv("HSK_SJLT_W32");  // 32 warps x fewer buckets (tuning)
+    if (w32 && w32[0] == '1') {
+        if (d <= 64) return sjlt::launch<4, 2, 32>(a, g, st);
+        if (d <= 128) return sjlt::launch<2, 4, 32>(a, g, st);
+        return sjlt::launch<2, 8, 32>(a, g, st);
+    }
     if (d <= 64) return sjlt::launch<4, 4, 16>(a, g, st);
     if (d <= 128) return sjlt::launch<2, 8, 16>(a, g, st);
     return sjlt::launch<2, 16, 16>(a, g, st);
