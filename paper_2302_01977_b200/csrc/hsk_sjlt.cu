@@ -620,7 +620,7 @@ static int launch(ApplyArgs a, const Geom &g, cudaStream_t st) {
     if (const char *env = getenv("HSK_SJLT_BATCH")) batch = env[0] == '1';
     // dedicated producer warp (TMA path only; 17 warps -> 96-register budget,
     // so it pairs with the unbatched consumer loops)
-    bool prod = true;
+    bool prod = NW < 32;  // a 33rd warp would cut the register budget to 56
     if (const char *env = getenv("HSK_SJLT_PROD")) prod = env[0] == '1';
     prod = prod && a.mode == 0;
     if (prod) batch = false;
@@ -738,8 +738,12 @@ extern "C" int hsk_sjlt_apply(const double *A, int64_t rows, int64_t cols, int64
     a.lds = lds;
     a.col0 = col0;
     cudaStream_t st = as_stream(stream);
-    const char *w32 = getenv("HSK_SJLT_W32");  // 32 warps x fewer buckets (tuning)
-    if (w32 && w32[0] == '1') {
+    // S: 32 warps x (DB/2) buckets -- twice the warps to hide the shared-memory
+    // latency of the entry -> tile -> DFMA chain (<= 64 registers per thread).
+    // S': 16 warps (its cp.async producer work is shared by all warps).
+    bool w32 = !trans;
+    if (const char *env = getenv("HSK_SJLT_W32")) w32 = env[0] == '1';
+    if (w32) {
         if (d <= 64) return sjlt::launch<4, 2, 32>(a, g, st);
         if (d <= 128) return sjlt::launch<2, 4, 32>(a, g, st);
         return sjlt::launch<2, 8, 32>(a, g, st);
