@@ -228,6 +228,57 @@ __device__ __forceinline__ void run_t4f(uint32_t &pe, uint32_t pend, uint32_t st
                  : "memory");
 }
 
+// Whole-chunk consumers: one PTX block walks all DB buckets of the warp
+// (bounds unpacked in-line, uniform branches, no convergence barriers
+// between buckets): ~4 instructions per empty bucket, 8 per entry.
+// one warp, one chunk, all 8 buckets, RPT = 2 (S tiles)
+__device__ __forceinline__ void chunk_s_2x8(double (&acc)[2][8], uint32_t sen, uint32_t sx, const uint32_t (&bw)[5]) {
+    asm volatile("{\n\t.reg .pred p;\n\t.reg .b32 o, x, gl, gh, a, t, pe, pend;\n\t.reg .f64 u, v, w, y, g;\n\tand.b32 t, %18, 65535;\n\tmad.lo.u32 pe, t, 16, %16;\n\tshr.u32 t, %18, 16;\n\tmad.lo.u32 pend, t, 16, %16;\n\tsetp.ge.u32 p, pe, pend;\n\t@p bra.uni B0_DONE;\n\tB0_LOOP:\n\tld.shared.v4.b32 {o, x, gl, gh}, [pe];\n\tadd.u32 a, o, %17;\n\tld.shared.v2.f64 {u, v}, [a];\n\tmov.b64 g, {gl, gh};\n\tfma.rn.f64 %0, u, g, %0;\n\tfma.rn.f64 %1, v, g, %1;\n\tadd.u32 pe, pe, 16;\n\tsetp.lt.u32 p, pe, pend;\n\t@p bra.uni B0_LOOP;\n\tB0_DONE:\n\tmov.b32 pe, pend;\n\tand.b32 t, %19, 65535;\n\tmad.lo.u32 pend, t, 16, %16;\n\tsetp.ge.u32 p, pe, pend;\n\t@p bra.uni B1_DONE;\n\tB1_LOOP:\n\tld.shared.v4.b32 {o, x, gl, gh}, [pe];\n\tadd.u32 a, o, %17;\n\tld.shared.v2.f64 {u, v}, [a];\n\tmov.b64 g, {gl, gh};\n\tfma.rn.f64 %2, u, g, %2;\n\tfma.rn.f64 %3, v, g, %3;\n\tadd.u32 pe, pe, 16;\n\tsetp.lt.u32 p, pe, pend;\n\t@p bra.uni B1_LOOP;\n\tB1_DONE:\n\tmov.b32 pe, pend;\n\tshr.u32 t, %19, 16;\n\tmad.lo.u32 pend, t, 16, %16;\n\tsetp.ge.u32 p, pe, pend;\n\t@p bra.uni B2_DONE;\n\tB2_LOOP:\n\tld.shared.v4.b32 {o, x, gl, gh}, [pe];\n\tadd.u32 a, o, %17;\n\tld.shared.v2.f64 {u, v}, [a];\n\tmov.b64 g, {gl, gh};\n\tfma.rn.f64 %4, u, g, %4;\n\tfma.rn.f64 %5, v, g, %5;\n\tadd.u32 pe, pe, 16;\n\tsetp.lt.u32 p, pe, pend;\n\t@p bra.uni B2_LOOP;\n\tB2_DONE:\n\tmov.b32 pe, pend;\n\tand.b32 t, %20, 65535;\n\tmad.lo.u32 pend, t, 16, %16;\n\tsetp.ge.u32 p, pe, pend;\n\t@p bra.uni B3_DONE;\n\tB3_LOOP:\n\tld.shared.v4.b32 {o, x, gl, gh}, [pe];\n\tadd.u32 a, o, %17;\n\tld.shared.v2.f64 {u, v}, [a];\n\tmov.b64 g, {gl, gh};\n\tfma.rn.f64 %6, u, g, %6;\n\tfma.rn.f64 %7, v, g, %7;\n\tadd.u32 pe, pe, 16;\n\tsetp.lt.u32 p, pe, pend;\n\t@p bra.uni B3_LOOP;\n\tB3_DONE:\n\tmov.b32 pe, pend;\n\tshr.u32 t, %20, 16;\n\tmad.lo.u32 pend, t, 16, %16;\n\tsetp.ge.u32 p, pe, pend;\n\t@p bra.uni B4_DONE;\n\tB4_LOOP:\n\tld.shared.v4.b32 {o, x, gl, gh}, [pe];\n\tadd.u32 a, o, %17;\n\tld.shared.v2.f64 {u, v}, [a];\n\tmov.b64 g, {gl, gh};\n\tfma.rn.f64 %8, u, g, %8;\n\tfma.rn.f64 %9, v, g, %9;\n\tadd.u32 pe, pe, 16;\n\tsetp.lt.u32 p, pe, pend;\n\t@p bra.uni B4_LOOP;\n\tB4_DONE:\n\tmov.b32 pe, pend;\n\tand.b32 t, %21, 65535;\n\tmad.lo.u32 pend, t, 16, %16;\n\tsetp.ge.u32 p, pe, pend;\n\t@p bra.uni B5_DONE;\n\tB5_LOOP:\n\tld.shared.v4.b32 {o, x, gl, gh}, [pe];\n\tadd.u32 a, o, %17;\n\tld.shared.v2.f64 {u, v}, [a];\n\tmov.b64 g, {gl, gh};\n\tfma.rn.f64 %10, u, g, %10;\n\tfma.rn.f64 %11, v, g, %11;\n\tadd.u32 pe, pe, 16;\n\tsetp.lt.u32 p, pe, pend;\n\t@p bra.uni B5_LOOP;\n\tB5_DONE:\n\tmov.b32 pe, pend;\n\tshr.u32 t, %21, 16;\n\tmad.lo.u32 pend, t, 16, %16;\n\tsetp.ge.u32 p, pe, pend;\n\t@p bra.uni B6_DONE;\n\tB6_LOOP:\n\tld.shared.v4.b32 {o, x, gl, gh}, [pe];\n\tadd.u32 a, o, %17;\n\tld.shared.v2.f64 {u, v}, [a];\n\tmov.b64 g, {gl, gh};\n\tfma.rn.f64 %12, u, g, %12;\n\tfma.rn.f64 %13, v, g, %13;\n\tadd.u32 pe, pe, 16;\n\tsetp.lt.u32 p, pe, pend;\n\t@p bra.uni B6_LOOP;\n\tB6_DONE:\n\tmov.b32 pe, pend;\n\tand.b32 t, %22, 65535;\n\tmad.lo.u32 pend, t, 16, %16;\n\tsetp.ge.u32 p, pe, pend;\n\t@p bra.uni B7_DONE;\n\tB7_LOOP:\n\tld.shared.v4.b32 {o, x, gl, gh}, [pe];\n\tadd.u32 a, o, %17;\n\tld.shared.v2.f64 {u, v}, [a];\n\tmov.b64 g, {gl, gh};\n\tfma.rn.f64 %14, u, g, %14;\n\tfma.rn.f64 %15, v, g, %15;\n\tadd.u32 pe, pe, 16;\n\tsetp.lt.u32 p, pe, pend;\n\t@p bra.uni B7_LOOP;\n\tB7_DONE:\n\tmov.b32 pe, pend;\n\t}"
+                 : "+d"(acc[0][0]), "+d"(acc[1][0]), "+d"(acc[0][1]), "+d"(acc[1][1]), "+d"(acc[0][2]), "+d"(acc[1][2]), "+d"(acc[0][3]), "+d"(acc[1][3]), "+d"(acc[0][4]), "+d"(acc[1][4]), "+d"(acc[0][5]), "+d"(acc[1][5]), "+d"(acc[0][6]), "+d"(acc[1][6]), "+d"(acc[0][7]), "+d"(acc[1][7])
+                 : "r"(sen), "r"(sx), "r"(bw[0]), "r"(bw[1]), "r"(bw[2]), "r"(bw[3]), "r"(bw[4])
+                 : "memory");
+}
+
+// one warp, one chunk, all 4 buckets, RPT = 2 (S tiles)
+__device__ __forceinline__ void chunk_s_2x4(double (&acc)[2][4], uint32_t sen, uint32_t sx, const uint32_t (&bw)[3]) {
+    asm volatile("{\n\t.reg .pred p;\n\t.reg .b32 o, x, gl, gh, a, t, pe, pend;\n\t.reg .f64 u, v, w, y, g;\n\tand.b32 t, %10, 65535;\n\tmad.lo.u32 pe, t, 16, %8;\n\tshr.u32 t, %10, 16;\n\tmad.lo.u32 pend, t, 16, %8;\n\tsetp.ge.u32 p, pe, pend;\n\t@p bra.uni B0_DONE;\n\tB0_LOOP:\n\tld.shared.v4.b32 {o, x, gl, gh}, [pe];\n\tadd.u32 a, o, %9;\n\tld.shared.v2.f64 {u, v}, [a];\n\tmov.b64 g, {gl, gh};\n\tfma.rn.f64 %0, u, g, %0;\n\tfma.rn.f64 %1, v, g, %1;\n\tadd.u32 pe, pe, 16;\n\tsetp.lt.u32 p, pe, pend;\n\t@p bra.uni B0_LOOP;\n\tB0_DONE:\n\tmov.b32 pe, pend;\n\tand.b32 t, %11, 65535;\n\tmad.lo.u32 pend, t, 16, %8;\n\tsetp.ge.u32 p, pe, pend;\n\t@p bra.uni B1_DONE;\n\tB1_LOOP:\n\tld.shared.v4.b32 {o, x, gl, gh}, [pe];\n\tadd.u32 a, o, %9;\n\tld.shared.v2.f64 {u, v}, [a];\n\tmov.b64 g, {gl, gh};\n\tfma.rn.f64 %2, u, g, %2;\n\tfma.rn.f64 %3, v, g, %3;\n\tadd.u32 pe, pe, 16;\n\tsetp.lt.u32 p, pe, pend;\n\t@p bra.uni B1_LOOP;\n\tB1_DONE:\n\tmov.b32 pe, pend;\n\tshr.u32 t, %11, 16;\n\tmad.lo.u32 pend, t, 16, %8;\n\tsetp.ge.u32 p, pe, pend;\n\t@p bra.uni B2_DONE;\n\tB2_LOOP:\n\tld.shared.v4.b32 {o, x, gl, gh}, [pe];\n\tadd.u32 a, o, %9;\n\tld.shared.v2.f64 {u, v}, [a];\n\tmov.b64 g, {gl, gh};\n\tfma.rn.f64 %4, u, g, %4;\n\tfma.rn.f64 %5, v, g, %5;\n\tadd.u32 pe, pe, 16;\n\tsetp.lt.u32 p, pe, pend;\n\t@p bra.uni B2_LOOP;\n\tB2_DONE:\n\tmov.b32 pe, pend;\n\tand.b32 t, %12, 65535;\n\tmad.lo.u32 pend, t, 16, %8;\n\tsetp.ge.u32 p, pe, pend;\n\t@p bra.uni B3_DONE;\n\tB3_LOOP:\n\tld.shared.v4.b32 {o, x, gl, gh}, [pe];\n\tadd.u32 a, o, %9;\n\tld.shared.v2.f64 {u, v}, [a];\n\tmov.b64 g, {gl, gh};\n\tfma.rn.f64 %6, u, g, %6;\n\tfma.rn.f64 %7, v, g, %7;\n\tadd.u32 pe, pe, 16;\n\tsetp.lt.u32 p, pe, pend;\n\t@p bra.uni B3_LOOP;\n\tB3_DONE:\n\tmov.b32 pe, pend;\n\t}"
+                 : "+d"(acc[0][0]), "+d"(acc[1][0]), "+d"(acc[0][1]), "+d"(acc[1][1]), "+d"(acc[0][2]), "+d"(acc[1][2]), "+d"(acc[0][3]), "+d"(acc[1][3])
+                 : "r"(sen), "r"(sx), "r"(bw[0]), "r"(bw[1]), "r"(bw[2])
+                 : "memory");
+}
+
+// one warp, one chunk, all 2 buckets, RPT = 4 (S tiles)
+__device__ __forceinline__ void chunk_s_4x2(double (&acc)[4][2], uint32_t sen, uint32_t sx, const uint32_t (&bw)[2]) {
+    asm volatile("{\n\t.reg .pred p;\n\t.reg .b32 o, x, gl, gh, a, t, pe, pend;\n\t.reg .f64 u, v, w, y, g;\n\tand.b32 t, %10, 65535;\n\tmad.lo.u32 pe, t, 16, %8;\n\tshr.u32 t, %10, 16;\n\tmad.lo.u32 pend, t, 16, %8;\n\tsetp.ge.u32 p, pe, pend;\n\t@p bra.uni B0_DONE;\n\tB0_LOOP:\n\tld.shared.v4.b32 {o, x, gl, gh}, [pe];\n\tadd.u32 a, o, %9;\n\tld.shared.v2.f64 {u, v}, [a];\n\tld.shared.v2.f64 {w, y}, [a+512];\n\tmov.b64 g, {gl, gh};\n\tfma.rn.f64 %0, u, g, %0;\n\tfma.rn.f64 %1, v, g, %1;\n\tfma.rn.f64 %2, w, g, %2;\n\tfma.rn.f64 %3, y, g, %3;\n\tadd.u32 pe, pe, 16;\n\tsetp.lt.u32 p, pe, pend;\n\t@p bra.uni B0_LOOP;\n\tB0_DONE:\n\tmov.b32 pe, pend;\n\tand.b32 t, %11, 65535;\n\tmad.lo.u32 pend, t, 16, %8;\n\tsetp.ge.u32 p, pe, pend;\n\t@p bra.uni B1_DONE;\n\tB1_LOOP:\n\tld.shared.v4.b32 {o, x, gl, gh}, [pe];\n\tadd.u32 a, o, %9;\n\tld.shared.v2.f64 {u, v}, [a];\n\tld.shared.v2.f64 {w, y}, [a+512];\n\tmov.b64 g, {gl, gh};\n\tfma.rn.f64 %4, u, g, %4;\n\tfma.rn.f64 %5, v, g, %5;\n\tfma.rn.f64 %6, w, g, %6;\n\tfma.rn.f64 %7, y, g, %7;\n\tadd.u32 pe, pe, 16;\n\tsetp.lt.u32 p, pe, pend;\n\t@p bra.uni B1_LOOP;\n\tB1_DONE:\n\tmov.b32 pe, pend;\n\t}"
+                 : "+d"(acc[0][0]), "+d"(acc[1][0]), "+d"(acc[2][0]), "+d"(acc[3][0]), "+d"(acc[0][1]), "+d"(acc[1][1]), "+d"(acc[2][1]), "+d"(acc[3][1])
+                 : "r"(sen), "r"(sx), "r"(bw[0]), "r"(bw[1])
+                 : "memory");
+}
+
+// one warp, one chunk, all 4 buckets, RPT = 4 (S tiles)
+__device__ __forceinline__ void chunk_s_4x4(double (&acc)[4][4], uint32_t sen, uint32_t sx, const uint32_t (&bw)[3]) {
+    asm volatile("{\n\t.reg .pred p;\n\t.reg .b32 o, x, gl, gh, a, t, pe, pend;\n\t.reg .f64 u, v, w, y, g;\n\tand.b32 t, %18, 65535;\n\tmad.lo.u32 pe, t, 16, %16;\n\tshr.u32 t, %18, 16;\n\tmad.lo.u32 pend, t, 16, %16;\n\tsetp.ge.u32 p, pe, pend;\n\t@p bra.uni B0_DONE;\n\tB0_LOOP:\n\tld.shared.v4.b32 {o, x, gl, gh}, [pe];\n\tadd.u32 a, o, %17;\n\tld.shared.v2.f64 {u, v}, [a];\n\tld.shared.v2.f64 {w, y}, [a+512];\n\tmov.b64 g, {gl, gh};\n\tfma.rn.f64 %0, u, g, %0;\n\tfma.rn.f64 %1, v, g, %1;\n\tfma.rn.f64 %2, w, g, %2;\n\tfma.rn.f64 %3, y, g, %3;\n\tadd.u32 pe, pe, 16;\n\tsetp.lt.u32 p, pe, pend;\n\t@p bra.uni B0_LOOP;\n\tB0_DONE:\n\tmov.b32 pe, pend;\n\tand.b32 t, %19, 65535;\n\tmad.lo.u32 pend, t, 16, %16;\n\tsetp.ge.u32 p, pe, pend;\n\t@p bra.uni B1_DONE;\n\tB1_LOOP:\n\tld.shared.v4.b32 {o, x, gl, gh}, [pe];\n\tadd.u32 a, o, %17;\n\tld.shared.v2.f64 {u, v}, [a];\n\tld.shared.v2.f64 {w, y}, [a+512];\n\tmov.b64 g, {gl, gh};\n\tfma.rn.f64 %4, u, g, %4;\n\tfma.rn.f64 %5, v, g, %5;\n\tfma.rn.f64 %6, w, g, %6;\n\tfma.rn.f64 %7, y, g, %7;\n\tadd.u32 pe, pe, 16;\n\tsetp.lt.u32 p, pe, pend;\n\t@p bra.uni B1_LOOP;\n\tB1_DONE:\n\tmov.b32 pe, pend;\n\tshr.u32 t, %19, 16;\n\tmad.lo.u32 pend, t, 16, %16;\n\tsetp.ge.u32 p, pe, pend;\n\t@p bra.uni B2_DONE;\n\tB2_LOOP:\n\tld.shared.v4.b32 {o, x, gl, gh}, [pe];\n\tadd.u32 a, o, %17;\n\tld.shared.v2.f64 {u, v}, [a];\n\tld.shared.v2.f64 {w, y}, [a+512];\n\tmov.b64 g, {gl, gh};\n\tfma.rn.f64 %8, u, g, %8;\n\tfma.rn.f64 %9, v, g, %9;\n\tfma.rn.f64 %10, w, g, %10;\n\tfma.rn.f64 %11, y, g, %11;\n\tadd.u32 pe, pe, 16;\n\tsetp.lt.u32 p, pe, pend;\n\t@p bra.uni B2_LOOP;\n\tB2_DONE:\n\tmov.b32 pe, pend;\n\tand.b32 t, %20, 65535;\n\tmad.lo.u32 pend, t, 16, %16;\n\tsetp.ge.u32 p, pe, pend;\n\t@p bra.uni B3_DONE;\n\tB3_LOOP:\n\tld.shared.v4.b32 {o, x, gl, gh}, [pe];\n\tadd.u32 a, o, %17;\n\tld.shared.v2.f64 {u, v}, [a];\n\tld.shared.v2.f64 {w, y}, [a+512];\n\tmov.b64 g, {gl, gh};\n\tfma.rn.f64 %12, u, g, %12;\n\tfma.rn.f64 %13, v, g, %13;\n\tfma.rn.f64 %14, w, g, %14;\n\tfma.rn.f64 %15, y, g, %15;\n\tadd.u32 pe, pe, 16;\n\tsetp.lt.u32 p, pe, pend;\n\t@p bra.uni B3_LOOP;\n\tB3_DONE:\n\tmov.b32 pe, pend;\n\t}"
+                 : "+d"(acc[0][0]), "+d"(acc[1][0]), "+d"(acc[2][0]), "+d"(acc[3][0]), "+d"(acc[0][1]), "+d"(acc[1][1]), "+d"(acc[2][1]), "+d"(acc[3][1]), "+d"(acc[0][2]), "+d"(acc[1][2]), "+d"(acc[2][2]), "+d"(acc[3][2]), "+d"(acc[0][3]), "+d"(acc[1][3]), "+d"(acc[2][3]), "+d"(acc[3][3])
+                 : "r"(sen), "r"(sx), "r"(bw[0]), "r"(bw[1]), "r"(bw[2])
+                 : "memory");
+}
+
+// one warp, one chunk, all 16 buckets, RPT = 2 (S tiles)
+__device__ __forceinline__ void chunk_s_2x16(double (&acc)[2][16], uint32_t sen, uint32_t sx, const uint32_t (&bw)[9]) {
+    asm volatile("{\n\t.reg .pred p;\n\t.reg .b32 o, x, gl, gh, a, t, pe, pend;\n\t.reg .f64 u, v, w, y, g;\n\tand.b32 t, %34, 65535;\n\tmad.lo.u32 pe, t, 16, %32;\n\tshr.u32 t, %34, 16;\n\tmad.lo.u32 pend, t, 16, %32;\n\tsetp.ge.u32 p, pe, pend;\n\t@p bra.uni B0_DONE;\n\tB0_LOOP:\n\tld.shared.v4.b32 {o, x, gl, gh}, [pe];\n\tadd.u32 a, o, %33;\n\tld.shared.v2.f64 {u, v}, [a];\n\tmov.b64 g, {gl, gh};\n\tfma.rn.f64 %0, u, g, %0;\n\tfma.rn.f64 %1, v, g, %1;\n\tadd.u32 pe, pe, 16;\n\tsetp.lt.u32 p, pe, pend;\n\t@p bra.uni B0_LOOP;\n\tB0_DONE:\n\tmov.b32 pe, pend;\n\tand.b32 t, %35, 65535;\n\tmad.lo.u32 pend, t, 16, %32;\n\tsetp.ge.u32 p, pe, pend;\n\t@p bra.uni B1_DONE;\n\tB1_LOOP:\n\tld.shared.v4.b32 {o, x, gl, gh}, [pe];\n\tadd.u32 a, o, %33;\n\tld.shared.v2.f64 {u, v}, [a];\n\tmov.b64 g, {gl, gh};\n\tfma.rn.f64 %2, u, g, %2;\n\tfma.rn.f64 %3, v, g, %3;\n\tadd.u32 pe, pe, 16;\n\tsetp.lt.u32 p, pe, pend;\n\t@p bra.uni B1_LOOP;\n\tB1_DONE:\n\tmov.b32 pe, pend;\n\tshr.u32 t, %35, 16;\n\tmad.lo.u32 pend, t, 16, %32;\n\tsetp.ge.u32 p, pe, pend;\n\t@p bra.uni B2_DONE;\n\tB2_LOOP:\n\tld.shared.v4.b32 {o, x, gl, gh}, [pe];\n\tadd.u32 a, o, %33;\n\tld.shared.v2.f64 {u, v}, [a];\n\tmov.b64 g, {gl, gh};\n\tfma.rn.f64 %4, u, g, %4;\n\tfma.rn.f64 %5, v, g, %5;\n\tadd.u32 pe, pe, 16;\n\tsetp.lt.u32 p, pe, pend;\n\t@p bra.uni B2_LOOP;\n\tB2_DONE:\n\tmov.b32 pe, pend;\n\tand.b32 t, %36, 65535;\n\tmad.lo.u32 pend, t, 16, %32;\n\tsetp.ge.u32 p, pe, pend;\n\t@p bra.uni B3_DONE;\n\tB3_LOOP:\n\tld.shared.v4.b32 {o, x, gl, gh}, [pe];\n\tadd.u32 a, o, %33;\n\tld.shared.v2.f64 {u, v}, [a];\n\tmov.b64 g, {gl, gh};\n\tfma.rn.f64 %6, u, g, %6;\n\tfma.rn.f64 %7, v, g, %7;\n\tadd.u32 pe, pe, 16;\n\tsetp.lt.u32 p, pe, pend;\n\t@p bra.uni B3_LOOP;\n\tB3_DONE:\n\tmov.b32 pe, pend;\n\tshr.u32 t, %36, 16;\n\tmad.lo.u32 pend, t, 16, %32;\n\tsetp.ge.u32 p, pe, pend;\n\t@p bra.uni B4_DONE;\n\tB4_LOOP:\n\tld.shared.v4.b32 {o, x, gl, gh}, [pe];\n\tadd.u32 a, o, %33;\n\tld.shared.v2.f64 {u, v}, [a];\n\tmov.b64 g, {gl, gh};\n\tfma.rn.f64 %8, u, g, %8;\n\tfma.rn.f64 %9, v, g, %9;\n\tadd.u32 pe, pe, 16;\n\tsetp.lt.u32 p, pe, pend;\n\t@p bra.uni B4_LOOP;\n\tB4_DONE:\n\tmov.b32 pe, pend;\n\tand.b32 t, %37, 65535;\n\tmad.lo.u32 pend, t, 16, %32;\n\tsetp.ge.u32 p, pe, pend;\n\t@p bra.uni B5_DONE;\n\tB5_LOOP:\n\tld.shared.v4.b32 {o, x, gl, gh}, [pe];\n\tadd.u32 a, o, %33;\n\tld.shared.v2.f64 {u, v}, [a];\n\tmov.b64 g, {gl, gh};\n\tfma.rn.f64 %10, u, g, %10;\n\tfma.rn.f64 %11, v, g, %11;\n\tadd.u32 pe, pe, 16;\n\tsetp.lt.u32 p, pe, pend;\n\t@p bra.uni B5_LOOP;\n\tB5_DONE:\n\tmov.b32 pe, pend;\n\tshr.u32 t, %37, 16;\n\tmad.lo.u32 pend, t, 16, %32;\n\tsetp.ge.u32 p, pe, pend;\n\t@p bra.uni B6_DONE;\n\tB6_LOOP:\n\tld.shared.v4.b32 {o, x, gl, gh}, [pe];\n\tadd.u32 a, o, %33;\n\tld.shared.v2.f64 {u, v}, [a];\n\tmov.b64 g, {gl, gh};\n\tfma.rn.f64 %12, u, g, %12;\n\tfma.rn.f64 %13, v, g, %13;\n\tadd.u32 pe, pe, 16;\n\tsetp.lt.u32 p, pe, pend;\n\t@p bra.uni B6_LOOP;\n\tB6_DONE:\n\tmov.b32 pe, pend;\n\tand.b32 t, %38, 65535;\n\tmad.lo.u32 pend, t, 16, %32;\n\tsetp.ge.u32 p, pe, pend;\n\t@p bra.uni B7_DONE;\n\tB7_LOOP:\n\tld.shared.v4.b32 {o, x, gl, gh}, [pe];\n\tadd.u32 a, o, %33;\n\tld.shared.v2.f64 {u, v}, [a];\n\tmov.b64 g, {gl, gh};\n\tfma.rn.f64 %14, u, g, %14;\n\tfma.rn.f64 %15, v, g, %15;\n\tadd.u32 pe, pe, 16;\n\tsetp.lt.u32 p, pe, pend;\n\t@p bra.uni B7_LOOP;\n\tB7_DONE:\n\tmov.b32 pe, pend;\n\tshr.u32 t, %38, 16;\n\tmad.lo.u32 pend, t, 16, %32;\n\tsetp.ge.u32 p, pe, pend;\n\t@p bra.uni B8_DONE;\n\tB8_LOOP:\n\tld.shared.v4.b32 {o, x, gl, gh}, [pe];\n\tadd.u32 a, o, %33;\n\tld.shared.v2.f64 {u, v}, [a];\n\tmov.b64 g, {gl, gh};\n\tfma.rn.f64 %16, u, g, %16;\n\tfma.rn.f64 %17, v, g, %17;\n\tadd.u32 pe, pe, 16;\n\tsetp.lt.u32 p, pe, pend;\n\t@p bra.uni B8_LOOP;\n\tB8_DONE:\n\tmov.b32 pe, pend;\n\tand.b32 t, %39, 65535;\n\tmad.lo.u32 pend, t, 16, %32;\n\tsetp.ge.u32 p, pe, pend;\n\t@p bra.uni B9_DONE;\n\tB9_LOOP:\n\tld.shared.v4.b32 {o, x, gl, gh}, [pe];\n\tadd.u32 a, o, %33;\n\tld.shared.v2.f64 {u, v}, [a];\n\tmov.b64 g, {gl, gh};\n\tfma.rn.f64 %18, u, g, %18;\n\tfma.rn.f64 %19, v, g, %19;\n\tadd.u32 pe, pe, 16;\n\tsetp.lt.u32 p, pe, pend;\n\t@p bra.uni B9_LOOP;\n\tB9_DONE:\n\tmov.b32 pe, pend;\n\tshr.u32 t, %39, 16;\n\tmad.lo.u32 pend, t, 16, %32;\n\tsetp.ge.u32 p, pe, pend;\n\t@p bra.uni B10_DONE;\n\tB10_LOOP:\n\tld.shared.v4.b32 {o, x, gl, gh}, [pe];\n\tadd.u32 a, o, %33;\n\tld.shared.v2.f64 {u, v}, [a];\n\tmov.b64 g, {gl, gh};\n\tfma.rn.f64 %20, u, g, %20;\n\tfma.rn.f64 %21, v, g, %21;\n\tadd.u32 pe, pe, 16;\n\tsetp.lt.u32 p, pe, pend;\n\t@p bra.uni B10_LOOP;\n\tB10_DONE:\n\tmov.b32 pe, pend;\n\tand.b32 t, %40, 65535;\n\tmad.lo.u32 pend, t, 16, %32;\n\tsetp.ge.u32 p, pe, pend;\n\t@p bra.uni B11_DONE;\n\tB11_LOOP:\n\tld.shared.v4.b32 {o, x, gl, gh}, [pe];\n\tadd.u32 a, o, %33;\n\tld.shared.v2.f64 {u, v}, [a];\n\tmov.b64 g, {gl, gh};\n\tfma.rn.f64 %22, u, g, %22;\n\tfma.rn.f64 %23, v, g, %23;\n\tadd.u32 pe, pe, 16;\n\tsetp.lt.u32 p, pe, pend;\n\t@p bra.uni B11_LOOP;\n\tB11_DONE:\n\tmov.b32 pe, pend;\n\tshr.u32 t, %40, 16;\n\tmad.lo.u32 pend, t, 16, %32;\n\tsetp.ge.u32 p, pe, pend;\n\t@p bra.uni B12_DONE;\n\tB12_LOOP:\n\tld.shared.v4.b32 {o, x, gl, gh}, [pe];\n\tadd.u32 a, o, %33;\n\tld.shared.v2.f64 {u, v}, [a];\n\tmov.b64 g, {gl, gh};\n\tfma.rn.f64 %24, u, g, %24;\n\tfma.rn.f64 %25, v, g, %25;\n\tadd.u32 pe, pe, 16;\n\tsetp.lt.u32 p, pe, pend;\n\t@p bra.uni B12_LOOP;\n\tB12_DONE:\n\tmov.b32 pe, pend;\n\tand.b32 t, %41, 65535;\n\tmad.lo.u32 pend, t, 16, %32;\n\tsetp.ge.u32 p, pe, pend;\n\t@p bra.uni B13_DONE;\n\tB13_LOOP:\n\tld.shared.v4.b32 {o, x, gl, gh}, [pe];\n\tadd.u32 a, o, %33;\n\tld.shared.v2.f64 {u, v}, [a];\n\tmov.b64 g, {gl, gh};\n\tfma.rn.f64 %26, u, g, %26;\n\tfma.rn.f64 %27, v, g, %27;\n\tadd.u32 pe, pe, 16;\n\tsetp.lt.u32 p, pe, pend;\n\t@p bra.uni B13_LOOP;\n\tB13_DONE:\n\tmov.b32 pe, pend;\n\tshr.u32 t, %41, 16;\n\tmad.lo.u32 pend, t, 16, %32;\n\tsetp.ge.u32 p, pe, pend;\n\t@p bra.uni B14_DONE;\n\tB14_LOOP:\n\tld.shared.v4.b32 {o, x, gl, gh}, [pe];\n\tadd.u32 a, o, %33;\n\tld.shared.v2.f64 {u, v}, [a];\n\tmov.b64 g, {gl, gh};\n\tfma.rn.f64 %28, u, g, %28;\n\tfma.rn.f64 %29, v, g, %29;\n\tadd.u32 pe, pe, 16;\n\tsetp.lt.u32 p, pe, pend;\n\t@p bra.uni B14_LOOP;\n\tB14_DONE:\n\tmov.b32 pe, pend;\n\tand.b32 t, %42, 65535;\n\tmad.lo.u32 pend, t, 16, %32;\n\tsetp.ge.u32 p, pe, pend;\n\t@p bra.uni B15_DONE;\n\tB15_LOOP:\n\tld.shared.v4.b32 {o, x, gl, gh}, [pe];\n\tadd.u32 a, o, %33;\n\tld.shared.v2.f64 {u, v}, [a];\n\tmov.b64 g, {gl, gh};\n\tfma.rn.f64 %30, u, g, %30;\n\tfma.rn.f64 %31, v, g, %31;\n\tadd.u32 pe, pe, 16;\n\tsetp.lt.u32 p, pe, pend;\n\t@p bra.uni B15_LOOP;\n\tB15_DONE:\n\tmov.b32 pe, pend;\n\t}"
+                 : "+d"(acc[0][0]), "+d"(acc[1][0]), "+d"(acc[0][1]), "+d"(acc[1][1]), "+d"(acc[0][2]), "+d"(acc[1][2]), "+d"(acc[0][3]), "+d"(acc[1][3]), "+d"(acc[0][4]), "+d"(acc[1][4]), "+d"(acc[0][5]), "+d"(acc[1][5]), "+d"(acc[0][6]), "+d"(acc[1][6]), "+d"(acc[0][7]), "+d"(acc[1][7]), "+d"(acc[0][8]), "+d"(acc[1][8]), "+d"(acc[0][9]), "+d"(acc[1][9]), "+d"(acc[0][10]), "+d"(acc[1][10]), "+d"(acc[0][11]), "+d"(acc[1][11]), "+d"(acc[0][12]), "+d"(acc[1][12]), "+d"(acc[0][13]), "+d"(acc[1][13]), "+d"(acc[0][14]), "+d"(acc[1][14]), "+d"(acc[0][15]), "+d"(acc[1][15])
+                 : "r"(sen), "r"(sx), "r"(bw[0]), "r"(bw[1]), "r"(bw[2]), "r"(bw[3]), "r"(bw[4]), "r"(bw[5]), "r"(bw[6]), "r"(bw[7]), "r"(bw[8])
+                 : "memory");
+}
+
+// one warp, one chunk, all 8 buckets, RPT = 4 (S tiles)
+__device__ __forceinline__ void chunk_s_4x8(double (&acc)[4][8], uint32_t sen, uint32_t sx, const uint32_t (&bw)[5]) {
+    asm volatile("{\n\t.reg .pred p;\n\t.reg .b32 o, x, gl, gh, a, t, pe, pend;\n\t.reg .f64 u, v, w, y, g;\n\tand.b32 t, %34, 65535;\n\tmad.lo.u32 pe, t, 16, %32;\n\tshr.u32 t, %34, 16;\n\tmad.lo.u32 pend, t, 16, %32;\n\tsetp.ge.u32 p, pe, pend;\n\t@p bra.uni B0_DONE;\n\tB0_LOOP:\n\tld.shared.v4.b32 {o, x, gl, gh}, [pe];\n\tadd.u32 a, o, %33;\n\tld.shared.v2.f64 {u, v}, [a];\n\tld.shared.v2.f64 {w, y}, [a+512];\n\tmov.b64 g, {gl, gh};\n\tfma.rn.f64 %0, u, g, %0;\n\tfma.rn.f64 %1, v, g, %1;\n\tfma.rn.f64 %2, w, g, %2;\n\tfma.rn.f64 %3, y, g, %3;\n\tadd.u32 pe, pe, 16;\n\tsetp.lt.u32 p, pe, pend;\n\t@p bra.uni B0_LOOP;\n\tB0_DONE:\n\tmov.b32 pe, pend;\n\tand.b32 t, %35, 65535;\n\tmad.lo.u32 pend, t, 16, %32;\n\tsetp.ge.u32 p, pe, pend;\n\t@p bra.uni B1_DONE;\n\tB1_LOOP:\n\tld.shared.v4.b32 {o, x, gl, gh}, [pe];\n\tadd.u32 a, o, %33;\n\tld.shared.v2.f64 {u, v}, [a];\n\tld.shared.v2.f64 {w, y}, [a+512];\n\tmov.b64 g, {gl, gh};\n\tfma.rn.f64 %4, u, g, %4;\n\tfma.rn.f64 %5, v, g, %5;\n\tfma.rn.f64 %6, w, g, %6;\n\tfma.rn.f64 %7, y, g, %7;\n\tadd.u32 pe, pe, 16;\n\tsetp.lt.u32 p, pe, pend;\n\t@p bra.uni B1_LOOP;\n\tB1_DONE:\n\tmov.b32 pe, pend;\n\tshr.u32 t, %35, 16;\n\tmad.lo.u32 pend, t, 16, %32;\n\tsetp.ge.u32 p, pe, pend;\n\t@p bra.uni B2_DONE;\n\tB2_LOOP:\n\tld.shared.v4.b32 {o, x, gl, gh}, [pe];\n\tadd.u32 a, o, %33;\n\tld.shared.v2.f64 {u, v}, [a];\n\tld.shared.v2.f64 {w, y}, [a+512];\n\tmov.b64 g, {gl, gh};\n\tfma.rn.f64 %8, u, g, %8;\n\tfma.rn.f64 %9, v, g, %9;\n\tfma.rn.f64 %10, w, g, %10;\n\tfma.rn.f64 %11, y, g, %11;\n\tadd.u32 pe, pe, 16;\n\tsetp.lt.u32 p, pe, pend;\n\t@p bra.uni B2_LOOP;\n\tB2_DONE:\n\tmov.b32 pe, pend;\n\tand.b32 t, %36, 65535;\n\tmad.lo.u32 pend, t, 16, %32;\n\tsetp.ge.u32 p, pe, pend;\n\t@p bra.uni B3_DONE;\n\tB3_LOOP:\n\tld.shared.v4.b32 {o, x, gl, gh}, [pe];\n\tadd.u32 a, o, %33;\n\tld.shared.v2.f64 {u, v}, [a];\n\tld.shared.v2.f64 {w, y}, [a+512];\n\tmov.b64 g, {gl, gh};\n\tfma.rn.f64 %12, u, g, %12;\n\tfma.rn.f64 %13, v, g, %13;\n\tfma.rn.f64 %14, w, g, %14;\n\tfma.rn.f64 %15, y, g, %15;\n\tadd.u32 pe, pe, 16;\n\tsetp.lt.u32 p, pe, pend;\n\t@p bra.uni B3_LOOP;\n\tB3_DONE:\n\tmov.b32 pe, pend;\n\tshr.u32 t, %36, 16;\n\tmad.lo.u32 pend, t, 16, %32;\n\tsetp.ge.u32 p, pe, pend;\n\t@p bra.uni B4_DONE;\n\tB4_LOOP:\n\tld.shared.v4.b32 {o, x, gl, gh}, [pe];\n\tadd.u32 a, o, %33;\n\tld.shared.v2.f64 {u, v}, [a];\n\tld.shared.v2.f64 {w, y}, [a+512];\n\tmov.b64 g, {gl, gh};\n\tfma.rn.f64 %16, u, g, %16;\n\tfma.rn.f64 %17, v, g, %17;\n\tfma.rn.f64 %18, w, g, %18;\n\tfma.rn.f64 %19, y, g, %19;\n\tadd.u32 pe, pe, 16;\n\tsetp.lt.u32 p, pe, pend;\n\t@p bra.uni B4_LOOP;\n\tB4_DONE:\n\tmov.b32 pe, pend;\n\tand.b32 t, %37, 65535;\n\tmad.lo.u32 pend, t, 16, %32;\n\tsetp.ge.u32 p, pe, pend;\n\t@p bra.uni B5_DONE;\n\tB5_LOOP:\n\tld.shared.v4.b32 {o, x, gl, gh}, [pe];\n\tadd.u32 a, o, %33;\n\tld.shared.v2.f64 {u, v}, [a];\n\tld.shared.v2.f64 {w, y}, [a+512];\n\tmov.b64 g, {gl, gh};\n\tfma.rn.f64 %20, u, g, %20;\n\tfma.rn.f64 %21, v, g, %21;\n\tfma.rn.f64 %22, w, g, %22;\n\tfma.rn.f64 %23, y, g, %23;\n\tadd.u32 pe, pe, 16;\n\tsetp.lt.u32 p, pe, pend;\n\t@p bra.uni B5_LOOP;\n\tB5_DONE:\n\tmov.b32 pe, pend;\n\tshr.u32 t, %37, 16;\n\tmad.lo.u32 pend, t, 16, %32;\n\tsetp.ge.u32 p, pe, pend;\n\t@p bra.uni B6_DONE;\n\tB6_LOOP:\n\tld.shared.v4.b32 {o, x, gl, gh}, [pe];\n\tadd.u32 a, o, %33;\n\tld.shared.v2.f64 {u, v}, [a];\n\tld.shared.v2.f64 {w, y}, [a+512];\n\tmov.b64 g, {gl, gh};\n\tfma.rn.f64 %24, u, g, %24;\n\tfma.rn.f64 %25, v, g, %25;\n\tfma.rn.f64 %26, w, g, %26;\n\tfma.rn.f64 %27, y, g, %27;\n\tadd.u32 pe, pe, 16;\n\tsetp.lt.u32 p, pe, pend;\n\t@p bra.uni B6_LOOP;\n\tB6_DONE:\n\tmov.b32 pe, pend;\n\tand.b32 t, %38, 65535;\n\tmad.lo.u32 pend, t, 16, %32;\n\tsetp.ge.u32 p, pe, pend;\n\t@p bra.uni B7_DONE;\n\tB7_LOOP:\n\tld.shared.v4.b32 {o, x, gl, gh}, [pe];\n\tadd.u32 a, o, %33;\n\tld.shared.v2.f64 {u, v}, [a];\n\tld.shared.v2.f64 {w, y}, [a+512];\n\tmov.b64 g, {gl, gh};\n\tfma.rn.f64 %28, u, g, %28;\n\tfma.rn.f64 %29, v, g, %29;\n\tfma.rn.f64 %30, w, g, %30;\n\tfma.rn.f64 %31, y, g, %31;\n\tadd.u32 pe, pe, 16;\n\tsetp.lt.u32 p, pe, pend;\n\t@p bra.uni B7_LOOP;\n\tB7_DONE:\n\tmov.b32 pe, pend;\n\t}"
+                 : "+d"(acc[0][0]), "+d"(acc[1][0]), "+d"(acc[2][0]), "+d"(acc[3][0]), "+d"(acc[0][1]), "+d"(acc[1][1]), "+d"(acc[2][1]), "+d"(acc[3][1]), "+d"(acc[0][2]), "+d"(acc[1][2]), "+d"(acc[2][2]), "+d"(acc[3][2]), "+d"(acc[0][3]), "+d"(acc[1][3]), "+d"(acc[2][3]), "+d"(acc[3][3]), "+d"(acc[0][4]), "+d"(acc[1][4]), "+d"(acc[2][4]), "+d"(acc[3][4]), "+d"(acc[0][5]), "+d"(acc[1][5]), "+d"(acc[2][5]), "+d"(acc[3][5]), "+d"(acc[0][6]), "+d"(acc[1][6]), "+d"(acc[2][6]), "+d"(acc[3][6]), "+d"(acc[0][7]), "+d"(acc[1][7]), "+d"(acc[2][7]), "+d"(acc[3][7])
+                 : "r"(sen), "r"(sx), "r"(bw[0]), "r"(bw[1]), "r"(bw[2]), "r"(bw[3]), "r"(bw[4])
+                 : "memory");
+}
+
 __device__ __forceinline__ uint4 lds_u4(uint32_t addr) {
     uint4 w;
     asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];"
@@ -258,7 +309,7 @@ struct ApplyArgs {
 // All NW warps own buckets (NW*DB per CTA slab) and share the producer work:
 // warp 0 / lane 0 issues TMA + bulk copies (mode 0); in modes 1/2 every lane
 // issues its share of 8-byte cp.async for the chunk STAGES-1 ahead.
-template <int RPT, int DB, int NW, bool TRANS, bool BATCH, bool PROD>
+template <int RPT, int DB, int NW, bool TRANS, bool BATCH, bool PROD, bool WHOLE = true>
 __global__ void __launch_bounds__((NW + (PROD ? 1 : 0)) * 32, 1)
     sjlt_apply_kernel(const ApplyArgs p, const __grid_constant__ CUtensorMap tmap) {
     constexpr int TM = 32 * RPT;
@@ -423,7 +474,14 @@ __global__ void __launch_bounds__((NW + (PROD ? 1 : 0)) * 32, 1)
         auto bound = [&](int jj) -> uint32_t {
             return (jj & 1) ? (bw[jj >> 1] >> 16) : (bw[jj >> 1] & 0xffffu);
         };
-        if (!BATCH) {
+        if (!BATCH && !TRANS && WHOLE) {
+            if constexpr (RPT == 2 && DB == 8) chunk_s_2x8(acc, sen, sx, bw);
+            else if constexpr (RPT == 2 && DB == 4) chunk_s_2x4(acc, sen, sx, bw);
+            else if constexpr (RPT == 2 && DB == 16) chunk_s_2x16(acc, sen, sx, bw);
+            else if constexpr (RPT == 4 && DB == 2) chunk_s_4x2(acc, sen, sx, bw);
+            else if constexpr (RPT == 4 && DB == 4) chunk_s_4x4(acc, sen, sx, bw);
+            else if constexpr (RPT == 4 && DB == 8) chunk_s_4x8(acc, sen, sx, bw);
+        } else if (!BATCH) {
             // per-bucket loops; the first entry of bucket jj+1 is loaded while
             // bucket jj runs (index <= estride: the null entry keeps it in range)
             uint32_t pe = sen + 16u * bound(0);
@@ -624,11 +682,14 @@ static int launch(ApplyArgs a, const Geom &g, cudaStream_t st) {
     if (const char *env = getenv("HSK_SJLT_PROD")) prod = env[0] == '1';
     prod = prod && a.mode == 0;
     if (prod) batch = false;
+    bool whole = true;
+    if (const char *env = getenv("HSK_SJLT_WHOLE")) whole = env[0] == '1';
     auto kern = a.trans ? (batch ? sjlt_apply_kernel<RPT, DB, NW, true, true, false>
                                  : sjlt_apply_kernel<RPT, DB, NW, true, false, false>)
                         : (prod ? sjlt_apply_kernel<RPT, DB, NW, false, false, true>
                                 : batch ? sjlt_apply_kernel<RPT, DB, NW, false, true, false>
-                                        : sjlt_apply_kernel<RPT, DB, NW, false, false, false>);
+                                        : whole ? sjlt_apply_kernel<RPT, DB, NW, false, false, false, true>
+                                                : sjlt_apply_kernel<RPT, DB, NW, false, false, false, false>);
     const int nthreads = (NW + (prod ? 1 : 0)) * 32;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e != cudaSuccess) return cuda_status(e, "sjlt: set smem attribute");
