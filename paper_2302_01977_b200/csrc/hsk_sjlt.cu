@@ -42,7 +42,7 @@ constexpr int kPlanSlab = 512;          // bucket-offset rows padded for slabs |
 constexpr int64_t kMaxD = (1 << 19);    // bucket index fits 19 bits of the sort key
 
 struct Geom {
-    int rpt;           // rows per lane: 4 for d <= 64, else 2
+    int rpt;           // rows per lane: 4 for d <= 64, 2 for d <= 256, else 1
     int tm;            // rows per CTA = 32 * rpt
     int pitch;         // tile pitch (doubles) = tm: TMA writes densely; the S'
                        // producer orders its transposing stores conflict-free
@@ -61,7 +61,7 @@ static inline int64_t roundup(int64_t x, int64_t m) { return (x + m - 1) / m * m
 // leaves room for >= 3 stages in shared memory, capped at 128.
 static inline int tk_for(int alpha, int tm) {
     int tk = 128;
-    if (const char *env = getenv("HSK_SJLT_TK")) tk = atoi(env);  // tuning override (power of 2)
+    if (const char *env = getenv("HSK_SJLT_TK")) return atoi(env);  // tuning override (power of 2)
     while (tk > 1 && (tk * alpha > kMaxChunkEntries || tk * (tm * 8 + 16 * alpha) > 72 * 1024))
         tk >>= 1;
     return tk;
@@ -69,7 +69,7 @@ static inline int tk_for(int alpha, int tm) {
 
 static Geom geom(int64_t n, int d, int alpha) {
     Geom g;
-    g.rpt = d <= 64 ? 4 : 2;
+    g.rpt = d <= 64 ? 4 : d <= 256 ? 2 : 1;
     g.tm = 32 * g.rpt;
     g.pitch = g.tm;
     g.tk = tk_for(alpha, g.tm);
@@ -279,6 +279,44 @@ __device__ __forceinline__ void chunk_s_4x8(double (&acc)[4][8], uint32_t sen, u
                  : "memory");
 }
 
+// RPT = 1 variants (32-row tiles): lane l owns row l.
+__device__ __forceinline__ void chunk_s_1x16(double (&acc)[1][16], uint32_t sen, uint32_t sx, const uint32_t (&bw)[9]) {
+    asm volatile("{\n\t.reg .pred p;\n\t.reg .b32 o, x, gl, gh, a, t, pe, pend;\n\t.reg .f64 u, g;\n\tand.b32 t, %18, 65535;\n\tmad.lo.u32 pe, t, 16, %16;\n\tshr.u32 t, %18, 16;\n\tmad.lo.u32 pend, t, 16, %16;\n\tsetp.ge.u32 p, pe, pend;\n\t@p bra.uni B0_DONE;\n\tB0_LOOP:\n\tld.shared.v4.b32 {o, x, gl, gh}, [pe];\n\tadd.u32 a, o, %17;\n\tld.shared.f64 u, [a];\n\tmov.b64 g, {gl, gh};\n\tfma.rn.f64 %0, u, g, %0;\n\tadd.u32 pe, pe, 16;\n\tsetp.lt.u32 p, pe, pend;\n\t@p bra.uni B0_LOOP;\n\tB0_DONE:\n\tmov.b32 pe, pend;\n\tand.b32 t, %19, 65535;\n\tmad.lo.u32 pend, t, 16, %16;\n\tsetp.ge.u32 p, pe, pend;\n\t@p bra.uni B1_DONE;\n\tB1_LOOP:\n\tld.shared.v4.b32 {o, x, gl, gh}, [pe];\n\tadd.u32 a, o, %17;\n\tld.shared.f64 u, [a];\n\tmov.b64 g, {gl, gh};\n\tfma.rn.f64 %1, u, g, %1;\n\tadd.u32 pe, pe, 16;\n\tsetp.lt.u32 p, pe, pend;\n\t@p bra.uni B1_LOOP;\n\tB1_DONE:\n\tmov.b32 pe, pend;\n\tshr.u32 t, %19, 16;\n\tmad.lo.u32 pend, t, 16, %16;\n\tsetp.ge.u32 p, pe, pend;\n\t@p bra.uni B2_DONE;\n\tB2_LOOP:\n\tld.shared.v4.b32 {o, x, gl, gh}, [pe];\n\tadd.u32 a, o, %17;\n\tld.shared.f64 u, [a];\n\tmov.b64 g, {gl, gh};\n\tfma.rn.f64 %2, u, g, %2;\n\tadd.u32 pe, pe, 16;\n\tsetp.lt.u32 p, pe, pend;\n\t@p bra.uni B2_LOOP;\n\tB2_DONE:\n\tmov.b32 pe, pend;\n\tand.b32 t, %20, 65535;\n\tmad.lo.u32 pend, t, 16, %16;\n\tsetp.ge.u32 p, pe, pend;\n\t@p bra.uni B3_DONE;\n\tB3_LOOP:\n\tld.shared.v4.b32 {o, x, gl, gh}, [pe];\n\tadd.u32 a, o, %17;\n\tld.shared.f64 u, [a];\n\tmov.b64 g, {gl, gh};\n\tfma.rn.f64 %3, u, g, %3;\n\tadd.u32 pe, pe, 16;\n\tsetp.lt.u32 p, pe, pend;\n\t@p bra.uni B3_LOOP;\n\tB3_DONE:\n\tmov.b32 pe, pend;\n\tshr.u32 t, %20, 16;\n\tmad.lo.u32 pend, t, 16, %16;\n\tsetp.ge.u32 p, pe, pend;\n\t@p bra.uni B4_DONE;\n\tB4_LOOP:\n\tld.shared.v4.b32 {o, x, gl, gh}, [pe];\n\tadd.u32 a, o, %17;\n\tld.shared.f64 u, [a];\n\tmov.b64 g, {gl, gh};\n\tfma.rn.f64 %4, u, g, %4;\n\tadd.u32 pe, pe, 16;\n\tsetp.lt.u32 p, pe, pend;\n\t@p bra.uni B4_LOOP;\n\tB4_DONE:\n\tmov.b32 pe, pend;\n\tand.b32 t, %21, 65535;\n\tmad.lo.u32 pend, t, 16, %16;\n\tsetp.ge.u32 p, pe, pend;\n\t@p bra.uni B5_DONE;\n\tB5_LOOP:\n\tld.shared.v4.b32 {o, x, gl, gh}, [pe];\n\tadd.u32 a, o, %17;\n\tld.shared.f64 u, [a];\n\tmov.b64 g, {gl, gh};\n\tfma.rn.f64 %5, u, g, %5;\n\tadd.u32 pe, pe, 16;\n\tsetp.lt.u32 p, pe, pend;\n\t@p bra.uni B5_LOOP;\n\tB5_DONE:\n\tmov.b32 pe, pend;\n\tshr.u32 t, %21, 16;\n\tmad.lo.u32 pend, t, 16, %16;\n\tsetp.ge.u32 p, pe, pend;\n\t@p bra.uni B6_DONE;\n\tB6_LOOP:\n\tld.shared.v4.b32 {o, x, gl, gh}, [pe];\n\tadd.u32 a, o, %17;\n\tld.shared.f64 u, [a];\n\tmov.b64 g, {gl, gh};\n\tfma.rn.f64 %6, u, g, %6;\n\tadd.u32 pe, pe, 16;\n\tsetp.lt.u32 p, pe, pend;\n\t@p bra.uni B6_LOOP;\n\tB6_DONE:\n\tmov.b32 pe, pend;\n\tand.b32 t, %22, 65535;\n\tmad.lo.u32 pend, t, 16, %16;\n\tsetp.ge.u32 p, pe, pend;\n\t@p bra.uni B7_DONE;\n\tB7_LOOP:\n\tld.shared.v4.b32 {o, x, gl, gh}, [pe];\n\tadd.u32 a, o, %17;\n\tld.shared.f64 u, [a];\n\tmov.b64 g, {gl, gh};\n\tfma.rn.f64 %7, u, g, %7;\n\tadd.u32 pe, pe, 16;\n\tsetp.lt.u32 p, pe, pend;\n\t@p bra.uni B7_LOOP;\n\tB7_DONE:\n\tmov.b32 pe, pend;\n\tshr.u32 t, %22, 16;\n\tmad.lo.u32 pend, t, 16, %16;\n\tsetp.ge.u32 p, pe, pend;\n\t@p bra.uni B8_DONE;\n\tB8_LOOP:\n\tld.shared.v4.b32 {o, x, gl, gh}, [pe];\n\tadd.u32 a, o, %17;\n\tld.shared.f64 u, [a];\n\tmov.b64 g, {gl, gh};\n\tfma.rn.f64 %8, u, g, %8;\n\tadd.u32 pe, pe, 16;\n\tsetp.lt.u32 p, pe, pend;\n\t@p bra.uni B8_LOOP;\n\tB8_DONE:\n\tmov.b32 pe, pend;\n\tand.b32 t, %23, 65535;\n\tmad.lo.u32 pend, t, 16, %16;\n\tsetp.ge.u32 p, pe, pend;\n\t@p bra.uni B9_DONE;\n\tB9_LOOP:\n\tld.shared.v4.b32 {o, x, gl, gh}, [pe];\n\tadd.u32 a, o, %17;\n\tld.shared.f64 u, [a];\n\tmov.b64 g, {gl, gh};\n\tfma.rn.f64 %9, u, g, %9;\n\tadd.u32 pe, pe, 16;\n\tsetp.lt.u32 p, pe, pend;\n\t@p bra.uni B9_LOOP;\n\tB9_DONE:\n\tmov.b32 pe, pend;\n\tshr.u32 t, %23, 16;\n\tmad.lo.u32 pend, t, 16, %16;\n\tsetp.ge.u32 p, pe, pend;\n\t@p bra.uni B10_DONE;\n\tB10_LOOP:\n\tld.shared.v4.b32 {o, x, gl, gh}, [pe];\n\tadd.u32 a, o, %17;\n\tld.shared.f64 u, [a];\n\tmov.b64 g, {gl, gh};\n\tfma.rn.f64 %10, u, g, %10;\n\tadd.u32 pe, pe, 16;\n\tsetp.lt.u32 p, pe, pend;\n\t@p bra.uni B10_LOOP;\n\tB10_DONE:\n\tmov.b32 pe, pend;\n\tand.b32 t, %24, 65535;\n\tmad.lo.u32 pend, t, 16, %16;\n\tsetp.ge.u32 p, pe, pend;\n\t@p bra.uni B11_DONE;\n\tB11_LOOP:\n\tld.shared.v4.b32 {o, x, gl, gh}, [pe];\n\tadd.u32 a, o, %17;\n\tld.shared.f64 u, [a];\n\tmov.b64 g, {gl, gh};\n\tfma.rn.f64 %11, u, g, %11;\n\tadd.u32 pe, pe, 16;\n\tsetp.lt.u32 p, pe, pend;\n\t@p bra.uni B11_LOOP;\n\tB11_DONE:\n\tmov.b32 pe, pend;\n\tshr.u32 t, %24, 16;\n\tmad.lo.u32 pend, t, 16, %16;\n\tsetp.ge.u32 p, pe, pend;\n\t@p bra.uni B12_DONE;\n\tB12_LOOP:\n\tld.shared.v4.b32 {o, x, gl, gh}, [pe];\n\tadd.u32 a, o, %17;\n\tld.shared.f64 u, [a];\n\tmov.b64 g, {gl, gh};\n\tfma.rn.f64 %12, u, g, %12;\n\tadd.u32 pe, pe, 16;\n\tsetp.lt.u32 p, pe, pend;\n\t@p bra.uni B12_LOOP;\n\tB12_DONE:\n\tmov.b32 pe, pend;\n\tand.b32 t, %25, 65535;\n\tmad.lo.u32 pend, t, 16, %16;\n\tsetp.ge.u32 p, pe, pend;\n\t@p bra.uni B13_DONE;\n\tB13_LOOP:\n\tld.shared.v4.b32 {o, x, gl, gh}, [pe];\n\tadd.u32 a, o, %17;\n\tld.shared.f64 u, [a];\n\tmov.b64 g, {gl, gh};\n\tfma.rn.f64 %13, u, g, %13;\n\tadd.u32 pe, pe, 16;\n\tsetp.lt.u32 p, pe, pend;\n\t@p bra.uni B13_LOOP;\n\tB13_DONE:\n\tmov.b32 pe, pend;\n\tshr.u32 t, %25, 16;\n\tmad.lo.u32 pend, t, 16, %16;\n\tsetp.ge.u32 p, pe, pend;\n\t@p bra.uni B14_DONE;\n\tB14_LOOP:\n\tld.shared.v4.b32 {o, x, gl, gh}, [pe];\n\tadd.u32 a, o, %17;\n\tld.shared.f64 u, [a];\n\tmov.b64 g, {gl, gh};\n\tfma.rn.f64 %14, u, g, %14;\n\tadd.u32 pe, pe, 16;\n\tsetp.lt.u32 p, pe, pend;\n\t@p bra.uni B14_LOOP;\n\tB14_DONE:\n\tmov.b32 pe, pend;\n\tand.b32 t, %26, 65535;\n\tmad.lo.u32 pend, t, 16, %16;\n\tsetp.ge.u32 p, pe, pend;\n\t@p bra.uni B15_DONE;\n\tB15_LOOP:\n\tld.shared.v4.b32 {o, x, gl, gh}, [pe];\n\tadd.u32 a, o, %17;\n\tld.shared.f64 u, [a];\n\tmov.b64 g, {gl, gh};\n\tfma.rn.f64 %15, u, g, %15;\n\tadd.u32 pe, pe, 16;\n\tsetp.lt.u32 p, pe, pend;\n\t@p bra.uni B15_LOOP;\n\tB15_DONE:\n\tmov.b32 pe, pend;\n\t}"
+                 : "+d"(acc[0][0]), "+d"(acc[0][1]), "+d"(acc[0][2]), "+d"(acc[0][3]), "+d"(acc[0][4]), "+d"(acc[0][5]), "+d"(acc[0][6]), "+d"(acc[0][7]), "+d"(acc[0][8]), "+d"(acc[0][9]), "+d"(acc[0][10]), "+d"(acc[0][11]), "+d"(acc[0][12]), "+d"(acc[0][13]), "+d"(acc[0][14]), "+d"(acc[0][15])
+                 : "r"(sen), "r"(sx), "r"(bw[0]), "r"(bw[1]), "r"(bw[2]), "r"(bw[3]), "r"(bw[4]), "r"(bw[5]), "r"(bw[6]), "r"(bw[7]), "r"(bw[8])
+                 : "memory");
+}
+__device__ __forceinline__ void chunk_s_1x32(double (&acc)[1][32], uint32_t sen, uint32_t sx, const uint32_t (&bw)[17]) {
+    asm volatile("{\n\t.reg .pred p;\n\t.reg .b32 o, x, gl, gh, a, t, pe, pend;\n\t.reg .f64 u, g;\n\tand.b32 t, %34, 65535;\n\tmad.lo.u32 pe, t, 16, %32;\n\tshr.u32 t, %34, 16;\n\tmad.lo.u32 pend, t, 16, %32;\n\tsetp.ge.u32 p, pe, pend;\n\t@p bra.uni B0_DONE;\n\tB0_LOOP:\n\tld.shared.v4.b32 {o, x, gl, gh}, [pe];\n\tadd.u32 a, o, %33;\n\tld.shared.f64 u, [a];\n\tmov.b64 g, {gl, gh};\n\tfma.rn.f64 %0, u, g, %0;\n\tadd.u32 pe, pe, 16;\n\tsetp.lt.u32 p, pe, pend;\n\t@p bra.uni B0_LOOP;\n\tB0_DONE:\n\tmov.b32 pe, pend;\n\tand.b32 t, %35, 65535;\n\tmad.lo.u32 pend, t, 16, %32;\n\tsetp.ge.u32 p, pe, pend;\n\t@p bra.uni B1_DONE;\n\tB1_LOOP:\n\tld.shared.v4.b32 {o, x, gl, gh}, [pe];\n\tadd.u32 a, o, %33;\n\tld.shared.f64 u, [a];\n\tmov.b64 g, {gl, gh};\n\tfma.rn.f64 %1, u, g, %1;\n\tadd.u32 pe, pe, 16;\n\tsetp.lt.u32 p, pe, pend;\n\t@p bra.uni B1_LOOP;\n\tB1_DONE:\n\tmov.b32 pe, pend;\n\tshr.u32 t, %35, 16;\n\tmad.lo.u32 pend, t, 16, %32;\n\tsetp.ge.u32 p, pe, pend;\n\t@p bra.uni B2_DONE;\n\tB2_LOOP:\n\tld.shared.v4.b32 {o, x, gl, gh}, [pe];\n\tadd.u32 a, o, %33;\n\tld.shared.f64 u, [a];\n\tmov.b64 g, {gl, gh};\n\tfma.rn.f64 %2, u, g, %2;\n\tadd.u32 pe, pe, 16;\n\tsetp.lt.u32 p, pe, pend;\n\t@p bra.uni B2_LOOP;\n\tB2_DONE:\n\tmov.b32 pe, pend;\n\tand.b32 t, %36, 65535;\n\tmad.lo.u32 pend, t, 16, %32;\n\tsetp.ge.u32 p, pe, pend;\n\t@p bra.uni B3_DONE;\n\tB3_LOOP:\n\tld.shared.v4.b32 {o, x, gl, gh}, [pe];\n\tadd.u32 a, o, %33;\n\tld.shared.f64 u, [a];\n\tmov.b64 g, {gl, gh};\n\tfma.rn.f64 %3, u, g, %3;\n\tadd.u32 pe, pe, 16;\n\tsetp.lt.u32 p, pe, pend;\n\t@p bra.uni B3_LOOP;\n\tB3_DONE:\n\tmov.b32 pe, pend;\n\tshr.u32 t, %36, 16;\n\tmad.lo.u32 pend, t, 16, %32;\n\tsetp.ge.u32 p, pe, pend;\n\t@p bra.uni B4_DONE;\n\tB4_LOOP:\n\tld.shared.v4.b32 {o, x, gl, gh}, [pe];\n\tadd.u32 a, o, %33;\n\tld.shared.f64 u, [a];\n\tmov.b64 g, {gl, gh};\n\tfma.rn.f64 %4, u, g, %4;\n\tadd.u32 pe, pe, 16;\n\tsetp.lt.u32 p, pe, pend;\n\t@p bra.uni B4_LOOP;\n\tB4_DONE:\n\tmov.b32 pe, pend;\n\tand.b32 t, %37, 65535;\n\tmad.lo.u32 pend, t, 16, %32;\n\tsetp.ge.u32 p, pe, pend;\n\t@p bra.uni B5_DONE;\n\tB5_LOOP:\n\tld.shared.v4.b32 {o, x, gl, gh}, [pe];\n\tadd.u32 a, o, %33;\n\tld.shared.f64 u, [a];\n\tmov.b64 g, {gl, gh};\n\tfma.rn.f64 %5, u, g, %5;\n\tadd.u32 pe, pe, 16;\n\tsetp.lt.u32 p, pe, pend;\n\t@p bra.uni B5_LOOP;\n\tB5_DONE:\n\tmov.b32 pe, pend;\n\tshr.u32 t, %37, 16;\n\tmad.lo.u32 pend, t, 16, %32;\n\tsetp.ge.u32 p, pe, pend;\n\t@p bra.uni B6_DONE;\n\tB6_LOOP:\n\tld.shared.v4.b32 {o, x, gl, gh}, [pe];\n\tadd.u32 a, o, %33;\n\tld.shared.f64 u, [a];\n\tmov.b64 g, {gl, gh};\n\tfma.rn.f64 %6, u, g, %6;\n\tadd.u32 pe, pe, 16;\n\tsetp.lt.u32 p, pe, pend;\n\t@p bra.uni B6_LOOP;\n\tB6_DONE:\n\tmov.b32 pe, pend;\n\tand.b32 t, %38, 65535;\n\tmad.lo.u32 pend, t, 16, %32;\n\tsetp.ge.u32 p, pe, pend;\n\t@p bra.uni B7_DONE;\n\tB7_LOOP:\n\tld.shared.v4.b32 {o, x, gl, gh}, [pe];\n\tadd.u32 a, o, %33;\n\tld.shared.f64 u, [a];\n\tmov.b64 g, {gl, gh};\n\tfma.rn.f64 %7, u, g, %7;\n\tadd.u32 pe, pe, 16;\n\tsetp.lt.u32 p, pe, pend;\n\t@p bra.uni B7_LOOP;\n\tB7_DONE:\n\tmov.b32 pe, pend;\n\tshr.u32 t, %38, 16;\n\tmad.lo.u32 pend, t, 16, %32;\n\tsetp.ge.u32 p, pe, pend;\n\t@p bra.uni B8_DONE;\n\tB8_LOOP:\n\tld.shared.v4.b32 {o, x, gl, gh}, [pe];\n\tadd.u32 a, o, %33;\n\tld.shared.f64 u, [a];\n\tmov.b64 g, {gl, gh};\n\tfma.rn.f64 %8, u, g, %8;\n\tadd.u32 pe, pe, 16;\n\tsetp.lt.u32 p, pe, pend;\n\t@p bra.uni B8_LOOP;\n\tB8_DONE:\n\tmov.b32 pe, pend;\n\tand.b32 t, %39, 65535;\n\tmad.lo.u32 pend, t, 16, %32;\n\tsetp.ge.u32 p, pe, pend;\n\t@p bra.uni B9_DONE;\n\tB9_LOOP:\n\tld.shared.v4.b32 {o, x, gl, gh}, [pe];\n\tadd.u32 a, o, %33;\n\tld.shared.f64 u, [a];\n\tmov.b64 g, {gl, gh};\n\tfma.rn.f64 %9, u, g, %9;\n\tadd.u32 pe, pe, 16;\n\tsetp.lt.u32 p, pe, pend;\n\t@p bra.uni B9_LOOP;\n\tB9_DONE:\n\tmov.b32 pe, pend;\n\tshr.u32 t, %39, 16;\n\tmad.lo.u32 pend, t, 16, %32;\n\tsetp.ge.u32 p, pe, pend;\n\t@p bra.uni B10_DONE;\n\tB10_LOOP:\n\tld.shared.v4.b32 {o, x, gl, gh}, [pe];\n\tadd.u32 a, o, %33;\n\tld.shared.f64 u, [a];\n\tmov.b64 g, {gl, gh};\n\tfma.rn.f64 %10, u, g, %10;\n\tadd.u32 pe, pe, 16;\n\tsetp.lt.u32 p, pe, pend;\n\t@p bra.uni B10_LOOP;\n\tB10_DONE:\n\tmov.b32 pe, pend;\n\tand.b32 t, %40, 65535;\n\tmad.lo.u32 pend, t, 16, %32;\n\tsetp.ge.u32 p, pe, pend;\n\t@p bra.uni B11_DONE;\n\tB11_LOOP:\n\tld.shared.v4.b32 {o, x, gl, gh}, [pe];\n\tadd.u32 a, o, %33;\n\tld.shared.f64 u, [a];\n\tmov.b64 g, {gl, gh};\n\tfma.rn.f64 %11, u, g, %11;\n\tadd.u32 pe, pe, 16;\n\tsetp.lt.u32 p, pe, pend;\n\t@p bra.uni B11_LOOP;\n\tB11_DONE:\n\tmov.b32 pe, pend;\n\tshr.u32 t, %40, 16;\n\tmad.lo.u32 pend, t, 16, %32;\n\tsetp.ge.u32 p, pe, pend;\n\t@p bra.uni B12_DONE;\n\tB12_LOOP:\n\tld.shared.v4.b32 {o, x, gl, gh}, [pe];\n\tadd.u32 a, o, %33;\n\tld.shared.f64 u, [a];\n\tmov.b64 g, {gl, gh};\n\tfma.rn.f64 %12, u, g, %12;\n\tadd.u32 pe, pe, 16;\n\tsetp.lt.u32 p, pe, pend;\n\t@p bra.uni B12_LOOP;\n\tB12_DONE:\n\tmov.b32 pe, pend;\n\tand.b32 t, %41, 65535;\n\tmad.lo.u32 pend, t, 16, %32;\n\tsetp.ge.u32 p, pe, pend;\n\t@p bra.uni B13_DONE;\n\tB13_LOOP:\n\tld.shared.v4.b32 {o, x, gl, gh}, [pe];\n\tadd.u32 a, o, %33;\n\tld.shared.f64 u, [a];\n\tmov.b64 g, {gl, gh};\n\tfma.rn.f64 %13, u, g, %13;\n\tadd.u32 pe, pe, 16;\n\tsetp.lt.u32 p, pe, pend;\n\t@p bra.uni B13_LOOP;\n\tB13_DONE:\n\tmov.b32 pe, pend;\n\tshr.u32 t, %41, 16;\n\tmad.lo.u32 pend, t, 16, %32;\n\tsetp.ge.u32 p, pe, pend;\n\t@p bra.uni B14_DONE;\n\tB14_LOOP:\n\tld.shared.v4.b32 {o, x, gl, gh}, [pe];\n\tadd.u32 a, o, %33;\n\tld.shared.f64 u, [a];\n\tmov.b64 g, {gl, gh};\n\tfma.rn.f64 %14, u, g, %14;\n\tadd.u32 pe, pe, 16;\n\tsetp.lt.u32 p, pe, pend;\n\t@p bra.uni B14_LOOP;\n\tB14_DONE:\n\tmov.b32 pe, pend;\n\tand.b32 t, %42, 65535;\n\tmad.lo.u32 pend, t, 16, %32;\n\tsetp.ge.u32 p, pe, pend;\n\t@p bra.uni B15_DONE;\n\tB15_LOOP:\n\tld.shared.v4.b32 {o, x, gl, gh}, [pe];\n\tadd.u32 a, o, %33;\n\tld.shared.f64 u, [a];\n\tmov.b64 g, {gl, gh};\n\tfma.rn.f64 %15, u, g, %15;\n\tadd.u32 pe, pe, 16;\n\tsetp.lt.u32 p, pe, pend;\n\t@p bra.uni B15_LOOP;\n\tB15_DONE:\n\tmov.b32 pe, pend;\n\tshr.u32 t, %42, 16;\n\tmad.lo.u32 pend, t, 16, %32;\n\tsetp.ge.u32 p, pe, pend;\n\t@p bra.uni B16_DONE;\n\tB16_LOOP:\n\tld.shared.v4.b32 {o, x, gl, gh}, [pe];\n\tadd.u32 a, o, %33;\n\tld.shared.f64 u, [a];\n\tmov.b64 g, {gl, gh};\n\tfma.rn.f64 %16, u, g, %16;\n\tadd.u32 pe, pe, 16;\n\tsetp.lt.u32 p, pe, pend;\n\t@p bra.uni B16_LOOP;\n\tB16_DONE:\n\tmov.b32 pe, pend;\n\tand.b32 t, %43, 65535;\n\tmad.lo.u32 pend, t, 16, %32;\n\tsetp.ge.u32 p, pe, pend;\n\t@p bra.uni B17_DONE;\n\tB17_LOOP:\n\tld.shared.v4.b32 {o, x, gl, gh}, [pe];\n\tadd.u32 a, o, %33;\n\tld.shared.f64 u, [a];\n\tmov.b64 g, {gl, gh};\n\tfma.rn.f64 %17, u, g, %17;\n\tadd.u32 pe, pe, 16;\n\tsetp.lt.u32 p, pe, pend;\n\t@p bra.uni B17_LOOP;\n\tB17_DONE:\n\tmov.b32 pe, pend;\n\tshr.u32 t, %43, 16;\n\tmad.lo.u32 pend, t, 16, %32;\n\tsetp.ge.u32 p, pe, pend;\n\t@p bra.uni B18_DONE;\n\tB18_LOOP:\n\tld.shared.v4.b32 {o, x, gl, gh}, [pe];\n\tadd.u32 a, o, %33;\n\tld.shared.f64 u, [a];\n\tmov.b64 g, {gl, gh};\n\tfma.rn.f64 %18, u, g, %18;\n\tadd.u32 pe, pe, 16;\n\tsetp.lt.u32 p, pe, pend;\n\t@p bra.uni B18_LOOP;\n\tB18_DONE:\n\tmov.b32 pe, pend;\n\tand.b32 t, %44, 65535;\n\tmad.lo.u32 pend, t, 16, %32;\n\tsetp.ge.u32 p, pe, pend;\n\t@p bra.uni B19_DONE;\n\tB19_LOOP:\n\tld.shared.v4.b32 {o, x, gl, gh}, [pe];\n\tadd.u32 a, o, %33;\n\tld.shared.f64 u, [a];\n\tmov.b64 g, {gl, gh};\n\tfma.rn.f64 %19, u, g, %19;\n\tadd.u32 pe, pe, 16;\n\tsetp.lt.u32 p, pe, pend;\n\t@p bra.uni B19_LOOP;\n\tB19_DONE:\n\tmov.b32 pe, pend;\n\tshr.u32 t, %44, 16;\n\tmad.lo.u32 pend, t, 16, %32;\n\tsetp.ge.u32 p, pe, pend;\n\t@p bra.uni B20_DONE;\n\tB20_LOOP:\n\tld.shared.v4.b32 {o, x, gl, gh}, [pe];\n\tadd.u32 a, o, %33;\n\tld.shared.f64 u, [a];\n\tmov.b64 g, {gl, gh};\n\tfma.rn.f64 %20, u, g, %20;\n\tadd.u32 pe, pe, 16;\n\tsetp.lt.u32 p, pe, pend;\n\t@p bra.uni B20_LOOP;\n\tB20_DONE:\n\tmov.b32 pe, pend;\n\tand.b32 t, %45, 65535;\n\tmad.lo.u32 pend, t, 16, %32;\n\tsetp.ge.u32 p, pe, pend;\n\t@p bra.uni B21_DONE;\n\tB21_LOOP:\n\tld.shared.v4.b32 {o, x, gl, gh}, [pe];\n\tadd.u32 a, o, %33;\n\tld.shared.f64 u, [a];\n\tmov.b64 g, {gl, gh};\n\tfma.rn.f64 %21, u, g, %21;\n\tadd.u32 pe, pe, 16;\n\tsetp.lt.u32 p, pe, pend;\n\t@p bra.uni B21_LOOP;\n\tB21_DONE:\n\tmov.b32 pe, pend;\n\tshr.u32 t, %45, 16;\n\tmad.lo.u32 pend, t, 16, %32;\n\tsetp.ge.u32 p, pe, pend;\n\t@p bra.uni B22_DONE;\n\tB22_LOOP:\n\tld.shared.v4.b32 {o, x, gl, gh}, [pe];\n\tadd.u32 a, o, %33;\n\tld.shared.f64 u, [a];\n\tmov.b64 g, {gl, gh};\n\tfma.rn.f64 %22, u, g, %22;\n\tadd.u32 pe, pe, 16;\n\tsetp.lt.u32 p, pe, pend;\n\t@p bra.uni B22_LOOP;\n\tB22_DONE:\n\tmov.b32 pe, pend;\n\tand.b32 t, %46, 65535;\n\tmad.lo.u32 pend, t, 16, %32;\n\tsetp.ge.u32 p, pe, pend;\n\t@p bra.uni B23_DONE;\n\tB23_LOOP:\n\tld.shared.v4.b32 {o, x, gl, gh}, [pe];\n\tadd.u32 a, o, %33;\n\tld.shared.f64 u, [a];\n\tmov.b64 g, {gl, gh};\n\tfma.rn.f64 %23, u, g, %23;\n\tadd.u32 pe, pe, 16;\n\tsetp.lt.u32 p, pe, pend;\n\t@p bra.uni B23_LOOP;\n\tB23_DONE:\n\tmov.b32 pe, pend;\n\tshr.u32 t, %46, 16;\n\tmad.lo.u32 pend, t, 16, %32;\n\tsetp.ge.u32 p, pe, pend;\n\t@p bra.uni B24_DONE;\n\tB24_LOOP:\n\tld.shared.v4.b32 {o, x, gl, gh}, [pe];\n\tadd.u32 a, o, %33;\n\tld.shared.f64 u, [a];\n\tmov.b64 g, {gl, gh};\n\tfma.rn.f64 %24, u, g, %24;\n\tadd.u32 pe, pe, 16;\n\tsetp.lt.u32 p, pe, pend;\n\t@p bra.uni B24_LOOP;\n\tB24_DONE:\n\tmov.b32 pe, pend;\n\tand.b32 t, %47, 65535;\n\tmad.lo.u32 pend, t, 16, %32;\n\tsetp.ge.u32 p, pe, pend;\n\t@p bra.uni B25_DONE;\n\tB25_LOOP:\n\tld.shared.v4.b32 {o, x, gl, gh}, [pe];\n\tadd.u32 a, o, %33;\n\tld.shared.f64 u, [a];\n\tmov.b64 g, {gl, gh};\n\tfma.rn.f64 %25, u, g, %25;\n\tadd.u32 pe, pe, 16;\n\tsetp.lt.u32 p, pe, pend;\n\t@p bra.uni B25_LOOP;\n\tB25_DONE:\n\tmov.b32 pe, pend;\n\tshr.u32 t, %47, 16;\n\tmad.lo.u32 pend, t, 16, %32;\n\tsetp.ge.u32 p, pe, pend;\n\t@p bra.uni B26_DONE;\n\tB26_LOOP:\n\tld.shared.v4.b32 {o, x, gl, gh}, [pe];\n\tadd.u32 a, o, %33;\n\tld.shared.f64 u, [a];\n\tmov.b64 g, {gl, gh};\n\tfma.rn.f64 %26, u, g, %26;\n\tadd.u32 pe, pe, 16;\n\tsetp.lt.u32 p, pe, pend;\n\t@p bra.uni B26_LOOP;\n\tB26_DONE:\n\tmov.b32 pe, pend;\n\tand.b32 t, %48, 65535;\n\tmad.lo.u32 pend, t, 16, %32;\n\tsetp.ge.u32 p, pe, pend;\n\t@p bra.uni B27_DONE;\n\tB27_LOOP:\n\tld.shared.v4.b32 {o, x, gl, gh}, [pe];\n\tadd.u32 a, o, %33;\n\tld.shared.f64 u, [a];\n\tmov.b64 g, {gl, gh};\n\tfma.rn.f64 %27, u, g, %27;\n\tadd.u32 pe, pe, 16;\n\tsetp.lt.u32 p, pe, pend;\n\t@p bra.uni B27_LOOP;\n\tB27_DONE:\n\tmov.b32 pe, pend;\n\tshr.u32 t, %48, 16;\n\tmad.lo.u32 pend, t, 16, %32;\n\tsetp.ge.u32 p, pe, pend;\n\t@p bra.uni B28_DONE;\n\tB28_LOOP:\n\tld.shared.v4.b32 {o, x, gl, gh}, [pe];\n\tadd.u32 a, o, %33;\n\tld.shared.f64 u, [a];\n\tmov.b64 g, {gl, gh};\n\tfma.rn.f64 %28, u, g, %28;\n\tadd.u32 pe, pe, 16;\n\tsetp.lt.u32 p, pe, pend;\n\t@p bra.uni B28_LOOP;\n\tB28_DONE:\n\tmov.b32 pe, pend;\n\tand.b32 t, %49, 65535;\n\tmad.lo.u32 pend, t, 16, %32;\n\tsetp.ge.u32 p, pe, pend;\n\t@p bra.uni B29_DONE;\n\tB29_LOOP:\n\tld.shared.v4.b32 {o, x, gl, gh}, [pe];\n\tadd.u32 a, o, %33;\n\tld.shared.f64 u, [a];\n\tmov.b64 g, {gl, gh};\n\tfma.rn.f64 %29, u, g, %29;\n\tadd.u32 pe, pe, 16;\n\tsetp.lt.u32 p, pe, pend;\n\t@p bra.uni B29_LOOP;\n\tB29_DONE:\n\tmov.b32 pe, pend;\n\tshr.u32 t, %49, 16;\n\tmad.lo.u32 pend, t, 16, %32;\n\tsetp.ge.u32 p, pe, pend;\n\t@p bra.uni B30_DONE;\n\tB30_LOOP:\n\tld.shared.v4.b32 {o, x, gl, gh}, [pe];\n\tadd.u32 a, o, %33;\n\tld.shared.f64 u, [a];\n\tmov.b64 g, {gl, gh};\n\tfma.rn.f64 %30, u, g, %30;\n\tadd.u32 pe, pe, 16;\n\tsetp.lt.u32 p, pe, pend;\n\t@p bra.uni B30_LOOP;\n\tB30_DONE:\n\tmov.b32 pe, pend;\n\tand.b32 t, %50, 65535;\n\tmad.lo.u32 pend, t, 16, %32;\n\tsetp.ge.u32 p, pe, pend;\n\t@p bra.uni B31_DONE;\n\tB31_LOOP:\n\tld.shared.v4.b32 {o, x, gl, gh}, [pe];\n\tadd.u32 a, o, %33;\n\tld.shared.f64 u, [a];\n\tmov.b64 g, {gl, gh};\n\tfma.rn.f64 %31, u, g, %31;\n\tadd.u32 pe, pe, 16;\n\tsetp.lt.u32 p, pe, pend;\n\t@p bra.uni B31_LOOP;\n\tB31_DONE:\n\tmov.b32 pe, pend;\n\t}"
+                 : "+d"(acc[0][0]), "+d"(acc[0][1]), "+d"(acc[0][2]), "+d"(acc[0][3]), "+d"(acc[0][4]), "+d"(acc[0][5]), "+d"(acc[0][6]), "+d"(acc[0][7]), "+d"(acc[0][8]), "+d"(acc[0][9]), "+d"(acc[0][10]), "+d"(acc[0][11]), "+d"(acc[0][12]), "+d"(acc[0][13]), "+d"(acc[0][14]), "+d"(acc[0][15]), "+d"(acc[0][16]), "+d"(acc[0][17]), "+d"(acc[0][18]), "+d"(acc[0][19]), "+d"(acc[0][20]), "+d"(acc[0][21]), "+d"(acc[0][22]), "+d"(acc[0][23]), "+d"(acc[0][24]), "+d"(acc[0][25]), "+d"(acc[0][26]), "+d"(acc[0][27]), "+d"(acc[0][28]), "+d"(acc[0][29]), "+d"(acc[0][30]), "+d"(acc[0][31])
+                 : "r"(sen), "r"(sx), "r"(bw[0]), "r"(bw[1]), "r"(bw[2]), "r"(bw[3]), "r"(bw[4]), "r"(bw[5]), "r"(bw[6]), "r"(bw[7]), "r"(bw[8]), "r"(bw[9]), "r"(bw[10]), "r"(bw[11]), "r"(bw[12]), "r"(bw[13]), "r"(bw[14]), "r"(bw[15]), "r"(bw[16])
+                 : "memory");
+}
+__device__ __forceinline__ void run_s1(uint32_t &pe, uint32_t pend, uint32_t sx, double &c0) {
+    asm volatile("{\n\t.reg .pred p;\n\t.reg .b32 o0, x0, l0, h0, a0;\n\t.reg .f64 u0, g0;\n\tsetp.ge.u32 p, %0, %2;\n\t@p bra.uni DONE;\n\tLOOP:\n\tld.shared.v4.b32 {o0, x0, l0, h0}, [%0];\n\tadd.u32 a0, o0, %3;\n\tld.shared.f64 u0, [a0];\n\tmov.b64 g0, {l0, h0};\n\tfma.rn.f64 %1, u0, g0, %1;\n\tadd.u32 %0, %0, 16;\n\tsetp.lt.u32 p, %0, %2;\n\t@p bra.uni LOOP;\n\tDONE:\n\t}"
+                 : "+r"(pe), "+d"(c0)
+                 : "r"(pend), "r"(sx)
+                 : "memory");
+}
+__device__ __forceinline__ void run_s1f(uint32_t &pe, uint32_t pend, uint32_t sx, uint4 f, double &c0) {
+    asm volatile("{\n\t.reg .pred p;\n\t.reg .b32 o0, x0, l0, h0, a0;\n\t.reg .f64 u0, g0;\n\tsetp.ge.u32 p, %0, %2;\n\t@p bra.uni DONE;\n\tadd.u32 a0, %4, %3;\n\tld.shared.f64 u0, [a0];\n\tmov.b64 g0, {%6, %7};\n\tfma.rn.f64 %1, u0, g0, %1;\n\tadd.u32 %0, %0, 16;\n\tsetp.ge.u32 p, %0, %2;\n\t@p bra.uni DONE;\n\tLOOP:\n\tld.shared.v4.b32 {o0, x0, l0, h0}, [%0];\n\tadd.u32 a0, o0, %3;\n\tld.shared.f64 u0, [a0];\n\tmov.b64 g0, {l0, h0};\n\tfma.rn.f64 %1, u0, g0, %1;\n\tadd.u32 %0, %0, 16;\n\tsetp.lt.u32 p, %0, %2;\n\t@p bra.uni LOOP;\n\tDONE:\n\t}"
+                 : "+r"(pe), "+d"(c0)
+                 : "r"(pend), "r"(sx), "r"(f.x), "r"(f.y), "r"(f.z), "r"(f.w)
+                 : "memory");
+}
+__device__ __forceinline__ void run_t1(uint32_t &pe, uint32_t pend, uint32_t st, uint32_t lane8, double &c0) {
+    asm volatile("{\n\t.reg .pred p;\n\t.reg .b32 o0, x0, l0, h0, a0;\n\t.reg .f64 u0, g0;\n\tsetp.ge.u32 p, %0, %2;\n\t@p bra.uni DONE;\n\tLOOP:\n\tld.shared.v4.b32 {o0, x0, l0, h0}, [%0];\n\txor.b32 a0, x0, %4;\n\tadd.u32 a0, a0, o0;\n\tadd.u32 a0, a0, %3;\n\tld.shared.f64 u0, [a0];\n\tmov.b64 g0, {l0, h0};\n\tfma.rn.f64 %1, u0, g0, %1;\n\tadd.u32 %0, %0, 16;\n\tsetp.lt.u32 p, %0, %2;\n\t@p bra.uni LOOP;\n\tDONE:\n\t}"
+                 : "+r"(pe), "+d"(c0)
+                 : "r"(pend), "r"(st), "r"(lane8)
+                 : "memory");
+}
+__device__ __forceinline__ void run_t1f(uint32_t &pe, uint32_t pend, uint32_t st, uint32_t lane8, uint4 f, double &c0) {
+    asm volatile("{\n\t.reg .pred p;\n\t.reg .b32 o0, x0, l0, h0, a0;\n\t.reg .f64 u0, g0;\n\tsetp.ge.u32 p, %0, %2;\n\t@p bra.uni DONE;\n\txor.b32 a0, %6, %4;\n\tadd.u32 a0, a0, %5;\n\tadd.u32 a0, a0, %3;\n\tld.shared.f64 u0, [a0];\n\tmov.b64 g0, {%7, %8};\n\tfma.rn.f64 %1, u0, g0, %1;\n\tadd.u32 %0, %0, 16;\n\tsetp.ge.u32 p, %0, %2;\n\t@p bra.uni DONE;\n\tLOOP:\n\tld.shared.v4.b32 {o0, x0, l0, h0}, [%0];\n\txor.b32 a0, x0, %4;\n\tadd.u32 a0, a0, o0;\n\tadd.u32 a0, a0, %3;\n\tld.shared.f64 u0, [a0];\n\tmov.b64 g0, {l0, h0};\n\tfma.rn.f64 %1, u0, g0, %1;\n\tadd.u32 %0, %0, 16;\n\tsetp.lt.u32 p, %0, %2;\n\t@p bra.uni LOOP;\n\tDONE:\n\t}"
+                 : "+r"(pe), "+d"(c0)
+                 : "r"(pend), "r"(st), "r"(lane8), "r"(f.x), "r"(f.y), "r"(f.z), "r"(f.w)
+                 : "memory");
+}
+
 __device__ __forceinline__ uint4 lds_u4(uint32_t addr) {
     uint4 w;
     asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];"
@@ -440,7 +478,7 @@ __global__ void __launch_bounds__((NW + (PROD ? 1 : 0)) * 32, 1)
 
     const uint32_t smem_base = smem_u32(stage0);
     const uint32_t lane8 = lane * 8u;
-    const uint32_t lane_off = TRANS ? 0u : lane * 16u;  // S tiles: rows 2l, 2l+1 (+64)
+    const uint32_t lane_off = TRANS ? 0u : lane * 8u * (RPT == 1 ? 1u : 2u);  // S: rows 2l,2l+1 (+64) / l
     int cs = 0;
     uint32_t cph = 0;
     for (int i = 0; i < nloc; ++i) {
@@ -475,7 +513,9 @@ __global__ void __launch_bounds__((NW + (PROD ? 1 : 0)) * 32, 1)
             return (jj & 1) ? (bw[jj >> 1] >> 16) : (bw[jj >> 1] & 0xffffu);
         };
         if (!BATCH && !TRANS && WHOLE) {
-            if constexpr (RPT == 2 && DB == 8) chunk_s_2x8(acc, sen, sx, bw);
+            if constexpr (RPT == 1 && DB == 16) chunk_s_1x16(acc, sen, sx, bw);
+            else if constexpr (RPT == 1 && DB == 32) chunk_s_1x32(acc, sen, sx, bw);
+            else if constexpr (RPT == 2 && DB == 8) chunk_s_2x8(acc, sen, sx, bw);
             else if constexpr (RPT == 2 && DB == 4) chunk_s_2x4(acc, sen, sx, bw);
             else if constexpr (RPT == 2 && DB == 16) chunk_s_2x16(acc, sen, sx, bw);
             else if constexpr (RPT == 4 && DB == 2) chunk_s_4x2(acc, sen, sx, bw);
@@ -491,12 +531,15 @@ __global__ void __launch_bounds__((NW + (PROD ? 1 : 0)) * 32, 1)
                 const uint32_t pend = sen + 16u * bound(jj + 1);
                 const uint4 w = wn;
                 if (jj + 1 < DB) wn = lds_u4(pend);
-                if (TRANS) {
-                    if (RPT == 2) run_t2f(pe, pend, st, lane8, w, acc[0][jj], acc[1][jj]);
-                    else run_t4f(pe, pend, st, lane8, w, acc[0][jj], acc[1][jj], acc[RPT - 2][jj],
-                                 acc[RPT - 1][jj]);
+                if constexpr (RPT == 1) {
+                    if (TRANS) run_t1f(pe, pend, st, lane8, w, acc[0][jj]);
+                    else run_s1f(pe, pend, sx, w, acc[0][jj]);
+                } else if constexpr (RPT == 2) {
+                    if (TRANS) run_t2f(pe, pend, st, lane8, w, acc[0][jj], acc[1][jj]);
+                    else run_s2f(pe, pend, sx, w, acc[0][jj], acc[1][jj]);
                 } else {
-                    if (RPT == 2) run_s2f(pe, pend, sx, w, acc[0][jj], acc[1][jj]);
+                    if (TRANS) run_t4f(pe, pend, st, lane8, w, acc[0][jj], acc[1][jj],
+                                       acc[RPT - 2][jj], acc[RPT - 1][jj]);
                     else run_s4f(pe, pend, sx, w, acc[0][jj], acc[1][jj], acc[RPT - 2][jj],
                                  acc[RPT - 1][jj]);
                 }
@@ -529,6 +572,10 @@ __global__ void __launch_bounds__((NW + (PROD ? 1 : 0)) * 32, 1)
                         asm volatile("ld.shared.f64 %0, [%1];" : "=d"(u) : "r"(ad + 256u * r) : "memory");
                         acc[r][jj] = fma(u, g, acc[r][jj]);
                     }
+                } else if constexpr (RPT == 1) {
+                    double u;
+                    asm volatile("ld.shared.f64 %0, [%1];" : "=d"(u) : "r"(sx + w[t].x) : "memory");
+                    acc[0][jj] = fma(u, g, acc[0][jj]);
                 } else {
                     const uint32_t ad = sx + w[t].x;
 #pragma unroll
@@ -547,12 +594,15 @@ __global__ void __launch_bounds__((NW + (PROD ? 1 : 0)) * 32, 1)
                 const int jj = g0 + t;
                 uint32_t pe = sen + 16u * (b[t] + 1);
                 const uint32_t pend = sen + 16u * b[t + 1];
-                if (TRANS) {
-                    if (RPT == 2) run_t2(pe, pend, st, lane8, acc[0][jj], acc[1][jj]);
-                    else run_t4(pe, pend, st, lane8, acc[0][jj], acc[1][jj], acc[RPT - 2][jj],
-                                acc[RPT - 1][jj]);
+                if constexpr (RPT == 1) {
+                    if (TRANS) run_t1(pe, pend, st, lane8, acc[0][jj]);
+                    else run_s1(pe, pend, sx, acc[0][jj]);
+                } else if constexpr (RPT == 2) {
+                    if (TRANS) run_t2(pe, pend, st, lane8, acc[0][jj], acc[1][jj]);
+                    else run_s2(pe, pend, sx, acc[0][jj], acc[1][jj]);
                 } else {
-                    if (RPT == 2) run_s2(pe, pend, sx, acc[0][jj], acc[1][jj]);
+                    if (TRANS) run_t4(pe, pend, st, lane8, acc[0][jj], acc[1][jj], acc[RPT - 2][jj],
+                                      acc[RPT - 1][jj]);
                     else run_s4(pe, pend, sx, acc[0][jj], acc[1][jj], acc[RPT - 2][jj],
                                 acc[RPT - 1][jj]);
                 }
@@ -616,6 +666,9 @@ __global__ void __launch_bounds__((NW + (PROD ? 1 : 0)) * 32, 1)
                     const int64_t row = r0 + lane + 32 * r;
                     if (row < p.m_out) col[row] = acc[r][jj] * p.scale;
                 }
+            } else if constexpr (RPT == 1) {
+                const int64_t row = r0 + lane;
+                if (row < p.m_out) col[row] = acc[0][jj] * p.scale;
             } else {      // lane owns rows 2l, 2l+1 (+64 for RPT 4)
 #pragma unroll
                 for (int h = 0; h < RPT / 2; ++h) {
@@ -804,6 +857,10 @@ extern "C" int hsk_sjlt_apply(const double *A, int64_t rows, int64_t cols, int64
     // S': 16 warps (its cp.async producer work is shared by all warps).
     bool w32 = !trans;
     if (const char *env = getenv("HSK_SJLT_W32")) w32 = env[0] == '1';
+    if (g.rpt == 1) {  // 32-row tiles, 512-bucket slabs
+        if (w32) return sjlt::launch<1, 16, 32>(a, g, st);
+        return sjlt::launch<1, 32, 16>(a, g, st);
+    }
     if (w32) {
         if (d <= 64) return sjlt::launch<4, 2, 32>(a, g, st);
         if (d <= 128) return sjlt::launch<2, 4, 32>(a, g, st);
