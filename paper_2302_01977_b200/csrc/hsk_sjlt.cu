@@ -41,45 +41,77 @@ constexpr int kMaxChunkEntries = 4096;  // TK * alpha bound (12-bit local index)
 constexpr int kPlanSlab = 512;          // bucket-offset rows padded for slabs | 512
 constexpr int64_t kMaxD = (1 << 19);    // bucket index fits 19 bits of the sort key
 
+// Per-direction sub-plan geometry.  One plan buffer holds a header, the S
+// sub-plan (trans 0) and the S' sub-plan (trans 1), because the best tile
+// shape differs: S keeps 64-row tiles (two 256-bucket slabs for d <= 512),
+// S' prefers 32-row tiles with TK = 256 (one 512-bucket slab, more entries
+// per bucket and chunk).
 struct Geom {
-    int rpt;           // rows per lane: 4 for d <= 64, 2 for d <= 256, else 1
-    int tm;            // rows per CTA = 32 * rpt
+    int rpt;           // rows per lane (tile rows tm = 32 * rpt)
+    int tm;
     int pitch;         // tile pitch (doubles) = tm: TMA writes densely; the S'
                        // producer orders its transposing stores conflict-free
-    int tk;
+    int tk;            // input indices per chunk
     int64_t nchunks;
     int64_t bstride;   // uint16 per bucket-offset row
     int64_t estride;   // entries per chunk row (tk*alpha)
-    int64_t bptr_off;  // bytes
-    int64_t ent_off;   // bytes
-    int64_t bytes;
+    int64_t bptr_off;  // bytes from the plan base
+    int64_t ent_off;   // bytes from the plan base
+    int64_t end;       // bytes from the plan base (end of this sub-plan)
 };
 
 static inline int64_t roundup(int64_t x, int64_t m) { return (x + m - 1) / m * m; }
 
-// TK: as long as a stage (TK x TM x 8 B tile + TK*alpha 16-byte entries)
-// leaves room for >= 3 stages in shared memory, capped at 128.
-static inline int tk_for(int alpha, int tm) {
-    int tk = 128;
-    if (const char *env = getenv("HSK_SJLT_TK")) return atoi(env);  // tuning override (power of 2)
-    while (tk > 1 && (tk * alpha > kMaxChunkEntries || tk * (tm * 8 + 16 * alpha) > 72 * 1024))
+static inline int stage_bytes_for(int tk, int tm, int alpha) {
+    return tk * tm * 8 + tm * 8 + 1152 + (tk * alpha + 1) * 16;
+}
+
+// largest power-of-two TK <= cap whose stage fits `per_stage` bytes
+static inline int tk_fit(int alpha, int tm, int cap, int per_stage) {
+    int tk = cap;
+    while (tk > 1 && (tk * alpha > kMaxChunkEntries || stage_bytes_for(tk, tm, alpha) > per_stage))
         tk >>= 1;
     return tk;
 }
 
-static Geom geom(int64_t n, int d, int alpha) {
+static Geom geom_dir(int64_t n, int d, int alpha, int trans, int64_t base) {
     Geom g;
-    g.rpt = d <= 64 ? 4 : d <= 256 ? 2 : 1;
+    int tk;
+    if (d <= 64) {                 // 128-row tiles, three or more stages
+        g.rpt = 4;
+        tk = tk_fit(alpha, 128, 128, 74 * 1024);
+    } else if (!trans && d <= 512) {  // S: 64-row tiles, TK 128, three stages
+        g.rpt = 2;
+        tk = tk_fit(alpha, 64, 128, 74 * 1024);
+    } else {                       // S', large d: 32-row tiles, TK 256 (two stages)
+        g.rpt = 1;
+        tk = tk_fit(alpha, 32, 256, 112 * 1024);
+    }
+    if (const char *env = getenv(trans ? "HSK_SJLT_TK_T" : "HSK_SJLT_TK")) tk = atoi(env);
+    if (const char *env = getenv(trans ? "HSK_SJLT_RPT_T" : "HSK_SJLT_RPT")) g.rpt = atoi(env);
     g.tm = 32 * g.rpt;
     g.pitch = g.tm;
-    g.tk = tk_for(alpha, g.tm);
+    g.tk = tk;
     g.nchunks = (n + g.tk - 1) / g.tk;
     g.bstride = roundup(d, kPlanSlab) + 8;
     g.estride = (int64_t)g.tk * alpha;
-    g.bptr_off = kHeaderBytes;
+    g.bptr_off = base;
     g.ent_off = roundup(g.bptr_off + (g.nchunks + 1) * g.bstride * 2, 128);
-    g.bytes = g.ent_off + roundup((g.nchunks + 1) * g.estride * 16, 128);
+    g.end = g.ent_off + roundup((g.nchunks + 1) * g.estride * 16, 128);
     return g;
+}
+
+struct Plan {
+    Geom s, t;
+    int64_t bytes;
+};
+
+static Plan plan_geom(int64_t n, int d, int alpha) {
+    Plan pl;
+    pl.s = geom_dir(n, d, alpha, 0, kHeaderBytes);
+    pl.t = geom_dir(n, d, alpha, 1, pl.s.end);
+    pl.bytes = pl.t.end;
+    return pl;
 }
 
 // ------------------------------------------------------------ plan build
@@ -775,7 +807,7 @@ using namespace hsk;
 extern "C" int64_t hsk_sjlt_plan_bytes(int64_t n, int32_t d, int32_t alpha) {
     if (n < 0 || d < 1 || alpha < 1 || d > sjlt::kMaxD || alpha > sjlt::kMaxChunkEntries)
         return HSK_EINVAL;
-    return sjlt::geom(n, d, alpha).bytes;
+    return sjlt::plan_geom(n, d, alpha).bytes;
 }
 
 extern "C" int hsk_sjlt_plan_build(const int32_t *pos, const int8_t *sgn, int64_t n, int32_t d,
@@ -787,23 +819,25 @@ extern "C" int hsk_sjlt_plan_build(const int32_t *pos, const int8_t *sgn, int64_
                 (long long)sjlt::kMaxD);
     HSK_REQUIRE(alpha <= sjlt::kMaxChunkEntries, HSK_EINVAL, "sjlt plan: alpha=%d too large", alpha);
     HSK_REQUIRE(n < (1ll << 31), HSK_EINVAL, "sjlt plan: n too large");
-    const sjlt::Geom g = sjlt::geom(n, d, alpha);
-    HSK_REQUIRE(plan != nullptr && plan_bytes >= g.bytes, HSK_EINVAL,
+    const sjlt::Plan pl = sjlt::plan_geom(n, d, alpha);
+    HSK_REQUIRE(plan != nullptr && plan_bytes >= pl.bytes, HSK_EINVAL,
                 "sjlt plan: buffer of %lld bytes, need %lld", (long long)plan_bytes,
-                (long long)g.bytes);
+                (long long)pl.bytes);
     HSK_REQUIRE(n == 0 || (pos != nullptr && sgn != nullptr), HSK_EINVAL, "sjlt plan: null pattern");
     cudaStream_t st = as_stream(stream);
     unsigned char *base = static_cast<unsigned char *>(plan);
-    cudaError_t e = cudaMemsetAsync(base, 0, g.bytes, st);
+    cudaError_t e = cudaMemsetAsync(base, 0, pl.bytes, st);
     if (e != cudaSuccess) return cuda_status(e, "sjlt plan: memset");
     if (n > 0) {
-        int p2 = 1;
-        while (p2 < g.tk * alpha) p2 <<= 1;
-        sjlt::sjlt_plan_kernel<<<(unsigned)g.nchunks, 256, p2 * sizeof(uint32_t), st>>>(
-            pos, sgn, n, d, alpha, g.tk, p2, g.bstride, g.estride, g.pitch,
-            reinterpret_cast<uint16_t *>(base + g.bptr_off),
-            reinterpret_cast<uint4 *>(base + g.ent_off), reinterpret_cast<int *>(base + 28));
-        HSK_CHECK_LAUNCH("sjlt_plan_kernel");
+        for (const sjlt::Geom *g : {&pl.s, &pl.t}) {
+            int p2 = 1;
+            while (p2 < g->tk * alpha) p2 <<= 1;
+            sjlt::sjlt_plan_kernel<<<(unsigned)g->nchunks, 256, p2 * sizeof(uint32_t), st>>>(
+                pos, sgn, n, d, alpha, g->tk, p2, g->bstride, g->estride, g->pitch,
+                reinterpret_cast<uint16_t *>(base + g->bptr_off),
+                reinterpret_cast<uint4 *>(base + g->ent_off), reinterpret_cast<int *>(base + 28));
+            HSK_CHECK_LAUNCH("sjlt_plan_kernel");
+        }
     }
     return HSK_OK;
 }
@@ -830,7 +864,8 @@ extern "C" int hsk_sjlt_apply(const double *A, int64_t rows, int64_t cols, int64
     HSK_REQUIRE(plan != nullptr && S != nullptr && (A != nullptr || n == 0), HSK_EINVAL,
                 "sjlt apply: null pointer");
     HSK_REQUIRE(m_out < (1ll << 31) && n < (1ll << 31), HSK_EINVAL, "sjlt apply: too large");
-    const sjlt::Geom g = sjlt::geom(n, d, alpha);
+    const sjlt::Plan pl = sjlt::plan_geom(n, d, alpha);
+    const sjlt::Geom &g = trans ? pl.t : pl.s;
     const unsigned char *base = static_cast<const unsigned char *>(plan);
     sjlt::ApplyArgs a{};
     a.A = A;
@@ -861,12 +896,14 @@ extern "C" int hsk_sjlt_apply(const double *A, int64_t rows, int64_t cols, int64
         if (w32) return sjlt::launch<1, 16, 32>(a, g, st);
         return sjlt::launch<1, 32, 16>(a, g, st);
     }
-    if (w32) {
-        if (d <= 64) return sjlt::launch<4, 2, 32>(a, g, st);
+    if (g.rpt == 4) {  // 128-row tiles, 64-bucket slabs
+        if (w32) return sjlt::launch<4, 2, 32>(a, g, st);
+        return sjlt::launch<4, 4, 16>(a, g, st);
+    }
+    if (w32) {          // 64-row tiles
         if (d <= 128) return sjlt::launch<2, 4, 32>(a, g, st);
         return sjlt::launch<2, 8, 32>(a, g, st);
     }
-    if (d <= 64) return sjlt::launch<4, 4, 16>(a, g, st);
     if (d <= 128) return sjlt::launch<2, 8, 16>(a, g, st);
     return sjlt::launch<2, 16, 16>(a, g, st);
 }
