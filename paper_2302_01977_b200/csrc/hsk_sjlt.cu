@@ -77,15 +77,17 @@ static inline int tk_fit(int alpha, int tm, int cap, int per_stage) {
 static Geom geom_dir(int64_t n, int d, int alpha, int trans, int64_t base) {
     Geom g;
     int tk;
-    if (d <= 64) {                 // 128-row tiles, three or more stages
+    // per-stage budgets: 3 stages (or 2) of the 226 KB ring
+    constexpr int kStage3 = (226 * 1024 - 256) / 3, kStage2 = (226 * 1024 - 256) / 2;
+    if (d <= 64) {                          // 128-row tiles, three or more stages
         g.rpt = 4;
-        tk = tk_fit(alpha, 128, 128, 74 * 1024);
-    } else if (!trans && d <= 512) {  // S: 64-row tiles, TK 128, three stages
+        tk = tk_fit(alpha, 128, 128, kStage3);
+    } else if (d <= 256 || (!trans && d <= 512)) {  // 64-row tiles, TK 128, three stages
         g.rpt = 2;
-        tk = tk_fit(alpha, 64, 128, 74 * 1024);
-    } else {                       // S', large d: 32-row tiles, TK 256 (two stages)
+        tk = tk_fit(alpha, 64, 128, kStage3);
+    } else {                                // 32-row tiles, TK 256, two stages
         g.rpt = 1;
-        tk = tk_fit(alpha, 32, 256, 112 * 1024);
+        tk = tk_fit(alpha, 32, 256, kStage2);
     }
     if (const char *env = getenv(trans ? "HSK_SJLT_TK_T" : "HSK_SJLT_TK")) tk = atoi(env);
     if (const char *env = getenv(trans ? "HSK_SJLT_RPT_T" : "HSK_SJLT_RPT")) g.rpt = atoi(env);
