@@ -459,13 +459,36 @@ __global__ void __launch_bounds__((NW + (PROD ? 1 : 0)) * 32, 1)
         const int nel = p.tk * TM;
         if (TRANS) {
             // element (kk, rr) = A[k0+kk, r0+rr] -> sx[kk*TM + (rr ^ (kk%32))];
-            // lanes along kk: coalesced reads, conflict-free swizzled writes
-            const int tkm = p.tk - 1, lg = p.log2tk;
-            for (int idx = threadIdx.x; idx < nel; idx += NW * 32) {
-                const int rr = idx >> lg, kk = idx & tkm;
-                const bool v = (kk < kc) && (r0 + rr < p.m_out);
+            // lanes along kk: coalesced reads, conflict-free swizzled writes.
+            // Thread t keeps kk = t % TK fixed and walks rows rr = t / TK + q*(NT/TK).
+            constexpr int NT = NW * 32;
+            const int tk = p.tk;
+            if (NT % tk == 0) {
+                const int kk = threadIdx.x & (tk - 1);
+                const int rstep = NT / tk;
+                int rr = threadIdx.x / tk;
+                const int sw = kk & 31;
                 const double *src = p.A + (r0 + rr) * p.lda + k0 + kk;
-                cp_async8(sx + kk * TM + (rr ^ (kk & 31)), v ? src : p.A, v);
+                const int64_t sstep = (int64_t)rstep * p.lda;
+                double *dbase = sx + kk * TM;
+                if (kk < kc && r0 + TM <= p.m_out) {
+#pragma unroll 4
+                    for (; rr < TM; rr += rstep, src += sstep) cp_async8(dbase + (rr ^ sw), src, true);
+                } else {
+                    const bool vk = kk < kc;
+                    for (; rr < TM; rr += rstep, src += sstep) {
+                        const bool v = vk && (r0 + rr < p.m_out);
+                        cp_async8(dbase + (rr ^ sw), v ? src : p.A, v);
+                    }
+                }
+            } else {
+                const int tkm = tk - 1, lg = p.log2tk;
+                for (int idx = threadIdx.x; idx < nel; idx += NT) {
+                    const int rr = idx >> lg, kk = idx & tkm;
+                    const bool v = (kk < kc) && (r0 + rr < p.m_out);
+                    const double *src = p.A + (r0 + rr) * p.lda + k0 + kk;
+                    cp_async8(sx + kk * TM + (rr ^ (kk & 31)), v ? src : p.A, v);
+                }
             }
         } else {
             for (int idx = threadIdx.x; idx < nel; idx += NW * 32) {
