@@ -382,7 +382,7 @@ struct ApplyArgs {
 // warp 0 / lane 0 issues TMA + bulk copies (mode 0); in modes 1/2 every lane
 // issues its share of 8-byte cp.async for the chunk STAGES-1 ahead.
 template <int RPT, int DB, int NW, bool TRANS, bool BATCH, bool PROD, bool WHOLE = true>
-__global__ void __launch_bounds__((NW + (PROD ? 1 : 0)) * 32, 1)
+__global__ void __launch_bounds__((NW + (PROD ? (TRANS ? 4 : 1) : 0)) * 32, 1)
     sjlt_apply_kernel(const ApplyArgs p, const __grid_constant__ CUtensorMap tmap) {
     constexpr int TM = 32 * RPT;
     constexpr int SLAB = NW * DB;
@@ -422,7 +422,8 @@ __global__ void __launch_bounds__((NW + (PROD ? 1 : 0)) * 32, 1)
                 make_uint4((uint32_t)p.zero_off, 0u, 0u, 0x3FF00000u);
     }
     if (threadIdx.x == 0) {
-        const uint32_t fcount = mode == 0 ? 1u : 1u + 32u * NW;
+        constexpr int PW = PROD ? (TRANS ? 4 : 1) : 0;  // dedicated producer warps
+        const uint32_t fcount = mode == 0 ? 1u : 1u + 32u * (PROD ? PW : NW);
         for (int s = 0; s < stages; ++s) {
             mbar_init(&full[s], fcount);
             mbar_init(&empty[s], NW);
@@ -444,13 +445,13 @@ __global__ void __launch_bounds__((NW + (PROD ? 1 : 0)) * 32, 1)
         bulk_g2s(st + p.bp_off, p.bptr + c * p.bstride + j0, bp_bytes, bar);
         bulk_g2s(st + p.en_off, p.ent + c * p.estride, en_bytes, bar);
     };
-    auto issue_coop = [&](int j) {  // every lane
+    auto issue_coop = [&](int j, int ptid, int pnt) {  // threads [0, pnt) of the producer set
         unsigned char *st = stage_of(j);
         uint64_t *bar = &full[j % stages];
         const int64_t c = c_begin + j;
         const int64_t k0 = c * p.tk;
         const int kc = (int)(p.n - k0 < p.tk ? p.n - k0 : p.tk);
-        if (threadIdx.x == 0) {
+        if (ptid == 0) {
             mbar_arrive_expect_tx(bar, bp_bytes + en_bytes);
             bulk_g2s(st + p.bp_off, p.bptr + c * p.bstride + j0, bp_bytes, bar);
             bulk_g2s(st + p.en_off, p.ent + c * p.estride, en_bytes, bar);
@@ -460,38 +461,27 @@ __global__ void __launch_bounds__((NW + (PROD ? 1 : 0)) * 32, 1)
         if (TRANS) {
             // element (kk, rr) = A[k0+kk, r0+rr] -> sx[kk*TM + (rr ^ (kk%32))];
             // lanes along kk: coalesced reads, conflict-free swizzled writes.
-            // Thread t keeps kk = t % TK fixed and walks rows rr = t / TK + q*(NT/TK).
-            constexpr int NT = NW * 32;
+            // Thread t owns columns kk = t, t + pnt, ... and walks all TM rows
+            // with pointer increments (lanes along kk: 256 B per instruction).
             const int tk = p.tk;
-            if (NT % tk == 0) {
-                const int kk = threadIdx.x & (tk - 1);
-                const int rstep = NT / tk;
-                int rr = threadIdx.x / tk;
+            const bool full_rows = r0 + TM <= p.m_out;
+            for (int kk = ptid; kk < tk; kk += pnt) {
                 const int sw = kk & 31;
-                const double *src = p.A + (r0 + rr) * p.lda + k0 + kk;
-                const int64_t sstep = (int64_t)rstep * p.lda;
+                const double *src = p.A + r0 * p.lda + k0 + kk;
                 double *dbase = sx + kk * TM;
-                if (kk < kc && r0 + TM <= p.m_out) {
-#pragma unroll 4
-                    for (; rr < TM; rr += rstep, src += sstep) cp_async8(dbase + (rr ^ sw), src, true);
+                if (kk < kc && full_rows) {
+#pragma unroll 8
+                    for (int rr = 0; rr < TM; ++rr, src += p.lda) cp_async8(dbase + (rr ^ sw), src, true);
                 } else {
                     const bool vk = kk < kc;
-                    for (; rr < TM; rr += rstep, src += sstep) {
+                    for (int rr = 0; rr < TM; ++rr, src += p.lda) {
                         const bool v = vk && (r0 + rr < p.m_out);
                         cp_async8(dbase + (rr ^ sw), v ? src : p.A, v);
                     }
                 }
-            } else {
-                const int tkm = tk - 1, lg = p.log2tk;
-                for (int idx = threadIdx.x; idx < nel; idx += NT) {
-                    const int rr = idx >> lg, kk = idx & tkm;
-                    const bool v = (kk < kc) && (r0 + rr < p.m_out);
-                    const double *src = p.A + (r0 + rr) * p.lda + k0 + kk;
-                    cp_async8(sx + kk * TM + (rr ^ (kk & 31)), v ? src : p.A, v);
-                }
             }
         } else {
-            for (int idx = threadIdx.x; idx < nel; idx += NW * 32) {
+            for (int idx = ptid; idx < nel; idx += pnt) {
                 const int kk = idx / TM, rr = idx % TM;
                 const bool v = (kk < kc) && (r0 + rr < p.m_out);
                 const double *src = p.A + (k0 + kk) * p.lda + r0 + rr;
@@ -503,13 +493,23 @@ __global__ void __launch_bounds__((NW + (PROD ? 1 : 0)) * 32, 1)
 
     int issued = 0;
     if (PROD) {
-        // dedicated producer warp (mode 0): refill a slot as soon as every
-        // consumer warp has released it
-        if (warp == NW) {
-            if (lane == 0) {
+        // dedicated producer warp(s): refill a slot as soon as every consumer
+        // warp has released it (mode 0: one TMA-issuing lane; modes 1/2: the
+        // producer warps share the 8-byte transposing copies)
+        if (warp >= NW) {
+            constexpr int PW = TRANS ? 4 : 1;
+            if (mode == 0) {
+                if (lane == 0 && warp == NW) {
+                    for (int j = 0; j < nloc; ++j) {
+                        if (j >= stages) mbar_wait(&empty[j % stages], (uint32_t)((j / stages) - 1) & 1u);
+                        issue_tma(j);
+                    }
+                }
+            } else {
+                const int ptid = threadIdx.x - NW * 32;
                 for (int j = 0; j < nloc; ++j) {
                     if (j >= stages) mbar_wait(&empty[j % stages], (uint32_t)((j / stages) - 1) & 1u);
-                    issue_tma(j);
+                    issue_coop(j, ptid, PW * 32);
                 }
             }
             __syncwarp();
@@ -524,7 +524,7 @@ __global__ void __launch_bounds__((NW + (PROD ? 1 : 0)) * 32, 1)
         if (warp == 0 && lane == 0)
             for (; issued < nloc && issued < stages; ++issued) issue_tma(issued);
     } else {
-        for (; issued < nloc && issued < stages - 1; ++issued) issue_coop(issued);
+        for (; issued < nloc && issued < stages - 1; ++issued) issue_coop(issued, threadIdx.x, NW * 32);
     }
 
     double acc[RPT][DB];
@@ -541,10 +541,10 @@ __global__ void __launch_bounds__((NW + (PROD ? 1 : 0)) * 32, 1)
     for (int i = 0; i < nloc; ++i) {
         // ---- producer duty (modes 1/2): chunk i + stages - 1 into the slot of
         // chunk i - 1, once every warp has finished chunk i - 1
-        if (mode != 0 && issued < nloc) {
+        if (!PROD && mode != 0 && issued < nloc) {
             const int j = issued;
             if (j >= stages) mbar_wait(&empty[j % stages], (uint32_t)((j / stages) - 1) & 1u);
-            issue_coop(j);
+            issue_coop(j, threadIdx.x, NW * 32);
             ++issued;
         }
 
@@ -790,17 +790,18 @@ static int launch(ApplyArgs a, const Geom &g, cudaStream_t st) {
     // so it pairs with the unbatched consumer loops)
     bool prod = NW < 32;  // a 33rd warp would cut the register budget to 56
     if (const char *env = getenv("HSK_SJLT_PROD")) prod = env[0] == '1';
-    prod = prod && a.mode == 0;
+    prod = prod && (a.mode == 0 || a.mode == 1) && NW + (a.trans ? 4 : 1) <= 32;
     if (prod) batch = false;
     bool whole = true;
     if (const char *env = getenv("HSK_SJLT_WHOLE")) whole = env[0] == '1';
-    auto kern = a.trans ? (batch ? sjlt_apply_kernel<RPT, DB, NW, true, true, false>
-                                 : sjlt_apply_kernel<RPT, DB, NW, true, false, false>)
+    auto kern = a.trans ? (prod ? sjlt_apply_kernel<RPT, DB, NW, true, false, true>
+                                : batch ? sjlt_apply_kernel<RPT, DB, NW, true, true, false>
+                                        : sjlt_apply_kernel<RPT, DB, NW, true, false, false>)
                         : (prod ? sjlt_apply_kernel<RPT, DB, NW, false, false, true>
                                 : batch ? sjlt_apply_kernel<RPT, DB, NW, false, true, false>
                                         : whole ? sjlt_apply_kernel<RPT, DB, NW, false, false, false, true>
                                                 : sjlt_apply_kernel<RPT, DB, NW, false, false, false, false>);
-    const int nthreads = (NW + (prod ? 1 : 0)) * 32;
+    const int nthreads = (NW + (prod ? (a.trans ? 4 : 1) : 0)) * 32;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e != cudaSuccess) return cuda_status(e, "sjlt: set smem attribute");
     const int64_t grid = tiles * a.nslabs * ks;
