@@ -42,10 +42,10 @@ constexpr int kPlanSlab = 512;          // bucket-offset rows padded for slabs |
 constexpr int64_t kMaxD = (1 << 19);    // bucket index fits 19 bits of the sort key
 
 // Per-direction sub-plan geometry.  One plan buffer holds a header, the S
-// sub-plan (trans 0) and the S' sub-plan (trans 1), because the best tile
-// shape differs: S keeps 64-row tiles (two 256-bucket slabs for d <= 512),
-// S' prefers 32-row tiles with TK = 256 (one 512-bucket slab, more entries
-// per bucket and chunk).
+// sub-plan (trans 0) and the S' sub-plan (trans 1): the best tile shape can
+// differ per direction (measured): 128-row tiles for d <= 64, 64-row tiles
+// (256-bucket slabs, TK 128) otherwise, except S with d > 512, which prefers
+// 32-row tiles with 512-bucket slabs and TK = 256 (half the slab re-reads).
 struct Geom {
     int rpt;           // rows per lane (tile rows tm = 32 * rpt)
     int tm;
@@ -82,10 +82,10 @@ static Geom geom_dir(int64_t n, int d, int alpha, int trans, int64_t base) {
     if (d <= 64) {                          // 128-row tiles, three or more stages
         g.rpt = 4;
         tk = tk_fit(alpha, 128, 128, kStage3);
-    } else if (d <= 256 || (!trans && d <= 512)) {  // 64-row tiles, TK 128, three stages
+    } else if (trans || d <= 512) {         // 64-row tiles, TK 128, three stages
         g.rpt = 2;
         tk = tk_fit(alpha, 64, 128, kStage3);
-    } else {                                // 32-row tiles, TK 256, two stages
+    } else {                                // S, d > 512: 32-row tiles (512-bucket slabs), TK 256
         g.rpt = 1;
         tk = tk_fit(alpha, 32, 256, kStage2);
     }
