@@ -16,6 +16,8 @@
 // DFMA.  Only the d sampled columns of the last log2(n_pad/B) stages are
 // ever formed (pruned FWHT).  Sample indices may repeat (the reference
 // draws with replacement, sketching.py:159).
+#include <string.h>
+
 #include <algorithm>
 
 #include "hsk_common.cuh"
@@ -32,6 +34,7 @@ struct Args {
     int64_t lda;
     int trans;
     int vec16;
+    int use_tma;
     int64_t m_out;   // number of vectors
     int64_t n;       // vector length (before padding)
     int64_t n_pad;
@@ -44,14 +47,19 @@ struct Args {
     int64_t lds, col0;
     int nslabs;
     int pitch;
+    int stages;
+    int64_t nseg;    // n_pad / seg
 };
 
-// Load segment g of the 32 vectors into X[k][r] (pitch doubles per k).
-__device__ __forceinline__ void load_segment(const Args &p, double *X, int64_t r0, int64_t g) {
+constexpr int kMaxStages = 4;
+
+// Segment g of the 32 vectors into X[k][r] (pitch doubles per k) with 8/16-byte
+// cp.async; used when TMA cannot be (S' tiles, unaligned A, n_pad < 256).
+__device__ __forceinline__ void load_segment_async(const Args &p, double *X, int64_t r0,
+                                                   int64_t g) {
     const int tid = threadIdx.x;
     const int64_t k0 = g * p.seg;
     if (!p.trans) {
-        // vector r = row r0+r of A; element k at A[k*lda + r0 + r]; 16 B = 2 rows
         for (int q = tid; q < p.seg * (TM / 2); q += NW * 32) {
             const int kk = q / (TM / 2), rr = (q % (TM / 2)) * 2;
             const int64_t gk = k0 + kk, gr = r0 + rr;
@@ -67,97 +75,121 @@ __device__ __forceinline__ void load_segment(const Args &p, double *X, int64_t r
             }
         }
     } else {
-        // vector r = column r0+r of A; element k at A[(r0+r)*lda + k].
-        // 16 consecutive k per half-warp: coalesced reads; pitch 33 makes the
-        // transposing shared stores conflict-free.
-        const int lane = tid & 31, warp = tid >> 5;
-        const int kl = lane & 15, rl = lane >> 4;
-        for (int rb = warp * 2; rb < TM; rb += NW * 2) {
-            const int rr = rb + rl;
-            const int64_t gr = r0 + rr;
-            const bool vr = gr < p.m_out;
-            const double *col = p.A + gr * p.lda + k0;
-            for (int kk = kl; kk < p.seg; kk += 16) {
-                const bool v = vr && (k0 + kk < p.n);
-                cp_async8(X + kk * p.pitch + rr, v ? col + kk : p.A, v);
+        // vector r = column r0+r of A; thread keeps kk fixed and walks rows
+        // (lanes along kk: coalesced reads; pitch 33: conflict-free stores)
+        for (int kk = tid % p.seg; kk < p.seg; kk += NW * 32) {
+            const int64_t gk = k0 + kk;
+            const bool vk = gk < p.n;
+            for (int rr = tid / p.seg; rr < TM; rr += (NW * 32 + p.seg - 1) / p.seg) {
+                const bool v = vk && (r0 + rr < p.m_out);
+                cp_async8(X + kk * p.pitch + rr, v ? p.A + (r0 + rr) * p.lda + gk : p.A, v);
             }
         }
     }
 }
 
+// In-register Walsh-Hadamard butterflies over the index bits of x[0..15].
+__device__ __forceinline__ void wht16(double (&x)[16]) {
+#pragma unroll
+    for (int h = 1; h < 16; h <<= 1)
+#pragma unroll
+        for (int q = 0; q < 16; ++q)
+            if (!(q & h)) {
+                const double a = x[q], b = x[q + h];
+                x[q] = a + b;
+                x[q + h] = a - b;
+            }
+}
+
 template <int TPW>
-__global__ void __launch_bounds__(NW * 32, 1) srht_kernel(const Args p) {
-    extern __shared__ __align__(128) double sm[];
+__global__ void __launch_bounds__(NW * 32, 1)
+    srht_kernel(const Args p, const __grid_constant__ CUtensorMap tmap) {
+    extern __shared__ __align__(128) unsigned char smem[];
+    uint64_t *full = reinterpret_cast<uint64_t *>(smem);
+    double *sgn_all = reinterpret_cast<double *>(smem + 64);            // stages x seg doubles
+    int *s_samp = reinterpret_cast<int *>(smem + 64 + kMaxStages * SEG * 8);  // NW*TPW
+    double *X0 = reinterpret_cast<double *>(smem + 64 + kMaxStages * SEG * 8 +
+                                            ((NW * TPW * 4 + 127) / 128) * 128);
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int slab = (int)(blockIdx.x % p.nslabs);
     const int64_t r0 = (blockIdx.x / p.nslabs) * TM;
     const int t0 = slab * NW * TPW;
     const int tile_elems = p.seg * p.pitch;
-    double *X0 = sm;
-    double *X1 = sm + tile_elems;
-    int *s_samp = reinterpret_cast<int *>(sm + 2 * tile_elems);
+    const int stages = p.stages;
+    const bool tma = p.use_tma != 0;
 
     for (int i = tid; i < NW * TPW; i += NW * 32) {
         const int t = t0 + i;
         s_samp[i] = t < p.d ? (int)p.sample[t] : 0;
     }
-    const int64_t G = p.n_pad / p.seg;
+    if (tid == 0) {
+        for (int q = 0; q < stages; ++q) mbar_init(&full[q], 1);
+        fence_mbar_init();
+        if (tma) prefetch_tmap(&tmap);
+    }
+    __syncthreads();
+    const int64_t G = p.nseg;
     const int lb = 31 - __clz(p.seg);  // log2(seg)
+
+    // issue segment g into slot g % stages (TMA path: one thread; else all)
+    auto issue = [&](int64_t g) {
+        const int q = (int)(g % stages);
+        double *X = X0 + (size_t)q * tile_elems;
+        double *sg = sgn_all + q * SEG;
+        if (tma) {
+            if (tid == 0) {
+                mbar_arrive_expect_tx(&full[q], (uint32_t)(p.seg * TM * 8 + p.seg * 8));
+                tma_load_2d(X, &tmap, (int)r0, (int)(g * p.seg), &full[q]);
+                bulk_g2s(sg, p.signs + g * p.seg, p.seg * 8, &full[q]);
+            }
+        } else {
+            load_segment_async(p, X, r0, g);
+            for (int k = tid; k < p.seg; k += NW * 32) cp_async8(sg + k, p.signs + g * p.seg + k, true);
+        }
+    };
 
     double acc[TPW];
 #pragma unroll
     for (int i = 0; i < TPW; ++i) acc[i] = 0.0;
 
-    load_segment(p, X0, r0, 0);
-    cp_async_commit();
+    for (int64_t g = 0; g < stages - 1 && g < G; ++g) {
+        issue(g);
+        if (!tma) cp_async_commit();
+    }
     for (int64_t g = 0; g < G; ++g) {
-        double *X = (g & 1) ? X1 : X0;
-        if (g + 1 < G) load_segment(p, (g & 1) ? X0 : X1, r0, g + 1);
-        cp_async_commit();
-        cp_async_wait<1>();
-        __syncthreads();
-        const int64_t kb = g * p.seg;
+        const int q = (int)(g % stages);
+        double *X = X0 + (size_t)q * tile_elems;
+        const double *sg = sgn_all + q * SEG;
+        // the slot of segment g-1 is free: every thread passed its last sync
+        if (g + stages - 1 < G) issue(g + stages - 1);
+        if (tma) {
+            mbar_wait(&full[q], (uint32_t)((g / stages) & 1));
+        } else {
+            cp_async_commit();
+            if (stages == 2) cp_async_wait<1>(); else cp_async_wait<2>();
+            __syncthreads();
+        }
         if (p.seg == SEG) {
-            // pass A: k = w + 16 q, butterflies over k bits 4..7 (q bits)
+            // pass A: k = w + 16 q, butterflies over k bits 4..7 (signs applied)
             double x[16];
 #pragma unroll
-            for (int q = 0; q < 16; ++q) {
-                const int k = warp + 16 * q;
-                const int64_t gk = kb + k;
-                x[q] = X[k * p.pitch + lane] * (gk < p.n ? p.signs[gk] : 0.0);
+            for (int u = 0; u < 16; ++u) {
+                const int k = warp + 16 * u;
+                x[u] = X[k * p.pitch + lane] * sg[k];
             }
+            wht16(x);
 #pragma unroll
-            for (int h = 1; h < 16; h <<= 1)
-#pragma unroll
-                for (int q = 0; q < 16; ++q)
-                    if (!(q & h)) {
-                        const double a = x[q], b = x[q + h];
-                        x[q] = a + b;
-                        x[q + h] = a - b;
-                    }
-#pragma unroll
-            for (int q = 0; q < 16; ++q) X[(warp + 16 * q) * p.pitch + lane] = x[q];
+            for (int u = 0; u < 16; ++u) X[(warp + 16 * u) * p.pitch + lane] = x[u];
             __syncthreads();
             // pass B: k = 16 w + q, butterflies over k bits 0..3
 #pragma unroll
-            for (int q = 0; q < 16; ++q) x[q] = X[(16 * warp + q) * p.pitch + lane];
+            for (int u = 0; u < 16; ++u) x[u] = X[(16 * warp + u) * p.pitch + lane];
+            wht16(x);
 #pragma unroll
-            for (int h = 1; h < 16; h <<= 1)
-#pragma unroll
-                for (int q = 0; q < 16; ++q)
-                    if (!(q & h)) {
-                        const double a = x[q], b = x[q + h];
-                        x[q] = a + b;
-                        x[q + h] = a - b;
-                    }
-#pragma unroll
-            for (int q = 0; q < 16; ++q) X[(16 * warp + q) * p.pitch + lane] = x[q];
+            for (int u = 0; u < 16; ++u) X[(16 * warp + u) * p.pitch + lane] = x[u];
         } else {
             // small n_pad (< 256): signs, then in-smem radix-2 stages
-            for (int k = warp; k < p.seg; k += NW) {
-                const int64_t gk = kb + k;
-                X[k * p.pitch + lane] *= (gk < p.n ? p.signs[gk] : 0.0);
-            }
+            for (int k = warp; k < p.seg; k += NW) X[k * p.pitch + lane] *= sg[k];
             __syncthreads();
             for (int h = 1; h < p.seg; h <<= 1) {
                 for (int pr = warp; pr < p.seg / 2; pr += NW) {
@@ -170,18 +202,22 @@ __global__ void __launch_bounds__(NW * 32, 1) srht_kernel(const Args p) {
             }
         }
         __syncthreads();
-        // fold segment g into the sampled outputs owned by this warp
+        // fold segment g into the warp's sampled outputs.  Lane i computes the
+        // Walsh sign of sample i for this segment; a ballot shares the mask.
+        {
+            const int sw = lane < TPW ? s_samp[warp * TPW + lane] : 0;
+            const uint32_t neg = __ballot_sync(0xffffffffu,
+                                               __popc((unsigned)(g & (sw >> lb))) & 1);
 #pragma unroll
-        for (int i = 0; i < TPW; ++i) {
-            const int s = s_samp[warp * TPW + i];
-            const int s_lo = s & (p.seg - 1);
-            const int s_hi = s >> lb;
-            const double sg = (__popcll((long long)(g & s_hi)) & 1) ? -1.0 : 1.0;
-            acc[i] = fma(X[s_lo * p.pitch + lane], sg, acc[i]);
+            for (int i = 0; i < TPW; ++i) {
+                const int s_lo = s_samp[warp * TPW + i] & (p.seg - 1);
+                const double gsg = __hiloint2double((int)(((neg >> i) & 1u) << 31 | 0x3FF00000u), 0);
+                acc[i] = fma(X[s_lo * p.pitch + lane], gsg, acc[i]);
+            }
         }
-        __syncthreads();  // X is overwritten by the load issued next iteration
+        __syncthreads();  // X (slot q) is refilled by the issue of segment g + 1
     }
-    cp_async_wait<0>();
+    if (!tma) cp_async_wait<0>();
 
     const int64_t row = r0 + lane;
     if (row < p.m_out) {
@@ -195,15 +231,29 @@ __global__ void __launch_bounds__(NW * 32, 1) srht_kernel(const Args p) {
 
 template <int TPW>
 static int launch(Args a, cudaStream_t st) {
+    // TMA for row tiles of aligned A with full 256-column segments
+    a.use_tma = !a.trans && a.vec16 && a.seg == SEG;
     a.pitch = a.trans ? TM + 1 : TM;
-    const int smem = 2 * a.seg * a.pitch * 8 + NW * TPW * 4 + 16;
+    a.nseg = a.n_pad / a.seg;
+    CUtensorMap tmap;
+    memset(&tmap, 0, sizeof(tmap));
+    if (a.use_tma) {
+        int rc = make_tmap_f64_2d(&tmap, a.A, (uint64_t)a.m_out, (uint64_t)a.n, (uint64_t)a.lda,
+                                  TM, SEG);
+        if (rc) return rc;
+    }
+    const int tile = a.seg * a.pitch * 8;
+    const int fixed = 64 + kMaxStages * SEG * 8 + ((NW * TPW * 4 + 127) / 128) * 128;
+    a.stages = (int)std::min<int64_t>(3, std::max<int64_t>(2, a.nseg));
+    while (a.stages > 2 && fixed + a.stages * tile > 227 * 1024) --a.stages;
+    const int smem = fixed + a.stages * tile;
     auto kern = srht_kernel<TPW>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e != cudaSuccess) return cuda_status(e, "srht: set smem attribute");
     a.nslabs = (a.d + NW * TPW - 1) / (NW * TPW);
     const int64_t grid = ((a.m_out + TM - 1) / TM) * a.nslabs;
     HSK_REQUIRE(grid < (1ll << 31), HSK_EINVAL, "srht: grid too large");
-    kern<<<(unsigned)grid, NW * 32, smem, st>>>(a);
+    kern<<<(unsigned)grid, NW * 32, smem, st>>>(a, tmap);
     HSK_CHECK_LAUNCH("srht_kernel");
     return HSK_OK;
 }
