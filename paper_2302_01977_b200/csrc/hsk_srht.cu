@@ -52,6 +52,9 @@ struct Args {
 };
 
 constexpr int kMaxStages = 4;
+// smem map: [full barriers 64 B][signs: kMaxStages x SEG doubles][samples]
+// [tiles from kTileOff: 1024-byte aligned for the TMA destination]
+constexpr int kTileOff = ((64 + kMaxStages * SEG * 8 + 32 * 32 * 4) + 1023) / 1024 * 1024;
 
 // Segment g of the 32 vectors into X[k][r] (pitch doubles per k) with 8/16-byte
 // cp.async; used when TMA cannot be (S' tiles, unaligned A, n_pad < 256).
@@ -108,8 +111,7 @@ __global__ void __launch_bounds__(NW * 32, 1)
     uint64_t *full = reinterpret_cast<uint64_t *>(smem);
     double *sgn_all = reinterpret_cast<double *>(smem + 64);            // stages x seg doubles
     int *s_samp = reinterpret_cast<int *>(smem + 64 + kMaxStages * SEG * 8);  // NW*TPW
-    double *X0 = reinterpret_cast<double *>(smem + 64 + kMaxStages * SEG * 8 +
-                                            ((NW * TPW * 4 + 127) / 128) * 128);
+    double *X0 = reinterpret_cast<double *>(smem + kTileOff);  // 1024-B aligned (TMA)
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int slab = (int)(blockIdx.x % p.nslabs);
     const int64_t r0 = (blockIdx.x / p.nslabs) * TM;
@@ -243,7 +245,8 @@ static int launch(Args a, cudaStream_t st) {
         if (rc) return rc;
     }
     const int tile = a.seg * a.pitch * 8;
-    const int fixed = 64 + kMaxStages * SEG * 8 + ((NW * TPW * 4 + 127) / 128) * 128;
+    static_assert(NW * 32 * 4 <= 32 * 32 * 4, "sample table must fit below kTileOff");
+    const int fixed = kTileOff;
     a.stages = (int)std::min<int64_t>(3, std::max<int64_t>(2, a.nseg));
     while (a.stages > 2 && fixed + a.stages * tile > 227 * 1024) --a.stages;
     const int smem = fixed + a.stages * tile;
