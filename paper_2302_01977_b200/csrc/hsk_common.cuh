@@ -29,6 +29,12 @@ int cuda_status(cudaError_t e, const char *what);
 
 int sm_count();
 
+// Scratch for cross-CTA partial sums: a zero-initialised flag array plus a
+// data area, one per (device, stream) so launches on different streams never
+// share it; launches on one stream are ordered, and every kernel that uses
+// the flags leaves them zero.  Grows on demand (never shrinks).
+int stream_workspace(cudaStream_t st, size_t data_bytes, int nflags, void **data, int **flags);
+
 inline cudaStream_t as_stream(void *s) { return reinterpret_cast<cudaStream_t>(s); }
 
 // 2-D float64 TMA descriptor over a column-major matrix: inner dimension =
@@ -113,6 +119,14 @@ __device__ __forceinline__ void tma_load_2d(void *dst, const CUtensorMap *map, i
         : "memory");
 }
 
+// Pull a TMA box into L2 ahead of its shared-memory load (no completion).
+__device__ __forceinline__ void tma_prefetch_2d(const CUtensorMap *map, int x, int y) {
+    asm volatile("cp.async.bulk.prefetch.tensor.2d.L2.global.tile [%0, {%1, %2}];" ::"l"(
+                     reinterpret_cast<uint64_t>(map)),
+                 "r"(x), "r"(y)
+                 : "memory");
+}
+
 __device__ __forceinline__ void prefetch_tmap(const CUtensorMap *map) {
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(map)) : "memory");
 }
@@ -159,6 +173,21 @@ __device__ __forceinline__ double ld_dsmem_f64(const double *local, uint32_t ran
     double v;
     asm volatile("ld.shared::cluster.f64 %0, [%1];" : "=d"(v) : "r"(remote) : "memory");
     return v;
+}
+
+// Named barrier over the first `nthreads` threads (id 1; id 0 = __syncthreads).
+__device__ __forceinline__ void bar_named(int nthreads) {
+    asm volatile("bar.sync 1, %0;" ::"r"(nthreads) : "memory");
+}
+
+__device__ __forceinline__ int ld_acquire_gpu(const int *p) {
+    int v;
+    asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+
+__device__ __forceinline__ void st_release_gpu(int *p, int v) {
+    asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 
 }  // namespace hsk

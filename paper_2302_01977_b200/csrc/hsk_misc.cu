@@ -6,6 +6,9 @@
 #include <string.h>
 
 #include <algorithm>
+#include <map>
+#include <mutex>
+#include <utility>
 
 #include <cudaTypedefs.h>
 
@@ -61,6 +64,52 @@ int sm_count() {
         if (cached <= 0) cached = 148;
     }
     return cached;
+}
+
+namespace {
+struct Workspace {
+    void *data = nullptr;
+    size_t data_bytes = 0;
+    int *flags = nullptr;
+    int nflags = 0;
+};
+std::mutex g_ws_mu;
+std::map<std::pair<int, cudaStream_t>, Workspace> g_ws;
+}  // namespace
+
+int stream_workspace(cudaStream_t st, size_t data_bytes, int nflags, void **data, int **flags) {
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return cuda_status(e, "workspace: device");
+    std::lock_guard<std::mutex> lk(g_ws_mu);
+    Workspace &w = g_ws[std::make_pair(dev, st)];
+    if (w.data_bytes < data_bytes) {
+        if (w.data) {
+            cudaStreamSynchronize(st);
+            cudaFree(w.data);
+        }
+        w.data = nullptr;
+        w.data_bytes = 0;
+        e = cudaMalloc(&w.data, data_bytes);
+        if (e != cudaSuccess) return cuda_status(e, "workspace: allocate");
+        w.data_bytes = data_bytes;
+    }
+    if (w.nflags < nflags) {
+        if (w.flags) {
+            cudaStreamSynchronize(st);
+            cudaFree(w.flags);
+        }
+        w.flags = nullptr;
+        w.nflags = 0;
+        e = cudaMalloc(reinterpret_cast<void **>(&w.flags), (size_t)nflags * sizeof(int));
+        if (e != cudaSuccess) return cuda_status(e, "workspace: allocate flags");
+        e = cudaMemsetAsync(w.flags, 0, (size_t)nflags * sizeof(int), st);
+        if (e != cudaSuccess) return cuda_status(e, "workspace: clear flags");
+        w.nflags = nflags;
+    }
+    *data = w.data;
+    *flags = w.flags;
+    return HSK_OK;
 }
 
 // A_ij = exp(-|x_i - x_j|^2 / (2 h^2)) + diag*(i==j); thread per element,

@@ -7,18 +7,21 @@
 //  * Plan.  The reference keeps R^T = s (B+ - B-) as index-only CSR/CSC.  The
 //    GPU plan re-blocks the same pattern by k-chunks of TK input indices: per
 //    chunk, its TK*alpha entries sorted by bucket (stable in (k, t)), plus
-//    per-chunk bucket offsets.  An entry is 16 bytes, pre-decoded for the
-//    consumer: {byte offset of row kk in the staged tile, 0, (double)+-1}, so
-//    the inner loop spends no instructions on decoding.  Two entry arrays
-//    are kept, one per tile pitch (S: TMA-dense, S': padded transpose).
-//    Built on device by a per-chunk bitonic sort.
+//    per-chunk bucket offsets.  An entry is one 4-byte word kk << 3 | neg << 31
+//    (kk = input index within the chunk): the consumer turns it into a tile
+//    address with one shift-add and into +-1.0 with one LOP3.  Broadcast
+//    entry loads are what fills the SM's register-writeback port (128 B/clk)
+//    besides the tile loads themselves, so the word is kept minimal.  Each
+//    direction has its own sub-plan (tile shape).  Built on device by a
+//    per-chunk bitonic sort.
 //  * Apply.  A CTA owns TM = 32*RPT output rows and a slab of NW*DB buckets.
 //    Consumer warp w owns buckets [j0 + w*DB, +DB); lane l owns rows
 //    l*RPT .. l*RPT+RPT-1, so each warp holds an RPT x DB register
 //    accumulator block: owner-computes, no atomics, a fixed summation order
-//    (deterministic).  Per entry: one broadcast LDS of the entry word, one
+//    (deterministic).  Per entry: one broadcast LDS.32 of the entry word, one
 //    LDS.128 (RPT = 2) of the staged A tile, RPT DFMAs with +-1 (exactly the
-//    reference's add/subtract, one rounding each; no data multiplies).
+//    reference's add/subtract, one rounding each; no data multiplies).  The
+//    walk over a warp's entries is software-pipelined (tools/gen_consumers.py).
 //  * Streaming.  A producer warp moves TK x TM tiles of A (every element
 //    read once from HBM) plus the chunk's plan slice into a STAGES-deep
 //    shared-memory ring: one TMA 2-D tile load (UTMALDG, OOB zero-filled)
@@ -32,6 +35,7 @@
 #include <algorithm>
 
 #include "hsk_common.cuh"
+#include "hsk_sjlt_pipe.cuh"
 
 namespace hsk {
 namespace sjlt {
@@ -63,7 +67,7 @@ struct Geom {
 static inline int64_t roundup(int64_t x, int64_t m) { return (x + m - 1) / m * m; }
 
 static inline int stage_bytes_for(int tk, int tm, int alpha) {
-    return tk * tm * 8 + tm * 8 + 1152 + (tk * alpha + 1) * 16;
+    return tk * tm * 8 + tm * 8 + 1152 + (tk * alpha + 8) * 4;
 }
 
 // largest power-of-two TK <= cap whose stage fits `per_stage` bytes
@@ -96,10 +100,10 @@ static Geom geom_dir(int64_t n, int d, int alpha, int trans, int64_t base) {
     g.tk = tk;
     g.nchunks = (n + g.tk - 1) / g.tk;
     g.bstride = roundup(d, kPlanSlab) + 8;
-    g.estride = (int64_t)g.tk * alpha;
+    g.estride = roundup((int64_t)g.tk * alpha, 4);  // 16-byte rows for the bulk copy
     g.bptr_off = base;
     g.ent_off = roundup(g.bptr_off + (g.nchunks + 1) * g.bstride * 2, 128);
-    g.end = g.ent_off + roundup((g.nchunks + 1) * g.estride * 16, 128);
+    g.end = g.ent_off + roundup((g.nchunks + 1) * g.estride * 4, 128);
     return g;
 }
 
@@ -121,8 +125,8 @@ static Plan plan_geom(int64_t n, int d, int alpha) {
 // entry words in that order and per-bucket lower bounds.
 __global__ void sjlt_plan_kernel(const int32_t *__restrict__ pos, const int8_t *__restrict__ sgn,
                                  int64_t n, int d, int alpha, int tk, int p2, int64_t bstride,
-                                 int64_t estride, int pitch, uint16_t *__restrict__ bptr,
-                                 uint4 *__restrict__ ent, int *err) {
+                                 int64_t estride, uint16_t *__restrict__ bptr,
+                                 uint32_t *__restrict__ ent, int *err) {
     extern __shared__ uint32_t keys[];
     const int64_t c = blockIdx.x;
     const int64_t k0 = c * tk;
@@ -157,15 +161,13 @@ __global__ void sjlt_plan_kernel(const int32_t *__restrict__ pos, const int8_t *
             __syncthreads();
         }
     }
-    uint4 *e_out = ent + c * estride;
+    uint32_t *e_out = ent + c * estride;
     for (int e = threadIdx.x; e < estride; e += blockDim.x) {
-        uint4 w = make_uint4(0, 0, 0, 0);
+        uint32_t w = (uint32_t)tk << 3;  // padding: the zero row
         if (e < cnt) {
             const int local = keys[e] & 4095;
             const uint32_t kk = (uint32_t)(local / alpha);
-            const uint32_t g_hi = sgn[q0 + local] < 0 ? 0xBFF00000u : 0x3FF00000u;  // -1.0 / +1.0
-            // .y: byte XOR of the S' tile swizzle (row ^ (kk mod 32))
-            w = make_uint4(kk * pitch * 8, (kk & 31u) * 8u, 0, g_hi);
+            w = (kk << 3) | (sgn[q0 + local] < 0 ? 0x80000000u : 0u);
         }
         e_out[e] = w;
     }
@@ -189,174 +191,12 @@ __global__ void sjlt_plan_kernel(const int32_t *__restrict__ pos, const int8_t *
 //
 // Stage layout in shared memory (per ring slot):
 //   [A tile: TK rows of TM doubles][zero row: TM doubles][bucket bounds]
-//   [entries: estride + 1 words of 16 B; the last is the null entry]
-// The null entry {offset of the zero row, 0, +1.0} lets a warp fold the
-// FIRST entry of every bucket in a batch without predication: empty
-// buckets read the zero row and add +0.0.
+//   [entries: estride words, then null words (kk = TK: the zero row)]
 //
 // Lane -> tile rows.  S tiles (dense, TMA-written): RPT = 2 -> rows 2l, 2l+1
 // (one LDS.128); RPT = 4 -> rows 2l, 2l+1, 64+2l, 64+2l+1 (two LDS.128, each
 // a contiguous 512 B).  S' tiles (swizzled, element (kk,row) at
 // kk*TM + (row ^ (kk%32))): rows l + 32 r (LDS.64 each, conflict-free).
-
-// Entries [pe, pend) of one bucket (shared byte addresses), one per
-// iteration: consecutive DFMAs on an accumulator are a full iteration (two
-// shared loads) apart.  `bra.uni`: every lane walks the same list.
-// run_*f: the bucket's first entry is passed in registers (prefetched while
-// the previous bucket ran), so a bucket's chain starts at its tile load.
-// run_s*: S tiles, rows {2l, 2l+1} at [sx + o] (and {64+2l, 64+2l+1} at +512).
-// run_t*: S' tiles, rows l + 32 r at st + o + (x ^ lane8) + 256 r.
-__device__ __forceinline__ void run_s2(uint32_t &pe, uint32_t pend, uint32_t sx, double &c0, double &c1) {
-    asm volatile("{\n\t.reg .pred p;\n\t.reg .b32 o0, x0, l0, h0, a0;\n\t.reg .f64 u0, v0, g0;\n\tsetp.ge.u32 p, %0, %3;\n\t@p bra.uni DONE;\n\tLOOP:\n\tld.shared.v4.b32 {o0, x0, l0, h0}, [%0];\n\tadd.u32 a0, o0, %4;\n\tld.shared.v2.f64 {u0, v0}, [a0];\n\tmov.b64 g0, {l0, h0};\n\tfma.rn.f64 %1, u0, g0, %1;\n\tfma.rn.f64 %2, v0, g0, %2;\n\tadd.u32 %0, %0, 16;\n\tsetp.lt.u32 p, %0, %3;\n\t@p bra.uni LOOP;\n\tDONE:\n\t}"
-                 : "+r"(pe), "+d"(c0), "+d"(c1)
-                 : "r"(pend), "r"(sx)
-                 : "memory");
-}
-
-__device__ __forceinline__ void run_s2f(uint32_t &pe, uint32_t pend, uint32_t sx, uint4 f, double &c0, double &c1) {
-    asm volatile("{\n\t.reg .pred p;\n\t.reg .b32 o0, x0, l0, h0, a0;\n\t.reg .f64 u0, v0, g0;\n\tsetp.ge.u32 p, %0, %3;\n\t@p bra.uni DONE;\n\tadd.u32 a0, %5, %4;\n\tld.shared.v2.f64 {u0, v0}, [a0];\n\tmov.b64 g0, {%7, %8};\n\tfma.rn.f64 %1, u0, g0, %1;\n\tfma.rn.f64 %2, v0, g0, %2;\n\tadd.u32 %0, %0, 16;\n\tsetp.ge.u32 p, %0, %3;\n\t@p bra.uni DONE;\n\tLOOP:\n\tld.shared.v4.b32 {o0, x0, l0, h0}, [%0];\n\tadd.u32 a0, o0, %4;\n\tld.shared.v2.f64 {u0, v0}, [a0];\n\tmov.b64 g0, {l0, h0};\n\tfma.rn.f64 %1, u0, g0, %1;\n\tfma.rn.f64 %2, v0, g0, %2;\n\tadd.u32 %0, %0, 16;\n\tsetp.lt.u32 p, %0, %3;\n\t@p bra.uni LOOP;\n\tDONE:\n\t}"
-                 : "+r"(pe), "+d"(c0), "+d"(c1)
-                 : "r"(pend), "r"(sx), "r"(f.x), "r"(f.y), "r"(f.z), "r"(f.w)
-                 : "memory");
-}
-
-__device__ __forceinline__ void run_t2(uint32_t &pe, uint32_t pend, uint32_t st, uint32_t lane8, double &c0, double &c1) {
-    asm volatile("{\n\t.reg .pred p;\n\t.reg .b32 o0, x0, l0, h0, a0;\n\t.reg .f64 u0, v0, g0;\n\tsetp.ge.u32 p, %0, %3;\n\t@p bra.uni DONE;\n\tLOOP:\n\tld.shared.v4.b32 {o0, x0, l0, h0}, [%0];\n\txor.b32 a0, x0, %5;\n\tadd.u32 a0, a0, o0;\n\tadd.u32 a0, a0, %4;\n\tld.shared.f64 u0, [a0];\n\tld.shared.f64 v0, [a0+256];\n\tmov.b64 g0, {l0, h0};\n\tfma.rn.f64 %1, u0, g0, %1;\n\tfma.rn.f64 %2, v0, g0, %2;\n\tadd.u32 %0, %0, 16;\n\tsetp.lt.u32 p, %0, %3;\n\t@p bra.uni LOOP;\n\tDONE:\n\t}"
-                 : "+r"(pe), "+d"(c0), "+d"(c1)
-                 : "r"(pend), "r"(st), "r"(lane8)
-                 : "memory");
-}
-
-__device__ __forceinline__ void run_t2f(uint32_t &pe, uint32_t pend, uint32_t st, uint32_t lane8, uint4 f, double &c0, double &c1) {
-    asm volatile("{\n\t.reg .pred p;\n\t.reg .b32 o0, x0, l0, h0, a0;\n\t.reg .f64 u0, v0, g0;\n\tsetp.ge.u32 p, %0, %3;\n\t@p bra.uni DONE;\n\txor.b32 a0, %7, %5;\n\tadd.u32 a0, a0, %6;\n\tadd.u32 a0, a0, %4;\n\tld.shared.f64 u0, [a0];\n\tld.shared.f64 v0, [a0+256];\n\tmov.b64 g0, {%8, %9};\n\tfma.rn.f64 %1, u0, g0, %1;\n\tfma.rn.f64 %2, v0, g0, %2;\n\tadd.u32 %0, %0, 16;\n\tsetp.ge.u32 p, %0, %3;\n\t@p bra.uni DONE;\n\tLOOP:\n\tld.shared.v4.b32 {o0, x0, l0, h0}, [%0];\n\txor.b32 a0, x0, %5;\n\tadd.u32 a0, a0, o0;\n\tadd.u32 a0, a0, %4;\n\tld.shared.f64 u0, [a0];\n\tld.shared.f64 v0, [a0+256];\n\tmov.b64 g0, {l0, h0};\n\tfma.rn.f64 %1, u0, g0, %1;\n\tfma.rn.f64 %2, v0, g0, %2;\n\tadd.u32 %0, %0, 16;\n\tsetp.lt.u32 p, %0, %3;\n\t@p bra.uni LOOP;\n\tDONE:\n\t}"
-                 : "+r"(pe), "+d"(c0), "+d"(c1)
-                 : "r"(pend), "r"(st), "r"(lane8), "r"(f.x), "r"(f.y), "r"(f.z), "r"(f.w)
-                 : "memory");
-}
-
-__device__ __forceinline__ void run_s4(uint32_t &pe, uint32_t pend, uint32_t sx, double &c0, double &c1, double &c2, double &c3) {
-    asm volatile("{\n\t.reg .pred p;\n\t.reg .b32 o0, x0, l0, h0, a0;\n\t.reg .f64 u0, v0, w0, y0, g0;\n\tsetp.ge.u32 p, %0, %5;\n\t@p bra.uni DONE;\n\tLOOP:\n\tld.shared.v4.b32 {o0, x0, l0, h0}, [%0];\n\tadd.u32 a0, o0, %6;\n\tld.shared.v2.f64 {u0, v0}, [a0];\n\tld.shared.v2.f64 {w0, y0}, [a0+512];\n\tmov.b64 g0, {l0, h0};\n\tfma.rn.f64 %1, u0, g0, %1;\n\tfma.rn.f64 %2, v0, g0, %2;\n\tfma.rn.f64 %3, w0, g0, %3;\n\tfma.rn.f64 %4, y0, g0, %4;\n\tadd.u32 %0, %0, 16;\n\tsetp.lt.u32 p, %0, %5;\n\t@p bra.uni LOOP;\n\tDONE:\n\t}"
-                 : "+r"(pe), "+d"(c0), "+d"(c1), "+d"(c2), "+d"(c3)
-                 : "r"(pend), "r"(sx)
-                 : "memory");
-}
-
-__device__ __forceinline__ void run_s4f(uint32_t &pe, uint32_t pend, uint32_t sx, uint4 f, double &c0, double &c1, double &c2, double &c3) {
-    asm volatile("{\n\t.reg .pred p;\n\t.reg .b32 o0, x0, l0, h0, a0;\n\t.reg .f64 u0, v0, w0, y0, g0;\n\tsetp.ge.u32 p, %0, %5;\n\t@p bra.uni DONE;\n\tadd.u32 a0, %7, %6;\n\tld.shared.v2.f64 {u0, v0}, [a0];\n\tld.shared.v2.f64 {w0, y0}, [a0+512];\n\tmov.b64 g0, {%9, %10};\n\tfma.rn.f64 %1, u0, g0, %1;\n\tfma.rn.f64 %2, v0, g0, %2;\n\tfma.rn.f64 %3, w0, g0, %3;\n\tfma.rn.f64 %4, y0, g0, %4;\n\tadd.u32 %0, %0, 16;\n\tsetp.ge.u32 p, %0, %5;\n\t@p bra.uni DONE;\n\tLOOP:\n\tld.shared.v4.b32 {o0, x0, l0, h0}, [%0];\n\tadd.u32 a0, o0, %6;\n\tld.shared.v2.f64 {u0, v0}, [a0];\n\tld.shared.v2.f64 {w0, y0}, [a0+512];\n\tmov.b64 g0, {l0, h0};\n\tfma.rn.f64 %1, u0, g0, %1;\n\tfma.rn.f64 %2, v0, g0, %2;\n\tfma.rn.f64 %3, w0, g0, %3;\n\tfma.rn.f64 %4, y0, g0, %4;\n\tadd.u32 %0, %0, 16;\n\tsetp.lt.u32 p, %0, %5;\n\t@p bra.uni LOOP;\n\tDONE:\n\t}"
-                 : "+r"(pe), "+d"(c0), "+d"(c1), "+d"(c2), "+d"(c3)
-                 : "r"(pend), "r"(sx), "r"(f.x), "r"(f.y), "r"(f.z), "r"(f.w)
-                 : "memory");
-}
-
-__device__ __forceinline__ void run_t4(uint32_t &pe, uint32_t pend, uint32_t st, uint32_t lane8, double &c0, double &c1, double &c2, double &c3) {
-    asm volatile("{\n\t.reg .pred p;\n\t.reg .b32 o0, x0, l0, h0, a0;\n\t.reg .f64 u0, v0, w0, y0, g0;\n\tsetp.ge.u32 p, %0, %5;\n\t@p bra.uni DONE;\n\tLOOP:\n\tld.shared.v4.b32 {o0, x0, l0, h0}, [%0];\n\txor.b32 a0, x0, %7;\n\tadd.u32 a0, a0, o0;\n\tadd.u32 a0, a0, %6;\n\tld.shared.f64 u0, [a0];\n\tld.shared.f64 v0, [a0+256];\n\tld.shared.f64 w0, [a0+512];\n\tld.shared.f64 y0, [a0+768];\n\tmov.b64 g0, {l0, h0};\n\tfma.rn.f64 %1, u0, g0, %1;\n\tfma.rn.f64 %2, v0, g0, %2;\n\tfma.rn.f64 %3, w0, g0, %3;\n\tfma.rn.f64 %4, y0, g0, %4;\n\tadd.u32 %0, %0, 16;\n\tsetp.lt.u32 p, %0, %5;\n\t@p bra.uni LOOP;\n\tDONE:\n\t}"
-                 : "+r"(pe), "+d"(c0), "+d"(c1), "+d"(c2), "+d"(c3)
-                 : "r"(pend), "r"(st), "r"(lane8)
-                 : "memory");
-}
-
-__device__ __forceinline__ void run_t4f(uint32_t &pe, uint32_t pend, uint32_t st, uint32_t lane8, uint4 f, double &c0, double &c1, double &c2, double &c3) {
-    asm volatile("{\n\t.reg .pred p;\n\t.reg .b32 o0, x0, l0, h0, a0;\n\t.reg .f64 u0, v0, w0, y0, g0;\n\tsetp.ge.u32 p, %0, %5;\n\t@p bra.uni DONE;\n\txor.b32 a0, %9, %7;\n\tadd.u32 a0, a0, %8;\n\tadd.u32 a0, a0, %6;\n\tld.shared.f64 u0, [a0];\n\tld.shared.f64 v0, [a0+256];\n\tld.shared.f64 w0, [a0+512];\n\tld.shared.f64 y0, [a0+768];\n\tmov.b64 g0, {%10, %11};\n\tfma.rn.f64 %1, u0, g0, %1;\n\tfma.rn.f64 %2, v0, g0, %2;\n\tfma.rn.f64 %3, w0, g0, %3;\n\tfma.rn.f64 %4, y0, g0, %4;\n\tadd.u32 %0, %0, 16;\n\tsetp.ge.u32 p, %0, %5;\n\t@p bra.uni DONE;\n\tLOOP:\n\tld.shared.v4.b32 {o0, x0, l0, h0}, [%0];\n\txor.b32 a0, x0, %7;\n\tadd.u32 a0, a0, o0;\n\tadd.u32 a0, a0, %6;\n\tld.shared.f64 u0, [a0];\n\tld.shared.f64 v0, [a0+256];\n\tld.shared.f64 w0, [a0+512];\n\tld.shared.f64 y0, [a0+768];\n\tmov.b64 g0, {l0, h0};\n\tfma.rn.f64 %1, u0, g0, %1;\n\tfma.rn.f64 %2, v0, g0, %2;\n\tfma.rn.f64 %3, w0, g0, %3;\n\tfma.rn.f64 %4, y0, g0, %4;\n\tadd.u32 %0, %0, 16;\n\tsetp.lt.u32 p, %0, %5;\n\t@p bra.uni LOOP;\n\tDONE:\n\t}"
-                 : "+r"(pe), "+d"(c0), "+d"(c1), "+d"(c2), "+d"(c3)
-                 : "r"(pend), "r"(st), "r"(lane8), "r"(f.x), "r"(f.y), "r"(f.z), "r"(f.w)
-                 : "memory");
-}
-
-// Whole-chunk consumers: one PTX block walks all DB buckets of the warp
-// (bounds unpacked in-line, uniform branches, no convergence barriers
-// between buckets): ~4 instructions per empty bucket, 8 per entry.
-// one warp, one chunk, all 8 buckets, RPT = 2 (S tiles)
-__device__ __forceinline__ void chunk_s_2x8(double (&acc)[2][8], uint32_t sen, uint32_t sx, const uint32_t (&bw)[5]) {
-    asm volatile("{\n\t.reg .pred p;\n\t.reg .b32 o, x, gl, gh, a, t, pe, pend;\n\t.reg .f64 u, v, w, y, g;\n\tand.b32 t, %18, 65535;\n\tmad.lo.u32 pe, t, 16, %16;\n\tshr.u32 t, %18, 16;\n\tmad.lo.u32 pend, t, 16, %16;\n\tsetp.ge.u32 p, pe, pend;\n\t@p bra.uni B0_DONE;\n\tB0_LOOP:\n\tld.shared.v4.b32 {o, x, gl, gh}, [pe];\n\tadd.u32 a, o, %17;\n\tld.shared.v2.f64 {u, v}, [a];\n\tmov.b64 g, {gl, gh};\n\tfma.rn.f64 %0, u, g, %0;\n\tfma.rn.f64 %1, v, g, %1;\n\tadd.u32 pe, pe, 16;\n\tsetp.lt.u32 p, pe, pend;\n\t@p bra.uni B0_LOOP;\n\tB0_DONE:\n\tmov.b32 pe, pend;\n\tand.b32 t, %19, 65535;\n\tmad.lo.u32 pend, t, 16, %16;\n\tsetp.ge.u32 p, pe, pend;\n\t@p bra.uni B1_DONE;\n\tB1_LOOP:\n\tld.shared.v4.b32 {o, x, gl, gh}, [pe];\n\tadd.u32 a, o, %17;\n\tld.shared.v2.f64 {u, v}, [a];\n\tmov.b64 g, {gl, gh};\n\tfma.rn.f64 %2, u, g, %2;\n\tfma.rn.f64 %3, v, g, %3;\n\tadd.u32 pe, pe, 16;\n\tsetp.lt.u32 p, pe, pend;\n\t@p bra.uni B1_LOOP;\n\tB1_DONE:\n\tmov.b32 pe, pend;\n\tshr.u32 t, %19, 16;\n\tmad.lo.u32 pend, t, 16, %16;\n\tsetp.ge.u32 p, pe, pend;\n\t@p bra.uni B2_DONE;\n\tB2_LOOP:\n\tld.shared.v4.b32 {o, x, gl, gh}, [pe];\n\tadd.u32 a, o, %17;\n\tld.shared.v2.f64 {u, v}, [a];\n\tmov.b64 g, {gl, gh};\n\tfma.rn.f64 %4, u, g, %4;\n\tfma.rn.f64 %5, v, g, %5;\n\tadd.u32 pe, pe, 16;\n\tsetp.lt.u32 p, pe, pend;\n\t@p bra.uni B2_LOOP;\n\tB2_DONE:\n\tmov.b32 pe, pend;\n\tand.b32 t, %20, 65535;\n\tmad.lo.u32 pend, t, 16, %16;\n\tsetp.ge.u32 p, pe, pend;\n\t@p bra.uni B3_DONE;\n\tB3_LOOP:\n\tld.shared.v4.b32 {o, x, gl, gh}, [pe];\n\tadd.u32 a, o, %17;\n\tld.shared.v2.f64 {u, v}, [a];\n\tmov.b64 g, {gl, gh};\n\tfma.rn.f64 %6, u, g, %6;\n\tfma.rn.f64 %7, v, g, %7;\n\tadd.u32 pe, pe, 16;\n\tsetp.lt.u32 p, pe, pend;\n\t@p bra.uni B3_LOOP;\n\tB3_DONE:\n\tmov.b32 pe, pend;\n\tshr.u32 t, %20, 16;\n\tmad.lo.u32 pend, t, 16, %16;\n\tsetp.ge.u32 p, pe, pend;\n\t@p bra.uni B4_DONE;\n\tB4_LOOP:\n\tld.shared.v4.b32 {o, x, gl, gh}, [pe];\n\tadd.u32 a, o, %17;\n\tld.shared.v2.f64 {u, v}, [a];\n\tmov.b64 g, {gl, gh};\n\tfma.rn.f64 %8, u, g, %8;\n\tfma.rn.f64 %9, v, g, %9;\n\tadd.u32 pe, pe, 16;\n\tsetp.lt.u32 p, pe, pend;\n\t@p bra.uni B4_LOOP;\n\tB4_DONE:\n\tmov.b32 pe, pend;\n\tand.b32 t, %21, 65535;\n\tmad.lo.u32 pend, t, 16, %16;\n\tsetp.ge.u32 p, pe, pend;\n\t@p bra.uni B5_DONE;\n\tB5_LOOP:\n\tld.shared.v4.b32 {o, x, gl, gh}, [pe];\n\tadd.u32 a, o, %17;\n\tld.shared.v2.f64 {u, v}, [a];\n\tmov.b64 g, {gl, gh};\n\tfma.rn.f64 %10, u, g, %10;\n\tfma.rn.f64 %11, v, g, %11;\n\tadd.u32 pe, pe, 16;\n\tsetp.lt.u32 p, pe, pend;\n\t@p bra.uni B5_LOOP;\n\tB5_DONE:\n\tmov.b32 pe, pend;\n\tshr.u32 t, %21, 16;\n\tmad.lo.u32 pend, t, 16, %16;\n\tsetp.ge.u32 p, pe, pend;\n\t@p bra.uni B6_DONE;\n\tB6_LOOP:\n\tld.shared.v4.b32 {o, x, gl, gh}, [pe];\n\tadd.u32 a, o, %17;\n\tld.shared.v2.f64 {u, v}, [a];\n\tmov.b64 g, {gl, gh};\n\tfma.rn.f64 %12, u, g, %12;\n\tfma.rn.f64 %13, v, g, %13;\n\tadd.u32 pe, pe, 16;\n\tsetp.lt.u32 p, pe, pend;\n\t@p bra.uni B6_LOOP;\n\tB6_DONE:\n\tmov.b32 pe, pend;\n\tand.b32 t, %22, 65535;\n\tmad.lo.u32 pend, t, 16, %16;\n\tsetp.ge.u32 p, pe, pend;\n\t@p bra.uni B7_DONE;\n\tB7_LOOP:\n\tld.shared.v4.b32 {o, x, gl, gh}, [pe];\n\tadd.u32 a, o, %17;\n\tld.shared.v2.f64 {u, v}, [a];\n\tmov.b64 g, {gl, gh};\n\tfma.rn.f64 %14, u, g, %14;\n\tfma.rn.f64 %15, v, g, %15;\n\tadd.u32 pe, pe, 16;\n\tsetp.lt.u32 p, pe, pend;\n\t@p bra.uni B7_LOOP;\n\tB7_DONE:\n\tmov.b32 pe, pend;\n\t}"
-                 : "+d"(acc[0][0]), "+d"(acc[1][0]), "+d"(acc[0][1]), "+d"(acc[1][1]), "+d"(acc[0][2]), "+d"(acc[1][2]), "+d"(acc[0][3]), "+d"(acc[1][3]), "+d"(acc[0][4]), "+d"(acc[1][4]), "+d"(acc[0][5]), "+d"(acc[1][5]), "+d"(acc[0][6]), "+d"(acc[1][6]), "+d"(acc[0][7]), "+d"(acc[1][7])
-                 : "r"(sen), "r"(sx), "r"(bw[0]), "r"(bw[1]), "r"(bw[2]), "r"(bw[3]), "r"(bw[4])
-                 : "memory");
-}
-
-// one warp, one chunk, all 4 buckets, RPT = 2 (S tiles)
-__device__ __forceinline__ void chunk_s_2x4(double (&acc)[2][4], uint32_t sen, uint32_t sx, const uint32_t (&bw)[3]) {
-    asm volatile("{\n\t.reg .pred p;\n\t.reg .b32 o, x, gl, gh, a, t, pe, pend;\n\t.reg .f64 u, v, w, y, g;\n\tand.b32 t, %10, 65535;\n\tmad.lo.u32 pe, t, 16, %8;\n\tshr.u32 t, %10, 16;\n\tmad.lo.u32 pend, t, 16, %8;\n\tsetp.ge.u32 p, pe, pend;\n\t@p bra.uni B0_DONE;\n\tB0_LOOP:\n\tld.shared.v4.b32 {o, x, gl, gh}, [pe];\n\tadd.u32 a, o, %9;\n\tld.shared.v2.f64 {u, v}, [a];\n\tmov.b64 g, {gl, gh};\n\tfma.rn.f64 %0, u, g, %0;\n\tfma.rn.f64 %1, v, g, %1;\n\tadd.u32 pe, pe, 16;\n\tsetp.lt.u32 p, pe, pend;\n\t@p bra.uni B0_LOOP;\n\tB0_DONE:\n\tmov.b32 pe, pend;\n\tand.b32 t, %11, 65535;\n\tmad.lo.u32 pend, t, 16, %8;\n\tsetp.ge.u32 p, pe, pend;\n\t@p bra.uni B1_DONE;\n\tB1_LOOP:\n\tld.shared.v4.b32 {o, x, gl, gh}, [pe];\n\tadd.u32 a, o, %9;\n\tld.shared.v2.f64 {u, v}, [a];\n\tmov.b64 g, {gl, gh};\n\tfma.rn.f64 %2, u, g, %2;\n\tfma.rn.f64 %3, v, g, %3;\n\tadd.u32 pe, pe, 16;\n\tsetp.lt.u32 p, pe, pend;\n\t@p bra.uni B1_LOOP;\n\tB1_DONE:\n\tmov.b32 pe, pend;\n\tshr.u32 t, %11, 16;\n\tmad.lo.u32 pend, t, 16, %8;\n\tsetp.ge.u32 p, pe, pend;\n\t@p bra.uni B2_DONE;\n\tB2_LOOP:\n\tld.shared.v4.b32 {o, x, gl, gh}, [pe];\n\tadd.u32 a, o, %9;\n\tld.shared.v2.f64 {u, v}, [a];\n\tmov.b64 g, {gl, gh};\n\tfma.rn.f64 %4, u, g, %4;\n\tfma.rn.f64 %5, v, g, %5;\n\tadd.u32 pe, pe, 16;\n\tsetp.lt.u32 p, pe, pend;\n\t@p bra.uni B2_LOOP;\n\tB2_DONE:\n\tmov.b32 pe, pend;\n\tand.b32 t, %12, 65535;\n\tmad.lo.u32 pend, t, 16, %8;\n\tsetp.ge.u32 p, pe, pend;\n\t@p bra.uni B3_DONE;\n\tB3_LOOP:\n\tld.shared.v4.b32 {o, x, gl, gh}, [pe];\n\tadd.u32 a, o, %9;\n\tld.shared.v2.f64 {u, v}, [a];\n\tmov.b64 g, {gl, gh};\n\tfma.rn.f64 %6, u, g, %6;\n\tfma.rn.f64 %7, v, g, %7;\n\tadd.u32 pe, pe, 16;\n\tsetp.lt.u32 p, pe, pend;\n\t@p bra.uni B3_LOOP;\n\tB3_DONE:\n\tmov.b32 pe, pend;\n\t}"
-                 : "+d"(acc[0][0]), "+d"(acc[1][0]), "+d"(acc[0][1]), "+d"(acc[1][1]), "+d"(acc[0][2]), "+d"(acc[1][2]), "+d"(acc[0][3]), "+d"(acc[1][3])
-                 : "r"(sen), "r"(sx), "r"(bw[0]), "r"(bw[1]), "r"(bw[2])
-                 : "memory");
-}
-
-// one warp, one chunk, all 2 buckets, RPT = 4 (S tiles)
-__device__ __forceinline__ void chunk_s_4x2(double (&acc)[4][2], uint32_t sen, uint32_t sx, const uint32_t (&bw)[2]) {
-    asm volatile("{\n\t.reg .pred p;\n\t.reg .b32 o, x, gl, gh, a, t, pe, pend;\n\t.reg .f64 u, v, w, y, g;\n\tand.b32 t, %10, 65535;\n\tmad.lo.u32 pe, t, 16, %8;\n\tshr.u32 t, %10, 16;\n\tmad.lo.u32 pend, t, 16, %8;\n\tsetp.ge.u32 p, pe, pend;\n\t@p bra.uni B0_DONE;\n\tB0_LOOP:\n\tld.shared.v4.b32 {o, x, gl, gh}, [pe];\n\tadd.u32 a, o, %9;\n\tld.shared.v2.f64 {u, v}, [a];\n\tld.shared.v2.f64 {w, y}, [a+512];\n\tmov.b64 g, {gl, gh};\n\tfma.rn.f64 %0, u, g, %0;\n\tfma.rn.f64 %1, v, g, %1;\n\tfma.rn.f64 %2, w, g, %2;\n\tfma.rn.f64 %3, y, g, %3;\n\tadd.u32 pe, pe, 16;\n\tsetp.lt.u32 p, pe, pend;\n\t@p bra.uni B0_LOOP;\n\tB0_DONE:\n\tmov.b32 pe, pend;\n\tand.b32 t, %11, 65535;\n\tmad.lo.u32 pend, t, 16, %8;\n\tsetp.ge.u32 p, pe, pend;\n\t@p bra.uni B1_DONE;\n\tB1_LOOP:\n\tld.shared.v4.b32 {o, x, gl, gh}, [pe];\n\tadd.u32 a, o, %9;\n\tld.shared.v2.f64 {u, v}, [a];\n\tld.shared.v2.f64 {w, y}, [a+512];\n\tmov.b64 g, {gl, gh};\n\tfma.rn.f64 %4, u, g, %4;\n\tfma.rn.f64 %5, v, g, %5;\n\tfma.rn.f64 %6, w, g, %6;\n\tfma.rn.f64 %7, y, g, %7;\n\tadd.u32 pe, pe, 16;\n\tsetp.lt.u32 p, pe, pend;\n\t@p bra.uni B1_LOOP;\n\tB1_DONE:\n\tmov.b32 pe, pend;\n\t}"
-                 : "+d"(acc[0][0]), "+d"(acc[1][0]), "+d"(acc[2][0]), "+d"(acc[3][0]), "+d"(acc[0][1]), "+d"(acc[1][1]), "+d"(acc[2][1]), "+d"(acc[3][1])
-                 : "r"(sen), "r"(sx), "r"(bw[0]), "r"(bw[1])
-                 : "memory");
-}
-
-// one warp, one chunk, all 4 buckets, RPT = 4 (S tiles)
-__device__ __forceinline__ void chunk_s_4x4(double (&acc)[4][4], uint32_t sen, uint32_t sx, const uint32_t (&bw)[3]) {
-    asm volatile("{\n\t.reg .pred p;\n\t.reg .b32 o, x, gl, gh, a, t, pe, pend;\n\t.reg .f64 u, v, w, y, g;\n\tand.b32 t, %18, 65535;\n\tmad.lo.u32 pe, t, 16, %16;\n\tshr.u32 t, %18, 16;\n\tmad.lo.u32 pend, t, 16, %16;\n\tsetp.ge.u32 p, pe, pend;\n\t@p bra.uni B0_DONE;\n\tB0_LOOP:\n\tld.shared.v4.b32 {o, x, gl, gh}, [pe];\n\tadd.u32 a, o, %17;\n\tld.shared.v2.f64 {u, v}, [a];\n\tld.shared.v2.f64 {w, y}, [a+512];\n\tmov.b64 g, {gl, gh};\n\tfma.rn.f64 %0, u, g, %0;\n\tfma.rn.f64 %1, v, g, %1;\n\tfma.rn.f64 %2, w, g, %2;\n\tfma.rn.f64 %3, y, g, %3;\n\tadd.u32 pe, pe, 16;\n\tsetp.lt.u32 p, pe, pend;\n\t@p bra.uni B0_LOOP;\n\tB0_DONE:\n\tmov.b32 pe, pend;\n\tand.b32 t, %19, 65535;\n\tmad.lo.u32 pend, t, 16, %16;\n\tsetp.ge.u32 p, pe, pend;\n\t@p bra.uni B1_DONE;\n\tB1_LOOP:\n\tld.shared.v4.b32 {o, x, gl, gh}, [pe];\n\tadd.u32 a, o, %17;\n\tld.shared.v2.f64 {u, v}, [a];\n\tld.shared.v2.f64 {w, y}, [a+512];\n\tmov.b64 g, {gl, gh};\n\tfma.rn.f64 %4, u, g, %4;\n\tfma.rn.f64 %5, v, g, %5;\n\tfma.rn.f64 %6, w, g, %6;\n\tfma.rn.f64 %7, y, g, %7;\n\tadd.u32 pe, pe, 16;\n\tsetp.lt.u32 p, pe, pend;\n\t@p bra.uni B1_LOOP;\n\tB1_DONE:\n\tmov.b32 pe, pend;\n\tshr.u32 t, %19, 16;\n\tmad.lo.u32 pend, t, 16, %16;\n\tsetp.ge.u32 p, pe, pend;\n\t@p bra.uni B2_DONE;\n\tB2_LOOP:\n\tld.shared.v4.b32 {o, x, gl, gh}, [pe];\n\tadd.u32 a, o, %17;\n\tld.shared.v2.f64 {u, v}, [a];\n\tld.shared.v2.f64 {w, y}, [a+512];\n\tmov.b64 g, {gl, gh};\n\tfma.rn.f64 %8, u, g, %8;\n\tfma.rn.f64 %9, v, g, %9;\n\tfma.rn.f64 %10, w, g, %10;\n\tfma.rn.f64 %11, y, g, %11;\n\tadd.u32 pe, pe, 16;\n\tsetp.lt.u32 p, pe, pend;\n\t@p bra.uni B2_LOOP;\n\tB2_DONE:\n\tmov.b32 pe, pend;\n\tand.b32 t, %20, 65535;\n\tmad.lo.u32 pend, t, 16, %16;\n\tsetp.ge.u32 p, pe, pend;\n\t@p bra.uni B3_DONE;\n\tB3_LOOP:\n\tld.shared.v4.b32 {o, x, gl, gh}, [pe];\n\tadd.u32 a, o, %17;\n\tld.shared.v2.f64 {u, v}, [a];\n\tld.shared.v2.f64 {w, y}, [a+512];\n\tmov.b64 g, {gl, gh};\n\tfma.rn.f64 %12, u, g, %12;\n\tfma.rn.f64 %13, v, g, %13;\n\tfma.rn.f64 %14, w, g, %14;\n\tfma.rn.f64 %15, y, g, %15;\n\tadd.u32 pe, pe, 16;\n\tsetp.lt.u32 p, pe, pend;\n\t@p bra.uni B3_LOOP;\n\tB3_DONE:\n\tmov.b32 pe, pend;\n\t}"
-                 : "+d"(acc[0][0]), "+d"(acc[1][0]), "+d"(acc[2][0]), "+d"(acc[3][0]), "+d"(acc[0][1]), "+d"(acc[1][1]), "+d"(acc[2][1]), "+d"(acc[3][1]), "+d"(acc[0][2]), "+d"(acc[1][2]), "+d"(acc[2][2]), "+d"(acc[3][2]), "+d"(acc[0][3]), "+d"(acc[1][3]), "+d"(acc[2][3]), "+d"(acc[3][3])
-                 : "r"(sen), "r"(sx), "r"(bw[0]), "r"(bw[1]), "r"(bw[2])
-                 : "memory");
-}
-
-// one warp, one chunk, all 16 buckets, RPT = 2 (S tiles)
-__device__ __forceinline__ void chunk_s_2x16(double (&acc)[2][16], uint32_t sen, uint32_t sx, const uint32_t (&bw)[9]) {
-    asm volatile("{\n\t.reg .pred p;\n\t.reg .b32 o, x, gl, gh, a, t, pe, pend;\n\t.reg .f64 u, v, w, y, g;\n\tand.b32 t, %34, 65535;\n\tmad.lo.u32 pe, t, 16, %32;\n\tshr.u32 t, %34, 16;\n\tmad.lo.u32 pend, t, 16, %32;\n\tsetp.ge.u32 p, pe, pend;\n\t@p bra.uni B0_DONE;\n\tB0_LOOP:\n\tld.shared.v4.b32 {o, x, gl, gh}, [pe];\n\tadd.u32 a, o, %33;\n\tld.shared.v2.f64 {u, v}, [a];\n\tmov.b64 g, {gl, gh};\n\tfma.rn.f64 %0, u, g, %0;\n\tfma.rn.f64 %1, v, g, %1;\n\tadd.u32 pe, pe, 16;\n\tsetp.lt.u32 p, pe, pend;\n\t@p bra.uni B0_LOOP;\n\tB0_DONE:\n\tmov.b32 pe, pend;\n\tand.b32 t, %35, 65535;\n\tmad.lo.u32 pend, t, 16, %32;\n\tsetp.ge.u32 p, pe, pend;\n\t@p bra.uni B1_DONE;\n\tB1_LOOP:\n\tld.shared.v4.b32 {o, x, gl, gh}, [pe];\n\tadd.u32 a, o, %33;\n\tld.shared.v2.f64 {u, v}, [a];\n\tmov.b64 g, {gl, gh};\n\tfma.rn.f64 %2, u, g, %2;\n\tfma.rn.f64 %3, v, g, %3;\n\tadd.u32 pe, pe, 16;\n\tsetp.lt.u32 p, pe, pend;\n\t@p bra.uni B1_LOOP;\n\tB1_DONE:\n\tmov.b32 pe, pend;\n\tshr.u32 t, %35, 16;\n\tmad.lo.u32 pend, t, 16, %32;\n\tsetp.ge.u32 p, pe, pend;\n\t@p bra.uni B2_DONE;\n\tB2_LOOP:\n\tld.shared.v4.b32 {o, x, gl, gh}, [pe];\n\tadd.u32 a, o, %33;\n\tld.shared.v2.f64 {u, v}, [a];\n\tmov.b64 g, {gl, gh};\n\tfma.rn.f64 %4, u, g, %4;\n\tfma.rn.f64 %5, v, g, %5;\n\tadd.u32 pe, pe, 16;\n\tsetp.lt.u32 p, pe, pend;\n\t@p bra.uni B2_LOOP;\n\tB2_DONE:\n\tmov.b32 pe, pend;\n\tand.b32 t, %36, 65535;\n\tmad.lo.u32 pend, t, 16, %32;\n\tsetp.ge.u32 p, pe, pend;\n\t@p bra.uni B3_DONE;\n\tB3_LOOP:\n\tld.shared.v4.b32 {o, x, gl, gh}, [pe];\n\tadd.u32 a, o, %33;\n\tld.shared.v2.f64 {u, v}, [a];\n\tmov.b64 g, {gl, gh};\n\tfma.rn.f64 %6, u, g, %6;\n\tfma.rn.f64 %7, v, g, %7;\n\tadd.u32 pe, pe, 16;\n\tsetp.lt.u32 p, pe, pend;\n\t@p bra.uni B3_LOOP;\n\tB3_DONE:\n\tmov.b32 pe, pend;\n\tshr.u32 t, %36, 16;\n\tmad.lo.u32 pend, t, 16, %32;\n\tsetp.ge.u32 p, pe, pend;\n\t@p bra.uni B4_DONE;\n\tB4_LOOP:\n\tld.shared.v4.b32 {o, x, gl, gh}, [pe];\n\tadd.u32 a, o, %33;\n\tld.shared.v2.f64 {u, v}, [a];\n\tmov.b64 g, {gl, gh};\n\tfma.rn.f64 %8, u, g, %8;\n\tfma.rn.f64 %9, v, g, %9;\n\tadd.u32 pe, pe, 16;\n\tsetp.lt.u32 p, pe, pend;\n\t@p bra.uni B4_LOOP;\n\tB4_DONE:\n\tmov.b32 pe, pend;\n\tand.b32 t, %37, 65535;\n\tmad.lo.u32 pend, t, 16, %32;\n\tsetp.ge.u32 p, pe, pend;\n\t@p bra.uni B5_DONE;\n\tB5_LOOP:\n\tld.shared.v4.b32 {o, x, gl, gh}, [pe];\n\tadd.u32 a, o, %33;\n\tld.shared.v2.f64 {u, v}, [a];\n\tmov.b64 g, {gl, gh};\n\tfma.rn.f64 %10, u, g, %10;\n\tfma.rn.f64 %11, v, g, %11;\n\tadd.u32 pe, pe, 16;\n\tsetp.lt.u32 p, pe, pend;\n\t@p bra.uni B5_LOOP;\n\tB5_DONE:\n\tmov.b32 pe, pend;\n\tshr.u32 t, %37, 16;\n\tmad.lo.u32 pend, t, 16, %32;\n\tsetp.ge.u32 p, pe, pend;\n\t@p bra.uni B6_DONE;\n\tB6_LOOP:\n\tld.shared.v4.b32 {o, x, gl, gh}, [pe];\n\tadd.u32 a, o, %33;\n\tld.shared.v2.f64 {u, v}, [a];\n\tmov.b64 g, {gl, gh};\n\tfma.rn.f64 %12, u, g, %12;\n\tfma.rn.f64 %13, v, g, %13;\n\tadd.u32 pe, pe, 16;\n\tsetp.lt.u32 p, pe, pend;\n\t@p bra.uni B6_LOOP;\n\tB6_DONE:\n\tmov.b32 pe, pend;\n\tand.b32 t, %38, 65535;\n\tmad.lo.u32 pend, t, 16, %32;\n\tsetp.ge.u32 p, pe, pend;\n\t@p bra.uni B7_DONE;\n\tB7_LOOP:\n\tld.shared.v4.b32 {o, x, gl, gh}, [pe];\n\tadd.u32 a, o, %33;\n\tld.shared.v2.f64 {u, v}, [a];\n\tmov.b64 g, {gl, gh};\n\tfma.rn.f64 %14, u, g, %14;\n\tfma.rn.f64 %15, v, g, %15;\n\tadd.u32 pe, pe, 16;\n\tsetp.lt.u32 p, pe, pend;\n\t@p bra.uni B7_LOOP;\n\tB7_DONE:\n\tmov.b32 pe, pend;\n\tshr.u32 t, %38, 16;\n\tmad.lo.u32 pend, t, 16, %32;\n\tsetp.ge.u32 p, pe, pend;\n\t@p bra.uni B8_DONE;\n\tB8_LOOP:\n\tld.shared.v4.b32 {o, x, gl, gh}, [pe];\n\tadd.u32 a, o, %33;\n\tld.shared.v2.f64 {u, v}, [a];\n\tmov.b64 g, {gl, gh};\n\tfma.rn.f64 %16, u, g, %16;\n\tfma.rn.f64 %17, v, g, %17;\n\tadd.u32 pe, pe, 16;\n\tsetp.lt.u32 p, pe, pend;\n\t@p bra.uni B8_LOOP;\n\tB8_DONE:\n\tmov.b32 pe, pend;\n\tand.b32 t, %39, 65535;\n\tmad.lo.u32 pend, t, 16, %32;\n\tsetp.ge.u32 p, pe, pend;\n\t@p bra.uni B9_DONE;\n\tB9_LOOP:\n\tld.shared.v4.b32 {o, x, gl, gh}, [pe];\n\tadd.u32 a, o, %33;\n\tld.shared.v2.f64 {u, v}, [a];\n\tmov.b64 g, {gl, gh};\n\tfma.rn.f64 %18, u, g, %18;\n\tfma.rn.f64 %19, v, g, %19;\n\tadd.u32 pe, pe, 16;\n\tsetp.lt.u32 p, pe, pend;\n\t@p bra.uni B9_LOOP;\n\tB9_DONE:\n\tmov.b32 pe, pend;\n\tshr.u32 t, %39, 16;\n\tmad.lo.u32 pend, t, 16, %32;\n\tsetp.ge.u32 p, pe, pend;\n\t@p bra.uni B10_DONE;\n\tB10_LOOP:\n\tld.shared.v4.b32 {o, x, gl, gh}, [pe];\n\tadd.u32 a, o, %33;\n\tld.shared.v2.f64 {u, v}, [a];\n\tmov.b64 g, {gl, gh};\n\tfma.rn.f64 %20, u, g, %20;\n\tfma.rn.f64 %21, v, g, %21;\n\tadd.u32 pe, pe, 16;\n\tsetp.lt.u32 p, pe, pend;\n\t@p bra.uni B10_LOOP;\n\tB10_DONE:\n\tmov.b32 pe, pend;\n\tand.b32 t, %40, 65535;\n\tmad.lo.u32 pend, t, 16, %32;\n\tsetp.ge.u32 p, pe, pend;\n\t@p bra.uni B11_DONE;\n\tB11_LOOP:\n\tld.shared.v4.b32 {o, x, gl, gh}, [pe];\n\tadd.u32 a, o, %33;\n\tld.shared.v2.f64 {u, v}, [a];\n\tmov.b64 g, {gl, gh};\n\tfma.rn.f64 %22, u, g, %22;\n\tfma.rn.f64 %23, v, g, %23;\n\tadd.u32 pe, pe, 16;\n\tsetp.lt.u32 p, pe, pend;\n\t@p bra.uni B11_LOOP;\n\tB11_DONE:\n\tmov.b32 pe, pend;\n\tshr.u32 t, %40, 16;\n\tmad.lo.u32 pend, t, 16, %32;\n\tsetp.ge.u32 p, pe, pend;\n\t@p bra.uni B12_DONE;\n\tB12_LOOP:\n\tld.shared.v4.b32 {o, x, gl, gh}, [pe];\n\tadd.u32 a, o, %33;\n\tld.shared.v2.f64 {u, v}, [a];\n\tmov.b64 g, {gl, gh};\n\tfma.rn.f64 %24, u, g, %24;\n\tfma.rn.f64 %25, v, g, %25;\n\tadd.u32 pe, pe, 16;\n\tsetp.lt.u32 p, pe, pend;\n\t@p bra.uni B12_LOOP;\n\tB12_DONE:\n\tmov.b32 pe, pend;\n\tand.b32 t, %41, 65535;\n\tmad.lo.u32 pend, t, 16, %32;\n\tsetp.ge.u32 p, pe, pend;\n\t@p bra.uni B13_DONE;\n\tB13_LOOP:\n\tld.shared.v4.b32 {o, x, gl, gh}, [pe];\n\tadd.u32 a, o, %33;\n\tld.shared.v2.f64 {u, v}, [a];\n\tmov.b64 g, {gl, gh};\n\tfma.rn.f64 %26, u, g, %26;\n\tfma.rn.f64 %27, v, g, %27;\n\tadd.u32 pe, pe, 16;\n\tsetp.lt.u32 p, pe, pend;\n\t@p bra.uni B13_LOOP;\n\tB13_DONE:\n\tmov.b32 pe, pend;\n\tshr.u32 t, %41, 16;\n\tmad.lo.u32 pend, t, 16, %32;\n\tsetp.ge.u32 p, pe, pend;\n\t@p bra.uni B14_DONE;\n\tB14_LOOP:\n\tld.shared.v4.b32 {o, x, gl, gh}, [pe];\n\tadd.u32 a, o, %33;\n\tld.shared.v2.f64 {u, v}, [a];\n\tmov.b64 g, {gl, gh};\n\tfma.rn.f64 %28, u, g, %28;\n\tfma.rn.f64 %29, v, g, %29;\n\tadd.u32 pe, pe, 16;\n\tsetp.lt.u32 p, pe, pend;\n\t@p bra.uni B14_LOOP;\n\tB14_DONE:\n\tmov.b32 pe, pend;\n\tand.b32 t, %42, 65535;\n\tmad.lo.u32 pend, t, 16, %32;\n\tsetp.ge.u32 p, pe, pend;\n\t@p bra.uni B15_DONE;\n\tB15_LOOP:\n\tld.shared.v4.b32 {o, x, gl, gh}, [pe];\n\tadd.u32 a, o, %33;\n\tld.shared.v2.f64 {u, v}, [a];\n\tmov.b64 g, {gl, gh};\n\tfma.rn.f64 %30, u, g, %30;\n\tfma.rn.f64 %31, v, g, %31;\n\tadd.u32 pe, pe, 16;\n\tsetp.lt.u32 p, pe, pend;\n\t@p bra.uni B15_LOOP;\n\tB15_DONE:\n\tmov.b32 pe, pend;\n\t}"
-                 : "+d"(acc[0][0]), "+d"(acc[1][0]), "+d"(acc[0][1]), "+d"(acc[1][1]), "+d"(acc[0][2]), "+d"(acc[1][2]), "+d"(acc[0][3]), "+d"(acc[1][3]), "+d"(acc[0][4]), "+d"(acc[1][4]), "+d"(acc[0][5]), "+d"(acc[1][5]), "+d"(acc[0][6]), "+d"(acc[1][6]), "+d"(acc[0][7]), "+d"(acc[1][7]), "+d"(acc[0][8]), "+d"(acc[1][8]), "+d"(acc[0][9]), "+d"(acc[1][9]), "+d"(acc[0][10]), "+d"(acc[1][10]), "+d"(acc[0][11]), "+d"(acc[1][11]), "+d"(acc[0][12]), "+d"(acc[1][12]), "+d"(acc[0][13]), "+d"(acc[1][13]), "+d"(acc[0][14]), "+d"(acc[1][14]), "+d"(acc[0][15]), "+d"(acc[1][15])
-                 : "r"(sen), "r"(sx), "r"(bw[0]), "r"(bw[1]), "r"(bw[2]), "r"(bw[3]), "r"(bw[4]), "r"(bw[5]), "r"(bw[6]), "r"(bw[7]), "r"(bw[8])
-                 : "memory");
-}
-
-// one warp, one chunk, all 8 buckets, RPT = 4 (S tiles)
-__device__ __forceinline__ void chunk_s_4x8(double (&acc)[4][8], uint32_t sen, uint32_t sx, const uint32_t (&bw)[5]) {
-    asm volatile("{\n\t.reg .pred p;\n\t.reg .b32 o, x, gl, gh, a, t, pe, pend;\n\t.reg .f64 u, v, w, y, g;\n\tand.b32 t, %34, 65535;\n\tmad.lo.u32 pe, t, 16, %32;\n\tshr.u32 t, %34, 16;\n\tmad.lo.u32 pend, t, 16, %32;\n\tsetp.ge.u32 p, pe, pend;\n\t@p bra.uni B0_DONE;\n\tB0_LOOP:\n\tld.shared.v4.b32 {o, x, gl, gh}, [pe];\n\tadd.u32 a, o, %33;\n\tld.shared.v2.f64 {u, v}, [a];\n\tld.shared.v2.f64 {w, y}, [a+512];\n\tmov.b64 g, {gl, gh};\n\tfma.rn.f64 %0, u, g, %0;\n\tfma.rn.f64 %1, v, g, %1;\n\tfma.rn.f64 %2, w, g, %2;\n\tfma.rn.f64 %3, y, g, %3;\n\tadd.u32 pe, pe, 16;\n\tsetp.lt.u32 p, pe, pend;\n\t@p bra.uni B0_LOOP;\n\tB0_DONE:\n\tmov.b32 pe, pend;\n\tand.b32 t, %35, 65535;\n\tmad.lo.u32 pend, t, 16, %32;\n\tsetp.ge.u32 p, pe, pend;\n\t@p bra.uni B1_DONE;\n\tB1_LOOP:\n\tld.shared.v4.b32 {o, x, gl, gh}, [pe];\n\tadd.u32 a, o, %33;\n\tld.shared.v2.f64 {u, v}, [a];\n\tld.shared.v2.f64 {w, y}, [a+512];\n\tmov.b64 g, {gl, gh};\n\tfma.rn.f64 %4, u, g, %4;\n\tfma.rn.f64 %5, v, g, %5;\n\tfma.rn.f64 %6, w, g, %6;\n\tfma.rn.f64 %7, y, g, %7;\n\tadd.u32 pe, pe, 16;\n\tsetp.lt.u32 p, pe, pend;\n\t@p bra.uni B1_LOOP;\n\tB1_DONE:\n\tmov.b32 pe, pend;\n\tshr.u32 t, %35, 16;\n\tmad.lo.u32 pend, t, 16, %32;\n\tsetp.ge.u32 p, pe, pend;\n\t@p bra.uni B2_DONE;\n\tB2_LOOP:\n\tld.shared.v4.b32 {o, x, gl, gh}, [pe];\n\tadd.u32 a, o, %33;\n\tld.shared.v2.f64 {u, v}, [a];\n\tld.shared.v2.f64 {w, y}, [a+512];\n\tmov.b64 g, {gl, gh};\n\tfma.rn.f64 %8, u, g, %8;\n\tfma.rn.f64 %9, v, g, %9;\n\tfma.rn.f64 %10, w, g, %10;\n\tfma.rn.f64 %11, y, g, %11;\n\tadd.u32 pe, pe, 16;\n\tsetp.lt.u32 p, pe, pend;\n\t@p bra.uni B2_LOOP;\n\tB2_DONE:\n\tmov.b32 pe, pend;\n\tand.b32 t, %36, 65535;\n\tmad.lo.u32 pend, t, 16, %32;\n\tsetp.ge.u32 p, pe, pend;\n\t@p bra.uni B3_DONE;\n\tB3_LOOP:\n\tld.shared.v4.b32 {o, x, gl, gh}, [pe];\n\tadd.u32 a, o, %33;\n\tld.shared.v2.f64 {u, v}, [a];\n\tld.shared.v2.f64 {w, y}, [a+512];\n\tmov.b64 g, {gl, gh};\n\tfma.rn.f64 %12, u, g, %12;\n\tfma.rn.f64 %13, v, g, %13;\n\tfma.rn.f64 %14, w, g, %14;\n\tfma.rn.f64 %15, y, g, %15;\n\tadd.u32 pe, pe, 16;\n\tsetp.lt.u32 p, pe, pend;\n\t@p bra.uni B3_LOOP;\n\tB3_DONE:\n\tmov.b32 pe, pend;\n\tshr.u32 t, %36, 16;\n\tmad.lo.u32 pend, t, 16, %32;\n\tsetp.ge.u32 p, pe, pend;\n\t@p bra.uni B4_DONE;\n\tB4_LOOP:\n\tld.shared.v4.b32 {o, x, gl, gh}, [pe];\n\tadd.u32 a, o, %33;\n\tld.shared.v2.f64 {u, v}, [a];\n\tld.shared.v2.f64 {w, y}, [a+512];\n\tmov.b64 g, {gl, gh};\n\tfma.rn.f64 %16, u, g, %16;\n\tfma.rn.f64 %17, v, g, %17;\n\tfma.rn.f64 %18, w, g, %18;\n\tfma.rn.f64 %19, y, g, %19;\n\tadd.u32 pe, pe, 16;\n\tsetp.lt.u32 p, pe, pend;\n\t@p bra.uni B4_LOOP;\n\tB4_DONE:\n\tmov.b32 pe, pend;\n\tand.b32 t, %37, 65535;\n\tmad.lo.u32 pend, t, 16, %32;\n\tsetp.ge.u32 p, pe, pend;\n\t@p bra.uni B5_DONE;\n\tB5_LOOP:\n\tld.shared.v4.b32 {o, x, gl, gh}, [pe];\n\tadd.u32 a, o, %33;\n\tld.shared.v2.f64 {u, v}, [a];\n\tld.shared.v2.f64 {w, y}, [a+512];\n\tmov.b64 g, {gl, gh};\n\tfma.rn.f64 %20, u, g, %20;\n\tfma.rn.f64 %21, v, g, %21;\n\tfma.rn.f64 %22, w, g, %22;\n\tfma.rn.f64 %23, y, g, %23;\n\tadd.u32 pe, pe, 16;\n\tsetp.lt.u32 p, pe, pend;\n\t@p bra.uni B5_LOOP;\n\tB5_DONE:\n\tmov.b32 pe, pend;\n\tshr.u32 t, %37, 16;\n\tmad.lo.u32 pend, t, 16, %32;\n\tsetp.ge.u32 p, pe, pend;\n\t@p bra.uni B6_DONE;\n\tB6_LOOP:\n\tld.shared.v4.b32 {o, x, gl, gh}, [pe];\n\tadd.u32 a, o, %33;\n\tld.shared.v2.f64 {u, v}, [a];\n\tld.shared.v2.f64 {w, y}, [a+512];\n\tmov.b64 g, {gl, gh};\n\tfma.rn.f64 %24, u, g, %24;\n\tfma.rn.f64 %25, v, g, %25;\n\tfma.rn.f64 %26, w, g, %26;\n\tfma.rn.f64 %27, y, g, %27;\n\tadd.u32 pe, pe, 16;\n\tsetp.lt.u32 p, pe, pend;\n\t@p bra.uni B6_LOOP;\n\tB6_DONE:\n\tmov.b32 pe, pend;\n\tand.b32 t, %38, 65535;\n\tmad.lo.u32 pend, t, 16, %32;\n\tsetp.ge.u32 p, pe, pend;\n\t@p bra.uni B7_DONE;\n\tB7_LOOP:\n\tld.shared.v4.b32 {o, x, gl, gh}, [pe];\n\tadd.u32 a, o, %33;\n\tld.shared.v2.f64 {u, v}, [a];\n\tld.shared.v2.f64 {w, y}, [a+512];\n\tmov.b64 g, {gl, gh};\n\tfma.rn.f64 %28, u, g, %28;\n\tfma.rn.f64 %29, v, g, %29;\n\tfma.rn.f64 %30, w, g, %30;\n\tfma.rn.f64 %31, y, g, %31;\n\tadd.u32 pe, pe, 16;\n\tsetp.lt.u32 p, pe, pend;\n\t@p bra.uni B7_LOOP;\n\tB7_DONE:\n\tmov.b32 pe, pend;\n\t}"
-                 : "+d"(acc[0][0]), "+d"(acc[1][0]), "+d"(acc[2][0]), "+d"(acc[3][0]), "+d"(acc[0][1]), "+d"(acc[1][1]), "+d"(acc[2][1]), "+d"(acc[3][1]), "+d"(acc[0][2]), "+d"(acc[1][2]), "+d"(acc[2][2]), "+d"(acc[3][2]), "+d"(acc[0][3]), "+d"(acc[1][3]), "+d"(acc[2][3]), "+d"(acc[3][3]), "+d"(acc[0][4]), "+d"(acc[1][4]), "+d"(acc[2][4]), "+d"(acc[3][4]), "+d"(acc[0][5]), "+d"(acc[1][5]), "+d"(acc[2][5]), "+d"(acc[3][5]), "+d"(acc[0][6]), "+d"(acc[1][6]), "+d"(acc[2][6]), "+d"(acc[3][6]), "+d"(acc[0][7]), "+d"(acc[1][7]), "+d"(acc[2][7]), "+d"(acc[3][7])
-                 : "r"(sen), "r"(sx), "r"(bw[0]), "r"(bw[1]), "r"(bw[2]), "r"(bw[3]), "r"(bw[4])
-                 : "memory");
-}
-
-// RPT = 1 variants (32-row tiles): lane l owns row l.
-__device__ __forceinline__ void chunk_s_1x16(double (&acc)[1][16], uint32_t sen, uint32_t sx, const uint32_t (&bw)[9]) {
-    asm volatile("{\n\t.reg .pred p;\n\t.reg .b32 o, x, gl, gh, a, t, pe, pend;\n\t.reg .f64 u, g;\n\tand.b32 t, %18, 65535;\n\tmad.lo.u32 pe, t, 16, %16;\n\tshr.u32 t, %18, 16;\n\tmad.lo.u32 pend, t, 16, %16;\n\tsetp.ge.u32 p, pe, pend;\n\t@p bra.uni B0_DONE;\n\tB0_LOOP:\n\tld.shared.v4.b32 {o, x, gl, gh}, [pe];\n\tadd.u32 a, o, %17;\n\tld.shared.f64 u, [a];\n\tmov.b64 g, {gl, gh};\n\tfma.rn.f64 %0, u, g, %0;\n\tadd.u32 pe, pe, 16;\n\tsetp.lt.u32 p, pe, pend;\n\t@p bra.uni B0_LOOP;\n\tB0_DONE:\n\tmov.b32 pe, pend;\n\tand.b32 t, %19, 65535;\n\tmad.lo.u32 pend, t, 16, %16;\n\tsetp.ge.u32 p, pe, pend;\n\t@p bra.uni B1_DONE;\n\tB1_LOOP:\n\tld.shared.v4.b32 {o, x, gl, gh}, [pe];\n\tadd.u32 a, o, %17;\n\tld.shared.f64 u, [a];\n\tmov.b64 g, {gl, gh};\n\tfma.rn.f64 %1, u, g, %1;\n\tadd.u32 pe, pe, 16;\n\tsetp.lt.u32 p, pe, pend;\n\t@p bra.uni B1_LOOP;\n\tB1_DONE:\n\tmov.b32 pe, pend;\n\tshr.u32 t, %19, 16;\n\tmad.lo.u32 pend, t, 16, %16;\n\tsetp.ge.u32 p, pe, pend;\n\t@p bra.uni B2_DONE;\n\tB2_LOOP:\n\tld.shared.v4.b32 {o, x, gl, gh}, [pe];\n\tadd.u32 a, o, %17;\n\tld.shared.f64 u, [a];\n\tmov.b64 g, {gl, gh};\n\tfma.rn.f64 %2, u, g, %2;\n\tadd.u32 pe, pe, 16;\n\tsetp.lt.u32 p, pe, pend;\n\t@p bra.uni B2_LOOP;\n\tB2_DONE:\n\tmov.b32 pe, pend;\n\tand.b32 t, %20, 65535;\n\tmad.lo.u32 pend, t, 16, %16;\n\tsetp.ge.u32 p, pe, pend;\n\t@p bra.uni B3_DONE;\n\tB3_LOOP:\n\tld.shared.v4.b32 {o, x, gl, gh}, [pe];\n\tadd.u32 a, o, %17;\n\tld.shared.f64 u, [a];\n\tmov.b64 g, {gl, gh};\n\tfma.rn.f64 %3, u, g, %3;\n\tadd.u32 pe, pe, 16;\n\tsetp.lt.u32 p, pe, pend;\n\t@p bra.uni B3_LOOP;\n\tB3_DONE:\n\tmov.b32 pe, pend;\n\tshr.u32 t, %20, 16;\n\tmad.lo.u32 pend, t, 16, %16;\n\tsetp.ge.u32 p, pe, pend;\n\t@p bra.uni B4_DONE;\n\tB4_LOOP:\n\tld.shared.v4.b32 {o, x, gl, gh}, [pe];\n\tadd.u32 a, o, %17;\n\tld.shared.f64 u, [a];\n\tmov.b64 g, {gl, gh};\n\tfma.rn.f64 %4, u, g, %4;\n\tadd.u32 pe, pe, 16;\n\tsetp.lt.u32 p, pe, pend;\n\t@p bra.uni B4_LOOP;\n\tB4_DONE:\n\tmov.b32 pe, pend;\n\tand.b32 t, %21, 65535;\n\tmad.lo.u32 pend, t, 16, %16;\n\tsetp.ge.u32 p, pe, pend;\n\t@p bra.uni B5_DONE;\n\tB5_LOOP:\n\tld.shared.v4.b32 {o, x, gl, gh}, [pe];\n\tadd.u32 a, o, %17;\n\tld.shared.f64 u, [a];\n\tmov.b64 g, {gl, gh};\n\tfma.rn.f64 %5, u, g, %5;\n\tadd.u32 pe, pe, 16;\n\tsetp.lt.u32 p, pe, pend;\n\t@p bra.uni B5_LOOP;\n\tB5_DONE:\n\tmov.b32 pe, pend;\n\tshr.u32 t, %21, 16;\n\tmad.lo.u32 pend, t, 16, %16;\n\tsetp.ge.u32 p, pe, pend;\n\t@p bra.uni B6_DONE;\n\tB6_LOOP:\n\tld.shared.v4.b32 {o, x, gl, gh}, [pe];\n\tadd.u32 a, o, %17;\n\tld.shared.f64 u, [a];\n\tmov.b64 g, {gl, gh};\n\tfma.rn.f64 %6, u, g, %6;\n\tadd.u32 pe, pe, 16;\n\tsetp.lt.u32 p, pe, pend;\n\t@p bra.uni B6_LOOP;\n\tB6_DONE:\n\tmov.b32 pe, pend;\n\tand.b32 t, %22, 65535;\n\tmad.lo.u32 pend, t, 16, %16;\n\tsetp.ge.u32 p, pe, pend;\n\t@p bra.uni B7_DONE;\n\tB7_LOOP:\n\tld.shared.v4.b32 {o, x, gl, gh}, [pe];\n\tadd.u32 a, o, %17;\n\tld.shared.f64 u, [a];\n\tmov.b64 g, {gl, gh};\n\tfma.rn.f64 %7, u, g, %7;\n\tadd.u32 pe, pe, 16;\n\tsetp.lt.u32 p, pe, pend;\n\t@p bra.uni B7_LOOP;\n\tB7_DONE:\n\tmov.b32 pe, pend;\n\tshr.u32 t, %22, 16;\n\tmad.lo.u32 pend, t, 16, %16;\n\tsetp.ge.u32 p, pe, pend;\n\t@p bra.uni B8_DONE;\n\tB8_LOOP:\n\tld.shared.v4.b32 {o, x, gl, gh}, [pe];\n\tadd.u32 a, o, %17;\n\tld.shared.f64 u, [a];\n\tmov.b64 g, {gl, gh};\n\tfma.rn.f64 %8, u, g, %8;\n\tadd.u32 pe, pe, 16;\n\tsetp.lt.u32 p, pe, pend;\n\t@p bra.uni B8_LOOP;\n\tB8_DONE:\n\tmov.b32 pe, pend;\n\tand.b32 t, %23, 65535;\n\tmad.lo.u32 pend, t, 16, %16;\n\tsetp.ge.u32 p, pe, pend;\n\t@p bra.uni B9_DONE;\n\tB9_LOOP:\n\tld.shared.v4.b32 {o, x, gl, gh}, [pe];\n\tadd.u32 a, o, %17;\n\tld.shared.f64 u, [a];\n\tmov.b64 g, {gl, gh};\n\tfma.rn.f64 %9, u, g, %9;\n\tadd.u32 pe, pe, 16;\n\tsetp.lt.u32 p, pe, pend;\n\t@p bra.uni B9_LOOP;\n\tB9_DONE:\n\tmov.b32 pe, pend;\n\tshr.u32 t, %23, 16;\n\tmad.lo.u32 pend, t, 16, %16;\n\tsetp.ge.u32 p, pe, pend;\n\t@p bra.uni B10_DONE;\n\tB10_LOOP:\n\tld.shared.v4.b32 {o, x, gl, gh}, [pe];\n\tadd.u32 a, o, %17;\n\tld.shared.f64 u, [a];\n\tmov.b64 g, {gl, gh};\n\tfma.rn.f64 %10, u, g, %10;\n\tadd.u32 pe, pe, 16;\n\tsetp.lt.u32 p, pe, pend;\n\t@p bra.uni B10_LOOP;\n\tB10_DONE:\n\tmov.b32 pe, pend;\n\tand.b32 t, %24, 65535;\n\tmad.lo.u32 pend, t, 16, %16;\n\tsetp.ge.u32 p, pe, pend;\n\t@p bra.uni B11_DONE;\n\tB11_LOOP:\n\tld.shared.v4.b32 {o, x, gl, gh}, [pe];\n\tadd.u32 a, o, %17;\n\tld.shared.f64 u, [a];\n\tmov.b64 g, {gl, gh};\n\tfma.rn.f64 %11, u, g, %11;\n\tadd.u32 pe, pe, 16;\n\tsetp.lt.u32 p, pe, pend;\n\t@p bra.uni B11_LOOP;\n\tB11_DONE:\n\tmov.b32 pe, pend;\n\tshr.u32 t, %24, 16;\n\tmad.lo.u32 pend, t, 16, %16;\n\tsetp.ge.u32 p, pe, pend;\n\t@p bra.uni B12_DONE;\n\tB12_LOOP:\n\tld.shared.v4.b32 {o, x, gl, gh}, [pe];\n\tadd.u32 a, o, %17;\n\tld.shared.f64 u, [a];\n\tmov.b64 g, {gl, gh};\n\tfma.rn.f64 %12, u, g, %12;\n\tadd.u32 pe, pe, 16;\n\tsetp.lt.u32 p, pe, pend;\n\t@p bra.uni B12_LOOP;\n\tB12_DONE:\n\tmov.b32 pe, pend;\n\tand.b32 t, %25, 65535;\n\tmad.lo.u32 pend, t, 16, %16;\n\tsetp.ge.u32 p, pe, pend;\n\t@p bra.uni B13_DONE;\n\tB13_LOOP:\n\tld.shared.v4.b32 {o, x, gl, gh}, [pe];\n\tadd.u32 a, o, %17;\n\tld.shared.f64 u, [a];\n\tmov.b64 g, {gl, gh};\n\tfma.rn.f64 %13, u, g, %13;\n\tadd.u32 pe, pe, 16;\n\tsetp.lt.u32 p, pe, pend;\n\t@p bra.uni B13_LOOP;\n\tB13_DONE:\n\tmov.b32 pe, pend;\n\tshr.u32 t, %25, 16;\n\tmad.lo.u32 pend, t, 16, %16;\n\tsetp.ge.u32 p, pe, pend;\n\t@p bra.uni B14_DONE;\n\tB14_LOOP:\n\tld.shared.v4.b32 {o, x, gl, gh}, [pe];\n\tadd.u32 a, o, %17;\n\tld.shared.f64 u, [a];\n\tmov.b64 g, {gl, gh};\n\tfma.rn.f64 %14, u, g, %14;\n\tadd.u32 pe, pe, 16;\n\tsetp.lt.u32 p, pe, pend;\n\t@p bra.uni B14_LOOP;\n\tB14_DONE:\n\tmov.b32 pe, pend;\n\tand.b32 t, %26, 65535;\n\tmad.lo.u32 pend, t, 16, %16;\n\tsetp.ge.u32 p, pe, pend;\n\t@p bra.uni B15_DONE;\n\tB15_LOOP:\n\tld.shared.v4.b32 {o, x, gl, gh}, [pe];\n\tadd.u32 a, o, %17;\n\tld.shared.f64 u, [a];\n\tmov.b64 g, {gl, gh};\n\tfma.rn.f64 %15, u, g, %15;\n\tadd.u32 pe, pe, 16;\n\tsetp.lt.u32 p, pe, pend;\n\t@p bra.uni B15_LOOP;\n\tB15_DONE:\n\tmov.b32 pe, pend;\n\t}"
-                 : "+d"(acc[0][0]), "+d"(acc[0][1]), "+d"(acc[0][2]), "+d"(acc[0][3]), "+d"(acc[0][4]), "+d"(acc[0][5]), "+d"(acc[0][6]), "+d"(acc[0][7]), "+d"(acc[0][8]), "+d"(acc[0][9]), "+d"(acc[0][10]), "+d"(acc[0][11]), "+d"(acc[0][12]), "+d"(acc[0][13]), "+d"(acc[0][14]), "+d"(acc[0][15])
-                 : "r"(sen), "r"(sx), "r"(bw[0]), "r"(bw[1]), "r"(bw[2]), "r"(bw[3]), "r"(bw[4]), "r"(bw[5]), "r"(bw[6]), "r"(bw[7]), "r"(bw[8])
-                 : "memory");
-}
-__device__ __forceinline__ void chunk_s_1x32(double (&acc)[1][32], uint32_t sen, uint32_t sx, const uint32_t (&bw)[17]) {
-    asm volatile("{\n\t.reg .pred p;\n\t.reg .b32 o, x, gl, gh, a, t, pe, pend;\n\t.reg .f64 u, g;\n\tand.b32 t, %34, 65535;\n\tmad.lo.u32 pe, t, 16, %32;\n\tshr.u32 t, %34, 16;\n\tmad.lo.u32 pend, t, 16, %32;\n\tsetp.ge.u32 p, pe, pend;\n\t@p bra.uni B0_DONE;\n\tB0_LOOP:\n\tld.shared.v4.b32 {o, x, gl, gh}, [pe];\n\tadd.u32 a, o, %33;\n\tld.shared.f64 u, [a];\n\tmov.b64 g, {gl, gh};\n\tfma.rn.f64 %0, u, g, %0;\n\tadd.u32 pe, pe, 16;\n\tsetp.lt.u32 p, pe, pend;\n\t@p bra.uni B0_LOOP;\n\tB0_DONE:\n\tmov.b32 pe, pend;\n\tand.b32 t, %35, 65535;\n\tmad.lo.u32 pend, t, 16, %32;\n\tsetp.ge.u32 p, pe, pend;\n\t@p bra.uni B1_DONE;\n\tB1_LOOP:\n\tld.shared.v4.b32 {o, x, gl, gh}, [pe];\n\tadd.u32 a, o, %33;\n\tld.shared.f64 u, [a];\n\tmov.b64 g, {gl, gh};\n\tfma.rn.f64 %1, u, g, %1;\n\tadd.u32 pe, pe, 16;\n\tsetp.lt.u32 p, pe, pend;\n\t@p bra.uni B1_LOOP;\n\tB1_DONE:\n\tmov.b32 pe, pend;\n\tshr.u32 t, %35, 16;\n\tmad.lo.u32 pend, t, 16, %32;\n\tsetp.ge.u32 p, pe, pend;\n\t@p bra.uni B2_DONE;\n\tB2_LOOP:\n\tld.shared.v4.b32 {o, x, gl, gh}, [pe];\n\tadd.u32 a, o, %33;\n\tld.shared.f64 u, [a];\n\tmov.b64 g, {gl, gh};\n\tfma.rn.f64 %2, u, g, %2;\n\tadd.u32 pe, pe, 16;\n\tsetp.lt.u32 p, pe, pend;\n\t@p bra.uni B2_LOOP;\n\tB2_DONE:\n\tmov.b32 pe, pend;\n\tand.b32 t, %36, 65535;\n\tmad.lo.u32 pend, t, 16, %32;\n\tsetp.ge.u32 p, pe, pend;\n\t@p bra.uni B3_DONE;\n\tB3_LOOP:\n\tld.shared.v4.b32 {o, x, gl, gh}, [pe];\n\tadd.u32 a, o, %33;\n\tld.shared.f64 u, [a];\n\tmov.b64 g, {gl, gh};\n\tfma.rn.f64 %3, u, g, %3;\n\tadd.u32 pe, pe, 16;\n\tsetp.lt.u32 p, pe, pend;\n\t@p bra.uni B3_LOOP;\n\tB3_DONE:\n\tmov.b32 pe, pend;\n\tshr.u32 t, %36, 16;\n\tmad.lo.u32 pend, t, 16, %32;\n\tsetp.ge.u32 p, pe, pend;\n\t@p bra.uni B4_DONE;\n\tB4_LOOP:\n\tld.shared.v4.b32 {o, x, gl, gh}, [pe];\n\tadd.u32 a, o, %33;\n\tld.shared.f64 u, [a];\n\tmov.b64 g, {gl, gh};\n\tfma.rn.f64 %4, u, g, %4;\n\tadd.u32 pe, pe, 16;\n\tsetp.lt.u32 p, pe, pend;\n\t@p bra.uni B4_LOOP;\n\tB4_DONE:\n\tmov.b32 pe, pend;\n\tand.b32 t, %37, 65535;\n\tmad.lo.u32 pend, t, 16, %32;\n\tsetp.ge.u32 p, pe, pend;\n\t@p bra.uni B5_DONE;\n\tB5_LOOP:\n\tld.shared.v4.b32 {o, x, gl, gh}, [pe];\n\tadd.u32 a, o, %33;\n\tld.shared.f64 u, [a];\n\tmov.b64 g, {gl, gh};\n\tfma.rn.f64 %5, u, g, %5;\n\tadd.u32 pe, pe, 16;\n\tsetp.lt.u32 p, pe, pend;\n\t@p bra.uni B5_LOOP;\n\tB5_DONE:\n\tmov.b32 pe, pend;\n\tshr.u32 t, %37, 16;\n\tmad.lo.u32 pend, t, 16, %32;\n\tsetp.ge.u32 p, pe, pend;\n\t@p bra.uni B6_DONE;\n\tB6_LOOP:\n\tld.shared.v4.b32 {o, x, gl, gh}, [pe];\n\tadd.u32 a, o, %33;\n\tld.shared.f64 u, [a];\n\tmov.b64 g, {gl, gh};\n\tfma.rn.f64 %6, u, g, %6;\n\tadd.u32 pe, pe, 16;\n\tsetp.lt.u32 p, pe, pend;\n\t@p bra.uni B6_LOOP;\n\tB6_DONE:\n\tmov.b32 pe, pend;\n\tand.b32 t, %38, 65535;\n\tmad.lo.u32 pend, t, 16, %32;\n\tsetp.ge.u32 p, pe, pend;\n\t@p bra.uni B7_DONE;\n\tB7_LOOP:\n\tld.shared.v4.b32 {o, x, gl, gh}, [pe];\n\tadd.u32 a, o, %33;\n\tld.shared.f64 u, [a];\n\tmov.b64 g, {gl, gh};\n\tfma.rn.f64 %7, u, g, %7;\n\tadd.u32 pe, pe, 16;\n\tsetp.lt.u32 p, pe, pend;\n\t@p bra.uni B7_LOOP;\n\tB7_DONE:\n\tmov.b32 pe, pend;\n\tshr.u32 t, %38, 16;\n\tmad.lo.u32 pend, t, 16, %32;\n\tsetp.ge.u32 p, pe, pend;\n\t@p bra.uni B8_DONE;\n\tB8_LOOP:\n\tld.shared.v4.b32 {o, x, gl, gh}, [pe];\n\tadd.u32 a, o, %33;\n\tld.shared.f64 u, [a];\n\tmov.b64 g, {gl, gh};\n\tfma.rn.f64 %8, u, g, %8;\n\tadd.u32 pe, pe, 16;\n\tsetp.lt.u32 p, pe, pend;\n\t@p bra.uni B8_LOOP;\n\tB8_DONE:\n\tmov.b32 pe, pend;\n\tand.b32 t, %39, 65535;\n\tmad.lo.u32 pend, t, 16, %32;\n\tsetp.ge.u32 p, pe, pend;\n\t@p bra.uni B9_DONE;\n\tB9_LOOP:\n\tld.shared.v4.b32 {o, x, gl, gh}, [pe];\n\tadd.u32 a, o, %33;\n\tld.shared.f64 u, [a];\n\tmov.b64 g, {gl, gh};\n\tfma.rn.f64 %9, u, g, %9;\n\tadd.u32 pe, pe, 16;\n\tsetp.lt.u32 p, pe, pend;\n\t@p bra.uni B9_LOOP;\n\tB9_DONE:\n\tmov.b32 pe, pend;\n\tshr.u32 t, %39, 16;\n\tmad.lo.u32 pend, t, 16, %32;\n\tsetp.ge.u32 p, pe, pend;\n\t@p bra.uni B10_DONE;\n\tB10_LOOP:\n\tld.shared.v4.b32 {o, x, gl, gh}, [pe];\n\tadd.u32 a, o, %33;\n\tld.shared.f64 u, [a];\n\tmov.b64 g, {gl, gh};\n\tfma.rn.f64 %10, u, g, %10;\n\tadd.u32 pe, pe, 16;\n\tsetp.lt.u32 p, pe, pend;\n\t@p bra.uni B10_LOOP;\n\tB10_DONE:\n\tmov.b32 pe, pend;\n\tand.b32 t, %40, 65535;\n\tmad.lo.u32 pend, t, 16, %32;\n\tsetp.ge.u32 p, pe, pend;\n\t@p bra.uni B11_DONE;\n\tB11_LOOP:\n\tld.shared.v4.b32 {o, x, gl, gh}, [pe];\n\tadd.u32 a, o, %33;\n\tld.shared.f64 u, [a];\n\tmov.b64 g, {gl, gh};\n\tfma.rn.f64 %11, u, g, %11;\n\tadd.u32 pe, pe, 16;\n\tsetp.lt.u32 p, pe, pend;\n\t@p bra.uni B11_LOOP;\n\tB11_DONE:\n\tmov.b32 pe, pend;\n\tshr.u32 t, %40, 16;\n\tmad.lo.u32 pend, t, 16, %32;\n\tsetp.ge.u32 p, pe, pend;\n\t@p bra.uni B12_DONE;\n\tB12_LOOP:\n\tld.shared.v4.b32 {o, x, gl, gh}, [pe];\n\tadd.u32 a, o, %33;\n\tld.shared.f64 u, [a];\n\tmov.b64 g, {gl, gh};\n\tfma.rn.f64 %12, u, g, %12;\n\tadd.u32 pe, pe, 16;\n\tsetp.lt.u32 p, pe, pend;\n\t@p bra.uni B12_LOOP;\n\tB12_DONE:\n\tmov.b32 pe, pend;\n\tand.b32 t, %41, 65535;\n\tmad.lo.u32 pend, t, 16, %32;\n\tsetp.ge.u32 p, pe, pend;\n\t@p bra.uni B13_DONE;\n\tB13_LOOP:\n\tld.shared.v4.b32 {o, x, gl, gh}, [pe];\n\tadd.u32 a, o, %33;\n\tld.shared.f64 u, [a];\n\tmov.b64 g, {gl, gh};\n\tfma.rn.f64 %13, u, g, %13;\n\tadd.u32 pe, pe, 16;\n\tsetp.lt.u32 p, pe, pend;\n\t@p bra.uni B13_LOOP;\n\tB13_DONE:\n\tmov.b32 pe, pend;\n\tshr.u32 t, %41, 16;\n\tmad.lo.u32 pend, t, 16, %32;\n\tsetp.ge.u32 p, pe, pend;\n\t@p bra.uni B14_DONE;\n\tB14_LOOP:\n\tld.shared.v4.b32 {o, x, gl, gh}, [pe];\n\tadd.u32 a, o, %33;\n\tld.shared.f64 u, [a];\n\tmov.b64 g, {gl, gh};\n\tfma.rn.f64 %14, u, g, %14;\n\tadd.u32 pe, pe, 16;\n\tsetp.lt.u32 p, pe, pend;\n\t@p bra.uni B14_LOOP;\n\tB14_DONE:\n\tmov.b32 pe, pend;\n\tand.b32 t, %42, 65535;\n\tmad.lo.u32 pend, t, 16, %32;\n\tsetp.ge.u32 p, pe, pend;\n\t@p bra.uni B15_DONE;\n\tB15_LOOP:\n\tld.shared.v4.b32 {o, x, gl, gh}, [pe];\n\tadd.u32 a, o, %33;\n\tld.shared.f64 u, [a];\n\tmov.b64 g, {gl, gh};\n\tfma.rn.f64 %15, u, g, %15;\n\tadd.u32 pe, pe, 16;\n\tsetp.lt.u32 p, pe, pend;\n\t@p bra.uni B15_LOOP;\n\tB15_DONE:\n\tmov.b32 pe, pend;\n\tshr.u32 t, %42, 16;\n\tmad.lo.u32 pend, t, 16, %32;\n\tsetp.ge.u32 p, pe, pend;\n\t@p bra.uni B16_DONE;\n\tB16_LOOP:\n\tld.shared.v4.b32 {o, x, gl, gh}, [pe];\n\tadd.u32 a, o, %33;\n\tld.shared.f64 u, [a];\n\tmov.b64 g, {gl, gh};\n\tfma.rn.f64 %16, u, g, %16;\n\tadd.u32 pe, pe, 16;\n\tsetp.lt.u32 p, pe, pend;\n\t@p bra.uni B16_LOOP;\n\tB16_DONE:\n\tmov.b32 pe, pend;\n\tand.b32 t, %43, 65535;\n\tmad.lo.u32 pend, t, 16, %32;\n\tsetp.ge.u32 p, pe, pend;\n\t@p bra.uni B17_DONE;\n\tB17_LOOP:\n\tld.shared.v4.b32 {o, x, gl, gh}, [pe];\n\tadd.u32 a, o, %33;\n\tld.shared.f64 u, [a];\n\tmov.b64 g, {gl, gh};\n\tfma.rn.f64 %17, u, g, %17;\n\tadd.u32 pe, pe, 16;\n\tsetp.lt.u32 p, pe, pend;\n\t@p bra.uni B17_LOOP;\n\tB17_DONE:\n\tmov.b32 pe, pend;\n\tshr.u32 t, %43, 16;\n\tmad.lo.u32 pend, t, 16, %32;\n\tsetp.ge.u32 p, pe, pend;\n\t@p bra.uni B18_DONE;\n\tB18_LOOP:\n\tld.shared.v4.b32 {o, x, gl, gh}, [pe];\n\tadd.u32 a, o, %33;\n\tld.shared.f64 u, [a];\n\tmov.b64 g, {gl, gh};\n\tfma.rn.f64 %18, u, g, %18;\n\tadd.u32 pe, pe, 16;\n\tsetp.lt.u32 p, pe, pend;\n\t@p bra.uni B18_LOOP;\n\tB18_DONE:\n\tmov.b32 pe, pend;\n\tand.b32 t, %44, 65535;\n\tmad.lo.u32 pend, t, 16, %32;\n\tsetp.ge.u32 p, pe, pend;\n\t@p bra.uni B19_DONE;\n\tB19_LOOP:\n\tld.shared.v4.b32 {o, x, gl, gh}, [pe];\n\tadd.u32 a, o, %33;\n\tld.shared.f64 u, [a];\n\tmov.b64 g, {gl, gh};\n\tfma.rn.f64 %19, u, g, %19;\n\tadd.u32 pe, pe, 16;\n\tsetp.lt.u32 p, pe, pend;\n\t@p bra.uni B19_LOOP;\n\tB19_DONE:\n\tmov.b32 pe, pend;\n\tshr.u32 t, %44, 16;\n\tmad.lo.u32 pend, t, 16, %32;\n\tsetp.ge.u32 p, pe, pend;\n\t@p bra.uni B20_DONE;\n\tB20_LOOP:\n\tld.shared.v4.b32 {o, x, gl, gh}, [pe];\n\tadd.u32 a, o, %33;\n\tld.shared.f64 u, [a];\n\tmov.b64 g, {gl, gh};\n\tfma.rn.f64 %20, u, g, %20;\n\tadd.u32 pe, pe, 16;\n\tsetp.lt.u32 p, pe, pend;\n\t@p bra.uni B20_LOOP;\n\tB20_DONE:\n\tmov.b32 pe, pend;\n\tand.b32 t, %45, 65535;\n\tmad.lo.u32 pend, t, 16, %32;\n\tsetp.ge.u32 p, pe, pend;\n\t@p bra.uni B21_DONE;\n\tB21_LOOP:\n\tld.shared.v4.b32 {o, x, gl, gh}, [pe];\n\tadd.u32 a, o, %33;\n\tld.shared.f64 u, [a];\n\tmov.b64 g, {gl, gh};\n\tfma.rn.f64 %21, u, g, %21;\n\tadd.u32 pe, pe, 16;\n\tsetp.lt.u32 p, pe, pend;\n\t@p bra.uni B21_LOOP;\n\tB21_DONE:\n\tmov.b32 pe, pend;\n\tshr.u32 t, %45, 16;\n\tmad.lo.u32 pend, t, 16, %32;\n\tsetp.ge.u32 p, pe, pend;\n\t@p bra.uni B22_DONE;\n\tB22_LOOP:\n\tld.shared.v4.b32 {o, x, gl, gh}, [pe];\n\tadd.u32 a, o, %33;\n\tld.shared.f64 u, [a];\n\tmov.b64 g, {gl, gh};\n\tfma.rn.f64 %22, u, g, %22;\n\tadd.u32 pe, pe, 16;\n\tsetp.lt.u32 p, pe, pend;\n\t@p bra.uni B22_LOOP;\n\tB22_DONE:\n\tmov.b32 pe, pend;\n\tand.b32 t, %46, 65535;\n\tmad.lo.u32 pend, t, 16, %32;\n\tsetp.ge.u32 p, pe, pend;\n\t@p bra.uni B23_DONE;\n\tB23_LOOP:\n\tld.shared.v4.b32 {o, x, gl, gh}, [pe];\n\tadd.u32 a, o, %33;\n\tld.shared.f64 u, [a];\n\tmov.b64 g, {gl, gh};\n\tfma.rn.f64 %23, u, g, %23;\n\tadd.u32 pe, pe, 16;\n\tsetp.lt.u32 p, pe, pend;\n\t@p bra.uni B23_LOOP;\n\tB23_DONE:\n\tmov.b32 pe, pend;\n\tshr.u32 t, %46, 16;\n\tmad.lo.u32 pend, t, 16, %32;\n\tsetp.ge.u32 p, pe, pend;\n\t@p bra.uni B24_DONE;\n\tB24_LOOP:\n\tld.shared.v4.b32 {o, x, gl, gh}, [pe];\n\tadd.u32 a, o, %33;\n\tld.shared.f64 u, [a];\n\tmov.b64 g, {gl, gh};\n\tfma.rn.f64 %24, u, g, %24;\n\tadd.u32 pe, pe, 16;\n\tsetp.lt.u32 p, pe, pend;\n\t@p bra.uni B24_LOOP;\n\tB24_DONE:\n\tmov.b32 pe, pend;\n\tand.b32 t, %47, 65535;\n\tmad.lo.u32 pend, t, 16, %32;\n\tsetp.ge.u32 p, pe, pend;\n\t@p bra.uni B25_DONE;\n\tB25_LOOP:\n\tld.shared.v4.b32 {o, x, gl, gh}, [pe];\n\tadd.u32 a, o, %33;\n\tld.shared.f64 u, [a];\n\tmov.b64 g, {gl, gh};\n\tfma.rn.f64 %25, u, g, %25;\n\tadd.u32 pe, pe, 16;\n\tsetp.lt.u32 p, pe, pend;\n\t@p bra.uni B25_LOOP;\n\tB25_DONE:\n\tmov.b32 pe, pend;\n\tshr.u32 t, %47, 16;\n\tmad.lo.u32 pend, t, 16, %32;\n\tsetp.ge.u32 p, pe, pend;\n\t@p bra.uni B26_DONE;\n\tB26_LOOP:\n\tld.shared.v4.b32 {o, x, gl, gh}, [pe];\n\tadd.u32 a, o, %33;\n\tld.shared.f64 u, [a];\n\tmov.b64 g, {gl, gh};\n\tfma.rn.f64 %26, u, g, %26;\n\tadd.u32 pe, pe, 16;\n\tsetp.lt.u32 p, pe, pend;\n\t@p bra.uni B26_LOOP;\n\tB26_DONE:\n\tmov.b32 pe, pend;\n\tand.b32 t, %48, 65535;\n\tmad.lo.u32 pend, t, 16, %32;\n\tsetp.ge.u32 p, pe, pend;\n\t@p bra.uni B27_DONE;\n\tB27_LOOP:\n\tld.shared.v4.b32 {o, x, gl, gh}, [pe];\n\tadd.u32 a, o, %33;\n\tld.shared.f64 u, [a];\n\tmov.b64 g, {gl, gh};\n\tfma.rn.f64 %27, u, g, %27;\n\tadd.u32 pe, pe, 16;\n\tsetp.lt.u32 p, pe, pend;\n\t@p bra.uni B27_LOOP;\n\tB27_DONE:\n\tmov.b32 pe, pend;\n\tshr.u32 t, %48, 16;\n\tmad.lo.u32 pend, t, 16, %32;\n\tsetp.ge.u32 p, pe, pend;\n\t@p bra.uni B28_DONE;\n\tB28_LOOP:\n\tld.shared.v4.b32 {o, x, gl, gh}, [pe];\n\tadd.u32 a, o, %33;\n\tld.shared.f64 u, [a];\n\tmov.b64 g, {gl, gh};\n\tfma.rn.f64 %28, u, g, %28;\n\tadd.u32 pe, pe, 16;\n\tsetp.lt.u32 p, pe, pend;\n\t@p bra.uni B28_LOOP;\n\tB28_DONE:\n\tmov.b32 pe, pend;\n\tand.b32 t, %49, 65535;\n\tmad.lo.u32 pend, t, 16, %32;\n\tsetp.ge.u32 p, pe, pend;\n\t@p bra.uni B29_DONE;\n\tB29_LOOP:\n\tld.shared.v4.b32 {o, x, gl, gh}, [pe];\n\tadd.u32 a, o, %33;\n\tld.shared.f64 u, [a];\n\tmov.b64 g, {gl, gh};\n\tfma.rn.f64 %29, u, g, %29;\n\tadd.u32 pe, pe, 16;\n\tsetp.lt.u32 p, pe, pend;\n\t@p bra.uni B29_LOOP;\n\tB29_DONE:\n\tmov.b32 pe, pend;\n\tshr.u32 t, %49, 16;\n\tmad.lo.u32 pend, t, 16, %32;\n\tsetp.ge.u32 p, pe, pend;\n\t@p bra.uni B30_DONE;\n\tB30_LOOP:\n\tld.shared.v4.b32 {o, x, gl, gh}, [pe];\n\tadd.u32 a, o, %33;\n\tld.shared.f64 u, [a];\n\tmov.b64 g, {gl, gh};\n\tfma.rn.f64 %30, u, g, %30;\n\tadd.u32 pe, pe, 16;\n\tsetp.lt.u32 p, pe, pend;\n\t@p bra.uni B30_LOOP;\n\tB30_DONE:\n\tmov.b32 pe, pend;\n\tand.b32 t, %50, 65535;\n\tmad.lo.u32 pend, t, 16, %32;\n\tsetp.ge.u32 p, pe, pend;\n\t@p bra.uni B31_DONE;\n\tB31_LOOP:\n\tld.shared.v4.b32 {o, x, gl, gh}, [pe];\n\tadd.u32 a, o, %33;\n\tld.shared.f64 u, [a];\n\tmov.b64 g, {gl, gh};\n\tfma.rn.f64 %31, u, g, %31;\n\tadd.u32 pe, pe, 16;\n\tsetp.lt.u32 p, pe, pend;\n\t@p bra.uni B31_LOOP;\n\tB31_DONE:\n\tmov.b32 pe, pend;\n\t}"
-                 : "+d"(acc[0][0]), "+d"(acc[0][1]), "+d"(acc[0][2]), "+d"(acc[0][3]), "+d"(acc[0][4]), "+d"(acc[0][5]), "+d"(acc[0][6]), "+d"(acc[0][7]), "+d"(acc[0][8]), "+d"(acc[0][9]), "+d"(acc[0][10]), "+d"(acc[0][11]), "+d"(acc[0][12]), "+d"(acc[0][13]), "+d"(acc[0][14]), "+d"(acc[0][15]), "+d"(acc[0][16]), "+d"(acc[0][17]), "+d"(acc[0][18]), "+d"(acc[0][19]), "+d"(acc[0][20]), "+d"(acc[0][21]), "+d"(acc[0][22]), "+d"(acc[0][23]), "+d"(acc[0][24]), "+d"(acc[0][25]), "+d"(acc[0][26]), "+d"(acc[0][27]), "+d"(acc[0][28]), "+d"(acc[0][29]), "+d"(acc[0][30]), "+d"(acc[0][31])
-                 : "r"(sen), "r"(sx), "r"(bw[0]), "r"(bw[1]), "r"(bw[2]), "r"(bw[3]), "r"(bw[4]), "r"(bw[5]), "r"(bw[6]), "r"(bw[7]), "r"(bw[8]), "r"(bw[9]), "r"(bw[10]), "r"(bw[11]), "r"(bw[12]), "r"(bw[13]), "r"(bw[14]), "r"(bw[15]), "r"(bw[16])
-                 : "memory");
-}
-__device__ __forceinline__ void run_s1(uint32_t &pe, uint32_t pend, uint32_t sx, double &c0) {
-    asm volatile("{\n\t.reg .pred p;\n\t.reg .b32 o0, x0, l0, h0, a0;\n\t.reg .f64 u0, g0;\n\tsetp.ge.u32 p, %0, %2;\n\t@p bra.uni DONE;\n\tLOOP:\n\tld.shared.v4.b32 {o0, x0, l0, h0}, [%0];\n\tadd.u32 a0, o0, %3;\n\tld.shared.f64 u0, [a0];\n\tmov.b64 g0, {l0, h0};\n\tfma.rn.f64 %1, u0, g0, %1;\n\tadd.u32 %0, %0, 16;\n\tsetp.lt.u32 p, %0, %2;\n\t@p bra.uni LOOP;\n\tDONE:\n\t}"
-                 : "+r"(pe), "+d"(c0)
-                 : "r"(pend), "r"(sx)
-                 : "memory");
-}
-__device__ __forceinline__ void run_s1f(uint32_t &pe, uint32_t pend, uint32_t sx, uint4 f, double &c0) {
-    asm volatile("{\n\t.reg .pred p;\n\t.reg .b32 o0, x0, l0, h0, a0;\n\t.reg .f64 u0, g0;\n\tsetp.ge.u32 p, %0, %2;\n\t@p bra.uni DONE;\n\tadd.u32 a0, %4, %3;\n\tld.shared.f64 u0, [a0];\n\tmov.b64 g0, {%6, %7};\n\tfma.rn.f64 %1, u0, g0, %1;\n\tadd.u32 %0, %0, 16;\n\tsetp.ge.u32 p, %0, %2;\n\t@p bra.uni DONE;\n\tLOOP:\n\tld.shared.v4.b32 {o0, x0, l0, h0}, [%0];\n\tadd.u32 a0, o0, %3;\n\tld.shared.f64 u0, [a0];\n\tmov.b64 g0, {l0, h0};\n\tfma.rn.f64 %1, u0, g0, %1;\n\tadd.u32 %0, %0, 16;\n\tsetp.lt.u32 p, %0, %2;\n\t@p bra.uni LOOP;\n\tDONE:\n\t}"
-                 : "+r"(pe), "+d"(c0)
-                 : "r"(pend), "r"(sx), "r"(f.x), "r"(f.y), "r"(f.z), "r"(f.w)
-                 : "memory");
-}
-__device__ __forceinline__ void run_t1(uint32_t &pe, uint32_t pend, uint32_t st, uint32_t lane8, double &c0) {
-    asm volatile("{\n\t.reg .pred p;\n\t.reg .b32 o0, x0, l0, h0, a0;\n\t.reg .f64 u0, g0;\n\tsetp.ge.u32 p, %0, %2;\n\t@p bra.uni DONE;\n\tLOOP:\n\tld.shared.v4.b32 {o0, x0, l0, h0}, [%0];\n\txor.b32 a0, x0, %4;\n\tadd.u32 a0, a0, o0;\n\tadd.u32 a0, a0, %3;\n\tld.shared.f64 u0, [a0];\n\tmov.b64 g0, {l0, h0};\n\tfma.rn.f64 %1, u0, g0, %1;\n\tadd.u32 %0, %0, 16;\n\tsetp.lt.u32 p, %0, %2;\n\t@p bra.uni LOOP;\n\tDONE:\n\t}"
-                 : "+r"(pe), "+d"(c0)
-                 : "r"(pend), "r"(st), "r"(lane8)
-                 : "memory");
-}
-__device__ __forceinline__ void run_t1f(uint32_t &pe, uint32_t pend, uint32_t st, uint32_t lane8, uint4 f, double &c0) {
-    asm volatile("{\n\t.reg .pred p;\n\t.reg .b32 o0, x0, l0, h0, a0;\n\t.reg .f64 u0, g0;\n\tsetp.ge.u32 p, %0, %2;\n\t@p bra.uni DONE;\n\txor.b32 a0, %6, %4;\n\tadd.u32 a0, a0, %5;\n\tadd.u32 a0, a0, %3;\n\tld.shared.f64 u0, [a0];\n\tmov.b64 g0, {%7, %8};\n\tfma.rn.f64 %1, u0, g0, %1;\n\tadd.u32 %0, %0, 16;\n\tsetp.ge.u32 p, %0, %2;\n\t@p bra.uni DONE;\n\tLOOP:\n\tld.shared.v4.b32 {o0, x0, l0, h0}, [%0];\n\txor.b32 a0, x0, %4;\n\tadd.u32 a0, a0, o0;\n\tadd.u32 a0, a0, %3;\n\tld.shared.f64 u0, [a0];\n\tmov.b64 g0, {l0, h0};\n\tfma.rn.f64 %1, u0, g0, %1;\n\tadd.u32 %0, %0, 16;\n\tsetp.lt.u32 p, %0, %2;\n\t@p bra.uni LOOP;\n\tDONE:\n\t}"
-                 : "+r"(pe), "+d"(c0)
-                 : "r"(pend), "r"(st), "r"(lane8), "r"(f.x), "r"(f.y), "r"(f.z), "r"(f.w)
-                 : "memory");
-}
-
-__device__ __forceinline__ uint4 lds_u4(uint32_t addr) {
-    uint4 w;
-    asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];"
-                 : "=r"(w.x), "=r"(w.y), "=r"(w.z), "=r"(w.w) : "r"(addr) : "memory");
-    return w;
-}
 
 struct ApplyArgs {
     const double *A;
@@ -370,46 +210,68 @@ struct ApplyArgs {
     int d, alpha, tk, log2tk;
     int64_t nchunks, bstride, estride;
     const uint16_t *bptr;
-    const uint4 *ent;
+    const uint32_t *ent;
     double scale;
     double *S;
     int64_t lds, col0;
     int nslabs, stages;
     int stage_bytes, zero_off, bp_off, en_off;
+    // persistent balanced schedule: `groups` groups of nslabs CTAs split the
+    // flattened (row tile, chunk) space of `units` chunks evenly; a row tile
+    // cut between groups is summed by the group holding its first chunk
+    int streamk, groups;
+    int dbg;
+    int pf;  // mode 0: chunks prefetched into L2 beyond the shared-memory ring
+    int64_t units;
+    double *ws;  // per-CTA partial tile (SLAB x TM doubles)
+    int *flags;  // per-CTA "partial published" flags (left zero)
 };
 
 // All NW warps own buckets (NW*DB per CTA slab) and share the producer work:
 // warp 0 / lane 0 issues TMA + bulk copies (mode 0); in modes 1/2 every lane
 // issues its share of 8-byte cp.async for the chunk STAGES-1 ahead.
-template <int RPT, int DB, int NW, bool TRANS, bool BATCH, bool PROD, bool WHOLE = true>
+template <int RPT, int DB, int NW, bool TRANS, bool PROD, bool SK>
 __global__ void __launch_bounds__((NW + (PROD ? (TRANS ? 4 : 1) : 0)) * 32, 1)
     sjlt_apply_kernel(const ApplyArgs p, const __grid_constant__ CUtensorMap tmap) {
     constexpr int TM = 32 * RPT;
     constexpr int SLAB = NW * DB;
-    constexpr int G = DB < 4 ? DB : 4;  // buckets whose first entries are folded as one batch
-    static_assert(DB % G == 0, "DB must be a multiple of the batch");
     extern __shared__ __align__(128) unsigned char smem[];
     uint64_t *full = reinterpret_cast<uint64_t *>(smem);
     uint64_t *empty = full + 8;
     unsigned *done = reinterpret_cast<unsigned *>(full + 16);  // per-slot finished-warp counters
+    int *sk = reinterpret_cast<int *>(smem + 192);  // stream-K roles (below)
     unsigned char *stage0 = smem + 256;
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int ks = p.ksplit;
-    const int kr = (int)(blockIdx.x % ks);  // == %cluster_ctarank (cluster = ks consecutive CTAs)
-    const int64_t bid = blockIdx.x / ks;
-    const int slab = (int)(bid % p.nslabs);
-    const int64_t tile = bid / p.nslabs;
-    const int64_t r0 = tile * TM;
+    int kr = 0;  // == %cluster_ctarank (cluster = ks consecutive CTAs)
+    int slab;
+    int64_t u0, u1;  // this CTA's chunks in the flattened (row tile, chunk) order
+    int64_t tile0;   // row tile of the first chunk
+    if (SK) {
+        const int64_t grp = blockIdx.x / p.nslabs;
+        slab = (int)(blockIdx.x % p.nslabs);
+        u0 = grp * p.units / p.groups;
+        u1 = (grp + 1) * p.units / p.groups;
+        tile0 = u0 / p.nchunks;
+    } else {
+        kr = (int)(blockIdx.x % ks);
+        const int64_t bid = blockIdx.x / ks;
+        slab = (int)(bid % p.nslabs);
+        const int64_t tile = bid / p.nslabs;
+        const int64_t per = (p.nchunks + ks - 1) / ks;
+        const int64_t c_begin = (int64_t)kr * per < p.nchunks ? (int64_t)kr * per : p.nchunks;
+        const int64_t c_end = c_begin + per < p.nchunks ? c_begin + per : p.nchunks;
+        u0 = tile * p.nchunks + c_begin;
+        u1 = tile * p.nchunks + c_end;
+        tile0 = tile;
+    }
     const int j0 = slab * SLAB;
-    const int64_t per = (p.nchunks + ks - 1) / ks;
-    const int64_t c_begin = (int64_t)kr * per < p.nchunks ? (int64_t)kr * per : p.nchunks;
-    const int64_t c_end = c_begin + per < p.nchunks ? c_begin + per : p.nchunks;
-    const int nloc = (int)(c_end - c_begin);
+    const int nloc = (int)(u1 - u0);
     const int mode = p.mode;
     const int stages = p.stages;
     const uint32_t bp_bytes = (SLAB + 8) * 2;
-    const uint32_t en_bytes = (uint32_t)p.estride * 16;
+    const uint32_t en_bytes = (uint32_t)p.estride * 4;
     const uint32_t tile_bytes = (uint32_t)p.tk * TM * 8;
 
     // zero rows + null entries, barriers
@@ -417,9 +279,10 @@ __global__ void __launch_bounds__((NW + (PROD ? (TRANS ? 4 : 1) : 0)) * 32, 1)
         unsigned char *st = stage0 + (size_t)s * p.stage_bytes;
         double *zr = reinterpret_cast<double *>(st + p.zero_off);
         for (int q = threadIdx.x; q < TM; q += blockDim.x) zr[q] = 0.0;
-        if (threadIdx.x == 0)
-            reinterpret_cast<uint4 *>(st + p.en_off)[p.estride] =
-                make_uint4((uint32_t)p.zero_off, 0u, 0u, 0x3FF00000u);
+        // two null entries after the chunk's list (the pipelined walk reads
+        // up to two entries past a warp's list)
+        if (threadIdx.x < 8)
+            reinterpret_cast<uint32_t *>(st + p.en_off)[p.estride + threadIdx.x] = (uint32_t)p.tk << 3;
     }
     if (threadIdx.x == 0) {
         constexpr int PW = PROD ? (TRANS ? 4 : 1) : 0;  // dedicated producer warps
@@ -431,24 +294,62 @@ __global__ void __launch_bounds__((NW + (PROD ? (TRANS ? 4 : 1) : 0)) * 32, 1)
         }
         fence_mbar_init();
         if (mode == 0) prefetch_tmap(&tmap);
+        if (SK) {
+            // sk[0]: the first segment is the tail of a tile (publish it);
+            // sk[1], sk[2]: the last segment is the head of a tile cut by the
+            // schedule -- count and first CTA of the later groups holding its
+            // tails (stride nslabs); sk[3]: first row tile
+            const int64_t grp = blockIdx.x / p.nslabs;
+            const int64_t tb = (u1 - 1) / p.nchunks * p.nchunks;  // start of the last tile
+            int nq = 0;
+            if (u1 % p.nchunks != 0 && tb >= u0)
+                for (int64_t q = grp + 1; q < p.groups && q * p.units / p.groups < tb + p.nchunks; ++q) ++nq;
+            sk[0] = u0 % p.nchunks != 0;
+            sk[1] = nq;
+            sk[2] = (int)((grp + 1) * p.nslabs + slab);
+            sk[3] = (int)tile0;
+        }
     }
     __syncthreads();
 
     // ---- producer helpers
+    // row offset and chunk index of the CTA's j-th chunk (stream-K: 32-bit
+    // arithmetic, the host keeps units < 2^31)
+    auto chunk_of = [&](int j, int64_t &r0, int64_t &c) {
+        if constexpr (SK) {
+            const uint32_t u = (uint32_t)u0 + (uint32_t)j;
+            const uint32_t t = u / (uint32_t)p.nchunks;
+            r0 = (int64_t)t * TM;
+            c = u - t * (uint32_t)p.nchunks;
+        } else {
+            r0 = tile0 * TM;
+            c = u0 - tile0 * p.nchunks + j;
+        }
+    };
     auto stage_of = [&](int j) { return stage0 + (size_t)(j % stages) * p.stage_bytes; };
     auto issue_tma = [&](int j) {  // warp 0, lane 0
         unsigned char *st = stage_of(j);
         uint64_t *bar = &full[j % stages];
-        const int64_t c = c_begin + j;
+        int64_t r0, c;
+        chunk_of(j, r0, c);
         mbar_arrive_expect_tx(bar, tile_bytes + bp_bytes + en_bytes);
         tma_load_2d(st, &tmap, (int)r0, (int)(c * p.tk), bar);
+        // keep the HBM stream ahead of the ring: chunk j + pf into L2 (chunks
+        // stages .. stages+pf-1 are requested together with the first loads)
+        const int jp = j < stages ? j + stages : j + p.pf;
+        if (p.pf > 0 && jp < nloc && (j < stages ? j < p.pf : true)) {
+            int64_t rp, cp;
+            chunk_of(jp, rp, cp);
+            tma_prefetch_2d(&tmap, (int)rp, (int)(cp * p.tk));
+        }
         bulk_g2s(st + p.bp_off, p.bptr + c * p.bstride + j0, bp_bytes, bar);
         bulk_g2s(st + p.en_off, p.ent + c * p.estride, en_bytes, bar);
     };
     auto issue_coop = [&](int j, int ptid, int pnt) {  // threads [0, pnt) of the producer set
         unsigned char *st = stage_of(j);
         uint64_t *bar = &full[j % stages];
-        const int64_t c = c_begin + j;
+        int64_t r0, c;
+        chunk_of(j, r0, c);
         const int64_t k0 = c * p.tk;
         const int kc = (int)(p.n - k0 < p.tk ? p.n - k0 : p.tk);
         if (ptid == 0) {
@@ -536,181 +437,8 @@ __global__ void __launch_bounds__((NW + (PROD ? (TRANS ? 4 : 1) : 0)) * 32, 1)
     const uint32_t smem_base = smem_u32(stage0);
     const uint32_t lane8 = lane * 8u;
     const uint32_t lane_off = TRANS ? 0u : lane * 8u * (RPT == 1 ? 1u : 2u);  // S: rows 2l,2l+1 (+64) / l
-    int cs = 0;
-    uint32_t cph = 0;
-    for (int i = 0; i < nloc; ++i) {
-        // ---- producer duty (modes 1/2): chunk i + stages - 1 into the slot of
-        // chunk i - 1, once every warp has finished chunk i - 1
-        if (!PROD && mode != 0 && issued < nloc) {
-            const int j = issued;
-            if (j >= stages) mbar_wait(&empty[j % stages], (uint32_t)((j / stages) - 1) & 1u);
-            issue_coop(j, threadIdx.x, NW * 32);
-            ++issued;
-        }
-
-        // ---- consume chunk i
-        const int s = cs;
-        mbar_wait(&full[s], cph);
-        const uint32_t st = smem_base + (uint32_t)s * p.stage_bytes;
-        const uint32_t sx = st + lane_off;
-        const uint32_t sen = st + p.en_off;
-        const uint16_t *sbp = reinterpret_cast<const uint16_t *>(
-                                  stage0 + (size_t)s * p.stage_bytes + p.bp_off) + warp * DB;
-        const uint32_t nul = (uint32_t)p.estride;
-        // the warp's DB+1 bucket bounds, preloaded (packed u16 pairs) so no
-        // bucket waits on a shared-memory load of its own bound
-        constexpr int NBW = DB / 2 + 1;
-        uint32_t bw[NBW];
-        {
-            const uint32_t *src = reinterpret_cast<const uint32_t *>(sbp);
-#pragma unroll
-            for (int q = 0; q < NBW; ++q) bw[q] = src[q];
-        }
-        auto bound = [&](int jj) -> uint32_t {
-            return (jj & 1) ? (bw[jj >> 1] >> 16) : (bw[jj >> 1] & 0xffffu);
-        };
-        if (!BATCH && !TRANS && WHOLE) {
-            if constexpr (RPT == 1 && DB == 16) chunk_s_1x16(acc, sen, sx, bw);
-            else if constexpr (RPT == 1 && DB == 32) chunk_s_1x32(acc, sen, sx, bw);
-            else if constexpr (RPT == 2 && DB == 8) chunk_s_2x8(acc, sen, sx, bw);
-            else if constexpr (RPT == 2 && DB == 4) chunk_s_2x4(acc, sen, sx, bw);
-            else if constexpr (RPT == 2 && DB == 16) chunk_s_2x16(acc, sen, sx, bw);
-            else if constexpr (RPT == 4 && DB == 2) chunk_s_4x2(acc, sen, sx, bw);
-            else if constexpr (RPT == 4 && DB == 4) chunk_s_4x4(acc, sen, sx, bw);
-            else if constexpr (RPT == 4 && DB == 8) chunk_s_4x8(acc, sen, sx, bw);
-        } else if (!BATCH) {
-            // per-bucket loops; the first entry of bucket jj+1 is loaded while
-            // bucket jj runs (index <= estride: the null entry keeps it in range)
-            uint32_t pe = sen + 16u * bound(0);
-            uint4 wn = lds_u4(pe);
-#pragma unroll
-            for (int jj = 0; jj < DB; ++jj) {
-                const uint32_t pend = sen + 16u * bound(jj + 1);
-                const uint4 w = wn;
-                if (jj + 1 < DB) wn = lds_u4(pend);
-                if constexpr (RPT == 1) {
-                    if (TRANS) run_t1f(pe, pend, st, lane8, w, acc[0][jj]);
-                    else run_s1f(pe, pend, sx, w, acc[0][jj]);
-                } else if constexpr (RPT == 2) {
-                    if (TRANS) run_t2f(pe, pend, st, lane8, w, acc[0][jj], acc[1][jj]);
-                    else run_s2f(pe, pend, sx, w, acc[0][jj], acc[1][jj]);
-                } else {
-                    if (TRANS) run_t4f(pe, pend, st, lane8, w, acc[0][jj], acc[1][jj],
-                                       acc[RPT - 2][jj], acc[RPT - 1][jj]);
-                    else run_s4f(pe, pend, sx, w, acc[0][jj], acc[1][jj], acc[RPT - 2][jj],
-                                 acc[RPT - 1][jj]);
-                }
-                pe = pend;
-            }
-        }
-#pragma unroll
-        for (int g0 = 0; g0 < (BATCH ? DB : 0); g0 += G) {
-            uint32_t b[G + 1];
-#pragma unroll
-            for (int t = 0; t <= G; ++t) b[t] = bound(g0 + t);
-            // batch: first entry of each of the G buckets (null if empty)
-            uint4 w[G];
-#pragma unroll
-            for (int t = 0; t < G; ++t) {
-                const uint32_t idx = b[t + 1] > b[t] ? b[t] : nul;
-                asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];"
-                             : "=r"(w[t].x), "=r"(w[t].y), "=r"(w[t].z), "=r"(w[t].w)
-                             : "r"(sen + 16u * idx) : "memory");
-            }
-#pragma unroll
-            for (int t = 0; t < G; ++t) {
-                const double g = __hiloint2double((int)w[t].w, (int)w[t].z);
-                const int jj = g0 + t;
-                if (TRANS) {
-                    const uint32_t ad = st + w[t].x + (w[t].y ^ lane8);
-#pragma unroll
-                    for (int r = 0; r < RPT; ++r) {
-                        double u;
-                        asm volatile("ld.shared.f64 %0, [%1];" : "=d"(u) : "r"(ad + 256u * r) : "memory");
-                        acc[r][jj] = fma(u, g, acc[r][jj]);
-                    }
-                } else if constexpr (RPT == 1) {
-                    double u;
-                    asm volatile("ld.shared.f64 %0, [%1];" : "=d"(u) : "r"(sx + w[t].x) : "memory");
-                    acc[0][jj] = fma(u, g, acc[0][jj]);
-                } else {
-                    const uint32_t ad = sx + w[t].x;
-#pragma unroll
-                    for (int h = 0; h < RPT / 2; ++h) {
-                        double u, v;
-                        asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(u), "=d"(v)
-                                     : "r"(ad + 512u * h) : "memory");
-                        acc[2 * h][jj] = fma(u, g, acc[2 * h][jj]);
-                        acc[2 * h + 1][jj] = fma(v, g, acc[2 * h + 1][jj]);
-                    }
-                }
-            }
-            // remaining entries of each bucket
-#pragma unroll
-            for (int t = 0; t < G; ++t) {
-                const int jj = g0 + t;
-                uint32_t pe = sen + 16u * (b[t] + 1);
-                const uint32_t pend = sen + 16u * b[t + 1];
-                if constexpr (RPT == 1) {
-                    if (TRANS) run_t1(pe, pend, st, lane8, acc[0][jj]);
-                    else run_s1(pe, pend, sx, acc[0][jj]);
-                } else if constexpr (RPT == 2) {
-                    if (TRANS) run_t2(pe, pend, st, lane8, acc[0][jj], acc[1][jj]);
-                    else run_s2(pe, pend, sx, acc[0][jj], acc[1][jj]);
-                } else {
-                    if (TRANS) run_t4(pe, pend, st, lane8, acc[0][jj], acc[1][jj], acc[RPT - 2][jj],
-                                      acc[RPT - 1][jj]);
-                    else run_s4(pe, pend, sx, acc[0][jj], acc[1][jj], acc[RPT - 2][jj],
-                                acc[RPT - 1][jj]);
-                }
-            }
-        }
-        __syncwarp();
-        if (lane == 0) {
-            if (mode == 0 && !PROD) {
-                // the last warp to finish chunk i refills its slot with chunk i + stages
-                if (atomicAdd(&done[s], 1u) == NW - 1) {
-                    done[s] = 0;
-                    if (i + stages < nloc) issue_tma(i + stages);
-                }
-            } else {
-                mbar_arrive(&empty[s]);
-            }
-        }
-        if (++cs == stages) {
-            cs = 0;
-            cph ^= 1u;
-        }
-    }
-
-    // ------------------------------------------- k-split: DSMEM reduction
-    // Partial sums of the ks CTAs of a cluster are combined by rank 0 in
-    // rank order (deterministic).  The stage ring is reused as the buffer.
-    if (ks > 1) {
-        double *red = reinterpret_cast<double *>(stage0);
-        __syncthreads();  // every stage consumed: the ring is free
-        if (kr > 0) {
-#pragma unroll
-            for (int jj = 0; jj < DB; ++jj)
-#pragma unroll
-                for (int r = 0; r < RPT; ++r)
-                    red[((warp * DB + jj) * RPT + r) * 32 + lane] = acc[r][jj];
-        }
-        cluster_sync();
-        if (kr == 0) {
-            for (int q = 1; q < ks; ++q) {
-#pragma unroll
-                for (int jj = 0; jj < DB; ++jj)
-#pragma unroll
-                    for (int r = 0; r < RPT; ++r)
-                        acc[r][jj] += ld_dsmem_f64(&red[((warp * DB + jj) * RPT + r) * 32 + lane], q);
-            }
-        }
-        cluster_sync();
-        if (kr > 0) return;
-    }
-
     // epilogue: one final scaling, as the reference (`out *= scale`)
+    auto store_tile = [&](const int64_t r0) {
     const bool vec_ok = ((p.lds & 1) == 0) && ((reinterpret_cast<uintptr_t>(p.S) & 15) == 0);
 #pragma unroll
     for (int jj = 0; jj < DB; ++jj) {
@@ -741,7 +469,149 @@ __global__ void __launch_bounds__((NW + (PROD ? (TRANS ? 4 : 1) : 0)) * 32, 1)
             }
         }
     }
+    };
+
+    // stream-K: loop index at which the current row-tile segment ends (the
+    // rest of the bookkeeping is recomputed there, off the hot loop)
+    int seg_end = SK ? (int)((tile0 + 1) * p.nchunks - u0) : 0;
+    seg_end = seg_end < nloc ? seg_end : nloc;
+    int ctile = (int)tile0;
+    int cs = 0;
+    uint32_t cph = 0;
+    for (int i = 0; i < nloc; ++i) {
+        // ---- producer duty (modes 1/2): chunk i + stages - 1 into the slot of
+        // chunk i - 1, once every warp has finished chunk i - 1
+        if (!PROD && mode != 0 && issued < nloc) {
+            const int j = issued;
+            if (j >= stages) mbar_wait(&empty[j % stages], (uint32_t)((j / stages) - 1) & 1u);
+            issue_coop(j, threadIdx.x, NW * 32);
+            ++issued;
+        }
+
+        // ---- consume chunk i
+        const int s = cs;
+        if (p.dbg != 2 || i < stages) mbar_wait(&full[s], cph);
+        const uint32_t st = smem_base + (uint32_t)s * p.stage_bytes;
+        const uint32_t sx = st + lane_off;
+        const uint32_t sen = st + p.en_off;
+        const uint16_t *sbp = reinterpret_cast<const uint16_t *>(
+                                  stage0 + (size_t)s * p.stage_bytes + p.bp_off) + warp * DB;
+        // the warp's DB+1 bucket bounds (packed u16 pairs)
+        constexpr int NBW = DB / 2 + 1;
+        uint32_t bw[NBW];
+        {
+            const uint32_t *src = reinterpret_cast<const uint32_t *>(sbp);
+#pragma unroll
+            for (int q = 0; q < NBW; ++q) bw[q] = src[q];
+        }
+        if (p.dbg == 1) {
+        } else if constexpr (TRANS) {
+            if constexpr (RPT == 1 && DB == 16) pipe_t_1x16(acc, sen, st, lane8, bw);
+            else if constexpr (RPT == 1 && DB == 32) pipe_t_1x32(acc, sen, st, lane8, bw);
+            else if constexpr (RPT == 2 && DB == 4) pipe_t_2x4(acc, sen, st, lane8, bw);
+            else if constexpr (RPT == 2 && DB == 8) pipe_t_2x8(acc, sen, st, lane8, bw);
+            else if constexpr (RPT == 2 && DB == 16) pipe_t_2x16(acc, sen, st, lane8, bw);
+            else if constexpr (RPT == 4 && DB == 2) pipe_t_4x2(acc, sen, st, lane8, bw);
+            else if constexpr (RPT == 4 && DB == 4) pipe_t_4x4(acc, sen, st, lane8, bw);
+            else if constexpr (RPT == 4 && DB == 8) pipe_t_4x8(acc, sen, st, lane8, bw);
+        } else {
+            if constexpr (RPT == 1 && DB == 16) pipe_s_1x16(acc, sen, sx, bw);
+            else if constexpr (RPT == 1 && DB == 32) pipe_s_1x32(acc, sen, sx, bw);
+            else if constexpr (RPT == 2 && DB == 4) pipe_s_2x4(acc, sen, sx, bw);
+            else if constexpr (RPT == 2 && DB == 8) pipe_s_2x8(acc, sen, sx, bw);
+            else if constexpr (RPT == 2 && DB == 16) pipe_s_2x16(acc, sen, sx, bw);
+            else if constexpr (RPT == 4 && DB == 2) pipe_s_4x2(acc, sen, sx, bw);
+            else if constexpr (RPT == 4 && DB == 4) pipe_s_4x4(acc, sen, sx, bw);
+            else if constexpr (RPT == 4 && DB == 8) pipe_s_4x8(acc, sen, sx, bw);
+        }
+        __syncwarp();
+        if (lane == 0) {
+            if (mode == 0 && !PROD) {
+                // the last warp to finish chunk i refills its slot with chunk i + stages
+                if (atomicAdd(&done[s], 1u) == NW - 1) {
+                    done[s] = 0;
+                    if (i + stages < nloc && p.dbg != 2) issue_tma(i + stages);
+                }
+            } else {
+                mbar_arrive(&empty[s]);
+            }
+        }
+        if (++cs == stages) {
+            cs = 0;
+            cph ^= 1u;
+        }
+        if (SK && i + 1 == seg_end) {
+            // segment of row tile `ctile` ends here; its role was fixed in the
+            // prologue (sk[]): the first segment may be a tail to publish, the
+            // last one a head that adds the later groups' tails in group order
+            constexpr int NT = NW * 32;
+            if (ctile == sk[3] && sk[0]) {
+                double *w = p.ws + (size_t)blockIdx.x * (SLAB * TM);
+#pragma unroll
+                for (int jj = 0; jj < DB; ++jj)
+#pragma unroll
+                    for (int r = 0; r < RPT; ++r)
+                        __stcg(&w[((warp * DB + jj) * RPT + r) * 32 + lane], acc[r][jj]);
+                __threadfence();
+                bar_named(NT);
+                if (threadIdx.x == 0) st_release_gpu(&p.flags[blockIdx.x], 1);
+            } else {
+                const int nq = i + 1 == nloc ? sk[1] : 0;
+                for (int q = 0; q < nq; ++q) {
+                    const int cq = sk[2] + q * p.nslabs;
+                    if (threadIdx.x == 0) {
+                        while (ld_acquire_gpu(&p.flags[cq]) == 0) __nanosleep(100);
+                        p.flags[cq] = 0;
+                    }
+                    bar_named(NT);
+                    const double *w = p.ws + (size_t)cq * (SLAB * TM);
+#pragma unroll
+                    for (int jj = 0; jj < DB; ++jj)
+#pragma unroll
+                        for (int r = 0; r < RPT; ++r)
+                            acc[r][jj] += __ldcg(&w[((warp * DB + jj) * RPT + r) * 32 + lane]);
+                }
+                store_tile((int64_t)ctile * TM);
+            }
+#pragma unroll
+            for (int r = 0; r < RPT; ++r)
+#pragma unroll
+                for (int jj = 0; jj < DB; ++jj) acc[r][jj] = 0.0;
+            ++ctile;
+            seg_end = i + 1 + (int)p.nchunks < nloc ? i + 1 + (int)p.nchunks : nloc;
+        }
+    }
+    if (SK) return;
+
+    // ------------------------------------------- k-split: DSMEM reduction
+    // Partial sums of the ks CTAs of a cluster are combined by rank 0 in
+    // rank order (deterministic).  The stage ring is reused as the buffer.
+    if (ks > 1) {
+        double *red = reinterpret_cast<double *>(stage0);
+        __syncthreads();  // every stage consumed: the ring is free
+        if (kr > 0) {
+#pragma unroll
+            for (int jj = 0; jj < DB; ++jj)
+#pragma unroll
+                for (int r = 0; r < RPT; ++r)
+                    red[((warp * DB + jj) * RPT + r) * 32 + lane] = acc[r][jj];
+        }
+        cluster_sync();
+        if (kr == 0) {
+            for (int q = 1; q < ks; ++q) {
+#pragma unroll
+                for (int jj = 0; jj < DB; ++jj)
+#pragma unroll
+                    for (int r = 0; r < RPT; ++r)
+                        acc[r][jj] += ld_dsmem_f64(&red[((warp * DB + jj) * RPT + r) * 32 + lane], q);
+            }
+        }
+        cluster_sync();
+        if (kr > 0) return;
+    }
+    store_tile(tile0 * TM);
 }
+
 
 template <int RPT, int DB, int NW>
 static int launch(ApplyArgs a, const Geom &g, cudaStream_t st) {
@@ -763,7 +633,7 @@ static int launch(ApplyArgs a, const Geom &g, cudaStream_t st) {
     a.zero_off = a_bytes;
     a.bp_off = (int)roundup(a_bytes + TM * 8, 128);
     a.en_off = (int)roundup(a.bp_off + (SLAB + 8) * 2, 128);
-    a.stage_bytes = (int)roundup(a.en_off + (a.estride + 1) * 16, 128);
+    a.stage_bytes = (int)roundup(a.en_off + (a.estride + 8) * 4, 128);
     a.nslabs = (a.d + SLAB - 1) / SLAB;
     const int64_t tiles = (a.m_out + TM - 1) / TM;
     // k-split across a cluster when the tile grid cannot fill the GPU
@@ -774,37 +644,57 @@ static int launch(ApplyArgs a, const Geom &g, cudaStream_t st) {
         while (ks > 1 && a.nchunks / ks < 8) --ks;
         if (ks == 3 || ks == 5 || ks == 6 || ks == 7) ks = ks >= 4 ? 4 : 2;
     }
+    // dedicated producer warp(s) (TMA issue for S, transposing copies for S');
+    // a 33rd warp would cut the register budget to 56, so 32-warp CTAs refill
+    // from the last consumer warp to release a slot instead
+    bool prod = NW < 32;
+    if (const char *env = getenv("HSK_SJLT_PROD")) prod = env[0] == '1';
+    prod = prod && (a.mode == 0 || a.mode == 1) && NW + (a.trans ? 4 : 1) <= 32;
+    // persistent balanced schedule (stream-K) when whole-tile CTAs would
+    // leave a partial last wave: one CTA per SM, groups of nslabs CTAs (the
+    // slabs of a row tile stay in lockstep, so A is read from HBM once)
+    const int sms = sm_count();
+    const int64_t plain = ctas * ks;
+    const int64_t waves = (plain + sms - 1) / sms;
+    const double eff = (double)plain / (double)(waves * sms);
+    a.units = tiles * a.nchunks;
+    a.groups = (int)std::min<int64_t>(sms / a.nslabs, a.units);
+    a.streamk = eff < 0.9;
+    if (const char *env = getenv("HSK_SJLT_STREAMK")) a.streamk = env[0] == '1';
+    a.streamk = a.streamk && a.groups >= 1 && a.nchunks > 0 && a.units < (1ll << 31);
+    if (a.streamk) {
+        ks = 1;
+        void *ws = nullptr;
+        int *flags = nullptr;
+        const int nct = a.groups * a.nslabs;
+        int rc = stream_workspace(st, (size_t)nct * SLAB * TM * sizeof(double), nct, &ws, &flags);
+        if (rc) return rc;
+        a.ws = static_cast<double *>(ws);
+        a.flags = flags;
+    }
     a.ksplit = ks;
-    const int per = (int)((a.nchunks + ks - 1) / ks);
+    const int per = (int)(a.streamk ? (a.units + a.groups - 1) / a.groups : (a.nchunks + ks - 1) / ks);
     const int budget = 226 * 1024;
     a.stages = std::max(2, std::min(8, (budget - 256) / a.stage_bytes));
     if (const char *env = getenv("HSK_SJLT_STAGES")) a.stages = std::max(2, std::min(a.stages, atoi(env)));
     if (per > 0 && a.stages > per + 1) a.stages = std::max(2, per + 1);
     int smem = 256 + a.stages * a.stage_bytes;
     if (ks > 1) smem = std::max(smem, 256 + NW * DB * RPT * 32 * 8);
-    // batched first-entry folding pays off when buckets hold several entries
-    // per chunk (lambda = tk*alpha/d); HSK_SJLT_BATCH=0/1 overrides
-    bool batch = (int64_t)a.tk * a.alpha >= 4 * (int64_t)a.d;
-    if (const char *env = getenv("HSK_SJLT_BATCH")) batch = env[0] == '1';
-    // dedicated producer warp (TMA path only; 17 warps -> 96-register budget,
-    // so it pairs with the unbatched consumer loops)
-    bool prod = NW < 32;  // a 33rd warp would cut the register budget to 56
-    if (const char *env = getenv("HSK_SJLT_PROD")) prod = env[0] == '1';
-    prod = prod && (a.mode == 0 || a.mode == 1) && NW + (a.trans ? 4 : 1) <= 32;
-    if (prod) batch = false;
-    bool whole = true;
-    if (const char *env = getenv("HSK_SJLT_WHOLE")) whole = env[0] == '1';
-    auto kern = a.trans ? (prod ? sjlt_apply_kernel<RPT, DB, NW, true, false, true>
-                                : batch ? sjlt_apply_kernel<RPT, DB, NW, true, true, false>
-                                        : sjlt_apply_kernel<RPT, DB, NW, true, false, false>)
-                        : (prod ? sjlt_apply_kernel<RPT, DB, NW, false, false, true>
-                                : batch ? sjlt_apply_kernel<RPT, DB, NW, false, true, false>
-                                        : whole ? sjlt_apply_kernel<RPT, DB, NW, false, false, false, true>
-                                                : sjlt_apply_kernel<RPT, DB, NW, false, false, false, false>);
+    auto kern = a.trans ? (prod ? (a.streamk ? sjlt_apply_kernel<RPT, DB, NW, true, true, true>
+                                             : sjlt_apply_kernel<RPT, DB, NW, true, true, false>)
+                                : (a.streamk ? sjlt_apply_kernel<RPT, DB, NW, true, false, true>
+                                             : sjlt_apply_kernel<RPT, DB, NW, true, false, false>))
+                        : (prod ? (a.streamk ? sjlt_apply_kernel<RPT, DB, NW, false, true, true>
+                                             : sjlt_apply_kernel<RPT, DB, NW, false, true, false>)
+                                : (a.streamk ? sjlt_apply_kernel<RPT, DB, NW, false, false, true>
+                                             : sjlt_apply_kernel<RPT, DB, NW, false, false, false>));
+    a.pf = a.mode == 0 ? 2 : 0;
+    a.dbg = getenv("HSK_SJLT_DBG") ? atoi(getenv("HSK_SJLT_DBG")) : 0;
+    if (const char *env = getenv("HSK_SJLT_PF")) a.pf = std::max(0, atoi(env));
     const int nthreads = (NW + (prod ? (a.trans ? 4 : 1) : 0)) * 32;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e != cudaSuccess) return cuda_status(e, "sjlt: set smem attribute");
-    const int64_t grid = tiles * a.nslabs * ks;
+    const int64_t grid = a.streamk ? (int64_t)a.groups * a.nslabs : tiles * a.nslabs * ks;
     HSK_REQUIRE(grid < (1ll << 31), HSK_EINVAL, "sjlt: grid too large");
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3((unsigned)grid, 1, 1);
@@ -812,12 +702,17 @@ static int launch(ApplyArgs a, const Geom &g, cudaStream_t st) {
     cfg.dynamicSmemBytes = smem;
     cfg.stream = st;
     cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeClusterDimension;
-    attr[0].val.clusterDim.x = ks;
-    attr[0].val.clusterDim.y = 1;
-    attr[0].val.clusterDim.z = 1;
+    if (a.streamk) {  // groups wait on later groups' partials: all CTAs co-resident
+        attr[0].id = cudaLaunchAttributeCooperative;
+        attr[0].val.cooperative = 1;
+    } else {
+        attr[0].id = cudaLaunchAttributeClusterDimension;
+        attr[0].val.clusterDim.x = ks;
+        attr[0].val.clusterDim.y = 1;
+        attr[0].val.clusterDim.z = 1;
+    }
     cfg.attrs = attr;
-    cfg.numAttrs = ks > 1 ? 1 : 0;  // plain launch unless the k-split needs a cluster
+    cfg.numAttrs = (ks > 1 || a.streamk) ? 1 : 0;  // plain launch unless needed
     if (const char *env = getenv("HSK_SJLT_FORCE_CLUSTER")) cfg.numAttrs = env[0] == '1' ? 1 : cfg.numAttrs;
     e = cudaLaunchKernelEx(&cfg, kern, a, tmap);
     if (e != cudaSuccess) return cuda_status(e, "sjlt_apply_kernel launch");
@@ -859,9 +754,9 @@ extern "C" int hsk_sjlt_plan_build(const int32_t *pos, const int8_t *sgn, int64_
             int p2 = 1;
             while (p2 < g->tk * alpha) p2 <<= 1;
             sjlt::sjlt_plan_kernel<<<(unsigned)g->nchunks, 256, p2 * sizeof(uint32_t), st>>>(
-                pos, sgn, n, d, alpha, g->tk, p2, g->bstride, g->estride, g->pitch,
+                pos, sgn, n, d, alpha, g->tk, p2, g->bstride, g->estride,
                 reinterpret_cast<uint16_t *>(base + g->bptr_off),
-                reinterpret_cast<uint4 *>(base + g->ent_off), reinterpret_cast<int *>(base + 28));
+                reinterpret_cast<uint32_t *>(base + g->ent_off), reinterpret_cast<int *>(base + 28));
             HSK_CHECK_LAUNCH("sjlt_plan_kernel");
         }
     }
@@ -907,16 +802,17 @@ extern "C" int hsk_sjlt_apply(const double *A, int64_t rows, int64_t cols, int64
     a.bstride = g.bstride;
     a.estride = g.estride;
     a.bptr = reinterpret_cast<const uint16_t *>(base + g.bptr_off);
-    a.ent = reinterpret_cast<const uint4 *>(base + g.ent_off);
+    a.ent = reinterpret_cast<const uint32_t *>(base + g.ent_off);
     a.scale = scale;
     a.S = S;
     a.lds = lds;
     a.col0 = col0;
     cudaStream_t st = as_stream(stream);
-    // S: 32 warps x (DB/2) buckets -- twice the warps to hide the shared-memory
-    // latency of the entry -> tile -> DFMA chain (<= 64 registers per thread).
-    // S': 16 warps (its cp.async producer work is shared by all warps).
-    bool w32 = !trans;
+    // 16 consumer warps (128-register budget: RPT x DB accumulators plus the
+    // walker's pipeline registers) and dedicated producer warp(s); the
+    // 32-warp variants (64 registers, half the buckets per warp) are kept
+    // for tuning (HSK_SJLT_W32=1).
+    bool w32 = false;
     if (const char *env = getenv("HSK_SJLT_W32")) w32 = env[0] == '1';
     if (g.rpt == 1) {  // 32-row tiles, 512-bucket slabs
         if (w32) return sjlt::launch<1, 16, 32>(a, g, st);

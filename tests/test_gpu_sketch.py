@@ -108,6 +108,33 @@ def test_sjlt_shapes_vs_oracle(cuda, m, n, d, alpha, cons):
     _close(sk.apply_right_transposed(B, op), ref_t, np.linalg.norm(B))
 
 
+@pytest.mark.parametrize("m,n,d,alpha", [
+    (5000, 3000, 300, 4), (9000, 1000, 64, 8), (4000, 2600, 700, 4), (3000, 5000, 2048, 8),
+    (150, 20000, 512, 4),
+])
+def test_sjlt_schedules_vs_oracle(cuda, monkeypatch, m, n, d, alpha):
+    """Whole-tile (k-split) and persistent stream-K schedules: both match the
+    oracle, and stream-K's cross-CTA tile fixup is bitwise repeatable."""
+    rng = np.random.default_rng(m + n + d)
+    op = sk.new_operator(sk.SJLT, n, d, seed=(m, d), alpha=alpha, construction=sk.BLOCK)
+    b = op.blocks[0]
+    A = rng.standard_normal((m, n))
+    B = rng.standard_normal((n, m))
+    ref = O.sjlt_right(A, b._pos, b._signs, d, b._scale)
+    ref_t = O.sjlt_right_t(B, b._pos, b._signs, d, b._scale)
+    dA, dB = device.DeviceMatrix.from_host(A), device.DeviceMatrix.from_host(B)
+    for mode in ("0", "1"):
+        monkeypatch.setenv("HSK_SJLT_STREAMK", mode)
+        s1 = sk.apply_right_device(dA, op).to_host()
+        s2 = sk.apply_right_device(dA, op).to_host()
+        _close(s1, ref, np.linalg.norm(A))
+        np.testing.assert_array_equal(s1, s2)
+        t1 = sk.apply_right_transposed_device(dB, op).to_host()
+        t2 = sk.apply_right_transposed_device(dB, op).to_host()
+        _close(t1, ref_t, np.linalg.norm(B))
+        np.testing.assert_array_equal(t1, t2)
+
+
 def test_odd_leading_dimension_and_column_offset(cuda):
     rng = np.random.default_rng(5)
     m, n, d = 77, 333, 96
