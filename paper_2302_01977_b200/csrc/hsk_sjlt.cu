@@ -78,17 +78,31 @@ static inline int tk_fit(int alpha, int tm, int cap, int per_stage) {
     return tk;
 }
 
+// largest multiple of 16 TK <= cap (<= 256: TMA box limit) whose stage fits
+static inline int tk_fit16(int alpha, int tm, int cap, int per_stage) {
+    int tk = cap;
+    while (tk > 16 && (tk * alpha > kMaxChunkEntries || stage_bytes_for(tk, tm, alpha) > per_stage))
+        tk -= 16;
+    return tk;
+}
+
 static Geom geom_dir(int64_t n, int d, int alpha, int trans, int64_t base) {
     Geom g;
     int tk;
     // per-stage budgets: 3 stages (or 2) of the 226 KB ring
     constexpr int kStage3 = (226 * 1024 - 256) / 3, kStage2 = (226 * 1024 - 256) / 2;
-    if (d <= 64) {                          // 128-row tiles, three or more stages
+    // S over long rows (n >= 8192): two stages of the largest TK -- more
+    // entries per bucket visit (lambda = TK*alpha/d) and fewer chunk
+    // boundaries outweigh the shallower ring (the dedicated producer warp
+    // refills a slot as soon as it is released).  Short rows keep three
+    // power-of-two stages so every CTA still has a deep pipeline.
+    const bool wide = !trans && n >= 8192;
+    if (d <= 64) {                          // 128-row tiles
         g.rpt = 4;
-        tk = tk_fit(alpha, 128, 128, kStage3);
-    } else if (trans || d <= 512) {         // 64-row tiles, TK 128, three stages
+        tk = wide ? tk_fit16(alpha, 128, 256, kStage2) : tk_fit(alpha, 128, 128, kStage3);
+    } else if (trans || d <= 512) {         // 64-row tiles
         g.rpt = 2;
-        tk = tk_fit(alpha, 64, 128, kStage3);
+        tk = wide ? tk_fit16(alpha, 64, 256, kStage2) : tk_fit(alpha, 64, 128, kStage3);
     } else {                                // S, d > 512: 32-row tiles (512-bucket slabs), TK 256
         g.rpt = 1;
         tk = tk_fit(alpha, 32, 256, kStage2);
