@@ -120,8 +120,13 @@ class DeviceMatrix:
         ncols = self.cols - col0 if ncols is None else ncols
         if self.rows == 0 or ncols == 0:
             return np.zeros((self.rows, ncols), order="F")
-        host = self.t[col0:col0 + ncols, :self.rows].cpu().numpy()
-        return host.T  # (rows, ncols) F-contiguous, owned by the caller
+        # D2H straight into pinned memory from torch's caching host allocator:
+        # full-rate DMA and no first-touch page faults on a fresh pageable
+        # buffer (which cost more than the copy itself).  The numpy view keeps
+        # the pinned block alive; it returns to the pool when the caller drops it.
+        host = torch.empty((ncols, self.rows), dtype=torch.float64, pin_memory=True)
+        host.copy_(self.t[col0:col0 + ncols, :self.rows])
+        return host.numpy().T  # (rows, ncols) F-contiguous, owned by the caller
 
     def column_view(self, col0: int, ncols: int) -> "DeviceMatrix":
         sub = DeviceMatrix.__new__(DeviceMatrix)

@@ -37,6 +37,7 @@ def launches(path):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--launches")
+    ap.add_argument("--command", default="python bench.py --steps 2 --warmup 3")
     ap.add_argument("--full", action="append", default=[])
     ap.add_argument("--tag", default="r01")
     args = ap.parse_args()
@@ -44,7 +45,7 @@ def main():
     if args.launches:
         by, total = launches(args.launches)
         out["launch_list"] = {"source": os.path.basename(args.launches),
-                              "command": "python bench.py --steps 5 --warmup 3 --no-cpu",
+                              "command": args.command,
                               "note": "ncu --metrics gpu__time_duration.sum --clock-control none "
                                       "(cold-cache, serialised: compare shares)",
                               "total_ms": total, "kernels": by}
