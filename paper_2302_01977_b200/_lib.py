@@ -58,7 +58,9 @@ def load(path: str | None = None):
     with _lock:
         if _lib is not None:
             return _lib
-        path = path or LIB_PATH
+        # HSK_LIB: load another build of the same ABI (A/B timing of kernel
+        # revisions on one GPU box; tools/ab_build.sh)
+        path = path or os.environ.get("HSK_LIB") or LIB_PATH
         if not os.path.exists(path):
             try:
                 from . import build as _build

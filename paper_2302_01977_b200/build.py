@@ -25,6 +25,8 @@ SOURCES = ["hsk_misc.cu", "hsk_sjlt.cu", "hsk_gauss.cu", "hsk_srht.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC_FLAGS = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC,-fvisibility=hidden",
               "-Xptxas", "-v", "--expt-relaxed-constexpr"]
+# diagnostic builds, e.g. HSK_NVCC_EXTRA="-DHSK_SJLT_DEBUG=1" (force a rebuild)
+NVCC_FLAGS += os.environ.get("HSK_NVCC_EXTRA", "").split()
 
 
 def nvcc() -> str:

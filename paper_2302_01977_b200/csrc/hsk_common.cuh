@@ -40,8 +40,10 @@ inline cudaStream_t as_stream(void *s) { return reinterpret_cast<cudaStream_t>(s
 // 2-D float64 TMA descriptor over a column-major matrix: inner dimension =
 // rows (contiguous), outer = columns, row stride lda*8 bytes (multiple of 16).
 // Out-of-bounds box elements are zero-filled by the TMA unit.
+// swizzle128: 128-byte TMA swizzle (16-byte chunk c of each 128-byte row r of
+// the box lands at chunk c ^ (r % 8); needs a 1024-byte aligned destination).
 int make_tmap_f64_2d(CUtensorMap *map, const void *base, uint64_t rows, uint64_t cols,
-                     uint64_t lda, uint32_t box_rows, uint32_t box_cols);
+                     uint64_t lda, uint32_t box_rows, uint32_t box_cols, bool swizzle128 = false);
 
 // ------------------------------------------------------------ PTX helpers
 __device__ __forceinline__ uint32_t smem_u32(const void *p) {

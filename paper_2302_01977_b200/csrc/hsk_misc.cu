@@ -33,7 +33,7 @@ int cuda_status(cudaError_t e, const char *what) {
 }
 
 int make_tmap_f64_2d(CUtensorMap *map, const void *base, uint64_t rows, uint64_t cols,
-                     uint64_t lda, uint32_t box_rows, uint32_t box_cols) {
+                     uint64_t lda, uint32_t box_rows, uint32_t box_cols, bool swizzle128) {
     static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
     if (!encode) {
         void *fn = nullptr;
@@ -49,7 +49,8 @@ int make_tmap_f64_2d(CUtensorMap *map, const void *base, uint64_t rows, uint64_t
     cuuint32_t estr[2] = {1, 1};
     CUresult r = encode(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<void *>(base), dims,
                         strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                        CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                        swizzle128 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_NONE,
+                        CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                         CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) return set_error(HSK_ECUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
     return HSK_OK;

@@ -37,6 +37,16 @@
 #include "hsk_common.cuh"
 #include "hsk_sjlt_pipe.cuh"
 
+// Diagnostic builds only (-DHSK_SJLT_DEBUG=1, then HSK_SJLT_DBG=<mode> at run
+// time): 1 = producers only (consumers skip the walk), 2 = consumers only (no
+// refills after the first ring fill; results are garbage), 3 = checked bucket
+// bounds and stream-K roles (device printf).  Production kernels compile none
+// of it -- the extra live values cost registers the walker needs.
+#ifndef HSK_SJLT_DEBUG
+#define HSK_SJLT_DEBUG 0
+#endif
+#define DBG_IS(m) (HSK_SJLT_DEBUG && p.dbg == (m))
+
 namespace hsk {
 namespace sjlt {
 
@@ -66,8 +76,9 @@ struct Geom {
 
 static inline int64_t roundup(int64_t x, int64_t m) { return (x + m - 1) / m * m; }
 
-static inline int stage_bytes_for(int tk, int tm, int alpha) {
-    return tk * tm * 8 + tm * 8 + 1152 + (tk * alpha + 8) * 4;
+static inline int stage_bytes_for(int tk, int tm, int alpha) {  // mirrors launch<>()
+    const int64_t tile = ((int64_t)(tk + 15) / 16 * 16 * tm * 8 + 1023) / 1024 * 1024;
+    return (int)((tile + 1152 + ((int64_t)tk * alpha + 8) * 4 + 1023) / 1024 * 1024);
 }
 
 // largest power-of-two TK <= cap whose stage fits `per_stage` bytes
@@ -90,7 +101,7 @@ static Geom geom_dir(int64_t n, int d, int alpha, int trans, int64_t base) {
     Geom g;
     int tk;
     // per-stage budgets: 3 stages (or 2) of the 226 KB ring
-    constexpr int kStage3 = (226 * 1024 - 256) / 3, kStage2 = (226 * 1024 - 256) / 2;
+    constexpr int kStage3 = (226 * 1024 - 2048) / 3, kStage2 = (226 * 1024 - 2048) / 2;
     // S over long rows (n >= 8192): two stages of the largest TK -- more
     // entries per bucket visit (lambda = TK*alpha/d) and fewer chunk
     // boundaries outweigh the shallower ring (the dedicated producer warp
@@ -135,11 +146,24 @@ static Plan plan_geom(int64_t n, int d, int alpha) {
 }
 
 // ------------------------------------------------------------ plan build
+// Entry word for input index kk of a chunk (sign in bit 31, or-ed in):
+//   S  tiles (tm_t = 0):  kk << 3  -- the walker forms kk*TM*8 with one shift-add
+//                                     (bit 31 shifts out)
+//   S' tiles (tm_t = TM): (kk/16)*TM*128 + (kk%16)*8 -- the byte offset of (kk, col 0)
+//                         in the TMA S' tile layout (below); a lane's address is
+//                         base_lane + ((e ^ 16*(lane%8)) & 0x7fffffff): one LOP3 + add
+//   S' tiles (tm_t = -TM, transposed layout of 128-row tiles): kk*TM*8 | (kk%32)*8 --
+//                         lane address st + ((e ^ 8*lane) & 0x7fffffff)
+__host__ __device__ inline uint32_t entry_word(uint32_t kk, int tm_t) {
+    if (tm_t < 0) return kk * (uint32_t)(-tm_t) * 8u + ((kk & 31u) << 3);
+    return tm_t ? (kk >> 4) * (uint32_t)tm_t * 128u + ((kk & 15u) << 3) : kk << 3;
+}
+
 // One CTA per chunk: sort the chunk's (bucket, local index) keys, emit
 // entry words in that order and per-bucket lower bounds.
 __global__ void sjlt_plan_kernel(const int32_t *__restrict__ pos, const int8_t *__restrict__ sgn,
                                  int64_t n, int d, int alpha, int tk, int p2, int64_t bstride,
-                                 int64_t estride, uint16_t *__restrict__ bptr,
+                                 int64_t estride, int tm_t, uint16_t *__restrict__ bptr,
                                  uint32_t *__restrict__ ent, int *err) {
     extern __shared__ uint32_t keys[];
     const int64_t c = blockIdx.x;
@@ -177,11 +201,13 @@ __global__ void sjlt_plan_kernel(const int32_t *__restrict__ pos, const int8_t *
     }
     uint32_t *e_out = ent + c * estride;
     for (int e = threadIdx.x; e < estride; e += blockDim.x) {
-        uint32_t w = (uint32_t)tk << 3;  // padding: the zero row
+        // padding (a partial last chunk): the pipelined walk may load, never
+        // accumulate, the word after a warp's list -- it must address the tile
+        uint32_t w = 0u;
         if (e < cnt) {
             const int local = keys[e] & 4095;
-            const uint32_t kk = (uint32_t)(local / alpha);
-            w = (kk << 3) | (sgn[q0 + local] < 0 ? 0x80000000u : 0u);
+            w = entry_word((uint32_t)(local / alpha), tm_t) |
+                (sgn[q0 + local] < 0 ? 0x80000000u : 0u);
         }
         e_out[e] = w;
     }
@@ -209,8 +235,16 @@ __global__ void sjlt_plan_kernel(const int32_t *__restrict__ pos, const int8_t *
 //
 // Lane -> tile rows.  S tiles (dense, TMA-written): RPT = 2 -> rows 2l, 2l+1
 // (one LDS.128); RPT = 4 -> rows 2l, 2l+1, 64+2l, 64+2l+1 (two LDS.128, each
-// a contiguous 512 B).  S' tiles (swizzled, element (kk,row) at
-// kk*TM + (row ^ (kk%32))): rows l + 32 r (LDS.64 each, conflict-free).
+// a contiguous 512 B).
+// S' tiles (32/64 rows) hold A's natural layout (k contiguous) as TMA writes
+// it: blocks of 16 input indices, one 128-byte row per output row, 128-byte
+// swizzle -- element (kk, c) at (kk/16)*TM*128 + c*128 + ((kk%16)*8 ^ 16*(c%8)).
+// Lane l owns output rows c = l + 32 r (LDS.64 each; 8-byte columns of a TMA
+// tile cannot be spread over all 16 bank pairs, so these loads are 2-way
+// conflicted -- the price of a transposition-free TMA producer).
+// S' tiles of 128 rows (d <= 64: alpha-heavy, consumer-bound) are instead
+// transposed on the way in by four cp.async producer warps: element (kk, c)
+// at kk*TM + (c ^ (kk%32)) doubles -- conflict-free for the consumer.
 
 struct ApplyArgs {
     const double *A;
@@ -245,16 +279,20 @@ struct ApplyArgs {
 // warp 0 / lane 0 issues TMA + bulk copies (mode 0); in modes 1/2 every lane
 // issues its share of 8-byte cp.async for the chunk STAGES-1 ahead.
 template <int RPT, int DB, int NW, bool TRANS, bool PROD, bool SK>
-__global__ void __launch_bounds__((NW + (PROD ? (TRANS ? 4 : 1) : 0)) * 32, 1)
+__global__ void __launch_bounds__((NW + (PROD ? (TRANS && RPT == 4 ? 4 : 1) : 0)) * 32, 1)
     sjlt_apply_kernel(const ApplyArgs p, const __grid_constant__ CUtensorMap tmap) {
     constexpr int TM = 32 * RPT;
     constexpr int SLAB = NW * DB;
+    constexpr bool XPOSE = TRANS && RPT == 4;       // transposed S' tile layout
+    constexpr int PW = PROD ? (XPOSE ? 4 : 1) : 0;  // dedicated producer warps
     extern __shared__ __align__(128) unsigned char smem[];
     uint64_t *full = reinterpret_cast<uint64_t *>(smem);
     uint64_t *empty = full + 8;
     unsigned *done = reinterpret_cast<unsigned *>(full + 16);  // per-slot finished-warp counters
     int *sk = reinterpret_cast<int *>(smem + 192);  // stream-K roles (below)
-    unsigned char *stage0 = smem + 256;
+    // stage ring from the first 1024-byte boundary past the 256-byte header
+    // (the S' tile layout relies on the TMA 128-byte swizzle pattern)
+    unsigned char *stage0 = smem + ((((smem_u32(smem) + 256u + 1023u) & ~1023u)) - smem_u32(smem));
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int ks = p.ksplit;
@@ -288,26 +326,25 @@ __global__ void __launch_bounds__((NW + (PROD ? (TRANS ? 4 : 1) : 0)) * 32, 1)
     const uint32_t en_bytes = (uint32_t)p.estride * 4;
     const uint32_t tile_bytes = (uint32_t)p.tk * TM * 8;
 
-    // zero rows + null entries, barriers
+    // null words after each chunk's list: the pipelined walk loads (never
+    // accumulates) up to two entries past a warp's list -- they only need to
+    // address the tile
     for (int s = 0; s < stages; ++s) {
         unsigned char *st = stage0 + (size_t)s * p.stage_bytes;
-        double *zr = reinterpret_cast<double *>(st + p.zero_off);
-        for (int q = threadIdx.x; q < TM; q += blockDim.x) zr[q] = 0.0;
-        // two null entries after the chunk's list (the pipelined walk reads
-        // up to two entries past a warp's list)
-        if (threadIdx.x < 8)
-            reinterpret_cast<uint32_t *>(st + p.en_off)[p.estride + threadIdx.x] = (uint32_t)p.tk << 3;
+        if (threadIdx.x < 8) reinterpret_cast<uint32_t *>(st + p.en_off)[p.estride + threadIdx.x] = 0u;
     }
+    const bool tma = mode == 0 || mode == 3;
     if (threadIdx.x == 0) {
-        constexpr int PW = PROD ? (TRANS ? 4 : 1) : 0;  // dedicated producer warps
-        const uint32_t fcount = mode == 0 ? 1u : 1u + 32u * (PROD ? PW : NW);
+        // TMA modes: one arrival (expect_tx); cp.async modes: every thread
+        // of the (consumer) warps that share the copies, plus the issuer
+        const uint32_t fcount = tma ? 1u : 1u + 32u * (PROD ? PW : NW);
         for (int s = 0; s < stages; ++s) {
             mbar_init(&full[s], fcount);
             mbar_init(&empty[s], NW);
             done[s] = 0;
         }
         fence_mbar_init();
-        if (mode == 0) prefetch_tmap(&tmap);
+        if (tma) prefetch_tmap(&tmap);
         if (SK) {
             // sk[0]: the first segment is the tail of a tile (publish it);
             // sk[1], sk[2]: the last segment is the head of a tile cut by the
@@ -322,6 +359,10 @@ __global__ void __launch_bounds__((NW + (PROD ? (TRANS ? 4 : 1) : 0)) * 32, 1)
             sk[1] = nq;
             sk[2] = (int)((grp + 1) * p.nslabs + slab);
             sk[3] = (int)tile0;
+            if (DBG_IS(3))
+                printf("sjlt dbg: cta %d grp %lld u0 %lld u1 %lld nloc %d sk %d %d %d %d stages %d\n",
+                       (int)blockIdx.x, (long long)grp, (long long)u0, (long long)u1, nloc, sk[0], sk[1],
+                       sk[2], sk[3], stages);
         }
     }
     __syncthreads();
@@ -347,7 +388,12 @@ __global__ void __launch_bounds__((NW + (PROD ? (TRANS ? 4 : 1) : 0)) * 32, 1)
         int64_t r0, c;
         chunk_of(j, r0, c);
         mbar_arrive_expect_tx(bar, tile_bytes + bp_bytes + en_bytes);
-        tma_load_2d(st, &tmap, (int)r0, (int)(c * p.tk), bar);
+        if constexpr (TRANS) {  // S': one 16 x TM box per 16 input indices
+            for (int kb = 0; kb < p.tk / 16; ++kb)
+                tma_load_2d(st + kb * TM * 128, &tmap, (int)(c * p.tk + kb * 16), (int)r0, bar);
+        } else {
+            tma_load_2d(st, &tmap, (int)r0, (int)(c * p.tk), bar);
+        }
         // keep the HBM stream ahead of the ring: chunk j + pf into L2 (chunks
         // stages .. stages+pf-1 are requested together with the first loads)
         const int jp = j < stages ? j + stages : j + p.pf;
@@ -373,11 +419,9 @@ __global__ void __launch_bounds__((NW + (PROD ? (TRANS ? 4 : 1) : 0)) * 32, 1)
         }
         double *sx = reinterpret_cast<double *>(st);
         const int nel = p.tk * TM;
-        if (TRANS) {
-            // element (kk, rr) = A[k0+kk, r0+rr] -> sx[kk*TM + (rr ^ (kk%32))];
-            // lanes along kk: coalesced reads, conflict-free swizzled writes.
-            // Thread t owns columns kk = t, t + pnt, ... and walks all TM rows
-            // with pointer increments (lanes along kk: 256 B per instruction).
+        if (XPOSE) {
+            // (kk, rr) = A[k0+kk, r0+rr] -> sx[kk*TM + (rr ^ (kk%32))]; lanes
+            // along kk: coalesced reads, conflict-free swizzled writes
             const int tk = p.tk;
             const bool full_rows = r0 + TM <= p.m_out;
             for (int kk = ptid; kk < tk; kk += pnt) {
@@ -393,6 +437,20 @@ __global__ void __launch_bounds__((NW + (PROD ? (TRANS ? 4 : 1) : 0)) * 32, 1)
                         const bool v = vk && (r0 + rr < p.m_out);
                         cp_async8(dbase + (rr ^ sw), v ? src : p.A, v);
                     }
+                }
+            }
+        } else if (TRANS) {
+            // unaligned A: the S' tile layout of the TMA path, written by
+            // 8-byte cp.async -- (kk, rr) at (kk/16)*TM*128 + rr*128 +
+            // ((kk%16)*8 ^ 16*(rr%8)); lanes along kk (coalesced reads)
+            const int tk = p.tk;
+            for (int kk = ptid; kk < tk; kk += pnt) {
+                const double *src = p.A + r0 * p.lda + k0 + kk;
+                unsigned char *dbase = st + (kk >> 4) * TM * 128 + ((kk & 15) << 3);
+                const bool vk = kk < kc;
+                for (int rr = 0; rr < TM; ++rr, src += p.lda) {
+                    const bool v = vk && (r0 + rr < p.m_out);
+                    cp_async8(dbase + ((rr * 128) ^ ((rr & 7) << 4)), v ? src : p.A, v);
                 }
             }
         } else {
@@ -411,18 +469,18 @@ __global__ void __launch_bounds__((NW + (PROD ? (TRANS ? 4 : 1) : 0)) * 32, 1)
         // dedicated producer warp(s): refill a slot as soon as every consumer
         // warp has released it (mode 0: one TMA-issuing lane; modes 1/2: the
         // producer warps share the 8-byte transposing copies)
-        if (warp >= NW) {
-            constexpr int PW = TRANS ? 4 : 1;
-            if (mode == 0) {
-                if (lane == 0 && warp == NW) {
-                    for (int j = 0; j < nloc; ++j) {
+        if (warp >= NW) {  // one TMA-issuing lane, or PW warps of transposing copies
+            const int jn = DBG_IS(2) && nloc > stages ? stages : nloc;
+            if (tma) {
+                if (lane == 0) {
+                    for (int j = 0; j < jn; ++j) {
                         if (j >= stages) mbar_wait(&empty[j % stages], (uint32_t)((j / stages) - 1) & 1u);
                         issue_tma(j);
                     }
                 }
             } else {
                 const int ptid = threadIdx.x - NW * 32;
-                for (int j = 0; j < nloc; ++j) {
+                for (int j = 0; j < jn; ++j) {
                     if (j >= stages) mbar_wait(&empty[j % stages], (uint32_t)((j / stages) - 1) & 1u);
                     issue_coop(j, ptid, PW * 32);
                 }
@@ -435,7 +493,7 @@ __global__ void __launch_bounds__((NW + (PROD ? (TRANS ? 4 : 1) : 0)) * 32, 1)
             }
             return;
         }
-    } else if (mode == 0) {
+    } else if (tma) {
         if (warp == 0 && lane == 0)
             for (; issued < nloc && issued < stages; ++issued) issue_tma(issued);
     } else {
@@ -449,8 +507,10 @@ __global__ void __launch_bounds__((NW + (PROD ? (TRANS ? 4 : 1) : 0)) * 32, 1)
         for (int jj = 0; jj < DB; ++jj) acc[r][jj] = 0.0;
 
     const uint32_t smem_base = smem_u32(stage0);
-    const uint32_t lane8 = lane * 8u;
-    const uint32_t lane_off = TRANS ? 0u : lane * 8u * (RPT == 1 ? 1u : 2u);  // S: rows 2l,2l+1 (+64) / l
+    // S' swizzle term of rows l + 32 r (TMA layout: 16-byte chunk; transposed: 8 bytes)
+    const uint32_t lanex = XPOSE ? lane * 8u : (uint32_t)(lane & 7) << 4;
+    // S: rows 2l, 2l+1 (+64) / l;  S': row l (TMA layout: 128 bytes per row)
+    const uint32_t lane_off = XPOSE ? 0u : TRANS ? lane * 128u : lane * 8u * (RPT == 1 ? 1u : 2u);
     // epilogue: one final scaling, as the reference (`out *= scale`)
     auto store_tile = [&](const int64_t r0) {
     const bool vec_ok = ((p.lds & 1) == 0) && ((reinterpret_cast<uintptr_t>(p.S) & 15) == 0);
@@ -495,7 +555,7 @@ __global__ void __launch_bounds__((NW + (PROD ? (TRANS ? 4 : 1) : 0)) * 32, 1)
     for (int i = 0; i < nloc; ++i) {
         // ---- producer duty (modes 1/2): chunk i + stages - 1 into the slot of
         // chunk i - 1, once every warp has finished chunk i - 1
-        if (!PROD && mode != 0 && issued < nloc) {
+        if (!PROD && !tma && issued < nloc) {
             const int j = issued;
             if (j >= stages) mbar_wait(&empty[j % stages], (uint32_t)((j / stages) - 1) & 1u);
             issue_coop(j, threadIdx.x, NW * 32);
@@ -504,13 +564,15 @@ __global__ void __launch_bounds__((NW + (PROD ? (TRANS ? 4 : 1) : 0)) * 32, 1)
 
         // ---- consume chunk i
         const int s = cs;
-        if (p.dbg != 2 || i < stages) mbar_wait(&full[s], cph);
+        if (!DBG_IS(2) || i < stages) mbar_wait(&full[s], cph);
         const uint32_t st = smem_base + (uint32_t)s * p.stage_bytes;
         const uint32_t sx = st + lane_off;
         const uint32_t sen = st + p.en_off;
         const uint16_t *sbp = reinterpret_cast<const uint16_t *>(
                                   stage0 + (size_t)s * p.stage_bytes + p.bp_off) + warp * DB;
-        // the warp's DB+1 bucket bounds (packed u16 pairs)
+        // the warp's DB+1 bucket bounds (packed u16 pairs), streamed by the walker
+        const uint32_t sbw = st + (uint32_t)p.bp_off + (uint32_t)(warp * DB * 2);
+#if HSK_SJLT_DEBUG
         constexpr int NBW = DB / 2 + 1;
         uint32_t bw[NBW];
         {
@@ -518,33 +580,48 @@ __global__ void __launch_bounds__((NW + (PROD ? (TRANS ? 4 : 1) : 0)) * 32, 1)
 #pragma unroll
             for (int q = 0; q < NBW; ++q) bw[q] = src[q];
         }
-        if (p.dbg == 1) {
+#endif
+#if HSK_SJLT_DEBUG
+        if (DBG_IS(3)) {  // checked mode: bucket bounds of this warp
+            uint32_t prev = 0;
+            for (int jj = 0; jj <= DB; ++jj) {
+                const uint32_t b = (jj & 1) ? (bw[jj >> 1] >> 16) : (bw[jj >> 1] & 0xffffu);
+                if (b < prev || b > (uint32_t)p.estride) {
+                    printf("sjlt dbg: cta %d warp %d chunk-iter %d bucket %d bound %u prev %u estride %d\n",
+                           (int)blockIdx.x, warp, i, jj, b, prev, (int)p.estride);
+                    __trap();
+                }
+                prev = b;
+            }
+        }
+#endif
+        if (DBG_IS(1)) {
         } else if constexpr (TRANS) {
-            if constexpr (RPT == 1 && DB == 16) pipe_t_1x16(acc, sen, st, lane8, bw);
-            else if constexpr (RPT == 1 && DB == 32) pipe_t_1x32(acc, sen, st, lane8, bw);
-            else if constexpr (RPT == 2 && DB == 4) pipe_t_2x4(acc, sen, st, lane8, bw);
-            else if constexpr (RPT == 2 && DB == 8) pipe_t_2x8(acc, sen, st, lane8, bw);
-            else if constexpr (RPT == 2 && DB == 16) pipe_t_2x16(acc, sen, st, lane8, bw);
-            else if constexpr (RPT == 4 && DB == 2) pipe_t_4x2(acc, sen, st, lane8, bw);
-            else if constexpr (RPT == 4 && DB == 4) pipe_t_4x4(acc, sen, st, lane8, bw);
-            else if constexpr (RPT == 4 && DB == 8) pipe_t_4x8(acc, sen, st, lane8, bw);
+            if constexpr (RPT == 1 && DB == 16) pipe_t_1x16(acc, sen, sx, lanex, sbw);
+            else if constexpr (RPT == 1 && DB == 32) pipe_t_1x32(acc, sen, sx, lanex, sbw);
+            else if constexpr (RPT == 2 && DB == 4) pipe_t_2x4(acc, sen, sx, lanex, sbw);
+            else if constexpr (RPT == 2 && DB == 8) pipe_t_2x8(acc, sen, sx, lanex, sbw);
+            else if constexpr (RPT == 2 && DB == 16) pipe_t_2x16(acc, sen, sx, lanex, sbw);
+            else if constexpr (RPT == 4 && DB == 2) pipe_t_4x2(acc, sen, sx, lanex, sbw);
+            else if constexpr (RPT == 4 && DB == 4) pipe_t_4x4(acc, sen, sx, lanex, sbw);
+            else if constexpr (RPT == 4 && DB == 8) pipe_t_4x8(acc, sen, sx, lanex, sbw);
         } else {
-            if constexpr (RPT == 1 && DB == 16) pipe_s_1x16(acc, sen, sx, bw);
-            else if constexpr (RPT == 1 && DB == 32) pipe_s_1x32(acc, sen, sx, bw);
-            else if constexpr (RPT == 2 && DB == 4) pipe_s_2x4(acc, sen, sx, bw);
-            else if constexpr (RPT == 2 && DB == 8) pipe_s_2x8(acc, sen, sx, bw);
-            else if constexpr (RPT == 2 && DB == 16) pipe_s_2x16(acc, sen, sx, bw);
-            else if constexpr (RPT == 4 && DB == 2) pipe_s_4x2(acc, sen, sx, bw);
-            else if constexpr (RPT == 4 && DB == 4) pipe_s_4x4(acc, sen, sx, bw);
-            else if constexpr (RPT == 4 && DB == 8) pipe_s_4x8(acc, sen, sx, bw);
+            if constexpr (RPT == 1 && DB == 16) pipe_s_1x16(acc, sen, sx, sbw);
+            else if constexpr (RPT == 1 && DB == 32) pipe_s_1x32(acc, sen, sx, sbw);
+            else if constexpr (RPT == 2 && DB == 4) pipe_s_2x4(acc, sen, sx, sbw);
+            else if constexpr (RPT == 2 && DB == 8) pipe_s_2x8(acc, sen, sx, sbw);
+            else if constexpr (RPT == 2 && DB == 16) pipe_s_2x16(acc, sen, sx, sbw);
+            else if constexpr (RPT == 4 && DB == 2) pipe_s_4x2(acc, sen, sx, sbw);
+            else if constexpr (RPT == 4 && DB == 4) pipe_s_4x4(acc, sen, sx, sbw);
+            else if constexpr (RPT == 4 && DB == 8) pipe_s_4x8(acc, sen, sx, sbw);
         }
         __syncwarp();
         if (lane == 0) {
-            if (mode == 0 && !PROD) {
+            if (tma && !PROD) {
                 // the last warp to finish chunk i refills its slot with chunk i + stages
                 if (atomicAdd(&done[s], 1u) == NW - 1) {
                     done[s] = 0;
-                    if (i + stages < nloc && p.dbg != 2) issue_tma(i + stages);
+                    if (i + stages < nloc && !DBG_IS(2)) issue_tma(i + stages);
                 }
             } else {
                 mbar_arrive(&empty[s]);
@@ -633,7 +710,10 @@ static int launch(ApplyArgs a, const Geom &g, cudaStream_t st) {
     constexpr int SLAB = NW * DB;
     HSK_REQUIRE(g.tm == TM, HSK_EINVAL, "sjlt: plan/config mismatch");
     const bool aligned = a.use_tma != 0;  // 16-byte aligned columns (lda even)
-    a.mode = a.trans ? 1 : (aligned ? 0 : 2);
+    // 0: TMA S tile; 1: cp.async S' tile (unaligned A); 2: cp.async S tile;
+    // 3: TMA S' tile (16 x TM boxes, 128-byte swizzle)
+    constexpr bool XPOSE = RPT == 4;  // (for S') transposed tile, cp.async producer
+    a.mode = a.trans ? (!XPOSE && aligned && a.tk % 16 == 0 ? 3 : 1) : (aligned ? 0 : 2);
     a.log2tk = 0;
     while ((1 << a.log2tk) < a.tk) ++a.log2tk;
     CUtensorMap tmap;
@@ -642,12 +722,18 @@ static int launch(ApplyArgs a, const Geom &g, cudaStream_t st) {
         int rc = make_tmap_f64_2d(&tmap, a.A, (uint64_t)a.m_out, (uint64_t)a.n, (uint64_t)a.lda,
                                   TM, (uint32_t)a.tk);
         if (rc) return rc;
+    } else if (a.mode == 3) {  // A is n x m_out: inner dimension = input index
+        int rc = make_tmap_f64_2d(&tmap, a.A, (uint64_t)a.n, (uint64_t)a.m_out, (uint64_t)a.lda,
+                                  16, TM, true);
+        if (rc) return rc;
     }
-    const int a_bytes = a.tk * TM * 8;
-    a.zero_off = a_bytes;
-    a.bp_off = (int)roundup(a_bytes + TM * 8, 128);
+    // S' tiles occupy whole 16-index blocks (the layout's unit); ring slots
+    // start on 1024-byte boundaries
+    const int a_bytes = (int)roundup((a.trans ? roundup(a.tk, 16) : a.tk) * (int64_t)TM * 8, 1024);
+    a.zero_off = 0;
+    a.bp_off = a_bytes;
     a.en_off = (int)roundup(a.bp_off + (SLAB + 8) * 2, 128);
-    a.stage_bytes = (int)roundup(a.en_off + (a.estride + 8) * 4, 128);
+    a.stage_bytes = (int)roundup(a.en_off + (a.estride + 8) * 4, 1024);
     a.nslabs = (a.d + SLAB - 1) / SLAB;
     const int64_t tiles = (a.m_out + TM - 1) / TM;
     // k-split across a cluster when the tile grid cannot fill the GPU
@@ -663,7 +749,8 @@ static int launch(ApplyArgs a, const Geom &g, cudaStream_t st) {
     // from the last consumer warp to release a slot instead
     bool prod = NW < 32;
     if (const char *env = getenv("HSK_SJLT_PROD")) prod = env[0] == '1';
-    prod = prod && (a.mode == 0 || a.mode == 1) && NW + (a.trans ? 4 : 1) <= 32;
+    const int pw = a.trans && XPOSE ? 4 : 1;
+    prod = prod && (a.mode == 0 || a.mode == 3 || (a.mode == 1 && XPOSE)) && NW + pw <= 32;
     // persistent balanced schedule (stream-K) when whole-tile CTAs would
     // leave a partial last wave: one CTA per SM, groups of nslabs CTAs (the
     // slabs of a row tile stay in lockstep, so A is read from HBM once)
@@ -689,11 +776,11 @@ static int launch(ApplyArgs a, const Geom &g, cudaStream_t st) {
     a.ksplit = ks;
     const int per = (int)(a.streamk ? (a.units + a.groups - 1) / a.groups : (a.nchunks + ks - 1) / ks);
     const int budget = 226 * 1024;
-    a.stages = std::max(2, std::min(8, (budget - 256) / a.stage_bytes));
+    a.stages = std::max(2, std::min(8, (budget - 2048) / a.stage_bytes));
     if (const char *env = getenv("HSK_SJLT_STAGES")) a.stages = std::max(2, std::min(a.stages, atoi(env)));
     if (per > 0 && a.stages > per + 1) a.stages = std::max(2, per + 1);
-    int smem = 256 + a.stages * a.stage_bytes;
-    if (ks > 1) smem = std::max(smem, 256 + NW * DB * RPT * 32 * 8);
+    int smem = 2048 + a.stages * a.stage_bytes;  // header + 1024-byte alignment slack
+    if (ks > 1) smem = std::max(smem, 2048 + NW * DB * RPT * 32 * 8);
     auto kern = a.trans ? (prod ? (a.streamk ? sjlt_apply_kernel<RPT, DB, NW, true, true, true>
                                              : sjlt_apply_kernel<RPT, DB, NW, true, true, false>)
                                 : (a.streamk ? sjlt_apply_kernel<RPT, DB, NW, true, false, true>
@@ -705,7 +792,7 @@ static int launch(ApplyArgs a, const Geom &g, cudaStream_t st) {
     a.pf = a.mode == 0 ? 2 : 0;
     a.dbg = getenv("HSK_SJLT_DBG") ? atoi(getenv("HSK_SJLT_DBG")) : 0;
     if (const char *env = getenv("HSK_SJLT_PF")) a.pf = std::max(0, atoi(env));
-    const int nthreads = (NW + (prod ? (a.trans ? 4 : 1) : 0)) * 32;
+    const int nthreads = (NW + (prod ? pw : 0)) * 32;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e != cudaSuccess) return cuda_status(e, "sjlt: set smem attribute");
     const int64_t grid = a.streamk ? (int64_t)a.groups * a.nslabs : tiles * a.nslabs * ks;
@@ -769,6 +856,7 @@ extern "C" int hsk_sjlt_plan_build(const int32_t *pos, const int8_t *sgn, int64_
             while (p2 < g->tk * alpha) p2 <<= 1;
             sjlt::sjlt_plan_kernel<<<(unsigned)g->nchunks, 256, p2 * sizeof(uint32_t), st>>>(
                 pos, sgn, n, d, alpha, g->tk, p2, g->bstride, g->estride,
+                g == &pl.t ? (g->rpt == 4 ? -g->tm : g->tm) : 0,
                 reinterpret_cast<uint16_t *>(base + g->bptr_off),
                 reinterpret_cast<uint32_t *>(base + g->ent_off), reinterpret_cast<int *>(base + 28));
             HSK_CHECK_LAUNCH("sjlt_plan_kernel");

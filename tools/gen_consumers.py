@@ -17,7 +17,13 @@ one word past the warp's list: the kernel keeps null words (pointing at a zero
 row) after each chunk's list.
 
   S  tiles (dense, TMA):  row 2l(+1) of lane l at  sx + kk*TM*8          (RPT 2)
-  S' tiles (swizzled):    row l+32r at  st + kk*TM*8 + (8l ^ 8(kk%32)) + 256r
+                          entry word e = kk << 3 | sign << 31
+  S' tiles (TMA, 128-B swizzle): (kk, c) at (kk/16)*TM*128 + 128c + ((kk%16)*8 ^ 16(c%8))
+                          entry word e = (kk/16)*TM*128 + (kk%16)*8 | sign << 31;
+                          row c = l + 32r at st + 128l + ((e ^ 16(l%8)) & 0x7fffffff) + 4096r
+  S' 128-row tiles (transposed, cp.async): (kk, c) at kk*TM*8 + 8(c ^ kk%32);
+                          e = kk*TM*8 | 8(kk%32) | sign << 31;
+                          row c = l + 32r at st + ((e ^ 8l) & 0x7fffffff) + 256r
 
 Usage: python tools/gen_consumers.py > paper_2302_01977_b200/csrc/hsk_sjlt_pipe.cuh
 """
@@ -38,21 +44,25 @@ def gen(rpt, db, trans, vote=False):
     a = L.append
     sen, base = nacc, nacc + 1
     lane8 = nacc + 2 if trans else None
-    bw0 = nacc + (3 if trans else 2)
+    sbw = nacc + (3 if trans else 2)  # shared address of the warp's packed u16 bounds
+    nw = db // 2 + 1                  # bound words (bounds 2q, 2q+1 in word q)
     a(".reg .pred p, q;")
     a(".reg .b32 pe, pend, pnx, t, ad, e, gh, zero, one;")
+    a(".reg .b32 " + ", ".join(f"w{k}" for k in range(nw)) + ";")
     a(".reg .f64 " + ", ".join(f"u{r}" for r in range(rpt)) + ", g;")
     a("mov.b32 zero, 0;")
     a("mov.b32 one, 1072693248;")
 
     def load_tile():
-        out = [f"shl.b32 t, e, {sh};"]
         if trans:
-            out += ["and.b32 ad, e, 248;", f"xor.b32 ad, ad, %{lane8};", "add.u32 ad, ad, t;",
-                    f"add.u32 ad, ad, %{base};"]
-            out += [f"ld.shared.f64 u{r}, [ad+{256 * r}];" for r in range(rpt)]
+            # e = (kk/16)*TM*128 + (kk%16)*8 | sign: (e ^ 16*(lane%8)) & 0x7fffffff in
+            # one LOP3 (lut 0x28); base = tile + 128*lane; rows l + 32 r at +4096 r
+            out = [f"lop3.b32 ad, e, %{lane8}, 2147483647, 0x28;", f"add.u32 ad, ad, %{base};"]
+            # 128-row S' tiles use the transposed layout (rows l + 32 r at +256 r)
+            stride = 256 if rpt == 4 else 4096
+            out += [f"ld.shared.f64 u{r}, [ad+{stride * r}];" for r in range(rpt)]
         else:
-            out += [f"add.u32 ad, t, %{base};"]
+            out = [f"shl.b32 t, e, {sh};", f"add.u32 ad, t, %{base};"]
             if rpt == 1:
                 out += ["ld.shared.f64 u0, [ad];"]
             else:
@@ -62,9 +72,9 @@ def gen(rpt, db, trans, vote=False):
         out += ["lop3.b32 gh, e, -2147483648, one, 0xEA;", "mov.b64 g, {zero, gh};"]
         return out
 
-    def bound_to(dst, jj):  # dst = sen + 4 * bound(jj); bound(jj) in bw[jj >> 1] lo/hi
-        w = bw0 + (jj >> 1)
-        return [(f"and.b32 t, %{w}, 65535;" if jj % 2 == 0 else f"shr.u32 t, %{w}, 16;"),
+    def bound_to(dst, b):  # dst = sen + 4 * bound(b); bound(b) in word b >> 1, lo/hi half
+        w = f"w{b >> 1}"
+        return [(f"and.b32 t, {w}, 65535;" if b % 2 == 0 else f"shr.u32 t, {w}, 16;"),
                 f"mad.lo.u32 {dst}, t, 4, %{sen};"]
 
     def branch(pred, label):
@@ -72,6 +82,12 @@ def gen(rpt, db, trans, vote=False):
             return [f"vote.sync.any.pred {pred}, {pred}, -1;", f"@{pred} bra.uni {label};"]
         return [f"@{pred} bra.uni {label};"]
 
+    # bound words stream in two buckets ahead of use: word q is first needed at
+    # bucket 2q - 2 (as bound 2q, the end of bucket 2q - 1) and is loaded at
+    # the start of bucket 2q - 4 (words 0 and 1 in the prologue)
+    a(f"ld.shared.b32 w0, [%{sbw}];")
+    if nw > 1:
+        a(f"ld.shared.b32 w1, [%{sbw}+4];")
     # prologue: U, G = entry pe; E = word pe + 1; pend = end of bucket 0
     L.extend(bound_to("pe", 0))
     a("ld.shared.b32 e, [pe];")
@@ -79,6 +95,9 @@ def gen(rpt, db, trans, vote=False):
     a("ld.shared.b32 e, [pe+4];")
     L.extend(bound_to("pend", 1))
     for jj in range(db):
+        if jj % 2 == 0 and jj // 2 + 2 < nw:
+            qn = jj // 2 + 2
+            a(f"ld.shared.b32 w{qn}, [%{sbw}+{4 * qn}];")
         # end of the next bucket, computed off the critical path
         if jj + 1 < db:
             L.extend(bound_to("pnx", jj + 2))
@@ -97,13 +116,11 @@ def gen(rpt, db, trans, vote=False):
             a("mov.b32 pend, pnx;")
     txt = "\\n\\t".join(L)
     outs = ", ".join(f'"+d"(acc[{k % rpt}][{k // rpt}])' for k in range(nacc))
-    nbw = db // 2 + 1
-    ins = ['"r"(sen)', '"r"(base)'] + (['"r"(lane8)'] if trans else []) + \
-        [f'"r"(bw[{q}])' for q in range(nbw)]
+    ins = ['"r"(sen)', '"r"(base)'] + (['"r"(lanex)'] if trans else []) + ['"r"(sbw)']
     name = f"pipe_{'t' if trans else 's'}_{rpt}x{db}"
-    sig = "uint32_t sen, uint32_t base, " + ("uint32_t lane8, " if trans else "")
+    sig = "uint32_t sen, uint32_t base, " + ("uint32_t lanex, " if trans else "")
     return (f"__device__ __forceinline__ void {name}(double (&acc)[{rpt}][{db}], {sig}"
-            f"const uint32_t (&bw)[{nbw}]) {{\n"
+            f"uint32_t sbw) {{\n"
             f'    asm volatile("{{\\n\\t{txt}\\n\\t}}"\n'
             f"                 : {outs}\n"
             f"                 : {', '.join(ins)}\n"
