@@ -102,21 +102,24 @@ static Geom geom_dir(int64_t n, int d, int alpha, int trans, int64_t base) {
     int tk;
     // per-stage budgets: 3 stages (or 2) of the 226 KB ring
     constexpr int kStage3 = (226 * 1024 - 2048) / 3, kStage2 = (226 * 1024 - 2048) / 2;
-    // S over long rows (n >= 8192): two stages of the largest TK -- more
-    // entries per bucket visit (lambda = TK*alpha/d) and fewer chunk
-    // boundaries outweigh the shallower ring (the dedicated producer warp
-    // refills a slot as soon as it is released).  Short rows keep three
-    // power-of-two stages so every CTA still has a deep pipeline.
-    const bool wide = !trans && n >= 8192;
-    if (d <= 64) {                          // 128-row tiles
+    // Long rows (n >= 8192): two stages of the largest TK -- more entries per
+    // bucket visit (lambda = TK*alpha/d) and fewer chunk boundaries outweigh
+    // the shallower ring (the dedicated producer refills a slot as soon as it
+    // is released).  Short rows keep three power-of-two stages so every CTA
+    // still has a deep pipeline.  Tiles: 128 rows for d <= 64, else 64 rows
+    // (measured better than 32-row / 512-bucket slabs even at d = 2048: the
+    // L2 re-reads of more slabs cost less than twice the entry walks).  The
+    // transposing cp.async producer of 128-row S' tiles keeps three stages.
+    // (S with more than two 256-bucket slabs keeps three stages: eight slab
+    // CTAs sharing each tile through L2 want the deeper ring -- measured at
+    // d = 2048, alpha = 8)
+    const bool wide = n >= 8192 && (trans || d <= 512);
+    if (d <= 64) {
         g.rpt = 4;
-        tk = wide ? tk_fit16(alpha, 128, 256, kStage2) : tk_fit(alpha, 128, 128, kStage3);
-    } else if (trans || d <= 512) {         // 64-row tiles
+        tk = wide && !trans ? tk_fit16(alpha, 128, 256, kStage2) : tk_fit(alpha, 128, 128, kStage3);
+    } else {
         g.rpt = 2;
         tk = wide ? tk_fit16(alpha, 64, 256, kStage2) : tk_fit(alpha, 64, 128, kStage3);
-    } else {                                // S, d > 512: 32-row tiles (512-bucket slabs), TK 256
-        g.rpt = 1;
-        tk = tk_fit(alpha, 32, 256, kStage2);
     }
     if (const char *env = getenv(trans ? "HSK_SJLT_TK_T" : "HSK_SJLT_TK")) tk = atoi(env);
     if (const char *env = getenv(trans ? "HSK_SJLT_RPT_T" : "HSK_SJLT_RPT")) g.rpt = atoi(env);
