@@ -161,20 +161,27 @@ __global__ void __launch_bounds__(WGM * WGN * 32) gauss_kernel(const Args p) {
         if (++rs == STAGES) rs = 0;
         const double *sB = sA + SM::A_ELEMS;
         const int fr = lane >> 2, fc = lane & 3;
-#pragma unroll
-        for (int k4 = 0; k4 < BK; k4 += 4) {
-            double a[MF], b[NF];
+        // fragments double-buffered in registers: step k4 + 4's loads are in
+        // flight while step k4's DMMAs issue
+        double a[2][MF], b[2][NF];
+        auto load_frags = [&](int k4, int buf) {
 #pragma unroll
             for (int i = 0; i < MF; ++i) {
                 const int m = wm0 + i * 8 + fr;
-                a[i] = TRANS ? sA[m * PKK + k4 + fc] : sA[(k4 + fc) * SM::PA + m];
+                a[buf][i] = TRANS ? sA[m * PKK + k4 + fc] : sA[(k4 + fc) * SM::PA + m];
             }
 #pragma unroll
-            for (int j = 0; j < NF; ++j) b[j] = sB[(wn0 + j * 8 + fr) * PKK + k4 + fc];
+            for (int j = 0; j < NF; ++j) b[buf][j] = sB[(wn0 + j * 8 + fr) * PKK + k4 + fc];
+        };
+        load_frags(0, 0);
+#pragma unroll
+        for (int k4 = 0; k4 < BK; k4 += 4) {
+            const int cur = (k4 / 4) & 1;
+            if (k4 + 4 < BK) load_frags(k4 + 4, cur ^ 1);
 #pragma unroll
             for (int i = 0; i < MF; ++i)
 #pragma unroll
-                for (int j = 0; j < NF; ++j) dmma(acc[i][j], a[i], b[j]);
+                for (int j = 0; j < NF; ++j) dmma(acc[i][j], a[cur][i], b[cur][j]);
         }
     }
     cp_async_wait<0>();
@@ -246,6 +253,25 @@ extern "C" int hsk_gauss_apply(const double *A, int64_t rows, int64_t cols, int6
     // tensor pipe fed.  HSK_GAUSS_CFG overrides: "128" (128x128, 2x4 warps),
     // "64x128" (2x4 warps).
     const char *cfg = getenv("HSK_GAUSS_CFG");
+    // tuning variants: warp tiles 32x64 / 64x32 (12 fragment loads per 32 DMMA)
+    if (cfg && !strcmp(cfg, "64x128w"))
+        return trans ? gauss::launch<64, 128, 1, 2, 2, 4>(a, st)
+                     : gauss::launch<64, 128, 0, 2, 2, 4>(a, st);
+    if (cfg && !strcmp(cfg, "128x64w"))
+        return trans ? gauss::launch<128, 64, 1, 2, 2, 4>(a, st)
+                     : gauss::launch<128, 64, 0, 2, 2, 4>(a, st);
+    if (cfg && !strcmp(cfg, "128x128w"))
+        return trans ? gauss::launch<128, 128, 1, 2, 2, 3>(a, st)
+                     : gauss::launch<128, 128, 0, 2, 2, 3>(a, st);
+    if (cfg && !strcmp(cfg, "64x64s3"))
+        return trans ? gauss::launch<64, 64, 1, 2, 2, 3>(a, st)
+                     : gauss::launch<64, 64, 0, 2, 2, 3>(a, st);
+    if (cfg && !strcmp(cfg, "64x64s2"))
+        return trans ? gauss::launch<64, 64, 1, 2, 2, 2>(a, st)
+                     : gauss::launch<64, 64, 0, 2, 2, 2>(a, st);
+    if (cfg && !strcmp(cfg, "64x64s6"))
+        return trans ? gauss::launch<64, 64, 1, 2, 2, 6>(a, st)
+                     : gauss::launch<64, 64, 0, 2, 2, 6>(a, st);
     if (cfg && !strcmp(cfg, "128"))
         return trans ? gauss::launch<128, 128, 1, 2, 4, 3>(a, st)
                      : gauss::launch<128, 128, 0, 2, 4, 3>(a, st);
