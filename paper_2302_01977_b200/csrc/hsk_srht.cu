@@ -40,6 +40,7 @@ struct Args {
     int64_t n_pad;
     int seg;         // min(SEG, n_pad)
     const double *signs;
+    const uint16_t *masks;  // seg == 256: per (segment, warp) sign bits of k = w + 16 u
     const int64_t *sample;
     int d;
     double scale;
@@ -52,9 +53,26 @@ struct Args {
 };
 
 constexpr int kMaxStages = 4;
-// smem map: [full barriers 64 B][signs: kMaxStages x SEG doubles][samples]
+// smem map: [full barriers 64 B][signs: kMaxStages x SEG doubles (n_pad < 256) or
+// kMaxStages x 16 u16 sign masks][sorted samples, their columns]
 // [tiles from kTileOff: 1024-byte aligned for the TMA destination]
-constexpr int kTileOff = ((64 + kMaxStages * SEG * 8 + 32 * 32 * 4) + 1023) / 1024 * 1024;
+constexpr int kSampOff = 64 + kMaxStages * SEG * 8;
+constexpr int kTileOff = ((kSampOff + 2 * 32 * 32 * 4) + 1023) / 1024 * 1024;
+
+// Sign masks for 256-element segments: bit u of masks[g*16 + w] is the sign
+// of element g*256 + w + 16u -- what warp w of the kernel's pass A needs, in
+// one 2-byte broadcast instead of 16 double loads.
+__global__ void srht_mask_kernel(const double *__restrict__ signs, int64_t nseg,
+                                 uint16_t *__restrict__ masks) {
+    for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < nseg * 16;
+         q += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t g = q >> 4;
+        const int w = (int)(q & 15);
+        uint32_t m = 0;
+        for (int u = 0; u < 16; ++u) m |= (signs[g * SEG + w + 16 * u] < 0.0 ? 1u : 0u) << u;
+        masks[q] = (uint16_t)m;
+    }
+}
 
 // Segment g of the 32 vectors into X[k][r] (pitch doubles per k) with 8/16-byte
 // cp.async; used when TMA cannot be (S' tiles, unaligned A, n_pad < 256).
@@ -110,7 +128,9 @@ __global__ void __launch_bounds__(NW * 32, 1)
     extern __shared__ __align__(128) unsigned char smem[];
     uint64_t *full = reinterpret_cast<uint64_t *>(smem);
     double *sgn_all = reinterpret_cast<double *>(smem + 64);            // stages x seg doubles
-    int *s_samp = reinterpret_cast<int *>(smem + 64 + kMaxStages * SEG * 8);  // NW*TPW
+    uint16_t *sgm_all = reinterpret_cast<uint16_t *>(smem + 64);        // stages x 16 masks
+    int *s_samp = reinterpret_cast<int *>(smem + kSampOff);             // NW*TPW, sorted per warp
+    int *s_col = s_samp + NW * 32;                                      // their output columns
     double *X0 = reinterpret_cast<double *>(smem + kTileOff);  // 1024-B aligned (TMA)
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int slab = (int)(blockIdx.x % p.nslabs);
@@ -120,9 +140,31 @@ __global__ void __launch_bounds__(NW * 32, 1)
     const int stages = p.stages;
     const bool tma = p.use_tma != 0;
 
-    for (int i = tid; i < NW * TPW; i += NW * 32) {
-        const int t = t0 + i;
-        s_samp[i] = t < p.d ? (int)p.sample[t] : 0;
+    // each warp sorts its TPW samples by position within a segment (s mod
+    // seg) so repeated positions reuse one tile load in the fold
+    {
+        const int t = t0 + warp * TPW + lane;
+        const bool valid = lane < TPW && t < p.d;
+        const int sv = valid ? (int)p.sample[t] : 0;
+        // key: (position, lane) -- invalid samples sort last
+        uint64_t key = ((uint64_t)(valid ? (uint32_t)(sv & (p.seg - 1)) : 0xFFFFFFu) << 32) |
+                       (uint32_t)lane;
+#pragma unroll
+        for (int kk = 2; kk <= 32; kk <<= 1)
+#pragma unroll
+            for (int jj = kk >> 1; jj > 0; jj >>= 1) {
+                const uint64_t o = __shfl_xor_sync(0xffffffffu, key, jj);
+                const bool up = ((lane & kk) == 0);
+                const bool lower = (lane & jj) == 0;
+                key = (lower == up) ? (o < key ? o : key) : (o > key ? o : key);
+            }
+        const int src = (int)(key & 31u);
+        const int s_sorted = __shfl_sync(0xffffffffu, sv, src);
+        const int valid_sorted = __shfl_sync(0xffffffffu, (int)valid, src);
+        if (lane < TPW) {
+            s_samp[warp * TPW + lane] = s_sorted;
+            s_col[warp * TPW + lane] = valid_sorted ? t0 + warp * TPW + src : -1;
+        }
     }
     if (tid == 0) {
         for (int q = 0; q < stages; ++q) mbar_init(&full[q], 1);
@@ -138,15 +180,19 @@ __global__ void __launch_bounds__(NW * 32, 1)
         const int q = (int)(g % stages);
         double *X = X0 + (size_t)q * tile_elems;
         double *sg = sgn_all + q * SEG;
-        if (tma) {
+        if (tma) {  // (TMA implies seg == 256: sign masks)
             if (tid == 0) {
-                mbar_arrive_expect_tx(&full[q], (uint32_t)(p.seg * TM * 8 + p.seg * 8));
+                mbar_arrive_expect_tx(&full[q], (uint32_t)(p.seg * TM * 8 + 32));
                 tma_load_2d(X, &tmap, (int)r0, (int)(g * p.seg), &full[q]);
-                bulk_g2s(sg, p.signs + g * p.seg, p.seg * 8, &full[q]);
+                bulk_g2s(sgm_all + q * 16, p.masks + g * 16, 32, &full[q]);
             }
         } else {
             load_segment_async(p, X, r0, g);
-            for (int k = tid; k < p.seg; k += NW * 32) cp_async8(sg + k, p.signs + g * p.seg + k, true);
+            if (p.seg == SEG) {
+                if (tid < 2) cp_async16(sgm_all + q * 16 + 8 * tid, p.masks + g * 16 + 8 * tid, true);
+            } else {
+                for (int k = tid; k < p.seg; k += NW * 32) cp_async8(sg + k, p.signs + g * p.seg + k, true);
+            }
         }
     };
 
@@ -172,12 +218,15 @@ __global__ void __launch_bounds__(NW * 32, 1)
             __syncthreads();
         }
         if (p.seg == SEG) {
-            // pass A: k = w + 16 q, butterflies over k bits 4..7 (signs applied)
+            // pass A: k = w + 16 q, butterflies over k bits 4..7 (signs applied
+            // by flipping sign bits: exact, as the reference's multiply by +-1)
             double x[16];
+            const uint32_t msk = sgm_all[q * 16 + warp];
 #pragma unroll
             for (int u = 0; u < 16; ++u) {
                 const int k = warp + 16 * u;
-                x[u] = X[k * p.pitch + lane] * sg[k];
+                x[u] = __longlong_as_double(__double_as_longlong(X[k * p.pitch + lane]) ^
+                                            ((long long)((msk >> u) & 1u) << 63));
             }
             wht16(x);
 #pragma unroll
@@ -225,8 +274,8 @@ __global__ void __launch_bounds__(NW * 32, 1)
     if (row < p.m_out) {
 #pragma unroll
         for (int i = 0; i < TPW; ++i) {
-            const int t = t0 + warp * TPW + i;
-            if (t < p.d) p.S[(p.col0 + t) * p.lds + row] = acc[i] * p.scale;
+            const int t = s_col[warp * TPW + i];
+            if (t >= 0) p.S[(p.col0 + t) * p.lds + row] = acc[i] * p.scale;
         }
     }
 }
@@ -245,7 +294,7 @@ static int launch(Args a, cudaStream_t st) {
         if (rc) return rc;
     }
     const int tile = a.seg * a.pitch * 8;
-    static_assert(NW * 32 * 4 <= 32 * 32 * 4, "sample table must fit below kTileOff");
+    static_assert(NW * 32 * 4 * 2 <= 2 * 32 * 32 * 4, "sample tables must fit below kTileOff");
     const int fixed = kTileOff;
     a.stages = (int)std::min<int64_t>(3, std::max<int64_t>(2, a.nseg));
     while (a.stages > 2 && fixed + a.stages * tile > 227 * 1024) --a.stages;
@@ -322,6 +371,19 @@ extern "C" int hsk_srht_apply(const double *A, int64_t rows, int64_t cols, int64
     a.seg = (int)std::min<int64_t>(srht::SEG, n_pad);
     a.signs = signs;
     a.sample = sample;
+    cudaStream_t st0 = as_stream(stream);
+    if (a.seg == srht::SEG) {  // per-(segment, warp) sign masks in the stream's workspace
+        const int64_t nseg = n_pad / srht::SEG;
+        void *ws = nullptr;
+        int *flags = nullptr;
+        int rc = stream_workspace(st0, (size_t)nseg * 16 * sizeof(uint16_t), 0, &ws, &flags);
+        if (rc) return rc;
+        a.masks = static_cast<const uint16_t *>(ws);
+        const unsigned blocks = (unsigned)std::min<int64_t>((nseg * 16 + 255) / 256, sm_count() * 4);
+        srht::srht_mask_kernel<<<std::max(1u, blocks), 256, 0, st0>>>(
+            signs, nseg, static_cast<uint16_t *>(ws));
+        HSK_CHECK_LAUNCH("srht_mask_kernel");
+    }
     a.d = d;
     a.scale = scale;
     a.S = S;
