@@ -122,6 +122,22 @@ HSK_API int hsk_gen_toeplitz_sin(int64_t n, int64_t row0, int64_t nrows, int64_t
 /* Streams `bytes` of scratch (device) to evict L2 between timed launches. */
 HSK_API int hsk_l2_flush(void *scratch, int64_t bytes, void *stream);
 
+/* ------------------------------------------ peer memory (multi-GPU S')
+ * Row-sharded S' = A^T R^T (BASELINE.json C5): the reference sums per-shard
+ * partials with a collective; here each rank's S' kernel writes destination
+ * block q directly into rank q's receive slot through an IPC mapping (the
+ * transfer rides on the kernel's epilogue stores), then the owner sums its
+ * slots in rank order.  Handles are HSK_IPC_HANDLE_BYTES opaque bytes. */
+#define HSK_IPC_HANDLE_BYTES 64
+HSK_API int hsk_ipc_alloc(int64_t bytes, void **ptr, void *handle);
+HSK_API int hsk_ipc_free(void *ptr);
+HSK_API int hsk_ipc_open(const void *handle, void **ptr);
+HSK_API int hsk_ipc_close(void *ptr);
+/* out(r, c) = sum over g = 0..nslices-1 (in order) of base[g*stride + c*ld + r];
+ * column-major rows x cols slices, deterministic. */
+HSK_API int hsk_sum_slices(const double *base, int32_t nslices, int64_t stride, int64_t rows,
+                   int64_t cols, int64_t ld, double *out, int64_t ldo, void *stream);
+
 #ifdef __cplusplus
 }
 #endif

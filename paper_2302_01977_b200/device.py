@@ -142,6 +142,23 @@ class DeviceMatrix:
         return sub
 
 
+class RawMatrix:
+    """Column-major rows x cols view of device memory this process does not
+    own through torch -- e.g. a peer GPU's receive slot mapped by CUDA IPC
+    (distributed.PeerSlots).  Kernel outputs only; no host transfers."""
+
+    __slots__ = ("rows", "cols", "ld", "ptr")
+
+    def __init__(self, ptr: int, rows: int, cols: int, ld: int):
+        if ld < max(1, rows):
+            raise ValueError("leading dimension smaller than the row count")
+        self.ptr, self.rows, self.cols, self.ld = int(ptr), int(rows), int(cols), int(ld)
+
+    @property
+    def shape(self) -> tuple[int, int]:
+        return (self.rows, self.cols)
+
+
 # --------------------------------------------------------------- R on device
 
 class _SjltState:

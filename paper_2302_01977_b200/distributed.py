@@ -13,10 +13,16 @@ The destination blocks are produced by separate launches over column
 slices of A_g (contiguous in the column-major layout), so each block is a
 contiguous (m_q x d) buffer and the reduce-scatter needs no repacking.
 
-Determinism: NCCL's reduce-scatter is deterministic for a fixed algorithm and
-topology; `deterministic=True` instead gathers every partial of block q on
-rank q and sums them in rank order (bitwise reproducible across runs and
-NCCL algorithms; also used for uneven shards).
+Transports for the S' exchange:
+  "p2p" (default on GPUs) -- no reduction collective: every rank's S' kernel
+        stores destination block q straight into rank q's receive slot
+        [rank] through a CUDA-IPC mapping of rank q's buffer (the kernel's
+        epilogue writes cross NVLink tile by tile while other tiles are
+        still computing); after a barrier each rank sums its slots in rank
+        order (hsk_sum_slices) -- deterministic, uneven shards allowed.
+  "nccl" -- reduce_scatter_tensor over the process group (the baseline), or
+        with `deterministic=True` a gather of every partial of block q on
+        rank q summed in rank order.
 
 SRHT mixes all input indices in its FWHT, so only S = A R^T row-shards; its
 S' is formed on column shards (`sketch_columns_local`).
@@ -88,9 +94,99 @@ def _gpu_local_transposed_blocks(A_shard, sub_op, bounds):
     return outs
 
 
+class PeerSlots:
+    """This rank's receive buffer for the p2p S' exchange -- `world` slots of
+    (ld x d) doubles, column-major, slot g written by rank g -- and CUDA-IPC
+    mappings of every peer's buffer (one process per GPU on one node)."""
+
+    def __init__(self, world: int, rank: int, ld: int, d: int, group=None):
+        import ctypes
+        from . import _lib
+        self.world, self.rank, self.ld, self.d = world, rank, ld, d
+        self.slot_elems = ld * d
+        own = ctypes.c_void_p()
+        handle = (ctypes.c_char * 64)()
+        _lib.call("hsk_ipc_alloc", world * self.slot_elems * 8, ctypes.byref(own), handle)
+        self.own = own.value
+        handles = [None] * world
+        if world > 1:
+            dist.all_gather_object(handles, bytes(handle), group=group)
+        self.peer = []
+        for q in range(world):
+            if q == rank:
+                self.peer.append(self.own)
+            else:
+                p = ctypes.c_void_p()
+                buf = ctypes.create_string_buffer(handles[q], 64)
+                _lib.call("hsk_ipc_open", buf, ctypes.byref(p))
+                self.peer.append(p.value)
+
+    def slot(self, q: int, rows: int):
+        """Rank q's slot for this rank's partial of block q (rows x d)."""
+        from . import device
+        return device.RawMatrix(self.peer[q] + self.rank * self.slot_elems * 8, rows, self.d,
+                                self.ld)
+
+    def reduce(self, rows: int, out_ptr: int, ldo: int, stream: int):
+        """out = sum of this rank's slots in rank order (first `rows` rows)."""
+        from . import _lib
+        _lib.call("hsk_sum_slices", self.own, self.world, self.slot_elems, rows, self.d, self.ld,
+                  out_ptr, ldo, stream)
+
+    def close(self):
+        from . import _lib
+        for q, p in enumerate(self.peer):
+            if q != self.rank and p:
+                _lib.call("hsk_ipc_close", p)
+        if self.own:
+            _lib.call("hsk_ipc_free", self.own)
+        self.peer, self.own = [], 0
+
+
+_SLOTS: dict = {}
+
+
+def peer_slots(world: int, rank: int, ld: int, d: int, group=None) -> PeerSlots:
+    """Receive slots for (group, shape), created collectively once and reused."""
+    key = (id(group), world, rank, ld, d, torch.cuda.current_device())
+    if key not in _SLOTS:
+        _SLOTS[key] = PeerSlots(world, rank, ld, d, group)
+    return _SLOTS[key]
+
+
+def release_peer_slots():
+    """Unmap and free every receive buffer (call collectively before exit)."""
+    for s in _SLOTS.values():
+        s.close()
+    _SLOTS.clear()
+
+
+def _p2p_transposed(A_shard, sub_op, bounds, rank: int, world: int, group):
+    """S' rows of this rank via direct peer stores + rank-ordered local sum."""
+    from . import device
+    from . import sketching as sk
+    m_max = max(b1 - b0 for b0, b1 in bounds)
+    slots = peer_slots(world, rank, m_max, sub_op.d, group)
+    for q, (c0, c1) in enumerate(bounds):
+        if c1 > c0:
+            view = A_shard.column_view(c0, c1 - c0)
+            sk.apply_right_transposed_device(view, sub_op, out=slots.slot(q, c1 - c0))
+    # every rank's stores into every slot are complete before anyone sums
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier(group=group)
+    r0, r1 = bounds[rank]
+    out = torch.empty((sub_op.d, max(1, r1 - r0)), dtype=torch.float64, device="cuda")
+    slots.reduce(r1 - r0, out.data_ptr(), max(1, r1 - r0), device.current_stream_ptr())
+    torch.cuda.synchronize()
+    if world > 1:  # the slots are free for the next call
+        dist.barrier(group=group)
+    return out[:, :r1 - r0]
+
+
 def sketch_row_sharded(A_shard, op, *, rank: int, world: int, n_rows: int,
                        transposed: bool = True, group=None, deterministic: bool = False,
-                       local_right=None, local_transposed=None):
+                       transport: str | None = None, local_right=None, local_transposed=None):
     """S rows and (optionally) S' rows of this rank's shard.
 
     A_shard: rows [r0, r1) of the global n_rows x op.n matrix (DeviceMatrix on
@@ -108,10 +204,18 @@ def sketch_row_sharded(A_shard, op, *, rank: int, world: int, n_rows: int,
     if op.n != n_rows:
         raise ValueError("S' = A^T R^T needs a square operator over the row space")
     sub = restrict_operator(op, r0, r1)
+    if transport is None:
+        transport = "nccl" if (local_transposed is not None or deterministic) else "p2p"
+    if transport == "p2p":
+        return S_local, _p2p_transposed(A_shard, sub, bounds, rank, world, group)
+    if transport != "nccl":
+        raise ValueError(f"unknown transport {transport!r}")
     local_transposed = local_transposed or _gpu_local_transposed_blocks
     parts = local_transposed(A_shard, sub, bounds)  # list of (d, m_q) tensors
     m_loc = r1 - r0
     d = op.d
+    if world == 1:  # the whole S' is local
+        return S_local, parts[0]
     if deterministic or any(b[1] - b[0] != m_loc for b in bounds):
         # fixed rank-order summation (bitwise reproducible; uneven shards OK)
         return S_local, _ordered_reduce_scatter(parts, rank, world, group)
@@ -161,4 +265,5 @@ def scaling_model(n: int, d: int, world: int, hbm_gbs: float, link_gbs: float = 
 
 
 __all__ = ["shard_bounds", "restrict_block", "restrict_operator", "sketch_row_sharded",
-           "sketch_columns_local", "scaling_model"]
+           "sketch_columns_local", "scaling_model", "PeerSlots", "peer_slots",
+           "release_peer_slots"]

@@ -104,3 +104,18 @@ def test_shard_bounds_and_restriction():
 def test_scaling_model():
     m = D.scaling_model(131072, 2048, 8, 6455.9)
     assert 0 < m["serial_eff"] < m["overlap_eff"] <= 1.0
+
+
+def test_transport_selection_and_validation():
+    """Unknown transports are rejected; the CPU test hooks select the
+    collective transport (the p2p transport needs CUDA IPC and is covered by
+    tests/test_gpu_p2p.py)."""
+    n, d = 64, 16
+    A = np.random.default_rng(1).standard_normal((n, n))
+    op = sk.new_operator(sk.SJLT, n, d, seed=3, alpha=2, construction=sk.GRAPH)
+    with pytest.raises(ValueError, match="unknown transport"):
+        D.sketch_row_sharded(HostMat(A), op, rank=0, world=1, n_rows=n, transport="carrier-pigeon",
+                             local_right=_local_right)
+    S, St = D.sketch_row_sharded(HostMat(A), op, rank=0, world=1, n_rows=n,
+                                 local_right=_local_right, local_transposed=_local_transposed)
+    np.testing.assert_allclose(St.numpy().T, O.apply_right_transposed(A, op), rtol=0, atol=1e-12)
