@@ -272,6 +272,9 @@ struct ApplyArgs {
     // cut between groups is summed by the group holding its first chunk
     int streamk, groups;
     int dbg;
+    // TMA multicast: the nslabs CTAs of a row tile form a cluster of `mc`
+    // CTAs; each loads 1/mc of every tile for all of them (1 = off)
+    int mc;
     int pf;  // mode 0: chunks prefetched into L2 beyond the shared-memory ring
     int64_t units;
     double *ws;  // per-CTA partial tile (SLAB x TM doubles)
@@ -343,7 +346,7 @@ __global__ void __launch_bounds__((NW + (PROD ? (TRANS && RPT == 4 ? 4 : 1) : 0)
         const uint32_t fcount = tma ? 1u : 1u + 32u * (PROD ? PW : NW);
         for (int s = 0; s < stages; ++s) {
             mbar_init(&full[s], fcount);
-            mbar_init(&empty[s], NW);
+            mbar_init(&empty[s], NW * p.mc);  // every consumer warp of the cluster
             done[s] = 0;
         }
         fence_mbar_init();
@@ -391,7 +394,19 @@ __global__ void __launch_bounds__((NW + (PROD ? (TRANS && RPT == 4 ? 4 : 1) : 0)
         int64_t r0, c;
         chunk_of(j, r0, c);
         mbar_arrive_expect_tx(bar, tile_bytes + bp_bytes + en_bytes);
-        if constexpr (TRANS) {  // S': one 16 x TM box per 16 input indices
+        if (p.mc > 1) {  // this CTA's share of the tile, for every CTA of the cluster
+            const uint32_t rank = cluster_ctarank();
+            const uint16_t mask = (uint16_t)((1u << p.mc) - 1u);
+            if constexpr (TRANS) {
+                for (int kb = (int)rank; kb < p.tk / 16; kb += p.mc)
+                    tma_load_2d_mc(st + kb * TM * 128, &tmap, (int)(c * p.tk + kb * 16), (int)r0, bar,
+                                   mask);
+            } else {
+                const int part = p.tk / p.mc;  // the box is TM x part
+                tma_load_2d_mc(st + (size_t)rank * part * TM * 8, &tmap, (int)r0,
+                               (int)(c * p.tk + rank * part), bar, mask);
+            }
+        } else if constexpr (TRANS) {  // S': one 16 x TM box per 16 input indices
             for (int kb = 0; kb < p.tk / 16; ++kb)
                 tma_load_2d(st + kb * TM * 128, &tmap, (int)(c * p.tk + kb * 16), (int)r0, bar);
         } else {
@@ -403,7 +418,8 @@ __global__ void __launch_bounds__((NW + (PROD ? (TRANS && RPT == 4 ? 4 : 1) : 0)
         if (p.pf > 0 && jp < nloc && (j < stages ? j < p.pf : true)) {
             int64_t rp, cp;
             chunk_of(jp, rp, cp);
-            tma_prefetch_2d(&tmap, (int)rp, (int)(cp * p.tk));
+            const int part = p.tk / p.mc;
+            tma_prefetch_2d(&tmap, (int)rp, (int)(cp * p.tk + (p.mc > 1 ? cluster_ctarank() * part : 0)));
         }
         bulk_g2s(st + p.bp_off, p.bptr + c * p.bstride + j0, bp_bytes, bar);
         bulk_g2s(st + p.en_off, p.ent + c * p.estride, en_bytes, bar);
@@ -494,6 +510,7 @@ __global__ void __launch_bounds__((NW + (PROD ? (TRANS && RPT == 4 ? 4 : 1) : 0)
                 cluster_sync();
                 cluster_sync();
             }
+            if (p.mc > 1) cluster_sync();  // peers stay alive for remote arrivals
             return;
         }
     } else if (tma) {
@@ -626,6 +643,10 @@ __global__ void __launch_bounds__((NW + (PROD ? (TRANS && RPT == 4 ? 4 : 1) : 0)
                     done[s] = 0;
                     if (i + stages < nloc && !DBG_IS(2)) issue_tma(i + stages);
                 }
+            } else if (p.mc > 1) {
+                // release the slot in every CTA of the cluster: no producer
+                // multicasts into it until all of them are done with it
+                for (int r = 0; r < p.mc; ++r) mbar_arrive_cluster(&empty[s], (uint32_t)r);
             } else {
                 mbar_arrive(&empty[s]);
             }
@@ -675,7 +696,10 @@ __global__ void __launch_bounds__((NW + (PROD ? (TRANS && RPT == 4 ? 4 : 1) : 0)
             seg_end = i + 1 + (int)p.nchunks < nloc ? i + 1 + (int)p.nchunks : nloc;
         }
     }
-    if (SK) return;
+    if (SK) {
+        if (p.mc > 1) cluster_sync();
+        return;
+    }
 
     // ------------------------------------------- k-split: DSMEM reduction
     // Partial sums of the ks CTAs of a cluster are combined by rank 0 in
@@ -704,6 +728,7 @@ __global__ void __launch_bounds__((NW + (PROD ? (TRANS && RPT == 4 ? 4 : 1) : 0)
         if (kr > 0) return;
     }
     store_tile(tile0 * TM);
+    if (p.mc > 1) cluster_sync();
 }
 
 
@@ -719,17 +744,6 @@ static int launch(ApplyArgs a, const Geom &g, cudaStream_t st) {
     a.mode = a.trans ? (!XPOSE && aligned && a.tk % 16 == 0 ? 3 : 1) : (aligned ? 0 : 2);
     a.log2tk = 0;
     while ((1 << a.log2tk) < a.tk) ++a.log2tk;
-    CUtensorMap tmap;
-    memset(&tmap, 0, sizeof(tmap));
-    if (a.mode == 0) {
-        int rc = make_tmap_f64_2d(&tmap, a.A, (uint64_t)a.m_out, (uint64_t)a.n, (uint64_t)a.lda,
-                                  TM, (uint32_t)a.tk);
-        if (rc) return rc;
-    } else if (a.mode == 3) {  // A is n x m_out: inner dimension = input index
-        int rc = make_tmap_f64_2d(&tmap, a.A, (uint64_t)a.n, (uint64_t)a.m_out, (uint64_t)a.lda,
-                                  16, TM, true);
-        if (rc) return rc;
-    }
     // S' tiles occupy whole 16-index blocks (the layout's unit); ring slots
     // start on 1024-byte boundaries
     const int a_bytes = (int)roundup((a.trans ? roundup(a.tk, 16) : a.tk) * (int64_t)TM * 8, 1024);
@@ -768,8 +782,67 @@ static int launch(ApplyArgs a, const Geom &g, cudaStream_t st) {
     a.streamk = eff < 0.9 && ctas >= sms;
     if (const char *env = getenv("HSK_SJLT_STREAMK")) a.streamk = env[0] == '1';
     a.streamk = a.streamk && a.groups >= 1 && a.nchunks > 0 && a.units < (1ll << 31);
+    if (a.streamk) ks = 1;
+    // TMA multicast across the slab CTAs of a row tile (they read the same
+    // tile): a cluster of nslabs CTAs, each loading 1/nslabs of every tile for
+    // all of them, cuts the L2 -> SM traffic by nslabs.  Opt-in only
+    // (HSK_SJLT_MC=1): measured slower -- C2 S 0.58 vs 0.47 ms, d = 2048 S
+    // 33.9 vs 5.9 ms -- because a slot is refilled only after every CTA of the
+    // cluster released it, which runs the slab CTAs in lockstep behind the
+    // slowest; without it each CTA runs ahead on its own and L2 absorbs the skew.
+    a.mc = 1;
+    const char *mc_env = getenv("HSK_SJLT_MC");
+    if (mc_env && mc_env[0] == '1' && prod && (a.mode == 0 || a.mode == 3) && ks == 1 &&
+        (a.nslabs == 2 || a.nslabs == 4 || a.nslabs == 8) && (a.mode == 3 || a.tk % a.nslabs == 0))
+        a.mc = a.nslabs;
+    CUtensorMap tmap;
+    memset(&tmap, 0, sizeof(tmap));
+    if (a.mode == 0) {
+        int rc = make_tmap_f64_2d(&tmap, a.A, (uint64_t)a.m_out, (uint64_t)a.n, (uint64_t)a.lda,
+                                  TM, (uint32_t)(a.tk / a.mc));
+        if (rc) return rc;
+    } else if (a.mode == 3) {  // A is n x m_out: inner dimension = input index
+        int rc = make_tmap_f64_2d(&tmap, a.A, (uint64_t)a.n, (uint64_t)a.m_out, (uint64_t)a.lda,
+                                  16, TM, true);
+        if (rc) return rc;
+    }
+    const int nthreads = (NW + (prod ? pw : 0)) * 32;
+    const int budget = 226 * 1024;
+    const int stages_max = std::max(2, std::min(8, (budget - 2048) / a.stage_bytes));
+    if (a.streamk && a.mc > 1) {
+        // every group is one cluster and groups wait on later groups: keep
+        // the grid to the clusters that can be co-resident
+        auto kprobe = a.trans ? sjlt_apply_kernel<RPT, DB, NW, true, true, true>
+                              : sjlt_apply_kernel<RPT, DB, NW, false, true, true>;
+        const int smem_max = 2048 + stages_max * a.stage_bytes;
+        cudaError_t e = cudaFuncSetAttribute(kprobe, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_max);
+        if (e != cudaSuccess) return cuda_status(e, "sjlt: set smem attribute");
+        cudaLaunchConfig_t pc = {};
+        pc.gridDim = dim3((unsigned)(a.groups * a.nslabs), 1, 1);
+        pc.blockDim = dim3(nthreads, 1, 1);
+        pc.dynamicSmemBytes = smem_max;
+        cudaLaunchAttribute pa[1];
+        pa[0].id = cudaLaunchAttributeClusterDimension;
+        pa[0].val.clusterDim.x = a.mc;
+        pa[0].val.clusterDim.y = 1;
+        pa[0].val.clusterDim.z = 1;
+        pc.attrs = pa;
+        pc.numAttrs = 1;
+        int nclusters = 0;
+        e = cudaOccupancyMaxActiveClusters(&nclusters, kprobe, &pc);
+        if (e != cudaSuccess) return cuda_status(e, "sjlt: cluster occupancy");
+        if (nclusters < 1) {
+            a.mc = 1;  // cannot place a cluster: plain launch
+            int rc = make_tmap_f64_2d(&tmap, a.A, a.mode == 0 ? (uint64_t)a.m_out : (uint64_t)a.n,
+                                      a.mode == 0 ? (uint64_t)a.n : (uint64_t)a.m_out, (uint64_t)a.lda,
+                                      a.mode == 0 ? TM : 16, a.mode == 0 ? (uint32_t)a.tk : TM,
+                                      a.mode == 3);
+            if (rc) return rc;
+        } else {
+            a.groups = std::min(a.groups, nclusters);
+        }
+    }
     if (a.streamk) {
-        ks = 1;
         void *ws = nullptr;
         int *flags = nullptr;
         const int nct = a.groups * a.nslabs;
@@ -780,8 +853,7 @@ static int launch(ApplyArgs a, const Geom &g, cudaStream_t st) {
     }
     a.ksplit = ks;
     const int per = (int)(a.streamk ? (a.units + a.groups - 1) / a.groups : (a.nchunks + ks - 1) / ks);
-    const int budget = 226 * 1024;
-    a.stages = std::max(2, std::min(8, (budget - 2048) / a.stage_bytes));
+    a.stages = stages_max;
     if (const char *env = getenv("HSK_SJLT_STAGES")) a.stages = std::max(2, std::min(a.stages, atoi(env)));
     if (per > 0 && a.stages > per + 1) a.stages = std::max(2, per + 1);
     int smem = 2048 + a.stages * a.stage_bytes;  // header + 1024-byte alignment slack
@@ -799,7 +871,6 @@ static int launch(ApplyArgs a, const Geom &g, cudaStream_t st) {
     a.pf = a.mode == 0 && a.streamk ? 2 : 0;
     a.dbg = getenv("HSK_SJLT_DBG") ? atoi(getenv("HSK_SJLT_DBG")) : 0;
     if (const char *env = getenv("HSK_SJLT_PF")) a.pf = std::max(0, atoi(env));
-    const int nthreads = (NW + (prod ? pw : 0)) * 32;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e != cudaSuccess) return cuda_status(e, "sjlt: set smem attribute");
     const int64_t grid = a.streamk ? (int64_t)a.groups * a.nslabs : tiles * a.nslabs * ks;
@@ -809,19 +880,23 @@ static int launch(ApplyArgs a, const Geom &g, cudaStream_t st) {
     cfg.blockDim = dim3(nthreads, 1, 1);
     cfg.dynamicSmemBytes = smem;
     cfg.stream = st;
-    cudaLaunchAttribute attr[1];
-    if (a.streamk) {  // groups wait on later groups' partials: all CTAs co-resident
-        attr[0].id = cudaLaunchAttributeCooperative;
-        attr[0].val.cooperative = 1;
-    } else {
-        attr[0].id = cudaLaunchAttributeClusterDimension;
-        attr[0].val.clusterDim.x = ks;
-        attr[0].val.clusterDim.y = 1;
-        attr[0].val.clusterDim.z = 1;
+    cudaLaunchAttribute attr[2];
+    int na = 0;
+    const int cdim = ks > 1 ? ks : a.mc;  // k-split and multicast never combine
+    if (cdim > 1) {
+        attr[na].id = cudaLaunchAttributeClusterDimension;
+        attr[na].val.clusterDim.x = cdim;
+        attr[na].val.clusterDim.y = 1;
+        attr[na].val.clusterDim.z = 1;
+        ++na;
+    }
+    if (a.streamk && cdim == 1) {  // groups wait on later groups' partials: co-resident
+        attr[na].id = cudaLaunchAttributeCooperative;
+        attr[na].val.cooperative = 1;
+        ++na;
     }
     cfg.attrs = attr;
-    cfg.numAttrs = (ks > 1 || a.streamk) ? 1 : 0;  // plain launch unless needed
-    if (const char *env = getenv("HSK_SJLT_FORCE_CLUSTER")) cfg.numAttrs = env[0] == '1' ? 1 : cfg.numAttrs;
+    cfg.numAttrs = na;
     e = cudaLaunchKernelEx(&cfg, kern, a, tmap);
     if (e != cudaSuccess) return cuda_status(e, "sjlt_apply_kernel launch");
     HSK_CHECK_LAUNCH("sjlt_apply_kernel");

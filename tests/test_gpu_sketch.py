@@ -113,8 +113,9 @@ def test_sjlt_shapes_vs_oracle(cuda, m, n, d, alpha, cons):
     (150, 20000, 512, 4),
 ])
 def test_sjlt_schedules_vs_oracle(cuda, monkeypatch, m, n, d, alpha):
-    """Whole-tile (k-split) and persistent stream-K schedules: both match the
-    oracle, and stream-K's cross-CTA tile fixup is bitwise repeatable."""
+    """Whole-tile (k-split) and persistent stream-K schedules, with and without
+    TMA multicast across slab clusters: all match the oracle, and stream-K's
+    cross-CTA tile fixup is bitwise repeatable."""
     rng = np.random.default_rng(m + n + d)
     op = sk.new_operator(sk.SJLT, n, d, seed=(m, d), alpha=alpha, construction=sk.BLOCK)
     b = op.blocks[0]
@@ -123,8 +124,11 @@ def test_sjlt_schedules_vs_oracle(cuda, monkeypatch, m, n, d, alpha):
     ref = O.sjlt_right(A, b._pos, b._signs, d, b._scale)
     ref_t = O.sjlt_right_t(B, b._pos, b._signs, d, b._scale)
     dA, dB = device.DeviceMatrix.from_host(A), device.DeviceMatrix.from_host(B)
-    for mode in ("0", "1"):
+    # whole-tile / stream-K schedules, each with and without slab-cluster
+    # TMA multicast (opt-in path)
+    for mode, mc in (("0", "0"), ("1", "0"), ("0", "1"), ("1", "1")):
         monkeypatch.setenv("HSK_SJLT_STREAMK", mode)
+        monkeypatch.setenv("HSK_SJLT_MC", mc)
         s1 = sk.apply_right_device(dA, op).to_host()
         s2 = sk.apply_right_device(dA, op).to_host()
         _close(s1, ref, np.linalg.norm(A))
