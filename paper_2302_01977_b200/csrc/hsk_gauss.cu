@@ -249,8 +249,9 @@ extern "C" int hsk_gauss_apply(const double *A, int64_t rows, int64_t cols, int6
     a.a16 = ((reinterpret_cast<uintptr_t>(A) & 15) == 0) && (lda % 2 == 0);
     a.b16 = ((reinterpret_cast<uintptr_t>(R) & 15) == 0) && (n % 2 == 0);
     cudaStream_t st = as_stream(stream);
-    // 64 x 64 tiles, 2 x 2 warps, 4 stages: many resident CTAs keep the FP64
-    // tensor pipe fed.  HSK_GAUSS_CFG overrides: "128" (128x128, 2x4 warps),
+    // 64 x 64 tiles, 2 x 2 warps (32 x 32 DMMA tiles each), 3 stages: many
+    // resident CTAs keep the FP64 tensor pipe fed (measured best among warp
+    // tiles 32x32 / 32x64 / 64x32 / 64x64 and 2-6 stages).  HSK_GAUSS_CFG overrides: "128" (128x128, 2x4 warps),
     // "64x128" (2x4 warps).
     const char *cfg = getenv("HSK_GAUSS_CFG");
     // tuning variants: warp tiles 32x64 / 64x32 (12 fragment loads per 32 DMMA)
@@ -281,5 +282,5 @@ extern "C" int hsk_gauss_apply(const double *A, int64_t rows, int64_t cols, int6
     if (cfg && !strcmp(cfg, "64x64x8"))
         return trans ? gauss::launch<64, 64, 1, 2, 4, 4>(a, st)
                      : gauss::launch<64, 64, 0, 2, 4, 4>(a, st);
-    return trans ? gauss::launch<64, 64, 1, 2, 2, 4>(a, st) : gauss::launch<64, 64, 0, 2, 2, 4>(a, st);
+    return trans ? gauss::launch<64, 64, 1, 2, 2, 3>(a, st) : gauss::launch<64, 64, 0, 2, 2, 3>(a, st);
 }
