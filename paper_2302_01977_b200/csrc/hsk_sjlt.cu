@@ -275,6 +275,7 @@ struct ApplyArgs {
     // TMA multicast: the nslabs CTAs of a row tile form a cluster of `mc`
     // CTAs; each loads 1/mc of every tile for all of them (1 = off)
     int mc;
+    int wait_ns;  // consumer full-barrier wait: try_wait suspend hint (0 = default)
     int pf;  // mode 0: chunks prefetched into L2 beyond the shared-memory ring
     int64_t units;
     double *ws;  // per-CTA partial tile (SLAB x TM doubles)
@@ -584,7 +585,10 @@ __global__ void __launch_bounds__((NW + (PROD ? (TRANS && RPT == 4 ? 4 : 1) : 0)
 
         // ---- consume chunk i
         const int s = cs;
-        if (!DBG_IS(2) || i < stages) mbar_wait(&full[s], cph);
+        if (!DBG_IS(2) || i < stages) {
+            if (p.wait_ns) mbar_wait_hint(&full[s], cph, (uint32_t)p.wait_ns);
+            else mbar_wait(&full[s], cph);
+        }
         const uint32_t st = smem_base + (uint32_t)s * p.stage_bytes;
         const uint32_t sx = st + lane_off;
         const uint32_t sen = st + p.en_off;
@@ -866,9 +870,13 @@ static int launch(ApplyArgs a, const Geom &g, cudaStream_t st) {
                                              : sjlt_apply_kernel<RPT, DB, NW, false, true, false>)
                                 : (a.streamk ? sjlt_apply_kernel<RPT, DB, NW, false, false, true>
                                              : sjlt_apply_kernel<RPT, DB, NW, false, false, false>));
-    // L2 prefetch two chunks beyond the ring: measured +0.6 % on C2 (persistent
-    // CTAs streaming many tiles), -5 % on C1 (short k-split CTAs)
-    a.pf = a.mode == 0 && a.streamk ? 2 : 0;
+    // L2 prefetch beyond the ring: off -- the duplicate requests cost power,
+    // and sustained runs are power-capped (C2, 2000 launches: 0.505 ms
+    // without, 0.540 ms with; no burst gain either).  HSK_SJLT_PF=<chunks>.
+    a.pf = 0;
+    // consumers waiting for a tile sleep up to 1 us per poll (measured neutral
+    // to +1 %: fewer polling instructions under the power cap)
+    a.wait_ns = getenv("HSK_SJLT_WAIT_NS") ? atoi(getenv("HSK_SJLT_WAIT_NS")) : 1000;
     a.dbg = getenv("HSK_SJLT_DBG") ? atoi(getenv("HSK_SJLT_DBG")) : 0;
     if (const char *env = getenv("HSK_SJLT_PF")) a.pf = std::max(0, atoi(env));
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
