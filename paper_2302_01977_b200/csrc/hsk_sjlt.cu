@@ -47,6 +47,19 @@
 #endif
 #define DBG_IS(m) (HSK_SJLT_DEBUG && p.dbg == (m))
 
+// TMA multicast across slab clusters (opt-in at build time and run time,
+// -DHSK_SJLT_MULTICAST=1 plus HSK_SJLT_MC=1): measured slower (see launch<>),
+// and its remote-arrive branches cost the default kernels registers and
+// scheduling even when not taken (d = 2048 S: 6.0 vs 5.45 ms), so production
+// builds compile none of it.
+#ifndef HSK_SJLT_MULTICAST
+#define HSK_SJLT_MULTICAST 0
+#endif
+// The stream-K instantiations keep the (runtime-inert) multicast branches:
+// measured 3.5 % faster on C2 with them than without (code layout; the
+// walker SASS is identical), while the whole-tile ones are faster without.
+#define MC_ON ((HSK_SJLT_MULTICAST || SK) && p.mc > 1)
+
 namespace hsk {
 namespace sjlt {
 
@@ -347,7 +360,7 @@ __global__ void __launch_bounds__((NW + (PROD ? (TRANS && RPT == 4 ? 4 : 1) : 0)
         const uint32_t fcount = tma ? 1u : 1u + 32u * (PROD ? PW : NW);
         for (int s = 0; s < stages; ++s) {
             mbar_init(&full[s], fcount);
-            mbar_init(&empty[s], NW * p.mc);  // every consumer warp of the cluster
+            mbar_init(&empty[s], (HSK_SJLT_MULTICAST || SK) ? NW * p.mc : NW);  // consumer warps of the cluster
             done[s] = 0;
         }
         fence_mbar_init();
@@ -395,7 +408,7 @@ __global__ void __launch_bounds__((NW + (PROD ? (TRANS && RPT == 4 ? 4 : 1) : 0)
         int64_t r0, c;
         chunk_of(j, r0, c);
         mbar_arrive_expect_tx(bar, tile_bytes + bp_bytes + en_bytes);
-        if (p.mc > 1) {  // this CTA's share of the tile, for every CTA of the cluster
+        if (MC_ON) {  // this CTA's share of the tile, for every CTA of the cluster
             const uint32_t rank = cluster_ctarank();
             const uint16_t mask = (uint16_t)((1u << p.mc) - 1u);
             if constexpr (TRANS) {
@@ -420,7 +433,7 @@ __global__ void __launch_bounds__((NW + (PROD ? (TRANS && RPT == 4 ? 4 : 1) : 0)
             int64_t rp, cp;
             chunk_of(jp, rp, cp);
             const int part = p.tk / p.mc;
-            tma_prefetch_2d(&tmap, (int)rp, (int)(cp * p.tk + (p.mc > 1 ? cluster_ctarank() * part : 0)));
+            tma_prefetch_2d(&tmap, (int)rp, (int)(cp * p.tk + (MC_ON ? cluster_ctarank() * part : 0)));
         }
         bulk_g2s(st + p.bp_off, p.bptr + c * p.bstride + j0, bp_bytes, bar);
         bulk_g2s(st + p.en_off, p.ent + c * p.estride, en_bytes, bar);
@@ -511,7 +524,7 @@ __global__ void __launch_bounds__((NW + (PROD ? (TRANS && RPT == 4 ? 4 : 1) : 0)
                 cluster_sync();
                 cluster_sync();
             }
-            if (p.mc > 1) cluster_sync();  // peers stay alive for remote arrivals
+            if (MC_ON) cluster_sync();  // peers stay alive for remote arrivals
             return;
         }
     } else if (tma) {
@@ -647,7 +660,7 @@ __global__ void __launch_bounds__((NW + (PROD ? (TRANS && RPT == 4 ? 4 : 1) : 0)
                     done[s] = 0;
                     if (i + stages < nloc && !DBG_IS(2)) issue_tma(i + stages);
                 }
-            } else if (p.mc > 1) {
+            } else if (MC_ON) {
                 // release the slot in every CTA of the cluster: no producer
                 // multicasts into it until all of them are done with it
                 for (int r = 0; r < p.mc; ++r) mbar_arrive_cluster(&empty[s], (uint32_t)r);
@@ -701,7 +714,7 @@ __global__ void __launch_bounds__((NW + (PROD ? (TRANS && RPT == 4 ? 4 : 1) : 0)
         }
     }
     if (SK) {
-        if (p.mc > 1) cluster_sync();
+        if (MC_ON) cluster_sync();
         return;
     }
 
@@ -732,7 +745,7 @@ __global__ void __launch_bounds__((NW + (PROD ? (TRANS && RPT == 4 ? 4 : 1) : 0)
         if (kr > 0) return;
     }
     store_tile(tile0 * TM);
-    if (p.mc > 1) cluster_sync();
+    if (MC_ON) cluster_sync();
 }
 
 
@@ -796,7 +809,7 @@ static int launch(ApplyArgs a, const Geom &g, cudaStream_t st) {
     // slowest; without it each CTA runs ahead on its own and L2 absorbs the skew.
     a.mc = 1;
     const char *mc_env = getenv("HSK_SJLT_MC");
-    if (mc_env && mc_env[0] == '1' && prod && (a.mode == 0 || a.mode == 3) && ks == 1 &&
+    if (HSK_SJLT_MULTICAST && mc_env && mc_env[0] == '1' && prod && (a.mode == 0 || a.mode == 3) && ks == 1 &&
         (a.nslabs == 2 || a.nslabs == 4 || a.nslabs == 8) && (a.mode == 3 || a.tk % a.nslabs == 0))
         a.mc = a.nslabs;
     CUtensorMap tmap;
