@@ -47,6 +47,12 @@
 #endif
 #define DBG_IS(m) (HSK_SJLT_DEBUG && p.dbg == (m))
 
+// producer warps of the transposing cp.async S' path (128-row tiles)
+#ifndef HSK_XPOSE_PRODUCERS
+#define HSK_XPOSE_PRODUCERS 4
+#endif
+constexpr int kXposeProducers = HSK_XPOSE_PRODUCERS;
+
 // TMA multicast across slab clusters (opt-in at build time and run time,
 // -DHSK_SJLT_MULTICAST=1 plus HSK_SJLT_MC=1): measured slower (see launch<>),
 // and its remote-arrive branches cost the default kernels registers and
@@ -299,12 +305,12 @@ struct ApplyArgs {
 // warp 0 / lane 0 issues TMA + bulk copies (mode 0); in modes 1/2 every lane
 // issues its share of 8-byte cp.async for the chunk STAGES-1 ahead.
 template <int RPT, int DB, int NW, bool TRANS, bool PROD, bool SK>
-__global__ void __launch_bounds__((NW + (PROD ? (TRANS && RPT == 4 ? 4 : 1) : 0)) * 32, 1)
+__global__ void __launch_bounds__((NW + (PROD ? (TRANS && RPT == 4 ? kXposeProducers : 1) : 0)) * 32, 1)
     sjlt_apply_kernel(const ApplyArgs p, const __grid_constant__ CUtensorMap tmap) {
     constexpr int TM = 32 * RPT;
     constexpr int SLAB = NW * DB;
     constexpr bool XPOSE = TRANS && RPT == 4;       // transposed S' tile layout
-    constexpr int PW = PROD ? (XPOSE ? 4 : 1) : 0;  // dedicated producer warps
+    constexpr int PW = PROD ? (XPOSE ? kXposeProducers : 1) : 0;  // dedicated producer warps
     extern __shared__ __align__(128) unsigned char smem[];
     uint64_t *full = reinterpret_cast<uint64_t *>(smem);
     uint64_t *empty = full + 8;
@@ -783,7 +789,7 @@ static int launch(ApplyArgs a, const Geom &g, cudaStream_t st) {
     // from the last consumer warp to release a slot instead
     bool prod = NW < 32;
     if (const char *env = getenv("HSK_SJLT_PROD")) prod = env[0] == '1';
-    const int pw = a.trans && XPOSE ? 4 : 1;
+    const int pw = a.trans && XPOSE ? kXposeProducers : 1;
     prod = prod && (a.mode == 0 || a.mode == 3 || (a.mode == 1 && XPOSE)) && NW + pw <= 32;
     // persistent balanced schedule (stream-K) when whole-tile CTAs would
     // leave a partial last wave: one CTA per SM, groups of nslabs CTAs (the
