@@ -6,7 +6,7 @@
 //
 // tcgen05.mma has no f64 kind, so the FP64 tensor path on sm_100a is the
 // warp-level mma.sync.m8n8k4.f64 (SASS DMMA.8x8x4).  CTA tile BM x BN with
-// BK = 16 k-steps staged by a STAGES-deep cp.async ring; 8 warps, each a
+// BK = 32 k-steps staged by a STAGES-deep cp.async ring; 4 warps, each a
 // (BM/2) x (BN/4) register tile of 8x8 DMMA fragments.  Shared-memory pitches
 // are chosen so every fragment load is conflict-free
 // (DESIGN.md §Gaussian).  R is the reference's d x n row-major `matrix`,
@@ -21,7 +21,7 @@
 namespace hsk {
 namespace gauss {
 
-constexpr int BK = 16;
+constexpr int BK = 32;  // (16 measured 1-3 % slower: twice the barriers per DMMA)
 constexpr int PKK = BK + 4;  // pitch of k-contiguous tiles (== 4 mod 16)
 
 struct Args {
@@ -249,7 +249,7 @@ extern "C" int hsk_gauss_apply(const double *A, int64_t rows, int64_t cols, int6
     a.a16 = ((reinterpret_cast<uintptr_t>(A) & 15) == 0) && (lda % 2 == 0);
     a.b16 = ((reinterpret_cast<uintptr_t>(R) & 15) == 0) && (n % 2 == 0);
     cudaStream_t st = as_stream(stream);
-    // 64 x 64 tiles, 2 x 2 warps (32 x 32 DMMA tiles each), 3 stages: many
+    // 64 x 64 tiles, 2 x 2 warps (32 x 32 DMMA tiles each), BK 32, 2 stages: many
     // resident CTAs keep the FP64 tensor pipe fed (measured best among warp
     // tiles 32x32 / 32x64 / 64x32 / 64x64 and 2-6 stages).  HSK_GAUSS_CFG overrides: "128" (128x128, 2x4 warps),
     // "64x128" (2x4 warps).
@@ -282,5 +282,5 @@ extern "C" int hsk_gauss_apply(const double *A, int64_t rows, int64_t cols, int6
     if (cfg && !strcmp(cfg, "64x64x8"))
         return trans ? gauss::launch<64, 64, 1, 2, 4, 4>(a, st)
                      : gauss::launch<64, 64, 0, 2, 4, 4>(a, st);
-    return trans ? gauss::launch<64, 64, 1, 2, 2, 3>(a, st) : gauss::launch<64, 64, 0, 2, 2, 3>(a, st);
+    return trans ? gauss::launch<64, 64, 1, 2, 2, 2>(a, st) : gauss::launch<64, 64, 0, 2, 2, 2>(a, st);
 }
