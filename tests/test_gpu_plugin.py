@@ -90,3 +90,27 @@ def test_c1_hss_error_matches_reference(cuda):
     assert stats(H_gpu).final_d == stats(H_ref).final_d
     print(f"C1 HSS relative error: reference {err_ref:.6e}, GPU sketch {err_gpu:.6e}, "
           f"final_d {stats(H_gpu).final_d}")
+
+
+@pytest.mark.slow
+def test_acceptance_5_sjlt_sketch_phase_faster_than_gaussian(installed):
+    """Reference acceptance criterion 5 through the drop-in: on the n=10000
+    quantum-chemistry Toeplitz matrix, the compressor's SJLT (alpha=2) sketch
+    phase takes <= 0.8x the Gaussian one (median over 5 seeds)."""
+    import statistics
+    from hsskit import build_uniform, compress
+    from hsskit.hss_compress import CompressOptions
+    from hsskit.matgen import qchem_toeplitz
+    acc = qchem_toeplitz(10000, 0.1)
+    tree = build_uniform(10000, 256)
+    acc.dense()
+    ratios = []
+    for seed in range(5):
+        seconds = {}
+        for kind, alpha in (("gaussian", None), ("sjlt", 2)):
+            opts = CompressOptions(d0=128, dd=64, eps_rel=1e-2, eps_abs=1e-8, kind=kind,
+                                   alpha=alpha, seed=seed, leaf_size=256)
+            seconds[kind] = compress(acc, tree, opts).sketch_seconds
+        ratios.append(seconds["sjlt"] / seconds["gaussian"])
+    print(f"acceptance 5 through the GPU: SJLT/Gaussian sketch-time ratios {ratios}")
+    assert statistics.median(ratios) <= 0.8
