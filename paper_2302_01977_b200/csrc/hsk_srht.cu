@@ -35,6 +35,7 @@ struct Args {
     int trans;
     int vec16;
     int use_tma;
+    int use_tma_t;  // S' of aligned A: TMA natural-layout staging + in-smem transpose
     int64_t m_out;   // number of vectors
     int64_t n;       // vector length (before padding)
     int64_t n_pad;
@@ -139,6 +140,13 @@ __global__ void __launch_bounds__(NW * 32, 1)
     const int tile_elems = p.seg * p.pitch;
     const int stages = p.stages;
     const bool tma = p.use_tma != 0;
+    // S' (vectors = columns of A, contiguous): TMA lands each 32-vector x
+    // 256 segment in its natural layout in a staging buffer; all warps
+    // transpose it into X[k][vector] (pitch 33), and the next segment's TMA
+    // flies while this one is transformed and folded.  One X slot suffices.
+    const bool tmat = p.use_tma_t != 0;
+    uint64_t *stg_full = full + (kMaxStages - 1);
+    const double *stg = X0 + (size_t)stages * tile_elems;
 
     // each warp sorts its TPW samples by position within a segment (s mod
     // seg) so repeated positions reuse one tile load in the fold
@@ -168,8 +176,9 @@ __global__ void __launch_bounds__(NW * 32, 1)
     }
     if (tid == 0) {
         for (int q = 0; q < stages; ++q) mbar_init(&full[q], 1);
+        if (tmat) mbar_init(stg_full, 1);
         fence_mbar_init();
-        if (tma) prefetch_tmap(&tmap);
+        if (tma || tmat) prefetch_tmap(&tmap);
     }
     __syncthreads();
     const int64_t G = p.nseg;
@@ -196,18 +205,42 @@ __global__ void __launch_bounds__(NW * 32, 1)
         }
     };
 
+    // S' staging issue (thread 0): segment g and its sign masks (mask slot g & 1)
+    auto issue_t = [&](int64_t g) {
+        mbar_arrive_expect_tx(stg_full, (uint32_t)(SEG * TM * 8 + 32));
+        tma_load_2d(const_cast<double *>(stg), &tmap, (int)(g * SEG), (int)r0, stg_full);
+        bulk_g2s(sgm_all + (g & 1) * 16, p.masks + g * 16, 32, stg_full);
+    };
+
     double acc[TPW];
 #pragma unroll
     for (int i = 0; i < TPW; ++i) acc[i] = 0.0;
 
-    for (int64_t g = 0; g < stages - 1 && g < G; ++g) {
-        issue(g);
-        if (!tma) cp_async_commit();
+    if (tmat) {
+        if (tid == 0 && G > 0) issue_t(0);
+    } else {
+        for (int64_t g = 0; g < stages - 1 && g < G; ++g) {
+            issue(g);
+            if (!tma) cp_async_commit();
+        }
     }
     for (int64_t g = 0; g < G; ++g) {
         const int q = (int)(g % stages);
         double *X = X0 + (size_t)q * tile_elems;
         const double *sg = sgn_all + q * SEG;
+        if (tmat) {
+            mbar_wait(stg_full, (uint32_t)(g & 1));
+            // natural layout stg[vector][k] -> X[k][vector]: lanes along k
+            // (conflict-free reads; pitch-33 writes are 2-way at worst)
+#pragma unroll 4
+            for (int it = 0; it < (SEG * TM) / (NW * 32); ++it) {
+                const int idx = it * NW * 32 + tid;
+                const int c = idx >> 8, k = idx & (SEG - 1);
+                X[k * p.pitch + c] = stg[c * SEG + k];
+            }
+            __syncthreads();  // staging consumed: fetch the next segment now
+            if (tid == 0 && g + 1 < G) issue_t(g + 1);
+        } else {
         // the slot of segment g-1 is free: every thread passed its last sync
         if (g + stages - 1 < G) issue(g + stages - 1);
         if (tma) {
@@ -217,11 +250,12 @@ __global__ void __launch_bounds__(NW * 32, 1)
             if (stages == 2) cp_async_wait<1>(); else cp_async_wait<2>();
             __syncthreads();
         }
+        }
         if (p.seg == SEG) {
             // pass A: k = w + 16 q, butterflies over k bits 4..7 (signs applied
             // by flipping sign bits: exact, as the reference's multiply by +-1)
             double x[16];
-            const uint32_t msk = sgm_all[q * 16 + warp];
+            const uint32_t msk = sgm_all[(tmat ? (int)(g & 1) : q) * 16 + warp];
 #pragma unroll
             for (int u = 0; u < 16; ++u) {
                 const int k = warp + 16 * u;
@@ -268,7 +302,7 @@ __global__ void __launch_bounds__(NW * 32, 1)
         }
         __syncthreads();  // X (slot q) is refilled by the issue of segment g + 1
     }
-    if (!tma) cp_async_wait<0>();
+    if (!tma && !tmat) cp_async_wait<0>();
 
     const int64_t row = r0 + lane;
     if (row < p.m_out) {
@@ -284,6 +318,7 @@ template <int TPW>
 static int launch(Args a, cudaStream_t st) {
     // TMA for row tiles of aligned A with full 256-column segments
     a.use_tma = !a.trans && a.vec16 && a.seg == SEG;
+    a.use_tma_t = a.trans && a.vec16 && a.seg == SEG;
     a.pitch = a.trans ? TM + 1 : TM;
     a.nseg = a.n_pad / a.seg;
     CUtensorMap tmap;
@@ -292,13 +327,18 @@ static int launch(Args a, cudaStream_t st) {
         int rc = make_tmap_f64_2d(&tmap, a.A, (uint64_t)a.m_out, (uint64_t)a.n, (uint64_t)a.lda,
                                   TM, SEG);
         if (rc) return rc;
+    } else if (a.use_tma_t) {  // A is n x m_out: box of SEG input indices x TM vectors
+        int rc = make_tmap_f64_2d(&tmap, a.A, (uint64_t)a.n, (uint64_t)a.m_out, (uint64_t)a.lda,
+                                  SEG, TM);
+        if (rc) return rc;
     }
     const int tile = a.seg * a.pitch * 8;
     static_assert(NW * 32 * 4 * 2 <= 2 * 32 * 32 * 4, "sample tables must fit below kTileOff");
     const int fixed = kTileOff;
     a.stages = (int)std::min<int64_t>(3, std::max<int64_t>(2, a.nseg));
     while (a.stages > 2 && fixed + a.stages * tile > 227 * 1024) --a.stages;
-    const int smem = fixed + a.stages * tile;
+    if (a.use_tma_t) a.stages = 1;  // one X slot + the staging tile
+    const int smem = fixed + a.stages * tile + (a.use_tma_t ? SEG * TM * 8 : 0);
     auto kern = srht_kernel<TPW>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e != cudaSuccess) return cuda_status(e, "srht: set smem attribute");

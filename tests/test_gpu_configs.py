@@ -105,7 +105,14 @@ def test_c4_srht_full_size(cuda):
         r1 = r0 + 64
         got = S.row_view(r0, 64).to_host()
         assert O.rel_frobenius(got, O.apply_right(_rows(A, r0, r1), op)) <= REL
-    del A, S
+    # S' = A^T R^T (columns of A transformed; TMA staging + in-smem transpose):
+    # column slabs of A against the oracle
+    St = sk.apply_right_transposed_device(A, op)
+    for c0 in (0, 40000):
+        c1 = c0 + 48
+        got = St.row_view(c0, c1 - c0).to_host()
+        assert O.rel_frobenius(got, O.apply_right_transposed(_cols(A, c0, c1), op)) <= REL
+    del A, S, St
     _free()
 
 

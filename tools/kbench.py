@@ -109,6 +109,8 @@ def main():
             ms = timeit(lambda: device.apply_block(blk, A, False, S, 0), max(3, args.reps // 4))
             byt = n * n * 8 + n * 512 * 8
             out["c4_S"] = {"ms": ms, "GBs": byt / ms / 1e6, "frac": byt / ms / 1e6 / PEAK}
+            ms = timeit(lambda: device.apply_block(blk, A, True, S, 0), max(3, args.reps // 4))
+            out["c4_St"] = {"ms": ms, "GBs": byt / ms / 1e6, "frac": byt / ms / 1e6 / PEAK}
         print(json.dumps({k: v for k, v in out.items() if k.startswith(c)}), flush=True)
     print(json.dumps({"env": {k: os.environ.get(k) for k in ("HSK_SJLT_CFG", "HSK_GAUSS_CFG")},
                       "results": out}))
