@@ -47,9 +47,10 @@
 #endif
 #define DBG_IS(m) (HSK_SJLT_DEBUG && p.dbg == (m))
 
-// producer warps of the transposing cp.async S' path (128-row tiles)
+// producer warps of the transposed 128-row S' tiles: mode 4 (TMA staging +
+// in-smem transpose) measured 10.9 ms on C3 with 8, 12.3 with 4; mode 1 (unaligned A)
 #ifndef HSK_XPOSE_PRODUCERS
-#define HSK_XPOSE_PRODUCERS 4
+#define HSK_XPOSE_PRODUCERS 8
 #endif
 constexpr int kXposeProducers = HSK_XPOSE_PRODUCERS;
 
@@ -370,7 +371,8 @@ __global__ void __launch_bounds__((NW + (PROD ? (TRANS && RPT == 4 ? kXposeProdu
             done[s] = 0;
         }
         fence_mbar_init();
-        if (tma) prefetch_tmap(&tmap);
+        if (tma || mode == 4) prefetch_tmap(&tmap);
+        if (mode == 4) mbar_init(full + 7, 1);  // staging buffer (stages <= 7 here)
         if (SK) {
             // sk[0]: the first segment is the tail of a tile (publish it);
             // sk[1], sk[2]: the last segment is the head of a tile cut by the
@@ -516,6 +518,50 @@ __global__ void __launch_bounds__((NW + (PROD ? (TRANS && RPT == 4 ? kXposeProdu
                         if (j >= stages) mbar_wait(&empty[j % stages], (uint32_t)((j / stages) - 1) & 1u);
                         issue_tma(j);
                     }
+                }
+            } else if (XPOSE && mode == 4) {
+                // transposed 128-row S' tiles of aligned A: one lane TMA-loads
+                // the chunk in A's natural layout (16 x TM boxes, 128-byte
+                // swizzle) into a staging buffer; the PW warps transpose it into
+                // the ring slot (conflict-free for the consumers); a named
+                // barrier among them frees the staging buffer for the next TMA
+                const int ptid = threadIdx.x - NW * 32;
+                unsigned char *stg = stage0 + (size_t)stages * p.stage_bytes;  // 1024-aligned
+                uint64_t *stg_full = full + 7;
+                auto issue_stg = [&](int j) {
+                    int64_t r0, c;
+                    chunk_of(j, r0, c);
+                    mbar_arrive_expect_tx(stg_full, tile_bytes);
+                    for (int kb = 0; kb < p.tk / 16; ++kb)
+                        tma_load_2d(stg + kb * TM * 128, &tmap, (int)(c * p.tk + kb * 16), (int)r0, stg_full);
+                };
+                if (ptid == 0 && jn > 0) issue_stg(0);
+                for (int j = 0; j < jn; ++j) {
+                    const int s = j % stages;
+                    unsigned char *st = stage0 + (size_t)s * p.stage_bytes;
+                    if (j >= stages) mbar_wait(&empty[s], (uint32_t)((j / stages) - 1) & 1u);
+                    if (ptid == 0) {
+                        int64_t r0, c;
+                        chunk_of(j, r0, c);
+                        mbar_arrive_expect_tx(&full[s], bp_bytes + en_bytes);
+                        bulk_g2s(st + p.bp_off, p.bptr + c * p.bstride + j0, bp_bytes, &full[s]);
+                        bulk_g2s(st + p.en_off, p.ent + c * p.estride, en_bytes, &full[s]);
+                    }
+                    mbar_wait(stg_full, (uint32_t)(j & 1));
+                    // (kk, kk+1) of column cc: one 16-byte load from the swizzled
+                    // staging tile, two 8-byte stores at kk*TM + (cc ^ kk%32)
+                    double *dst = reinterpret_cast<double *>(st);
+                    for (int u = ptid; u < (p.tk / 2) * TM; u += PW * 32) {
+                        const int cc = u % TM, kk = 2 * (u / TM);
+                        const uint32_t off = (uint32_t)((kk >> 4) * TM * 128 + cc * 128) +
+                                             ((uint32_t)((kk & 15) * 8) ^ ((uint32_t)(cc & 7) << 4));
+                        const double2 v = *reinterpret_cast<const double2 *>(stg + off);
+                        dst[kk * TM + (cc ^ (kk & 31))] = v.x;
+                        dst[(kk + 1) * TM + (cc ^ ((kk + 1) & 31))] = v.y;
+                    }
+                    asm volatile("bar.sync 2, %0;" ::"r"(PW * 32) : "memory");  // staging read
+                    if (ptid == 0 && j + 1 < jn) issue_stg(j + 1);
+                    mbar_arrive(&full[s]);  // this thread's stores of slot s are done
                 }
             } else {
                 const int ptid = threadIdx.x - NW * 32;
@@ -764,7 +810,8 @@ static int launch(ApplyArgs a, const Geom &g, cudaStream_t st) {
     // 0: TMA S tile; 1: cp.async S' tile (unaligned A); 2: cp.async S tile;
     // 3: TMA S' tile (16 x TM boxes, 128-byte swizzle)
     constexpr bool XPOSE = RPT == 4;  // (for S') transposed tile, cp.async producer
-    a.mode = a.trans ? (!XPOSE && aligned && a.tk % 16 == 0 ? 3 : 1) : (aligned ? 0 : 2);
+    // 4: TMA S' staging + in-smem transpose into the transposed 128-row tile
+    a.mode = a.trans ? (aligned && a.tk % 16 == 0 ? (XPOSE ? 4 : 3) : 1) : (aligned ? 0 : 2);
     a.log2tk = 0;
     while ((1 << a.log2tk) < a.tk) ++a.log2tk;
     // S' tiles occupy whole 16-index blocks (the layout's unit); ring slots
@@ -790,7 +837,9 @@ static int launch(ApplyArgs a, const Geom &g, cudaStream_t st) {
     bool prod = NW < 32;
     if (const char *env = getenv("HSK_SJLT_PROD")) prod = env[0] == '1';
     const int pw = a.trans && XPOSE ? kXposeProducers : 1;
-    prod = prod && (a.mode == 0 || a.mode == 3 || (a.mode == 1 && XPOSE)) && NW + pw <= 32;
+    prod = prod && (a.mode == 0 || a.mode == 3 || ((a.mode == 1 || a.mode == 4) && XPOSE)) &&
+           NW + pw <= 32;
+    if (a.mode == 4 && !prod) a.mode = 1;  // the staging transpose needs the producer warps
     // persistent balanced schedule (stream-K) when whole-tile CTAs would
     // leave a partial last wave: one CTA per SM, groups of nslabs CTAs (the
     // slabs of a row tile stay in lockstep, so A is read from HBM once)
@@ -824,14 +873,15 @@ static int launch(ApplyArgs a, const Geom &g, cudaStream_t st) {
         int rc = make_tmap_f64_2d(&tmap, a.A, (uint64_t)a.m_out, (uint64_t)a.n, (uint64_t)a.lda,
                                   TM, (uint32_t)(a.tk / a.mc));
         if (rc) return rc;
-    } else if (a.mode == 3) {  // A is n x m_out: inner dimension = input index
+    } else if (a.mode == 3 || a.mode == 4) {  // A is n x m_out: inner dimension = input index
         int rc = make_tmap_f64_2d(&tmap, a.A, (uint64_t)a.n, (uint64_t)a.m_out, (uint64_t)a.lda,
                                   16, TM, true);
         if (rc) return rc;
     }
     const int nthreads = (NW + (prod ? pw : 0)) * 32;
     const int budget = 226 * 1024;
-    const int stages_max = std::max(2, std::min(8, (budget - 2048) / a.stage_bytes));
+    const int stg_bytes = a.mode == 4 ? a_bytes : 0;  // mode 4 staging buffer
+    const int stages_max = std::max(2, std::min(7, (budget - 2048 - stg_bytes) / a.stage_bytes));
     if (a.streamk && a.mc > 1) {
         // every group is one cluster and groups wait on later groups: keep
         // the grid to the clusters that can be co-resident
@@ -879,7 +929,7 @@ static int launch(ApplyArgs a, const Geom &g, cudaStream_t st) {
     a.stages = stages_max;
     if (const char *env = getenv("HSK_SJLT_STAGES")) a.stages = std::max(2, std::min(a.stages, atoi(env)));
     if (per > 0 && a.stages > per + 1) a.stages = std::max(2, per + 1);
-    int smem = 2048 + a.stages * a.stage_bytes;  // header + 1024-byte alignment slack
+    int smem = 2048 + a.stages * a.stage_bytes + stg_bytes;  // header + 1024-byte alignment slack
     if (ks > 1) smem = std::max(smem, 2048 + NW * DB * RPT * 32 * 8);
     auto kern = a.trans ? (prod ? (a.streamk ? sjlt_apply_kernel<RPT, DB, NW, true, true, true>
                                              : sjlt_apply_kernel<RPT, DB, NW, true, true, false>)
