@@ -138,6 +138,12 @@ HSK_API int hsk_ipc_close(void *ptr);
 HSK_API int hsk_sum_slices(const double *base, int32_t nslices, int64_t stride, int64_t rows,
                    int64_t cols, int64_t ld, double *out, int64_t ldo, void *stream);
 
+/* Strided async copy of `height` rows of `width` bytes (pitches in bytes);
+ * kind 1 = host -> device, 2 = device -> host.  Used to stream row slabs of a
+ * pinned host matrix through the kernels (copy / compute overlap). */
+HSK_API int hsk_memcpy2d(void *dst, int64_t dpitch, const void *src, int64_t spitch, int64_t width,
+                 int64_t height, int32_t kind, void *stream);
+
 #ifdef __cplusplus
 }
 #endif

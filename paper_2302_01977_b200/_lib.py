@@ -48,6 +48,7 @@ SIGNATURES = {
     "hsk_ipc_close": (ctypes.c_int, [_c_p]),
     "hsk_sum_slices": (ctypes.c_int, [_c_p, _c_i32, _c_i64, _c_i64, _c_i64, _c_i64, _c_p, _c_i64,
                                       _c_p]),
+    "hsk_memcpy2d": (ctypes.c_int, [_c_p, _c_i64, _c_p, _c_i64, _c_i64, _c_i64, _c_i32, _c_p]),
 }
 
 _lock = threading.Lock()

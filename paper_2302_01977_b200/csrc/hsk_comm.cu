@@ -89,3 +89,20 @@ extern "C" int hsk_sum_slices(const double *base, int32_t nslices, int64_t strid
     HSK_CHECK_LAUNCH("sum_slices_kernel");
     return HSK_OK;
 }
+
+// Strided 2-D copy (host <-> device, async on `stream`): `height` rows of
+// `width` bytes, pitches in bytes -- row slabs of column-major matrices for
+// the pipelined host path (sketching.apply_right on pinned host arrays).
+// kind: 1 = host to device, 2 = device to host.
+extern "C" int hsk_memcpy2d(void *dst, int64_t dpitch, const void *src, int64_t spitch,
+                            int64_t width, int64_t height, int32_t kind, void *stream) {
+    HSK_REQUIRE(kind == 1 || kind == 2, HSK_EINVAL, "memcpy2d: kind must be 1 or 2");
+    HSK_REQUIRE(width >= 0 && height >= 0 && dpitch >= width && spitch >= width, HSK_EINVAL,
+                "memcpy2d: bad shape");
+    if (width == 0 || height == 0) return HSK_OK;
+    cudaError_t e = cudaMemcpy2DAsync(dst, (size_t)dpitch, src, (size_t)spitch, (size_t)width,
+                                      (size_t)height,
+                                      kind == 1 ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToHost,
+                                      as_stream(stream));
+    return e == cudaSuccess ? HSK_OK : cuda_status(e, "memcpy2d");
+}

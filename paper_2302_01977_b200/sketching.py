@@ -191,6 +191,9 @@ def apply_right(A, op: SketchOperator) -> np.ndarray:
         raise ValueError(f"operator is over dimension {op.n}, matrix has {k} columns")
     if m == 0:
         return np.empty((0, op.d), order="F")
+    buf = _pinned_host_buffer(A)
+    if buf is not None:
+        return _streamed(buf, op, transpose=False)
     return apply_right_device(A, op).to_host()
 
 
@@ -201,4 +204,88 @@ def apply_right_transposed(A, op: SketchOperator) -> np.ndarray:
         raise ValueError(f"operator is over dimension {op.n}, matrix has {k} rows")
     if m == 0:
         return np.empty((0, op.d), order="F")
+    buf = _pinned_host_buffer(A)
+    if buf is not None:
+        return _streamed(buf, op, transpose=True)
     return apply_right_transposed_device(A, op).to_host()
+
+
+# ------------------------------------------------- streamed host matrices
+# A pinned host matrix of at least STREAM_MIN_BYTES is moved in slabs whose
+# H2D copy overlaps the previous slab's kernels and D2H copy (three streams,
+# two device slab buffers): the transfer, not the sketch, bounds this path,
+# and everything but the last slab's compute hides under it.  S rows (S'
+# rows) depend only on the same rows (columns) of A, so the result is
+# bit-identical to the one-shot device path.
+STREAM_MIN_BYTES = 256 << 20
+STREAM_SLABS = 8
+
+
+def _pinned_host_buffer(A):
+    """The F-ordered float64 host buffer of a raw array if it is page-locked
+    and large enough to stream; otherwise None."""
+    if isinstance(A, _dev.DeviceMatrix) or _is_accessor(A) or not isinstance(A, np.ndarray):
+        return None
+    if A.ndim != 2 or A.dtype != np.float64 or not A.flags.f_contiguous:
+        return None
+    if A.nbytes < STREAM_MIN_BYTES:
+        return None
+    try:
+        import torch
+        pinned = torch.from_numpy(A.T).is_pinned()  # (cols, rows) C-contiguous view
+    except Exception:  # noqa: BLE001
+        return None
+    return A if pinned else None
+
+
+def _streamed(buf: np.ndarray, op: SketchOperator, transpose: bool) -> np.ndarray:
+    import torch
+    from . import _lib
+    rows, cols = buf.shape
+    m_out = cols if transpose else rows       # output rows
+    nslab = max(1, min(STREAM_SLABS, m_out // 256))
+    step = -(-m_out // nslab)
+    step += step & 1                          # even leading dimension (16-byte TMA rows)
+    comp = torch.cuda.current_stream()
+    h2d, d2h = torch.cuda.Stream(), torch.cuda.Stream()
+    # slab buffers: S: `step` rows of A (ld step); S': `step` columns (ld rows)
+    sl_ld = step if not transpose else _dev.even_ld(rows)
+    sl_cols = cols if not transpose else step
+    slabs = [_dev.DeviceMatrix(step if not transpose else rows, sl_cols, ld=sl_ld) for _ in range(2)]
+    out = _dev.DeviceMatrix.empty(m_out, op.d)
+    host = torch.empty((op.d, m_out), dtype=torch.float64, pin_memory=True)
+    ev_in = [torch.cuda.Event() for _ in range(nslab)]
+    ev_k = [torch.cuda.Event() for _ in range(nslab)]
+    base = buf.ctypes.data
+    for i in range(nslab):
+        r0 = i * step
+        r1 = min(m_out, r0 + step)
+        if r0 >= r1:
+            break
+        h = r1 - r0
+        b = slabs[i % 2]
+        if i >= 2:
+            h2d.wait_event(ev_k[i - 2])       # slab buffer free
+        if transpose:   # columns [r0, r1) of A: h contiguous columns of `rows` doubles
+            _lib.call("hsk_memcpy2d", b.ptr, b.ld * 8, base + r0 * rows * 8, rows * 8, rows * 8, h, 1,
+                      h2d.cuda_stream)
+        else:           # rows [r0, r1) of A: `cols` columns of h doubles, pitch `rows`
+            _lib.call("hsk_memcpy2d", b.ptr, b.ld * 8, base + r0 * 8, rows * 8, h * 8, cols, 1,
+                      h2d.cuda_stream)
+        ev_in[i].record(h2d)
+        comp.wait_event(ev_in[i])
+        view = _dev.DeviceMatrix.__new__(_dev.DeviceMatrix)
+        if transpose:
+            view.rows, view.cols, view.ld, view.t = rows, h, b.ld, b.t[:h]
+            apply_right_transposed_device(view, op, out=out.row_view(r0, h))
+        else:
+            view.rows, view.cols, view.ld, view.t = h, cols, b.ld, b.t
+            apply_right_device(view, op, out=out.row_view(r0, h))
+        ev_k[i].record(comp)
+        d2h.wait_event(ev_k[i])
+        _lib.call("hsk_memcpy2d", host.data_ptr() + r0 * 8, m_out * 8, out.ptr + r0 * 8, out.ld * 8,
+                  h * 8, op.d, 2, d2h.cuda_stream)
+    d2h.synchronize()
+    comp.synchronize()
+    del slabs
+    return host.numpy().T                     # (m_out, d) F-contiguous, caller-owned

@@ -262,3 +262,27 @@ def test_adaptive_append_matches_one_shot(cuda):
         _close(ds.transposed(), O.apply_right_transposed(A, op), np.linalg.norm(A))
         # the one-shot API gives the identical bytes (same kernels, same order)
         np.testing.assert_array_equal(ds.right(), sk.apply_right(A, op))
+
+
+def test_streamed_pinned_host_path_is_bit_identical(cuda, monkeypatch):
+    """Pinned host matrices are streamed in slabs (H2D / kernels / D2H
+    overlapped); rows of S and S' depend only on their own rows / columns of
+    A, so the result must equal the one-shot device path bit for bit."""
+    import torch
+    monkeypatch.setattr(sk, "STREAM_MIN_BYTES", 1)
+    rng = np.random.default_rng(21)
+    m, n = 1111, 1500                          # odd sizes: ragged last slab
+    pin = torch.empty((n, m), dtype=torch.float64, pin_memory=True)
+    pin.copy_(torch.from_numpy(rng.standard_normal((n, m))))
+    A = pin.numpy().T                          # F-ordered m x n view of pinned memory
+    pinT = torch.empty((m, n), dtype=torch.float64, pin_memory=True)
+    pinT.copy_(torch.from_numpy(np.ascontiguousarray(A)))
+    B = pinT.numpy().T                         # F-ordered n x m (for S' over n rows)
+    assert sk._pinned_host_buffer(A) is not None and sk._pinned_host_buffer(B) is not None
+    for kind, kw in ((sk.SJLT, dict(alpha=4, construction=sk.BLOCK)), (sk.GAUSSIAN, {}),
+                     (sk.SRHT, {})):
+        op = sk.new_operator(kind, n, 96, seed=5, **kw)
+        ref = sk.apply_right_device(device.DeviceMatrix.from_host(A), op).to_host()
+        np.testing.assert_array_equal(sk.apply_right(A, op), ref)
+        ref_t = sk.apply_right_transposed_device(device.DeviceMatrix.from_host(B), op).to_host()
+        np.testing.assert_array_equal(sk.apply_right_transposed(B, op), ref_t)
