@@ -192,17 +192,92 @@ def run_reference(args):
 
 # --------------------------------------------------------------------- ours
 
+def run_rowshard(args):
+    """Opt-in (--workload c5_rowshard): BASELINE.json C5 shape, weak-scaled.
+
+    Global A is the (16384*world)^2 Gaussian-kernel matrix (x_i ~ U[0,1]^16,
+    h = 1.0 -- configs c5_sjlt); rank g holds rows [16384 g, 16384 (g+1)),
+    i.e. 16384 x 131072 per GPU at world 8, exactly C5's shard.  One step =
+    S rows (local, no communication) + S' rows through the p2p transport
+    (kernel epilogues store into peers' CUDA-IPC receive slots, then a
+    rank-ordered local sum), SJLT d = 2048, alpha = 8.  Device time on the
+    default stream between events, max over ranks.
+    """
+    import torch
+    import torch.distributed as dist
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    from paper_2302_01977_b200 import _lib, distributed as hd, matgen
+    from paper_2302_01977_b200 import sketching as sk
+    _lib.load()
+    rows, d, alpha = N, 2048, 8
+    n_glob = rows * world
+    pts = matgen.kernel_points(n_glob, 16, 0)
+    A = matgen.gaussian_kernel(n_glob, 16, 1.0, 1e-2, row0=rank * rows, nrows=rows, points=pts)
+    op = sk.new_operator(sk.SJLT, n_glob, d, np.random.SeedSequence((0, 0)), alpha=alpha,
+                         construction=sk.BLOCK)
+    stream = torch.cuda.current_stream()
+
+    def step():
+        return hd.sketch_row_sharded(A, op, rank=rank, world=world, n_rows=n_glob,
+                                     transport="p2p")
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(args.steps):
+        step()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / args.steps
+    if world > 1:
+        t = torch.tensor([ms], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    a_bytes = rows * n_glob * 8 * world
+    line = {
+        "metric": "row-sharded S and S' (p2p): A-streamed GB/s, 2 passes per step",
+        "value": 2 * a_bytes / (ms * 1e-3) / 1e9, "unit": "GB/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic",
+        "config": {"workload": "c5_rowshard", "n": n_glob, "rows_per_gpu": rows, "d": d,
+                   "alpha": alpha, "construction": "block",
+                   "matrix": "gaussian kernel 16-D h=1.0", "transport": "p2p",
+                   "parallelism": f"rowshard{world}"},
+    }
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    hd.release_peer_slots()
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=400)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default="c2_sjlt_S", choices=["c2_sjlt_S", "c5_rowshard"],
+                    help="c5_rowshard: opt-in multi-GPU S/S' exchange leg (not the headline)")
     ap.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline leg")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     if args.impl == "reference":
         run_reference(args)
+        return
+    if args.workload == "c5_rowshard":
+        run_rowshard(args)
         return
 
     import torch

@@ -73,6 +73,25 @@ def restrict_operator(op, r0: int, r1: int):
     return ops.SketchOperator(op.kind, r1 - r0, blocks, op.alpha, op.construction)
 
 
+_RESTRICTED: dict = {}
+
+
+def _restricted_cached(op, r0: int, r1: int):
+    """restrict_operator, memoised per (operator blocks, shard) so the device
+    state of the restricted blocks (SJLT plans, Gaussian matrices) is built
+    once, not on every sketch call.  Keeps the source blocks alive so ids
+    are not reused; an operator grown by append_columns has new blocks and
+    therefore a new key."""
+    key = (tuple(id(b) for b in op.blocks), r0, r1)
+    hit = _RESTRICTED.get(key)
+    if hit is None:
+        if len(_RESTRICTED) > 64:
+            _RESTRICTED.clear()
+        hit = (op.blocks, restrict_operator(op, r0, r1))
+        _RESTRICTED[key] = hit
+    return hit[1]
+
+
 # --------------------------------------------------------------- local math
 
 def _gpu_local_right(A_shard, op):
@@ -203,7 +222,7 @@ def sketch_row_sharded(A_shard, op, *, rank: int, world: int, n_rows: int,
         return S_local, None
     if op.n != n_rows:
         raise ValueError("S' = A^T R^T needs a square operator over the row space")
-    sub = restrict_operator(op, r0, r1)
+    sub = _restricted_cached(op, r0, r1)
     if transport is None:
         transport = "nccl" if (local_transposed is not None or deterministic) else "p2p"
     if transport == "p2p":

@@ -9,3 +9,4 @@ timeout 600 python bench.py > gpurun_out/bench.log 2>&1; echo rc=$?; tail -1 gpu
 timeout 600 python bench.py --steps 2 --warmup 3 > /dev/null 2>&1 && \
   timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/launches.csv python bench.py --steps 2 --warmup 3 > gpurun_out/ncu_l.log 2>&1; echo ncu1=$?
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:sjlt_apply -s 4 -c 1 -o gpurun_out/prof_bench_sjlt -f python bench.py --steps 2 --warmup 3 > gpurun_out/ncu_f.log 2>&1; echo ncu2=$?
+timeout 300 python -m torch.distributed.run --nnodes=1 --nproc-per-node 1 --master-addr 127.0.0.1 --master-port 29533 bench.py --workload c5_rowshard --steps 5 --warmup 3 > gpurun_out/rowshard.log 2>&1; echo rowshard=$?; tail -1 gpurun_out/rowshard.log
