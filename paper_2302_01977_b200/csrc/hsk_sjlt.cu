@@ -394,6 +394,9 @@ __global__ void __launch_bounds__((NW + (PROD ? (TRANS && RPT == 4 ? kXposeProdu
         }
     }
     __syncthreads();
+    // multicast loads and remote releases target the peers' barriers: every
+    // CTA of the cluster has initialised its ring before any of them issues
+    if (MC_ON) cluster_sync();
 
     // ---- producer helpers
     // row offset and chunk index of the CTA's j-th chunk (stream-K: 32-bit

@@ -123,7 +123,7 @@ __device__ __forceinline__ void wht16(double (&x)[16]) {
             }
 }
 
-template <int TPW>
+template <int TPW, bool TMAT>
 __global__ void __launch_bounds__(NW * 32, 1)
     srht_kernel(const Args p, const __grid_constant__ CUtensorMap tmap) {
     extern __shared__ __align__(128) unsigned char smem[];
@@ -132,6 +132,7 @@ __global__ void __launch_bounds__(NW * 32, 1)
     uint16_t *sgm_all = reinterpret_cast<uint16_t *>(smem + 64);        // stages x 16 masks
     int *s_samp = reinterpret_cast<int *>(smem + kSampOff);             // NW*TPW, sorted per warp
     int *s_col = s_samp + NW * 32;                                      // their output columns
+    uint32_t *s_pk = reinterpret_cast<uint32_t *>(s_col + NW * 32);     // NW x 8 packed positions
     double *X0 = reinterpret_cast<double *>(smem + kTileOff);  // 1024-B aligned (TMA)
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int slab = (int)(blockIdx.x % p.nslabs);
@@ -139,12 +140,15 @@ __global__ void __launch_bounds__(NW * 32, 1)
     const int t0 = slab * NW * TPW;
     const int tile_elems = p.seg * p.pitch;
     const int stages = p.stages;
-    const bool tma = p.use_tma != 0;
+    const bool tma = !TMAT && p.use_tma != 0;
     // S' (vectors = columns of A, contiguous): TMA lands each 32-vector x
     // 256 segment in its natural layout in a staging buffer; all warps
     // transpose it into X[k][vector] (pitch 33), and the next segment's TMA
-    // flies while this one is transformed and folded.  One X slot suffices.
-    const bool tmat = p.use_tma_t != 0;
+    // flies while this one is transformed and folded.  Two X slots: segment
+    // g+1 is transposed while slow warps may still fold segment g, so the
+    // fold needs no trailing barrier (slot g+1 was last read before the
+    // pass-A barrier of segment g).
+    const bool tmat = TMAT;  // == p.use_tma_t (separate instantiation: codegen)
     uint64_t *stg_full = full + (kMaxStages - 1);
     const double *stg = X0 + (size_t)stages * tile_elems;
 
@@ -173,6 +177,14 @@ __global__ void __launch_bounds__(NW * 32, 1)
             s_samp[warp * TPW + lane] = s_sorted;
             s_col[warp * TPW + lane] = valid_sorted ? t0 + warp * TPW + src : -1;
         }
+        // the same positions within a segment, one byte each: the fold reads
+        // them as two broadcast 16-byte loads per segment instead of TPW
+        // 4-byte ones (registers are full: TPW = 32 sits at 127)
+        const uint32_t byte = (uint32_t)(s_sorted & (p.seg - 1));
+        uint32_t w = byte << (8 * (lane & 3));
+        w |= __shfl_down_sync(0xffffffffu, w, 1);
+        w |= __shfl_down_sync(0xffffffffu, w, 2);
+        if ((lane & 3) == 0 && lane < TPW) s_pk[warp * 8 + (lane >> 2)] = w;
     }
     if (tid == 0) {
         for (int q = 0; q < stages; ++q) mbar_init(&full[q], 1);
@@ -242,7 +254,8 @@ __global__ void __launch_bounds__(NW * 32, 1)
             if (tid == 0 && g + 1 < G) issue_t(g + 1);
         } else {
         // the slot of segment g-1 is free: every thread passed its last sync
-        if (g + stages - 1 < G) issue(g + stages - 1);
+        // (TMA path: issued after pass A's barrier below instead)
+        if (!tma && g + stages - 1 < G) issue(g + stages - 1);
         if (tma) {
             mbar_wait(&full[q], (uint32_t)((g / stages) & 1));
         } else {
@@ -266,6 +279,9 @@ __global__ void __launch_bounds__(NW * 32, 1)
 #pragma unroll
             for (int u = 0; u < 16; ++u) X[(warp + 16 * u) * p.pitch + lane] = x[u];
             __syncthreads();
+            // TMA path: every thread is past the fold of segment g-1 here, so
+            // its slot is refilled now and the fold needs no trailing barrier
+            if (tma && g + stages - 1 < G) issue(g + stages - 1);
             // pass B: k = 16 w + q, butterflies over k bits 0..3
 #pragma unroll
             for (int u = 0; u < 16; ++u) x[u] = X[(16 * warp + u) * p.pitch + lane];
@@ -293,14 +309,23 @@ __global__ void __launch_bounds__(NW * 32, 1)
             const int sw = lane < TPW ? s_samp[warp * TPW + lane] : 0;
             const uint32_t neg = __ballot_sync(0xffffffffu,
                                                __popc((unsigned)(g & (sw >> lb))) & 1);
+            uint32_t pk[(TPW + 3) / 4];
+#pragma unroll
+            for (int v = 0; v < (TPW + 3) / 4; v += 4) {
+                const uint4 q4 = *reinterpret_cast<const uint4 *>(s_pk + warp * 8 + v);
+                pk[v] = q4.x;
+                if (v + 1 < (TPW + 3) / 4) pk[v + 1] = q4.y;
+                if (v + 2 < (TPW + 3) / 4) pk[v + 2] = q4.z;
+                if (v + 3 < (TPW + 3) / 4) pk[v + 3] = q4.w;
+            }
 #pragma unroll
             for (int i = 0; i < TPW; ++i) {
-                const int s_lo = s_samp[warp * TPW + i] & (p.seg - 1);
+                const int s_lo = (int)__byte_perm(pk[i >> 2], 0u, 0x4440u | (uint32_t)(i & 3));
                 const double gsg = __hiloint2double((int)(((neg >> i) & 1u) << 31 | 0x3FF00000u), 0);
                 acc[i] = fma(X[s_lo * p.pitch + lane], gsg, acc[i]);
             }
         }
-        __syncthreads();  // X (slot q) is refilled by the issue of segment g + 1
+        if (!tma && !tmat) __syncthreads();  // X (slot q) is refilled by the issue of segment g + 1
     }
     if (!tma && !tmat) cp_async_wait<0>();
 
@@ -333,13 +358,13 @@ static int launch(Args a, cudaStream_t st) {
         if (rc) return rc;
     }
     const int tile = a.seg * a.pitch * 8;
-    static_assert(NW * 32 * 4 * 2 <= 2 * 32 * 32 * 4, "sample tables must fit below kTileOff");
+    static_assert(kSampOff + NW * 32 * 4 * 2 + NW * 8 * 4 <= kTileOff, "sample tables must fit below kTileOff");
     const int fixed = kTileOff;
     a.stages = (int)std::min<int64_t>(3, std::max<int64_t>(2, a.nseg));
     while (a.stages > 2 && fixed + a.stages * tile > 227 * 1024) --a.stages;
-    if (a.use_tma_t) a.stages = 1;  // one X slot + the staging tile
+    if (a.use_tma_t) a.stages = 2;  // two X slots + the staging tile
     const int smem = fixed + a.stages * tile + (a.use_tma_t ? SEG * TM * 8 : 0);
-    auto kern = srht_kernel<TPW>;
+    auto kern = a.use_tma_t ? srht_kernel<TPW, true> : srht_kernel<TPW, false>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e != cudaSuccess) return cuda_status(e, "srht: set smem attribute");
     a.nslabs = (a.d + NW * TPW - 1) / (NW * TPW);
