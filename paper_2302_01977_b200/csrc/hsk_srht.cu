@@ -35,7 +35,7 @@ struct Args {
     int trans;
     int vec16;
     int use_tma;
-    int use_tma_t;  // S' of aligned A: TMA natural-layout staging + in-smem transpose
+    int use_tma_t;  // S' of aligned A: swizzled TMA staging read by pass A
     int64_t m_out;   // number of vectors
     int64_t n;       // vector length (before padding)
     int64_t n_pad;
@@ -142,12 +142,14 @@ __global__ void __launch_bounds__(NW * 32, 1)
     const int stages = p.stages;
     const bool tma = !TMAT && p.use_tma != 0;
     // S' (vectors = columns of A, contiguous): TMA lands each 32-vector x
-    // 256 segment in its natural layout in a staging buffer; all warps
-    // transpose it into X[k][vector] (pitch 33), and the next segment's TMA
-    // flies while this one is transformed and folded.  Two X slots: segment
-    // g+1 is transposed while slow warps may still fold segment g, so the
-    // fold needs no trailing barrier (slot g+1 was last read before the
-    // pass-A barrier of segment g).
+    // 256 segment in A's natural layout -- 16 boxes of 16 inputs x 32
+    // vectors, 128-byte swizzle -- in a staging buffer, and pass A reads it
+    // from there (lane = vector; 4-way bank conflicts, the price of not
+    // transposing) and writes X[k][vector]; the next segment's TMA is issued
+    // once pass A's barrier shows the staging buffer consumed.  Two X slots:
+    // pass A of segment g+1 may run while slow warps still fold segment g
+    // (slot g+1 was last read before the pass-A barrier of segment g), so
+    // the fold needs no trailing barrier.
     const bool tmat = TMAT;  // == p.use_tma_t (separate instantiation: codegen)
     uint64_t *stg_full = full + (kMaxStages - 1);
     const double *stg = X0 + (size_t)stages * tile_elems;
@@ -220,7 +222,9 @@ __global__ void __launch_bounds__(NW * 32, 1)
     // S' staging issue (thread 0): segment g and its sign masks (mask slot g & 1)
     auto issue_t = [&](int64_t g) {
         mbar_arrive_expect_tx(stg_full, (uint32_t)(SEG * TM * 8 + 32));
-        tma_load_2d(const_cast<double *>(stg), &tmap, (int)(g * SEG), (int)r0, stg_full);
+        for (int u = 0; u < SEG / 16; ++u)  // box u: inputs 16u.. of the 32 vectors (4 KB)
+            tma_load_2d(const_cast<double *>(stg) + u * 16 * TM, &tmap, (int)(g * SEG + 16 * u), (int)r0,
+                        stg_full);
         bulk_g2s(sgm_all + (g & 1) * 16, p.masks + g * 16, 32, stg_full);
     };
 
@@ -242,16 +246,6 @@ __global__ void __launch_bounds__(NW * 32, 1)
         const double *sg = sgn_all + q * SEG;
         if (tmat) {
             mbar_wait(stg_full, (uint32_t)(g & 1));
-            // natural layout stg[vector][k] -> X[k][vector]: lanes along k
-            // (conflict-free reads; pitch-33 writes are 2-way at worst)
-#pragma unroll 4
-            for (int it = 0; it < (SEG * TM) / (NW * 32); ++it) {
-                const int idx = it * NW * 32 + tid;
-                const int c = idx >> 8, k = idx & (SEG - 1);
-                X[k * p.pitch + c] = stg[c * SEG + k];
-            }
-            __syncthreads();  // staging consumed: fetch the next segment now
-            if (tid == 0 && g + 1 < G) issue_t(g + 1);
         } else {
         // the slot of segment g-1 is free: every thread passed its last sync
         // (TMA path: issued after pass A's barrier below instead)
@@ -269,11 +263,21 @@ __global__ void __launch_bounds__(NW * 32, 1)
             // by flipping sign bits: exact, as the reference's multiply by +-1)
             double x[16];
             const uint32_t msk = sgm_all[(tmat ? (int)(g & 1) : q) * 16 + warp];
+            if (tmat) {
+                // input w + 16u of vector `lane`: box u, 128-byte row `lane`,
+                // 16-byte chunk (w/2) ^ (lane%8)
+                const double *sb = stg + lane * 16 + ((((warp * 8) ^ ((lane & 7) << 4))) >> 3);
 #pragma unroll
-            for (int u = 0; u < 16; ++u) {
-                const int k = warp + 16 * u;
-                x[u] = __longlong_as_double(__double_as_longlong(X[k * p.pitch + lane]) ^
-                                            ((long long)((msk >> u) & 1u) << 63));
+                for (int u = 0; u < 16; ++u)
+                    x[u] = __longlong_as_double(__double_as_longlong(sb[u * 16 * TM]) ^
+                                                ((long long)((msk >> u) & 1u) << 63));
+            } else {
+#pragma unroll
+                for (int u = 0; u < 16; ++u) {
+                    const int k = warp + 16 * u;
+                    x[u] = __longlong_as_double(__double_as_longlong(X[k * p.pitch + lane]) ^
+                                                ((long long)((msk >> u) & 1u) << 63));
+                }
             }
             wht16(x);
 #pragma unroll
@@ -282,6 +286,8 @@ __global__ void __launch_bounds__(NW * 32, 1)
             // TMA path: every thread is past the fold of segment g-1 here, so
             // its slot is refilled now and the fold needs no trailing barrier
             if (tma && g + stages - 1 < G) issue(g + stages - 1);
+            // S': every warp is past pass A, the staging buffer is free
+            if (tmat && tid == 0 && g + 1 < G) issue_t(g + 1);
             // pass B: k = 16 w + q, butterflies over k bits 0..3
 #pragma unroll
             for (int u = 0; u < 16; ++u) x[u] = X[(16 * warp + u) * p.pitch + lane];
@@ -344,7 +350,7 @@ static int launch(Args a, cudaStream_t st) {
     // TMA for row tiles of aligned A with full 256-column segments
     a.use_tma = !a.trans && a.vec16 && a.seg == SEG;
     a.use_tma_t = a.trans && a.vec16 && a.seg == SEG;
-    a.pitch = a.trans ? TM + 1 : TM;
+    a.pitch = a.trans && !a.use_tma_t ? TM + 1 : TM;  // pitch 33: transposing cp.async stores
     a.nseg = a.n_pad / a.seg;
     CUtensorMap tmap;
     memset(&tmap, 0, sizeof(tmap));
@@ -352,9 +358,9 @@ static int launch(Args a, cudaStream_t st) {
         int rc = make_tmap_f64_2d(&tmap, a.A, (uint64_t)a.m_out, (uint64_t)a.n, (uint64_t)a.lda,
                                   TM, SEG);
         if (rc) return rc;
-    } else if (a.use_tma_t) {  // A is n x m_out: box of SEG input indices x TM vectors
+    } else if (a.use_tma_t) {  // A is n x m_out: boxes of 16 input indices x TM vectors, swizzled
         int rc = make_tmap_f64_2d(&tmap, a.A, (uint64_t)a.n, (uint64_t)a.m_out, (uint64_t)a.lda,
-                                  SEG, TM);
+                                  16, TM, true);
         if (rc) return rc;
     }
     const int tile = a.seg * a.pitch * 8;
