@@ -123,7 +123,9 @@ __device__ __forceinline__ void wht16(double (&x)[16]) {
             }
 }
 
-template <int TPW, bool TMAT>
+// PATH 0: cp.async segments (unaligned A, n_pad < 256); 1: TMA S tiles;
+// 2: TMA S' staging (separate instantiations: code generation)
+template <int TPW, int PATH>
 __global__ void __launch_bounds__(NW * 32, 1)
     srht_kernel(const Args p, const __grid_constant__ CUtensorMap tmap) {
     extern __shared__ __align__(128) unsigned char smem[];
@@ -140,7 +142,7 @@ __global__ void __launch_bounds__(NW * 32, 1)
     const int t0 = slab * NW * TPW;
     const int tile_elems = p.seg * p.pitch;
     const int stages = p.stages;
-    const bool tma = !TMAT && p.use_tma != 0;
+    constexpr bool tma = PATH == 1;  // == p.use_tma
     // S' (vectors = columns of A, contiguous): TMA lands each 32-vector x
     // 256 segment in A's natural layout -- 16 boxes of 16 inputs x 32
     // vectors, 128-byte swizzle -- in a staging buffer, and pass A reads it
@@ -150,7 +152,7 @@ __global__ void __launch_bounds__(NW * 32, 1)
     // pass A of segment g+1 may run while slow warps still fold segment g
     // (slot g+1 was last read before the pass-A barrier of segment g), so
     // the fold needs no trailing barrier.
-    const bool tmat = TMAT;  // == p.use_tma_t (separate instantiation: codegen)
+    constexpr bool tmat = PATH == 2;  // == p.use_tma_t
     uint64_t *stg_full = full + (kMaxStages - 1);
     const double *stg = X0 + (size_t)stages * tile_elems;
 
@@ -370,7 +372,7 @@ static int launch(Args a, cudaStream_t st) {
     while (a.stages > 2 && fixed + a.stages * tile > 227 * 1024) --a.stages;
     if (a.use_tma_t) a.stages = 2;  // two X slots + the staging tile
     const int smem = fixed + a.stages * tile + (a.use_tma_t ? SEG * TM * 8 : 0);
-    auto kern = a.use_tma_t ? srht_kernel<TPW, true> : srht_kernel<TPW, false>;
+    auto kern = a.use_tma_t ? srht_kernel<TPW, 2> : a.use_tma ? srht_kernel<TPW, 1> : srht_kernel<TPW, 0>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e != cudaSuccess) return cuda_status(e, "srht: set smem attribute");
     a.nslabs = (a.d + NW * TPW - 1) / (NW * TPW);
