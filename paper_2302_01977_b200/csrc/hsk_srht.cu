@@ -137,10 +137,14 @@ __global__ void __launch_bounds__(NW * 32, 1)
     uint32_t *s_pk = reinterpret_cast<uint32_t *>(s_col + NW * 32);     // NW x 8 packed positions
     double *X0 = reinterpret_cast<double *>(smem + kTileOff);  // 1024-B aligned (TMA)
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    // the TMA paths always run 256-input segments at pitch TM: compile-time
+    // constants there (shared-memory addresses become immediate offsets)
+    const int pitch = PATH == 0 ? p.pitch : TM;
+    const int seg = PATH == 0 ? p.seg : SEG;
     const int slab = (int)(blockIdx.x % p.nslabs);
     const int64_t r0 = (blockIdx.x / p.nslabs) * TM;
     const int t0 = slab * NW * TPW;
-    const int tile_elems = p.seg * p.pitch;
+    const int tile_elems = seg * pitch;
     const int stages = p.stages;
     constexpr bool tma = PATH == 1;  // == p.use_tma
     // S' (vectors = columns of A, contiguous): TMA lands each 32-vector x
@@ -163,7 +167,7 @@ __global__ void __launch_bounds__(NW * 32, 1)
         const bool valid = lane < TPW && t < p.d;
         const int sv = valid ? (int)p.sample[t] : 0;
         // key: (position, lane) -- invalid samples sort last
-        uint64_t key = ((uint64_t)(valid ? (uint32_t)(sv & (p.seg - 1)) : 0xFFFFFFu) << 32) |
+        uint64_t key = ((uint64_t)(valid ? (uint32_t)(sv & (seg - 1)) : 0xFFFFFFu) << 32) |
                        (uint32_t)lane;
 #pragma unroll
         for (int kk = 2; kk <= 32; kk <<= 1)
@@ -184,7 +188,7 @@ __global__ void __launch_bounds__(NW * 32, 1)
         // the same positions within a segment, one byte each: the fold reads
         // them as two broadcast 16-byte loads per segment instead of TPW
         // 4-byte ones (registers are full: TPW = 32 sits at 127)
-        const uint32_t byte = (uint32_t)(s_sorted & (p.seg - 1));
+        const uint32_t byte = (uint32_t)(s_sorted & (seg - 1));
         uint32_t w = byte << (8 * (lane & 3));
         w |= __shfl_down_sync(0xffffffffu, w, 1);
         w |= __shfl_down_sync(0xffffffffu, w, 2);
@@ -198,25 +202,24 @@ __global__ void __launch_bounds__(NW * 32, 1)
     }
     __syncthreads();
     const int64_t G = p.nseg;
-    const int lb = 31 - __clz(p.seg);  // log2(seg)
+    const int lb = 31 - __clz(seg);  // log2(seg)
 
-    // issue segment g into slot g % stages (TMA path: one thread; else all)
-    auto issue = [&](int64_t g) {
-        const int q = (int)(g % stages);
+    // issue segment g into slot q == g % stages (TMA path: one thread; else all)
+    auto issue = [&](int64_t g, int q) {
         double *X = X0 + (size_t)q * tile_elems;
         double *sg = sgn_all + q * SEG;
         if (tma) {  // (TMA implies seg == 256: sign masks)
             if (tid == 0) {
-                mbar_arrive_expect_tx(&full[q], (uint32_t)(p.seg * TM * 8 + 32));
-                tma_load_2d(X, &tmap, (int)r0, (int)(g * p.seg), &full[q]);
+                mbar_arrive_expect_tx(&full[q], (uint32_t)(seg * TM * 8 + 32));
+                tma_load_2d(X, &tmap, (int)r0, (int)(g * seg), &full[q]);
                 bulk_g2s(sgm_all + q * 16, p.masks + g * 16, 32, &full[q]);
             }
         } else {
             load_segment_async(p, X, r0, g);
-            if (p.seg == SEG) {
+            if (seg == SEG) {
                 if (tid < 2) cp_async16(sgm_all + q * 16 + 8 * tid, p.masks + g * 16 + 8 * tid, true);
             } else {
-                for (int k = tid; k < p.seg; k += NW * 32) cp_async8(sg + k, p.signs + g * p.seg + k, true);
+                for (int k = tid; k < seg; k += NW * 32) cp_async8(sg + k, p.signs + g * seg + k, true);
             }
         }
     };
@@ -238,12 +241,15 @@ __global__ void __launch_bounds__(NW * 32, 1)
         if (tid == 0 && G > 0) issue_t(0);
     } else {
         for (int64_t g = 0; g < stages - 1 && g < G; ++g) {
-            issue(g);
+            issue(g, (int)g);
             if (!tma) cp_async_commit();
         }
     }
+    // slot q = g % stages and its full-barrier parity (g / stages) & 1, kept
+    // incrementally (no 64-bit division per segment); qi = slot of g - 1
+    int q = 0, qi = stages - 1;
+    uint32_t fph = 0;
     for (int64_t g = 0; g < G; ++g) {
-        const int q = (int)(g % stages);
         double *X = X0 + (size_t)q * tile_elems;
         const double *sg = sgn_all + q * SEG;
         if (tmat) {
@@ -251,16 +257,16 @@ __global__ void __launch_bounds__(NW * 32, 1)
         } else {
         // the slot of segment g-1 is free: every thread passed its last sync
         // (TMA path: issued after pass A's barrier below instead)
-        if (!tma && g + stages - 1 < G) issue(g + stages - 1);
+        if (!tma && g + stages - 1 < G) issue(g + stages - 1, qi);
         if (tma) {
-            mbar_wait(&full[q], (uint32_t)((g / stages) & 1));
+            mbar_wait(&full[q], fph);
         } else {
             cp_async_commit();
             if (stages == 2) cp_async_wait<1>(); else cp_async_wait<2>();
             __syncthreads();
         }
         }
-        if (p.seg == SEG) {
+        if (seg == SEG) {
             // pass A: k = w + 16 q, butterflies over k bits 4..7 (signs applied
             // by flipping sign bits: exact, as the reference's multiply by +-1)
             double x[16];
@@ -277,35 +283,35 @@ __global__ void __launch_bounds__(NW * 32, 1)
 #pragma unroll
                 for (int u = 0; u < 16; ++u) {
                     const int k = warp + 16 * u;
-                    x[u] = __longlong_as_double(__double_as_longlong(X[k * p.pitch + lane]) ^
+                    x[u] = __longlong_as_double(__double_as_longlong(X[k * pitch + lane]) ^
                                                 ((long long)((msk >> u) & 1u) << 63));
                 }
             }
             wht16(x);
 #pragma unroll
-            for (int u = 0; u < 16; ++u) X[(warp + 16 * u) * p.pitch + lane] = x[u];
+            for (int u = 0; u < 16; ++u) X[(warp + 16 * u) * pitch + lane] = x[u];
             __syncthreads();
             // TMA path: every thread is past the fold of segment g-1 here, so
             // its slot is refilled now and the fold needs no trailing barrier
-            if (tma && g + stages - 1 < G) issue(g + stages - 1);
+            if (tma && g + stages - 1 < G) issue(g + stages - 1, qi);
             // S': every warp is past pass A, the staging buffer is free
             if (tmat && tid == 0 && g + 1 < G) issue_t(g + 1);
             // pass B: k = 16 w + q, butterflies over k bits 0..3
 #pragma unroll
-            for (int u = 0; u < 16; ++u) x[u] = X[(16 * warp + u) * p.pitch + lane];
+            for (int u = 0; u < 16; ++u) x[u] = X[(16 * warp + u) * pitch + lane];
             wht16(x);
 #pragma unroll
-            for (int u = 0; u < 16; ++u) X[(16 * warp + u) * p.pitch + lane] = x[u];
+            for (int u = 0; u < 16; ++u) X[(16 * warp + u) * pitch + lane] = x[u];
         } else {
             // small n_pad (< 256): signs, then in-smem radix-2 stages
-            for (int k = warp; k < p.seg; k += NW) X[k * p.pitch + lane] *= sg[k];
+            for (int k = warp; k < seg; k += NW) X[k * pitch + lane] *= sg[k];
             __syncthreads();
-            for (int h = 1; h < p.seg; h <<= 1) {
-                for (int pr = warp; pr < p.seg / 2; pr += NW) {
+            for (int h = 1; h < seg; h <<= 1) {
+                for (int pr = warp; pr < seg / 2; pr += NW) {
                     const int a_i = (pr / h) * 2 * h + (pr % h);
-                    const double a = X[a_i * p.pitch + lane], b = X[(a_i + h) * p.pitch + lane];
-                    X[a_i * p.pitch + lane] = a + b;
-                    X[(a_i + h) * p.pitch + lane] = a - b;
+                    const double a = X[a_i * pitch + lane], b = X[(a_i + h) * pitch + lane];
+                    X[a_i * pitch + lane] = a + b;
+                    X[(a_i + h) * pitch + lane] = a - b;
                 }
                 __syncthreads();
             }
@@ -326,14 +332,34 @@ __global__ void __launch_bounds__(NW * 32, 1)
                 if (v + 2 < (TPW + 3) / 4) pk[v + 2] = q4.z;
                 if (v + 3 < (TPW + 3) / 4) pk[v + 3] = q4.w;
             }
+            if constexpr (PATH != 0) {
+                // pitch 32: byte offset s_lo*256 + lane*8 assembled by one PRMT
+                // (byte 0 = lane*8, byte 1 = s_lo); the Walsh sign goes onto the
+                // value's sign bit (exact, as the +-1 product) and a DADD adds it
+                const char *xb = reinterpret_cast<const char *>(X);
+                const uint32_t lane8 = (uint32_t)lane * 8u;
 #pragma unroll
-            for (int i = 0; i < TPW; ++i) {
-                const int s_lo = (int)__byte_perm(pk[i >> 2], 0u, 0x4440u | (uint32_t)(i & 3));
-                const double gsg = __hiloint2double((int)(((neg >> i) & 1u) << 31 | 0x3FF00000u), 0);
-                acc[i] = fma(X[s_lo * p.pitch + lane], gsg, acc[i]);
+                for (int i = 0; i < TPW; ++i) {
+                    const uint32_t off = __byte_perm(pk[i >> 2], lane8, 0x5504u | ((uint32_t)(i & 3) << 4));
+                    const double v = *reinterpret_cast<const double *>(xb + off);
+                    const int hi = __double2hiint(v) ^ (int)((neg << (31 - i)) & 0x80000000u);
+                    acc[i] += __hiloint2double(hi, __double2loint(v));
+                }
+            } else {
+#pragma unroll
+                for (int i = 0; i < TPW; ++i) {
+                    const int s_lo = (int)__byte_perm(pk[i >> 2], 0u, 0x4440u | (uint32_t)(i & 3));
+                    const double gsg = __hiloint2double((int)(((neg >> i) & 1u) << 31 | 0x3FF00000u), 0);
+                    acc[i] = fma(X[s_lo * pitch + lane], gsg, acc[i]);
+                }
             }
         }
         if (!tma && !tmat) __syncthreads();  // X (slot q) is refilled by the issue of segment g + 1
+        qi = q;
+        if (++q == stages) {
+            q = 0;
+            fph ^= 1u;
+        }
     }
     if (!tma && !tmat) cp_async_wait<0>();
 
