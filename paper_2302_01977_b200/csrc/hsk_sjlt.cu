@@ -72,7 +72,6 @@ namespace sjlt {
 
 constexpr int kHeaderBytes = 128;
 constexpr int kMaxChunkEntries = 4096;  // TK * alpha bound (12-bit local index)
-constexpr int kPlanSlab = 512;          // bucket-offset rows padded for slabs | 512
 constexpr int64_t kMaxD = (1 << 19);    // bucket index fits 19 bits of the sort key
 
 // Per-direction sub-plan geometry.  One plan buffer holds a header, the S
@@ -82,39 +81,56 @@ constexpr int64_t kMaxD = (1 << 19);    // bucket index fits 19 bits of the sort
 // 32-row tiles with 512-bucket slabs and TK = 256 (half the slab re-reads).
 struct Geom {
     int rpt;           // rows per lane (tile rows tm = 32 * rpt)
+    int db, nw;        // buckets per consumer warp, consumer warps per CTA
+    int64_t ngroups;   // warp groups of db buckets (nslabs * nw)
     int tm;
     int pitch;         // tile pitch (doubles) = tm: TMA writes densely; the S'
                        // producer orders its transposing stores conflict-free
     int tk;            // input indices per chunk
     int64_t nchunks;
-    int64_t bstride;   // uint16 per bucket-offset row
-    int64_t estride;   // entries per chunk row (tk*alpha)
-    int64_t bptr_off;  // bytes from the plan base
+    int64_t gstride;   // uint32 per group-start row (ngroups + 1, padded)
+    int64_t estride;   // words per chunk row (tk*alpha entries + ngroups terminators)
+    int64_t gptr_off;  // bytes from the plan base
     int64_t ent_off;   // bytes from the plan base
     int64_t end;       // bytes from the plan base (end of this sub-plan)
 };
 
 static inline int64_t roundup(int64_t x, int64_t m) { return (x + m - 1) / m * m; }
 
-static inline int stage_bytes_for(int tk, int tm, int alpha) {  // mirrors launch<>()
-    const int64_t tile = ((int64_t)(tk + 15) / 16 * 16 * tm * 8 + 1023) / 1024 * 1024;
-    return (int)((tile + 1152 + ((int64_t)tk * alpha + 8) * 4 + 1023) / 1024 * 1024);
+// ring slot bytes: [tile][group starts][entry words + null words] (mirrors launch<>())
+static inline int stage_bytes_for(int tk, int tm, int alpha, int64_t ngroups, int nw) {
+    const int64_t tile = roundup((int64_t)(tk + 15) / 16 * 16 * tm * 8, 1024);
+    const int64_t en_off = roundup(tile + (nw + 4) / 4 * 16, 128);
+    return (int)roundup(en_off + (roundup((int64_t)tk * alpha + ngroups, 4) + 8) * 4, 1024);
 }
 
 // largest power-of-two TK <= cap whose stage fits `per_stage` bytes
-static inline int tk_fit(int alpha, int tm, int cap, int per_stage) {
+static inline int tk_fit(int alpha, int tm, int cap, int per_stage, int64_t ng, int nw) {
     int tk = cap;
-    while (tk > 1 && (tk * alpha > kMaxChunkEntries || stage_bytes_for(tk, tm, alpha) > per_stage))
+    while (tk > 1 && (tk * alpha > kMaxChunkEntries || stage_bytes_for(tk, tm, alpha, ng, nw) > per_stage))
         tk >>= 1;
     return tk;
 }
 
 // largest multiple of 16 TK <= cap (<= 256: TMA box limit) whose stage fits
-static inline int tk_fit16(int alpha, int tm, int cap, int per_stage) {
+static inline int tk_fit16(int alpha, int tm, int cap, int per_stage, int64_t ng, int nw) {
     int tk = cap;
-    while (tk > 16 && (tk * alpha > kMaxChunkEntries || stage_bytes_for(tk, tm, alpha) > per_stage))
+    while (tk > 16 && (tk * alpha > kMaxChunkEntries || stage_bytes_for(tk, tm, alpha, ng, nw) > per_stage))
         tk -= 16;
     return tk;
+}
+
+// consumer warps and buckets per warp of the kernel that walks a sub-plan
+// (16 consumer warps: the 96-register budget holds RPT x DB accumulators plus
+// the walker; the 32-warp variants, half the buckets per warp, are kept for
+// tuning: HSK_SJLT_W32=1)
+static inline void warp_shape(int rpt, int d, int &db, int &nw) {
+    bool w32 = false;
+    if (const char *env = getenv("HSK_SJLT_W32")) w32 = env[0] == '1';
+    nw = w32 ? 32 : 16;
+    if (rpt == 1) db = w32 ? 16 : 32;        // 32-row tiles, 512-bucket slabs
+    else if (rpt == 4) db = w32 ? 2 : 4;     // 128-row tiles, 64-bucket slabs
+    else db = (d <= 128 ? 4 : 8) * (w32 ? 1 : 2);  // 64-row tiles
 }
 
 static Geom geom_dir(int64_t n, int d, int alpha, int trans, int64_t base) {
@@ -134,23 +150,26 @@ static Geom geom_dir(int64_t n, int d, int alpha, int trans, int64_t base) {
     // CTAs sharing each tile through L2 want the deeper ring -- measured at
     // d = 2048, alpha = 8)
     const bool wide = n >= 8192 && (trans || d <= 512);
+    g.rpt = d <= 64 ? 4 : 2;
+    if (const char *env = getenv(trans ? "HSK_SJLT_RPT_T" : "HSK_SJLT_RPT")) g.rpt = atoi(env);
+    warp_shape(g.rpt, d, g.db, g.nw);
+    g.ngroups = roundup(d, (int64_t)g.db * g.nw) / g.db;
     if (d <= 64) {
-        g.rpt = 4;
-        tk = wide && !trans ? tk_fit16(alpha, 128, 256, kStage2) : tk_fit(alpha, 128, 128, kStage3);
+        tk = wide && !trans ? tk_fit16(alpha, 128, 256, kStage2, g.ngroups, g.nw)
+                            : tk_fit(alpha, 128, 128, kStage3, g.ngroups, g.nw);
     } else {
-        g.rpt = 2;
-        tk = wide ? tk_fit16(alpha, 64, 256, kStage2) : tk_fit(alpha, 64, 128, kStage3);
+        tk = wide ? tk_fit16(alpha, 64, 256, kStage2, g.ngroups, g.nw)
+                  : tk_fit(alpha, 64, 128, kStage3, g.ngroups, g.nw);
     }
     if (const char *env = getenv(trans ? "HSK_SJLT_TK_T" : "HSK_SJLT_TK")) tk = atoi(env);
-    if (const char *env = getenv(trans ? "HSK_SJLT_RPT_T" : "HSK_SJLT_RPT")) g.rpt = atoi(env);
     g.tm = 32 * g.rpt;
     g.pitch = g.tm;
     g.tk = tk;
     g.nchunks = (n + g.tk - 1) / g.tk;
-    g.bstride = roundup(d, kPlanSlab) + 8;
-    g.estride = roundup((int64_t)g.tk * alpha, 4);  // 16-byte rows for the bulk copy
-    g.bptr_off = base;
-    g.ent_off = roundup(g.bptr_off + (g.nchunks + 1) * g.bstride * 2, 128);
+    g.gstride = roundup(g.ngroups + 4, 4);  // a CTA copies nw + 1 starts, 16-byte rows
+    g.estride = roundup((int64_t)g.tk * alpha + g.ngroups, 4);  // 16-byte rows for the bulk copy
+    g.gptr_off = base;
+    g.ent_off = roundup(g.gptr_off + (g.nchunks + 1) * g.gstride * 4, 128);
     g.end = g.ent_off + roundup((g.nchunks + 1) * g.estride * 4, 128);
     return g;
 }
@@ -169,24 +188,29 @@ static Plan plan_geom(int64_t n, int d, int alpha) {
 }
 
 // ------------------------------------------------------------ plan build
-// Entry word for input index kk of a chunk (sign in bit 31, or-ed in):
-//   S  tiles (tm_t = 0):  kk << 3  -- the walker forms kk*TM*8 with one shift-add
-//                                     (bit 31 shifts out)
+// A chunk's entries are sorted by (bucket, input index); the entries of every
+// group of db buckets (the ones one consumer warp owns) are closed by a
+// terminator, so a warp's list is contiguous and self-delimiting.  Entry word:
+//   (sign < 0) << 31 | (bucket mod db) << 24 | address bits,
+// terminator bucket field = db (address bits 0).  Address bits of input index kk:
+//   S  tiles (tm_t = 0):  kk  -- the walker forms kk*TM*8 with one shift (the
+//                         sign and bucket bits shift out)
 //   S' tiles (tm_t = TM): (kk/16)*TM*128 + (kk%16)*8 -- the byte offset of (kk, col 0)
 //                         in the TMA S' tile layout (below); a lane's address is
-//                         base_lane + ((e ^ 16*(lane%8)) & 0x7fffffff): one LOP3 + add
+//                         base_lane + ((e ^ 16*(lane%8)) & 0xffffff): one LOP3 + add
 //   S' tiles (tm_t = -TM, transposed layout of 128-row tiles): kk*TM*8 | (kk%32)*8 --
-//                         lane address st + ((e ^ 8*lane) & 0x7fffffff)
-__host__ __device__ inline uint32_t entry_word(uint32_t kk, int tm_t) {
+//                         lane address st + (e & 0xffff00) + ((e & 248) ^ 8*lane)
+// Group starts: gptr[c * gstride + g] = index of group g's first word.
+__host__ __device__ inline uint32_t entry_addr(uint32_t kk, int tm_t) {
     if (tm_t < 0) return kk * (uint32_t)(-tm_t) * 8u + ((kk & 31u) << 3);
-    return tm_t ? (kk >> 4) * (uint32_t)tm_t * 128u + ((kk & 15u) << 3) : kk << 3;
+    return tm_t ? (kk >> 4) * (uint32_t)tm_t * 128u + ((kk & 15u) << 3) : kk;
 }
 
 // One CTA per chunk: sort the chunk's (bucket, local index) keys, emit
-// entry words in that order and per-bucket lower bounds.
+// bucket-tagged entry words, group terminators and group starts.
 __global__ void sjlt_plan_kernel(const int32_t *__restrict__ pos, const int8_t *__restrict__ sgn,
-                                 int64_t n, int d, int alpha, int tk, int p2, int64_t bstride,
-                                 int64_t estride, int tm_t, uint16_t *__restrict__ bptr,
+                                 int64_t n, int d, int alpha, int tk, int p2, int db, int64_t ngroups,
+                                 int64_t gstride, int64_t estride, int tm_t, uint32_t *__restrict__ gptr,
                                  uint32_t *__restrict__ ent, int *err) {
     extern __shared__ uint32_t keys[];
     const int64_t c = blockIdx.x;
@@ -223,22 +247,22 @@ __global__ void sjlt_plan_kernel(const int32_t *__restrict__ pos, const int8_t *
         }
     }
     uint32_t *e_out = ent + c * estride;
-    for (int e = threadIdx.x; e < estride; e += blockDim.x) {
-        // padding (a partial last chunk): the pipelined walk may load, never
-        // accumulate, the word after a warp's list -- it must address the tile
-        uint32_t w = 0u;
-        if (e < cnt) {
-            const int local = keys[e] & 4095;
-            w = entry_word((uint32_t)(local / alpha), tm_t) |
-                (sgn[q0 + local] < 0 ? 0x80000000u : 0u);
-        }
-        e_out[e] = w;
+    // padding after the last terminator (the walk loads, never uses, one word
+    // past a terminator): null words
+    for (int64_t e = cnt + ngroups + threadIdx.x; e < estride; e += blockDim.x) e_out[e] = 0u;
+    for (int e = threadIdx.x; e < cnt; e += blockDim.x) {
+        const uint32_t key = keys[e];
+        const uint32_t b = key >> 12;
+        const int local = key & 4095;
+        e_out[e + b / (uint32_t)db] = (sgn[q0 + local] < 0 ? 0x80000000u : 0u) | ((b % (uint32_t)db) << 24) |
+                                      entry_addr((uint32_t)(local / alpha), tm_t);
     }
-    uint16_t *b_out = bptr + c * bstride;
-    for (int64_t j = threadIdx.x; j < bstride; j += blockDim.x) {
+    uint32_t *g_out = gptr + c * gstride;
+    for (int64_t g = threadIdx.x; g < gstride; g += blockDim.x) {
+        // lb(g) = number of keys with bucket < g * db
         int lb = cnt;
-        if (j < d) {  // number of keys with bucket < j
-            const uint32_t target = (uint32_t)j << 12;
+        if (g < ngroups) {
+            const uint32_t target = (uint32_t)(g * db) << 12;
             int lo = 0, hi = cnt;
             while (lo < hi) {
                 const int mid = (lo + hi) >> 1;
@@ -246,7 +270,10 @@ __global__ void sjlt_plan_kernel(const int32_t *__restrict__ pos, const int8_t *
             }
             lb = lo;
         }
-        b_out[j] = (uint16_t)lb;
+        const int64_t gg = g < ngroups ? g : ngroups;
+        g_out[g] = (uint32_t)(lb + gg);
+        // group g-1 ends where group g starts: its terminator
+        if (g >= 1 && g <= ngroups) e_out[lb + g - 1] = (uint32_t)db << 24;
     }
 }
 
@@ -279,14 +306,14 @@ struct ApplyArgs {
     int64_t m_out;  // output rows (rows of A for trans 0, cols of A for trans 1)
     int64_t n;      // input index extent (= op.n)
     int d, alpha, tk, log2tk;
-    int64_t nchunks, bstride, estride;
-    const uint16_t *bptr;
+    int64_t nchunks, gstride, estride;
+    const uint32_t *gptr;  // group starts (plan)
     const uint32_t *ent;
     double scale;
     double *S;
     int64_t lds, col0;
     int nslabs, stages;
-    int stage_bytes, zero_off, bp_off, en_off;
+    int stage_bytes, zero_off, gs_off, en_off;
     // persistent balanced schedule: `groups` groups of nslabs CTAs split the
     // flattened (row tile, chunk) space of `units` chunks evenly; a row tile
     // cut between groups is summed by the group holding its first chunk
@@ -349,7 +376,9 @@ __global__ void __launch_bounds__((NW + (PROD ? (TRANS && RPT == 4 ? kXposeProdu
     const int nloc = (int)(u1 - u0);
     const int mode = p.mode;
     const int stages = p.stages;
-    const uint32_t bp_bytes = (SLAB + 8) * 2;
+    // this CTA's NW + 1 group starts (16-byte multiple for the bulk copy)
+    const uint32_t gs_bytes = (uint32_t)((NW + 4) / 4 * 16);
+    const int g0 = slab * NW;  // first warp group of the slab
     const uint32_t en_bytes = (uint32_t)p.estride * 4;
     const uint32_t tile_bytes = (uint32_t)p.tk * TM * 8;
 
@@ -418,7 +447,7 @@ __global__ void __launch_bounds__((NW + (PROD ? (TRANS && RPT == 4 ? kXposeProdu
         uint64_t *bar = &full[j % stages];
         int64_t r0, c;
         chunk_of(j, r0, c);
-        mbar_arrive_expect_tx(bar, tile_bytes + bp_bytes + en_bytes);
+        mbar_arrive_expect_tx(bar, tile_bytes + gs_bytes + en_bytes);
         if (MC_ON) {  // this CTA's share of the tile, for every CTA of the cluster
             const uint32_t rank = cluster_ctarank();
             const uint16_t mask = (uint16_t)((1u << p.mc) - 1u);
@@ -446,7 +475,7 @@ __global__ void __launch_bounds__((NW + (PROD ? (TRANS && RPT == 4 ? kXposeProdu
             const int part = p.tk / p.mc;
             tma_prefetch_2d(&tmap, (int)rp, (int)(cp * p.tk + (MC_ON ? cluster_ctarank() * part : 0)));
         }
-        bulk_g2s(st + p.bp_off, p.bptr + c * p.bstride + j0, bp_bytes, bar);
+        bulk_g2s(st + p.gs_off, p.gptr + c * p.gstride + g0, gs_bytes, bar);
         bulk_g2s(st + p.en_off, p.ent + c * p.estride, en_bytes, bar);
     };
     auto issue_coop = [&](int j, int ptid, int pnt) {  // threads [0, pnt) of the producer set
@@ -457,8 +486,8 @@ __global__ void __launch_bounds__((NW + (PROD ? (TRANS && RPT == 4 ? kXposeProdu
         const int64_t k0 = c * p.tk;
         const int kc = (int)(p.n - k0 < p.tk ? p.n - k0 : p.tk);
         if (ptid == 0) {
-            mbar_arrive_expect_tx(bar, bp_bytes + en_bytes);
-            bulk_g2s(st + p.bp_off, p.bptr + c * p.bstride + j0, bp_bytes, bar);
+            mbar_arrive_expect_tx(bar, gs_bytes + en_bytes);
+            bulk_g2s(st + p.gs_off, p.gptr + c * p.gstride + g0, gs_bytes, bar);
             bulk_g2s(st + p.en_off, p.ent + c * p.estride, en_bytes, bar);
         }
         double *sx = reinterpret_cast<double *>(st);
@@ -546,8 +575,8 @@ __global__ void __launch_bounds__((NW + (PROD ? (TRANS && RPT == 4 ? kXposeProdu
                     if (ptid == 0) {
                         int64_t r0, c;
                         chunk_of(j, r0, c);
-                        mbar_arrive_expect_tx(&full[s], bp_bytes + en_bytes);
-                        bulk_g2s(st + p.bp_off, p.bptr + c * p.bstride + j0, bp_bytes, &full[s]);
+                        mbar_arrive_expect_tx(&full[s], gs_bytes + en_bytes);
+                        bulk_g2s(st + p.gs_off, p.gptr + c * p.gstride + g0, gs_bytes, &full[s]);
                         bulk_g2s(st + p.en_off, p.ent + c * p.estride, en_bytes, &full[s]);
                     }
                     mbar_wait(stg_full, (uint32_t)(j & 1));
@@ -660,30 +689,21 @@ __global__ void __launch_bounds__((NW + (PROD ? (TRANS && RPT == 4 ? kXposeProdu
         const uint32_t st = smem_base + (uint32_t)s * p.stage_bytes;
         const uint32_t sx = st + lane_off;
         const uint32_t sen = st + p.en_off;
-        const uint16_t *sbp = reinterpret_cast<const uint16_t *>(
-                                  stage0 + (size_t)s * p.stage_bytes + p.bp_off) + warp * DB;
-        // the warp's DB+1 bucket bounds (packed u16 pairs), streamed by the walker
-        const uint32_t sbw = st + (uint32_t)p.bp_off + (uint32_t)(warp * DB * 2);
+        // shared address of the warp's group start (index of its first word)
+        const uint32_t sbw = st + (uint32_t)p.gs_off + (uint32_t)(warp * 4);
 #if HSK_SJLT_DEBUG
-        constexpr int NBW = DB / 2 + 1;
-        uint32_t bw[NBW];
-        {
-            const uint32_t *src = reinterpret_cast<const uint32_t *>(sbp);
-#pragma unroll
-            for (int q = 0; q < NBW; ++q) bw[q] = src[q];
-        }
-#endif
-#if HSK_SJLT_DEBUG
-        if (DBG_IS(3)) {  // checked mode: bucket bounds of this warp
-            uint32_t prev = 0;
-            for (int jj = 0; jj <= DB; ++jj) {
-                const uint32_t b = (jj & 1) ? (bw[jj >> 1] >> 16) : (bw[jj >> 1] & 0xffffu);
-                if (b < prev || b > (uint32_t)p.estride) {
-                    printf("sjlt dbg: cta %d warp %d chunk-iter %d bucket %d bound %u prev %u estride %d\n",
-                           (int)blockIdx.x, warp, i, jj, b, prev, (int)p.estride);
-                    __trap();
-                }
-                prev = b;
+        if (DBG_IS(3)) {  // checked mode: the warp's list lies in the chunk and ends in its terminator
+            const uint32_t *gs = reinterpret_cast<const uint32_t *>(stage0 + (size_t)s * p.stage_bytes + p.gs_off);
+            const uint32_t *en = reinterpret_cast<const uint32_t *>(stage0 + (size_t)s * p.stage_bytes + p.en_off);
+            const uint32_t b0 = gs[warp], b1 = gs[warp + 1];
+            bool bad = b0 >= b1 || b1 > (uint32_t)p.estride || ((en[b1 - 1] >> 24) & 127u) != (uint32_t)DB;
+            for (uint32_t q = b0; !bad && q + 1 < b1; ++q)
+                bad = ((en[q] >> 24) & 127u) >= (uint32_t)DB ||
+                      (q > b0 && ((en[q] >> 24) & 127u) < ((en[q - 1] >> 24) & 127u));
+            if (bad) {
+                printf("sjlt dbg: cta %d warp %d chunk-iter %d bad list [%u, %u) estride %d\n",
+                       (int)blockIdx.x, warp, i, b0, b1, (int)p.estride);
+                __trap();
             }
         }
 #endif
@@ -808,7 +828,7 @@ template <int RPT, int DB, int NW>
 static int launch(ApplyArgs a, const Geom &g, cudaStream_t st) {
     constexpr int TM = 32 * RPT;
     constexpr int SLAB = NW * DB;
-    HSK_REQUIRE(g.tm == TM, HSK_EINVAL, "sjlt: plan/config mismatch");
+    HSK_REQUIRE(g.tm == TM && g.db == DB && g.nw == NW, HSK_EINVAL, "sjlt: plan/config mismatch");
     const bool aligned = a.use_tma != 0;  // 16-byte aligned columns (lda even)
     // 0: TMA S tile; 1: cp.async S' tile (unaligned A); 2: cp.async S tile;
     // 3: TMA S' tile (16 x TM boxes, 128-byte swizzle)
@@ -821,8 +841,8 @@ static int launch(ApplyArgs a, const Geom &g, cudaStream_t st) {
     // start on 1024-byte boundaries
     const int a_bytes = (int)roundup((a.trans ? roundup(a.tk, 16) : a.tk) * (int64_t)TM * 8, 1024);
     a.zero_off = 0;
-    a.bp_off = a_bytes;
-    a.en_off = (int)roundup(a.bp_off + (SLAB + 8) * 2, 128);
+    a.gs_off = a_bytes;
+    a.en_off = (int)roundup(a.gs_off + (NW + 4) / 4 * 16, 128);
     a.stage_bytes = (int)roundup(a.en_off + (a.estride + 8) * 4, 1024);
     a.nslabs = (a.d + SLAB - 1) / SLAB;
     const int64_t tiles = (a.m_out + TM - 1) / TM;
@@ -1017,9 +1037,9 @@ extern "C" int hsk_sjlt_plan_build(const int32_t *pos, const int8_t *sgn, int64_
             int p2 = 1;
             while (p2 < g->tk * alpha) p2 <<= 1;
             sjlt::sjlt_plan_kernel<<<(unsigned)g->nchunks, 256, p2 * sizeof(uint32_t), st>>>(
-                pos, sgn, n, d, alpha, g->tk, p2, g->bstride, g->estride,
+                pos, sgn, n, d, alpha, g->tk, p2, g->db, g->ngroups, g->gstride, g->estride,
                 g == &pl.t ? (g->rpt == 4 ? -g->tm : g->tm) : 0,
-                reinterpret_cast<uint16_t *>(base + g->bptr_off),
+                reinterpret_cast<uint32_t *>(base + g->gptr_off),
                 reinterpret_cast<uint32_t *>(base + g->ent_off), reinterpret_cast<int *>(base + 28));
             HSK_CHECK_LAUNCH("sjlt_plan_kernel");
         }
@@ -1063,33 +1083,26 @@ extern "C" int hsk_sjlt_apply(const double *A, int64_t rows, int64_t cols, int64
     a.alpha = alpha;
     a.tk = g.tk;
     a.nchunks = g.nchunks;
-    a.bstride = g.bstride;
+    a.gstride = g.gstride;
     a.estride = g.estride;
-    a.bptr = reinterpret_cast<const uint16_t *>(base + g.bptr_off);
+    a.gptr = reinterpret_cast<const uint32_t *>(base + g.gptr_off);
     a.ent = reinterpret_cast<const uint32_t *>(base + g.ent_off);
     a.scale = scale;
     a.S = S;
     a.lds = lds;
     a.col0 = col0;
     cudaStream_t st = as_stream(stream);
-    // 16 consumer warps (128-register budget: RPT x DB accumulators plus the
-    // walker's pipeline registers) and dedicated producer warp(s); the
-    // 32-warp variants (64 registers, half the buckets per warp) are kept
-    // for tuning (HSK_SJLT_W32=1).
-    bool w32 = false;
-    if (const char *env = getenv("HSK_SJLT_W32")) w32 = env[0] == '1';
-    if (g.rpt == 1) {  // 32-row tiles, 512-bucket slabs
-        if (w32) return sjlt::launch<1, 16, 32>(a, g, st);
-        return sjlt::launch<1, 32, 16>(a, g, st);
+    // the plan was built for this warp shape (warp_shape): one kernel each
+    const int shape = g.rpt * 1000 + g.db * 10 + (g.nw == 32);
+    switch (shape) {
+        case 1320: return sjlt::launch<1, 32, 16>(a, g, st);   // 32-row tiles, 512-bucket slabs
+        case 1161: return sjlt::launch<1, 16, 32>(a, g, st);
+        case 4040: return sjlt::launch<4, 4, 16>(a, g, st);    // 128-row tiles, 64-bucket slabs
+        case 4021: return sjlt::launch<4, 2, 32>(a, g, st);
+        case 2080: return sjlt::launch<2, 8, 16>(a, g, st);    // 64-row tiles
+        case 2041: return sjlt::launch<2, 4, 32>(a, g, st);
+        case 2081: return sjlt::launch<2, 8, 32>(a, g, st);
+        case 2160: return sjlt::launch<2, 16, 16>(a, g, st);
+        default: return set_error(HSK_EINVAL, "sjlt apply: no kernel for rpt=%d db=%d nw=%d", g.rpt, g.db, g.nw);
     }
-    if (g.rpt == 4) {  // 128-row tiles, 64-bucket slabs
-        if (w32) return sjlt::launch<4, 2, 32>(a, g, st);
-        return sjlt::launch<4, 4, 16>(a, g, st);
-    }
-    if (w32) {          // 64-row tiles
-        if (d <= 128) return sjlt::launch<2, 4, 32>(a, g, st);
-        return sjlt::launch<2, 8, 32>(a, g, st);
-    }
-    if (d <= 128) return sjlt::launch<2, 8, 16>(a, g, st);
-    return sjlt::launch<2, 16, 16>(a, g, st);
 }
