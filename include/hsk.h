@@ -67,8 +67,10 @@ HSK_API int hsk_device_info(int *sm_count, int *cc_major, int *cc_minor, int64_t
  * builds index-only CSR/CSC views of B+ and B- (PAPER.md:864-901); the GPU
  * plan is the same pattern re-blocked for the kernel: per k-chunk of the
  * input index, the entries sorted by bucket (stable in (k, t)), each entry a
- * 32-bit word (tile offset of k within the chunk | sign in bit 31; one
- * sub-plan per direction), plus per-chunk u16 bucket offsets.
+ * 32-bit word (sign in bit 31 | bucket within its warp group << 24 | tile
+ * offset of k), every group of buckets one consumer warp owns closed by a
+ * terminator word, plus per-chunk u32 group starts (one sub-plan per
+ * direction).
  *   pos: n x alpha int32 (reference `_pos`), values in [0, d)
  *   sgn: n x alpha int8  (reference `_signs`), values +-1
  * hsk_sjlt_plan_bytes gives the size of the device buffer `plan`. */
