@@ -150,8 +150,8 @@ __global__ void __launch_bounds__(NW * 32, 1)
     // S' (vectors = columns of A, contiguous): TMA lands each 32-vector x
     // 256 segment in A's natural layout -- 16 boxes of 16 inputs x 32
     // vectors, 128-byte swizzle -- in a staging buffer, and pass A reads it
-    // from there (lane = vector; 4-way bank conflicts, the price of not
-    // transposing) and writes X[k][vector]; the next segment's TMA is issued
+    // from there (lane pairs share a 16-byte chunk: conflict-free) and
+    // writes X[k][vector]; the next segment's TMA is issued
     // once pass A's barrier shows the staging buffer consumed.  Two X slots:
     // pass A of segment g+1 may run while slow warps still fold segment g
     // (slot g+1 was last read before the pass-A barrier of segment g), so
@@ -270,35 +270,49 @@ __global__ void __launch_bounds__(NW * 32, 1)
             // pass A: k = w + 16 q, butterflies over k bits 4..7 (signs applied
             // by flipping sign bits: exact, as the reference's multiply by +-1)
             double x[16];
-            const uint32_t msk = sgm_all[(tmat ? (int)(g & 1) : q) * 16 + warp];
             if (tmat) {
-                // input w + 16u of vector `lane`: box u, 128-byte row `lane`,
-                // 16-byte chunk (w/2) ^ (lane%8)
-                const double *sb = stg + lane * 16 + ((((warp * 8) ^ ((lane & 7) << 4))) >> 3);
+                // lane -> (vector v = 16 (w/8) + l/2, input kl = 2 (w%8) + l%2): the
+                // two lanes of a vector read the two 8-byte halves of one 16-byte
+                // chunk, so each half-warp's 16 loads (64-bit loads are serviced
+                // per half-warp) hit 16 distinct bank pairs -- one wavefront each
+                // (one input of 16 vectors would share 8 bank pairs: ncu showed 4
+                // wavefronts per load).  Input kl + 16u of vector v: box u,
+                // 128-byte row v, 16-byte chunk (kl/2) ^ (v%8).  X columns of odd
+                // inputs are XOR 8 permuted (vector v of input k at column
+                // v ^ 8(k%2)), so the two lanes of a vector store to different
+                // bank pairs as well; pass B undoes it when it reads.
+                const int v = 16 * (warp >> 3) + (lane >> 1), kl = 2 * (warp & 7) + (lane & 1);
+                const uint32_t msk = sgm_all[(int)(g & 1) * 16 + kl];
+                const double *sb = stg + v * 16 + (((kl * 8) ^ ((v & 7) << 4)) >> 3);
 #pragma unroll
                 for (int u = 0; u < 16; ++u)
                     x[u] = __longlong_as_double(__double_as_longlong(sb[u * 16 * TM]) ^
                                                 ((long long)((msk >> u) & 1u) << 63));
+                wht16(x);
+#pragma unroll
+                for (int u = 0; u < 16; ++u) X[(kl + 16 * u) * pitch + (v ^ ((kl & 1) << 3))] = x[u];
             } else {
+            const uint32_t msk = sgm_all[q * 16 + warp];
 #pragma unroll
                 for (int u = 0; u < 16; ++u) {
                     const int k = warp + 16 * u;
                     x[u] = __longlong_as_double(__double_as_longlong(X[k * pitch + lane]) ^
                                                 ((long long)((msk >> u) & 1u) << 63));
                 }
-            }
             wht16(x);
 #pragma unroll
             for (int u = 0; u < 16; ++u) X[(warp + 16 * u) * pitch + lane] = x[u];
+            }
             __syncthreads();
             // TMA path: every thread is past the fold of segment g-1 here, so
             // its slot is refilled now and the fold needs no trailing barrier
             if (tma && g + stages - 1 < G) issue(g + stages - 1, qi);
             // S': every warp is past pass A, the staging buffer is free
             if (tmat && tid == 0 && g + 1 < G) issue_t(g + 1);
-            // pass B: k = 16 w + q, butterflies over k bits 0..3
+            // pass B: k = 16 w + q, butterflies over k bits 0..3 (S': odd inputs
+            // of vector `lane` at column lane ^ 8, see pass A)
 #pragma unroll
-            for (int u = 0; u < 16; ++u) x[u] = X[(16 * warp + u) * pitch + lane];
+            for (int u = 0; u < 16; ++u) x[u] = X[(16 * warp + u) * pitch + (tmat ? lane ^ ((u & 1) << 3) : lane)];
             wht16(x);
 #pragma unroll
             for (int u = 0; u < 16; ++u) X[(16 * warp + u) * pitch + lane] = x[u];
