@@ -1,0 +1,165 @@
+#!/usr/bin/env python
+"""Sketch phase of the paper's Table 7.1 on one B200.
+
+The paper times STRUMPACK's HSS sketch phase (every adaptive increment, both
+A R^T and A^T R^T) on an 8-thread Ryzen 9 3950X.  This tool
+replays the same sketch phase through this repo's device API for the two test
+matrices that can be generated here:
+
+  covariance  G_ij = exp(-|x_i - x_j| / 0.2), x on the k^3 grid of [0,1]^3
+              (hsskit matgen.covariance_matrix; natural grid
+              order -- the paper's recursive-bisection ordering permutes rows
+              and columns, which does not change the cost of a dense product)
+  QChem       T_ij = pi^2/(6 h^2) (i == j), (-1)^(i-j) / (h^2 (i-j)^2) else,
+              h = 0.1 (hsskit matgen.qchem_toeplitz)
+
+Sketch schedule (the paper's settings): d0 = 128, dd = 64; the
+first operator has d0 + dd = 192 columns, and each adaptation round appends a
+64-column block, so a run with final d (Table B.1) sketches
+final_d + 64 columns in 1 + (final_d - 128)/64 blocks.  Operators are drawn
+exactly as the reference draws them (SJLT: block construction).
+The impedance and Poisson-front matrices are not generated (no data / solver
+here).
+
+Reported per run: device_ms (CUDA events around the whole phase: operator
+uploads / SJLT plans + every product), wall_ms (host clock around the same,
+synchronised), draw_ms (host RNG draws of R, the reference's numpy streams),
+and the paper's CPU time.
+
+    python tools/paper_table.py [--out profiles/paper_table71_r01.json]
+"""
+import argparse
+import json
+import os
+import sys
+import time
+
+import numpy as np
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+from paper_2302_01977_b200 import adaptive, device  # noqa: E402
+from paper_2302_01977_b200 import sketching as sk  # noqa: E402
+
+KINDS = ["G", "S1", "S2", "S4", "S8"]
+
+# Table 7.1 sketching time (ms), PAPER.md lines as cited in BASELINE.md §A
+PAPER_MS = {
+    ("cov", 1e-2, 10): (3, 1, 1, 2, 4), ("cov", 1e-2, 20): (393, 146, 166, 224, 366),
+    ("cov", 1e-2, 30): (6632, 2194, 2470, 3506, 5456),
+    ("cov", 1e-4, 10): (3, 1, 1, 3, 6), ("cov", 1e-4, 20): (1282, 581, 669, 843, 1459),
+    ("cov", 1e-4, 30): (36416, 13466, 15943, 21668, 33530),
+    ("cov", 1e-6, 10): (7, 1, 2, 5, 9), ("cov", 1e-6, 20): (1844, 777, 911, 1259, 2189),
+    ("cov", 1e-6, 30): (48224, 18032, 21280, 28923, 46099),
+    ("qchem", 1e-2, 10000): (288, 72, 85, 112, 187), ("qchem", 1e-2, 20000): (1171, 295, 316, 402, 682),
+    ("qchem", 1e-2, 40000): (4552, 1366, 1645, 2273, 3441),
+    ("qchem", 1e-4, 10000): (287, 74, 84, 113, 183), ("qchem", 1e-4, 20000): (1160, 294, 313, 404, 679),
+    ("qchem", 1e-4, 40000): (4576, 1370, 1672, 2264, 3409),
+    ("qchem", 1e-6, 10000): (289, 72, 84, 112, 189), ("qchem", 1e-6, 20000): (1165, 295, 317, 407, 677),
+    ("qchem", 1e-6, 40000): (4569, 1368, 1658, 2243, 3456),
+}
+# Table B.1 final d (without dd); QChem is 128 everywhere
+FINAL_D = {
+    (1e-2, 10): (128, 128, 128, 128, 128), (1e-2, 20): (256, 256, 256, 256, 256),
+    (1e-2, 30): (384, 384, 320, 384, 384),
+    (1e-4, 10): (192, 128, 192, 192, 192), (1e-4, 20): (832, 896, 832, 896, 832),
+    (1e-4, 30): (1984, 2176, 2112, 2112, 2112),
+    (1e-6, 10): (320, 192, 256, 320, 320), (1e-6, 20): (1088, 1216, 1216, 1216, 1280),
+    (1e-6, 30): (2816, 2880, 2880, 2880, 2880),
+}
+
+
+def covariance(k: int, lam: float = 0.2) -> device.DeviceMatrix:
+    ax = torch.linspace(0.0, 1.0, k, dtype=torch.float64, device="cuda")
+    gx, gy, gz = torch.meshgrid(ax, ax, ax, indexing="ij")
+    pts = torch.stack([gx.reshape(-1), gy.reshape(-1), gz.reshape(-1)], 1)
+    n = pts.shape[0]
+    A = device.DeviceMatrix.empty(n, n)
+    for c0 in range(0, n, 4096):  # column blocks (A is symmetric)
+        c1 = min(n, c0 + 4096)
+        A.t[c0:c1, :n] = torch.exp(-torch.cdist(pts[c0:c1], pts) / lam)
+    return A
+
+
+def qchem(n: int, h: float = 0.1) -> device.DeviceMatrix:
+    kk = torch.arange(n, dtype=torch.float64, device="cuda")
+    t = torch.where(kk.remainder(2) == 1, -1.0, 1.0) / (h * h * kk.clamp(min=1.0) ** 2)
+    t[0] = np.pi ** 2 / (6.0 * h * h)
+    A = device.DeviceMatrix.empty(n, n)
+    idx = torch.arange(n, device="cuda")
+    for c0 in range(0, n, 2048):
+        c1 = min(n, c0 + 2048)
+        A.t[c0:c1, :n] = t[(idx[c0:c1, None] - idx[None, :]).abs()]
+    return A
+
+
+def sketch_phase(A, kind: str, final_d: int, seed: int = 0):
+    n = A.rows
+    alpha = None if kind == "G" else int(kind[1:])
+    skind = sk.GAUSSIAN if kind == "G" else sk.SJLT
+    kw = {} if kind == "G" else dict(alpha=alpha, construction=sk.BLOCK)
+    rounds = (final_d - 128) // 64
+    t0 = time.perf_counter()
+    ops = [sk.new_operator(skind, n, 192, np.random.SeedSequence((seed, 0)), **kw)]
+    for r in range(1, rounds + 1):
+        ops.append(sk.append_columns(ops[-1], 64, np.random.SeedSequence((seed, r))))
+    draw_ms = (time.perf_counter() - t0) * 1e3
+    ds = adaptive.DeviceSketch(A, final_d + 64)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    w0 = time.perf_counter()
+    e0.record()
+    ds.start(ops[0])
+    for op in ops[1:]:
+        ds.extend(op)
+    e1.record()
+    torch.cuda.synchronize()
+    wall_ms = (time.perf_counter() - w0) * 1e3
+    assert ds.d == final_d + 64
+    return {"device_ms": e0.elapsed_time(e1), "wall_ms": wall_ms, "draw_ms": draw_ms,
+            "blocks": 1 + rounds, "cols": final_d + 64}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--out", default=None)
+    ap.add_argument("--quick", action="store_true", help="smallest size of each matrix only")
+    args = ap.parse_args()
+    torch.cuda.set_device(0)
+    rows = []
+    cov_ks = [10] if args.quick else [10, 20, 30]
+    qn = [10000] if args.quick else [10000, 20000, 40000]
+    for k in cov_ks:
+        A = covariance(k)
+        for eps in (1e-2, 1e-4, 1e-6):
+            for i, kind in enumerate(KINDS):
+                sketch_phase(A, kind, FINAL_D[(eps, k)][i])  # warm-up (module load, plan cache)
+                r = sketch_phase(A, kind, FINAL_D[(eps, k)][i])
+                r.update(matrix="covariance", n=k ** 3, eps=eps, kind=kind,
+                         final_d=FINAL_D[(eps, k)][i], paper_cpu_ms=PAPER_MS[("cov", eps, k)][i])
+                rows.append(r)
+                print(json.dumps(r), flush=True)
+        del A
+        torch.cuda.empty_cache()
+    for n in qn:
+        A = qchem(n)
+        for i, kind in enumerate(KINDS):
+            sketch_phase(A, kind, 128)
+            r = sketch_phase(A, kind, 128)
+            # every eps row has final d 128: one run, compared with each row
+            r.update(matrix="qchem_toeplitz", n=n, eps="all", kind=kind, final_d=128,
+                     paper_cpu_ms=[PAPER_MS[("qchem", e, n)][i] for e in (1e-2, 1e-4, 1e-6)])
+            rows.append(r)
+            print(json.dumps(r), flush=True)
+        del A
+        torch.cuda.empty_cache()
+    out = {"tool": "tools/paper_table.py", "gpu": torch.cuda.get_device_name(0),
+           "paper": "Table 7.1 sketching time, STRUMPACK on Ryzen 9 3950X, 8 threads (PAPER.md:973-1056)",
+           "rows": rows}
+    if args.out:
+        with open(args.out, "w") as f:
+            json.dump(out, f, indent=1)
+
+
+if __name__ == "__main__":
+    main()
