@@ -394,7 +394,12 @@ def main():
         host.copy_(A.t[:, :N])
         A_host = host.numpy().T           # F-ordered view of the pinned buffer
         e2e_steps = max(3, min(args.steps, 10))
-        sk.apply_right(A_host, op)
+        # warm-up as steady state looks: each call returns a fresh caller-owned
+        # pinned array while the caller still holds the previous one, so the
+        # second call is the one that grows the pinned pool (a one-time
+        # cudaHostAlloc, ~27 ms measured)
+        for _ in range(max(3, args.warmup)):
+            S_host = sk.apply_right(A_host, op)
         torch.cuda.synchronize()
         e0.record(stream)
         for _ in range(e2e_steps):
