@@ -4,7 +4,7 @@
 set -x
 mkdir -p gpurun_out
 timeout 900 python -m pytest tests -m gpu -q -x > gpurun_out/pt_all.log 2>&1; tail -3 gpurun_out/pt_all.log
-timeout 300 python tools/kbench.py 2>&1 | grep -v env > gpurun_out/kb.log; cat gpurun_out/kb.log
+timeout 400 python tools/kbench.py --cases c1,c2s,c2g,c3,c4,c5s 2>&1 | grep -v env > gpurun_out/kb.log; cat gpurun_out/kb.log
 timeout 600 python bench.py > gpurun_out/bench.log 2>&1; echo rc=$?; tail -1 gpurun_out/bench.log
 timeout 600 python bench.py --steps 2 --warmup 3 > /dev/null 2>&1 && \
   timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/launches.csv python bench.py --steps 2 --warmup 3 > gpurun_out/ncu_l.log 2>&1; echo ncu1=$?
