@@ -78,6 +78,25 @@ HSK_API int64_t hsk_sjlt_plan_bytes(int64_t n, int32_t d, int32_t alpha);
 HSK_API int hsk_sjlt_plan_build(const int32_t *pos, const int8_t *sgn, int64_t n, int32_t d,
                         int32_t alpha, void *plan, int64_t plan_bytes, void *stream);
 
+/* Chunked patterns (flags = HSK_SJLT_CHUNKED): the block construction
+ * (SjltBlock.__init__, sketching.py:246-250) places entry t of every input
+ * index in chunk t of d/alpha buckets, pos(k,t) in [t*d/alpha, (t+1)*d/alpha).
+ * With d/alpha = 8 and d a multiple of 64 (C3: alpha = 8 increments of 64) the
+ * plan pairs the chunks: one consumer warp owns two chunks and reads each
+ * element once for both (alpha/2 tile reads per element instead of alpha).
+ * Other shapes ignore the flag.  The caller guarantees the chunk property
+ * (the plan kernel flags violations, the host checks before passing it);
+ * plan_bytes / plan_build / apply must all get the same flags. */
+#define HSK_SJLT_CHUNKED 1
+HSK_API int64_t hsk_sjlt_plan_bytes_ex(int64_t n, int32_t d, int32_t alpha, int32_t flags);
+HSK_API int hsk_sjlt_plan_build_ex(const int32_t *pos, const int8_t *sgn, int64_t n, int32_t d,
+                           int32_t alpha, int32_t flags, void *plan, int64_t plan_bytes,
+                           void *stream);
+HSK_API int hsk_sjlt_apply_ex(const double *A, int64_t rows, int64_t cols, int64_t lda,
+                      int32_t trans, const void *plan, int64_t n, int32_t d, int32_t alpha,
+                      int32_t flags, double scale, double *S, int64_t lds, int64_t col0,
+                      void *stream);
+
 /* Replaces SjltBlock.apply_right (trans 0, sketching.py:322-332) and
  * SjltBlock.apply_right_transposed (trans 1, sketching.py:334-351):
  * S[:, col0 + j] = scale * sum_k sgn(k,t) A[:, k]  over (k,t) with pos = j. */

@@ -32,6 +32,11 @@ SIGNATURES = {
     "hsk_sjlt_plan_build": (ctypes.c_int, [_c_p, _c_p, _c_i64, _c_i32, _c_i32, _c_p, _c_i64, _c_p]),
     "hsk_sjlt_apply": (ctypes.c_int, [_c_p, _c_i64, _c_i64, _c_i64, _c_i32, _c_p, _c_i64, _c_i32,
                                       _c_i32, _c_d, _c_p, _c_i64, _c_i64, _c_p]),
+    "hsk_sjlt_plan_bytes_ex": (_c_i64, [_c_i64, _c_i32, _c_i32, _c_i32]),
+    "hsk_sjlt_plan_build_ex": (ctypes.c_int, [_c_p, _c_p, _c_i64, _c_i32, _c_i32, _c_i32, _c_p, _c_i64,
+                                              _c_p]),
+    "hsk_sjlt_apply_ex": (ctypes.c_int, [_c_p, _c_i64, _c_i64, _c_i64, _c_i32, _c_p, _c_i64, _c_i32,
+                                         _c_i32, _c_i32, _c_d, _c_p, _c_i64, _c_i64, _c_p]),
     "hsk_gauss_apply": (ctypes.c_int, [_c_p, _c_i64, _c_i64, _c_i64, _c_i32, _c_p, _c_i64, _c_i32,
                                        _c_p, _c_i64, _c_i64, _c_p]),
     "hsk_srht_apply": (ctypes.c_int, [_c_p, _c_i64, _c_i64, _c_i64, _c_i32, _c_p, _c_i64, _c_i64,

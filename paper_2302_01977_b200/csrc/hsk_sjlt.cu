@@ -80,6 +80,7 @@ constexpr int64_t kMaxD = (1 << 19);    // bucket index fits 19 bits of the sort
 // (256-bucket slabs, TK 128) otherwise, except S with d > 512, which prefers
 // 32-row tiles with 512-bucket slabs and TK = 256 (half the slab re-reads).
 struct Geom {
+    int pair;          // paired plan (block construction, d/alpha = 8): below
     int rpt;           // rows per lane (tile rows tm = 32 * rpt)
     int db, nw;        // buckets per consumer warp, consumer warps per CTA
     int64_t ngroups;   // warp groups of db buckets (nslabs * nw)
@@ -133,9 +134,43 @@ static inline void warp_shape(int rpt, int d, int &db, int &nw) {
     else db = (d <= 128 ? 4 : 8) * (w32 ? 1 : 2);  // 64-row tiles
 }
 
-static Geom geom_dir(int64_t n, int d, int alpha, int trans, int64_t base) {
+// Paired sub-plans (block construction with chunk d/alpha = 8, d a multiple
+// of 64: C3's alpha = 8 increments of 64).  Every input index has exactly one
+// bucket in each construction chunk, so a warp owning the 16 buckets of two
+// chunks (t1 = 2p, t2 = 2p + 1) sees every input index of its k-range exactly
+// once: one tile load feeds both buckets.  64-row tiles, 16 consumer warps =
+// 4 k-groups (quarters of the chunk's TK indices) x 4 chunk pairs; a slab is
+// 64 buckets; the k-groups' partial sums are added in k-group order at the end
+// of a row tile (deterministic).  Per (row, element): alpha/2 tile reads
+// instead of alpha.
+constexpr int kPairKg = 4;     // k-groups per CTA
+constexpr int kPairSlab = 64;  // buckets per slab (4 chunk pairs)
+
+static Geom geom_dir(int64_t n, int d, int alpha, int trans, int64_t base, int pair = 0) {
     Geom g;
     int tk;
+    g.pair = pair;
+    if (pair) {
+        constexpr int kStage3 = (226 * 1024 - 2048) / 3, kStage2 = (226 * 1024 - 2048) / 2;
+        const int ae = alpha / 2;  // entries per input index
+        g.rpt = 2;
+        g.db = 16;
+        g.nw = 16;
+        g.ngroups = (int64_t)(d / kPairSlab) * g.nw;
+        tk = n >= 8192 ? tk_fit16(ae, 64, 256, kStage2, g.ngroups, g.nw)
+                       : tk_fit16(ae, 64, 128, kStage3, g.ngroups, g.nw);
+        if (const char *env = getenv(trans ? "HSK_SJLT_TK_T" : "HSK_SJLT_TK")) tk = atoi(env) / 16 * 16;
+        g.tm = 64;
+        g.pitch = g.tm;
+        g.tk = tk;
+        g.nchunks = (n + g.tk - 1) / g.tk;
+        g.gstride = roundup(g.ngroups + 4, 4);
+        g.estride = roundup((int64_t)g.tk * ae + g.ngroups, 4);
+        g.gptr_off = base;
+        g.ent_off = roundup(g.gptr_off + (g.nchunks + 1) * g.gstride * 4, 128);
+        g.end = g.ent_off + roundup((g.nchunks + 1) * g.estride * 4, 128);
+        return g;
+    }
     // per-stage budgets: 3 stages (or 2) of the 226 KB ring
     constexpr int kStage3 = (226 * 1024 - 2048) / 3, kStage2 = (226 * 1024 - 2048) / 2;
     // Long rows (n >= 8192): two stages of the largest TK -- more entries per
@@ -179,10 +214,15 @@ struct Plan {
     int64_t bytes;
 };
 
-static Plan plan_geom(int64_t n, int d, int alpha) {
+static inline bool pair_shape(int d, int alpha) {
+    return d % kPairSlab == 0 && alpha * 8 == d;
+}
+
+static Plan plan_geom(int64_t n, int d, int alpha, int pair = 0) {
     Plan pl;
-    pl.s = geom_dir(n, d, alpha, 0, kHeaderBytes);
-    pl.t = geom_dir(n, d, alpha, 1, pl.s.end);
+    pair = pair && pair_shape(d, alpha) && n > 0;
+    pl.s = geom_dir(n, d, alpha, 0, kHeaderBytes, pair);
+    pl.t = geom_dir(n, d, alpha, 1, pl.s.end, pair);
     pl.bytes = pl.t.end;
     return pl;
 }
@@ -210,17 +250,29 @@ __host__ __device__ inline uint32_t entry_addr(uint32_t kk, int tm_t) {
 // bucket-tagged entry words, group terminators and group starts.
 __global__ void sjlt_plan_kernel(const int32_t *__restrict__ pos, const int8_t *__restrict__ sgn,
                                  int64_t n, int d, int alpha, int tk, int p2, int db, int64_t ngroups,
-                                 int64_t gstride, int64_t estride, int tm_t, uint32_t *__restrict__ gptr,
-                                 uint32_t *__restrict__ ent, int *err) {
+                                 int64_t gstride, int64_t estride, int tm_t, int pair,
+                                 uint32_t *__restrict__ gptr, uint32_t *__restrict__ ent, int *err) {
     extern __shared__ uint32_t keys[];
     const int64_t c = blockIdx.x;
     const int64_t k0 = c * tk;
     const int kc = (int)(n - k0 < tk ? n - k0 : tk);
-    const int cnt = kc * alpha;
+    const int np = alpha / 2;  // paired plans: entries per input index
+    const int cnt = kc * (pair ? np : alpha);
     const int64_t q0 = k0 * alpha;
+    // paired key: group << 14 | combo << 8 | kk, group = slab * 16 + kgroup * 4
+    // + pair mod 4 (the consumer warp), combo = c1 * 8 + c2
+    const int kgw = tk / kPairKg;
+    const int gsh = pair ? 14 : 12;
     for (int i = threadIdx.x; i < p2; i += blockDim.x) {
         uint32_t key = 0xFFFFFFFFu;
-        if (i < cnt) {
+        if (pair && i < cnt) {
+            const int kk = i / np, pg = i - kk * np;
+            const int b1 = pos[q0 + (int64_t)kk * alpha + 2 * pg] - 16 * pg;
+            const int b2 = pos[q0 + (int64_t)kk * alpha + 2 * pg + 1] - 16 * pg - 8;
+            if (b1 < 0 || b1 >= 8 || b2 < 0 || b2 >= 8) atomicOr(err, 2);
+            const uint32_t grp = (uint32_t)((pg >> 2) * 16 + (kk / kgw) * 4 + (pg & 3));
+            key = (grp << 14) | ((uint32_t)((b1 & 7) * 8 + (b2 & 7)) << 8) | (uint32_t)kk;
+        } else if (i < cnt) {
             int p = pos[q0 + i];
             if (p < 0 || p >= d) {
                 atomicOr(err, 1);
@@ -252,6 +304,14 @@ __global__ void sjlt_plan_kernel(const int32_t *__restrict__ pos, const int8_t *
     for (int64_t e = cnt + ngroups + threadIdx.x; e < estride; e += blockDim.x) e_out[e] = 0u;
     for (int e = threadIdx.x; e < cnt; e += blockDim.x) {
         const uint32_t key = keys[e];
+        if (pair) {
+            const uint32_t grp = key >> 14, kk = key & 255u, combo = (key >> 8) & 63u;
+            const int pg = (int)((grp >> 4) * 4 + (grp & 3));
+            const int64_t q = q0 + (int64_t)kk * alpha + 2 * pg;
+            e_out[e + grp] = (sgn[q] < 0 ? 0x80000000u : 0u) | (combo << 24) |
+                             (sgn[q + 1] < 0 ? 0x00800000u : 0u) | entry_addr(kk, tm_t);
+            continue;
+        }
         const uint32_t b = key >> 12;
         const int local = key & 4095;
         e_out[e + b / (uint32_t)db] = (sgn[q0 + local] < 0 ? 0x80000000u : 0u) | ((b % (uint32_t)db) << 24) |
@@ -262,7 +322,7 @@ __global__ void sjlt_plan_kernel(const int32_t *__restrict__ pos, const int8_t *
         // lb(g) = number of keys with bucket < g * db
         int lb = cnt;
         if (g < ngroups) {
-            const uint32_t target = (uint32_t)(g * db) << 12;
+            const uint32_t target = pair ? (uint32_t)g << gsh : (uint32_t)(g * db) << 12;
             int lo = 0, hi = cnt;
             while (lo < hi) {
                 const int mid = (lo + hi) >> 1;
@@ -273,7 +333,7 @@ __global__ void sjlt_plan_kernel(const int32_t *__restrict__ pos, const int8_t *
         const int64_t gg = g < ngroups ? g : ngroups;
         g_out[g] = (uint32_t)(lb + gg);
         // group g-1 ends where group g starts: its terminator
-        if (g >= 1 && g <= ngroups) e_out[lb + g - 1] = (uint32_t)db << 24;
+        if (g >= 1 && g <= ngroups) e_out[lb + g - 1] = (uint32_t)(pair ? 64 : db) << 24;
     }
 }
 
@@ -332,12 +392,15 @@ struct ApplyArgs {
 // All NW warps own buckets (NW*DB per CTA slab) and share the producer work:
 // warp 0 / lane 0 issues TMA + bulk copies (mode 0); in modes 1/2 every lane
 // issues its share of 8-byte cp.async for the chunk STAGES-1 ahead.
-template <int RPT, int DB, int NW, bool TRANS, bool PROD, bool SK>
+template <int RPT, int DB, int NW, bool TRANS, bool PROD, bool SK, bool PAIR>
 __global__ void __launch_bounds__((NW + (PROD ? (TRANS && RPT == 4 ? kXposeProducers : 1) : 0)) * 32, 1)
     sjlt_apply_kernel(const ApplyArgs p, const __grid_constant__ CUtensorMap tmap) {
     constexpr int TM = 32 * RPT;
-    constexpr int SLAB = NW * DB;
+    constexpr int SLAB = PAIR ? kPairSlab : NW * DB;
     constexpr bool XPOSE = TRANS && RPT == 4;       // transposed S' tile layout
+    // paired plans: warps [0, 4) (k-group 0) hold a row tile's sums once the
+    // k-groups are folded; only they publish and store
+    const bool owner = !PAIR || (threadIdx.x >> 5) < 4;
     constexpr int PW = PROD ? (XPOSE ? kXposeProducers : 1) : 0;  // dedicated producer warps
     extern __shared__ __align__(128) unsigned char smem[];
     uint64_t *full = reinterpret_cast<uint64_t *>(smem);
@@ -519,11 +582,12 @@ __global__ void __launch_bounds__((NW + (PROD ? (TRANS && RPT == 4 ? kXposeProdu
             const int tk = p.tk;
             for (int kk = ptid; kk < tk; kk += pnt) {
                 const double *src = p.A + r0 * p.lda + k0 + kk;
-                unsigned char *dbase = st + (kk >> 4) * TM * 128 + ((kk & 15) << 3);
+                unsigned char *dbase = st + (kk >> 4) * TM * 128;
+                const int kx = (kk & 15) << 3;
                 const bool vk = kk < kc;
                 for (int rr = 0; rr < TM; ++rr, src += p.lda) {
                     const bool v = vk && (r0 + rr < p.m_out);
-                    cp_async8(dbase + ((rr * 128) ^ ((rr & 7) << 4)), v ? src : p.A, v);
+                    cp_async8(dbase + rr * 128 + (kx ^ ((rr & 7) << 4)), v ? src : p.A, v);
                 }
             }
         } else {
@@ -631,6 +695,7 @@ __global__ void __launch_bounds__((NW + (PROD ? (TRANS && RPT == 4 ? kXposeProdu
     const uint32_t lane_off = XPOSE ? 0u : TRANS ? lane * 128u : lane * 8u * (RPT == 1 ? 1u : 2u);
     // epilogue: one final scaling, as the reference (`out *= scale`)
     auto store_tile = [&](const int64_t r0) {
+    if (!owner) return;
     const bool vec_ok = ((p.lds & 1) == 0) && ((reinterpret_cast<uintptr_t>(p.S) & 15) == 0);
 #pragma unroll
     for (int jj = 0; jj < DB; ++jj) {
@@ -708,6 +773,10 @@ __global__ void __launch_bounds__((NW + (PROD ? (TRANS && RPT == 4 ? kXposeProdu
         }
 #endif
         if (DBG_IS(1)) {
+        } else if constexpr (PAIR && TRANS) {
+            pipe_t_pair(acc, sen, sx, lanex, sbw);
+        } else if constexpr (PAIR) {
+            pipe_s_pair(acc, sen, sx, sbw);
         } else if constexpr (TRANS) {
             if constexpr (RPT == 1 && DB == 16) pipe_t_1x16(acc, sen, sx, lanex, sbw);
             else if constexpr (RPT == 1 && DB == 32) pipe_t_1x32(acc, sen, sx, lanex, sbw);
@@ -726,6 +795,35 @@ __global__ void __launch_bounds__((NW + (PROD ? (TRANS && RPT == 4 ? kXposeProdu
             else if constexpr (RPT == 4 && DB == 2) pipe_s_4x2(acc, sen, sx, sbw);
             else if constexpr (RPT == 4 && DB == 4) pipe_s_4x4(acc, sen, sx, sbw);
             else if constexpr (RPT == 4 && DB == 8) pipe_s_4x8(acc, sen, sx, sbw);
+        }
+        if constexpr (PAIR) {
+            // a row tile ends here: fold k-groups 1..3 into k-group 0 (in
+            // k-group order) through slot s, before the slot is released
+            if (SK ? i + 1 == seg_end : i + 1 == nloc) {
+                constexpr int NT = NW * 32;
+                double *red = reinterpret_cast<double *>(stage0 + (size_t)s * p.stage_bytes);
+                const int kg = warp >> 2, pw = warp & 3;
+                bar_named(NT);  // every warp is done with the slot
+                for (int q = 1; q < kPairKg; ++q) {
+                    if (kg == q) {
+#pragma unroll
+                        for (int jj = 0; jj < DB; ++jj)
+#pragma unroll
+                            for (int r = 0; r < RPT; ++r) {
+                                red[((pw * DB + jj) * RPT + r) * 32 + lane] = acc[r][jj];
+                                acc[r][jj] = 0.0;
+                            }
+                    }
+                    bar_named(NT);
+                    if (kg == 0) {
+#pragma unroll
+                        for (int jj = 0; jj < DB; ++jj)
+#pragma unroll
+                            for (int r = 0; r < RPT; ++r) acc[r][jj] += red[((pw * DB + jj) * RPT + r) * 32 + lane];
+                    }
+                    bar_named(NT);
+                }
+            }
         }
         __syncwarp();
         if (lane == 0) {
@@ -754,11 +852,13 @@ __global__ void __launch_bounds__((NW + (PROD ? (TRANS && RPT == 4 ? kXposeProdu
             constexpr int NT = NW * 32;
             if (ctile == sk[3] && sk[0]) {
                 double *w = p.ws + (size_t)blockIdx.x * (SLAB * TM);
+                if (owner) {
 #pragma unroll
-                for (int jj = 0; jj < DB; ++jj)
+                    for (int jj = 0; jj < DB; ++jj)
 #pragma unroll
-                    for (int r = 0; r < RPT; ++r)
-                        __stcg(&w[((warp * DB + jj) * RPT + r) * 32 + lane], acc[r][jj]);
+                        for (int r = 0; r < RPT; ++r)
+                            __stcg(&w[((warp * DB + jj) * RPT + r) * 32 + lane], acc[r][jj]);
+                }
                 __threadfence();
                 bar_named(NT);
                 if (threadIdx.x == 0) st_release_gpu(&p.flags[blockIdx.x], 1);
@@ -772,11 +872,13 @@ __global__ void __launch_bounds__((NW + (PROD ? (TRANS && RPT == 4 ? kXposeProdu
                     }
                     bar_named(NT);
                     const double *w = p.ws + (size_t)cq * (SLAB * TM);
+                    if (owner) {
 #pragma unroll
                     for (int jj = 0; jj < DB; ++jj)
 #pragma unroll
                         for (int r = 0; r < RPT; ++r)
                             acc[r][jj] += __ldcg(&w[((warp * DB + jj) * RPT + r) * 32 + lane]);
+                    }
                 }
                 store_tile((int64_t)ctile * TM);
             }
@@ -799,7 +901,7 @@ __global__ void __launch_bounds__((NW + (PROD ? (TRANS && RPT == 4 ? kXposeProdu
     if (ks > 1) {
         double *red = reinterpret_cast<double *>(stage0);
         __syncthreads();  // every stage consumed: the ring is free
-        if (kr > 0) {
+        if (kr > 0 && owner) {
 #pragma unroll
             for (int jj = 0; jj < DB; ++jj)
 #pragma unroll
@@ -807,7 +909,7 @@ __global__ void __launch_bounds__((NW + (PROD ? (TRANS && RPT == 4 ? kXposeProdu
                     red[((warp * DB + jj) * RPT + r) * 32 + lane] = acc[r][jj];
         }
         cluster_sync();
-        if (kr == 0) {
+        if (kr == 0 && owner) {
             for (int q = 1; q < ks; ++q) {
 #pragma unroll
                 for (int jj = 0; jj < DB; ++jj)
@@ -824,10 +926,10 @@ __global__ void __launch_bounds__((NW + (PROD ? (TRANS && RPT == 4 ? kXposeProdu
 }
 
 
-template <int RPT, int DB, int NW>
+template <int RPT, int DB, int NW, bool PAIR = false>
 static int launch(ApplyArgs a, const Geom &g, cudaStream_t st) {
     constexpr int TM = 32 * RPT;
-    constexpr int SLAB = NW * DB;
+    constexpr int SLAB = PAIR ? kPairSlab : NW * DB;
     HSK_REQUIRE(g.tm == TM && g.db == DB && g.nw == NW, HSK_EINVAL, "sjlt: plan/config mismatch");
     const bool aligned = a.use_tma != 0;  // 16-byte aligned columns (lda even)
     // 0: TMA S tile; 1: cp.async S' tile (unaligned A); 2: cp.async S tile;
@@ -908,8 +1010,8 @@ static int launch(ApplyArgs a, const Geom &g, cudaStream_t st) {
     if (a.streamk && a.mc > 1) {
         // every group is one cluster and groups wait on later groups: keep
         // the grid to the clusters that can be co-resident
-        auto kprobe = a.trans ? sjlt_apply_kernel<RPT, DB, NW, true, true, true>
-                              : sjlt_apply_kernel<RPT, DB, NW, false, true, true>;
+        auto kprobe = a.trans ? sjlt_apply_kernel<RPT, DB, NW, true, true, true, PAIR>
+                              : sjlt_apply_kernel<RPT, DB, NW, false, true, true, PAIR>;
         const int smem_max = 2048 + stages_max * a.stage_bytes;
         cudaError_t e = cudaFuncSetAttribute(kprobe, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_max);
         if (e != cudaSuccess) return cuda_status(e, "sjlt: set smem attribute");
@@ -954,14 +1056,14 @@ static int launch(ApplyArgs a, const Geom &g, cudaStream_t st) {
     if (per > 0 && a.stages > per + 1) a.stages = std::max(2, per + 1);
     int smem = 2048 + a.stages * a.stage_bytes + stg_bytes;  // header + 1024-byte alignment slack
     if (ks > 1) smem = std::max(smem, 2048 + NW * DB * RPT * 32 * 8);
-    auto kern = a.trans ? (prod ? (a.streamk ? sjlt_apply_kernel<RPT, DB, NW, true, true, true>
-                                             : sjlt_apply_kernel<RPT, DB, NW, true, true, false>)
-                                : (a.streamk ? sjlt_apply_kernel<RPT, DB, NW, true, false, true>
-                                             : sjlt_apply_kernel<RPT, DB, NW, true, false, false>))
-                        : (prod ? (a.streamk ? sjlt_apply_kernel<RPT, DB, NW, false, true, true>
-                                             : sjlt_apply_kernel<RPT, DB, NW, false, true, false>)
-                                : (a.streamk ? sjlt_apply_kernel<RPT, DB, NW, false, false, true>
-                                             : sjlt_apply_kernel<RPT, DB, NW, false, false, false>));
+    auto kern = a.trans ? (prod ? (a.streamk ? sjlt_apply_kernel<RPT, DB, NW, true, true, true, PAIR>
+                                             : sjlt_apply_kernel<RPT, DB, NW, true, true, false, PAIR>)
+                                : (a.streamk ? sjlt_apply_kernel<RPT, DB, NW, true, false, true, PAIR>
+                                             : sjlt_apply_kernel<RPT, DB, NW, true, false, false, PAIR>))
+                        : (prod ? (a.streamk ? sjlt_apply_kernel<RPT, DB, NW, false, true, true, PAIR>
+                                             : sjlt_apply_kernel<RPT, DB, NW, false, true, false, PAIR>)
+                                : (a.streamk ? sjlt_apply_kernel<RPT, DB, NW, false, false, true, PAIR>
+                                             : sjlt_apply_kernel<RPT, DB, NW, false, false, false, PAIR>));
     // L2 prefetch beyond the ring: off -- the duplicate requests cost power,
     // and sustained runs are power-capped (C2, 2000 launches: 0.505 ms
     // without, 0.540 ms with; no burst gain either).  HSK_SJLT_PF=<chunks>.
@@ -1008,14 +1110,26 @@ static int launch(ApplyArgs a, const Geom &g, cudaStream_t st) {
 
 using namespace hsk;
 
-extern "C" int64_t hsk_sjlt_plan_bytes(int64_t n, int32_t d, int32_t alpha) {
-    if (n < 0 || d < 1 || alpha < 1 || d > sjlt::kMaxD || alpha > sjlt::kMaxChunkEntries)
+extern "C" int64_t hsk_sjlt_plan_bytes_ex(int64_t n, int32_t d, int32_t alpha, int32_t flags) {
+    if (n < 0 || d < 1 || alpha < 1 || d > sjlt::kMaxD || alpha > sjlt::kMaxChunkEntries ||
+        (flags & ~HSK_SJLT_CHUNKED))
         return HSK_EINVAL;
-    return sjlt::plan_geom(n, d, alpha).bytes;
+    return sjlt::plan_geom(n, d, alpha, flags & HSK_SJLT_CHUNKED).bytes;
+}
+
+extern "C" int64_t hsk_sjlt_plan_bytes(int64_t n, int32_t d, int32_t alpha) {
+    return hsk_sjlt_plan_bytes_ex(n, d, alpha, 0);
 }
 
 extern "C" int hsk_sjlt_plan_build(const int32_t *pos, const int8_t *sgn, int64_t n, int32_t d,
                                    int32_t alpha, void *plan, int64_t plan_bytes, void *stream) {
+    return hsk_sjlt_plan_build_ex(pos, sgn, n, d, alpha, 0, plan, plan_bytes, stream);
+}
+
+extern "C" int hsk_sjlt_plan_build_ex(const int32_t *pos, const int8_t *sgn, int64_t n, int32_t d,
+                                      int32_t alpha, int32_t flags, void *plan, int64_t plan_bytes,
+                                      void *stream) {
+    HSK_REQUIRE((flags & ~HSK_SJLT_CHUNKED) == 0, HSK_EINVAL, "sjlt plan: unknown flags %d", flags);
     HSK_REQUIRE(n >= 0 && d >= 1 && alpha >= 1, HSK_EINVAL,
                 "sjlt plan: need n >= 0, d >= 1, alpha >= 1 (n=%lld d=%d alpha=%d)",
                 (long long)n, d, alpha);
@@ -1023,7 +1137,7 @@ extern "C" int hsk_sjlt_plan_build(const int32_t *pos, const int8_t *sgn, int64_
                 (long long)sjlt::kMaxD);
     HSK_REQUIRE(alpha <= sjlt::kMaxChunkEntries, HSK_EINVAL, "sjlt plan: alpha=%d too large", alpha);
     HSK_REQUIRE(n < (1ll << 31), HSK_EINVAL, "sjlt plan: n too large");
-    const sjlt::Plan pl = sjlt::plan_geom(n, d, alpha);
+    const sjlt::Plan pl = sjlt::plan_geom(n, d, alpha, flags & HSK_SJLT_CHUNKED);
     HSK_REQUIRE(plan != nullptr && plan_bytes >= pl.bytes, HSK_EINVAL,
                 "sjlt plan: buffer of %lld bytes, need %lld", (long long)plan_bytes,
                 (long long)pl.bytes);
@@ -1035,10 +1149,10 @@ extern "C" int hsk_sjlt_plan_build(const int32_t *pos, const int8_t *sgn, int64_
     if (n > 0) {
         for (const sjlt::Geom *g : {&pl.s, &pl.t}) {
             int p2 = 1;
-            while (p2 < g->tk * alpha) p2 <<= 1;
+            while (p2 < g->tk * (g->pair ? alpha / 2 : alpha)) p2 <<= 1;
             sjlt::sjlt_plan_kernel<<<(unsigned)g->nchunks, 256, p2 * sizeof(uint32_t), st>>>(
                 pos, sgn, n, d, alpha, g->tk, p2, g->db, g->ngroups, g->gstride, g->estride,
-                g == &pl.t ? (g->rpt == 4 ? -g->tm : g->tm) : 0,
+                g == &pl.t ? (g->rpt == 4 ? -g->tm : g->tm) : 0, g->pair,
                 reinterpret_cast<uint32_t *>(base + g->gptr_off),
                 reinterpret_cast<uint32_t *>(base + g->ent_off), reinterpret_cast<int *>(base + 28));
             HSK_CHECK_LAUNCH("sjlt_plan_kernel");
@@ -1051,6 +1165,15 @@ extern "C" int hsk_sjlt_apply(const double *A, int64_t rows, int64_t cols, int64
                               int32_t trans, const void *plan, int64_t n, int32_t d,
                               int32_t alpha, double scale, double *S, int64_t lds, int64_t col0,
                               void *stream) {
+    return hsk_sjlt_apply_ex(A, rows, cols, lda, trans, plan, n, d, alpha, 0, scale, S, lds, col0,
+                             stream);
+}
+
+extern "C" int hsk_sjlt_apply_ex(const double *A, int64_t rows, int64_t cols, int64_t lda,
+                                 int32_t trans, const void *plan, int64_t n, int32_t d,
+                                 int32_t alpha, int32_t flags, double scale, double *S, int64_t lds,
+                                 int64_t col0, void *stream) {
+    HSK_REQUIRE((flags & ~HSK_SJLT_CHUNKED) == 0, HSK_EINVAL, "sjlt apply: unknown flags %d", flags);
     HSK_REQUIRE(trans == 0 || trans == 1, HSK_EINVAL, "sjlt apply: trans must be 0 or 1");
     HSK_REQUIRE(rows >= 0 && cols >= 0 && lda >= std::max<int64_t>(rows, 1), HSK_EINVAL,
                 "sjlt apply: bad A shape rows=%lld cols=%lld lda=%lld", (long long)rows,
@@ -1069,7 +1192,7 @@ extern "C" int hsk_sjlt_apply(const double *A, int64_t rows, int64_t cols, int64
     HSK_REQUIRE(plan != nullptr && S != nullptr && (A != nullptr || n == 0), HSK_EINVAL,
                 "sjlt apply: null pointer");
     HSK_REQUIRE(m_out < (1ll << 31) && n < (1ll << 31), HSK_EINVAL, "sjlt apply: too large");
-    const sjlt::Plan pl = sjlt::plan_geom(n, d, alpha);
+    const sjlt::Plan pl = sjlt::plan_geom(n, d, alpha, flags & HSK_SJLT_CHUNKED);
     const sjlt::Geom &g = trans ? pl.t : pl.s;
     const unsigned char *base = static_cast<const unsigned char *>(plan);
     sjlt::ApplyArgs a{};
@@ -1093,6 +1216,7 @@ extern "C" int hsk_sjlt_apply(const double *A, int64_t rows, int64_t cols, int64
     a.col0 = col0;
     cudaStream_t st = as_stream(stream);
     // the plan was built for this warp shape (warp_shape): one kernel each
+    if (g.pair) return sjlt::launch<2, 16, 16, true>(a, g, st);
     const int shape = g.rpt * 1000 + g.db * 10 + (g.nw == 32);
     switch (shape) {
         case 1320: return sjlt::launch<1, 32, 16>(a, g, st);   // 32-row tiles, 512-bucket slabs

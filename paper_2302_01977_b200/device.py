@@ -19,6 +19,7 @@ PyTorch is used only as plumbing here (device allocation, streams, host
 from __future__ import annotations
 
 import math
+import os
 import weakref
 
 import numpy as np
@@ -162,7 +163,20 @@ class RawMatrix:
 # --------------------------------------------------------------- R on device
 
 class _SjltState:
-    __slots__ = ("pos", "sgn", "plan", "n", "d", "alpha", "scale")
+    __slots__ = ("pos", "sgn", "plan", "n", "d", "alpha", "scale", "flags")
+
+
+HSK_SJLT_CHUNKED = 1  # include/hsk.h
+
+
+def sjlt_chunked(pos: np.ndarray, d: int, alpha: int) -> bool:
+    """The block construction's chunk property (sketching.py:246-250): entry t
+    of every input index lies in chunk t of d/alpha buckets.  Checked on the
+    pattern itself (from_pattern blocks qualify too); HSK_SJLT_NOCHUNK=1 turns
+    the paired plan off (A/B runs)."""
+    if os.environ.get("HSK_SJLT_NOCHUNK") == "1" or d % alpha or pos.size == 0:
+        return False
+    return bool((pos // (d // alpha) == np.arange(alpha, dtype=pos.dtype)).all())
 
 
 class _GaussState:
@@ -204,11 +218,12 @@ def block_state(block):
         st.sgn = torch.from_numpy(np.ascontiguousarray(block._signs, dtype=np.int8).reshape(-1)).to(dev)
         st.n, st.d, st.alpha = n, d, alpha
         st.scale = float(block._scale)
-        nbytes = _lib.load().hsk_sjlt_plan_bytes(n, d, alpha)
-        _lib.check(nbytes, "hsk_sjlt_plan_bytes")
+        st.flags = HSK_SJLT_CHUNKED if sjlt_chunked(pos, d, alpha) else 0
+        nbytes = _lib.load().hsk_sjlt_plan_bytes_ex(n, d, alpha, st.flags)
+        _lib.check(nbytes, "hsk_sjlt_plan_bytes_ex")
         st.plan = torch.empty(int(nbytes), dtype=torch.uint8, device=dev)
-        _lib.call("hsk_sjlt_plan_build", st.pos.data_ptr(), st.sgn.data_ptr(), n, d, alpha,
-                  st.plan.data_ptr(), int(nbytes), stream)
+        _lib.call("hsk_sjlt_plan_build_ex", st.pos.data_ptr(), st.sgn.data_ptr(), n, d, alpha,
+                  st.flags, st.plan.data_ptr(), int(nbytes), stream)
     elif kind == "gaussian":
         st = _GaussState()
         st.R = torch.from_numpy(np.ascontiguousarray(block.matrix, dtype=np.float64)).to(dev)
@@ -236,8 +251,8 @@ def apply_block(block, A: DeviceMatrix, transpose: bool, S: DeviceMatrix, col0: 
         raise ValueError("output buffer does not match the sketch shape")
     kind = block.kind
     if kind == "sjlt":
-        _lib.call("hsk_sjlt_apply", A.ptr, A.rows, A.cols, A.ld, trans, st.plan.data_ptr(),
-                  st.n, st.d, st.alpha, st.scale, S.ptr, S.ld, col0, stream)
+        _lib.call("hsk_sjlt_apply_ex", A.ptr, A.rows, A.cols, A.ld, trans, st.plan.data_ptr(),
+                  st.n, st.d, st.alpha, st.flags, st.scale, S.ptr, S.ld, col0, stream)
     elif kind == "gaussian":
         _lib.call("hsk_gauss_apply", A.ptr, A.rows, A.cols, A.ld, trans, st.R.data_ptr(),
                   st.n, st.d, S.ptr, S.ld, col0, stream)

@@ -155,7 +155,7 @@ def test_odd_leading_dimension_and_column_offset(cuda):
         _close(got[:, 5:5 + d], ref, np.linalg.norm(A))
         assert np.all(got[:, :5] == 0) and np.all(got[:, 5 + d:] == 0)
         B = rng.standard_normal((n, m))
-        dB = device.DeviceMatrix(n, m, ld=n + 1)
+        dB = device.DeviceMatrix(n, m, ld=n + 2)  # odd: unaligned columns (cp.async producers)
         dB.upload(B)
         ref_t = O.apply_right_transposed(B, op)
         _close(sk.apply_right_transposed_device(dB, op).to_host(), ref_t, np.linalg.norm(B))
@@ -286,3 +286,69 @@ def test_streamed_pinned_host_path_is_bit_identical(cuda, monkeypatch):
         np.testing.assert_array_equal(sk.apply_right(A, op), ref)
         ref_t = sk.apply_right_transposed_device(device.DeviceMatrix.from_host(B), op).to_host()
         np.testing.assert_array_equal(sk.apply_right_transposed(B, op), ref_t)
+
+
+@pytest.mark.parametrize("m,n,d,alpha", [
+    (64, 64, 64, 8), (100, 1000, 64, 8), (3000, 9000, 64, 8), (257, 4100, 128, 16),
+    (70, 20000, 64, 8), (1, 300, 64, 8),
+])
+def test_sjlt_paired_plan_vs_oracle(cuda, monkeypatch, m, n, d, alpha):
+    """Chunked (block-construction) patterns with d/alpha = 8 take the paired
+    plan (one tile read feeds a warp's two chunks, k-groups folded per row
+    tile): oracle parity on every schedule, odd leading dimensions (cp.async
+    producers) and column offsets; bitwise repeatable; the unpaired plan of the
+    same operator (HSK_SJLT_NOCHUNK=1) agrees to the same tolerance."""
+    rng = np.random.default_rng(m + n + d)
+    A = rng.standard_normal((m, n))
+    B = rng.standard_normal((n, m))
+    res = {}
+    for nochunk in ("0", "1"):
+        monkeypatch.setenv("HSK_SJLT_NOCHUNK", nochunk)
+        op = sk.new_operator(sk.SJLT, n, d, seed=(m, n, d), alpha=alpha, construction=sk.BLOCK)
+        b = op.blocks[0]
+        ref = O.sjlt_right(A, b._pos, b._signs, d, b._scale)
+        ref_t = O.sjlt_right_t(B, b._pos, b._signs, d, b._scale)
+        assert device.block_state(b).flags == (0 if nochunk == "1" else device.HSK_SJLT_CHUNKED)
+        for sched in ("0", "1"):
+            monkeypatch.setenv("HSK_SJLT_STREAMK", sched)
+            for ld_pad in (0, 1):
+                dA = device.DeviceMatrix(m, n, ld=m + ld_pad)
+                dA.upload(A)
+                out = device.DeviceMatrix.zeros(m, d + 3)
+                sk.apply_right_device(dA, op, out=out, col0=2)
+                s1 = out.to_host()
+                _close(s1[:, 2:2 + d], ref, np.linalg.norm(A))
+                assert np.all(s1[:, :2] == 0) and np.all(s1[:, 2 + d:] == 0)
+                sk.apply_right_device(dA, op, out=out, col0=2)
+                np.testing.assert_array_equal(out.to_host(), s1)
+                dB = device.DeviceMatrix(n, m, ld=n + ld_pad)
+                dB.upload(B)
+                t1 = sk.apply_right_transposed_device(dB, op).to_host()
+                _close(t1, ref_t, np.linalg.norm(B))
+                np.testing.assert_array_equal(sk.apply_right_transposed_device(dB, op).to_host(), t1)
+                res[(nochunk, sched, ld_pad)] = (s1[:, 2:2 + d], t1)
+    a, b = res[("0", "0", 0)], res[("1", "0", 0)]
+    assert O.rel_frobenius(a[0], b[0]) <= REL and O.rel_frobenius(a[1], b[1]) <= REL
+
+
+def test_sjlt_chunk_property_detection(cuda):
+    """Only patterns with entry t in chunk t take the paired plan: graph
+    construction at the same shape, and a from_pattern block that breaks the
+    property, stay on the general plan (and still match the oracle)."""
+    n, d, alpha = 500, 64, 8
+    g = sk.new_operator(sk.SJLT, n, d, seed=3, alpha=alpha, construction=sk.GRAPH).blocks[0]
+    blk = sk.new_operator(sk.SJLT, n, d, seed=3, alpha=alpha, construction=sk.BLOCK).blocks[0]
+    pos = np.array(blk._pos)
+    pos[7, [0, 1]] = pos[7, [1, 0]]  # entries 0 and 1 of k = 7 swap chunks
+    bad = sk.SjltBlock.from_pattern(n, d, alpha, pos, blk._signs)
+    good = sk.SjltBlock.from_pattern(n, d, alpha, blk._pos, blk._signs)
+    assert device.block_state(good).flags == device.HSK_SJLT_CHUNKED
+    A = np.random.default_rng(1).standard_normal((90, n))
+    for b in (g, bad):
+        assert device.block_state(b).flags == 0
+    for b in (g, bad, good):
+        op = sk.SketchOperator(sk.SJLT, n, (b,), alpha=alpha)
+        ref = O.sjlt_right(A, b._pos, b._signs, d, b._scale)
+        _close(sk.apply_right(A, op), ref, np.linalg.norm(A))
+        ref_t = O.sjlt_right_t(np.asfortranarray(A.T), b._pos, b._signs, d, b._scale)
+        _close(sk.apply_right_transposed(np.asfortranarray(A.T), op), ref_t, np.linalg.norm(A))

@@ -33,6 +33,15 @@ Address bits (the sign and bucket bits never reach an address):
                           e = kk*TM*8 | 8(kk%32);
                           row c = l + 32r at st + (e & 0xffff00) + ((e & 248) ^ 8l) + 256r
 
+Paired walkers (pipe_{s,t}_pair; block construction with d/alpha = 8): a warp
+owns the 16 buckets of two construction chunks t1 = 2p, t2 = 2p + 1, so every
+input index of its k-range carries exactly one entry for the pair,
+
+    e = neg1 << 31 | (c1 * 8 + c2) << 24 | neg2 << 23 | address bits,
+
+(c1, c2 = bucket mod 8 in chunks t1, t2; terminator combo field = 64): one
+tile load feeds two buckets, and the chain runs over the 64 combos.
+
 Usage: python tools/gen_consumers.py > paper_2302_01977_b200/csrc/hsk_sjlt_pipe.cuh
 """
 import sys
@@ -119,6 +128,69 @@ def gen(rpt, db, trans):
             f'                 : "memory");\n}}\n')
 
 
+def gen_pair(trans):
+    """RPT = 2 rows per lane, 16 buckets = two chunks of 8 (see the docstring)."""
+    rpt, nacc = 2, 32
+    L = []
+    a = L.append
+    sen, base = nacc, nacc + 1
+    lane8 = nacc + 2 if trans else None
+    sgs = nacc + (3 if trans else 2)
+    a(".reg .pred q;")
+    a(".reg .b32 pe, t, t2, ad, e, k, gh, gh2, zero, one;")
+    a(".reg .f64 u0, u1, g, g2;")
+    a("mov.b32 zero, 0;")
+    a("mov.b32 one, 1072693248;")
+
+    def load_tile():
+        if trans:
+            # neg2 (bit 23) stays out of the address: mask 0x7fffff
+            out = [f"lop3.b32 ad, e, %{lane8}, 8388607, 0x28;", f"add.u32 ad, ad, %{base};",
+                   "ld.shared.f64 u0, [ad];", "ld.shared.f64 u1, [ad+4096];"]
+        else:
+            out = ["shl.b32 t, e, 9;", f"add.u32 ad, t, %{base};", "ld.shared.v2.f64 {u0, u1}, [ad];"]
+        out += ["lop3.b32 gh, e, -2147483648, one, 0xEA;", "mov.b64 g, {zero, gh};",
+                "shl.b32 t2, e, 8;", "lop3.b32 gh2, t2, -2147483648, one, 0xEA;",
+                "mov.b64 g2, {zero, gh2};"]
+        return out
+
+    a(f"ld.shared.b32 t, [%{sgs}];")
+    a(f"mad.lo.u32 pe, t, 4, %{sen};")
+    a("ld.shared.b32 e, [pe];")
+    L.extend(load_tile())
+    a("and.b32 k, e, 2130706432;")
+    a("ld.shared.b32 e, [pe+4];")
+    for cc in range(64):
+        nxt = f"T{cc + 1}" if cc + 1 < 64 else "DONE"
+        c1, c2 = cc // 8, cc % 8
+        a(f"T{cc}:")
+        a(f"setp.ne.u32 q, k, {cc << 24};")
+        a(f"@q bra.uni {nxt};")
+        a(f"S{cc}:")
+        for r in range(rpt):
+            k1, k2 = c1 * rpt + r, (8 + c2) * rpt + r
+            a(f"fma.rn.f64 %{k1}, u{r}, g, %{k1};")
+            a(f"fma.rn.f64 %{k2}, u{r}, g2, %{k2};")
+        L.extend(load_tile())
+        a("and.b32 k, e, 2130706432;")
+        a("add.u32 pe, pe, 4;")
+        a("ld.shared.b32 e, [pe+4];")
+        a(f"setp.eq.u32 q, k, {cc << 24};")
+        a(f"@q bra.uni S{cc};")
+    a("DONE:")
+    txt = "\\n\\t".join(L)
+    outs = ", ".join(f'"+d"(acc[{k % rpt}][{k // rpt}])' for k in range(nacc))
+    ins = ['"r"(sen)', '"r"(base)'] + (['"r"(lanex)'] if trans else []) + ['"r"(sgs)']
+    name = f"pipe_{'t' if trans else 's'}_pair"
+    sig = "uint32_t sen, uint32_t base, " + ("uint32_t lanex, " if trans else "")
+    return (f"__device__ __forceinline__ void {name}(double (&acc)[{rpt}][16], {sig}"
+            f"uint32_t sgs) {{\n"
+            f'    asm volatile("{{\\n\\t{txt}\\n\\t}}"\n'
+            f"                 : {outs}\n"
+            f"                 : {', '.join(ins)}\n"
+            f'                 : "memory");\n}}\n')
+
+
 def main():
     out = ["// GENERATED by tools/gen_consumers.py -- do not edit by hand.",
            "// Software-pipelined whole-chunk SJLT walkers (state-tagged entries); see the generator.",
@@ -127,6 +199,8 @@ def main():
         out.append(gen(rpt, db, False))
     for rpt, db in T_CONFIGS:
         out.append(gen(rpt, db, True))
+    out.append(gen_pair(False))
+    out.append(gen_pair(True))
     sys.stdout.write("\n".join(out))
 
 
