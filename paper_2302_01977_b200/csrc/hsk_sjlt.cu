@@ -136,14 +136,15 @@ static inline void warp_shape(int rpt, int d, int &db, int &nw) {
 
 // Paired sub-plans (block construction with chunk d/alpha = 8, d a multiple
 // of 64: C3's alpha = 8 increments of 64).  Every input index has exactly one
-// bucket in each construction chunk, so a warp owning the 16 buckets of two
-// chunks (t1 = 2p, t2 = 2p + 1) sees every input index of its k-range exactly
-// once: one tile load feeds both buckets.  64-row tiles, 16 consumer warps =
-// 4 k-groups (quarters of the chunk's TK indices) x 4 chunk pairs; a slab is
-// 64 buckets; the k-groups' partial sums are added in k-group order at the end
-// of a row tile (deterministic).  Per (row, element): alpha/2 tile reads
-// instead of alpha.
-constexpr int kPairKg = 4;     // k-groups per CTA
+// bucket in each construction chunk, so one entry can carry an index's
+// buckets in two chunks (t1 = 2p, t2 = 2p + 1) and one tile load feeds both.
+// 64-row tiles, a slab is 64 buckets (4 chunk pairs), 16 consumer warps =
+// 4 chunk pairs x 4 quarters of chunk t1: warp (p, h) walks the indices whose
+// t1 bucket lies in quarter h (2 of its 8 buckets, complete in the warp) and
+// accumulates their chunk-t2 buckets (8, partial); the four quarters' t2
+// partials are added in quarter order at the end of a row tile
+// (deterministic).  Per (row, element): alpha/2 tile reads instead of alpha;
+// 16 (t1, t2) bucket combos per warp.
 constexpr int kPairSlab = 64;  // buckets per slab (4 chunk pairs)
 
 static Geom geom_dir(int64_t n, int d, int alpha, int trans, int64_t base, int pair = 0) {
@@ -159,7 +160,8 @@ static Geom geom_dir(int64_t n, int d, int alpha, int trans, int64_t base, int p
         g.ngroups = (int64_t)(d / kPairSlab) * g.nw;
         tk = n >= 8192 ? tk_fit16(ae, 64, 256, kStage2, g.ngroups, g.nw)
                        : tk_fit16(ae, 64, 128, kStage3, g.ngroups, g.nw);
-        if (const char *env = getenv(trans ? "HSK_SJLT_TK_T" : "HSK_SJLT_TK")) tk = atoi(env) / 16 * 16;
+        if (const char *env = getenv(trans ? "HSK_SJLT_TK_T" : "HSK_SJLT_TK"))
+            tk = std::max(128, atoi(env) / 16 * 16);  // the fold buffer needs 64 KB of tile
         g.tm = 64;
         g.pitch = g.tm;
         g.tk = tk;
@@ -259,9 +261,8 @@ __global__ void sjlt_plan_kernel(const int32_t *__restrict__ pos, const int8_t *
     const int np = alpha / 2;  // paired plans: entries per input index
     const int cnt = kc * (pair ? np : alpha);
     const int64_t q0 = k0 * alpha;
-    // paired key: group << 14 | combo << 8 | kk, group = slab * 16 + kgroup * 4
-    // + pair mod 4 (the consumer warp), combo = c1 * 8 + c2
-    const int kgw = tk / kPairKg;
+    // paired key: group << 14 | combo << 8 | kk, group = slab * 16 + (pair mod
+    // 4) * 4 + c1 / 2 (the consumer warp), combo = (c1 & 1) * 8 + c2
     const int gsh = pair ? 14 : 12;
     for (int i = threadIdx.x; i < p2; i += blockDim.x) {
         uint32_t key = 0xFFFFFFFFu;
@@ -270,8 +271,8 @@ __global__ void sjlt_plan_kernel(const int32_t *__restrict__ pos, const int8_t *
             const int b1 = pos[q0 + (int64_t)kk * alpha + 2 * pg] - 16 * pg;
             const int b2 = pos[q0 + (int64_t)kk * alpha + 2 * pg + 1] - 16 * pg - 8;
             if (b1 < 0 || b1 >= 8 || b2 < 0 || b2 >= 8) atomicOr(err, 2);
-            const uint32_t grp = (uint32_t)((pg >> 2) * 16 + (kk / kgw) * 4 + (pg & 3));
-            key = (grp << 14) | ((uint32_t)((b1 & 7) * 8 + (b2 & 7)) << 8) | (uint32_t)kk;
+            const uint32_t grp = (uint32_t)((pg >> 2) * 16 + (pg & 3) * 4 + ((b1 & 7) >> 1));
+            key = (grp << 14) | ((uint32_t)((b1 & 1) * 8 + (b2 & 7)) << 8) | (uint32_t)kk;
         } else if (i < cnt) {
             int p = pos[q0 + i];
             if (p < 0 || p >= d) {
@@ -306,7 +307,7 @@ __global__ void sjlt_plan_kernel(const int32_t *__restrict__ pos, const int8_t *
         const uint32_t key = keys[e];
         if (pair) {
             const uint32_t grp = key >> 14, kk = key & 255u, combo = (key >> 8) & 63u;
-            const int pg = (int)((grp >> 4) * 4 + (grp & 3));
+            const int pg = (int)((grp >> 4) * 4 + ((grp >> 2) & 3));
             const int64_t q = q0 + (int64_t)kk * alpha + 2 * pg;
             e_out[e + grp] = (sgn[q] < 0 ? 0x80000000u : 0u) | (combo << 24) |
                              (sgn[q + 1] < 0 ? 0x00800000u : 0u) | entry_addr(kk, tm_t);
@@ -333,7 +334,7 @@ __global__ void sjlt_plan_kernel(const int32_t *__restrict__ pos, const int8_t *
         const int64_t gg = g < ngroups ? g : ngroups;
         g_out[g] = (uint32_t)(lb + gg);
         // group g-1 ends where group g starts: its terminator
-        if (g >= 1 && g <= ngroups) e_out[lb + g - 1] = (uint32_t)(pair ? 64 : db) << 24;
+        if (g >= 1 && g <= ngroups) e_out[lb + g - 1] = (uint32_t)(pair ? 16 : db) << 24;
     }
 }
 
@@ -398,9 +399,10 @@ __global__ void __launch_bounds__((NW + (PROD ? (TRANS && RPT == 4 ? kXposeProdu
     constexpr int TM = 32 * RPT;
     constexpr int SLAB = PAIR ? kPairSlab : NW * DB;
     constexpr bool XPOSE = TRANS && RPT == 4;       // transposed S' tile layout
-    // paired plans: warps [0, 4) (k-group 0) hold a row tile's sums once the
-    // k-groups are folded; only they publish and store
-    const bool owner = !PAIR || (threadIdx.x >> 5) < 4;
+    // (paired plans: warp (p, h) = 4p + h holds t1 buckets 16p + 2h + {0, 1}
+    // in acc[.][0..1] and, once the quarters are folded into h = 0, the t2
+    // buckets 16p + 8 + c2 in acc[.][2 + c2]; partials published / reduced
+    // across CTAs keep the per-warp layout of the unpaired kernels)
     constexpr int PW = PROD ? (XPOSE ? kXposeProducers : 1) : 0;  // dedicated producer warps
     extern __shared__ __align__(128) unsigned char smem[];
     uint64_t *full = reinterpret_cast<uint64_t *>(smem);
@@ -695,11 +697,12 @@ __global__ void __launch_bounds__((NW + (PROD ? (TRANS && RPT == 4 ? kXposeProdu
     const uint32_t lane_off = XPOSE ? 0u : TRANS ? lane * 128u : lane * 8u * (RPT == 1 ? 1u : 2u);
     // epilogue: one final scaling, as the reference (`out *= scale`)
     auto store_tile = [&](const int64_t r0) {
-    if (!owner) return;
     const bool vec_ok = ((p.lds & 1) == 0) && ((reinterpret_cast<uintptr_t>(p.S) & 15) == 0);
 #pragma unroll
-    for (int jj = 0; jj < DB; ++jj) {
-        const int j = j0 + warp * DB + jj;
+    for (int jj = 0; jj < (PAIR ? 10 : DB); ++jj) {
+        if (PAIR && jj >= 2 && (warp & 3) != 0) break;
+        const int j = PAIR ? j0 + (warp >> 2) * 16 + (jj < 2 ? 2 * (warp & 3) + jj : 6 + jj)
+                           : j0 + warp * DB + jj;
         if (j < p.d) {
             double *col = p.S + (p.col0 + j) * p.lds;
             if (TRANS) {  // lane owns rows lane + 32 r
@@ -797,32 +800,32 @@ __global__ void __launch_bounds__((NW + (PROD ? (TRANS && RPT == 4 ? kXposeProdu
             else if constexpr (RPT == 4 && DB == 8) pipe_s_4x8(acc, sen, sx, sbw);
         }
         if constexpr (PAIR) {
-            // a row tile ends here: fold k-groups 1..3 into k-group 0 (in
-            // k-group order) through slot s, before the slot is released
+            // a row tile ends here: fold quarters 1..3's chunk-t2 partials into
+            // quarter 0 (in quarter order) through slot s, before its release
             if (SK ? i + 1 == seg_end : i + 1 == nloc) {
                 constexpr int NT = NW * 32;
                 double *red = reinterpret_cast<double *>(stage0 + (size_t)s * p.stage_bytes);
-                const int kg = warp >> 2, pw = warp & 3;
+                const int h = warp & 3;
                 bar_named(NT);  // every warp is done with the slot
-                for (int q = 1; q < kPairKg; ++q) {
-                    if (kg == q) {
+                if (h > 0) {
 #pragma unroll
-                        for (int jj = 0; jj < DB; ++jj)
+                    for (int jj = 2; jj < 10; ++jj)
 #pragma unroll
-                            for (int r = 0; r < RPT; ++r) {
-                                red[((pw * DB + jj) * RPT + r) * 32 + lane] = acc[r][jj];
-                                acc[r][jj] = 0.0;
-                            }
-                    }
-                    bar_named(NT);
-                    if (kg == 0) {
-#pragma unroll
-                        for (int jj = 0; jj < DB; ++jj)
-#pragma unroll
-                            for (int r = 0; r < RPT; ++r) acc[r][jj] += red[((pw * DB + jj) * RPT + r) * 32 + lane];
-                    }
-                    bar_named(NT);
+                        for (int r = 0; r < RPT; ++r) {
+                            red[((warp * 8 + jj - 2) * RPT + r) * 32 + lane] = acc[r][jj];
+                            acc[r][jj] = 0.0;
+                        }
                 }
+                bar_named(NT);
+                if (h == 0) {
+                    for (int q = 1; q < 4; ++q)
+#pragma unroll
+                        for (int jj = 2; jj < 10; ++jj)
+#pragma unroll
+                            for (int r = 0; r < RPT; ++r)
+                                acc[r][jj] += red[(((warp + q) * 8 + jj - 2) * RPT + r) * 32 + lane];
+                }
+                bar_named(NT);
             }
         }
         __syncwarp();
@@ -851,14 +854,12 @@ __global__ void __launch_bounds__((NW + (PROD ? (TRANS && RPT == 4 ? kXposeProdu
             // last one a head that adds the later groups' tails in group order
             constexpr int NT = NW * 32;
             if (ctile == sk[3] && sk[0]) {
-                double *w = p.ws + (size_t)blockIdx.x * (SLAB * TM);
-                if (owner) {
+                double *w = p.ws + (size_t)blockIdx.x * (NW * DB * TM);
 #pragma unroll
-                    for (int jj = 0; jj < DB; ++jj)
+                for (int jj = 0; jj < DB; ++jj)
 #pragma unroll
-                        for (int r = 0; r < RPT; ++r)
-                            __stcg(&w[((warp * DB + jj) * RPT + r) * 32 + lane], acc[r][jj]);
-                }
+                    for (int r = 0; r < RPT; ++r)
+                        __stcg(&w[((warp * DB + jj) * RPT + r) * 32 + lane], acc[r][jj]);
                 __threadfence();
                 bar_named(NT);
                 if (threadIdx.x == 0) st_release_gpu(&p.flags[blockIdx.x], 1);
@@ -871,14 +872,12 @@ __global__ void __launch_bounds__((NW + (PROD ? (TRANS && RPT == 4 ? kXposeProdu
                         p.flags[cq] = 0;
                     }
                     bar_named(NT);
-                    const double *w = p.ws + (size_t)cq * (SLAB * TM);
-                    if (owner) {
+                    const double *w = p.ws + (size_t)cq * (NW * DB * TM);
 #pragma unroll
                     for (int jj = 0; jj < DB; ++jj)
 #pragma unroll
                         for (int r = 0; r < RPT; ++r)
                             acc[r][jj] += __ldcg(&w[((warp * DB + jj) * RPT + r) * 32 + lane]);
-                    }
                 }
                 store_tile((int64_t)ctile * TM);
             }
@@ -901,7 +900,7 @@ __global__ void __launch_bounds__((NW + (PROD ? (TRANS && RPT == 4 ? kXposeProdu
     if (ks > 1) {
         double *red = reinterpret_cast<double *>(stage0);
         __syncthreads();  // every stage consumed: the ring is free
-        if (kr > 0 && owner) {
+        if (kr > 0) {
 #pragma unroll
             for (int jj = 0; jj < DB; ++jj)
 #pragma unroll
@@ -909,7 +908,7 @@ __global__ void __launch_bounds__((NW + (PROD ? (TRANS && RPT == 4 ? kXposeProdu
                     red[((warp * DB + jj) * RPT + r) * 32 + lane] = acc[r][jj];
         }
         cluster_sync();
-        if (kr == 0 && owner) {
+        if (kr == 0) {
             for (int q = 1; q < ks; ++q) {
 #pragma unroll
                 for (int jj = 0; jj < DB; ++jj)
@@ -1044,7 +1043,7 @@ static int launch(ApplyArgs a, const Geom &g, cudaStream_t st) {
         void *ws = nullptr;
         int *flags = nullptr;
         const int nct = a.groups * a.nslabs;
-        int rc = stream_workspace(st, (size_t)nct * SLAB * TM * sizeof(double), nct, &ws, &flags);
+        int rc = stream_workspace(st, (size_t)nct * NW * DB * TM * sizeof(double), nct, &ws, &flags);
         if (rc) return rc;
         a.ws = static_cast<double *>(ws);
         a.flags = flags;

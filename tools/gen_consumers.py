@@ -33,14 +33,17 @@ Address bits (the sign and bucket bits never reach an address):
                           e = kk*TM*8 | 8(kk%32);
                           row c = l + 32r at st + (e & 0xffff00) + ((e & 248) ^ 8l) + 256r
 
-Paired walkers (pipe_{s,t}_pair; block construction with d/alpha = 8): a warp
-owns the 16 buckets of two construction chunks t1 = 2p, t2 = 2p + 1, so every
-input index of its k-range carries exactly one entry for the pair,
+Paired walkers (pipe_{s,t}_pair; block construction with d/alpha = 8): the
+four warps of chunk pair (t1 = 2p, t2 = 2p + 1) split chunk t1's 8 buckets into
+quarters; warp h walks every input index whose t1 bucket c1 lies in quarter h,
+with one entry carrying both of its buckets,
 
-    e = neg1 << 31 | (c1 * 8 + c2) << 24 | neg2 << 23 | address bits,
+    e = neg1 << 31 | ((c1 & 1) * 8 + c2) << 24 | neg2 << 23 | address bits,
 
-(c1, c2 = bucket mod 8 in chunks t1, t2; terminator combo field = 64): one
-tile load feeds two buckets, and the chain runs over the 64 combos.
+(c1, c2 = bucket mod 8 in chunks t1, t2; terminator combo field = 16): one tile
+load feeds two buckets, and the chain runs over 16 combos.  Accumulators: the
+warp's two t1 buckets in acc[.][0..1] (complete), chunk t2's 8 buckets in
+acc[.][2..9] (partial over the quarter; the kernel folds the four warps).
 
 Usage: python tools/gen_consumers.py > paper_2302_01977_b200/csrc/hsk_sjlt_pipe.cuh
 """
@@ -130,7 +133,7 @@ def gen(rpt, db, trans):
 
 def gen_pair(trans):
     """RPT = 2 rows per lane, 16 buckets = two chunks of 8 (see the docstring)."""
-    rpt, nacc = 2, 32
+    rpt, nacc = 2, 20
     L = []
     a = L.append
     sen, base = nacc, nacc + 1
@@ -160,15 +163,15 @@ def gen_pair(trans):
     L.extend(load_tile())
     a("and.b32 k, e, 2130706432;")
     a("ld.shared.b32 e, [pe+4];")
-    for cc in range(64):
-        nxt = f"T{cc + 1}" if cc + 1 < 64 else "DONE"
+    for cc in range(16):
+        nxt = f"T{cc + 1}" if cc + 1 < 16 else "DONE"
         c1, c2 = cc // 8, cc % 8
         a(f"T{cc}:")
         a(f"setp.ne.u32 q, k, {cc << 24};")
         a(f"@q bra.uni {nxt};")
         a(f"S{cc}:")
         for r in range(rpt):
-            k1, k2 = c1 * rpt + r, (8 + c2) * rpt + r
+            k1, k2 = c1 * rpt + r, (2 + c2) * rpt + r
             a(f"fma.rn.f64 %{k1}, u{r}, g, %{k1};")
             a(f"fma.rn.f64 %{k2}, u{r}, g2, %{k2};")
         L.extend(load_tile())
