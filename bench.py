@@ -262,14 +262,95 @@ def run_rowshard(args):
         dist.destroy_process_group()
 
 
+def run_adaptive(args):
+    """Opt-in (--workload c3_adaptive): BASELINE.json configs[2] on one GPU per rank.
+
+    A = 1/(1+|i-j|) + 0.1 sin(i+2j)/n, n = 65536 (34.4 GB, generated in HBM);
+    one step = the whole adaptive schedule through adaptive.DeviceSketch:
+    start with a d = 64 SJLT block (alpha = 8, block construction), then 15
+    append_columns increments of 64 (SeedSequence((0, i))), each extending
+    S = A R^T and S' = A^T R^T in place (32 products, 1.10 TB of A streamed).
+    Operator draws (host numpy, the reference's own) and their device plans
+    are made before the timed region; device time on the default stream
+    between CUDA events, max over ranks (weak: every rank its own A)."""
+    import torch
+    import torch.distributed as dist
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    from paper_2302_01977_b200 import _lib, adaptive, device, matgen
+    from paper_2302_01977_b200 import sketching as sk
+    _lib.load()
+    n, dd, incs, alpha = 65536, 64, 16, 8
+    A = matgen.toeplitz_sin(n)
+    ops = [sk.new_operator(sk.SJLT, n, dd, np.random.SeedSequence((0, 0)), alpha=alpha,
+                           construction=sk.BLOCK)]
+    for i in range(1, incs):
+        ops.append(sk.append_columns(ops[-1], dd, np.random.SeedSequence((0, i))))
+    for b in ops[-1].blocks:
+        device.block_state(b)
+    ds = adaptive.DeviceSketch(A, dd * incs)
+    stream = torch.cuda.current_stream()
+
+    def step():
+        ds.start(ops[0])
+        for op in ops[1:]:
+            ds.extend(op)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(args.steps):
+        step()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / args.steps
+    if world > 1:
+        t = torch.tensor([ms], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    a_bytes = 8 * n * n
+    per_launch = a_bytes + 8 * n * dd
+    launches = 2 * incs
+    peak, _ = _peaks()
+    ach = launches * per_launch / (ms * 1e-3) / 1e9
+    line = {
+        "metric": "adaptive SJLT sketch (S and S' per 64-column increment): A-streamed GB/s",
+        "value": world * launches * a_bytes / (ms * 1e-3) / 1e9, "unit": "GB/s",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic",
+        "config": {"workload": "c3_adaptive", "n": n, "d_final": dd * incs, "dd": dd,
+                   "alpha": alpha, "construction": "block", "matrix": "toeplitz-sine",
+                   "products_per_step": launches, "parallelism": f"replica{world}",
+                   "l2": "inputs larger than L2 (34.4 GB A)"},
+        "roofline": {"bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s",
+                     "frac": ach / peak, "algorithmic_bytes_per_launch": per_launch},
+        "gpu_launches": launches * args.steps,
+    }
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=400)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--workload", default="c2_sjlt_S", choices=["c2_sjlt_S", "c5_rowshard"],
-                    help="c5_rowshard: opt-in multi-GPU S/S' exchange leg (not the headline)")
+    ap.add_argument("--workload", default="c2_sjlt_S", choices=["c2_sjlt_S", "c5_rowshard", "c3_adaptive"],
+                    help="c5_rowshard: opt-in multi-GPU S/S' exchange leg; c3_adaptive: opt-in "
+                         "adaptive schedule (BASELINE configs[2]); neither is the headline")
     ap.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline leg")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
@@ -278,6 +359,9 @@ def main():
         return
     if args.workload == "c5_rowshard":
         run_rowshard(args)
+        return
+    if args.workload == "c3_adaptive":
+        run_adaptive(args)
         return
 
     import torch
