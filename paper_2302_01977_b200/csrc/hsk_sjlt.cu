@@ -303,20 +303,55 @@ __global__ void sjlt_plan_kernel(const int32_t *__restrict__ pos, const int8_t *
     // padding after the last terminator (the walk loads, never uses, one word
     // past a terminator): null words
     for (int64_t e = cnt + ngroups + threadIdx.x; e < estride; e += blockDim.x) e_out[e] = 0u;
+    // paired S' plans on TMA-landed tiles (tm_t > 0): within each (warp,
+    // combo) run, entries of opposite input parity are emitted as adjacent
+    // pairs (head word flagged, bit 29) ahead of the run's singles: the walker
+    // reads a pair's two entries in one set of conflict-free loads (the
+    // 8-byte half of a tile word is the index parity; see pipe_t_pair)
+    const bool parity = pair && tm_t > 0;
+    uint32_t *tw = keys + p2;  // parity: words in sorted order
     for (int e = threadIdx.x; e < cnt; e += blockDim.x) {
         const uint32_t key = keys[e];
         if (pair) {
             const uint32_t grp = key >> 14, kk = key & 255u, combo = (key >> 8) & 63u;
             const int pg = (int)((grp >> 4) * 4 + ((grp >> 2) & 3));
             const int64_t q = q0 + (int64_t)kk * alpha + 2 * pg;
-            e_out[e + grp] = (sgn[q] < 0 ? 0x80000000u : 0u) | (combo << 24) |
-                             (sgn[q + 1] < 0 ? 0x00800000u : 0u) | entry_addr(kk, tm_t);
+            const uint32_t w = (sgn[q] < 0 ? 0x80000000u : 0u) | (combo << 24) |
+                               (sgn[q + 1] < 0 ? 0x00800000u : 0u) | entry_addr(kk, tm_t);
+            if (parity) tw[e] = w;
+            else e_out[e + grp] = w;
             continue;
         }
         const uint32_t b = key >> 12;
         const int local = key & 4095;
         e_out[e + b / (uint32_t)db] = (sgn[q0 + local] < 0 ? 0x80000000u : 0u) | ((b % (uint32_t)db) << 24) |
                                       entry_addr((uint32_t)(local / alpha), tm_t);
+    }
+    if (parity) {
+        __syncthreads();
+        // one thread per run start: pairs (even, odd) first, then the rest
+        for (int e = threadIdx.x; e < cnt; e += blockDim.x) {
+            const uint32_t run = keys[e] >> 8;
+            if (e > 0 && (keys[e - 1] >> 8) == run) continue;
+            int end = e + 1;
+            while (end < cnt && (keys[end] >> 8) == run) ++end;
+            uint32_t *o = e_out + e + (run >> 6);  // + one terminator per earlier group
+            int ie = e, io = e, w = 0;
+            auto next_par = [&](int i, uint32_t par) {
+                while (i < end && (keys[i] & 1u) != par) ++i;
+                return i;
+            };
+            ie = next_par(ie, 0u);
+            io = next_par(io, 1u);
+            while (ie < end && io < end) {
+                o[w++] = tw[ie] | (1u << 29);
+                o[w++] = tw[io];
+                ie = next_par(ie + 1, 0u);
+                io = next_par(io + 1, 1u);
+            }
+            for (; ie < end; ie = next_par(ie + 1, 0u)) o[w++] = tw[ie];
+            for (; io < end; io = next_par(io + 1, 1u)) o[w++] = tw[io];
+        }
     }
     uint32_t *g_out = gptr + c * gstride;
     for (int64_t g = threadIdx.x; g < gstride; g += blockDim.x) {
@@ -1149,7 +1184,7 @@ extern "C" int hsk_sjlt_plan_build_ex(const int32_t *pos, const int8_t *sgn, int
         for (const sjlt::Geom *g : {&pl.s, &pl.t}) {
             int p2 = 1;
             while (p2 < g->tk * (g->pair ? alpha / 2 : alpha)) p2 <<= 1;
-            sjlt::sjlt_plan_kernel<<<(unsigned)g->nchunks, 256, p2 * sizeof(uint32_t), st>>>(
+            sjlt::sjlt_plan_kernel<<<(unsigned)g->nchunks, 256, 2 * p2 * sizeof(uint32_t), st>>>(
                 pos, sgn, n, d, alpha, g->tk, p2, g->db, g->ngroups, g->gstride, g->estride,
                 g == &pl.t ? (g->rpt == 4 ? -g->tm : g->tm) : 0, g->pair,
                 reinterpret_cast<uint32_t *>(base + g->gptr_off),

@@ -194,6 +194,120 @@ def gen_pair(trans):
             f'                 : "memory");\n}}\n')
 
 
+def gen_pair_t():
+    """Paired S' walker on TMA-landed tiles with parity pairs.
+
+    A combo's entries come as (even, odd) input-index pairs -- head word
+    flagged with bit 29 -- followed by the leftover singles.  In a pair
+    iteration lanes with (lane & 8) == 0 load entry a for their rows and
+    lanes with (lane & 8) != 0 entry b, then the other way round: each
+    half-warp's 64-bit loads cover 8 rows at an even index and 8 at an odd
+    one, i.e. all 16 bank pairs (a single entry's loads are 2-way
+    conflicted: the tile's 128-byte swizzle cannot move an element's 8-byte
+    half).  Singles walk as in pipe_t_pair.  Registers: h = the current
+    item's head word; the pair loop prefetches the next two words (E2, F2);
+    entering a pair loop from the chain, or leaving it for singles, issues
+    that item's loads without the one-iteration lead (once per combo)."""
+    rpt, nacc = 2, 20
+    L = []
+    a = L.append
+    sen, base, lane8, sgs = nacc, nacc + 1, nacc + 2, nacc + 3
+    PF = 1 << 29
+    a(".reg .pred q, lo;")
+    a(".reg .b32 pe, t, t2, ad, e, k, gh, gh2, gy, gy2, zero, one, h, wa, wb, wx, wy, E2, F2;")
+    a(".reg .f64 u0, u1, v0, v1, g, g2, gx, gx2;")
+    a("mov.b32 zero, 0;")
+    a("mov.b32 one, 1072693248;")
+    a("mov.u32 t, %laneid;")
+    a("and.b32 t, t, 8;")
+    a("setp.eq.u32 lo, t, 0;")
+
+    def signs(w, hi, hi2, d1, d2):
+        return [f"lop3.b32 {hi}, {w}, -2147483648, one, 0xEA;", f"mov.b64 {d1}, {{zero, {hi}}};",
+                f"shl.b32 t2, {w}, 8;", f"lop3.b32 {hi2}, t2, -2147483648, one, 0xEA;",
+                f"mov.b64 {d2}, {{zero, {hi2}}};"]
+
+    def load_single():  # from e: rows l, l + 32 of entry e
+        out = [f"lop3.b32 ad, e, %{lane8}, 8388607, 0x28;", f"add.u32 ad, ad, %{base};",
+               "ld.shared.f64 u0, [ad];", "ld.shared.f64 u1, [ad+4096];"]
+        return out + signs("e", "gh", "gh2", "g", "g2")
+
+    def load_pair():  # from (wa, wb): X = own half's entry, Y = the other
+        out = ["selp.b32 wx, wa, wb, lo;", "selp.b32 wy, wb, wa, lo;",
+               f"lop3.b32 ad, wx, %{lane8}, 8388607, 0x28;", f"add.u32 ad, ad, %{base};",
+               "ld.shared.f64 u0, [ad];", "ld.shared.f64 u1, [ad+4096];",
+               f"lop3.b32 ad, wy, %{lane8}, 8388607, 0x28;", f"add.u32 ad, ad, %{base};",
+               "ld.shared.f64 v0, [ad];", "ld.shared.f64 v1, [ad+4096];"]
+        return out + signs("wx", "gh", "gh2", "g", "g2") + signs("wy", "gy", "gy2", "gx", "gx2")
+
+    def fma(c1, c2, u, gg, gg2):
+        out = []
+        for r in range(rpt):
+            k1, k2 = c1 * rpt + r, (2 + c2) * rpt + r
+            out += [f"fma.rn.f64 %{k1}, {u}{r}, {gg}, %{k1};", f"fma.rn.f64 %{k2}, {u}{r}, {gg2}, %{k2};"]
+        return out
+
+    a(f"ld.shared.b32 t, [%{sgs}];")
+    a(f"mad.lo.u32 pe, t, 4, %{sen};")
+    a("ld.shared.b32 e, [pe];")
+    a("mov.b32 h, e;")
+    L.extend(load_single())
+    a("and.b32 k, e, 2130706432;")
+    a("ld.shared.b32 e, [pe+4];")
+    for cc in range(16):
+        nxt = f"T{cc + 1}" if cc + 1 < 16 else "DONE"
+        c1, c2 = cc // 8, cc % 8
+        a(f"T{cc}:")
+        a(f"setp.ne.u32 q, k, {(cc << 24) | PF};")
+        a(f"@q bra.uni U{cc};")
+        # pair entry: head h at pe, second word e
+        a("mov.b32 wa, h;")
+        a("mov.b32 wb, e;")
+        L.extend(load_pair())
+        a("ld.shared.b32 E2, [pe+8];")
+        a("ld.shared.b32 F2, [pe+12];")
+        a(f"P{cc}:")
+        L.extend(fma(c1, c2, "u", "g", "g2"))
+        L.extend(fma(c1, c2, "v", "gx", "gx2"))
+        a("mov.b32 wa, E2;")
+        a("mov.b32 wb, F2;")
+        a("and.b32 k, wa, 2130706432;")
+        a("add.u32 pe, pe, 8;")
+        a(f"setp.ne.u32 q, k, {(cc << 24) | PF};")
+        a(f"@q bra.uni X{cc};")
+        L.extend(load_pair())
+        a("ld.shared.b32 E2, [pe+8];")
+        a("ld.shared.b32 F2, [pe+12];")
+        a(f"bra.uni P{cc};")
+        a(f"X{cc}:")  # next item (head wa at pe) is not a pair of this combo
+        a("mov.b32 h, wa;")
+        a("mov.b32 e, wa;")
+        L.extend(load_single())
+        a("mov.b32 e, wb;")
+        a(f"U{cc}:")
+        a(f"setp.ne.u32 q, k, {cc << 24};")
+        a(f"@q bra.uni {nxt};")
+        a(f"S{cc}:")
+        L.extend(fma(c1, c2, "u", "g", "g2"))
+        a("mov.b32 h, e;")
+        L.extend(load_single())
+        a("and.b32 k, e, 2130706432;")
+        a("add.u32 pe, pe, 4;")
+        a("ld.shared.b32 e, [pe+4];")
+        a(f"setp.eq.u32 q, k, {cc << 24};")
+        a(f"@q bra.uni S{cc};")
+    a("DONE:")
+    txt = "\\n\\t".join(L)
+    outs = ", ".join(f'"+d"(acc[{k % rpt}][{k // rpt}])' for k in range(nacc))
+    ins = ['"r"(sen)', '"r"(base)', '"r"(lanex)', '"r"(sgs)']
+    return (f"__device__ __forceinline__ void pipe_t_pair(double (&acc)[{rpt}][16], uint32_t sen, "
+            f"uint32_t base, uint32_t lanex, uint32_t sgs) {{\n"
+            f'    asm volatile("{{\\n\\t{txt}\\n\\t}}"\n'
+            f"                 : {outs}\n"
+            f"                 : {', '.join(ins)}\n"
+            f'                 : "memory");\n}}\n')
+
+
 def main():
     out = ["// GENERATED by tools/gen_consumers.py -- do not edit by hand.",
            "// Software-pipelined whole-chunk SJLT walkers (state-tagged entries); see the generator.",
@@ -203,7 +317,7 @@ def main():
     for rpt, db in T_CONFIGS:
         out.append(gen(rpt, db, True))
     out.append(gen_pair(False))
-    out.append(gen_pair(True))
+    out.append(gen_pair_t())
     sys.stdout.write("\n".join(out))
 
 
