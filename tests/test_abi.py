@@ -50,6 +50,19 @@ def test_plan_bytes_is_host_only_and_validates():
     assert lib.hsk_sjlt_plan_bytes(4096, 256, 0) == _lib.HSK_EINVAL
 
 
+def test_chunked_plan_flag():
+    """HSK_SJLT_CHUNKED changes the plan only for the paired shapes (d/alpha
+    = 8, d a multiple of 64); unknown flags are rejected on the host."""
+    lib = _lib.load()
+    assert lib.hsk_sjlt_plan_bytes_ex(16384, 512, 4, 1) == lib.hsk_sjlt_plan_bytes(16384, 512, 4)
+    assert lib.hsk_sjlt_plan_bytes_ex(65536, 64, 8, 0) == lib.hsk_sjlt_plan_bytes(65536, 64, 8)
+    paired = lib.hsk_sjlt_plan_bytes_ex(65536, 64, 8, 1)
+    assert 0 < paired < lib.hsk_sjlt_plan_bytes(65536, 64, 8)  # alpha/2 entries per index
+    assert lib.hsk_sjlt_plan_bytes_ex(65536, 64, 8, 2) == _lib.HSK_EINVAL
+    rc = lib.hsk_sjlt_apply_ex(None, 5, 12, 5, 0, None, 12, 64, 8, 4, 0.5, None, 5, 0, None)
+    assert rc == _lib.HSK_EINVAL and "unknown flags" in _lib.last_error()
+
+
 def test_apply_dimension_mismatch_is_einval():
     lib = _lib.load()
     # S = A R^T needs cols == n: 10 columns vs an operator over 12
