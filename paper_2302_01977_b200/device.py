@@ -169,13 +169,20 @@ class _SjltState:
 HSK_SJLT_CHUNKED = 1  # include/hsk.h
 
 
-def sjlt_chunked(pos: np.ndarray, d: int, alpha: int) -> bool:
-    """The block construction's chunk property (sketching.py:246-250): entry t
-    of every input index lies in chunk t of d/alpha buckets.  Checked on the
-    pattern itself (from_pattern blocks qualify too); HSK_SJLT_NOCHUNK=1 turns
-    the paired plan off (A/B runs)."""
-    if os.environ.get("HSK_SJLT_NOCHUNK") == "1" or d % alpha or pos.size == 0:
+def sjlt_chunked(pos: np.ndarray, d: int, alpha: int, construction=None) -> bool:
+    """Whether to build the paired plan: only for the shapes it serves (d/alpha
+    = 8, d a multiple of 64; include/hsk.h), and only for patterns with the
+    block construction's chunk property (sketching.py:246-250: entry t of
+    every input index in chunk t of d/alpha buckets) -- guaranteed by the
+    reference's block construction, checked on the pattern otherwise
+    (from_pattern blocks qualify too).  HSK_SJLT_NOCHUNK=1 turns it off (A/B
+    runs)."""
+    if os.environ.get("HSK_SJLT_NOCHUNK") == "1" or pos.size == 0:
         return False
+    if d % 64 or alpha * 8 != d:
+        return False
+    if construction == "block":
+        return True
     return bool((pos // (d // alpha) == np.arange(alpha, dtype=pos.dtype)).all())
 
 
@@ -218,7 +225,8 @@ def block_state(block):
         st.sgn = torch.from_numpy(np.ascontiguousarray(block._signs, dtype=np.int8).reshape(-1)).to(dev)
         st.n, st.d, st.alpha = n, d, alpha
         st.scale = float(block._scale)
-        st.flags = HSK_SJLT_CHUNKED if sjlt_chunked(pos, d, alpha) else 0
+        chunked = sjlt_chunked(pos, d, alpha, getattr(block, "construction", None))
+        st.flags = HSK_SJLT_CHUNKED if chunked else 0
         nbytes = _lib.load().hsk_sjlt_plan_bytes_ex(n, d, alpha, st.flags)
         _lib.check(nbytes, "hsk_sjlt_plan_bytes_ex")
         st.plan = torch.empty(int(nbytes), dtype=torch.uint8, device=dev)

@@ -92,3 +92,19 @@ def test_oracle_library_exports():
                  "oracle_fwht", "oracle_reduceat_segment"):
         assert hasattr(lib, name)
     assert isinstance(lib, ctypes.CDLL)
+
+
+def test_chunked_flag_host_rule():
+    """device.sjlt_chunked: only the paired shapes, trusted for the reference's
+    block construction, checked on the pattern otherwise."""
+    import numpy as np
+    from paper_2302_01977_b200 import device, operators
+    blk = operators.new_operator("sjlt", 300, 64, seed=1, alpha=8, construction="block").blocks[0]
+    pos = np.asarray(blk._pos)
+    assert device.sjlt_chunked(pos, 64, 8, "block")
+    assert device.sjlt_chunked(pos, 64, 8, None)
+    bad = pos.copy()
+    bad[5, [0, 1]] = bad[5, [1, 0]]
+    assert not device.sjlt_chunked(bad, 64, 8, "graph")
+    b2 = operators.new_operator("sjlt", 600, 512, seed=1, alpha=4, construction="block").blocks[0]
+    assert not device.sjlt_chunked(np.asarray(b2._pos), 512, 4, "block")  # not a paired shape
