@@ -111,6 +111,18 @@ def main():
                 byt = n * n * 8 + n * 64 * 8
                 out[f"c3_{'St' if tr else 'S'}"] = {"ms": ms, "GBs": byt / ms / 1e6,
                                                     "frac": byt / ms / 1e6 / PEAK}
+        elif c == "c3a4":  # C3's matrix with the paper's default alpha = 4 increments of 64
+            n = 65536
+            A = mat(n, kind="toep")
+            op = sk.new_operator(sk.SJLT, n, 64, np.random.SeedSequence((0, 5)), alpha=4,
+                                 construction="block")
+            blk = op.blocks[0]
+            S = device.DeviceMatrix.empty(n, 64)
+            for tr in (False, True):
+                ms = timeit(lambda: device.apply_block(blk, A, tr, S, 0), max(3, args.reps // 4))
+                byt = n * n * 8 + n * 64 * 8
+                out[f"c3a4_{'St' if tr else 'S'}"] = {"ms": ms, "GBs": byt / ms / 1e6,
+                                                      "frac": byt / ms / 1e6 / PEAK}
         elif c == "c4":
             n = 65536
             A = mat(n, 8, 0.25)
