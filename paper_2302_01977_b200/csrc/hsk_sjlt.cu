@@ -22,6 +22,9 @@
 //    LDS.128 (RPT = 2) of the staged A tile, RPT DFMAs with +-1 (exactly the
 //    reference's add/subtract, one rounding each; no data multiplies).  The
 //    walk over a warp's entries is software-pipelined (tools/gen_consumers.py).
+//  * Paired plans (HSK_SJLT_CHUNKED, block construction with d/alpha = 8):
+//    one entry carries an index's buckets in two construction chunks, so
+//    each tile element is read alpha/2 times instead of alpha (geom_dir).
 //  * Streaming.  A producer warp moves TK x TM tiles of A (every element
 //    read once from HBM) plus the chunk's plan slice into a STAGES-deep
 //    shared-memory ring: one TMA 2-D tile load (UTMALDG, OOB zero-filled)
