@@ -84,9 +84,10 @@ HSK_API int hsk_sjlt_plan_build(const int32_t *pos, const int8_t *sgn, int64_t n
  * With d/alpha = 8 and d a multiple of 64 (C3: alpha = 8 increments of 64) the
  * plan pairs the chunks: one consumer warp owns two chunks and reads each
  * element once for both (alpha/2 tile reads per element instead of alpha).
- * Other shapes ignore the flag.  The caller guarantees the chunk property
- * (the plan kernel flags violations, the host checks before passing it);
- * plan_bytes / plan_build / apply must all get the same flags. */
+ * Other shapes ignore the flag.  For paired shapes plan_build verifies the
+ * chunk property on the device and returns HSK_EINVAL if it fails (it then
+ * synchronises `stream` once); plan_bytes / plan_build / apply must all get
+ * the same flags. */
 #define HSK_SJLT_CHUNKED 1
 HSK_API int64_t hsk_sjlt_plan_bytes_ex(int64_t n, int32_t d, int32_t alpha, int32_t flags);
 HSK_API int hsk_sjlt_plan_build_ex(const int32_t *pos, const int8_t *sgn, int64_t n, int32_t d,

@@ -1194,6 +1194,17 @@ extern "C" int hsk_sjlt_plan_build_ex(const int32_t *pos, const int8_t *sgn, int
                 reinterpret_cast<uint32_t *>(base + g->ent_off), reinterpret_cast<int *>(base + 28));
             HSK_CHECK_LAUNCH("sjlt_plan_kernel");
         }
+        if (pl.s.pair) {
+            // paired plans rely on the chunk property: read the plan kernel's
+            // violation flag back (one stream sync, once per operator block)
+            int err = 0;
+            e = cudaMemcpyAsync(&err, base + 28, sizeof(int), cudaMemcpyDeviceToHost, st);
+            if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+            if (e != cudaSuccess) return cuda_status(e, "sjlt plan: check");
+            if (err & 2)
+                return set_error(HSK_EINVAL, "sjlt plan: HSK_SJLT_CHUNKED given for a pattern whose "
+                                             "entry t is not in chunk t of d/alpha buckets");
+        }
     }
     return HSK_OK;
 }

@@ -346,6 +346,15 @@ def test_sjlt_chunk_property_detection(cuda):
     A = np.random.default_rng(1).standard_normal((90, n))
     for b in (g, bad):
         assert device.block_state(b).flags == 0
+    # the C ABI refuses HSK_SJLT_CHUNKED for a pattern without the property
+    import torch
+    from paper_2302_01977_b200 import _lib
+    st = device.block_state(bad)
+    nb = _lib.load().hsk_sjlt_plan_bytes_ex(n, d, alpha, device.HSK_SJLT_CHUNKED)
+    plan = torch.empty(int(nb), dtype=torch.uint8, device="cuda")
+    with pytest.raises(ValueError, match="chunk"):
+        _lib.call("hsk_sjlt_plan_build_ex", st.pos.data_ptr(), st.sgn.data_ptr(), n, d, alpha,
+                  device.HSK_SJLT_CHUNKED, plan.data_ptr(), int(nb), device.current_stream_ptr())
     for b in (g, bad, good):
         op = sk.SketchOperator(sk.SJLT, n, (b,), alpha=alpha)
         ref = O.sjlt_right(A, b._pos, b._signs, d, b._scale)
