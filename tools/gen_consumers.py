@@ -213,7 +213,7 @@ def gen_pair_t():
     a = L.append
     sen, base, lane8, sgs = nacc, nacc + 1, nacc + 2, nacc + 3
     PF = 1 << 29
-    a(".reg .pred q, lo;")
+    a(".reg .pred q, lo, sp;")
     a(".reg .b32 pe, t, t2, ad, e, k, gh, gh2, gy, gy2, zero, one, h, wa, wb, wx, wy, E2, F2;")
     a(".reg .f64 u0, u1, v0, v1, g, g2, gx, gx2;")
     a("mov.b32 zero, 0;")
@@ -228,8 +228,11 @@ def gen_pair_t():
                 f"mov.b64 {d2}, {{zero, {hi2}}};"]
 
     def load_single():  # from e: rows l, l + 32 of entry e
-        out = [f"lop3.b32 ad, e, %{lane8}, 8388607, 0x28;", f"add.u32 ad, ad, %{base};",
-               "ld.shared.f64 u0, [ad];", "ld.shared.f64 u1, [ad+4096];"]
+        # skipped when e heads a pair: the chain then enters that combo's pair
+        # loop, which loads the pair itself (no wasted 2-way-conflicted loads)
+        out = ["and.b32 t, e, 536870912;", "setp.eq.u32 sp, t, 0;",
+               f"lop3.b32 ad, e, %{lane8}, 8388607, 0x28;", f"add.u32 ad, ad, %{base};",
+               "@sp ld.shared.f64 u0, [ad];", "@sp ld.shared.f64 u1, [ad+4096];"]
         return out + signs("e", "gh", "gh2", "g", "g2")
 
     def load_pair():  # from (wa, wb): X = own half's entry, Y = the other
