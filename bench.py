@@ -2,20 +2,34 @@
 """Benchmark of the sketch hot path (BASELINE.json metric) -- one JSON line.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--no-configs] [--no-cpu] [--share-gpu] [--c5-n N5]
 
-Workload (BASELINE.json configs[1], "C2"): A = n x n Gaussian-kernel matrix,
+Headline (BASELINE.json configs[1], "C2"): A = n x n Gaussian-kernel matrix,
 n = 16384, x_i ~ U[0,1]^8 (seed = rank), h = 0.5, +1e-2 on the diagonal,
 generated in HBM (2.15 GB, far larger than the 126 MB L2, so no flush is
 needed between steps).  One STEP = the SJLT sketch S = A R^T with d = 512,
 alpha = 4 (block construction, R drawn by the reference's generator with
 SeedSequence((0, 0))), i.e. one full pass over A.  `value` is the A-streamed
-GB/s of the whole job (sum over ranks / max-over-ranks time).  The Gaussian
-d = 512 product on the same A (the config's comparison) is reported under
-"gaussian" in FP64 TFLOP/s, next to cuBLAS DGEMM on the same operands.
+GB/s of the whole job (sum over ranks / max-over-ranks time).  Beside it:
+S' on the same A, the Gaussian d = 512 product (FP64 TFLOP/s, next to cuBLAS
+DGEMM on the same operands), a sustained (>= 400 launch) figure, and the end
+to end numbers through the public API from pinned and from pageable host
+arrays.
 
-Multi-GPU (torchrun, one rank per GPU): every rank sketches its own C2
-matrix with the same R -- row-block sharding needs no collective for
-S = A R^T, so this is weak scaling.
+Sub-records under "configs" (the other BASELINE.json configs, N = 1 only
+unless noted): c1 (n = 4096 S and S', graph R, L2 flushed between launches),
+c3_adaptive (the whole 16-increment S + S' schedule of configs[2]),
+c4_srht (configs[3]) and c5 (configs[4], at EVERY N: strong-scaled
+n = 131072 row-sharded over the ranks, S local + S' summed through the p2p
+peer-store exchange, SJLT d = 2048 alpha = 8 and Gaussian d = 512).  Each
+carries ms, its roofline fraction (MEASURED_PEAKS.json) and the CPU-port
+baseline on a bounded slab of the same workload.
+
+Multi-GPU: `--gpus N` without torchrun re-launches itself under
+torch.distributed.run with N ranks (one per GPU; fails if fewer are
+visible); under torchrun WORLD_SIZE must equal --gpus.  `--share-gpu` puts
+every rank on GPU 0 with a gloo group (exercises the multi-rank path on a
+one-GPU box; its timings are not scaling numbers).
 
 --impl reference times the reference algorithm on the host CPU: the C
 restatement in oracle/ (bit-exact with hsskit's SjltBlock.apply_right; the
@@ -26,8 +40,10 @@ on all host cores, one bounded row slab of the same workload per step.
 from __future__ import annotations
 
 import argparse
+import gc
 import json
 import os
+import socket
 import statistics
 import subprocess
 import sys
@@ -127,6 +143,7 @@ class ClockSampler:
             except ValueError:
                 return None
         sm = [num(p[1]) for p in win if num(p[1]) is not None]
+        pw = [num(p[3]) for p in win if num(p[3]) is not None]
         reasons = set()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         for p in win:
@@ -135,6 +152,7 @@ class ClockSampler:
                     reasons.add(name)
         return {"sm_mhz": statistics.median(sm) if sm else None,
                 "sm_max_mhz": num(win[0][2]), "reasons": sorted(reasons),
+                "power_w_max": max(pw) if pw else None,
                 "samples": len(win), "source": src}
 
 
@@ -190,193 +208,116 @@ def run_reference(args):
     print(json.dumps(line), flush=True)
 
 
-# --------------------------------------------------------------------- ours
+# ------------------------------------------------------------- rank setup
 
-def run_rowshard(args):
-    """Opt-in (--workload c5_rowshard): BASELINE.json C5 shape, weak-scaled.
+class Ctx:
+    """Rank, world, device and process group of this bench process."""
 
-    Global A is the (16384*world)^2 Gaussian-kernel matrix (x_i ~ U[0,1]^16,
-    h = 1.0 -- configs c5_sjlt); rank g holds rows [16384 g, 16384 (g+1)),
-    i.e. 16384 x 131072 per GPU at world 8, exactly C5's shard.  One step =
-    S rows (local, no communication) + S' rows through the p2p transport
-    (kernel epilogues store into peers' CUDA-IPC receive slots, then a
-    rank-ordered local sum), SJLT d = 2048, alpha = 8.  Device time on the
-    default stream between events, max over ranks.
-    """
+    def __init__(self, args):
+        import torch
+        import torch.distributed as dist
+        self.world = int(os.environ.get("WORLD_SIZE", "1"))
+        self.rank = int(os.environ.get("RANK", "0"))
+        self.local = int(os.environ.get("LOCAL_RANK", "0"))
+        if self.world != args.gpus:
+            raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={self.world}")
+        if not torch.cuda.is_available():
+            raise SystemExit("bench.py: no CUDA device visible")
+        self.share = args.share_gpu
+        self.dev_index = 0 if self.share else self.local
+        if not self.share and torch.cuda.device_count() <= self.local:
+            raise SystemExit(f"bench.py: rank {self.rank} needs GPU {self.local}, "
+                             f"{torch.cuda.device_count()} visible")
+        torch.cuda.set_device(self.dev_index)
+        self.group = None
+        if self.world > 1:
+            if self.share:
+                dist.init_process_group("gloo")
+            else:
+                dist.init_process_group("nccl", device_id=torch.device("cuda", self.local))
+        self.dist = dist if self.world > 1 else None
+
+    def barrier(self):
+        if self.dist is not None:
+            self.dist.barrier()
+
+    def max_over_ranks(self, values):
+        """Element-wise max of a list of floats over all ranks."""
+        import torch
+        if self.dist is None:
+            return list(values)
+        t = torch.tensor(list(values), dtype=torch.float64,
+                         device="cpu" if self.share else "cuda")
+        self.dist.all_reduce(t, op=self.dist.ReduceOp.MAX)
+        return [float(v) for v in t.tolist()]
+
+    def close(self):
+        if self.dist is not None:
+            self.dist.barrier()
+            self.dist.destroy_process_group()
+
+
+def _free():
     import torch
-    import torch.distributed as dist
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
-    torch.cuda.set_device(local)
-    if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    from paper_2302_01977_b200 import _lib, distributed as hd, matgen
-    from paper_2302_01977_b200 import sketching as sk
-    _lib.load()
-    rows, d, alpha = N, 2048, 8
-    n_glob = rows * world
-    pts = matgen.kernel_points(n_glob, 16, 0)
-    A = matgen.gaussian_kernel(n_glob, 16, 1.0, 1e-2, row0=rank * rows, nrows=rows, points=pts)
-    op = sk.new_operator(sk.SJLT, n_glob, d, np.random.SeedSequence((0, 0)), alpha=alpha,
-                         construction=sk.BLOCK)
-    stream = torch.cuda.current_stream()
-
-    def step():
-        return hd.sketch_row_sharded(A, op, rank=rank, world=world, n_rows=n_glob,
-                                     transport="p2p")
-
-    for _ in range(args.warmup):
-        step()
+    gc.collect()
     torch.cuda.synchronize()
-    if world > 1:
-        dist.barrier()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record(stream)
-    for _ in range(args.steps):
-        step()
-    e1.record(stream)
-    torch.cuda.synchronize()
-    ms = e0.elapsed_time(e1) / args.steps
-    if world > 1:
-        t = torch.tensor([ms], device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t.item())
-    a_bytes = rows * n_glob * 8 * world
-    line = {
-        "metric": "row-sharded S and S' (p2p): A-streamed GB/s, 2 passes per step",
-        "value": 2 * a_bytes / (ms * 1e-3) / 1e9, "unit": "GB/s", "n_gpus": world,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic",
-        "config": {"workload": "c5_rowshard", "n": n_glob, "rows_per_gpu": rows, "d": d,
-                   "alpha": alpha, "construction": "block",
-                   "matrix": "gaussian kernel 16-D h=1.0", "transport": "p2p",
-                   "parallelism": f"rowshard{world}"},
-    }
-    if rank == 0:
-        print(json.dumps(line), flush=True)
-    hd.release_peer_slots()
-    if world > 1:
-        dist.barrier()
-        dist.destroy_process_group()
+    torch.cuda.empty_cache()
 
 
-def run_adaptive(args):
-    """Opt-in (--workload c3_adaptive): BASELINE.json configs[2] on one GPU per rank.
-
-    A = 1/(1+|i-j|) + 0.1 sin(i+2j)/n, n = 65536 (34.4 GB, generated in HBM);
-    one step = the whole adaptive schedule through adaptive.DeviceSketch:
-    start with a d = 64 SJLT block (alpha = 8, block construction), then 15
-    append_columns increments of 64 (SeedSequence((0, i))), each extending
-    S = A R^T and S' = A^T R^T in place (32 products, 1.10 TB of A streamed).
-    Operator draws (host numpy, the reference's own) and their device plans
-    are made before the timed region; device time on the default stream
-    between CUDA events, max over ranks (weak: every rank its own A)."""
+def _events(n):
     import torch
-    import torch.distributed as dist
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
-    torch.cuda.set_device(local)
-    if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    from paper_2302_01977_b200 import _lib, adaptive, device, matgen
-    from paper_2302_01977_b200 import sketching as sk
-    _lib.load()
-    n, dd, incs, alpha = 65536, 64, 16, 8
-    A = matgen.toeplitz_sin(n)
-    ops = [sk.new_operator(sk.SJLT, n, dd, np.random.SeedSequence((0, 0)), alpha=alpha,
-                           construction=sk.BLOCK)]
-    for i in range(1, incs):
-        ops.append(sk.append_columns(ops[-1], dd, np.random.SeedSequence((0, i))))
-    for b in ops[-1].blocks:
-        device.block_state(b)
-    ds = adaptive.DeviceSketch(A, dd * incs)
-    stream = torch.cuda.current_stream()
-
-    def step():
-        ds.start(ops[0])
-        for op in ops[1:]:
-            ds.extend(op)
-
-    for _ in range(args.warmup):
-        step()
-    torch.cuda.synchronize()
-    if world > 1:
-        dist.barrier()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record(stream)
-    for _ in range(args.steps):
-        step()
-    e1.record(stream)
-    torch.cuda.synchronize()
-    ms = e0.elapsed_time(e1) / args.steps
-    if world > 1:
-        t = torch.tensor([ms], device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t.item())
-    a_bytes = 8 * n * n
-    per_launch = a_bytes + 8 * n * dd
-    launches = 2 * incs
-    peak, _ = _peaks()
-    ach = launches * per_launch / (ms * 1e-3) / 1e9
-    line = {
-        "metric": "adaptive SJLT sketch (S and S' per 64-column increment): A-streamed GB/s",
-        "value": world * launches * a_bytes / (ms * 1e-3) / 1e9, "unit": "GB/s",
-        "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic",
-        "config": {"workload": "c3_adaptive", "n": n, "d_final": dd * incs, "dd": dd,
-                   "alpha": alpha, "construction": "block", "matrix": "toeplitz-sine",
-                   "products_per_step": launches, "parallelism": f"replica{world}",
-                   "l2": "inputs larger than L2 (34.4 GB A)"},
-        "roofline": {"bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s",
-                     "frac": ach / peak, "algorithmic_bytes_per_launch": per_launch},
-        "gpu_launches": launches * args.steps,
-    }
-    if rank == 0:
-        print(json.dumps(line), flush=True)
-    if world > 1:
-        dist.barrier()
-        dist.destroy_process_group()
+    return [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+            for _ in range(n)]
 
 
-def main():
-    ap = argparse.ArgumentParser()
-    ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=400)
-    ap.add_argument("--warmup", type=int, default=5)
-    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--workload", default="c2_sjlt_S", choices=["c2_sjlt_S", "c5_rowshard", "c3_adaptive"],
-                    help="c5_rowshard: opt-in multi-GPU S/S' exchange leg; c3_adaptive: opt-in "
-                         "adaptive schedule (BASELINE configs[2]); neither is the headline")
-    ap.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline leg")
-    args = ap.parse_args()
-    args.warmup = max(args.warmup, 3)
-    if args.impl == "reference":
-        run_reference(args)
-        return
-    if args.workload == "c5_rowshard":
-        run_rowshard(args)
-        return
-    if args.workload == "c3_adaptive":
-        run_adaptive(args)
-        return
-
+def time_launches(fn, reps: int, warmup: int, stream, flush=None):
+    """Average device ms per call of fn over `reps` calls, each bracketed by
+    CUDA events on `stream` (an optional L2 flush runs between calls, outside
+    the events)."""
     import torch
-    import torch.distributed as dist
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
-    torch.cuda.set_device(local)
-    if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    for _ in range(warmup):
+        fn()
+        if flush is not None:
+            flush()
+    torch.cuda.synchronize()
+    evs = _events(reps)
+    for e0, e1 in evs:
+        e0.record(stream)
+        fn()
+        e1.record(stream)
+        if flush is not None:
+            flush()
+    torch.cuda.synchronize()
+    return statistics.mean(a.elapsed_time(b) for a, b in evs)
 
-    from paper_2302_01977_b200 import _lib, device, matgen
+
+def roofline(bytes_per_launch: float, ms: float, peak: float):
+    ach = bytes_per_launch / (ms * 1e-3) / 1e9
+    return {"bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s", "frac": ach / peak,
+            "algorithmic_bytes_per_launch": int(bytes_per_launch), "avg_launch_ms": ms}
+
+
+def cpu_rate(fn, nbytes: int, budget_s: float = 6.0, min_reps: int = 2):
+    """Host GB/s of fn() streaming nbytes of A per call (median)."""
+    fn()
+    ts = []
+    t_start = time.perf_counter()
+    while len(ts) < min_reps or (time.perf_counter() - t_start < budget_s and len(ts) < 30):
+        t0 = time.perf_counter()
+        fn()
+        ts.append(time.perf_counter() - t0)
+    t = statistics.median(ts)
+    return nbytes / t / 1e9, t, len(ts)
+
+
+# --------------------------------------------------------------- headline
+
+def run_headline(args, ctx, out):
+    import torch
+    from paper_2302_01977_b200 import device, matgen
     from paper_2302_01977_b200 import sketching as sk
-    _lib.load()
 
+    world, rank = ctx.world, ctx.rank
     stream = torch.cuda.current_stream()
     sptr = stream.cuda_stream
     op = sk.new_operator(sk.SJLT, N, D, np.random.SeedSequence((0, 0)), alpha=ALPHA,
@@ -387,8 +328,8 @@ def main():
     device.block_state(blk)
     torch.cuda.synchronize()
 
-    def sjlt(trans=False, out=S):
-        device.apply_block(blk, A, trans, out, 0, sptr)
+    def sjlt(trans=False, o=S):
+        device.apply_block(blk, A, trans, o, 0, sptr)
 
     for _ in range(args.warmup):
         sjlt()
@@ -396,10 +337,8 @@ def main():
 
     sampler = ClockSampler(torch.cuda.current_device()).start()
     time.sleep(0.3)
-    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
-           for _ in range(args.steps)]
-    if world > 1:
-        dist.barrier()
+    evs = _events(args.steps)
+    ctx.barrier()
     torch.cuda.synchronize()
     t_wall0 = time.perf_counter()
     g0 = torch.cuda.Event(enable_timing=True)
@@ -412,17 +351,28 @@ def main():
     g1.record(stream)
     torch.cuda.synchronize()
     t_wall1 = time.perf_counter()
-    if world > 1:
-        dist.barrier()
+    ctx.barrier()
     total_ms = g0.elapsed_time(g1)
     launch_ms = [a.elapsed_time(b) for a, b in evs]
-    if world > 1:
-        t = torch.tensor([total_ms], device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        total_ms = float(t.item())
+    total_ms, = ctx.max_over_ranks([total_ms])
+
+    # sustained: >= 400 back-to-back launches (the board's 1 kW cap engages
+    # within ~100 ms of this kernel; the K-step region above is a burst when K
+    # is small)
+    sus_n = 400
+    sus_evs = _events(sus_n)
+    t_sus0 = time.perf_counter()
+    for e0, e1 in sus_evs:
+        e0.record(stream)
+        sjlt()
+        e1.record(stream)
+    torch.cuda.synchronize()
+    t_sus1 = time.perf_counter()
+    sus_ms = statistics.mean(a.elapsed_time(b) for a, b in sus_evs)
     time.sleep(0.25)
     sampler.stop()
     clocks = sampler.summary(t_wall0, t_wall1)
+    clocks_sus = sampler.summary(t_sus0, t_sus1)
 
     ms_per_step = total_ms / args.steps
     a_bytes = N * N * 8
@@ -430,124 +380,382 @@ def main():
     value = world * a_bytes / (ms_per_step * 1e-3) / 1e9
     avg_launch = statistics.mean(launch_ms)
     peak, peak_src = _peaks()
-    achieved = (a_bytes + s_bytes) / (avg_launch * 1e-3) / 1e9
+    roof = roofline(a_bytes + s_bytes, avg_launch, peak)
+    roof["peak_source"] = peak_src
+    roof["traffic"] = _traffic_from_profiles("sjlt_apply_S")
 
-    # S' = A^T R^T on the same A (secondary, same algorithmic bytes)
+    # S' = A^T R^T on the same A (same algorithmic bytes)
     St = device.DeviceMatrix.empty(N, D)
-    for _ in range(3):
-        sjlt(True, St)
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    reps = max(10, min(args.steps, 100))
-    e0.record(stream)
-    for _ in range(reps):
-        sjlt(True, St)
-    e1.record(stream)
-    torch.cuda.synchronize()
-    st_ms = e0.elapsed_time(e1) / reps
+    st_ms = time_launches(lambda: sjlt(True, St), max(20, min(args.steps, 100)), 3, stream)
 
-    # Gaussian d=512 on the same A (config's comparison) + cuBLAS DGEMM
+    # Gaussian d=512 on the same A (the config's comparison) + cuBLAS DGEMM
     gop = sk.new_operator(sk.GAUSSIAN, N, D, np.random.SeedSequence((0, 0)))
     gblk = gop.blocks[0]
     gst = device.block_state(gblk)
     SG = device.DeviceMatrix.empty(N, D)
-    for _ in range(2):
-        device.apply_block(gblk, A, False, SG, 0, sptr)
-    greps = 5
-    e0.record(stream)
-    for _ in range(greps):
-        device.apply_block(gblk, A, False, SG, 0, sptr)
-    e1.record(stream)
-    torch.cuda.synchronize()
-    g_ms = e0.elapsed_time(e1) / greps
+    g_ms = time_launches(lambda: device.apply_block(gblk, A, False, SG, 0, sptr), 5, 2, stream)
+    gt_ms = time_launches(lambda: device.apply_block(gblk, A, True, SG, 0, sptr), 5, 2, stream)
     flops = 2.0 * N * N * D
     At = A.t[:, :N]               # (cols, rows) = A^T as a row-major tensor
-    for _ in range(2):
-        ref_c = torch.matmul(gst.R, At)   # R A^T = (A R^T)^T, cuBLAS DGEMM
+    holder = {}
+
+    def cublas():
+        holder["c"] = torch.matmul(gst.R, At)   # R A^T = (A R^T)^T, cuBLAS DGEMM
+    cublas_ms = time_launches(cublas, 5, 2, stream)
+    holder.clear()
+    del SG, St
+
+    # end to end through the public API: host A -> H2D -> kernel -> D2H S
+    e2e = e2e_pageable = None
+    host = torch.empty((N, N), dtype=torch.float64, pin_memory=True)
+    host.copy_(A.t[:, :N])
+    A_host = host.numpy().T           # F-ordered view of the pinned buffer
+    e2e_steps = max(3, min(args.steps, 10))
+    # warm-up as steady state looks: each call returns a fresh caller-owned
+    # pinned array while the caller still holds the previous one, so the
+    # second call is the one that grows the pinned pool (a one-time
+    # cudaHostAlloc, ~27 ms measured)
+    for _ in range(max(3, args.warmup)):
+        S_host = sk.apply_right(A_host, op)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ctx.barrier()
     e0.record(stream)
-    for _ in range(greps):
-        ref_c = torch.matmul(gst.R, At)
+    for _ in range(e2e_steps):
+        S_host = sk.apply_right(A_host, op)
     e1.record(stream)
     torch.cuda.synchronize()
-    cublas_ms = e0.elapsed_time(e1) / greps
-    del ref_c
-
-    # end to end through the public API: pinned host A -> H2D -> kernel -> D2H S
-    e2e = None
-    if rank == 0 or world > 1:
-        host = torch.empty((N, N), dtype=torch.float64, pin_memory=True)
-        host.copy_(A.t[:, :N])
-        A_host = host.numpy().T           # F-ordered view of the pinned buffer
-        e2e_steps = max(3, min(args.steps, 10))
-        # warm-up as steady state looks: each call returns a fresh caller-owned
-        # pinned array while the caller still holds the previous one, so the
-        # second call is the one that grows the pinned pool (a one-time
-        # cudaHostAlloc, ~27 ms measured)
-        for _ in range(max(3, args.warmup)):
-            S_host = sk.apply_right(A_host, op)
-        torch.cuda.synchronize()
-        e0.record(stream)
-        for _ in range(e2e_steps):
-            S_host = sk.apply_right(A_host, op)
-        e1.record(stream)
-        torch.cuda.synchronize()
-        e2e_ms = e0.elapsed_time(e1) / e2e_steps
-        if world > 1:
-            t = torch.tensor([e2e_ms], device="cuda")
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            e2e_ms = float(t.item())
-        e2e = {"value": world * a_bytes / (e2e_ms * 1e-3) / 1e9, "unit": "GB/s",
-               "h2d_bytes_per_step": a_bytes, "d2h_bytes_per_step": int(S_host.nbytes),
-               "ms_per_step": e2e_ms, "path": "sketching.apply_right(pinned host array)"}
-        del host, A_host
+    e2e_ms, = ctx.max_over_ranks([e0.elapsed_time(e1) / e2e_steps])
+    e2e = {"value": world * a_bytes / (e2e_ms * 1e-3) / 1e9, "unit": "GB/s",
+           "h2d_bytes_per_step": a_bytes, "d2h_bytes_per_step": int(S_host.nbytes),
+           "ms_per_step": e2e_ms, "path": "sketching.apply_right(pinned host array)"}
+    # the same call on a plain (pageable) numpy array -- what hsskit hands over
+    page = np.empty((N, N), order="F")
+    page[...] = A_host
+    del host, A_host
+    sk.apply_right(page, op)
+    torch.cuda.synchronize()
+    ctx.barrier()
+    t0 = time.perf_counter()
+    e0.record(stream)
+    for _ in range(3):
+        S_host = sk.apply_right(page, op)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    pg_ms, = ctx.max_over_ranks([e0.elapsed_time(e1) / 3])
+    e2e_pageable = {"value": world * a_bytes / (pg_ms * 1e-3) / 1e9, "unit": "GB/s",
+                    "h2d_bytes_per_step": a_bytes, "d2h_bytes_per_step": int(S_host.nbytes),
+                    "ms_per_step": pg_ms, "path": "sketching.apply_right(pageable numpy array)"}
+    del page, S_host
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
         from oracle import oracle as O
         threads = os.cpu_count() or 1
         rows = 2048
-        slab = A.row_view(0, rows).to_host()
-        slab = np.asfortranarray(slab)
-        O.sjlt_right(slab, blk._pos, blk._signs, D, blk._scale, nthreads=threads)
-        ts = []
-        t_start = time.perf_counter()
-        while len(ts) < 3 or (time.perf_counter() - t_start < 10.0 and len(ts) < 50):
-            t0 = time.perf_counter()
-            O.sjlt_right(slab, blk._pos, blk._signs, D, blk._scale, nthreads=threads)
-            ts.append(time.perf_counter() - t0)
-        cpu = {"value": slab.nbytes / statistics.median(ts) / 1e9, "unit": "GB/s",
-               "cores": threads, "kind": "port",
+        slab = np.asfortranarray(A.row_view(0, rows).to_host())
+        gbs, t, reps = cpu_rate(lambda: O.sjlt_right(slab, blk._pos, blk._signs, D, blk._scale,
+                                                     nthreads=threads), slab.nbytes, 10.0, 3)
+        cpu = {"value": gbs, "unit": "GB/s", "cores": threads, "kind": "port",
                "sample": f"oracle SjltBlock.apply_right restatement on a {rows} x {N} row slab "
-                         f"of the same A, median of {len(ts)}"}
+                         f"of the same A, median of {reps}"}
+    del A, S
+    _free()
 
-    line = {
+    out.update({
         "metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic",
         "config": {"workload": "c2_sjlt_S", "n": N, "d": D, "alpha": ALPHA,
                    "construction": "block", "matrix": "gaussian kernel 8-D h=0.5",
-                   "parallelism": f"rowshard{world}", "l2": "inputs larger than L2 (2.15 GB A)"},
-        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                     "frac": achieved / peak, "peak_source": peak_src,
-                     "traffic": _traffic_from_profiles("sjlt_apply_S"),
-                     "algorithmic_bytes_per_launch": a_bytes + s_bytes,
-                     "avg_launch_ms": avg_launch},
+                   "parallelism": f"rowshard{world}" + ("-shared-gpu" if ctx.share else ""),
+                   "l2": "inputs larger than L2 (2.15 GB A)"},
+        "roofline": roof,
         "gpu_launches": args.steps,
         "clocks": clocks,
+        "sustained": {"launches": sus_n, "avg_launch_ms": sus_ms,
+                      "frac": (a_bytes + s_bytes) / (sus_ms * 1e-3) / 1e9 / peak,
+                      "clocks": clocks_sus},
         "e2e": e2e,
+        "e2e_pageable": e2e_pageable,
         "cpu_baseline": cpu,
         "transposed": {"metric": "S'=A^T R^T A-streamed GB/s", "ms": st_ms,
                        "value": a_bytes / (st_ms * 1e-3) / 1e9,
                        "frac": (a_bytes + s_bytes) / (st_ms * 1e-3) / 1e9 / peak},
         "gaussian": {"metric": "FP64 TFLOP/s, S=A R^T d=512 (DMMA)", "ms": g_ms,
                      "value": flops / (g_ms * 1e-3) / 1e12, "unit": "TFLOP/s",
+                     "transposed_ms": gt_ms,
+                     "transposed_value": flops / (gt_ms * 1e-3) / 1e12,
                      "cublas_dgemm_ms": cublas_ms,
-                     "cublas_dgemm_tflops": flops / (cublas_ms * 1e-3) / 1e12},
-    }
-    if rank == 0:
-        print(json.dumps(line), flush=True)
-    if world > 1:
-        dist.destroy_process_group()
+                     "cublas_dgemm_tflops": flops / (cublas_ms * 1e-3) / 1e12,
+                     "vs_cublas": cublas_ms / g_ms},
+    })
+
+
+# ------------------------------------------------------------ sub-records
+
+def cfg_c1(args, peak):
+    """configs[0]: n = 4096, SJLT d = 256, alpha = 4, graph construction; S and
+    S' per launch with the 126 MB L2 flushed between launches (A is 134 MB)."""
+    import torch
+    from paper_2302_01977_b200 import _lib, device, matgen
+    from paper_2302_01977_b200 import sketching as sk
+    n, d = 4096, 256
+    stream = torch.cuda.current_stream()
+    A = matgen.gaussian_kernel(n, 8, 0.5)
+    op = sk.new_operator(sk.SJLT, n, d, np.random.SeedSequence((0, 0)), alpha=4,
+                         construction=sk.GRAPH)
+    blk = op.blocks[0]
+    device.block_state(blk)
+    S = device.DeviceMatrix.empty(n, d)
+    scratch = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+
+    def flush():
+        _lib.call("hsk_l2_flush", scratch.data_ptr(), scratch.numel(), stream.cuda_stream)
+    bytes_ = n * n * 8 + n * d * 8
+    s_ms = time_launches(lambda: device.apply_block(blk, A, False, S, 0), 200, 5, stream, flush)
+    t_ms = time_launches(lambda: device.apply_block(blk, A, True, S, 0), 200, 5, stream, flush)
+    rec = {"workload": "c1: n=4096 gaussian kernel, SJLT d=256 alpha=4 graph, S and S'",
+           "l2": "flushed between launches", "S_ms": s_ms, "St_ms": t_ms,
+           "roofline_S": roofline(bytes_, s_ms, peak), "roofline_St": roofline(bytes_, t_ms, peak),
+           "gpu_launches": 400}
+    if not args.no_cpu:
+        from oracle import oracle as O
+        Ah = A.to_host()
+        th = os.cpu_count() or 1
+        gbs, t, reps = cpu_rate(lambda: O.sjlt_right(Ah, blk._pos, blk._signs, d, blk._scale,
+                                                     nthreads=th), Ah.nbytes, 4.0)
+        gbs_t, t_t, _ = cpu_rate(lambda: O.sjlt_right_t(Ah, blk._pos, blk._signs, d, blk._scale,
+                                                        nthreads=th), Ah.nbytes, 4.0)
+        rec["cpu_baseline"] = {"value": gbs, "unit": "GB/s", "St_value": gbs_t, "cores": th,
+                               "kind": "port", "sample": f"full C1 S and S' (median of {reps})",
+                               "S_ms": t * 1e3, "St_ms": t_t * 1e3}
+    del A, S, scratch
+    _free()
+    return rec
+
+
+def cfg_c3(args, peak):
+    """configs[2]: the adaptive schedule (16 increments of 64 columns, alpha = 8,
+    S and S' extended in place per increment) on the n = 65536 Toeplitz-sine A."""
+    import torch
+    from paper_2302_01977_b200 import adaptive, device, matgen
+    from paper_2302_01977_b200 import sketching as sk
+    n, dd, incs, alpha = 65536, 64, 16, 8
+    stream = torch.cuda.current_stream()
+    A = matgen.toeplitz_sin(n)
+    ops = [sk.new_operator(sk.SJLT, n, dd, np.random.SeedSequence((0, 0)), alpha=alpha,
+                           construction=sk.BLOCK)]
+    for i in range(1, incs):
+        ops.append(sk.append_columns(ops[-1], dd, np.random.SeedSequence((0, i))))
+    for b in ops[-1].blocks:
+        device.block_state(b)
+    ds = adaptive.DeviceSketch(A, dd * incs)
+
+    def step():
+        ds.start(ops[0])
+        for o in ops[1:]:
+            ds.extend(o)
+    ms = time_launches(step, 5, 3, stream)
+    a_bytes = 8 * n * n
+    per = a_bytes + 8 * n * dd
+    rec = {"workload": "c3_adaptive: n=65536 toeplitz-sine, 16 x 64-column SJLT increments "
+                       "alpha=8, S and S' per increment",
+           "ms_per_schedule": ms, "products": ds.products_per_schedule(incs),
+           "A_passes": ds.passes_per_schedule(incs),
+           "value": ds.passes_per_schedule(incs) * a_bytes / (ms * 1e-3) / 1e9, "unit": "GB/s",
+           "fused": ds.fused,
+           "roofline": roofline(ds.passes_per_schedule(incs) * per, ms, peak),
+           "gpu_launches": 5 * ds.launches_per_schedule(incs)}
+    rec["roofline"]["note"] = ("achieved = algorithmic bytes of the schedule's passes over A "
+                               "(A + the increment's S and S' columns per pass) / schedule time")
+    if not args.no_cpu:
+        from oracle import oracle as O
+        blk = ops[0].blocks[0]
+        rows = np.asfortranarray(A.row_view(0, 256).to_host())
+        cols = np.asfortranarray(A.to_host(0, 256))
+        th = os.cpu_count() or 1
+        gbs, _, _ = cpu_rate(lambda: O.sjlt_right(rows, blk._pos, blk._signs, dd, blk._scale,
+                                                  nthreads=th), rows.nbytes, 3.0)
+        gbs_t, _, _ = cpu_rate(lambda: O.sjlt_right_t(cols, blk._pos, blk._signs, dd, blk._scale,
+                                                      nthreads=th), cols.nbytes, 3.0)
+        sched_s = incs * (a_bytes / (gbs * 1e9) + a_bytes / (gbs_t * 1e9))
+        rec["cpu_baseline"] = {"value": 2 * incs * a_bytes / sched_s / 1e9, "unit": "GB/s",
+                               "cores": th, "kind": "port",
+                               "sample": "one 64-column block on a 256-row slab (S) and a "
+                                         "256-column slab (S'), extrapolated to the schedule",
+                               "schedule_s_extrapolated": sched_s}
+    del A, ds
+    _free()
+    return rec
+
+
+def cfg_c4(args, peak):
+    """configs[3]: SRHT d = 512 on the n = 2^16 Gaussian kernel (h = 0.25)."""
+    import torch
+    from paper_2302_01977_b200 import device, matgen
+    from paper_2302_01977_b200 import sketching as sk
+    n, d = 65536, 512
+    stream = torch.cuda.current_stream()
+    A = matgen.gaussian_kernel(n, 8, 0.25)
+    op = sk.new_operator(sk.SRHT, n, d, np.random.SeedSequence((0, 0)))
+    blk = op.blocks[0]
+    device.block_state(blk)
+    S = device.DeviceMatrix.empty(n, d)
+    s_ms = time_launches(lambda: device.apply_block(blk, A, False, S, 0), 10, 2, stream)
+    t_ms = time_launches(lambda: device.apply_block(blk, A, True, S, 0), 10, 2, stream)
+    bytes_ = 8 * n * n + 8 * n * d
+    rec = {"workload": "c4_srht: n=65536 gaussian kernel h=0.25, SRHT d=512, S and S'",
+           "S_ms": s_ms, "St_ms": t_ms, "roofline_S": roofline(bytes_, s_ms, peak),
+           "roofline_St": roofline(bytes_, t_ms, peak), "gpu_launches": 20}
+    if not args.no_cpu:
+        from oracle import oracle as O
+        rows = np.asfortranarray(A.row_view(0, 64).to_host())
+        th = os.cpu_count() or 1
+        gbs, _, _ = cpu_rate(lambda: O.srht(rows, blk.signs, blk.sample, d, blk.scale, False,
+                                            nthreads=th), rows.nbytes, 4.0)
+        rec["cpu_baseline"] = {"value": gbs, "unit": "GB/s", "cores": th, "kind": "port",
+                               "sample": "SrhtBlock._transform restatement on a 64-row slab"}
+    del A, S
+    _free()
+    return rec
+
+
+def cfg_c5(args, ctx, peak):
+    """configs[4] at this world size, strong-scaled: n = n5 (131072) rows
+    sharded over the ranks; per rank S = A_g R^T (local) and S' through the
+    p2p exchange (distributed.sketch_row_sharded), SJLT d = 2048 alpha = 8 and
+    Gaussian d = 512.  Device times, max over ranks."""
+    import torch
+    from paper_2302_01977_b200 import device, matgen
+    from paper_2302_01977_b200 import distributed as hd
+    from paper_2302_01977_b200 import sketching as sk
+    n = args.c5_n
+    world, rank = ctx.world, ctx.rank
+    stream = torch.cuda.current_stream()
+    r0, r1 = hd.shard_bounds(n, world)[rank]
+    pts = matgen.kernel_points(n, 16, 0)
+    A = matgen.gaussian_kernel(n, 16, 1.0, 1e-2, row0=r0, nrows=r1 - r0, points=pts)
+    rec = {"workload": f"c5: n={n} gaussian kernel 16-D h=1.0 row-sharded over {world} rank(s); "
+                       "S local, S' via p2p peer stores + rank-ordered sum",
+           "n": n, "rows_per_rank": r1 - r0, "scaling": "strong", "transport": "p2p"}
+    a_bytes = 8 * n * n
+    res = {}
+    for kind, d, kw in (("sjlt", 2048, dict(alpha=8, construction=sk.BLOCK)),
+                        ("gaussian", 512, {})):
+        op = sk.new_operator(kind, n, d, np.random.SeedSequence((0, 0)), **kw)
+        sub = hd._restricted_cached(op, r0, r1)
+        for b in op.blocks + sub.blocks:
+            device.block_state(b)
+        S = device.DeviceMatrix.empty(r1 - r0, d)
+        reps, warm = (5, 3) if kind == "sjlt" else (2, 1)
+
+        def fS():
+            sk.apply_right_device(A, op, out=S)
+
+        def fSt():
+            hd.sketch_row_sharded(A, op, rank=rank, world=world, n_rows=n, transport="p2p",
+                                  local_right=lambda *_: None)
+        ctx.barrier()
+        s_ms = time_launches(fS, reps, warm, stream)
+        ctx.barrier()
+        t_ms = time_launches(fSt, reps, warm, stream)
+        s_ms, t_ms = ctx.max_over_ranks([s_ms, t_ms])
+        ent = {"S_ms": s_ms, "St_ms": t_ms, "step_ms": s_ms + t_ms}
+        if kind == "sjlt":
+            per = a_bytes / world + 8 * (r1 - r0) * d
+            ent["value"] = 2 * a_bytes / ((s_ms + t_ms) * 1e-3) / 1e9
+            ent["unit"] = "GB/s (A-streamed, S and S', whole job)"
+            ent["roofline_S"] = roofline(per, s_ms, peak)
+            ent["roofline_St"] = roofline(per, t_ms, peak)
+            ent["roofline_St"]["note"] = "S' time includes the peer-store exchange and the slot sum"
+        else:
+            fl = 2.0 * n * n * d
+            ent["value"] = 2 * fl / ((s_ms + t_ms) * 1e-3) / 1e12
+            ent["unit"] = "TFLOP/s (FP64, S and S', whole job)"
+            ent["S_tflops"] = fl / (s_ms * 1e-3) / 1e12
+        res[kind] = ent
+        del S
+        _free()
+    rec.update(res)
+    if rank == 0 and world == 1 and not args.no_cpu:
+        from oracle import oracle as O
+        th = os.cpu_count() or 1
+        op = sk.new_operator(sk.SJLT, n, 2048, np.random.SeedSequence((0, 0)), alpha=8,
+                             construction=sk.BLOCK)
+        blk = op.blocks[0]
+        rows = np.asfortranarray(A.row_view(0, 64).to_host())
+        gbs, _, _ = cpu_rate(lambda: O.sjlt_right(rows, blk._pos, blk._signs, 2048, blk._scale,
+                                                  nthreads=th), rows.nbytes, 4.0)
+        rec["cpu_baseline"] = {"value": gbs, "unit": "GB/s", "cores": th, "kind": "port",
+                               "sample": "SJLT d=2048 S on a 64-row slab of the C5 matrix"}
+    hd.release_peer_slots()
+    del A
+    _free()
+    return rec
+
+
+# --------------------------------------------------------------------- main
+
+def _relaunch(args) -> int:
+    """--gpus N > 1 without torchrun: run this script under
+    torch.distributed.run with N ranks on this node."""
+    import torch
+    if not args.share_gpu and torch.cuda.device_count() < args.gpus:
+        print(json.dumps({"error": f"--gpus {args.gpus} but {torch.cuda.device_count()} GPU(s) "
+                                   "visible"}), flush=True)
+        return 2
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--master-addr", "127.0.0.1",
+           "--master-port", str(port), os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=400)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline legs")
+    ap.add_argument("--no-configs", action="store_true",
+                    help="headline only (skip the c1/c3/c4/c5 sub-records)")
+    ap.add_argument("--configs", default="c1,c3,c4,c5",
+                    help="comma list of sub-records to run (N = 1: c1,c3,c4,c5; N > 1: c5)")
+    ap.add_argument("--share-gpu", action="store_true",
+                    help="all ranks on GPU 0 (gloo group): exercises the multi-rank path")
+    ap.add_argument("--c5-n", type=int, default=131072)
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+    if args.impl == "reference":
+        run_reference(args)
+        return
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(_relaunch(args))
+
+    ctx = Ctx(args)
+    from paper_2302_01977_b200 import _lib
+    _lib.load()
+    out = {}
+    run_headline(args, ctx, out)
+    peak, _ = _peaks()
+    configs = {}
+    want = [] if args.no_configs else [c for c in args.configs.split(",") if c]
+    single = ctx.world == 1
+    for name, fn in (("c1", cfg_c1), ("c3_adaptive", cfg_c3), ("c4_srht", cfg_c4)):
+        if single and name.split("_")[0] in want:
+            configs[name] = fn(args, peak)
+    if "c5" in want:
+        configs["c5"] = cfg_c5(args, ctx, peak)
+    if configs:
+        out["configs"] = configs
+    if ctx.rank == 0:
+        print(json.dumps(out), flush=True)
+    ctx.close()
 
 
 if __name__ == "__main__":

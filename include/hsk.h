@@ -55,6 +55,12 @@ extern "C" {
 
 HSK_API int hsk_abi_version(void);
 
+/* Tuning knobs (HSK_SJLT_* / HSK_GAUSS_CFG environment variables, see
+ * DESIGN.md) are read once, on first use; this re-reads them after the
+ * environment changed in-process (A/B tools and tests).  No reference
+ * counterpart. */
+HSK_API int hsk_tuning_reload(void);
+
 /* Copies the calling thread's last error message into buf (NUL-terminated);
  * returns its full length. */
 HSK_API int hsk_last_error(char *buf, size_t len);

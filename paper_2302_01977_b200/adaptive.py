@@ -59,6 +59,19 @@ class DeviceSketch:
         self.op = op
         return self
 
+    # bookkeeping for benchmarks: per schedule of `incs` single-block increments
+    fused = False
+
+    def products_per_schedule(self, incs: int) -> int:
+        return incs * ((self.S is not None) + (self.St is not None))
+
+    def passes_per_schedule(self, incs: int) -> int:
+        """Full passes over A (HBM streams) per schedule."""
+        return self.products_per_schedule(incs)
+
+    def launches_per_schedule(self, incs: int) -> int:
+        return self.products_per_schedule(incs)
+
     def right(self) -> np.ndarray:
         return self.S.to_host(0, self.d)
 

@@ -29,6 +29,16 @@ int cuda_status(cudaError_t e, const char *what);
 
 int sm_count();
 
+// Run-time tuning knobs (HSK_* environment variables), read once and cached:
+// a launch costs no getenv() scans.  hsk_tuning_reload() re-reads them (tests
+// and A/B tools that change the environment in-process).  -1 = unset.
+struct Tuning {
+    int sjlt_w32, sjlt_tk, sjlt_tk_t, sjlt_rpt, sjlt_rpt_t, sjlt_prod, sjlt_streamk, sjlt_mc,
+        sjlt_stages, sjlt_wait_ns, sjlt_dbg, sjlt_pf, sjlt_fused;
+    char gauss_cfg[32];
+};
+const Tuning &tuning();
+
 // Scratch for cross-CTA partial sums: a zero-initialised flag array plus a
 // data area, one per (device, stream) so launches on different streams never
 // share it; launches on one stream are ordered, and every kernel that uses

@@ -18,6 +18,10 @@
 
 #include "hsk_common.cuh"
 
+#ifndef HSK_TUNING
+#define HSK_TUNING 0
+#endif
+
 namespace hsk {
 namespace gauss {
 
@@ -253,34 +257,32 @@ extern "C" int hsk_gauss_apply(const double *A, int64_t rows, int64_t cols, int6
     // resident CTAs keep the FP64 tensor pipe fed (measured best among warp
     // tiles 32x32 / 32x64 / 64x32 / 64x64 and 2-6 stages).  HSK_GAUSS_CFG overrides: "128" (128x128, 2x4 warps),
     // "64x128" (2x4 warps).
-    const char *cfg = getenv("HSK_GAUSS_CFG");
-    // tuning variants: warp tiles 32x64 / 64x32 (12 fragment loads per 32 DMMA)
-    if (cfg && !strcmp(cfg, "64x128w"))
+#if HSK_TUNING  // A/B variants of DESIGN.md §7 (HSK_GAUSS_CFG); the 128-wide tiles spill
+    const char *cfg = tuning().gauss_cfg;
+    if (!strcmp(cfg, "64x128w"))
         return trans ? gauss::launch<64, 128, 1, 2, 2, 4>(a, st)
                      : gauss::launch<64, 128, 0, 2, 2, 4>(a, st);
-    if (cfg && !strcmp(cfg, "128x64w"))
+    if (!strcmp(cfg, "128x64w"))
         return trans ? gauss::launch<128, 64, 1, 2, 2, 4>(a, st)
                      : gauss::launch<128, 64, 0, 2, 2, 4>(a, st);
-    if (cfg && !strcmp(cfg, "128x128w"))
+    if (!strcmp(cfg, "128x128w"))
         return trans ? gauss::launch<128, 128, 1, 2, 2, 3>(a, st)
                      : gauss::launch<128, 128, 0, 2, 2, 3>(a, st);
-    if (cfg && !strcmp(cfg, "64x64s3"))
+    if (!strcmp(cfg, "64x64s3"))
         return trans ? gauss::launch<64, 64, 1, 2, 2, 3>(a, st)
                      : gauss::launch<64, 64, 0, 2, 2, 3>(a, st);
-    if (cfg && !strcmp(cfg, "64x64s2"))
-        return trans ? gauss::launch<64, 64, 1, 2, 2, 2>(a, st)
-                     : gauss::launch<64, 64, 0, 2, 2, 2>(a, st);
-    if (cfg && !strcmp(cfg, "64x64s6"))
+    if (!strcmp(cfg, "64x64s6"))
         return trans ? gauss::launch<64, 64, 1, 2, 2, 6>(a, st)
                      : gauss::launch<64, 64, 0, 2, 2, 6>(a, st);
-    if (cfg && !strcmp(cfg, "128"))
+    if (!strcmp(cfg, "128"))
         return trans ? gauss::launch<128, 128, 1, 2, 4, 3>(a, st)
                      : gauss::launch<128, 128, 0, 2, 4, 3>(a, st);
-    if (cfg && !strcmp(cfg, "64x128"))
+    if (!strcmp(cfg, "64x128"))
         return trans ? gauss::launch<64, 128, 1, 2, 4, 3>(a, st)
                      : gauss::launch<64, 128, 0, 2, 4, 3>(a, st);
-    if (cfg && !strcmp(cfg, "64x64x8"))
+    if (!strcmp(cfg, "64x64x8"))
         return trans ? gauss::launch<64, 64, 1, 2, 4, 4>(a, st)
                      : gauss::launch<64, 64, 0, 2, 4, 4>(a, st);
+#endif
     return trans ? gauss::launch<64, 64, 1, 2, 2, 2>(a, st) : gauss::launch<64, 64, 0, 2, 2, 2>(a, st);
 }

@@ -7,6 +7,7 @@
 
 #include <algorithm>
 #include <map>
+#include <atomic>
 #include <mutex>
 #include <utility>
 
@@ -65,6 +66,48 @@ int sm_count() {
         if (cached <= 0) cached = 148;
     }
     return cached;
+}
+
+namespace {
+Tuning g_tuning;
+std::atomic<int> g_tuning_ready{0};
+std::mutex g_tuning_mu;
+
+int env_int(const char *name) {
+    const char *v = getenv(name);
+    return (v && *v) ? atoi(v) : -1;
+}
+
+void tuning_load() {
+    Tuning t;
+    t.sjlt_w32 = env_int("HSK_SJLT_W32");
+    t.sjlt_tk = env_int("HSK_SJLT_TK");
+    t.sjlt_tk_t = env_int("HSK_SJLT_TK_T");
+    t.sjlt_rpt = env_int("HSK_SJLT_RPT");
+    t.sjlt_rpt_t = env_int("HSK_SJLT_RPT_T");
+    t.sjlt_prod = env_int("HSK_SJLT_PROD");
+    t.sjlt_streamk = env_int("HSK_SJLT_STREAMK");
+    t.sjlt_mc = env_int("HSK_SJLT_MC");
+    t.sjlt_stages = env_int("HSK_SJLT_STAGES");
+    t.sjlt_wait_ns = env_int("HSK_SJLT_WAIT_NS");
+    t.sjlt_dbg = env_int("HSK_SJLT_DBG");
+    t.sjlt_pf = env_int("HSK_SJLT_PF");
+    t.sjlt_fused = env_int("HSK_SJLT_FUSED");
+    const char *g = getenv("HSK_GAUSS_CFG");
+    snprintf(t.gauss_cfg, sizeof(t.gauss_cfg), "%s", g ? g : "");
+    g_tuning = t;
+}
+}  // namespace
+
+const Tuning &tuning() {
+    if (!g_tuning_ready.load(std::memory_order_acquire)) {
+        std::lock_guard<std::mutex> lk(g_tuning_mu);
+        if (!g_tuning_ready.load(std::memory_order_relaxed)) {
+            tuning_load();
+            g_tuning_ready.store(1, std::memory_order_release);
+        }
+    }
+    return g_tuning;
 }
 
 namespace {
@@ -159,6 +202,13 @@ __global__ void l2_flush_kernel(double4 *p, int64_t n4, double v) {
 using namespace hsk;
 
 extern "C" int hsk_abi_version(void) { return HSK_ABI_VERSION; }
+
+extern "C" int hsk_tuning_reload(void) {
+    std::lock_guard<std::mutex> lk(g_tuning_mu);
+    tuning_load();
+    g_tuning_ready.store(1, std::memory_order_release);
+    return HSK_OK;
+}
 
 extern "C" int hsk_last_error(char *buf, size_t len) {
     const int n = (int)strlen(g_err);

@@ -48,6 +48,10 @@
 #ifndef HSK_SJLT_DEBUG
 #define HSK_SJLT_DEBUG 0
 #endif
+// tuning builds (-DHSK_TUNING=1) add the A/B kernel variants of DESIGN.md §7
+#ifndef HSK_TUNING
+#define HSK_TUNING 0
+#endif
 #define DBG_IS(m) (HSK_SJLT_DEBUG && p.dbg == (m))
 
 // producer warps of the transposed 128-row S' tiles: mode 4 (TMA staging +
@@ -116,11 +120,15 @@ static inline int tk_fit(int alpha, int tm, int cap, int per_stage, int64_t ng, 
     return tk;
 }
 
-// largest multiple of 16 TK <= cap (<= 256: TMA box limit) whose stage fits
+// largest multiple of 16 TK <= cap (<= 256: TMA box limit) whose stage fits;
+// when not even TK = 16 keeps TK * alpha within a chunk's 12-bit local index
+// (alpha > 256), the power-of-two rule (down to 1) of tk_fit
 static inline int tk_fit16(int alpha, int tm, int cap, int per_stage, int64_t ng, int nw) {
     int tk = cap;
     while (tk > 16 && (tk * alpha > kMaxChunkEntries || stage_bytes_for(tk, tm, alpha, ng, nw) > per_stage))
         tk -= 16;
+    if (tk * alpha > kMaxChunkEntries || stage_bytes_for(tk, tm, alpha, ng, nw) > per_stage)
+        return tk_fit(alpha, tm, 16, per_stage, ng, nw);
     return tk;
 }
 
@@ -129,8 +137,11 @@ static inline int tk_fit16(int alpha, int tm, int cap, int per_stage, int64_t ng
 // the walker; the 32-warp variants, half the buckets per warp, are kept for
 // tuning: HSK_SJLT_W32=1)
 static inline void warp_shape(int rpt, int d, int &db, int &nw) {
-    bool w32 = false;
-    if (const char *env = getenv("HSK_SJLT_W32")) w32 = env[0] == '1';
+#if HSK_TUNING
+    const bool w32 = tuning().sjlt_w32 == 1;
+#else
+    const bool w32 = false;  // 32-warp variants are compiled only in tuning builds
+#endif
     nw = w32 ? 32 : 16;
     if (rpt == 1) db = w32 ? 16 : 32;        // 32-row tiles, 512-bucket slabs
     else if (rpt == 4) db = w32 ? 2 : 4;     // 128-row tiles, 64-bucket slabs
@@ -163,8 +174,8 @@ static Geom geom_dir(int64_t n, int d, int alpha, int trans, int64_t base, int p
         g.ngroups = (int64_t)(d / kPairSlab) * g.nw;
         tk = n >= 8192 ? tk_fit16(ae, 64, 256, kStage2, g.ngroups, g.nw)
                        : tk_fit16(ae, 64, 128, kStage3, g.ngroups, g.nw);
-        if (const char *env = getenv(trans ? "HSK_SJLT_TK_T" : "HSK_SJLT_TK"))
-            tk = std::max(128, atoi(env) / 16 * 16);  // the fold buffer needs 64 KB of tile
+        if (const int e = trans ? tuning().sjlt_tk_t : tuning().sjlt_tk; e > 0)
+            tk = std::max(16, e / 16 * 16);
         g.tm = 64;
         g.pitch = g.tm;
         g.tk = tk;
@@ -191,7 +202,7 @@ static Geom geom_dir(int64_t n, int d, int alpha, int trans, int64_t base, int p
     // d = 2048, alpha = 8)
     const bool wide = n >= 8192 && (trans || d <= 512);
     g.rpt = d <= 64 ? 4 : 2;
-    if (const char *env = getenv(trans ? "HSK_SJLT_RPT_T" : "HSK_SJLT_RPT")) g.rpt = atoi(env);
+    if (const int e = trans ? tuning().sjlt_rpt_t : tuning().sjlt_rpt; e == 1 || e == 2 || e == 4) g.rpt = e;
     warp_shape(g.rpt, d, g.db, g.nw);
     g.ngroups = roundup(d, (int64_t)g.db * g.nw) / g.db;
     if (d <= 64) {
@@ -201,7 +212,7 @@ static Geom geom_dir(int64_t n, int d, int alpha, int trans, int64_t base, int p
         tk = wide ? tk_fit16(alpha, 64, 256, kStage2, g.ngroups, g.nw)
                   : tk_fit(alpha, 64, 128, kStage3, g.ngroups, g.nw);
     }
-    if (const char *env = getenv(trans ? "HSK_SJLT_TK_T" : "HSK_SJLT_TK")) tk = atoi(env);
+    if (const int e = trans ? tuning().sjlt_tk_t : tuning().sjlt_tk; e > 0) tk = e;
     g.tm = 32 * g.rpt;
     g.pitch = g.tm;
     g.tk = tk;
@@ -230,6 +241,14 @@ static Plan plan_geom(int64_t n, int d, int alpha, int pair = 0) {
     pl.t = geom_dir(n, d, alpha, 1, pl.s.end, pair);
     pl.bytes = pl.t.end;
     return pl;
+}
+
+// A chunk's sort key holds its entry index in 12 bits (paired: the input
+// index in 8): a geometry outside that can never build a valid plan.
+static bool geom_ok(const Geom &g, int alpha) {
+    if (g.tk < 1) return false;
+    if (g.pair) return g.tk <= 256 && (int64_t)g.tk * (alpha / 2) <= kMaxChunkEntries;
+    return (int64_t)g.tk * alpha <= kMaxChunkEntries;
 }
 
 // ------------------------------------------------------------ plan build
@@ -983,6 +1002,11 @@ static int launch(ApplyArgs a, const Geom &g, cudaStream_t st) {
     a.gs_off = a_bytes;
     a.en_off = (int)roundup(a.gs_off + (NW + 4) / 4 * 16, 128);
     a.stage_bytes = (int)roundup(a.en_off + (a.estride + 8) * 4, 1024);
+    // paired plans fold the quarters' t2 partials through the slot of a row
+    // tile's last chunk: NW warps x 8 buckets x RPT x 32 lanes doubles (64 KB)
+    // must lie inside that slot (the next slot may already hold a landed or
+    // in-flight chunk)
+    if (PAIR) a.stage_bytes = std::max(a.stage_bytes, (int)roundup((int64_t)NW * 8 * RPT * 32 * 8, 1024));
     a.nslabs = (a.d + SLAB - 1) / SLAB;
     const int64_t tiles = (a.m_out + TM - 1) / TM;
     // k-split across a cluster when the tile grid cannot fill the GPU
@@ -997,7 +1021,7 @@ static int launch(ApplyArgs a, const Geom &g, cudaStream_t st) {
     // a 33rd warp would cut the register budget to 56, so 32-warp CTAs refill
     // from the last consumer warp to release a slot instead
     bool prod = NW < 32;
-    if (const char *env = getenv("HSK_SJLT_PROD")) prod = env[0] == '1';
+    if (tuning().sjlt_prod >= 0) prod = tuning().sjlt_prod == 1;
     const int pw = a.trans && XPOSE ? kXposeProducers : 1;
     prod = prod && (a.mode == 0 || a.mode == 3 || ((a.mode == 1 || a.mode == 4) && XPOSE)) &&
            NW + pw <= 32;
@@ -1014,7 +1038,7 @@ static int launch(ApplyArgs a, const Geom &g, cudaStream_t st) {
     // (grids smaller than the GPU split k over a cluster instead: measured
     // better on C1, where stream-K's per-CTA fixups are a large share)
     a.streamk = eff < 0.9 && ctas >= sms;
-    if (const char *env = getenv("HSK_SJLT_STREAMK")) a.streamk = env[0] == '1';
+    if (tuning().sjlt_streamk >= 0) a.streamk = tuning().sjlt_streamk == 1;
     a.streamk = a.streamk && a.groups >= 1 && a.nchunks > 0 && a.units < (1ll << 31);
     if (a.streamk) ks = 1;
     // TMA multicast across the slab CTAs of a row tile (they read the same
@@ -1025,8 +1049,7 @@ static int launch(ApplyArgs a, const Geom &g, cudaStream_t st) {
     // cluster released it, which runs the slab CTAs in lockstep behind the
     // slowest; without it each CTA runs ahead on its own and L2 absorbs the skew.
     a.mc = 1;
-    const char *mc_env = getenv("HSK_SJLT_MC");
-    if (HSK_SJLT_MULTICAST && mc_env && mc_env[0] == '1' && prod && (a.mode == 0 || a.mode == 3) && ks == 1 &&
+    if (HSK_SJLT_MULTICAST && tuning().sjlt_mc == 1 && prod && (a.mode == 0 || a.mode == 3) && ks == 1 &&
         (a.nslabs == 2 || a.nslabs == 4 || a.nslabs == 8) && (a.mode == 3 || a.tk % a.nslabs == 0))
         a.mc = a.nslabs;
     CUtensorMap tmap;
@@ -1089,7 +1112,7 @@ static int launch(ApplyArgs a, const Geom &g, cudaStream_t st) {
     a.ksplit = ks;
     const int per = (int)(a.streamk ? (a.units + a.groups - 1) / a.groups : (a.nchunks + ks - 1) / ks);
     a.stages = stages_max;
-    if (const char *env = getenv("HSK_SJLT_STAGES")) a.stages = std::max(2, std::min(a.stages, atoi(env)));
+    if (tuning().sjlt_stages > 0) a.stages = std::max(2, std::min(a.stages, tuning().sjlt_stages));
     if (per > 0 && a.stages > per + 1) a.stages = std::max(2, per + 1);
     int smem = 2048 + a.stages * a.stage_bytes + stg_bytes;  // header + 1024-byte alignment slack
     if (ks > 1) smem = std::max(smem, 2048 + NW * DB * RPT * 32 * 8);
@@ -1107,9 +1130,9 @@ static int launch(ApplyArgs a, const Geom &g, cudaStream_t st) {
     a.pf = 0;
     // consumers waiting for a tile sleep up to 1 us per poll (measured neutral
     // to +1 %: fewer polling instructions under the power cap)
-    a.wait_ns = getenv("HSK_SJLT_WAIT_NS") ? atoi(getenv("HSK_SJLT_WAIT_NS")) : 1000;
-    a.dbg = getenv("HSK_SJLT_DBG") ? atoi(getenv("HSK_SJLT_DBG")) : 0;
-    if (const char *env = getenv("HSK_SJLT_PF")) a.pf = std::max(0, atoi(env));
+    a.wait_ns = tuning().sjlt_wait_ns >= 0 ? tuning().sjlt_wait_ns : 1000;
+    a.dbg = std::max(0, tuning().sjlt_dbg);
+    a.pf = std::max(0, tuning().sjlt_pf);
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e != cudaSuccess) return cuda_status(e, "sjlt: set smem attribute");
     const int64_t grid = a.streamk ? (int64_t)a.groups * a.nslabs : tiles * a.nslabs * ks;
@@ -1175,6 +1198,8 @@ extern "C" int hsk_sjlt_plan_build_ex(const int32_t *pos, const int8_t *sgn, int
     HSK_REQUIRE(alpha <= sjlt::kMaxChunkEntries, HSK_EINVAL, "sjlt plan: alpha=%d too large", alpha);
     HSK_REQUIRE(n < (1ll << 31), HSK_EINVAL, "sjlt plan: n too large");
     const sjlt::Plan pl = sjlt::plan_geom(n, d, alpha, flags & HSK_SJLT_CHUNKED);
+    HSK_REQUIRE(n == 0 || (sjlt::geom_ok(pl.s, alpha) && sjlt::geom_ok(pl.t, alpha)), HSK_EINVAL,
+                "sjlt plan: no chunk geometry for d=%d alpha=%d (TK %d / %d)", d, alpha, pl.s.tk, pl.t.tk);
     HSK_REQUIRE(plan != nullptr && plan_bytes >= pl.bytes, HSK_EINVAL,
                 "sjlt plan: buffer of %lld bytes, need %lld", (long long)plan_bytes,
                 (long long)pl.bytes);
@@ -1194,17 +1219,17 @@ extern "C" int hsk_sjlt_plan_build_ex(const int32_t *pos, const int8_t *sgn, int
                 reinterpret_cast<uint32_t *>(base + g->ent_off), reinterpret_cast<int *>(base + 28));
             HSK_CHECK_LAUNCH("sjlt_plan_kernel");
         }
-        if (pl.s.pair) {
-            // paired plans rely on the chunk property: read the plan kernel's
-            // violation flag back (one stream sync, once per operator block)
-            int err = 0;
-            e = cudaMemcpyAsync(&err, base + 28, sizeof(int), cudaMemcpyDeviceToHost, st);
-            if (e == cudaSuccess) e = cudaStreamSynchronize(st);
-            if (e != cudaSuccess) return cuda_status(e, "sjlt plan: check");
-            if (err & 2)
-                return set_error(HSK_EINVAL, "sjlt plan: HSK_SJLT_CHUNKED given for a pattern whose "
-                                             "entry t is not in chunk t of d/alpha buckets");
-        }
+        // the plan kernel flags positions outside [0, d) (bit 0) and, for
+        // paired plans, entries outside their construction chunk (bit 1):
+        // read the flags back (one stream sync, once per operator block)
+        int err = 0;
+        e = cudaMemcpyAsync(&err, base + 28, sizeof(int), cudaMemcpyDeviceToHost, st);
+        if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+        if (e != cudaSuccess) return cuda_status(e, "sjlt plan: check");
+        if (err & 1) return set_error(HSK_ERANGE, "sjlt plan: pattern positions must lie in [0, %d)", d);
+        if (err & 2)
+            return set_error(HSK_EINVAL, "sjlt plan: HSK_SJLT_CHUNKED given for a pattern whose "
+                                         "entry t is not in chunk t of d/alpha buckets");
     }
     return HSK_OK;
 }
@@ -1242,6 +1267,8 @@ extern "C" int hsk_sjlt_apply_ex(const double *A, int64_t rows, int64_t cols, in
     HSK_REQUIRE(m_out < (1ll << 31) && n < (1ll << 31), HSK_EINVAL, "sjlt apply: too large");
     const sjlt::Plan pl = sjlt::plan_geom(n, d, alpha, flags & HSK_SJLT_CHUNKED);
     const sjlt::Geom &g = trans ? pl.t : pl.s;
+    HSK_REQUIRE(n == 0 || sjlt::geom_ok(g, alpha), HSK_EINVAL,
+                "sjlt apply: no chunk geometry for d=%d alpha=%d (TK %d)", d, alpha, g.tk);
     const unsigned char *base = static_cast<const unsigned char *>(plan);
     sjlt::ApplyArgs a{};
     a.A = A;
@@ -1268,13 +1295,15 @@ extern "C" int hsk_sjlt_apply_ex(const double *A, int64_t rows, int64_t cols, in
     const int shape = g.rpt * 1000 + g.db * 10 + (g.nw == 32);
     switch (shape) {
         case 1320: return sjlt::launch<1, 32, 16>(a, g, st);   // 32-row tiles, 512-bucket slabs
-        case 1161: return sjlt::launch<1, 16, 32>(a, g, st);
         case 4040: return sjlt::launch<4, 4, 16>(a, g, st);    // 128-row tiles, 64-bucket slabs
-        case 4021: return sjlt::launch<4, 2, 32>(a, g, st);
         case 2080: return sjlt::launch<2, 8, 16>(a, g, st);    // 64-row tiles
+        case 2160: return sjlt::launch<2, 16, 16>(a, g, st);
+#if HSK_TUNING  // 32-warp variants (HSK_SJLT_W32=1): spill, never selected by default
+        case 1161: return sjlt::launch<1, 16, 32>(a, g, st);
+        case 4021: return sjlt::launch<4, 2, 32>(a, g, st);
         case 2041: return sjlt::launch<2, 4, 32>(a, g, st);
         case 2081: return sjlt::launch<2, 8, 32>(a, g, st);
-        case 2160: return sjlt::launch<2, 16, 16>(a, g, st);
+#endif
         default: return set_error(HSK_EINVAL, "sjlt apply: no kernel for rpt=%d db=%d nw=%d", g.rpt, g.db, g.nw);
     }
 }

@@ -114,18 +114,21 @@ def _gpu_local_transposed_blocks(A_shard, sub_op, bounds):
 
 
 class PeerSlots:
-    """This rank's receive buffer for the p2p S' exchange -- `world` slots of
-    (ld x d) doubles, column-major, slot g written by rank g -- and CUDA-IPC
-    mappings of every peer's buffer (one process per GPU on one node)."""
+    """This rank's receive buffer for the p2p S' exchange -- two sets (calls
+    alternate between them) of `world` slots of (ld x d) doubles, column-major,
+    slot g written by rank g -- and CUDA-IPC mappings of every peer's buffer
+    (one process per GPU on one node)."""
 
     def __init__(self, world: int, rank: int, ld: int, d: int, group=None):
         import ctypes
         from . import _lib
         self.world, self.rank, self.ld, self.d = world, rank, ld, d
         self.slot_elems = ld * d
+        self.set_elems = world * self.slot_elems
+        self.phase = 0  # the slot set of the next call
         own = ctypes.c_void_p()
         handle = (ctypes.c_char * 64)()
-        _lib.call("hsk_ipc_alloc", world * self.slot_elems * 8, ctypes.byref(own), handle)
+        _lib.call("hsk_ipc_alloc", 2 * self.set_elems * 8, ctypes.byref(own), handle)
         self.own = own.value
         handles = [None] * world
         if world > 1:
@@ -141,16 +144,18 @@ class PeerSlots:
                 self.peer.append(p.value)
 
     def slot(self, q: int, rows: int):
-        """Rank q's slot for this rank's partial of block q (rows x d)."""
+        """Rank q's slot (current set) for this rank's partial of block q (rows x d)."""
         from . import device
-        return device.RawMatrix(self.peer[q] + self.rank * self.slot_elems * 8, rows, self.d,
-                                self.ld)
+        off = (self.phase * self.set_elems + self.rank * self.slot_elems) * 8
+        return device.RawMatrix(self.peer[q] + off, rows, self.d, self.ld)
 
     def reduce(self, rows: int, out_ptr: int, ldo: int, stream: int):
-        """out = sum of this rank's slots in rank order (first `rows` rows)."""
+        """out = sum of this rank's slots of the current set in rank order
+        (first `rows` rows); the next call uses the other set."""
         from . import _lib
-        _lib.call("hsk_sum_slices", self.own, self.world, self.slot_elems, rows, self.d, self.ld,
-                  out_ptr, ldo, stream)
+        _lib.call("hsk_sum_slices", self.own + self.phase * self.set_elems * 8, self.world,
+                  self.slot_elems, rows, self.d, self.ld, out_ptr, ldo, stream)
+        self.phase ^= 1
 
     def close(self):
         from . import _lib
@@ -180,8 +185,29 @@ def release_peer_slots():
     _SLOTS.clear()
 
 
+_FENCE: dict = {}
+
+
+def _stream_fence(group):
+    """A device-side barrier in stream order: a one-element all-reduce that
+    no rank completes before every rank's earlier kernels have finished (the
+    current stream waits on it; no host synchronisation)."""
+    t = _FENCE.get(id(group))
+    if t is None:
+        t = _FENCE[id(group)] = torch.zeros(1, dtype=torch.int32, device="cuda")
+    dist.all_reduce(t, group=group)
+
+
 def _p2p_transposed(A_shard, sub_op, bounds, rank: int, world: int, group):
-    """S' rows of this rank via direct peer stores + rank-ordered local sum."""
+    """S' rows of this rank via direct peer stores + rank-ordered local sum.
+
+    Ordering without host round trips: the peer stores of every rank's S'
+    kernels land before the stream-ordered fence (a kernel's stores are
+    visible at its completion); each rank sums its slots after the fence.
+    Calls alternate between two slot sets, so the writes of call t+1 go to
+    the other set, and those of call t+2 -- issued after call t+1's fence,
+    which every rank reaches only after its call-t sum -- never overwrite
+    slots still being summed."""
     from . import device
     from . import sketching as sk
     m_max = max(b1 - b0 for b0, b1 in bounds)
@@ -190,16 +216,11 @@ def _p2p_transposed(A_shard, sub_op, bounds, rank: int, world: int, group):
         if c1 > c0:
             view = A_shard.column_view(c0, c1 - c0)
             sk.apply_right_transposed_device(view, sub_op, out=slots.slot(q, c1 - c0))
-    # every rank's stores into every slot are complete before anyone sums
-    torch.cuda.synchronize()
     if world > 1:
-        dist.barrier(group=group)
+        _stream_fence(group)
     r0, r1 = bounds[rank]
     out = torch.empty((sub_op.d, max(1, r1 - r0)), dtype=torch.float64, device="cuda")
     slots.reduce(r1 - r0, out.data_ptr(), max(1, r1 - r0), device.current_stream_ptr())
-    torch.cuda.synchronize()
-    if world > 1:  # the slots are free for the next call
-        dist.barrier(group=group)
     return out[:, :r1 - r0]
 
 

@@ -81,6 +81,7 @@ def from_file(path, slab_bytes: int = _SLAB_BYTES):
     bufs = [torch.empty((step, rows), dtype=torch.float64, pin_memory=True) for _ in range(2)]
     done = [None, None]
     stream = torch.cuda.Stream()
+    stream.wait_stream(torch.cuda.current_stream())  # dm's block may still be in use there
     with open(path, "rb", buffering=0) as fh:
         fh.seek(_HEADER)
         for i, c0 in enumerate(range(0, cols, step)):

@@ -2,7 +2,8 @@
 
 Host-side mirror of the reference's operator model (hsskit sketching.py:
 blocks :123-360, SketchOperator :367-387, construction/append :390-428,
-dense_rows :460-476, jl_dimension_bound :479-499).  A block carries only
+dense_rows :460-476; jl_dimension_bound :479-499 is a sizing helper
+outside the sketch path and is not restated).  A block carries only
 its random draw (draws.py) plus the metadata the GPU engine needs; block
 products (`apply_right`, `apply_right_transposed`) launch libhsk.so kernels
 through device.py -- there is no host implementation of them here.
@@ -222,20 +223,3 @@ def dense_rows(op: SketchOperator, I, col_range) -> np.ndarray:
             out[:, sel] = blk.dense_rows(I, cols[sel] - lo)
     return out
 
-
-def jl_dimension_bound(kind: str, eps: float, delta: float, n: int | None = None, *,
-                       sjlt_c: float = 20.0) -> tuple[int, int | None]:
-    """Table 4.1 sketch sizes (Thms 5.2-5.4)."""
-    if not (0.0 < eps < 1.0) or not (0.0 < delta < 1.0):
-        raise ValueError("need eps, delta in (0, 1)")
-    if kind == GAUSSIAN:
-        return math.ceil(20.0 / eps**2 * math.log(2.0 / delta)), None
-    if kind == SRHT:
-        if n is None:
-            raise ValueError("SRHT bound needs the ambient dimension n")
-        return math.ceil(2.0 / eps**2 * math.log(4.0 * n**2 / delta)**2
-                         * math.log(4.0 / delta)), None
-    if kind == SJLT:
-        d = math.ceil(sjlt_c / eps**2 * math.log(1.0 / delta))
-        return d, math.ceil(eps * d)
-    raise ValueError(f"unknown operator kind {kind!r}")

@@ -12,7 +12,10 @@ same argument meaning, return type and exception class:
   append_columns                    operators          sketching.py:367-428
   apply_right                       S  = A R^T         sketching.py:431-442
   apply_right_transposed            S' = A^T R^T       sketching.py:445-457
-  dense_rows, jl_dimension_bound    host helpers       sketching.py:460-499
+  dense_rows                        host helper        sketching.py:460-476
+
+(jl_dimension_bound, sketching.py:479-499, sizes operators from the
+Table 4.1 bounds; it is not on the sketch path and is not restated.)
 
 The two products (and fwht) run sm_100a kernels from libhsk.so; operator
 draws are bit-identical to the reference's (draws.py).  Results are float64,
@@ -30,7 +33,7 @@ import numpy as np
 from . import device as _dev
 from .operators import (BLOCK, CONSTRUCTIONS, GAUSSIAN, GRAPH, KINDS, SJLT, SRHT,
                         GaussianBlock, SjltBlock, SjltStorage, SketchOperator, SrhtBlock,
-                        append_columns, dense_rows, jl_dimension_bound, new_operator)
+                        append_columns, dense_rows, new_operator)
 from .draws import next_pow2 as _next_pow2
 
 __all__ = [
@@ -38,7 +41,7 @@ __all__ = [
     "MatrixAccessor", "DenseAccessor", "DeviceAccessor", "fwht",
     "GaussianBlock", "SrhtBlock", "SjltBlock", "SjltStorage", "SketchOperator",
     "new_operator", "append_columns", "apply_right", "apply_right_transposed",
-    "dense_rows", "jl_dimension_bound", "device_matrix_of", "apply_right_device",
+    "dense_rows", "device_matrix_of", "apply_right_device",
     "apply_right_transposed_device",
 ]
 
@@ -85,10 +88,13 @@ class DeviceAccessor(MatrixAccessor):
     """MatrixAccessor whose buffer lives in HBM (a device.DeviceMatrix).
 
     Products use the device copy directly (no host round trip); extract()
-    gathers the requested entries on the device."""
+    gathers the requested entries on the device.  dense() honours the
+    accessor contract (sketching.py:41-43: the same buffer on every call): the
+    host copy is made once, on first request, and cached."""
 
     def __init__(self, dm: "_dev.DeviceMatrix"):
         self.dm = dm
+        self._host = None
 
     @property
     def shape(self) -> tuple[int, int]:
@@ -103,7 +109,9 @@ class DeviceAccessor(MatrixAccessor):
         return np.ascontiguousarray(sub.cpu().numpy().T)
 
     def dense(self) -> np.ndarray:
-        return self.dm.to_host()
+        if self._host is None:
+            self._host = self.dm.to_host()
+        return self._host
 
 
 def _buffer_of(A) -> np.ndarray:
@@ -254,6 +262,10 @@ def _streamed(buf: np.ndarray, op: SketchOperator, transpose: bool) -> np.ndarra
     slabs = [_dev.DeviceMatrix(step if not transpose else rows, sl_cols, ld=sl_ld) for _ in range(2)]
     out = _dev.DeviceMatrix.empty(m_out, op.d)
     host = torch.empty((op.d, m_out), dtype=torch.float64, pin_memory=True)
+    # the slab and output buffers come from the caching allocator on `comp`:
+    # kernels still queued there may have used those blocks last
+    h2d.wait_stream(comp)
+    d2h.wait_stream(comp)
     ev_in = [torch.cuda.Event() for _ in range(nslab)]
     ev_k = [torch.cuda.Event() for _ in range(nslab)]
     base = buf.ctypes.data

@@ -57,3 +57,18 @@ def case_inputs(case):
 
 def seed_of(s):
     return tuple(s) if isinstance(s, list) else s
+
+
+@pytest.fixture
+def tune(monkeypatch):
+    """Set an HSK_* tuning variable for one test: libhsk reads them once and
+    caches them, so every change (and the undo at teardown) is followed by
+    hsk_tuning_reload()."""
+    from paper_2302_01977_b200 import _lib
+
+    def set_(name, value):
+        monkeypatch.setenv(name, value)
+        _lib.load().hsk_tuning_reload()
+    yield set_
+    monkeypatch.undo()
+    _lib.load().hsk_tuning_reload()

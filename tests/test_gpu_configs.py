@@ -69,6 +69,11 @@ def test_c2_full_size(cuda):
     G = sk.apply_right_device(A, gop).to_host()
     rows = slice(777, 777 + 384)
     assert O.rel_frobenius(G[rows], O.apply_right(np.asfortranarray(Ah[rows]), gop)) <= REL
+    # Gaussian S' = A^T R^T: rows of S' are columns of A
+    Gt = sk.apply_right_transposed_device(A, gop).to_host()
+    cols = (9000, 9000 + 384)
+    assert O.rel_frobenius(Gt[cols[0]:cols[1]],
+                           O.apply_right_transposed(np.asfortranarray(Ah[:, cols[0]:cols[1]]), gop)) <= REL
     del A, Ah
     _free()
 
@@ -127,8 +132,20 @@ def test_c5_single_gpu_full_size(cuda):
     assert O.rel_frobenius(S.row_view(r0, 64).to_host(), O.apply_right(_rows(A, r0, r0 + 64), op)) <= REL
     del S
     _free()
+    # S' = A^T R^T: a column slab of A against the oracle (rows of S')
+    St = sk.apply_right_transposed_device(A, op)
+    c0 = 100000
+    assert O.rel_frobenius(St.row_view(c0, 64).to_host(),
+                           O.apply_right_transposed(_cols(A, c0, c0 + 64), op)) <= REL
+    del St
+    _free()
     gop = sk.new_operator(sk.GAUSSIAN, n, 512, np.random.SeedSequence((0, 0)))
     G = sk.apply_right_device(A, gop)
     assert O.rel_frobenius(G.row_view(r0, 32).to_host(), O.apply_right(_rows(A, r0, r0 + 32), gop)) <= REL
-    del A, G
+    del G
+    _free()
+    Gt = sk.apply_right_transposed_device(A, gop)
+    assert O.rel_frobenius(Gt.row_view(c0, 32).to_host(),
+                           O.apply_right_transposed(_cols(A, c0, c0 + 32), gop)) <= REL
+    del A, Gt
     _free()

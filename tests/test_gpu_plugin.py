@@ -1,9 +1,11 @@
 """Drop-in through the reference's own compressor (hsskit).
 
-The reference package is installed into baseline/_ref (git-ignored; it
-travels to the GPU box).  plugin.install() rebinds hsskit.sketching.apply_right
-/ apply_right_transposed; the compressor, operator draws and dense_rows stay
-the reference's.  Skipped when hsskit is not importable.
+The reference package is installed into baseline/_ref by
+__graft_entry__.build() (git-ignored; it travels to the GPU box with the
+snapshot).  plugin.install() rebinds hsskit.sketching.apply_right /
+apply_right_transposed; the compressor, operator draws and dense_rows stay
+the reference's.  These are the drop-in's parity gates, so a missing hsskit is
+a FAILURE under -m gpu (with the ImportError), never a skip.
 """
 
 import os
@@ -16,12 +18,24 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 REF = os.path.join(ROOT, "baseline", "_ref")
 if os.path.isdir(REF) and REF not in sys.path:
     sys.path.append(REF)
-hsskit = pytest.importorskip("hsskit")
+try:
+    import hsskit  # noqa: F401
+    _IMPORT_ERROR = None
+except ImportError as exc:  # reported by the `hsskit` fixture below
+    hsskit = None
+    _IMPORT_ERROR = exc
 
 from oracle import oracle as O  # noqa: E402
 from paper_2302_01977_b200 import matgen, plugin  # noqa: E402
 
 pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(autouse=True)
+def _require_reference():
+    if hsskit is None:
+        pytest.fail(f"reference package hsskit not importable from {REF} ({_IMPORT_ERROR!r}); "
+                    "run __graft_entry__.build() where /root/reference exists")
 
 
 @pytest.fixture

@@ -112,7 +112,7 @@ def test_sjlt_shapes_vs_oracle(cuda, m, n, d, alpha, cons):
     (5000, 3000, 300, 4), (9000, 1000, 64, 8), (4000, 2600, 700, 4), (3000, 5000, 2048, 8),
     (150, 20000, 512, 4),
 ])
-def test_sjlt_schedules_vs_oracle(cuda, monkeypatch, m, n, d, alpha):
+def test_sjlt_schedules_vs_oracle(cuda, tune, m, n, d, alpha):
     """Whole-tile (k-split) and persistent stream-K schedules, with and without
     TMA multicast across slab clusters: all match the oracle, and stream-K's
     cross-CTA tile fixup is bitwise repeatable."""
@@ -127,8 +127,8 @@ def test_sjlt_schedules_vs_oracle(cuda, monkeypatch, m, n, d, alpha):
     # whole-tile / stream-K schedules, each with and without slab-cluster
     # TMA multicast (opt-in path)
     for mode, mc in (("0", "0"), ("1", "0"), ("0", "1"), ("1", "1")):
-        monkeypatch.setenv("HSK_SJLT_STREAMK", mode)
-        monkeypatch.setenv("HSK_SJLT_MC", mc)
+        tune("HSK_SJLT_STREAMK", mode)
+        tune("HSK_SJLT_MC", mc)
         s1 = sk.apply_right_device(dA, op).to_host()
         s2 = sk.apply_right_device(dA, op).to_host()
         _close(s1, ref, np.linalg.norm(A))
@@ -291,8 +291,10 @@ def test_streamed_pinned_host_path_is_bit_identical(cuda, monkeypatch):
 @pytest.mark.parametrize("m,n,d,alpha", [
     (64, 64, 64, 8), (100, 1000, 64, 8), (3000, 9000, 64, 8), (257, 4100, 128, 16),
     (70, 20000, 64, 8), (1, 300, 64, 8),
+    # TK < 128: the quarter fold's 64 KB must still fit one ring slot
+    (130, 3000, 1024, 128), (70, 9000, 704, 88),
 ])
-def test_sjlt_paired_plan_vs_oracle(cuda, monkeypatch, m, n, d, alpha):
+def test_sjlt_paired_plan_vs_oracle(cuda, tune, m, n, d, alpha):
     """Chunked (block-construction) patterns with d/alpha = 8 take the paired
     plan (one tile read feeds a warp's two chunks, k-groups folded per row
     tile): oracle parity on every schedule, odd leading dimensions (cp.async
@@ -303,14 +305,14 @@ def test_sjlt_paired_plan_vs_oracle(cuda, monkeypatch, m, n, d, alpha):
     B = rng.standard_normal((n, m))
     res = {}
     for nochunk in ("0", "1"):
-        monkeypatch.setenv("HSK_SJLT_NOCHUNK", nochunk)
+        tune("HSK_SJLT_NOCHUNK", nochunk)
         op = sk.new_operator(sk.SJLT, n, d, seed=(m, n, d), alpha=alpha, construction=sk.BLOCK)
         b = op.blocks[0]
         ref = O.sjlt_right(A, b._pos, b._signs, d, b._scale)
         ref_t = O.sjlt_right_t(B, b._pos, b._signs, d, b._scale)
         assert device.block_state(b).flags == (0 if nochunk == "1" else device.HSK_SJLT_CHUNKED)
         for sched in ("0", "1"):
-            monkeypatch.setenv("HSK_SJLT_STREAMK", sched)
+            tune("HSK_SJLT_STREAMK", sched)
             for ld_pad in (0, 1):
                 dA = device.DeviceMatrix(m, n, ld=m + ld_pad)
                 dA.upload(A)

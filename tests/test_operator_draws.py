@@ -144,17 +144,6 @@ def test_dense_rows_bounds_and_subsets():
         sk.dense_rows(op, np.array([0]), np.array([6]))
 
 
-def test_jl_dimension_bound_reference_values():
-    assert sk.jl_dimension_bound(sk.GAUSSIAN, 0.5, 0.01) == (424, None)
-    assert sk.jl_dimension_bound(sk.SJLT, 0.5, 0.01) == (369, 185)
-    d, _ = sk.jl_dimension_bound(sk.SRHT, 0.5, 0.01, n=1000)
-    assert d == math.ceil(2.0 / 0.25 * math.log(4.0 * 1000 ** 2 / 0.01) ** 2 * math.log(400.0))
-    with pytest.raises(ValueError):
-        sk.jl_dimension_bound(sk.SRHT, 0.5, 0.01)
-    with pytest.raises(ValueError):
-        sk.jl_dimension_bound(sk.GAUSSIAN, 1.0, 0.01)
-
-
 def test_dense_accessor_contract():
     A = np.arange(12.0).reshape(3, 4)
     acc = sk.DenseAccessor(A)
