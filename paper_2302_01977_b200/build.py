@@ -21,7 +21,7 @@ INCLUDE = os.path.join(os.path.dirname(HERE), "include")
 LIB = os.path.join(HERE, "libhsk.so")
 OBJDIR = os.path.join(HERE, "_build")
 
-SOURCES = ["hsk_misc.cu", "hsk_sjlt.cu", "hsk_gauss.cu", "hsk_srht.cu", "hsk_comm.cu"]
+SOURCES = ["hsk_misc.cu", "hsk_sjlt.cu", "hsk_gauss.cu", "hsk_srht.cu", "hsk_comm.cu", "hsk_pqr.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC_FLAGS = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC,-fvisibility=hidden",
               "-Xptxas", "-v", "--expt-relaxed-constexpr"]
