@@ -167,6 +167,24 @@ HSK_API int hsk_ipc_close(void *ptr);
 HSK_API int hsk_sum_slices(const double *base, int32_t nslices, int64_t stride, int64_t rows,
                    int64_t cols, int64_t ld, double *out, int64_t ldo, void *stream);
 
+/* ------------------------------------------ HSS sweep dense kernels
+ * Column-pivoted Householder QR truncated at the numerical rank: replaces
+ * scipy.linalg.qr(S, mode="r", pivoting=True) (LAPACK dgeqp3) and the rank
+ * count of interpolative_decomposition (dense_kernels.py:54-82).
+ *   M: m x n column-major (ldm), OVERWRITTEN.  Pivoting as LAPACK's
+ *   dgeqp2/dlaqp2 (first position of maximal partial column norm; dlarfg
+ *   reflectors; dlaqp2 norm downdates).  Stops at the first step j with
+ *   |R_jj| < max(eps_abs, eps_rel |R_00|) (an all-zero M has rank 0).
+ *   perm: n int64 (perm[i] = column at pivot position i); R: the first
+ *   *rank rows of R in pivot order, column-major (ldr >= max(min(m,n),1));
+ *   rank: ONE int32 in DEVICE memory (stream-ordered; read it after a sync).
+ *   work: hsk_pqr_work_bytes(m, n) bytes of device scratch.
+ * One cooperative launch (co-resident CTAs, a grid barrier per step). */
+HSK_API int64_t hsk_pqr_work_bytes(int64_t m, int64_t n);
+HSK_API int hsk_pqr(double *M, int64_t m, int64_t n, int64_t ldm, double eps_rel, double eps_abs,
+                    int64_t *perm, double *R, int64_t ldr, int32_t *rank, void *work,
+                    int64_t work_bytes, void *stream);
+
 /* Strided async copy of `height` rows of `width` bytes (pitches in bytes);
  * kind 1 = host -> device, 2 = device -> host.  Used to stream row slabs of a
  * pinned host matrix through the kernels (copy / compute overlap). */

@@ -18,18 +18,41 @@ from . import sketching as _sk
 
 
 class DeviceSketch:
-    def __init__(self, A, n_cols_max: int, *, right: bool = True, transposed: bool = True):
+    """S = A R^T and S' = A^T R^T in HBM, column-major with `capacity` columns.
+
+    growable=True doubles the capacity when an increment does not fit (the
+    sketched columns are copied once into the larger buffer); otherwise an
+    overflow raises ValueError."""
+
+    def __init__(self, A, n_cols_max: int, *, right: bool = True, transposed: bool = True,
+                 growable: bool = False):
         self.A = _sk.device_matrix_of(A)
         self.capacity = int(n_cols_max)
+        self.growable = growable
         self.d = 0
         self.op = None
         self.S = _dev.DeviceMatrix.empty(self.A.rows, self.capacity) if right else None
         self.St = _dev.DeviceMatrix.empty(self.A.cols, self.capacity) if transposed else None
 
+    def _grow(self, need: int):
+        cap = max(need, 2 * self.capacity)
+        for name in ("S", "St"):
+            old = getattr(self, name)
+            if old is None:
+                continue
+            new = _dev.DeviceMatrix.empty(old.rows, cap)
+            if self.d:
+                new.t[:self.d].copy_(old.t[:self.d])
+            setattr(self, name, new)
+        self.capacity = cap
+
     def _sketch_block(self, blk):
         if self.d + blk.rows > self.capacity:
-            raise ValueError(f"sketch capacity {self.capacity} exceeded "
-                             f"(d={self.d}, block rows={blk.rows})")
+            if self.growable:
+                self._grow(self.d + blk.rows)
+            else:
+                raise ValueError(f"sketch capacity {self.capacity} exceeded "
+                                 f"(d={self.d}, block rows={blk.rows})")
         if self.S is not None:
             _dev.apply_block(blk, self.A, False, self.S, self.d)
         if self.St is not None:

@@ -13,6 +13,12 @@ untouched.  `uninstall()` restores the originals.
     import hsskit
     from paper_2302_01977_b200 import plugin
     plugin.install()          # every compress() sketch now runs on sm_100a
+
+`install(compressor=True)` additionally rebinds `hsskit.hss_compress._Driver`
+(resolved by `compress()` at call time, hss_compress.py:385) to
+hss_device.DeviceDriver: the reference's sweep logic with the sketch, the
+local samples, the gate QR / projections and the interpolative
+decompositions kept on the device.
 """
 
 from __future__ import annotations
@@ -53,8 +59,15 @@ def gpu_apply_right_transposed(A, op) -> np.ndarray:
     return _sk.apply_right_transposed_device(A, op).to_host()
 
 
-def install(mod=None) -> None:
-    """Route the reference's sketch products through libhsk.so."""
+def _compress_module(mod):
+    """hsskit.hss_compress of the package whose sketching module is `mod`."""
+    pkg = mod.__name__.rsplit(".", 1)[0]
+    return importlib.import_module(pkg + ".hss_compress")
+
+
+def install(mod=None, compressor: bool = False) -> None:
+    """Route the reference's sketch products through libhsk.so (and, with
+    compressor=True, the whole compression sweep through the device driver)."""
     _dev.require_cuda()
     mod = _module(mod)
     key = id(mod)
@@ -62,6 +75,13 @@ def install(mod=None) -> None:
         _saved[key] = (mod, mod.apply_right, mod.apply_right_transposed)
     mod.apply_right = gpu_apply_right
     mod.apply_right_transposed = gpu_apply_right_transposed
+    if compressor:
+        from . import hss_device
+        hc = _compress_module(mod)
+        ck = ("driver", id(hc))
+        if ck not in _saved:
+            _saved[ck] = (hc, hc._Driver)
+        hc._Driver = hss_device.device_driver_class(hc, base=_saved[ck][1])
 
 
 def uninstall(mod=None) -> None:
@@ -71,6 +91,13 @@ def uninstall(mod=None) -> None:
         _, ar, art = entry
         mod.apply_right = ar
         mod.apply_right_transposed = art
+    try:
+        hc = _compress_module(mod)
+    except ImportError:
+        return
+    dentry = _saved.pop(("driver", id(hc)), None)
+    if dentry is not None:
+        hc._Driver = dentry[1]
 
 
 def installed(mod=None) -> bool:
