@@ -300,7 +300,9 @@ extern "C" int hsk_pqr(double *M, int64_t m, int64_t n, int64_t ldm, double eps_
     int per_sm = 0;
     e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, pqr::kThreads, smem);
     if (e != cudaSuccess) return cuda_status(e, "pqr: occupancy");
-    per_sm = std::max(1, std::min(per_sm, 2));
+    // one CTA per SM: two factorisations (a node's row and column IDs) can
+    // then run concurrently on two streams, both grids co-resident
+    per_sm = std::max(1, std::min(per_sm, 1));
     // a CTA per ~kWarps columns, at most what is co-resident
     const int64_t want = (n + pqr::kWarps - 1) / pqr::kWarps;
     const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(want, (int64_t)sm_count() * per_sm));

@@ -105,33 +105,60 @@ def _project_out(Q, S):
     return resid
 
 
-def row_interpolative_decomposition(S, eps_rel: float, eps_abs: float):
-    """dense_kernels.row_interpolative_decomposition (:85-90) on the device:
-    S ~= U S[J, :], U[J, :] = I.  Returns (U (rows x r) device, J host intp).
+_SIDE_STREAM = {}
 
-    The column ID of S^T (interpolative_decomposition, :54-82) runs the
-    column-pivoted QR kernel hsk_pqr on a copy of S (row j of S = column j of
-    S^T, contiguous), stopped at the numerical rank, then solves the leading
-    triangle against the remaining columns."""
+
+def row_interpolative_decompositions(S1, S2, eps_rel: float, eps_abs: float):
+    """Two independent row IDs (a node's row and column samples), the second
+    on a side stream so the two latency-bound factorisations overlap."""
+    dev = torch.cuda.current_device()
+    side = _SIDE_STREAM.get(dev)
+    if side is None:
+        side = _SIDE_STREAM[dev] = torch.cuda.Stream()
+    cur = torch.cuda.current_stream()
+    side.wait_stream(cur)
+    with torch.cuda.stream(side):
+        M2 = _pqr_launch(S2, eps_rel, eps_abs)
+    M1 = _pqr_launch(S1, eps_rel, eps_abs)
+    r1 = _pqr_finish(S1, M1)
+    with torch.cuda.stream(side):
+        r2 = _pqr_finish(S2, M2)
+    cur.wait_stream(side)
+    r2[0].record_stream(cur)   # made on the side stream, used on this one
+    return r1, r2
+
+
+def _pqr_launch(S, eps_rel: float, eps_abs: float):
+    """Queue hsk_pqr on a copy of S on the current stream (no host sync)."""
     if eps_rel < 0 or eps_abs < 0:
         raise ValueError("tolerances must be nonnegative")
     rows, width = S.shape
-    dev = S.device
     if S.numel() == 0:
-        return torch.zeros((rows, 0), dtype=torch.float64, device=dev), np.empty(0, dtype=np.intp)
+        return None
+    dev = S.device
     M = S.contiguous().clone()           # (rows, width) row-major = S^T column-major, ld width
     m, n = width, rows                   # S^T is m x n
-    kmax = min(m, n)
-    ldr = max(kmax, 1)
+    ldr = max(min(m, n), 1)
     perm = torch.empty(n, dtype=torch.int64, device=dev)
-    Rb = torch.empty((n, ldr), dtype=torch.float64, device=dev)  # column-major kmax x n
+    Rb = torch.empty((n, ldr), dtype=torch.float64, device=dev)  # column-major min(m,n) x n
     rank_t = torch.zeros(1, dtype=torch.int32, device=dev)
-    L = _lib.load()
-    wbytes = int(L.hsk_pqr_work_bytes(m, n))
+    wbytes = int(_lib.load().hsk_pqr_work_bytes(m, n))
     work = torch.empty(wbytes, dtype=torch.uint8, device=dev)
     _lib.call("hsk_pqr", M.data_ptr(), m, n, width, float(eps_rel), float(eps_abs), perm.data_ptr(),
               Rb.data_ptr(), ldr, rank_t.data_ptr(), work.data_ptr(), wbytes,
               _dev.current_stream_ptr())
+    return (M, perm, Rb, rank_t, work)
+
+
+def _pqr_finish(S, launched):
+    """Rank readback, triangular solve and Y assembly (interpolative_decomposition
+    :70-82); returns (U = Y^T, J)."""
+    rows = S.shape[0]
+    dev = S.device
+    if launched is None:
+        return torch.zeros((rows, 0), dtype=torch.float64, device=dev), np.empty(0, dtype=np.intp)
+    _, perm, Rb, rank_t, _ = launched
+    n = rows
     r = int(rank_t.item())
     Y = torch.zeros((r, n), dtype=torch.float64, device=dev)
     if r > 0:
@@ -142,6 +169,17 @@ def row_interpolative_decomposition(S, eps_rel: float, eps_abs: float):
             Y[:, perm[r:]] = T
     J = perm[:r].cpu().numpy().astype(np.intp)
     return Y.T, J
+
+
+def row_interpolative_decomposition(S, eps_rel: float, eps_abs: float):
+    """dense_kernels.row_interpolative_decomposition (:85-90) on the device:
+    S ~= U S[J, :], U[J, :] = I.  Returns (U (rows x r) device, J host intp).
+
+    The column ID of S^T (interpolative_decomposition, :54-82) runs the
+    column-pivoted QR kernel hsk_pqr on a copy of S (row j of S = column j of
+    S^T, contiguous), stopped at the numerical rank, then solves the leading
+    triangle against the remaining columns."""
+    return _pqr_finish(S, _pqr_launch(S, eps_rel, eps_abs))
 
 
 def device_driver_class(hc, base=None):
@@ -380,7 +418,10 @@ def device_driver_class(hc, base=None):
             w_attr = "omega_first_row" if side == "row" else "omega_first_col"
             Q = getattr(dv, q_attr)
             if Q is None:
-                Q, om = _qr(S[:, :self.d])
+                # economic QR of a wide block (rows < d): the reflectors, Q and
+                # R's leading diagonal come from the first `rows` columns alone
+                # (the rest of R is never read), so factor only those
+                Q, om = _qr(S[:, :min(self.d, S.shape[0])])
                 setattr(dv, q_attr, Q)
                 diag = torch.diagonal(om)
                 setattr(node, w_attr, abs(float(diag[0].item())) if diag.numel() else 0.0)
@@ -399,8 +440,8 @@ def device_driver_class(hc, base=None):
             tnode = self.tree.nodes[nid]
             node = self.nodes[nid]
             dv = self.dv[nid]
-            dv.U, node.J_row = row_interpolative_decomposition(dv.Sr.view(), eps_rel, eps_abs)
-            dv.V, node.J_col = row_interpolative_decomposition(dv.Sc.view(), eps_rel, eps_abs)
+            (dv.U, node.J_row), (dv.V, node.J_col) = row_interpolative_decompositions(
+                dv.Sr.view(), dv.Sc.view(), eps_rel, eps_abs)
             dv.Jr_t = dv.Jc_t = None
             if tnode.is_leaf:
                 base = np.arange(tnode.lo, tnode.hi)
@@ -455,4 +496,5 @@ def compress(A, tree, opts, hss_compress=None):
         hc._Driver = saved
 
 
-__all__ = ["device_driver_class", "compress", "row_interpolative_decomposition", "ColBuf"]
+__all__ = ["device_driver_class", "compress", "row_interpolative_decomposition",
+           "row_interpolative_decompositions", "ColBuf"]
