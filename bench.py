@@ -291,6 +291,25 @@ def time_launches(fn, reps: int, warmup: int, stream, flush=None):
     return statistics.mean(a.elapsed_time(b) for a, b in evs)
 
 
+def fp64_tensor_peak(stream) -> float:
+    """FP64 tensor-pipe TFLOP/s of this GPU, measured live (MEASURED_PEAKS.json
+    has no FP64 entry): hsk_dmma_probe, best of 3."""
+    import torch
+    from paper_2302_01977_b200 import _lib
+    L = _lib.load()
+    x = torch.zeros(1, dtype=torch.float64, device="cuda")
+    iters = 20000
+    best = 0.0
+    for _ in range(4):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        _lib.call("hsk_dmma_probe", iters, x.data_ptr(), stream.cuda_stream)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        best = max(best, L.hsk_dmma_probe_flops(iters) / (e0.elapsed_time(e1) * 1e-3) / 1e12)
+    return best
+
+
 def roofline(bytes_per_launch: float, ms: float, peak: float):
     ach = bytes_per_launch / (ms * 1e-3) / 1e9
     return {"bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s", "frac": ach / peak,
@@ -404,6 +423,7 @@ def run_headline(args, ctx, out):
     cublas_ms = time_launches(cublas, 5, 2, stream)
     holder.clear()
     del SG, St
+    fp64_peak = fp64_tensor_peak(stream)
 
     # end to end through the public API: host A -> H2D -> kernel -> D2H S
     e2e = e2e_pageable = None
@@ -489,7 +509,13 @@ def run_headline(args, ctx, out):
                      "transposed_value": flops / (gt_ms * 1e-3) / 1e12,
                      "cublas_dgemm_ms": cublas_ms,
                      "cublas_dgemm_tflops": flops / (cublas_ms * 1e-3) / 1e12,
-                     "vs_cublas": cublas_ms / g_ms},
+                     "vs_cublas": cublas_ms / g_ms,
+                     "roofline": {"bound": "tensor", "achieved": flops / (g_ms * 1e-3) / 1e12,
+                                  "peak": fp64_peak, "unit": "TFLOP/s",
+                                  "frac": flops / (g_ms * 1e-3) / 1e12 / fp64_peak,
+                                  "cublas_frac": flops / (cublas_ms * 1e-3) / 1e12 / fp64_peak,
+                                  "peak_source": "measured live: hsk_dmma_probe (independent "
+                                                 "DMMA.8x8x4 chains on every SM)"}},
     })
 
 

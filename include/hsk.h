@@ -120,6 +120,13 @@ HSK_API int hsk_gauss_apply(const double *A, int64_t rows, int64_t cols, int64_t
                     const double *R, int64_t n, int32_t d, double *S, int64_t lds,
                     int64_t col0, void *stream);
 
+/* FP64 tensor-pipe peak probe (no reference counterpart): sm_count * 2 CTAs of
+ * 8 warps, each `iters` x 8 independent DMMA.8x8x4; hsk_dmma_probe_flops gives
+ * the flops of one launch.  Time it with events for the FP64 roofline
+ * denominator of hsk_gauss_apply (bench.py).  scratch: one device double. */
+HSK_API int64_t hsk_dmma_probe_flops(int64_t iters);
+HSK_API int hsk_dmma_probe(int64_t iters, double *scratch, void *stream);
+
 /* ------------------------------------------------------------------ SRHT
  * Replaces SrhtBlock._transform (sketching.py:162-176):
  *   S[r, col0 + t] = scale * FWHT_npad(pad(x_r) .* signs)[sample[t]]

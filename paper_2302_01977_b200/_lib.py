@@ -57,6 +57,8 @@ SIGNATURES = {
     "hsk_pqr_work_bytes": (_c_i64, [_c_i64, _c_i64]),
     "hsk_pqr": (ctypes.c_int, [_c_p, _c_i64, _c_i64, _c_i64, _c_d, _c_d, _c_p, _c_p, _c_i64, _c_p, _c_p,
                                _c_i64, _c_p]),
+    "hsk_dmma_probe_flops": (_c_i64, [_c_i64]),
+    "hsk_dmma_probe": (ctypes.c_int, [_c_i64, _c_p, _c_p]),
     "hsk_memcpy2d": (ctypes.c_int, [_c_p, _c_i64, _c_p, _c_i64, _c_i64, _c_i64, _c_i32, _c_p]),
 }
 

@@ -37,6 +37,10 @@ struct Args {
     int64_t lds, col0;
     int a16, b16;  // 16-byte cp.async allowed
     int ntiles_n;
+    // split-K: blockIdx.y = split; splits > 1 store partial tiles to ws
+    // (split-major, column-major M x N each) for the ordered reduction
+    int splits;
+    double *ws;
 };
 
 __device__ __forceinline__ void dmma(double (&c)[2], double a, double b) {
@@ -81,7 +85,10 @@ __global__ void __launch_bounds__(WGM * WGN * 32) gauss_kernel(const Args p) {
     const int64_t nt = blockIdx.x % p.ntiles_n, mt = blockIdx.x / p.ntiles_n;
     const int64_t m0 = mt * BM, n0 = nt * BN;
     const int wm0 = (warp / WGN) * WM, wn0 = (warp % WGN) * WN;
-    const int64_t ktiles = (p.K + BK - 1) / BK;
+    const int64_t ktiles_all = (p.K + BK - 1) / BK;
+    const int64_t kper = (ktiles_all + p.splits - 1) / p.splits;
+    const int64_t kt0 = std::min<int64_t>(ktiles_all, (int64_t)blockIdx.y * kper);
+    const int64_t ktiles = std::min<int64_t>(ktiles_all, kt0 + kper) - kt0;
 
     // interior tiles (all rows/columns/k in range, 16-byte aligned operands)
     // take an unpredicated copy path
@@ -89,7 +96,7 @@ __global__ void __launch_bounds__(WGM * WGN * 32) gauss_kernel(const Args p) {
     auto load_stage = [&](int64_t kt, int s) {
         double *sA = sm + s * SM::STAGE;
         double *sB = sA + SM::A_ELEMS;
-        const int64_t k0 = kt * BK;
+        const int64_t k0 = (kt0 + kt) * BK;
         if (full_mn && k0 + BK <= p.K) {
             if (!TRANS) {
 #pragma unroll
@@ -191,6 +198,8 @@ __global__ void __launch_bounds__(WGM * WGN * 32) gauss_kernel(const Args p) {
     cp_async_wait<0>();
 
     const int fr = lane >> 2, fc = lane & 3;
+    double *out = p.splits > 1 ? p.ws + (int64_t)blockIdx.y * p.M * p.N : p.S + p.col0 * p.lds;
+    const int64_t ldo = p.splits > 1 ? p.M : p.lds;
 #pragma unroll
     for (int i = 0; i < MF; ++i) {
         const int64_t m = m0 + wm0 + i * 8 + fr;
@@ -198,9 +207,22 @@ __global__ void __launch_bounds__(WGM * WGN * 32) gauss_kernel(const Args p) {
 #pragma unroll
         for (int j = 0; j < NF; ++j) {
             const int64_t c = n0 + wn0 + j * 8 + 2 * fc;
-            if (c < p.N) p.S[(p.col0 + c) * p.lds + m] = acc[i][j][0];
-            if (c + 1 < p.N) p.S[(p.col0 + c + 1) * p.lds + m] = acc[i][j][1];
+            if (c < p.N) out[c * ldo + m] = acc[i][j][0];
+            if (c + 1 < p.N) out[(c + 1) * ldo + m] = acc[i][j][1];
         }
+    }
+}
+
+// S[:, col0 + c] = sum over splits s (in order) of ws[s] -- deterministic
+__global__ void splitk_reduce_kernel(const double *__restrict__ ws, int splits, int64_t M, int64_t N,
+                                     double *__restrict__ S, int64_t lds, int64_t col0) {
+    const int64_t total = M * N, stride = M * N;
+    for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < total;
+         q += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t c = q / M, m = q - c * M;
+        double acc = ws[q];
+        for (int s = 1; s < splits; ++s) acc += ws[s * stride + q];
+        S[(col0 + c) * lds + m] = acc;
     }
 }
 
@@ -213,9 +235,39 @@ static int launch(Args a, cudaStream_t st) {
     a.ntiles_n = (int)((a.N + BN - 1) / BN);
     const int64_t grid = ((a.M + BM - 1) / BM) * a.ntiles_n;
     HSK_REQUIRE(grid < (1ll << 31), HSK_EINVAL, "gauss: grid too large");
-    kern<<<(unsigned)grid, WGM * WGN * 32, SM::BYTES, st>>>(a);
+    if (a.splits < 1) a.splits = 1;
+    if (a.splits > 1) {
+        void *ws = nullptr;
+        int *flags = nullptr;
+        int rc = stream_workspace(st, (size_t)a.splits * a.M * a.N * sizeof(double), 1, &ws, &flags);
+        if (rc) return rc;
+        a.ws = static_cast<double *>(ws);
+    }
+    kern<<<dim3((unsigned)grid, (unsigned)a.splits, 1), WGM * WGN * 32, SM::BYTES, st>>>(a);
     HSK_CHECK_LAUNCH("gauss_kernel");
+    if (a.splits > 1) {
+        splitk_reduce_kernel<<<sm_count() * 4, 256, 0, st>>>(a.ws, a.splits, a.M, a.N, a.S, a.lds,
+                                                            a.col0);
+        HSK_CHECK_LAUNCH("splitk_reduce_kernel");
+    }
     return HSK_OK;
+}
+
+// FP64 tensor-pipe peak probe: independent DMMA.8x8x4 chains only (8 per
+// warp), for the roofline denominator of the Gaussian product (bench.py)
+__global__ void dmma_probe_kernel(double *out, int64_t iters) {
+    double c[8][2];
+    const double a = threadIdx.x * 1e-9, b = 1.0 + blockIdx.x * 1e-9;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) c[i][0] = c[i][1] = 0.0;
+    for (int64_t it = 0; it < iters; ++it) {
+#pragma unroll
+        for (int i = 0; i < 8; ++i) dmma(c[i], a, b);
+    }
+    double s = 0.0;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) s += c[i][0] + c[i][1];
+    if (s == 1234.5) out[0] = s;  // keeps the chains live
 }
 
 }  // namespace gauss
@@ -252,6 +304,7 @@ extern "C" int hsk_gauss_apply(const double *A, int64_t rows, int64_t cols, int6
     a.col0 = col0;
     a.a16 = ((reinterpret_cast<uintptr_t>(A) & 15) == 0) && (lda % 2 == 0);
     a.b16 = ((reinterpret_cast<uintptr_t>(R) & 15) == 0) && (n % 2 == 0);
+    a.splits = tuning().gauss_splits > 0 ? tuning().gauss_splits : 1;
     cudaStream_t st = as_stream(stream);
     // 64 x 64 tiles, 2 x 2 warps (32 x 32 DMMA tiles each), BK 32, 2 stages: many
     // resident CTAs keep the FP64 tensor pipe fed (measured best among warp
@@ -285,4 +338,15 @@ extern "C" int hsk_gauss_apply(const double *A, int64_t rows, int64_t cols, int6
                      : gauss::launch<64, 64, 0, 2, 4, 4>(a, st);
 #endif
     return trans ? gauss::launch<64, 64, 1, 2, 2, 2>(a, st) : gauss::launch<64, 64, 0, 2, 2, 2>(a, st);
+}
+
+extern "C" int64_t hsk_dmma_probe_flops(int64_t iters) {
+    return (int64_t)sm_count() * 2 * 8 * iters * 8 * (2 * 8 * 8 * 4);
+}
+
+extern "C" int hsk_dmma_probe(int64_t iters, double *scratch, void *stream) {
+    HSK_REQUIRE(iters >= 1 && scratch, HSK_EINVAL, "dmma probe: bad arguments");
+    gauss::dmma_probe_kernel<<<sm_count() * 2, 8 * 32, 0, as_stream(stream)>>>(scratch, iters);
+    HSK_CHECK_LAUNCH("dmma_probe_kernel");
+    return HSK_OK;
 }

@@ -1049,9 +1049,13 @@ static int launch(ApplyArgs a, const Geom &g, cudaStream_t st) {
     // cluster released it, which runs the slab CTAs in lockstep behind the
     // slowest; without it each CTA runs ahead on its own and L2 absorbs the skew.
     a.mc = 1;
-    if (HSK_SJLT_MULTICAST && tuning().sjlt_mc == 1 && prod && (a.mode == 0 || a.mode == 3) && ks == 1 &&
-        (a.nslabs == 2 || a.nslabs == 4 || a.nslabs == 8) && (a.mode == 3 || a.tk % a.nslabs == 0))
-        a.mc = a.nslabs;
+    // HSK_SJLT_MC=1: clusters of all nslabs slab CTAs; =2/4/8: clusters of that
+    // many consecutive slabs of a row tile (nslabs a multiple of it)
+    const int mc_req = tuning().sjlt_mc == 1 ? a.nslabs : tuning().sjlt_mc;
+    if (HSK_SJLT_MULTICAST && mc_req >= 2 && prod && (a.mode == 0 || a.mode == 3) && ks == 1 &&
+        (mc_req == 2 || mc_req == 4 || mc_req == 8) && a.nslabs % mc_req == 0 &&
+        (a.mode == 3 || a.tk % mc_req == 0))
+        a.mc = mc_req;
     CUtensorMap tmap;
     memset(&tmap, 0, sizeof(tmap));
     if (a.mode == 0) {

@@ -202,6 +202,9 @@ def apply_right(A, op: SketchOperator) -> np.ndarray:
     buf = _pinned_host_buffer(A)
     if buf is not None:
         return _streamed(buf, op, transpose=False)
+    buf = _pageable_host_buffer(A)
+    if buf is not None:
+        return _streamed(buf, op, transpose=False, staged=True)
     return apply_right_device(A, op).to_host()
 
 
@@ -215,6 +218,9 @@ def apply_right_transposed(A, op: SketchOperator) -> np.ndarray:
     buf = _pinned_host_buffer(A)
     if buf is not None:
         return _streamed(buf, op, transpose=True)
+    buf = _pageable_host_buffer(A)
+    if buf is not None:
+        return _streamed(buf, op, transpose=True, staged=True)
     return apply_right_transposed_device(A, op).to_host()
 
 
@@ -246,7 +252,44 @@ def _pinned_host_buffer(A):
     return A if pinned else None
 
 
-def _streamed(buf: np.ndarray, op: SketchOperator, transpose: bool) -> np.ndarray:
+def _pageable_host_buffer(A):
+    """A large F-ordered float64 host array that is NOT page-locked (what the
+    reference's callers hand over): streamed through pinned staging."""
+    if isinstance(A, _dev.DeviceMatrix) or _is_accessor(A) or not isinstance(A, np.ndarray):
+        return None
+    if A.ndim != 2 or A.dtype != np.float64 or not A.flags.f_contiguous:
+        return None
+    return A if A.nbytes >= STREAM_MIN_BYTES else None
+
+
+_STAGE_POOL = None
+
+
+def _stage_pool():
+    global _STAGE_POOL
+    if _STAGE_POOL is None:
+        import concurrent.futures
+        import os
+        _STAGE_POOL = concurrent.futures.ThreadPoolExecutor(max_workers=min(8, os.cpu_count() or 1))
+    return _STAGE_POOL
+
+
+def _stage_copy(dst: np.ndarray, src: np.ndarray):
+    """dst[...] = src with the pool's threads over column blocks (numpy's copy
+    loops release the GIL, so the pageable -> pinned memcpy runs in parallel)."""
+    pool = _stage_pool()
+    k = dst.shape[1]
+    parts = min(pool._max_workers, max(1, k))
+    bounds = [(k * i) // parts for i in range(parts + 1)]
+    futs = [pool.submit(np.copyto, dst[:, a:b], src[:, a:b]) for a, b in zip(bounds[:-1], bounds[1:]) if b > a]
+    for f in futs:
+        f.result()
+
+
+def _streamed(buf: np.ndarray, op: SketchOperator, transpose: bool, staged: bool = False) -> np.ndarray:
+    """Slab pipeline.  staged=True (pageable host array): each slab is first
+    copied by host threads into one of two pinned staging buffers (the copy
+    of slab i+1 overlaps slab i's DMA and kernels), then DMA'd from there."""
     import torch
     from . import _lib
     rows, cols = buf.shape
@@ -269,6 +312,10 @@ def _streamed(buf: np.ndarray, op: SketchOperator, transpose: bool) -> np.ndarra
     ev_in = [torch.cuda.Event() for _ in range(nslab)]
     ev_k = [torch.cuda.Event() for _ in range(nslab)]
     base = buf.ctypes.data
+    stage = None
+    if staged:  # two pinned slab images: S: h x cols (pitch h); S': rows x h
+        shape = (cols, step) if not transpose else (step, rows)
+        stage = [torch.empty(shape, dtype=torch.float64, pin_memory=True) for _ in range(2)]
     for i in range(nslab):
         r0 = i * step
         r1 = min(m_out, r0 + step)
@@ -278,7 +325,21 @@ def _streamed(buf: np.ndarray, op: SketchOperator, transpose: bool) -> np.ndarra
         b = slabs[i % 2]
         if i >= 2:
             h2d.wait_event(ev_k[i - 2])       # slab buffer free
-        if transpose:   # columns [r0, r1) of A: h contiguous columns of `rows` doubles
+        if staged:
+            if i >= 2:
+                ev_in[i - 2].synchronize()    # staging buffer's DMA has landed
+            sg = stage[i % 2]
+            if transpose:
+                img = sg[:h].numpy().T        # rows x h, F-ordered
+                _stage_copy(img, buf[:, r0:r1])
+                _lib.call("hsk_memcpy2d", b.ptr, b.ld * 8, sg.data_ptr(), rows * 8, rows * 8, h, 1,
+                          h2d.cuda_stream)
+            else:
+                img = sg[:, :h].numpy().T     # h x cols view, pitch step
+                _stage_copy(img, buf[r0:r1, :])
+                _lib.call("hsk_memcpy2d", b.ptr, b.ld * 8, sg.data_ptr(), step * 8, h * 8, cols, 1,
+                          h2d.cuda_stream)
+        elif transpose:   # columns [r0, r1) of A: h contiguous columns of `rows` doubles
             _lib.call("hsk_memcpy2d", b.ptr, b.ld * 8, base + r0 * rows * 8, rows * 8, rows * 8, h, 1,
                       h2d.cuda_stream)
         else:           # rows [r0, r1) of A: `cols` columns of h doubles, pitch `rows`

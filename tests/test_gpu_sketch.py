@@ -288,6 +288,25 @@ def test_streamed_pinned_host_path_is_bit_identical(cuda, monkeypatch):
         np.testing.assert_array_equal(sk.apply_right_transposed(B, op), ref_t)
 
 
+def test_streamed_pageable_host_path_is_bit_identical(cuda, monkeypatch):
+    """Plain (pageable) numpy arrays -- what the reference's callers pass --
+    are staged slab by slab through pinned buffers by host threads; same
+    bytes as the one-shot device path, ragged last slab included."""
+    monkeypatch.setattr(sk, "STREAM_MIN_BYTES", 1)
+    rng = np.random.default_rng(22)
+    m, n = 1111, 1500
+    A = np.asfortranarray(rng.standard_normal((m, n)))
+    B = np.asfortranarray(rng.standard_normal((n, m)))
+    assert sk._pinned_host_buffer(A) is None and sk._pageable_host_buffer(A) is not None
+    for kind, kw in ((sk.SJLT, dict(alpha=4, construction=sk.BLOCK)), (sk.GAUSSIAN, {}),
+                     (sk.SRHT, {})):
+        op = sk.new_operator(kind, n, 96, seed=6, **kw)
+        ref = sk.apply_right_device(device.DeviceMatrix.from_host(A), op).to_host()
+        np.testing.assert_array_equal(sk.apply_right(A, op), ref)
+        ref_t = sk.apply_right_transposed_device(device.DeviceMatrix.from_host(B), op).to_host()
+        np.testing.assert_array_equal(sk.apply_right_transposed(B, op), ref_t)
+
+
 @pytest.mark.parametrize("m,n,d,alpha", [
     (64, 64, 64, 8), (100, 1000, 64, 8), (3000, 9000, 64, 8), (257, 4100, 128, 16),
     (70, 20000, 64, 8), (1, 300, 64, 8),

@@ -86,6 +86,33 @@ def main():
                 byt = n * n * 8 + n * d * 8
                 out[f"{c}_{'St' if tr else 'S'}"] = {"ms": ms, "GBs": byt / ms / 1e6,
                                                      "frac": byt / ms / 1e6 / PEAK}
+        elif c in ("c5shard", "c5shard_t"):
+            # BASELINE configs[4] at 8 GPUs: the 16384 x 131072 row shard of the
+            # n = 131072 kernel matrix; S = A_g R^T (d = 2048, alpha = 8) and the
+            # shard's S' partial A_g^T R_g^T (16384 input indices, 131072 output rows)
+            n, rows, d = 131072, 16384, 2048
+            key = ("c5shard",)
+            if key not in mats:
+                mats.clear()
+                torch.cuda.empty_cache()
+                pts = matgen.kernel_points(n, 16, 0)
+                mats[key] = matgen.gaussian_kernel(n, 16, 1.0, 1e-2, row0=0, nrows=rows, points=pts)
+            A = mats[key]
+            op = sk.new_operator(sk.SJLT, n, d, np.random.SeedSequence((0, 0)), alpha=8,
+                                 construction="block")
+            if c == "c5shard":
+                blk = op.blocks[0]
+                S = device.DeviceMatrix.empty(rows, d)
+                ms = timeit(lambda: device.apply_block(blk, A, False, S, 0), max(3, args.reps // 4))
+                byt = rows * n * 8 + rows * d * 8
+                out["c5shard_S"] = {"ms": ms, "GBs": byt / ms / 1e6, "frac": byt / ms / 1e6 / PEAK}
+            else:
+                from paper_2302_01977_b200 import distributed as hd
+                sub = hd.restrict_operator(op, 0, rows).blocks[0]
+                S = device.DeviceMatrix.empty(n, d)
+                ms = timeit(lambda: device.apply_block(sub, A, True, S, 0), max(3, args.reps // 4))
+                byt = rows * n * 8 + n * d * 8
+                out["c5shard_St"] = {"ms": ms, "GBs": byt / ms / 1e6, "frac": byt / ms / 1e6 / PEAK}
         elif c == "c2g":
             n, d = 16384, 512
             A = mat(n)
@@ -135,7 +162,7 @@ def main():
             ms = timeit(lambda: device.apply_block(blk, A, True, S, 0), max(3, args.reps // 4))
             out["c4_St"] = {"ms": ms, "GBs": byt / ms / 1e6, "frac": byt / ms / 1e6 / PEAK}
         print(json.dumps({k: v for k, v in out.items() if k.startswith(c)}), flush=True)
-    print(json.dumps({"env": {k: os.environ.get(k) for k in ("HSK_SJLT_CFG", "HSK_GAUSS_CFG")},
+    print(json.dumps({"env": {k: v for k, v in os.environ.items() if k.startswith("HSK_")},
                       "results": out}))
 
 
