@@ -20,8 +20,47 @@ CASES = {
 }
 
 
+def c5shard(direction):
+    """BASELINE configs[4] row shard at 8 GPUs: 16384 x 131072 of the n = 131072
+    kernel matrix, SJLT d = 2048 alpha = 8 (S, or the shard's S' partial)."""
+    from paper_2302_01977_b200 import distributed as hd
+    n, rows, d = 131072, 16384, 2048
+    A = matgen.gaussian_kernel(n, 16, 1.0, 1e-2, row0=0, nrows=rows,
+                               points=matgen.kernel_points(n, 16, 0))
+    op = sk.new_operator(sk.SJLT, n, d, np.random.SeedSequence((0, 0)), alpha=8,
+                         construction="block")
+    if direction == "S":
+        blk, S = op.blocks[0], device.DeviceMatrix.empty(rows, d)
+    else:
+        blk, S = hd.restrict_operator(op, 0, rows).blocks[0], device.DeviceMatrix.empty(n, d)
+    for _ in range(2):
+        device.apply_block(blk, A, direction == "St", S, 0)
+    torch.cuda.synchronize()
+
+
+def pqr():
+    """The C1 compression's largest interpolative decomposition shape: a
+    2000 x 2048 sample (rank ~1990) through hsk_pqr."""
+    from paper_2302_01977_b200 import hss_device
+    rng = np.random.default_rng(0)
+    rows, width = 2000, 2048
+    sv = np.logspace(0, -9, rows)
+    U0, _ = np.linalg.qr(rng.standard_normal((rows, rows)))
+    V0, _ = np.linalg.qr(rng.standard_normal((width, rows)))
+    S = torch.as_tensor((U0 * sv) @ V0.T, device="cuda")
+    for _ in range(2):
+        hss_device.row_interpolative_decomposition(S, 1e-12, 1e-300)
+    torch.cuda.synchronize()
+
+
 def main():
     for arg in sys.argv[1:]:
+        if arg.startswith("c5shard_"):
+            c5shard(arg.split("_")[1])
+            continue
+        if arg == "pqr":
+            pqr()
+            continue
         case, direction = arg.split("_")
         kind, n, d, alpha, cons, mat = CASES[case]
         A = (matgen.toeplitz_sin(n) if mat == "toep" else
