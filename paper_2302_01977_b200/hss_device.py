@@ -108,13 +108,18 @@ def _project_out(Q, S):
 _SIDE_STREAM = {}
 
 
-def row_interpolative_decompositions(S1, S2, eps_rel: float, eps_abs: float):
-    """Two independent row IDs (a node's row and column samples), the second
-    on a side stream so the two latency-bound factorisations overlap."""
+def _side_stream():
     dev = torch.cuda.current_device()
     side = _SIDE_STREAM.get(dev)
     if side is None:
         side = _SIDE_STREAM[dev] = torch.cuda.Stream()
+    return side
+
+
+def row_interpolative_decompositions(S1, S2, eps_rel: float, eps_abs: float):
+    """Two independent row IDs (a node's row and column samples), the second
+    on a side stream so the two latency-bound factorisations overlap."""
+    side = _side_stream()
     cur = torch.cuda.current_stream()
     side.wait_stream(cur)
     with torch.cuda.stream(side):
@@ -209,6 +214,7 @@ def device_driver_class(hc, base=None):
                 if los == list(range(0, self.n, b)):
                     self._uniform_leaf = b
             self._leaf_batch = None   # (c0, c1) -> (sr, sc, R) of every leaf, this round
+            self._gate_cache = None   # both sides' gate results of the node being gated
 
         # -------------------------------------------------------- sketch
         def init_sketch(self) -> None:
@@ -410,13 +416,15 @@ def device_driver_class(hc, base=None):
             return rr, rc
 
         # ------------------------------------------- gating / compression
-        def _gate_side(self, node, side: str, eps_rel: float, eps_abs: float) -> bool:
-            nid = self._nid[id(node)]
-            dv = self.dv[nid]
+        def _gate_stage1(self, node, side: str):
+            """Device part of _gate_side (:270-286) up to the Frobenius test:
+            the first QR if the side has no basis yet, the projection and the
+            two norms.  Returns (S_hat, [omega_first?, lhs, ref] tensors)."""
+            dv = self.dv[self._nid[id(node)]]
             S = (dv.Sr if side == "row" else dv.Sc).view()
             q_attr = "Qr" if side == "row" else "Qc"
-            w_attr = "omega_first_row" if side == "row" else "omega_first_col"
             Q = getattr(dv, q_attr)
+            first = None
             if Q is None:
                 # economic QR of a wide block (rows < d): the reflectors, Q and
                 # R's leading diagonal come from the first `rows` columns alone
@@ -424,17 +432,63 @@ def device_driver_class(hc, base=None):
                 Q, om = _qr(S[:, :min(self.d, S.shape[0])])
                 setattr(dv, q_attr, Q)
                 diag = torch.diagonal(om)
-                setattr(node, w_attr, abs(float(diag[0].item())) if diag.numel() else 0.0)
+                first = diag[:1].abs() if diag.numel() else torch.zeros(1, dtype=torch.float64,
+                                                                        device=S.device)
             window = S[:, self.d:]
             S_hat = _project_out(Q, window)
-            lhs, ref = torch.stack([torch.linalg.norm(S_hat), torch.linalg.norm(window)]).tolist()
-            # hss_compress.frobenius_stop (:106-117) on the two norms
-            if lhs < eps_abs or ref == 0.0 or lhs < eps_rel * ref:
-                return True
-            qi, omi = _qr(S_hat)
-            setattr(dv, q_attr, torch.cat([Q, qi], dim=1))
-            return hc.rank_deficiency_stop(torch.diagonal(omi).cpu().numpy(),
-                                           getattr(node, w_attr), eps_rel, eps_abs)
+            norms = torch.stack([torch.linalg.norm(S_hat), torch.linalg.norm(window)])
+            return S_hat, first, norms
+
+        def _gate_both(self, node, eps_rel: float, eps_abs: float):
+            """Both sides' gates of a node (the reference evaluates row then
+            column, :341-342, always both): the column side's device work runs
+            on the side stream, and the scalars of both sides cross to the host
+            together -- two host syncs per node instead of up to six."""
+            cur = torch.cuda.current_stream()
+            side = _side_stream()
+            side.wait_stream(cur)
+            with torch.cuda.stream(side):
+                hat_c, first_c, norms_c = self._gate_stage1(node, "col")
+            hat_r, first_r, norms_r = self._gate_stage1(node, "row")
+            cur.wait_stream(side)
+            dv = self.dv[self._nid[id(node)]]
+            for t in (hat_c, first_c, norms_c, dv.Qc):   # made on the side stream, used here
+                if t is not None:
+                    t.record_stream(cur)
+            parts = [norms_r, norms_c] + [f for f in (first_r, first_c) if f is not None]
+            vals = torch.cat(parts).tolist()
+            (lhs_r, ref_r, lhs_c, ref_c), rest = vals[:4], vals[4:]
+            if first_r is not None:
+                node.omega_first_row = rest.pop(0)
+            if first_c is not None:
+                node.omega_first_col = rest.pop(0)
+            out = {}
+            pending = []
+            for sname, hat, lhs, ref, q_attr, w_attr in (
+                    ("row", hat_r, lhs_r, ref_r, "Qr", "omega_first_row"),
+                    ("col", hat_c, lhs_c, ref_c, "Qc", "omega_first_col")):
+                # hss_compress.frobenius_stop (:106-117) on the two norms
+                if lhs < eps_abs or ref == 0.0 or lhs < eps_rel * ref:
+                    out[sname] = True
+                    continue
+                qi, omi = _qr(hat)
+                setattr(dv, q_attr, torch.cat([getattr(dv, q_attr), qi], dim=1))
+                pending.append((sname, torch.diagonal(omi), w_attr))
+            if pending:
+                diags = torch.cat([d for _, d, _ in pending]).cpu().numpy()
+                o = 0
+                for sname, dg, w_attr in pending:
+                    k = dg.numel()
+                    out[sname] = hc.rank_deficiency_stop(diags[o:o + k], getattr(node, w_attr),
+                                                         eps_rel, eps_abs)
+                    o += k
+            return out
+
+        def _gate_side(self, node, side: str, eps_rel: float, eps_abs: float) -> bool:
+            key = (id(node), self.d, eps_rel, eps_abs)
+            if side == "row" or self._gate_cache is None or self._gate_cache[0] != key:
+                self._gate_cache = (key, self._gate_both(node, eps_rel, eps_abs))
+            return self._gate_cache[1][side]
 
         def compress_node(self, nid: int, eps_rel: float, eps_abs: float) -> None:
             tnode = self.tree.nodes[nid]
