@@ -453,16 +453,17 @@ def run_headline(args, ctx, out):
     page = np.empty((N, N), order="F")
     page[...] = A_host
     del host, A_host
-    sk.apply_right(page, op)
+    for _ in range(max(3, args.warmup)):   # staging + result buffers into the pinned pool
+        S_host = sk.apply_right(page, op)
     torch.cuda.synchronize()
     ctx.barrier()
     t0 = time.perf_counter()
     e0.record(stream)
-    for _ in range(3):
+    for _ in range(e2e_steps):
         S_host = sk.apply_right(page, op)
     e1.record(stream)
     torch.cuda.synchronize()
-    pg_ms, = ctx.max_over_ranks([e0.elapsed_time(e1) / 3])
+    pg_ms, = ctx.max_over_ranks([e0.elapsed_time(e1) / e2e_steps])
     e2e_pageable = {"value": world * a_bytes / (pg_ms * 1e-3) / 1e9, "unit": "GB/s",
                     "h2d_bytes_per_step": a_bytes, "d2h_bytes_per_step": int(S_host.nbytes),
                     "ms_per_step": pg_ms, "path": "sketching.apply_right(pageable numpy array)"}

@@ -232,7 +232,7 @@ def apply_right_transposed(A, op: SketchOperator) -> np.ndarray:
 # rows) depend only on the same rows (columns) of A, so the result is
 # bit-identical to the one-shot device path.
 STREAM_MIN_BYTES = 256 << 20
-STREAM_SLABS = 8
+STREAM_SLABS = int(__import__("os").environ.get("HSK_STREAM_SLABS", "8"))
 
 
 def _pinned_host_buffer(A):
@@ -270,7 +270,8 @@ def _stage_pool():
     if _STAGE_POOL is None:
         import concurrent.futures
         import os
-        _STAGE_POOL = concurrent.futures.ThreadPoolExecutor(max_workers=min(8, os.cpu_count() or 1))
+        n = int(os.environ.get("HSK_STAGE_THREADS", "0")) or min(8, os.cpu_count() or 1)
+        _STAGE_POOL = concurrent.futures.ThreadPoolExecutor(max_workers=n)
     return _STAGE_POOL
 
 
