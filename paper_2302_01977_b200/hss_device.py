@@ -17,8 +17,10 @@ while every matrix it touches stays in HBM:
 
   * the sketch lives in an adaptive.DeviceSketch (S and S' appended in place
     by the libhsk kernels; no host concatenation, no D2H of S);
-  * A is the device copy (DeviceAccessor / the accessor's cached upload):
-    diagonal and cross blocks are gathered on the device;
+  * A is the device copy (DeviceAccessor / the accessor's cached upload) for
+    the sketch; diagonal and cross blocks are requested through the accessor's
+    extract() exactly as the reference requests them (gathered in HBM for a
+    DeviceAccessor);
   * the random rows R^T(I_tau, cols) are materialised on the device from the
     operator's device state (bit-identical to the reference's dense_rows);
   * local samples and reduced randoms grow in preallocated column buffers;
@@ -360,11 +362,18 @@ def device_driver_class(hc, base=None):
             return sr, sc
 
         def _extract(self, rows, cols):
-            """A.extract(rows, cols) from the device copy of A."""
-            t = self.A_dev.t
-            r = torch.as_tensor(np.asarray(rows, dtype=np.int64), device="cuda")
-            c = torch.as_tensor(np.asarray(cols, dtype=np.int64), device="cuda")
-            return t.index_select(0, c).index_select(1, r).T.contiguous()
+            """A.extract(rows, cols) on the device.  A DeviceAccessor's entries
+            are gathered from HBM; any other accessor is asked through its own
+            extract() -- the reference's matrix-access contract (the diagonal
+            and cross blocks are the only entries requested, hss_compress.py
+            module docstring and :213-229) -- and the block uploaded."""
+            if isinstance(self.A, _sk.DeviceAccessor):
+                t = self.A_dev.t
+                r = torch.as_tensor(np.asarray(rows, dtype=np.int64), device="cuda")
+                c = torch.as_tensor(np.asarray(cols, dtype=np.int64), device="cuda")
+                return t.index_select(0, c).index_select(1, r).T.contiguous()
+            blk = np.asarray(self.A.extract(rows, cols), dtype=np.float64)
+            return torch.as_tensor(np.ascontiguousarray(blk), device="cuda")
 
         def _fetch_cross_blocks(self, nid: int) -> None:
             tnode = self.tree.nodes[nid]
@@ -379,7 +388,8 @@ def device_driver_class(hc, base=None):
             dv = self.dv[nid]
             rng = (0, self.width)
             if tnode.is_leaf:
-                dv.D = self.A_dev.t[tnode.lo:tnode.hi, tnode.lo:tnode.hi].T.contiguous()
+                idx = np.arange(tnode.lo, tnode.hi)
+                dv.D = self._extract(idx, idx)
                 sr, sc, _ = self._leaf_windows(nid, rng)
             else:
                 self._fetch_cross_blocks(nid)
