@@ -14,11 +14,6 @@ def pytest_configure(config):
 
     from paper_2302_01977_b200 import plugin
     plugin.install(hs, compressor=True)
-    config._hsk_installed = True
-
-
-def pytest_report_header(config):
     import hsskit.hss_compress as hc
-    import hsskit.sketching as hs
-    return [f"hsk drop-in: sketching.apply_right -> {hs.apply_right.__module__}."
-            f"{hs.apply_right.__name__}; hss_compress._Driver -> {hc._Driver.__name__}"]
+    print(f"hsk drop-in: sketching.apply_right -> {hs.apply_right.__module__}."
+          f"{hs.apply_right.__name__}; hss_compress._Driver -> {hc._Driver.__name__}", flush=True)
