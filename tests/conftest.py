@@ -29,6 +29,19 @@ def pytest_configure(config):
     config.addinivalue_line("markers", "slow: long-running")
 
 
+# Modules that drive the reference package (hsskit from baseline/_ref, installed
+# by __graft_entry__.build()).  Without it they FAIL (never skip); they run
+# last so that, under `pytest -x`, a missing install cannot hide the results of
+# the engine's own parity tests.
+_REFERENCE_MODULES = ("test_gpu_plugin.py", "test_gpu_hss_device.py", "test_gpu_reference_suite.py")
+
+
+def pytest_collection_modifyitems(session, config, items):
+    def uses_reference(item):
+        return os.path.basename(str(item.fspath)) in _REFERENCE_MODULES
+    items.sort(key=uses_reference)   # stable: original order within each group
+
+
 @pytest.fixture(scope="session")
 def golden():
     arrays = np.load(os.path.join(GOLDEN_DIR, "golden.npz"))
