@@ -25,7 +25,27 @@
 namespace hsk {
 namespace gauss {
 
-constexpr int BK = 32;  // (16 measured 1-3 % slower: twice the barriers per DMMA)
+// BK = 16, 2 stages, 2 x 2 warps: 38 KB of shared memory per CTA, so the
+// register file (120 per thread) sets 4 resident CTAs = 16 warps per SM.  r02
+// sweep on C2 (S / S' ms, cuBLAS 7.71): BK 32 2-st 8.16 / 8.20 (3 CTAs/SM);
+// BK 16 2-st 7.95 / 7.89; 3-st 7.96 / 7.91; 4-st 7.98 / 8.01; BK 8 4-st
+// 8.09 / 8.01; 2 x 4 warps 8.58 / 8.44; 5 CTAs (94 registers) 8.15 / 8.06.
+#ifndef HSK_GAUSS_BK
+#define HSK_GAUSS_BK 16
+#endif
+#ifndef HSK_GAUSS_STAGES
+#define HSK_GAUSS_STAGES 2
+#endif
+#ifndef HSK_GAUSS_MINB
+#define HSK_GAUSS_MINB 4  // <= 128 registers: 4 resident CTAs
+#endif
+#ifndef HSK_GAUSS_WGM
+#define HSK_GAUSS_WGM 2
+#endif
+#ifndef HSK_GAUSS_WGN
+#define HSK_GAUSS_WGN 2
+#endif
+constexpr int BK = HSK_GAUSS_BK;
 constexpr int PKK = BK + 4;  // pitch of k-contiguous tiles (== 4 mod 16)
 
 struct Args {
@@ -74,7 +94,7 @@ struct Smem {
 
 // WGM x WGN warps, each a (BM/WGM) x (BN/WGN) tile of 8x8 DMMA fragments.
 template <int BM, int BN, int TRANS, int WGM, int WGN, int STAGES>
-__global__ void __launch_bounds__(WGM * WGN * 32) gauss_kernel(const Args p) {
+__global__ void __launch_bounds__(WGM * WGN * 32, HSK_GAUSS_MINB) gauss_kernel(const Args p) {
     using SM = Smem<BM, BN, TRANS, STAGES>;
     constexpr int NT = WGM * WGN * 32;
     constexpr int WM = BM / WGM, WN = BN / WGN;
@@ -352,7 +372,8 @@ extern "C" int hsk_gauss_apply(const double *A, int64_t rows, int64_t cols, int6
         return trans ? gauss::launch<64, 64, 1, 2, 4, 4>(a, st)
                      : gauss::launch<64, 64, 0, 2, 4, 4>(a, st);
 #endif
-    return trans ? gauss::launch<64, 64, 1, 2, 2, 2>(a, st) : gauss::launch<64, 64, 0, 2, 2, 2>(a, st);
+    return trans ? gauss::launch<64, 64, 1, HSK_GAUSS_WGM, HSK_GAUSS_WGN, HSK_GAUSS_STAGES>(a, st)
+                 : gauss::launch<64, 64, 0, HSK_GAUSS_WGM, HSK_GAUSS_WGN, HSK_GAUSS_STAGES>(a, st);
 }
 
 extern "C" int64_t hsk_dmma_probe_flops(int64_t iters) {
