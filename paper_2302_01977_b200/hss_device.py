@@ -120,19 +120,41 @@ def _side_stream():
 
 def row_interpolative_decompositions(S1, S2, eps_rel: float, eps_abs: float):
     """Two independent row IDs (a node's row and column samples), the second
-    on a side stream so the two latency-bound factorisations overlap."""
+    on a side stream so the two latency-bound factorisations overlap; both
+    ranks and pivot orders come to the host in one copy."""
     side = _side_stream()
     cur = torch.cuda.current_stream()
     side.wait_stream(cur)
     with torch.cuda.stream(side):
         M2 = _pqr_launch(S2, eps_rel, eps_abs)
     M1 = _pqr_launch(S1, eps_rel, eps_abs)
-    r1 = _pqr_finish(S1, M1)
-    with torch.cuda.stream(side):
-        r2 = _pqr_finish(S2, M2)
     cur.wait_stream(side)
-    r2[0].record_stream(cur)   # made on the side stream, used on this one
-    return r1, r2
+    if M2 is not None:
+        for t in M2:
+            t.record_stream(cur)
+    host = _pqr_host([M1, M2])
+    return _pqr_finish(S1, M1, host[0]), _pqr_finish(S2, M2, host[1])
+
+
+def _pqr_host(launched):
+    """(rank, pivot order) of each queued factorisation, one D2H copy."""
+    parts, sizes = [], []
+    for L in launched:
+        if L is None:
+            sizes.append(None)
+            continue
+        _, perm, _, rank_t, _ = L
+        parts += [rank_t.to(torch.int64), perm]
+        sizes.append(perm.numel())
+    flat = torch.cat(parts).cpu().numpy() if parts else np.empty(0, dtype=np.int64)
+    out, o = [], 0
+    for sz in sizes:
+        if sz is None:
+            out.append(None)
+            continue
+        out.append((int(flat[o]), flat[o + 1:o + 1 + sz]))
+        o += 1 + sz
+    return out
 
 
 def _pqr_launch(S, eps_rel: float, eps_abs: float):
@@ -157,16 +179,16 @@ def _pqr_launch(S, eps_rel: float, eps_abs: float):
     return (M, perm, Rb, rank_t, work)
 
 
-def _pqr_finish(S, launched):
-    """Rank readback, triangular solve and Y assembly (interpolative_decomposition
-    :70-82); returns (U = Y^T, J)."""
+def _pqr_finish(S, launched, host=None):
+    """Triangular solve and Y assembly (interpolative_decomposition :70-82)
+    from the rank and pivot order; returns (U = Y^T, J)."""
     rows = S.shape[0]
     dev = S.device
     if launched is None:
         return torch.zeros((rows, 0), dtype=torch.float64, device=dev), np.empty(0, dtype=np.intp)
     _, perm, Rb, rank_t, _ = launched
+    r, perm_h = host if host is not None else _pqr_host([launched])[0]
     n = rows
-    r = int(rank_t.item())
     Y = torch.zeros((r, n), dtype=torch.float64, device=dev)
     if r > 0:
         R = Rb[:, :r].T                  # r x n, pivot order
@@ -174,8 +196,7 @@ def _pqr_finish(S, launched):
         if r < n:
             T = torch.linalg.solve_triangular(R[:, :r], R[:, r:], upper=True)
             Y[:, perm[r:]] = T
-    J = perm[:r].cpu().numpy().astype(np.intp)
-    return Y.T, J
+    return Y.T, perm_h[:r].astype(np.intp)
 
 
 def row_interpolative_decomposition(S, eps_rel: float, eps_abs: float):
@@ -217,6 +238,8 @@ def device_driver_class(hc, base=None):
                     self._uniform_leaf = b
             self._leaf_batch = None   # (c0, c1) -> (sr, sc, R) of every leaf, this round
             self._gate_cache = None   # both sides' gate results of the node being gated
+            self._n_leaves = len(leaves)
+            self._leaves_with_D = 0
 
         # -------------------------------------------------------- sketch
         def init_sketch(self) -> None:
@@ -326,7 +349,7 @@ def device_driver_class(hc, base=None):
             tnode = self.tree.nodes[nid]
             dv = self.dv[nid]
             if (self._uniform_leaf is not None and c0 == self.d and
-                    all(self.dv[t.nid].D is not None for t in self.tree.nodes if t.is_leaf)):
+                    self._leaves_with_D == self._n_leaves):
                 sr, sc, R = self._leaf_batch_windows(c0, c1)
                 i = tnode.lo // self._uniform_leaf
                 return sr[i], sc[i], R[i]
@@ -390,6 +413,7 @@ def device_driver_class(hc, base=None):
             if tnode.is_leaf:
                 idx = np.arange(tnode.lo, tnode.hi)
                 dv.D = self._extract(idx, idx)
+                self._leaves_with_D += 1
                 sr, sc, _ = self._leaf_windows(nid, rng)
             else:
                 self._fetch_cross_blocks(nid)
