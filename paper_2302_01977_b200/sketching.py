@@ -270,7 +270,7 @@ def _stage_pool():
     if _STAGE_POOL is None:
         import concurrent.futures
         import os
-        n = int(os.environ.get("HSK_STAGE_THREADS", "0")) or min(8, os.cpu_count() or 1)
+        n = int(os.environ.get("HSK_STAGE_THREADS", "0")) or min(32, os.cpu_count() or 1)
         _STAGE_POOL = concurrent.futures.ThreadPoolExecutor(max_workers=n)
     return _STAGE_POOL
 

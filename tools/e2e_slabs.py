@@ -1,3 +1,5 @@
+"""e2e A/B of the host-array slab pipeline: HSK_STAGE_THREADS / HSK_STREAM_SLABS
+on a pageable and a pinned C2 matrix (wall clock per sketching.apply_right)."""
 import os, sys, time, json
 sys.path.insert(0, '.')
 import numpy as np, torch
@@ -5,7 +7,7 @@ from paper_2302_01977_b200 import matgen, sketching as sk
 N=16384
 A = matgen.gaussian_kernel(N, 8, 0.5)
 op = sk.new_operator(sk.SJLT, N, 512, np.random.SeedSequence((0, 0)), alpha=4, construction=sk.BLOCK)
-page = np.asfortranarray(A.to_host())
+page = np.array(A.to_host(), order='F', copy=True)   # a plain pageable copy
 host = torch.empty((N, N), dtype=torch.float64, pin_memory=True); host.copy_(A.t[:, :N]); pin = host.numpy().T
 res = {}
 for name, arr in (("pageable", page), ("pinned", pin)):
