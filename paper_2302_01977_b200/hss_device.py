@@ -102,8 +102,8 @@ def _project_out(Q, S):
     """dense_kernels.project_out (:38-51): two block Gram-Schmidt passes."""
     if Q.numel() == 0:
         return S.clone()
-    resid = S - Q @ (Q.T @ S)
-    resid -= Q @ (Q.T @ resid)
+    resid = torch.addmm(S, Q, Q.T @ S, alpha=-1.0)
+    resid.addmm_(Q, Q.T @ resid, alpha=-1.0)
     return resid
 
 
@@ -227,6 +227,7 @@ def device_driver_class(hc, base=None):
             self._nid = {id(nd): i for i, nd in enumerate(self.nodes)}
             self._ds = None
             self._blk_cache = {}
+            self._Rt = None           # dense R^T, n x width (ColBuf)
             leaves = [t for t in tree.nodes if t.is_leaf]
             sizes = {t.size for t in leaves}
             # batched leaf updates need equal leaves tiling [0, n) in order
@@ -253,6 +254,9 @@ def device_driver_class(hc, base=None):
             self._ds.start(self.op)
             torch.cuda.current_stream().synchronize()
             self.sketch_seconds += time.perf_counter() - start
+            self._Rt = None
+            for blk in self.op.blocks:
+                self._append_dense_rows(blk)
 
         def extend_sketch(self) -> None:
             self.rounds += 1
@@ -263,6 +267,7 @@ def device_driver_class(hc, base=None):
             self._ds.extend(self.op)      # only the new block touches A
             torch.cuda.current_stream().synchronize()
             self.sketch_seconds += time.perf_counter() - start
+            self._append_dense_rows(self.op.blocks[-1])
             self._leaf_batch = None
 
         def _sketch_rows(self, which: str, lo: int, hi: int, c0: int, c1: int):
@@ -286,35 +291,38 @@ def device_driver_class(hc, base=None):
                 ent = ent[1]
             return st, ent
 
+        def _append_dense_rows(self, blk):
+            """R^T of a new block for every input index, appended once to the
+            device buffer the windows read (the rows a leaf needs are then a
+            view) -- the blocks' dense_rows (sketching.py:140-141, :184-191,
+            :353-360) for I = all indices: exact values (0, +-scale, the
+            Gaussian entries)."""
+            st, ent = self._block_dev(blk)
+            n = self.n
+            if blk.kind == "sjlt":
+                pos, val = ent
+                full = torch.zeros((n, blk.rows), dtype=torch.float64, device="cuda")
+                full.scatter_(1, pos, val)
+                cols = full.T
+            elif blk.kind == "gaussian":
+                cols = ent[0]
+            else:
+                signs, sample = ent
+                i = torch.arange(n, device="cuda", dtype=torch.int64)[None, :]
+                x = sample[:, None] & i
+                for sh in (32, 16, 8, 4, 2, 1):
+                    x = x ^ (x >> sh)
+                H = 1.0 - 2.0 * (x & 1).to(torch.float64)
+                cols = H * signs[None, :n] * st.scale
+            if self._Rt is None:
+                self._Rt = ColBuf(cols.T)        # n x width (R^T), column-major rows
+            else:
+                self._Rt.append(cols.T)
+
         def _random_rows_dev(self, lo: int, hi: int, c0: int, c1: int):
-            """R^T(lo:hi, c0:c1) on the device -- sketching.dense_rows
-            (:460-476) with the blocks' dense_rows (:140-141, :184-191,
-            :353-360): exact values (0, +-scale, the Gaussian entries)."""
-            h = hi - lo
-            out = torch.zeros((h, c1 - c0), dtype=torch.float64, device="cuda")
-            b0 = 0
-            for blk in self.op.blocks:
-                b1 = b0 + blk.rows
-                s0, s1 = max(c0, b0), min(c1, b1)
-                if s0 < s1:
-                    st, ent = self._block_dev(blk)
-                    if blk.kind == "sjlt":
-                        pos, val = ent
-                        full = torch.zeros((h, blk.rows), dtype=torch.float64, device="cuda")
-                        full.scatter_(1, pos[lo:hi], val[lo:hi])
-                        out[:, s0 - c0:s1 - c0] = full[:, s0 - b0:s1 - b0]
-                    elif blk.kind == "gaussian":
-                        out[:, s0 - c0:s1 - c0] = ent[0][s0 - b0:s1 - b0, lo:hi].T
-                    else:
-                        signs, sample = ent
-                        i = torch.arange(lo, hi, device="cuda", dtype=torch.int64)[:, None]
-                        x = i & sample[s0 - b0:s1 - b0][None, :]
-                        for sh in (32, 16, 8, 4, 2, 1):
-                            x = x ^ (x >> sh)
-                        H = 1.0 - 2.0 * (x & 1).to(torch.float64)
-                        out[:, s0 - c0:s1 - c0] = signs[lo:hi, None] * H * st.scale
-                b0 = b1
-            return out
+            """R^T(lo:hi, c0:c1) (sketching.dense_rows, :460-476): a view of the
+            dense buffer."""
+            return self._Rt.view(c0, c1)[lo:hi]
 
         # ------------------------------------------------- sample updates
         @staticmethod
@@ -336,11 +344,11 @@ def device_driver_class(hc, base=None):
             w = c1 - c0
             leaves = [t for t in self.tree.nodes if t.is_leaf]
             Ds = torch.stack([self.dv[t.nid].D for t in sorted(leaves, key=lambda t: t.lo)])
-            R = self._random_rows_dev(0, self.n, c0, c1).view(L, b, w)
+            R = self._random_rows_dev(0, self.n, c0, c1).reshape(L, b, w)
             Sr = self._ds.S.t[c0:c1, :self.n].T.reshape(L, b, w)
             Sc = self._ds.St.t[c0:c1, :self.n].T.reshape(L, b, w)
-            sr = Sr - torch.bmm(Ds, R)
-            sc = Sc - torch.bmm(Ds.transpose(1, 2), R)
+            sr = torch.baddbmm(Sr, Ds, R, alpha=-1.0)
+            sc = torch.baddbmm(Sc, Ds.transpose(1, 2), R, alpha=-1.0)
             self._leaf_batch = (key, (sr, sc, R))
             return sr, sc, R
 
@@ -354,8 +362,8 @@ def device_driver_class(hc, base=None):
                 i = tnode.lo // self._uniform_leaf
                 return sr[i], sc[i], R[i]
             R = self._random_rows_dev(tnode.lo, tnode.hi, c0, c1)
-            sr = self._sketch_rows("r", tnode.lo, tnode.hi, c0, c1) - dv.D @ R
-            sc = self._sketch_rows("c", tnode.lo, tnode.hi, c0, c1) - dv.D.T @ R
+            sr = torch.addmm(self._sketch_rows("r", tnode.lo, tnode.hi, c0, c1), dv.D, R, alpha=-1.0)
+            sc = torch.addmm(self._sketch_rows("c", tnode.lo, tnode.hi, c0, c1), dv.D.T, R, alpha=-1.0)
             return sr, sc, R
 
         def _idx(self, nid: int, side: str):
@@ -375,12 +383,16 @@ def device_driver_class(hc, base=None):
             l, r = tnode.left.nid, tnode.right.nid
             d1, d2 = self.dv[l], self.dv[r]
             sr = torch.cat([
-                d1.Sr.view(c0, c1).index_select(0, self._idx(l, "r")) - dv.B12 @ d2.Rc.view(c0, c1),
-                d2.Sr.view(c0, c1).index_select(0, self._idx(r, "r")) - dv.B21 @ d1.Rc.view(c0, c1),
+                torch.addmm(d1.Sr.view(c0, c1).index_select(0, self._idx(l, "r")), dv.B12,
+                            d2.Rc.view(c0, c1), alpha=-1.0),
+                torch.addmm(d2.Sr.view(c0, c1).index_select(0, self._idx(r, "r")), dv.B21,
+                            d1.Rc.view(c0, c1), alpha=-1.0),
             ])
             sc = torch.cat([
-                d1.Sc.view(c0, c1).index_select(0, self._idx(l, "c")) - dv.B21.T @ d2.Rr.view(c0, c1),
-                d2.Sc.view(c0, c1).index_select(0, self._idx(r, "c")) - dv.B12.T @ d1.Rr.view(c0, c1),
+                torch.addmm(d1.Sc.view(c0, c1).index_select(0, self._idx(l, "c")), dv.B21.T,
+                            d2.Rr.view(c0, c1), alpha=-1.0),
+                torch.addmm(d2.Sc.view(c0, c1).index_select(0, self._idx(r, "c")), dv.B12.T,
+                            d1.Rr.view(c0, c1), alpha=-1.0),
             ])
             return sr, sc
 
