@@ -104,24 +104,31 @@ __device__ __forceinline__ bool mbar_test_wait(uint64_t *bar, uint32_t parity) {
     return ok != 0;
 }
 
+// The wait loops are PTX loops inside one asm block (labels are local to its
+// braces): a C++ loop around
+// try_wait is a potentially divergent branch to ptxas, and any such branch on
+// a path into the SJLT walker makes it bracket every walker branch with
+// BSSY/BSYNC (see hsk_sjlt.cu).
 __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
-    while (!mbar_try_wait(bar, parity)) {
-    }
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "HSK_WAIT:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra HSK_WAIT;\n\t}"
+        ::"r"(smem_u32(bar)), "r"(parity)
+        : "memory");
 }
 
 // try_wait with an explicit suspend-time hint (ns): a waiting warp sleeps
 // until the phase completes or the hint elapses instead of re-polling
 __device__ __forceinline__ void mbar_wait_hint(uint64_t *bar, uint32_t parity, uint32_t ns) {
-    uint32_t ok;
-    do {
-        asm volatile(
-            "{\n\t.reg .pred p;\n\t"
-            "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n\t"
-            "selp.u32 %0, 1, 0, p;\n\t}"
-            : "=r"(ok)
-            : "r"(smem_u32(bar)), "r"(parity), "r"(ns)
-            : "memory");
-    } while (!ok);
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "HSK_WAITH:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n\t"
+        "@!p bra HSK_WAITH;\n\t}"
+        ::"r"(smem_u32(bar)), "r"(parity), "r"(ns)
+        : "memory");
 }
 
 // TMA bulk copy global -> shared, completion counted on an mbarrier

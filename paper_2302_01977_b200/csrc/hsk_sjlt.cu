@@ -69,10 +69,7 @@ constexpr int kXposeProducers = HSK_XPOSE_PRODUCERS;
 #ifndef HSK_SJLT_MULTICAST
 #define HSK_SJLT_MULTICAST 0
 #endif
-// The stream-K instantiations keep the (runtime-inert) multicast branches:
-// measured 3.5 % faster on C2 with them than without (code layout; the
-// walker SASS is identical), while the whole-tile ones are faster without.
-#define MC_ON ((HSK_SJLT_MULTICAST || SK) && p.mc > 1)
+#define MC_ON (HSK_SJLT_MULTICAST && p.mc > 1)
 
 namespace hsk {
 namespace sjlt {
@@ -414,6 +411,32 @@ __global__ void sjlt_plan_kernel(const int32_t *__restrict__ pos, const int8_t *
 // transposed on the way in by four cp.async producer warps: element (kk, c)
 // at kk*TM + (c ^ (kk%32)) doubles -- conflict-free for the consumer.
 
+constexpr int kMaxGroups = 160;  // stream-K groups (<= SMs)
+
+// n / d for 0 <= n < 2^31 by multiply-high and shift (d = 1: m = 0, the
+// identity): the kernel prologue divides with it so its values stay on the
+// warp-uniform datapath (a division routine's results land in per-lane
+// registers, and a chunk loop bounded by them is divergent to ptxas)
+struct FastDiv {
+    uint32_t d, m, s;
+};
+
+static inline FastDiv make_fastdiv(uint32_t d) {
+    FastDiv f{d, 0u, 0u};
+    if (d > 1) {
+        uint32_t l = 0;
+        while ((1ull << l) < d) ++l;  // ceil(log2 d)
+        const uint32_t p = 31 + l;
+        f.m = (uint32_t)(((1ull << p) + d - 1) / d);
+        f.s = p - 32;
+    }
+    return f;
+}
+
+__device__ __forceinline__ uint32_t fdiv(uint32_t n, const FastDiv &f) {
+    return f.d == 1 ? n : __umulhi(n, f.m) >> f.s;
+}
+
 struct ApplyArgs {
     const double *A;
     int64_t lda;
@@ -440,19 +463,285 @@ struct ApplyArgs {
     // TMA multicast: the nslabs CTAs of a row tile form a cluster of `mc`
     // CTAs; each loads 1/mc of every tile for all of them (1 = off)
     int mc;
-    int wait_ns;  // consumer full-barrier wait: try_wait suspend hint (0 = default)
+    int wait_ns;  // consumer full-barrier wait: try_wait suspend hint (ns)
     int pf;  // mode 0: chunks prefetched into L2 beyond the shared-memory ring
     int64_t units;
+    FastDiv div_slabs, div_ks;
+    int32_t per;                   // whole-tile CTAs: chunks per k-split rank
+    // stream-K, per group g (host-computed): first chunk, first row tile,
+    // chunks in the first segment, segments, and roles (bit 0: the first
+    // segment is the tail of a cut tile; bits 1..: count of later groups
+    // holding the tails of the tile the last segment heads)
+    int32_t sk_g[kMaxGroups + 1][4];
     double *ws;  // per-CTA partial tile (SLAB x TM doubles)
     int *flags;  // per-CTA "partial published" flags (left zero)
 };
 
-// All NW warps own buckets (NW*DB per CTA slab) and share the producer work:
-// warp 0 / lane 0 issues TMA + bulk copies (mode 0); in modes 1/2 every lane
-// issues its share of 8-byte cp.async for the chunk STAGES-1 ahead.
+// Control flow of the apply kernel (measured on C2 S: 72 BSSY in the round-1
+// kernel, a chain link 6 instructions, 4 of them reconvergence markers).
+// ptxas brackets a branch with BSSY/BSYNC reconvergence markers unless it can
+// prove the predicate warp-uniform; it ignores bra.uni, and a word loaded from
+// shared memory is per-lane to it, so every chain link and loop-back branch of
+// a walker got brackets.  The 64-row walkers therefore pass their branch
+// predicates through vote.sync.any (tools/gen_consumers.py), and the kernel
+// keeps every loop around a walker provably uniform: chunk and segment counts
+// come from launch constants through 32-bit fast divisions and host-computed
+// stream-K tables (a 64-bit division is a called routine with a per-lane fast
+// path), the chunk loop restarts its own counter per segment (an inner loop
+// that continues the outer loop's counter is divergent to ptxas), the producer
+// role test reads a broadcast warp index, and the consumers' epilogue stores
+// through selected addresses (out-of-range rows and buckets go to a sink) with
+// the k-split and paired-fold exchanges done by every warp.
+// Per-CTA ring bookkeeping shared by the producer and consumer paths.
+struct Ring {
+    unsigned char *stage0;  // first ring slot (1024-byte aligned)
+    uint64_t *full, *empty;
+    int64_t u0, u1, tile0;  // chunk range in the flattened (row tile, chunk) order
+    int nloc, stages, g0, slab;
+    uint32_t gs_bytes, en_bytes, tile_bytes;
+};
+
+// sink of the epilogue's out-of-range stores
+__device__ double g_sjlt_sink[32];
+
+// row offset and chunk index of the CTA's j-th chunk (stream-K: 32-bit
+// arithmetic, the host keeps units < 2^31)
+template <int TM, bool SK>
+__device__ __forceinline__ void chunk_of(const ApplyArgs &p, const Ring &R, int j, int64_t &r0, int64_t &c) {
+    if constexpr (SK) {
+        const uint32_t u = (uint32_t)R.u0 + (uint32_t)j;
+        const uint32_t t = u / (uint32_t)p.nchunks;
+        r0 = (int64_t)t * TM;
+        c = u - t * (uint32_t)p.nchunks;
+    } else {
+        r0 = R.tile0 * TM;
+        c = R.u0 - R.tile0 * p.nchunks + j;
+    }
+}
+
+// one TMA tile (S) or 16 x TM boxes (S') plus the chunk's plan slice into
+// the slot of chunk j, completing on its full barrier (one issuing lane)
+template <int TM, bool TRANS, bool SK>
+__device__ __forceinline__ void issue_tma(const ApplyArgs &p, const CUtensorMap *tmap, const Ring &R, int j) {
+    unsigned char *st = R.stage0 + (size_t)(j % R.stages) * p.stage_bytes;
+    uint64_t *bar = &R.full[j % R.stages];
+    int64_t r0, c;
+    chunk_of<TM, SK>(p, R, j, r0, c);
+    mbar_arrive_expect_tx(bar, R.tile_bytes + R.gs_bytes + R.en_bytes);
+    uint32_t mc_off = 0;
+#if HSK_SJLT_MULTICAST
+    if (p.mc > 1) {  // this CTA's share of the tile, for every CTA of the cluster
+        const uint32_t rank = cluster_ctarank();
+        const uint16_t mask = (uint16_t)((1u << p.mc) - 1u);
+        if constexpr (TRANS) {
+            for (int kb = (int)rank; kb < p.tk / 16; kb += p.mc)
+                tma_load_2d_mc(st + kb * TM * 128, tmap, (int)(c * p.tk + kb * 16), (int)r0, bar, mask);
+        } else {
+            const int part = p.tk / p.mc;  // the box is TM x part
+            tma_load_2d_mc(st + (size_t)rank * part * TM * 8, tmap, (int)r0, (int)(c * p.tk + rank * part),
+                           bar, mask);
+        }
+        mc_off = rank * (uint32_t)(p.tk / p.mc);
+    } else
+#endif
+    if constexpr (TRANS) {  // S': one 16 x TM box per 16 input indices
+        for (int kb = 0; kb < p.tk / 16; ++kb)
+            tma_load_2d(st + kb * TM * 128, tmap, (int)(c * p.tk + kb * 16), (int)r0, bar);
+    } else {
+        tma_load_2d(st, tmap, (int)r0, (int)(c * p.tk), bar);
+    }
+    // keep the HBM stream ahead of the ring: chunk j + pf into L2 (chunks
+    // stages .. stages+pf-1 are requested together with the first loads)
+    const int jp = j < R.stages ? j + R.stages : j + p.pf;
+    if (p.pf > 0 && jp < R.nloc && (j < R.stages ? j < p.pf : true)) {
+        int64_t rp, cp;
+        chunk_of<TM, SK>(p, R, jp, rp, cp);
+        tma_prefetch_2d(tmap, (int)rp, (int)(cp * p.tk + mc_off));
+    }
+    bulk_g2s(st + p.gs_off, p.gptr + c * p.gstride + R.g0, R.gs_bytes, bar);
+    bulk_g2s(st + p.en_off, p.ent + c * p.estride, R.en_bytes, bar);
+}
+
+// cp.async producer of chunk j: threads [0, pnt) of the producer set
+template <int TM, bool TRANS, bool XPOSE, bool SK>
+__device__ __forceinline__ void issue_coop(const ApplyArgs &p, const Ring &R, int j, int ptid, int pnt) {
+    unsigned char *st = R.stage0 + (size_t)(j % R.stages) * p.stage_bytes;
+    uint64_t *bar = &R.full[j % R.stages];
+    int64_t r0, c;
+    chunk_of<TM, SK>(p, R, j, r0, c);
+    const int64_t k0 = c * p.tk;
+    const int kc = (int)(p.n - k0 < p.tk ? p.n - k0 : p.tk);
+    if (ptid == 0) {
+        mbar_arrive_expect_tx(bar, R.gs_bytes + R.en_bytes);
+        bulk_g2s(st + p.gs_off, p.gptr + c * p.gstride + R.g0, R.gs_bytes, bar);
+        bulk_g2s(st + p.en_off, p.ent + c * p.estride, R.en_bytes, bar);
+    }
+    double *sx = reinterpret_cast<double *>(st);
+    const int nel = p.tk * TM;
+    if (XPOSE) {
+        // (kk, rr) = A[k0+kk, r0+rr] -> sx[kk*TM + (rr ^ (kk%32))]; lanes
+        // along kk: coalesced reads, conflict-free swizzled writes
+        const int tk = p.tk;
+        const bool full_rows = r0 + TM <= p.m_out;
+        for (int kk = ptid; kk < tk; kk += pnt) {
+            const int sw = kk & 31;
+            const double *src = p.A + r0 * p.lda + k0 + kk;
+            double *dbase = sx + kk * TM;
+            if (kk < kc && full_rows) {
+#pragma unroll 8
+                for (int rr = 0; rr < TM; ++rr, src += p.lda) cp_async8(dbase + (rr ^ sw), src, true);
+            } else {
+                const bool vk = kk < kc;
+                for (int rr = 0; rr < TM; ++rr, src += p.lda) {
+                    const bool v = vk && (r0 + rr < p.m_out);
+                    cp_async8(dbase + (rr ^ sw), v ? src : p.A, v);
+                }
+            }
+        }
+    } else if (TRANS) {
+        // unaligned A: the S' tile layout of the TMA path, written by
+        // 8-byte cp.async -- (kk, rr) at (kk/16)*TM*128 + rr*128 +
+        // ((kk%16)*8 ^ 16*(rr%8)); lanes along kk (coalesced reads)
+        const int tk = p.tk;
+        for (int kk = ptid; kk < tk; kk += pnt) {
+            const double *src = p.A + r0 * p.lda + k0 + kk;
+            unsigned char *dbase = st + (kk >> 4) * TM * 128;
+            const int kx = (kk & 15) << 3;
+            const bool vk = kk < kc;
+            for (int rr = 0; rr < TM; ++rr, src += p.lda) {
+                const bool v = vk && (r0 + rr < p.m_out);
+                cp_async8(dbase + rr * 128 + (kx ^ ((rr & 7) << 4)), v ? src : p.A, v);
+            }
+        }
+    } else {
+        for (int idx = ptid; idx < nel; idx += pnt) {
+            const int kk = idx / TM, rr = idx % TM;
+            const bool v = (kk < kc) && (r0 + rr < p.m_out);
+            const double *src = p.A + (k0 + kk) * p.lda + r0 + rr;
+            cp_async8(sx + kk * TM + rr, v ? src : p.A, v);
+        }
+    }
+    cp_async_mbar_arrive(bar);
+}
+
+// Barrier set-up (thread 0) and the null words after each slot's entry list.
+__device__ __forceinline__ void ring_setup(const ApplyArgs &p, const CUtensorMap *tmap, const Ring R,
+                                        uint32_t fcount, uint32_t ecount) {
+    unsigned *done = reinterpret_cast<unsigned *>(R.full + 16);  // per-slot finished-warp counters
+    // null words after each chunk's list: the pipelined walk loads (never
+    // accumulates) up to two entries past a warp's list -- they only need to
+    // address the tile
+    for (int s = 0; s < R.stages; ++s) {
+        unsigned char *st = R.stage0 + (size_t)s * p.stage_bytes;
+        if (threadIdx.x < 8) reinterpret_cast<uint32_t *>(st + p.en_off)[p.estride + threadIdx.x] = 0u;
+    }
+    if (threadIdx.x != 0) return;
+    for (int s = 0; s < R.stages; ++s) {
+        mbar_init(&R.full[s], fcount);
+        mbar_init(&R.empty[s], ecount);
+        done[s] = 0;
+    }
+    mbar_init(R.empty + 7, ecount);  // sink of deferred releases (stages <= 7)
+    fence_mbar_init();
+    if (p.mode == 0 || p.mode == 3 || p.mode == 4) prefetch_tmap(tmap);
+    if (p.mode == 4) mbar_init(R.full + 7, 1);  // staging buffer (stages <= 7 here)
+}
+
+// Dedicated producer warp(s): refill a slot as soon as every consumer warp
+// has released it (modes 0 / 3: one TMA-issuing lane; mode 4: TMA staging +
+// PW transposing warps; mode 1: PW warps of transposing cp.async copies).
+template <int TM, int PW, bool TRANS, bool XPOSE, bool SK>
+__device__ __forceinline__ void producer_warps(const ApplyArgs &p, const CUtensorMap *tmap, const Ring R) {
+    const int lane = threadIdx.x & 31;
+    const int ptid = threadIdx.x - (blockDim.x - PW * 32);
+    const int jn = DBG_IS(2) && R.nloc > R.stages ? R.stages : R.nloc;
+    const int stages = R.stages;
+    if (p.mode == 0 || p.mode == 3) {
+        if (lane == 0) {
+            for (int j = 0; j < jn; ++j) {
+                if (j >= stages) mbar_wait(&R.empty[j % stages], (uint32_t)((j / stages) - 1) & 1u);
+                issue_tma<TM, TRANS, SK>(p, tmap, R, j);
+            }
+        }
+    } else if (XPOSE && p.mode == 4) {
+        // transposed 128-row S' tiles of aligned A: one lane TMA-loads the
+        // chunk in A's natural layout (16 x TM boxes, 128-byte swizzle) into a
+        // staging buffer; the PW warps transpose it into the ring slot
+        // (conflict-free for the consumers); a named barrier among them frees
+        // the staging buffer for the next TMA
+        unsigned char *stg = R.stage0 + (size_t)stages * p.stage_bytes;  // 1024-aligned
+        uint64_t *stg_full = R.full + 7;
+        auto issue_stg = [&](int j) {
+            int64_t r0, c;
+            chunk_of<TM, SK>(p, R, j, r0, c);
+            mbar_arrive_expect_tx(stg_full, R.tile_bytes);
+            for (int kb = 0; kb < p.tk / 16; ++kb)
+                tma_load_2d(stg + kb * TM * 128, tmap, (int)(c * p.tk + kb * 16), (int)r0, stg_full);
+        };
+        if (ptid == 0 && jn > 0) issue_stg(0);
+        for (int j = 0; j < jn; ++j) {
+            const int s = j % stages;
+            unsigned char *st = R.stage0 + (size_t)s * p.stage_bytes;
+            if (j >= stages) mbar_wait(&R.empty[s], (uint32_t)((j / stages) - 1) & 1u);
+            if (ptid == 0) {
+                int64_t r0, c;
+                chunk_of<TM, SK>(p, R, j, r0, c);
+                mbar_arrive_expect_tx(&R.full[s], R.gs_bytes + R.en_bytes);
+                bulk_g2s(st + p.gs_off, p.gptr + c * p.gstride + R.g0, R.gs_bytes, &R.full[s]);
+                bulk_g2s(st + p.en_off, p.ent + c * p.estride, R.en_bytes, &R.full[s]);
+            }
+            mbar_wait(stg_full, (uint32_t)(j & 1));
+            // (kk, kk+1) of column cc: one 16-byte load from the swizzled
+            // staging tile, two 8-byte stores at kk*TM + (cc ^ kk%32)
+            double *dst = reinterpret_cast<double *>(st);
+            for (int u = ptid; u < (p.tk / 2) * TM; u += PW * 32) {
+                const int cc = u % TM, kk = 2 * (u / TM);
+                const uint32_t off = (uint32_t)((kk >> 4) * TM * 128 + cc * 128) +
+                                     ((uint32_t)((kk & 15) * 8) ^ ((uint32_t)(cc & 7) << 4));
+                const double2 v = *reinterpret_cast<const double2 *>(stg + off);
+                dst[kk * TM + (cc ^ (kk & 31))] = v.x;
+                dst[(kk + 1) * TM + (cc ^ ((kk + 1) & 31))] = v.y;
+            }
+            asm volatile("bar.sync 2, %0;" ::"r"(PW * 32) : "memory");  // staging read
+            if (ptid == 0 && j + 1 < jn) issue_stg(j + 1);
+            mbar_arrive(&R.full[s]);  // this thread's stores of slot s are done
+        }
+    } else {
+        for (int j = 0; j < jn; ++j) {
+            if (j >= stages) mbar_wait(&R.empty[j % stages], (uint32_t)((j / stages) - 1) & 1u);
+            issue_coop<TM, TRANS, XPOSE, SK>(p, R, j, ptid, PW * 32);
+        }
+    }
+    __syncwarp();
+    if (!SK) {  // match the consumers' barriers of the (k-split) epilogue
+        __syncthreads();
+        if (p.ksplit > 1) {
+            cluster_sync();
+            cluster_sync();
+        }
+    }
+    if (MC_ON) cluster_sync();  // peers stay alive for remote arrivals
+}
+
+// stream-K hand-off of a cut row tile's partials (thread 0): wait for the
+// flag of CTA cq and clear it for the next launch / publish this CTA's
+__device__ __noinline__ void sk_take_flag(int *flag) {
+    if (threadIdx.x == 0) {
+        while (ld_acquire_gpu(flag) == 0) __nanosleep(100);
+        *flag = 0;
+    }
+}
+__device__ __noinline__ void sk_post_flag(int *flag, int pub) {
+    if (pub && threadIdx.x == 0) st_release_gpu(flag, 1);
+}
+
+// All NW warps own buckets (NW*DB per CTA slab); PROD adds dedicated
+// producer warps (TMA issue, or transposing copies for 128-row S' tiles);
+// without them the consumers share the producer work (modes 1/2: every lane
+// issues its share of 8-byte cp.async for the chunk STAGES-1 ahead).
 template <int RPT, int DB, int NW, bool TRANS, bool PROD, bool SK, bool PAIR>
 __global__ void __launch_bounds__((NW + (PROD ? (TRANS && RPT == 4 ? kXposeProducers : 1) : 0)) * 32, 1)
-    sjlt_apply_kernel(const ApplyArgs p, const __grid_constant__ CUtensorMap tmap) {
+    sjlt_apply_kernel(const __grid_constant__ ApplyArgs p, const __grid_constant__ CUtensorMap tmap) {
     constexpr int TM = 32 * RPT;
     constexpr int SLAB = PAIR ? kPairSlab : NW * DB;
     constexpr bool XPOSE = TRANS && RPT == 4;       // transposed S' tile layout
@@ -461,284 +750,109 @@ __global__ void __launch_bounds__((NW + (PROD ? (TRANS && RPT == 4 ? kXposeProdu
     // buckets 16p + 8 + c2 in acc[.][2 + c2]; partials published / reduced
     // across CTAs keep the per-warp layout of the unpaired kernels)
     constexpr int PW = PROD ? (XPOSE ? kXposeProducers : 1) : 0;  // dedicated producer warps
+    constexpr int NT = NW * 32;
+    constexpr int NJ = PAIR ? 10 : DB;  // accumulator columns in use
+    // slot release: lane 0 of each consumer warp arrives (PROD: inline; the
+    // other paths through release_lane0)
+    constexpr bool LANE_REL = !PROD || HSK_SJLT_MULTICAST;
     extern __shared__ __align__(128) unsigned char smem[];
-    uint64_t *full = reinterpret_cast<uint64_t *>(smem);
-    uint64_t *empty = full + 8;
-    unsigned *done = reinterpret_cast<unsigned *>(full + 16);  // per-slot finished-warp counters
-    int *sk = reinterpret_cast<int *>(smem + 192);  // stream-K roles (below)
+    Ring R;
+    R.full = reinterpret_cast<uint64_t *>(smem);
+    R.empty = R.full + 8;
+    unsigned *done = reinterpret_cast<unsigned *>(R.full + 16);
     // stage ring from the first 1024-byte boundary past the 256-byte header
     // (the S' tile layout relies on the TMA 128-byte swizzle pattern)
-    unsigned char *stage0 = smem + ((((smem_u32(smem) + 256u + 1023u) & ~1023u)) - smem_u32(smem));
+    R.stage0 = smem + ((((smem_u32(smem) + 256u + 1023u) & ~1023u)) - smem_u32(smem));
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int ks = p.ksplit;
     int kr = 0;  // == %cluster_ctarank (cluster = ks consecutive CTAs)
-    int slab;
-    int64_t u0, u1;  // this CTA's chunks in the flattened (row tile, chunk) order
-    int64_t tile0;   // row tile of the first chunk
+    // (32-bit index arithmetic on launch constants: fast divisions and host
+    // tables instead of a division routine; the chunk and segment loops must
+    // be warp-uniform to ptxas -- a loop whose bound may differ between lanes
+    // is divergent, and so is every walker branch inside it)
+    const uint32_t bx = blockIdx.x, nch = (uint32_t)p.nchunks;
+    int grp = 0, nloc, nseg, seg_end;
+    int sk_tail = 0, sk_nq = 0;
     if (SK) {
-        const int64_t grp = blockIdx.x / p.nslabs;
-        slab = (int)(blockIdx.x % p.nslabs);
-        u0 = grp * p.units / p.groups;
-        u1 = (grp + 1) * p.units / p.groups;
-        tile0 = u0 / p.nchunks;
+        grp = (int)fdiv(bx, p.div_slabs);
+        R.slab = (int)(bx - (uint32_t)grp * p.div_slabs.d);
+        R.u0 = p.sk_g[grp][0];
+        R.u1 = p.sk_g[grp + 1][0];
+        R.tile0 = p.sk_g[grp][1];
+        seg_end = p.sk_g[grp][2];
+        nseg = p.sk_g[grp][3] & 0xffff;
+        sk_tail = (p.sk_g[grp][3] >> 16) & 1;
+        sk_nq = p.sk_g[grp][3] >> 17;
+        nloc = (int)(R.u1 - R.u0);
     } else {
-        kr = (int)(blockIdx.x % ks);
-        const int64_t bid = blockIdx.x / ks;
-        slab = (int)(bid % p.nslabs);
-        const int64_t tile = bid / p.nslabs;
-        const int64_t per = (p.nchunks + ks - 1) / ks;
-        const int64_t c_begin = (int64_t)kr * per < p.nchunks ? (int64_t)kr * per : p.nchunks;
-        const int64_t c_end = c_begin + per < p.nchunks ? c_begin + per : p.nchunks;
-        u0 = tile * p.nchunks + c_begin;
-        u1 = tile * p.nchunks + c_end;
-        tile0 = tile;
+        const uint32_t bid = fdiv(bx, p.div_ks);
+        kr = (int)(bx - bid * (uint32_t)ks);
+        const uint32_t tile = fdiv(bid, p.div_slabs);
+        R.slab = (int)(bid - tile * p.div_slabs.d);
+        const uint32_t per = (uint32_t)p.per;
+        const uint32_t kb = (uint32_t)kr * per;
+        const uint32_t c_begin = kb < nch ? kb : nch;
+        const uint32_t c_end = c_begin + per < nch ? c_begin + per : nch;
+        R.u0 = (int64_t)tile * nch + c_begin;
+        R.u1 = (int64_t)tile * nch + c_end;
+        R.tile0 = tile;
+        nloc = (int)(c_end - c_begin);
+        nseg = 1;
+        seg_end = nloc;
     }
-    const int j0 = slab * SLAB;
-    const int nloc = (int)(u1 - u0);
-    const int mode = p.mode;
+    // loop bounds broadcast from lane 0: warp-uniform to ptxas whatever
+    // datapath computed them
+    nloc = __shfl_sync(0xffffffffu, nloc, 0);
+    nseg = __shfl_sync(0xffffffffu, nseg, 0);
+    seg_end = __shfl_sync(0xffffffffu, seg_end, 0);
+    sk_nq = __shfl_sync(0xffffffffu, sk_nq, 0);
+    const int j0 = R.slab * SLAB;
+    R.nloc = nloc;
     const int stages = p.stages;
+    R.stages = stages;
+    R.g0 = R.slab * NW;  // first warp group of the slab
     // this CTA's NW + 1 group starts (16-byte multiple for the bulk copy)
-    const uint32_t gs_bytes = (uint32_t)((NW + 4) / 4 * 16);
-    const int g0 = slab * NW;  // first warp group of the slab
-    const uint32_t en_bytes = (uint32_t)p.estride * 4;
-    const uint32_t tile_bytes = (uint32_t)p.tk * TM * 8;
-
-    // null words after each chunk's list: the pipelined walk loads (never
-    // accumulates) up to two entries past a warp's list -- they only need to
-    // address the tile
-    for (int s = 0; s < stages; ++s) {
-        unsigned char *st = stage0 + (size_t)s * p.stage_bytes;
-        if (threadIdx.x < 8) reinterpret_cast<uint32_t *>(st + p.en_off)[p.estride + threadIdx.x] = 0u;
-    }
-    const bool tma = mode == 0 || mode == 3;
-    if (threadIdx.x == 0) {
+    R.gs_bytes = (uint32_t)((NW + 4) / 4 * 16);
+    R.en_bytes = (uint32_t)p.estride * 4;
+    R.tile_bytes = (uint32_t)p.tk * TM * 8;
+    const int64_t tile0 = R.tile0;
+    const bool tma = p.mode == 0 || p.mode == 3;
+    // stream-K: the later groups holding the tails of the tile this CTA's
+    // last segment heads start at CTA sk_cq (stride nslabs)
+    const int sk_cq = (grp + 1) * p.nslabs + R.slab;
+    if (SK && DBG_IS(3) && threadIdx.x == 0)
+        printf("sjlt dbg: cta %d grp %d u0 %lld u1 %lld nloc %d nseg %d seg0 %d tail %d nq %d stages %d\n",
+               (int)blockIdx.x, grp, (long long)R.u0, (long long)R.u1, nloc, nseg, seg_end, sk_tail, sk_nq,
+               p.stages);
+    {
         // TMA modes: one arrival (expect_tx); cp.async modes: every thread
         // of the (consumer) warps that share the copies, plus the issuer
         const uint32_t fcount = tma ? 1u : 1u + 32u * (PROD ? PW : NW);
-        for (int s = 0; s < stages; ++s) {
-            mbar_init(&full[s], fcount);
-            mbar_init(&empty[s], (HSK_SJLT_MULTICAST || SK) ? NW * p.mc : NW);  // consumer warps of the cluster
-            done[s] = 0;
-        }
-        fence_mbar_init();
-        if (tma || mode == 4) prefetch_tmap(&tmap);
-        if (mode == 4) mbar_init(full + 7, 1);  // staging buffer (stages <= 7 here)
-        if (SK) {
-            // sk[0]: the first segment is the tail of a tile (publish it);
-            // sk[1], sk[2]: the last segment is the head of a tile cut by the
-            // schedule -- count and first CTA of the later groups holding its
-            // tails (stride nslabs); sk[3]: first row tile
-            const int64_t grp = blockIdx.x / p.nslabs;
-            const int64_t tb = (u1 - 1) / p.nchunks * p.nchunks;  // start of the last tile
-            int nq = 0;
-            if (u1 % p.nchunks != 0 && tb >= u0)
-                for (int64_t q = grp + 1; q < p.groups && q * p.units / p.groups < tb + p.nchunks; ++q) ++nq;
-            sk[0] = u0 % p.nchunks != 0;
-            sk[1] = nq;
-            sk[2] = (int)((grp + 1) * p.nslabs + slab);
-            sk[3] = (int)tile0;
-            if (DBG_IS(3))
-                printf("sjlt dbg: cta %d grp %lld u0 %lld u1 %lld nloc %d sk %d %d %d %d stages %d\n",
-                       (int)blockIdx.x, (long long)grp, (long long)u0, (long long)u1, nloc, sk[0], sk[1],
-                       sk[2], sk[3], stages);
-        }
+        const uint32_t ecount = (uint32_t)(NW * p.mc);  // consumer warps of the cluster
+        ring_setup(p, &tmap, R, fcount, ecount);
     }
     __syncthreads();
     // multicast loads and remote releases target the peers' barriers: every
     // CTA of the cluster has initialised its ring before any of them issues
     if (MC_ON) cluster_sync();
 
-    // ---- producer helpers
-    // row offset and chunk index of the CTA's j-th chunk (stream-K: 32-bit
-    // arithmetic, the host keeps units < 2^31)
-    auto chunk_of = [&](int j, int64_t &r0, int64_t &c) {
-        if constexpr (SK) {
-            const uint32_t u = (uint32_t)u0 + (uint32_t)j;
-            const uint32_t t = u / (uint32_t)p.nchunks;
-            r0 = (int64_t)t * TM;
-            c = u - t * (uint32_t)p.nchunks;
-        } else {
-            r0 = tile0 * TM;
-            c = u0 - tile0 * p.nchunks + j;
-        }
-    };
-    auto stage_of = [&](int j) { return stage0 + (size_t)(j % stages) * p.stage_bytes; };
-    auto issue_tma = [&](int j) {  // warp 0, lane 0
-        unsigned char *st = stage_of(j);
-        uint64_t *bar = &full[j % stages];
-        int64_t r0, c;
-        chunk_of(j, r0, c);
-        mbar_arrive_expect_tx(bar, tile_bytes + gs_bytes + en_bytes);
-        if (MC_ON) {  // this CTA's share of the tile, for every CTA of the cluster
-            const uint32_t rank = cluster_ctarank();
-            const uint16_t mask = (uint16_t)((1u << p.mc) - 1u);
-            if constexpr (TRANS) {
-                for (int kb = (int)rank; kb < p.tk / 16; kb += p.mc)
-                    tma_load_2d_mc(st + kb * TM * 128, &tmap, (int)(c * p.tk + kb * 16), (int)r0, bar,
-                                   mask);
-            } else {
-                const int part = p.tk / p.mc;  // the box is TM x part
-                tma_load_2d_mc(st + (size_t)rank * part * TM * 8, &tmap, (int)r0,
-                               (int)(c * p.tk + rank * part), bar, mask);
-            }
-        } else if constexpr (TRANS) {  // S': one 16 x TM box per 16 input indices
-            for (int kb = 0; kb < p.tk / 16; ++kb)
-                tma_load_2d(st + kb * TM * 128, &tmap, (int)(c * p.tk + kb * 16), (int)r0, bar);
-        } else {
-            tma_load_2d(st, &tmap, (int)r0, (int)(c * p.tk), bar);
-        }
-        // keep the HBM stream ahead of the ring: chunk j + pf into L2 (chunks
-        // stages .. stages+pf-1 are requested together with the first loads)
-        const int jp = j < stages ? j + stages : j + p.pf;
-        if (p.pf > 0 && jp < nloc && (j < stages ? j < p.pf : true)) {
-            int64_t rp, cp;
-            chunk_of(jp, rp, cp);
-            const int part = p.tk / p.mc;
-            tma_prefetch_2d(&tmap, (int)rp, (int)(cp * p.tk + (MC_ON ? cluster_ctarank() * part : 0)));
-        }
-        bulk_g2s(st + p.gs_off, p.gptr + c * p.gstride + g0, gs_bytes, bar);
-        bulk_g2s(st + p.en_off, p.ent + c * p.estride, en_bytes, bar);
-    };
-    auto issue_coop = [&](int j, int ptid, int pnt) {  // threads [0, pnt) of the producer set
-        unsigned char *st = stage_of(j);
-        uint64_t *bar = &full[j % stages];
-        int64_t r0, c;
-        chunk_of(j, r0, c);
-        const int64_t k0 = c * p.tk;
-        const int kc = (int)(p.n - k0 < p.tk ? p.n - k0 : p.tk);
-        if (ptid == 0) {
-            mbar_arrive_expect_tx(bar, gs_bytes + en_bytes);
-            bulk_g2s(st + p.gs_off, p.gptr + c * p.gstride + g0, gs_bytes, bar);
-            bulk_g2s(st + p.en_off, p.ent + c * p.estride, en_bytes, bar);
-        }
-        double *sx = reinterpret_cast<double *>(st);
-        const int nel = p.tk * TM;
-        if (XPOSE) {
-            // (kk, rr) = A[k0+kk, r0+rr] -> sx[kk*TM + (rr ^ (kk%32))]; lanes
-            // along kk: coalesced reads, conflict-free swizzled writes
-            const int tk = p.tk;
-            const bool full_rows = r0 + TM <= p.m_out;
-            for (int kk = ptid; kk < tk; kk += pnt) {
-                const int sw = kk & 31;
-                const double *src = p.A + r0 * p.lda + k0 + kk;
-                double *dbase = sx + kk * TM;
-                if (kk < kc && full_rows) {
-#pragma unroll 8
-                    for (int rr = 0; rr < TM; ++rr, src += p.lda) cp_async8(dbase + (rr ^ sw), src, true);
-                } else {
-                    const bool vk = kk < kc;
-                    for (int rr = 0; rr < TM; ++rr, src += p.lda) {
-                        const bool v = vk && (r0 + rr < p.m_out);
-                        cp_async8(dbase + (rr ^ sw), v ? src : p.A, v);
-                    }
-                }
-            }
-        } else if (TRANS) {
-            // unaligned A: the S' tile layout of the TMA path, written by
-            // 8-byte cp.async -- (kk, rr) at (kk/16)*TM*128 + rr*128 +
-            // ((kk%16)*8 ^ 16*(rr%8)); lanes along kk (coalesced reads)
-            const int tk = p.tk;
-            for (int kk = ptid; kk < tk; kk += pnt) {
-                const double *src = p.A + r0 * p.lda + k0 + kk;
-                unsigned char *dbase = st + (kk >> 4) * TM * 128;
-                const int kx = (kk & 15) << 3;
-                const bool vk = kk < kc;
-                for (int rr = 0; rr < TM; ++rr, src += p.lda) {
-                    const bool v = vk && (r0 + rr < p.m_out);
-                    cp_async8(dbase + rr * 128 + (kx ^ ((rr & 7) << 4)), v ? src : p.A, v);
-                }
-            }
-        } else {
-            for (int idx = ptid; idx < nel; idx += pnt) {
-                const int kk = idx / TM, rr = idx % TM;
-                const bool v = (kk < kc) && (r0 + rr < p.m_out);
-                const double *src = p.A + (k0 + kk) * p.lda + r0 + rr;
-                cp_async8(sx + kk * TM + rr, v ? src : p.A, v);
-            }
-        }
-        cp_async_mbar_arrive(bar);
-    };
-
-    int issued = 0;
-    if (PROD) {
-        // dedicated producer warp(s): refill a slot as soon as every consumer
-        // warp has released it (mode 0: one TMA-issuing lane; modes 1/2: the
-        // producer warps share the 8-byte transposing copies)
-        if (warp >= NW) {  // one TMA-issuing lane, or PW warps of transposing copies
-            const int jn = DBG_IS(2) && nloc > stages ? stages : nloc;
-            if (tma) {
-                if (lane == 0) {
-                    for (int j = 0; j < jn; ++j) {
-                        if (j >= stages) mbar_wait(&empty[j % stages], (uint32_t)((j / stages) - 1) & 1u);
-                        issue_tma(j);
-                    }
-                }
-            } else if (XPOSE && mode == 4) {
-                // transposed 128-row S' tiles of aligned A: one lane TMA-loads
-                // the chunk in A's natural layout (16 x TM boxes, 128-byte
-                // swizzle) into a staging buffer; the PW warps transpose it into
-                // the ring slot (conflict-free for the consumers); a named
-                // barrier among them frees the staging buffer for the next TMA
-                const int ptid = threadIdx.x - NW * 32;
-                unsigned char *stg = stage0 + (size_t)stages * p.stage_bytes;  // 1024-aligned
-                uint64_t *stg_full = full + 7;
-                auto issue_stg = [&](int j) {
-                    int64_t r0, c;
-                    chunk_of(j, r0, c);
-                    mbar_arrive_expect_tx(stg_full, tile_bytes);
-                    for (int kb = 0; kb < p.tk / 16; ++kb)
-                        tma_load_2d(stg + kb * TM * 128, &tmap, (int)(c * p.tk + kb * 16), (int)r0, stg_full);
-                };
-                if (ptid == 0 && jn > 0) issue_stg(0);
-                for (int j = 0; j < jn; ++j) {
-                    const int s = j % stages;
-                    unsigned char *st = stage0 + (size_t)s * p.stage_bytes;
-                    if (j >= stages) mbar_wait(&empty[s], (uint32_t)((j / stages) - 1) & 1u);
-                    if (ptid == 0) {
-                        int64_t r0, c;
-                        chunk_of(j, r0, c);
-                        mbar_arrive_expect_tx(&full[s], gs_bytes + en_bytes);
-                        bulk_g2s(st + p.gs_off, p.gptr + c * p.gstride + g0, gs_bytes, &full[s]);
-                        bulk_g2s(st + p.en_off, p.ent + c * p.estride, en_bytes, &full[s]);
-                    }
-                    mbar_wait(stg_full, (uint32_t)(j & 1));
-                    // (kk, kk+1) of column cc: one 16-byte load from the swizzled
-                    // staging tile, two 8-byte stores at kk*TM + (cc ^ kk%32)
-                    double *dst = reinterpret_cast<double *>(st);
-                    for (int u = ptid; u < (p.tk / 2) * TM; u += PW * 32) {
-                        const int cc = u % TM, kk = 2 * (u / TM);
-                        const uint32_t off = (uint32_t)((kk >> 4) * TM * 128 + cc * 128) +
-                                             ((uint32_t)((kk & 15) * 8) ^ ((uint32_t)(cc & 7) << 4));
-                        const double2 v = *reinterpret_cast<const double2 *>(stg + off);
-                        dst[kk * TM + (cc ^ (kk & 31))] = v.x;
-                        dst[(kk + 1) * TM + (cc ^ ((kk + 1) & 31))] = v.y;
-                    }
-                    asm volatile("bar.sync 2, %0;" ::"r"(PW * 32) : "memory");  // staging read
-                    if (ptid == 0 && j + 1 < jn) issue_stg(j + 1);
-                    mbar_arrive(&full[s]);  // this thread's stores of slot s are done
-                }
-            } else {
-                const int ptid = threadIdx.x - NW * 32;
-                for (int j = 0; j < jn; ++j) {
-                    if (j >= stages) mbar_wait(&empty[j % stages], (uint32_t)((j / stages) - 1) & 1u);
-                    issue_coop(j, ptid, PW * 32);
-                }
-            }
-            __syncwarp();
-            if (ks > 1) {  // match the consumers' barriers of the k-split reduction
-                __syncthreads();
-                cluster_sync();
-                cluster_sync();
-            }
-            if (MC_ON) cluster_sync();  // peers stay alive for remote arrivals
+    if constexpr (PROD) {
+        // (role test on a broadcast warp index: warp-uniform to ptxas)
+        if (__shfl_sync(0xffffffffu, warp, 0) >= NW) {
+            producer_warps<TM, PW, TRANS, XPOSE, SK>(p, &tmap, R);
             return;
         }
-    } else if (tma) {
-        if (warp == 0 && lane == 0)
-            for (; issued < nloc && issued < stages; ++issued) issue_tma(issued);
-    } else {
-        for (; issued < nloc && issued < stages - 1; ++issued) issue_coop(issued, threadIdx.x, NW * 32);
+    }
+    int issued = 0;
+    if constexpr (!PROD) {
+        if (tma) {
+            if (warp == 0 && lane == 0)
+                for (; issued < nloc && issued < stages; ++issued) issue_tma<TM, TRANS, SK>(p, &tmap, R, issued);
+        } else {
+            for (; issued < nloc && issued < stages - 1; ++issued)
+                issue_coop<TM, TRANS, XPOSE, SK>(p, R, issued, threadIdx.x, NT);
+        }
     }
 
     double acc[RPT][DB];
@@ -747,206 +861,201 @@ __global__ void __launch_bounds__((NW + (PROD ? (TRANS && RPT == 4 ? kXposeProdu
 #pragma unroll
         for (int jj = 0; jj < DB; ++jj) acc[r][jj] = 0.0;
 
-    const uint32_t smem_base = smem_u32(stage0);
+    const uint32_t smem_base = smem_u32(R.stage0);
     // S' swizzle term of rows l + 32 r (TMA layout: 16-byte chunk; transposed: 8 bytes)
     const uint32_t lanex = XPOSE ? lane * 8u : (uint32_t)(lane & 7) << 4;
     // S: rows 2l, 2l+1 (+64) / l;  S': row l (TMA layout: 128 bytes per row)
     const uint32_t lane_off = XPOSE ? 0u : TRANS ? lane * 128u : lane * 8u * (RPT == 1 ? 1u : 2u);
-    // epilogue: one final scaling, as the reference (`out *= scale`)
-    auto store_tile = [&](const int64_t r0) {
-    const bool vec_ok = ((p.lds & 1) == 0) && ((reinterpret_cast<uintptr_t>(p.S) & 15) == 0);
+
+    // Epilogue: one store per accumulator, every one executed: to S scaled
+    // once (the reference's `out *= scale`) -- rows past m_out and buckets
+    // past d (or a paired quarter's folded-away t2 buckets) to the sink --
+    // or, pubw != nullptr, the raw partial into the CTA's stream-K slot.
+    auto store_acc = [&](const int64_t r0, double *pubw) {
+        const bool pub = pubw != nullptr;
 #pragma unroll
-    for (int jj = 0; jj < (PAIR ? 10 : DB); ++jj) {
-        if (PAIR && jj >= 2 && (warp & 3) != 0) break;
-        const int j = PAIR ? j0 + (warp >> 2) * 16 + (jj < 2 ? 2 * (warp & 3) + jj : 6 + jj)
-                           : j0 + warp * DB + jj;
-        if (j < p.d) {
+        for (int jj = 0; jj < NJ; ++jj) {
+            const int j = PAIR ? j0 + (warp >> 2) * 16 + (jj < 2 ? 2 * (warp & 3) + jj : 6 + jj)
+                               : j0 + warp * DB + jj;
+            const bool jok = j < p.d && (!PAIR || jj < 2 || (warp & 3) == 0);
             double *col = p.S + (p.col0 + j) * p.lds;
-            if (TRANS) {  // lane owns rows lane + 32 r
 #pragma unroll
-                for (int r = 0; r < RPT; ++r) {
-                    const int64_t row = r0 + lane + 32 * r;
-                    if (row < p.m_out) col[row] = acc[r][jj] * p.scale;
-                }
-            } else if constexpr (RPT == 1) {
-                const int64_t row = r0 + lane;
-                if (row < p.m_out) col[row] = acc[0][jj] * p.scale;
-            } else {      // lane owns rows 2l, 2l+1 (+64 for RPT 4)
-#pragma unroll
-                for (int h = 0; h < RPT / 2; ++h) {
-                    const int64_t row = r0 + 64 * h + 2 * lane;
-                    const double x0 = acc[2 * h][jj] * p.scale, x1 = acc[2 * h + 1][jj] * p.scale;
-                    if (vec_ok && row + 1 < p.m_out) {
-                        *reinterpret_cast<double2 *>(col + row) = make_double2(x0, x1);
-                    } else {
-                        if (row < p.m_out) col[row] = x0;
-                        if (row + 1 < p.m_out) col[row + 1] = x1;
-                    }
-                }
+            for (int r = 0; r < RPT; ++r) {
+                int64_t row;
+                if (TRANS) row = r0 + lane + 32 * r;             // lane owns rows lane + 32 r
+                else if (RPT == 1) row = r0 + lane;
+                else row = r0 + 64 * (r >> 1) + 2 * lane + (r & 1);  // rows 2l, 2l+1 (+64)
+                double *dst = pub ? pubw + ((warp * DB + jj) * RPT + r) * 32 + lane
+                                  : (jok && row < p.m_out ? col + row : g_sjlt_sink + lane);
+                __stcg(dst, pub ? acc[r][jj] : acc[r][jj] * p.scale);
             }
         }
-    }
     };
-
-    // stream-K: loop index at which the current row-tile segment ends (the
-    // rest of the bookkeeping is recomputed there, off the hot loop)
-    int seg_end = SK ? (int)((tile0 + 1) * p.nchunks - u0) : 0;
-    seg_end = seg_end < nloc ? seg_end : nloc;
-    int ctile = (int)tile0;
-    int cs = 0;
-    uint32_t cph = 0;
-    for (int i = 0; i < nloc; ++i) {
-        // ---- producer duty (modes 1/2): chunk i + stages - 1 into the slot of
-        // chunk i - 1, once every warp has finished chunk i - 1
-        if (!PROD && !tma && issued < nloc) {
-            const int j = issued;
-            if (j >= stages) mbar_wait(&empty[j % stages], (uint32_t)((j / stages) - 1) & 1u);
-            issue_coop(j, threadIdx.x, NW * 32);
-            ++issued;
-        }
-
-        // ---- consume chunk i
-        const int s = cs;
-        if (!DBG_IS(2) || i < stages) {
-            if (p.wait_ns) mbar_wait_hint(&full[s], cph, (uint32_t)p.wait_ns);
-            else mbar_wait(&full[s], cph);
-        }
-        const uint32_t st = smem_base + (uint32_t)s * p.stage_bytes;
-        const uint32_t sx = st + lane_off;
-        const uint32_t sen = st + p.en_off;
-        // shared address of the warp's group start (index of its first word)
-        const uint32_t sbw = st + (uint32_t)p.gs_off + (uint32_t)(warp * 4);
-#if HSK_SJLT_DEBUG
-        if (DBG_IS(3)) {  // checked mode: the warp's list lies in the chunk and ends in its terminator
-            const uint32_t *gs = reinterpret_cast<const uint32_t *>(stage0 + (size_t)s * p.stage_bytes + p.gs_off);
-            const uint32_t *en = reinterpret_cast<const uint32_t *>(stage0 + (size_t)s * p.stage_bytes + p.en_off);
-            const uint32_t b0 = gs[warp], b1 = gs[warp + 1];
-            bool bad = b0 >= b1 || b1 > (uint32_t)p.estride || ((en[b1 - 1] >> 24) & 127u) != (uint32_t)DB;
-            for (uint32_t q = b0; !bad && q + 1 < b1; ++q)
-                bad = ((en[q] >> 24) & 127u) >= (uint32_t)DB ||
-                      (q > b0 && ((en[q] >> 24) & 127u) < ((en[q - 1] >> 24) & 127u));
-            if (bad) {
-                printf("sjlt dbg: cta %d warp %d chunk-iter %d bad list [%u, %u) estride %d\n",
-                       (int)blockIdx.x, warp, i, b0, b1, (int)p.estride);
-                __trap();
-            }
-        }
-#endif
-        if (DBG_IS(1)) {
-        } else if constexpr (PAIR && TRANS) {
-            pipe_t_pair(acc, sen, sx, lanex, sbw);
-        } else if constexpr (PAIR) {
-            pipe_s_pair(acc, sen, sx, sbw);
-        } else if constexpr (TRANS) {
-            if constexpr (RPT == 1 && DB == 16) pipe_t_1x16(acc, sen, sx, lanex, sbw);
-            else if constexpr (RPT == 1 && DB == 32) pipe_t_1x32(acc, sen, sx, lanex, sbw);
-            else if constexpr (RPT == 2 && DB == 4) pipe_t_2x4(acc, sen, sx, lanex, sbw);
-            else if constexpr (RPT == 2 && DB == 8) pipe_t_2x8(acc, sen, sx, lanex, sbw);
-            else if constexpr (RPT == 2 && DB == 16) pipe_t_2x16(acc, sen, sx, lanex, sbw);
-            else if constexpr (RPT == 4 && DB == 2) pipe_t_4x2(acc, sen, sx, lanex, sbw);
-            else if constexpr (RPT == 4 && DB == 4) pipe_t_4x4(acc, sen, sx, lanex, sbw);
-            else if constexpr (RPT == 4 && DB == 8) pipe_t_4x8(acc, sen, sx, lanex, sbw);
-        } else {
-            if constexpr (RPT == 1 && DB == 16) pipe_s_1x16(acc, sen, sx, sbw);
-            else if constexpr (RPT == 1 && DB == 32) pipe_s_1x32(acc, sen, sx, sbw);
-            else if constexpr (RPT == 2 && DB == 4) pipe_s_2x4(acc, sen, sx, sbw);
-            else if constexpr (RPT == 2 && DB == 8) pipe_s_2x8(acc, sen, sx, sbw);
-            else if constexpr (RPT == 2 && DB == 16) pipe_s_2x16(acc, sen, sx, sbw);
-            else if constexpr (RPT == 4 && DB == 2) pipe_s_4x2(acc, sen, sx, sbw);
-            else if constexpr (RPT == 4 && DB == 4) pipe_s_4x4(acc, sen, sx, sbw);
-            else if constexpr (RPT == 4 && DB == 8) pipe_s_4x8(acc, sen, sx, sbw);
-        }
-        if constexpr (PAIR) {
-            // a row tile ends here: fold quarters 1..3's chunk-t2 partials into
-            // quarter 0 (in quarter order) through slot s, before its release
-            if (SK ? i + 1 == seg_end : i + 1 == nloc) {
-                constexpr int NT = NW * 32;
-                double *red = reinterpret_cast<double *>(stage0 + (size_t)s * p.stage_bytes);
-                const int h = warp & 3;
-                bar_named(NT);  // every warp is done with the slot
-                if (h > 0) {
-#pragma unroll
-                    for (int jj = 2; jj < 10; ++jj)
-#pragma unroll
-                        for (int r = 0; r < RPT; ++r) {
-                            red[((warp * 8 + jj - 2) * RPT + r) * 32 + lane] = acc[r][jj];
-                            acc[r][jj] = 0.0;
-                        }
-                }
-                bar_named(NT);
-                if (h == 0) {
-                    for (int q = 1; q < 4; ++q)
-#pragma unroll
-                        for (int jj = 2; jj < 10; ++jj)
-#pragma unroll
-                            for (int r = 0; r < RPT; ++r)
-                                acc[r][jj] += red[(((warp + q) * 8 + jj - 2) * RPT + r) * 32 + lane];
-                }
-                bar_named(NT);
-            }
-        }
+    // lane-0 slot release (paths with LANE_REL): arrive, or (no dedicated
+    // producer, TMA) let the last warp to finish chunk ic refill its slot
+    auto release_lane0 = [&](const int s, const int ic) {
         __syncwarp();
         if (lane == 0) {
             if (tma && !PROD) {
-                // the last warp to finish chunk i refills its slot with chunk i + stages
                 if (atomicAdd(&done[s], 1u) == NW - 1) {
                     done[s] = 0;
-                    if (i + stages < nloc && !DBG_IS(2)) issue_tma(i + stages);
+                    if (ic + stages < nloc && !DBG_IS(2)) issue_tma<TM, TRANS, SK>(p, &tmap, R, ic + stages);
                 }
             } else if (MC_ON) {
                 // release the slot in every CTA of the cluster: no producer
                 // multicasts into it until all of them are done with it
-                for (int r = 0; r < p.mc; ++r) mbar_arrive_cluster(&empty[s], (uint32_t)r);
+                for (int q = 0; q < p.mc; ++q) mbar_arrive_cluster(&R.empty[s], (uint32_t)q);
             } else {
-                mbar_arrive(&empty[s]);
+                mbar_arrive(&R.empty[s]);
             }
         }
-        if (++cs == stages) {
-            cs = 0;
-            cph ^= 1u;
+    };
+
+    // Segments: stream-K CTAs walk consecutive row tiles (the first may be
+    // the tail of a tile cut by the schedule, the last its head); whole-tile
+    // CTAs one tile.
+    int cs = 0;
+    uint32_t cph = 0;
+    int i = 0;  // chunks consumed before the current segment
+    // (the chunk loop restarts its own counter per segment: an inner loop
+    // continuing the outer loop's counter is divergent to ptxas)
+#pragma unroll 1
+    for (int seg = 0; seg < nseg; ++seg) {
+        const int seg_len = seg == 0 ? seg_end : (nloc - i < (int)nch ? nloc - i : (int)nch);
+#pragma unroll 1
+        for (int k = 0; k < seg_len; ++k) {
+            const int ic = i + k;  // chunk index
+            // ---- producer duty (no producer warps, modes 1/2): chunk
+            // i + stages - 1 into the slot of chunk i - 1, once every warp
+            // has finished chunk i - 1
+            if constexpr (!PROD) {
+                if (!tma && issued < nloc) {
+                    const int j = issued;
+                    if (j >= stages) mbar_wait(&R.empty[j % stages], (uint32_t)((j / stages) - 1) & 1u);
+                    issue_coop<TM, TRANS, XPOSE, SK>(p, R, j, threadIdx.x, NT);
+                    ++issued;
+                }
+            }
+            // ---- consume chunk i
+            const int s = cs;
+            if (!DBG_IS(2) || ic < stages) mbar_wait_hint(&R.full[s], cph, (uint32_t)p.wait_ns);
+            const uint32_t st = smem_base + (uint32_t)s * p.stage_bytes;
+            const uint32_t sx = st + lane_off;
+            const uint32_t sen = st + p.en_off;
+            // shared address of the warp's group start (index of its first word)
+            const uint32_t sbw = st + (uint32_t)p.gs_off + (uint32_t)(warp * 4);
+#if HSK_SJLT_DEBUG
+            if (DBG_IS(3)) {  // checked mode: the warp's list lies in the chunk and ends in its terminator
+                const uint32_t *gs = reinterpret_cast<const uint32_t *>(R.stage0 + (size_t)s * p.stage_bytes + p.gs_off);
+                const uint32_t *en = reinterpret_cast<const uint32_t *>(R.stage0 + (size_t)s * p.stage_bytes + p.en_off);
+                const uint32_t b0 = gs[warp], b1 = gs[warp + 1];
+                bool bad = b0 >= b1 || b1 > (uint32_t)p.estride || ((en[b1 - 1] >> 24) & 127u) != (uint32_t)DB;
+                for (uint32_t q = b0; !bad && q + 1 < b1; ++q)
+                    bad = ((en[q] >> 24) & 127u) >= (uint32_t)DB ||
+                          (q > b0 && ((en[q] >> 24) & 127u) < ((en[q - 1] >> 24) & 127u));
+                if (bad) {
+                    printf("sjlt dbg: cta %d warp %d chunk-iter %d bad list [%u, %u) estride %d\n",
+                           (int)blockIdx.x, warp, ic, b0, b1, (int)p.estride);
+                    __trap();
+                }
+            }
+#endif
+            if (DBG_IS(1)) {
+            } else if constexpr (PAIR && TRANS) {
+                pipe_t_pair(acc, sen, sx, lanex, sbw);
+            } else if constexpr (PAIR) {
+                pipe_s_pair(acc, sen, sx, sbw);
+            } else if constexpr (TRANS) {
+                if constexpr (RPT == 1 && DB == 16) pipe_t_1x16(acc, sen, sx, lanex, sbw);
+                else if constexpr (RPT == 1 && DB == 32) pipe_t_1x32(acc, sen, sx, lanex, sbw);
+                else if constexpr (RPT == 2 && DB == 4) pipe_t_2x4(acc, sen, sx, lanex, sbw);
+                else if constexpr (RPT == 2 && DB == 8) pipe_t_2x8(acc, sen, sx, lanex, sbw);
+                else if constexpr (RPT == 2 && DB == 16) pipe_t_2x16(acc, sen, sx, lanex, sbw);
+                else if constexpr (RPT == 4 && DB == 2) pipe_t_4x2(acc, sen, sx, lanex, sbw);
+                else if constexpr (RPT == 4 && DB == 4) pipe_t_4x4(acc, sen, sx, lanex, sbw);
+                else if constexpr (RPT == 4 && DB == 8) pipe_t_4x8(acc, sen, sx, lanex, sbw);
+            } else {
+                if constexpr (RPT == 1 && DB == 16) pipe_s_1x16(acc, sen, sx, sbw);
+                else if constexpr (RPT == 1 && DB == 32) pipe_s_1x32(acc, sen, sx, sbw);
+                else if constexpr (RPT == 2 && DB == 4) pipe_s_2x4(acc, sen, sx, sbw);
+                else if constexpr (RPT == 2 && DB == 8) pipe_s_2x8(acc, sen, sx, sbw);
+                else if constexpr (RPT == 2 && DB == 16) pipe_s_2x16(acc, sen, sx, sbw);
+                else if constexpr (RPT == 4 && DB == 2) pipe_s_4x2(acc, sen, sx, sbw);
+                else if constexpr (RPT == 4 && DB == 4) pipe_s_4x4(acc, sen, sx, sbw);
+                else if constexpr (RPT == 4 && DB == 8) pipe_s_4x8(acc, sen, sx, sbw);
+            }
+            // ---- release the slot (a paired plan folds its quarters through
+            // the slot of a row tile's last chunk: that release waits for the
+            // fold; meanwhile lane 0 arrives on the sink barrier)
+            if constexpr (!LANE_REL) {
+                __syncwarp();
+                if (lane == 0) mbar_arrive(PAIR && k + 1 == seg_len ? R.empty + 7 : &R.empty[s]);
+            } else {
+                if (!PAIR || k + 1 < seg_len) release_lane0(s, ic);
+            }
+            if (++cs == stages) {
+                cs = 0;
+                cph ^= 1u;
+            }
         }
-        if (SK && i + 1 == seg_end) {
-            // segment of row tile `ctile` ends here; its role was fixed in the
-            // prologue (sk[]): the first segment may be a tail to publish, the
-            // last one a head that adds the later groups' tails in group order
-            constexpr int NT = NW * 32;
-            if (ctile == sk[3] && sk[0]) {
-                double *w = p.ws + (size_t)blockIdx.x * (NW * DB * TM);
+        i += seg_len;
+        if constexpr (PAIR) {
+            // a row tile ends here: fold quarters 1..3's chunk-t2 partials into
+            // quarter 0 (in quarter order) through the slot of the tile's last
+            // chunk, then release it.  Every warp stores and loads (quarter 0's
+            // stores are never read; the other quarters add nothing).
+            const int sl = cs == 0 ? stages - 1 : cs - 1;
+            double *red = reinterpret_cast<double *>(R.stage0 + (size_t)sl * p.stage_bytes);
+            const int h = warp & 3;
+            bar_named(NT);  // every warp is done with the slot
 #pragma unroll
-                for (int jj = 0; jj < DB; ++jj)
+            for (int jj = 2; jj < 10; ++jj)
+#pragma unroll
+                for (int r = 0; r < RPT; ++r) {
+                    red[((warp * 8 + jj - 2) * RPT + r) * 32 + lane] = acc[r][jj];
+                    acc[r][jj] = h > 0 ? 0.0 : acc[r][jj];
+                }
+            bar_named(NT);
+            for (int q = 1; q < 4; ++q)
+#pragma unroll
+                for (int jj = 2; jj < 10; ++jj)
+#pragma unroll
+                    for (int r = 0; r < RPT; ++r) {
+                        const double v = red[((((warp & ~3) + q) * 8 + jj - 2) * RPT + r) * 32 + lane];
+                        acc[r][jj] += h == 0 ? v : 0.0;
+                    }
+            bar_named(NT);
+            if constexpr (!LANE_REL) { if (lane == 0) mbar_arrive(&R.empty[sl]); }
+            else release_lane0(sl, i - 1);
+        }
+        if constexpr (SK) {
+            // segment of row tile tile0 + seg ends here: the first segment may
+            // be a tail to publish, the last one a head that adds the later
+            // groups' tails in group order
+            const int pub = seg == 0 && sk_tail;
+            const int nq = seg == nseg - 1 && !pub ? sk_nq : 0;
+            for (int q = 0; q < nq; ++q) {
+                const int cq = sk_cq + q * p.nslabs;
+                sk_take_flag(&p.flags[cq]);
+                bar_named(NT);
+                const double *w = p.ws + (size_t)cq * (NW * DB * TM);
+#pragma unroll
+                for (int jj = 0; jj < NJ; ++jj)
 #pragma unroll
                     for (int r = 0; r < RPT; ++r)
-                        __stcg(&w[((warp * DB + jj) * RPT + r) * 32 + lane], acc[r][jj]);
-                __threadfence();
-                bar_named(NT);
-                if (threadIdx.x == 0) st_release_gpu(&p.flags[blockIdx.x], 1);
-            } else {
-                const int nq = i + 1 == nloc ? sk[1] : 0;
-                for (int q = 0; q < nq; ++q) {
-                    const int cq = sk[2] + q * p.nslabs;
-                    if (threadIdx.x == 0) {
-                        while (ld_acquire_gpu(&p.flags[cq]) == 0) __nanosleep(100);
-                        p.flags[cq] = 0;
-                    }
-                    bar_named(NT);
-                    const double *w = p.ws + (size_t)cq * (NW * DB * TM);
-#pragma unroll
-                    for (int jj = 0; jj < DB; ++jj)
-#pragma unroll
-                        for (int r = 0; r < RPT; ++r)
-                            acc[r][jj] += __ldcg(&w[((warp * DB + jj) * RPT + r) * 32 + lane]);
-                }
-                store_tile((int64_t)ctile * TM);
+                        acc[r][jj] += __ldcg(&w[((warp * DB + jj) * RPT + r) * 32 + lane]);
             }
+            store_acc((tile0 + seg) * TM, pub ? p.ws + (size_t)blockIdx.x * (NW * DB * TM) : nullptr);
+            __threadfence();
+            bar_named(NT);
+            sk_post_flag(&p.flags[blockIdx.x], pub);
 #pragma unroll
             for (int r = 0; r < RPT; ++r)
 #pragma unroll
                 for (int jj = 0; jj < DB; ++jj) acc[r][jj] = 0.0;
-            ++ctile;
-            seg_end = i + 1 + (int)p.nchunks < nloc ? i + 1 + (int)p.nchunks : nloc;
         }
     }
-    if (SK) {
+    if constexpr (SK) {
         if (MC_ON) cluster_sync();
         return;
     }
@@ -954,30 +1063,29 @@ __global__ void __launch_bounds__((NW + (PROD ? (TRANS && RPT == 4 ? kXposeProdu
     // ------------------------------------------- k-split: DSMEM reduction
     // Partial sums of the ks CTAs of a cluster are combined by rank 0 in
     // rank order (deterministic).  The stage ring is reused as the buffer.
-    if (ks > 1) {
-        double *red = reinterpret_cast<double *>(stage0);
+    // Every CTA stores its partial and reads its peers' (rank 0 adds them;
+    // with ks = 1 the cluster is the CTA itself and nothing is read).
+    {
+        double *red = reinterpret_cast<double *>(R.stage0);
         __syncthreads();  // every stage consumed: the ring is free
-        if (kr > 0) {
+#pragma unroll
+        for (int jj = 0; jj < DB; ++jj)
+#pragma unroll
+            for (int r = 0; r < RPT; ++r) red[((warp * DB + jj) * RPT + r) * 32 + lane] = acc[r][jj];
+        if (ks > 1) cluster_sync();
+        for (int q = 1; q < ks; ++q) {
 #pragma unroll
             for (int jj = 0; jj < DB; ++jj)
 #pragma unroll
-                for (int r = 0; r < RPT; ++r)
-                    red[((warp * DB + jj) * RPT + r) * 32 + lane] = acc[r][jj];
+                for (int r = 0; r < RPT; ++r) {
+                    const double v = ld_dsmem_f64(&red[((warp * DB + jj) * RPT + r) * 32 + lane], (uint32_t)q);
+                    acc[r][jj] += kr == 0 ? v : 0.0;
+                }
         }
-        cluster_sync();
-        if (kr == 0) {
-            for (int q = 1; q < ks; ++q) {
-#pragma unroll
-                for (int jj = 0; jj < DB; ++jj)
-#pragma unroll
-                    for (int r = 0; r < RPT; ++r)
-                        acc[r][jj] += ld_dsmem_f64(&red[((warp * DB + jj) * RPT + r) * 32 + lane], q);
-            }
-        }
-        cluster_sync();
+        if (ks > 1) cluster_sync();
         if (kr > 0) return;
     }
-    store_tile(tile0 * TM);
+    store_acc(tile0 * TM, nullptr);
     if (MC_ON) cluster_sync();
 }
 
@@ -1039,7 +1147,7 @@ static int launch(ApplyArgs a, const Geom &g, cudaStream_t st) {
     // better on C1, where stream-K's per-CTA fixups are a large share)
     a.streamk = eff < 0.9 && ctas >= sms;
     if (tuning().sjlt_streamk >= 0) a.streamk = tuning().sjlt_streamk == 1;
-    a.streamk = a.streamk && a.groups >= 1 && a.nchunks > 0 && a.units < (1ll << 31);
+    a.streamk = a.streamk && a.groups >= 1 && a.groups <= kMaxGroups && a.nchunks > 0 && a.units < (1ll << 31);
     if (a.streamk) ks = 1;
     // TMA multicast across the slab CTAs of a row tile (they read the same
     // tile): a cluster of nslabs CTAs, each loading 1/nslabs of every tile for
@@ -1105,6 +1213,17 @@ static int launch(ApplyArgs a, const Geom &g, cudaStream_t st) {
         }
     }
     if (a.streamk) {
+        for (int g = 0; g <= a.groups; ++g) a.sk_g[g][0] = (int32_t)(g * a.units / a.groups);
+        for (int g = 0; g < a.groups; ++g) {
+            const int64_t u0 = a.sk_g[g][0], u1 = a.sk_g[g + 1][0], nch = a.nchunks;
+            const int64_t tile0 = u0 / nch, tb = (u1 - 1) / nch * nch;  // start of the last tile
+            int nq = 0;
+            if (u1 % nch != 0 && tb >= u0)
+                for (int q = g + 1; q < a.groups && a.sk_g[q][0] < tb + nch; ++q) ++nq;
+            a.sk_g[g][1] = (int32_t)tile0;
+            a.sk_g[g][2] = (int32_t)std::min((tile0 + 1) * nch - u0, u1 - u0);
+            a.sk_g[g][3] = (int32_t)(((u1 - 1) / nch - tile0 + 1) | (u0 % nch != 0) << 16 | nq << 17);
+        }
         void *ws = nullptr;
         int *flags = nullptr;
         const int nct = a.groups * a.nslabs;
@@ -1114,12 +1233,16 @@ static int launch(ApplyArgs a, const Geom &g, cudaStream_t st) {
         a.flags = flags;
     }
     a.ksplit = ks;
+    a.div_slabs = make_fastdiv((uint32_t)a.nslabs);
+    a.div_ks = make_fastdiv((uint32_t)ks);
+    a.per = (int32_t)((a.nchunks + ks - 1) / ks);
     const int per = (int)(a.streamk ? (a.units + a.groups - 1) / a.groups : (a.nchunks + ks - 1) / ks);
     a.stages = stages_max;
     if (tuning().sjlt_stages > 0) a.stages = std::max(2, std::min(a.stages, tuning().sjlt_stages));
     if (per > 0 && a.stages > per + 1) a.stages = std::max(2, per + 1);
     int smem = 2048 + a.stages * a.stage_bytes + stg_bytes;  // header + 1024-byte alignment slack
-    if (ks > 1) smem = std::max(smem, 2048 + NW * DB * RPT * 32 * 8);
+    // whole-tile CTAs stage their partial in the ring for the (k-split) epilogue
+    if (!a.streamk) smem = std::max(smem, 2048 + NW * DB * RPT * 32 * 8);
     auto kern = a.trans ? (prod ? (a.streamk ? sjlt_apply_kernel<RPT, DB, NW, true, true, true, PAIR>
                                              : sjlt_apply_kernel<RPT, DB, NW, true, true, false, PAIR>)
                                 : (a.streamk ? sjlt_apply_kernel<RPT, DB, NW, true, false, true, PAIR>

@@ -45,6 +45,17 @@ load feeds two buckets, and the chain runs over 16 combos.  Accumulators: the
 warp's two t1 buckets in acc[.][0..1] (complete), chunk t2's 8 buckets in
 acc[.][2..9] (partial over the quarter; the kernel folds the four warps).
 
+Uniform branches (VOTE_DOC).  ptxas does not trust bra.uni: a predicate
+computed from a shared-memory word is per-lane to its divergence analysis, so
+every chain link and loop-back branch of a walker that sits in a loop gets
+BSSY/BSYNC reconvergence brackets -- a chain link then costs six instructions
+(ISETP, BRA, 2 BSSY, 2 BSYNC) instead of two.  vote.sync.any on the predicate
+(all lanes hold the same word, so it is the predicate itself) makes it
+warp-uniform to ptxas: no brackets, at one VOTE per branch -- a link costs
+three instructions, an entry one more.  That pays where entries per bucket
+and chunk are few (64-row tiles: C1 ~2, C2 1.6, C5 0.5) and not on the
+alpha-heavy 128-row tiles (C3: 16), which keep plain branches.
+
 Usage: python tools/gen_consumers.py > paper_2302_01977_b200/csrc/hsk_sjlt_pipe.cuh
 """
 import sys
@@ -57,7 +68,12 @@ def log2(x):
     return x.bit_length() - 1
 
 
-def gen(rpt, db, trans):
+def gen(rpt, db, trans, vote=None):
+    # vote: make every branch predicate warp-uniform with vote.sync.any (see
+    # VOTE_DOC); by default on the 64-row tiles (rpt 2: C1, C2, C5 -- few
+    # entries per bucket and chunk), off for the alpha-heavy 128-row tiles
+    if vote is None:
+        vote = rpt == 2
     nacc = rpt * db
     sh = log2(32 * rpt * 8)  # e << sh == kk * TM * 8 (the state byte shifts out)
     L = []
@@ -102,10 +118,12 @@ def gen(rpt, db, trans):
     L.extend(load_tile())
     a("and.b32 k, e, 2130706432;")
     a("ld.shared.b32 e, [pe+4];")
+    uni = ["vote.sync.any.pred q, q, -1;"] if vote else []
     for jj in range(db):
         nxt = f"T{jj + 1}" if jj + 1 < db else "DONE"
         a(f"T{jj}:")
         a(f"setp.ne.u32 q, k, {jj << 24};")
+        L.extend(uni)
         a(f"@q bra.uni {nxt};")
         a(f"S{jj}:")
         for r in range(rpt):
@@ -116,6 +134,7 @@ def gen(rpt, db, trans):
         a("add.u32 pe, pe, 4;")
         a("ld.shared.b32 e, [pe+4];")
         a(f"setp.eq.u32 q, k, {jj << 24};")
+        L.extend(uni)
         a(f"@q bra.uni S{jj};")
     a("DONE:")
     txt = "\\n\\t".join(L)
