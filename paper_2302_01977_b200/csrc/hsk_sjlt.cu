@@ -199,7 +199,8 @@ static Geom geom_dir(int64_t n, int d, int alpha, int trans, int64_t base, int p
     // d = 2048, alpha = 8)
     const bool wide = n >= 8192 && (trans || d <= 512);
     g.rpt = d <= 64 ? 4 : 2;
-    if (const int e = trans ? tuning().sjlt_rpt_t : tuning().sjlt_rpt; e == 1 || e == 2 || e == 4) g.rpt = e;
+    if (const int e = trans ? tuning().sjlt_rpt_t : tuning().sjlt_rpt; e == 2 || e == 4 || (HSK_TUNING && e == 1))
+        g.rpt = e;
     warp_shape(g.rpt, d, g.db, g.nw);
     g.ngroups = roundup(d, (int64_t)g.db * g.nw) / g.db;
     if (d <= 64) {
@@ -1421,11 +1422,11 @@ extern "C" int hsk_sjlt_apply_ex(const double *A, int64_t rows, int64_t cols, in
     if (g.pair) return sjlt::launch<2, 16, 16, true>(a, g, st);
     const int shape = g.rpt * 1000 + g.db * 10 + (g.nw == 32);
     switch (shape) {
-        case 1320: return sjlt::launch<1, 32, 16>(a, g, st);   // 32-row tiles, 512-bucket slabs
         case 4040: return sjlt::launch<4, 4, 16>(a, g, st);    // 128-row tiles, 64-bucket slabs
         case 2080: return sjlt::launch<2, 8, 16>(a, g, st);    // 64-row tiles
         case 2160: return sjlt::launch<2, 16, 16>(a, g, st);
-#if HSK_TUNING  // 32-warp variants (HSK_SJLT_W32=1): spill, never selected by default
+#if HSK_TUNING  // 32-row tiles (HSK_SJLT_RPT=1) and the 32-warp variants (HSK_SJLT_W32=1): never selected by default
+        case 1320: return sjlt::launch<1, 32, 16>(a, g, st);   // 32-row tiles, 512-bucket slabs
         case 1161: return sjlt::launch<1, 16, 32>(a, g, st);
         case 4021: return sjlt::launch<4, 2, 32>(a, g, st);
         case 2041: return sjlt::launch<2, 4, 32>(a, g, st);
