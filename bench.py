@@ -40,6 +40,7 @@ on all host cores, one bounded row slab of the same workload per step.
 from __future__ import annotations
 
 import argparse
+import contextlib
 import gc
 import json
 import os
@@ -480,6 +481,27 @@ def run_headline(args, ctx, out):
         cpu = {"value": gbs, "unit": "GB/s", "cores": threads, "kind": "port",
                "sample": f"oracle SjltBlock.apply_right restatement on a {rows} x {N} row slab "
                          f"of the same A, median of {reps}"}
+        # Gaussian: the reference's GaussianBlock.apply_right is numpy's
+        # `buf @ matrix.T` (OpenBLAS dgemm, sketching.py:134-135) -- timed as is on
+        # the same slab, at every host core and at one thread
+        gflop = 2.0 * rows * N * D / 1e9
+        Rh = gblk.matrix
+        rates = {}
+        try:
+            from threadpoolctl import threadpool_limits
+        except ImportError:  # pragma: no cover
+            threadpool_limits = None
+        for nth in (threads, 1):
+            if threadpool_limits is None and nth == 1:
+                continue
+            ctxm = threadpool_limits(limits=nth) if threadpool_limits else contextlib.nullcontext()
+            with ctxm:
+                _, tg, rg = cpu_rate(lambda: slab @ Rh.T, slab.nbytes, 6.0, 2)
+            rates[nth] = (gflop / tg / 1e3, rg)
+        cpu["gaussian"] = {"value": rates[threads][0], "unit": "TFLOP/s", "cores": threads,
+                           "value_1_thread": rates.get(1, (None,))[0], "kind": "reference",
+                           "sample": f"numpy (OpenBLAS) slab @ R^T on the {rows} x {N} slab, "
+                                     f"d={D}: the reference GaussianBlock.apply_right itself"}
     del A, S
     _free()
 
