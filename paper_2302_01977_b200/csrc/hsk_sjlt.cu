@@ -133,12 +133,26 @@ static inline int tk_fit16(int alpha, int tm, int cap, int per_stage, int64_t ng
 // (16 consumer warps: the 96-register budget holds RPT x DB accumulators plus
 // the walker; the 32-warp variants, half the buckets per warp, are kept for
 // tuning: HSK_SJLT_W32=1)
-static inline void warp_shape(int rpt, int d, int &db, int &nw) {
+static inline void warp_shape(int rpt, int d, int trans, int &db, int &nw) {
 #if HSK_TUNING
     const bool w32 = tuning().sjlt_w32 == 1;
 #else
     const bool w32 = false;  // 32-warp variants are compiled only in tuning builds
 #endif
+    // S on 64-row tiles: more, narrower consumer warps hide more of the
+    // walker's latency (slabs of 260 / 264 buckets; measured r02):
+    // 20 x 13 for d <= 512, 24 x 11 above.  S' keeps 16 x 16 (its walk is
+    // bound by the shared-memory port, and more warps measured slower).
+    // HSK_SJLT_W32 = 16 / 20 / 24 forces a shape (28: tuning builds).
+    const int ws = tuning().sjlt_w32;
+    if (rpt == 2 && d > 128 && !w32 && ws != 16 && (!trans || (HSK_TUNING && ws >= 20))) {
+        const int pick = ws >= 20 ? ws : d > 512 ? 24 : 20;
+        if (pick == 20) { nw = 20; db = 13; return; }
+        if (pick == 24) { nw = 24; db = 11; return; }
+#if HSK_TUNING
+        if (pick == 28) { nw = 28; db = 10; return; }
+#endif
+    }
     nw = w32 ? 32 : 16;
     if (rpt == 1) db = w32 ? 16 : 32;        // 32-row tiles, 512-bucket slabs
     else if (rpt == 4) db = w32 ? 2 : 4;     // 128-row tiles, 64-bucket slabs
@@ -201,7 +215,7 @@ static Geom geom_dir(int64_t n, int d, int alpha, int trans, int64_t base, int p
     g.rpt = d <= 64 ? 4 : 2;
     if (const int e = trans ? tuning().sjlt_rpt_t : tuning().sjlt_rpt; e == 2 || e == 4 || (HSK_TUNING && e == 1))
         g.rpt = e;
-    warp_shape(g.rpt, d, g.db, g.nw);
+    warp_shape(g.rpt, d, trans, g.db, g.nw);
     g.ngroups = roundup(d, (int64_t)g.db * g.nw) / g.db;
     if (d <= 64) {
         tk = wide && !trans ? tk_fit16(alpha, 128, 256, kStage2, g.ngroups, g.nw)
@@ -972,6 +986,9 @@ __global__ void __launch_bounds__((NW + (PROD ? (TRANS && RPT == 4 ? kXposeProdu
                 else if constexpr (RPT == 2 && DB == 4) pipe_t_2x4(acc, sen, sx, lanex, sbw);
                 else if constexpr (RPT == 2 && DB == 8) pipe_t_2x8(acc, sen, sx, lanex, sbw);
                 else if constexpr (RPT == 2 && DB == 16) pipe_t_2x16(acc, sen, sx, lanex, sbw);
+                else if constexpr (RPT == 2 && DB == 10) pipe_t_2x10(acc, sen, sx, lanex, sbw);
+                else if constexpr (RPT == 2 && DB == 11) pipe_t_2x11(acc, sen, sx, lanex, sbw);
+                else if constexpr (RPT == 2 && DB == 13) pipe_t_2x13(acc, sen, sx, lanex, sbw);
                 else if constexpr (RPT == 4 && DB == 2) pipe_t_4x2(acc, sen, sx, lanex, sbw);
                 else if constexpr (RPT == 4 && DB == 4) pipe_t_4x4(acc, sen, sx, lanex, sbw);
                 else if constexpr (RPT == 4 && DB == 8) pipe_t_4x8(acc, sen, sx, lanex, sbw);
@@ -981,6 +998,9 @@ __global__ void __launch_bounds__((NW + (PROD ? (TRANS && RPT == 4 ? kXposeProdu
                 else if constexpr (RPT == 2 && DB == 4) pipe_s_2x4(acc, sen, sx, sbw);
                 else if constexpr (RPT == 2 && DB == 8) pipe_s_2x8(acc, sen, sx, sbw);
                 else if constexpr (RPT == 2 && DB == 16) pipe_s_2x16(acc, sen, sx, sbw);
+                else if constexpr (RPT == 2 && DB == 10) pipe_s_2x10(acc, sen, sx, sbw);
+                else if constexpr (RPT == 2 && DB == 11) pipe_s_2x11(acc, sen, sx, sbw);
+                else if constexpr (RPT == 2 && DB == 13) pipe_s_2x13(acc, sen, sx, sbw);
                 else if constexpr (RPT == 4 && DB == 2) pipe_s_4x2(acc, sen, sx, sbw);
                 else if constexpr (RPT == 4 && DB == 4) pipe_s_4x4(acc, sen, sx, sbw);
                 else if constexpr (RPT == 4 && DB == 8) pipe_s_4x8(acc, sen, sx, sbw);
@@ -1091,8 +1111,12 @@ __global__ void __launch_bounds__((NW + (PROD ? (TRANS && RPT == 4 ? kXposeProdu
 }
 
 
-template <int RPT, int DB, int NW, bool PAIR = false>
+// SONLY: the shape serves S only (no S' kernels are instantiated for it)
+template <int RPT, int DB, int NW, bool PAIR = false, bool SONLY = false>
 static int launch(ApplyArgs a, const Geom &g, cudaStream_t st) {
+    // a slab's group starts are bulk-copied from word slab * NW: 16-byte aligned
+    static_assert(NW % 4 == 0, "consumer warps per CTA must be a multiple of 4");
+    if (SONLY && a.trans) return set_error(HSK_EINVAL, "sjlt apply: no S' kernel for rpt=%d db=%d nw=%d", RPT, DB, NW);
     constexpr int TM = 32 * RPT;
     constexpr int SLAB = PAIR ? kPairSlab : NW * DB;
     HSK_REQUIRE(g.tm == TM && g.db == DB && g.nw == NW, HSK_EINVAL, "sjlt: plan/config mismatch");
@@ -1183,8 +1207,9 @@ static int launch(ApplyArgs a, const Geom &g, cudaStream_t st) {
     if (a.streamk && a.mc > 1) {
         // every group is one cluster and groups wait on later groups: keep
         // the grid to the clusters that can be co-resident
-        auto kprobe = a.trans ? sjlt_apply_kernel<RPT, DB, NW, true, true, true, PAIR>
-                              : sjlt_apply_kernel<RPT, DB, NW, false, true, true, PAIR>;
+        auto kprobe = sjlt_apply_kernel<RPT, DB, NW, false, true, true, PAIR>;
+        if constexpr (!SONLY)
+            if (a.trans) kprobe = sjlt_apply_kernel<RPT, DB, NW, true, true, true, PAIR>;
         const int smem_max = 2048 + stages_max * a.stage_bytes;
         cudaError_t e = cudaFuncSetAttribute(kprobe, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_max);
         if (e != cudaSuccess) return cuda_status(e, "sjlt: set smem attribute");
@@ -1244,14 +1269,16 @@ static int launch(ApplyArgs a, const Geom &g, cudaStream_t st) {
     int smem = 2048 + a.stages * a.stage_bytes + stg_bytes;  // header + 1024-byte alignment slack
     // whole-tile CTAs stage their partial in the ring for the (k-split) epilogue
     if (!a.streamk) smem = std::max(smem, 2048 + NW * DB * RPT * 32 * 8);
-    auto kern = a.trans ? (prod ? (a.streamk ? sjlt_apply_kernel<RPT, DB, NW, true, true, true, PAIR>
-                                             : sjlt_apply_kernel<RPT, DB, NW, true, true, false, PAIR>)
-                                : (a.streamk ? sjlt_apply_kernel<RPT, DB, NW, true, false, true, PAIR>
-                                             : sjlt_apply_kernel<RPT, DB, NW, true, false, false, PAIR>))
-                        : (prod ? (a.streamk ? sjlt_apply_kernel<RPT, DB, NW, false, true, true, PAIR>
-                                             : sjlt_apply_kernel<RPT, DB, NW, false, true, false, PAIR>)
-                                : (a.streamk ? sjlt_apply_kernel<RPT, DB, NW, false, false, true, PAIR>
-                                             : sjlt_apply_kernel<RPT, DB, NW, false, false, false, PAIR>));
+    auto kern = prod ? (a.streamk ? sjlt_apply_kernel<RPT, DB, NW, false, true, true, PAIR>
+                                  : sjlt_apply_kernel<RPT, DB, NW, false, true, false, PAIR>)
+                     : (a.streamk ? sjlt_apply_kernel<RPT, DB, NW, false, false, true, PAIR>
+                                  : sjlt_apply_kernel<RPT, DB, NW, false, false, false, PAIR>);
+    if constexpr (!SONLY)
+        if (a.trans)
+            kern = prod ? (a.streamk ? sjlt_apply_kernel<RPT, DB, NW, true, true, true, PAIR>
+                                     : sjlt_apply_kernel<RPT, DB, NW, true, true, false, PAIR>)
+                        : (a.streamk ? sjlt_apply_kernel<RPT, DB, NW, true, false, true, PAIR>
+                                     : sjlt_apply_kernel<RPT, DB, NW, true, false, false, PAIR>);
     // L2 prefetch beyond the ring: off -- the duplicate requests cost power,
     // and sustained runs are power-capped (C2, 2000 launches: 0.505 ms
     // without, 0.540 ms with; no burst gain either).  HSK_SJLT_PF=<chunks>.
@@ -1425,8 +1452,19 @@ extern "C" int hsk_sjlt_apply_ex(const double *A, int64_t rows, int64_t cols, in
         case 4040: return sjlt::launch<4, 4, 16>(a, g, st);    // 128-row tiles, 64-bucket slabs
         case 2080: return sjlt::launch<2, 8, 16>(a, g, st);    // 64-row tiles
         case 2160: return sjlt::launch<2, 16, 16>(a, g, st);
+        case 2130:  // S: 20 x 13 (S' only when forced in a tuning build)
+#if HSK_TUNING
+            if (trans) return sjlt::launch<2, 13, 20>(a, g, st);
+#endif
+            return sjlt::launch<2, 13, 20, false, true>(a, g, st);
+        case 2110:  // S: 24 x 11
+#if HSK_TUNING
+            if (trans) return sjlt::launch<2, 11, 24>(a, g, st);
+#endif
+            return sjlt::launch<2, 11, 24, false, true>(a, g, st);
 #if HSK_TUNING  // 32-row tiles (HSK_SJLT_RPT=1) and the 32-warp variants (HSK_SJLT_W32=1): never selected by default
         case 1320: return sjlt::launch<1, 32, 16>(a, g, st);   // 32-row tiles, 512-bucket slabs
+        case 2100: return sjlt::launch<2, 10, 28>(a, g, st);   // HSK_SJLT_W32 = 28
         case 1161: return sjlt::launch<1, 16, 32>(a, g, st);
         case 4021: return sjlt::launch<4, 2, 32>(a, g, st);
         case 2041: return sjlt::launch<2, 4, 32>(a, g, st);

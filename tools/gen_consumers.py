@@ -60,8 +60,8 @@ Usage: python tools/gen_consumers.py > paper_2302_01977_b200/csrc/hsk_sjlt_pipe.
 """
 import sys
 
-S_CONFIGS = [(1, 16), (1, 32), (2, 4), (2, 8), (2, 16), (4, 2), (4, 4), (4, 8)]
-T_CONFIGS = [(1, 16), (1, 32), (2, 4), (2, 8), (2, 16), (4, 2), (4, 4), (4, 8)]
+S_CONFIGS = [(1, 16), (1, 32), (2, 4), (2, 8), (2, 10), (2, 11), (2, 13), (2, 16), (4, 2), (4, 4), (4, 8)]
+T_CONFIGS = [(1, 16), (1, 32), (2, 4), (2, 8), (2, 10), (2, 11), (2, 13), (2, 16), (4, 2), (4, 4), (4, 8)]
 
 
 def log2(x):
