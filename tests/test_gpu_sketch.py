@@ -139,6 +139,25 @@ def test_sjlt_schedules_vs_oracle(cuda, tune, m, n, d, alpha):
         np.testing.assert_array_equal(t1, t2)
 
 
+@pytest.mark.parametrize("ws", ["16", "20", "24"])
+def test_sjlt_warp_shapes_vs_oracle(cuda, tune, ws):
+    """S's consumer-warp shapes (16 x 16, 20 x 13, 24 x 11: slabs of 256 / 260 /
+    264 buckets, the last one partial) under both schedules; a forced shape
+    leaves S' on its 16 x 16 kernels."""
+    m, n, d = 1000, 3000, 700
+    rng = np.random.default_rng(7)
+    op = sk.new_operator(sk.SJLT, n, d, seed=(m, d), alpha=4, construction=sk.BLOCK)
+    b = op.blocks[0]
+    A = rng.standard_normal((m, n))
+    B = rng.standard_normal((n, m))
+    tune("HSK_SJLT_W32", ws)
+    for mode in ("0", "1"):
+        tune("HSK_SJLT_STREAMK", mode)
+        _close(sk.apply_right(A, op), O.sjlt_right(A, b._pos, b._signs, d, b._scale), np.linalg.norm(A))
+        _close(sk.apply_right_transposed(B, op), O.sjlt_right_t(B, b._pos, b._signs, d, b._scale),
+               np.linalg.norm(B))
+
+
 def test_odd_leading_dimension_and_column_offset(cuda):
     rng = np.random.default_rng(5)
     m, n, d = 77, 333, 96
