@@ -704,8 +704,14 @@ def cfg_c5(args, ctx, peak):
             sk.apply_right_device(A, op, out=S)
 
         def fSt():
-            hd.sketch_row_sharded(A, op, rank=rank, world=world, n_rows=n, transport="p2p",
-                                  local_right=lambda *_: None)
+            try:
+                hd.sketch_row_sharded(A, op, rank=rank, world=world, n_rows=n,
+                                      transport=rec["transport"], local_right=lambda *_: None)
+            except hd.PeerMappingError:   # raised on every rank together: all fall back
+                rec["transport"] = "nccl"
+                rec["workload"] = rec["workload"].replace("p2p peer stores + rank-ordered sum",
+                                                          "NCCL reduce-scatter")
+                fSt()
         ctx.barrier()
         s_ms = time_launches(fS, reps, warm, stream)
         ctx.barrier()

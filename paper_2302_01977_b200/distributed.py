@@ -134,14 +134,23 @@ class PeerSlots:
         if world > 1:
             dist.all_gather_object(handles, bytes(handle), group=group)
         self.peer = []
+        err = None
         for q in range(world):
             if q == rank:
                 self.peer.append(self.own)
-            else:
-                p = ctypes.c_void_p()
-                buf = ctypes.create_string_buffer(handles[q], 64)
+                continue
+            p = ctypes.c_void_p()
+            buf = ctypes.create_string_buffer(handles[q], 64)
+            try:
                 _lib.call("hsk_ipc_open", buf, ctypes.byref(p))
-                self.peer.append(p.value)
+            except RuntimeError as e:  # no peer mapping between these GPUs
+                err = err or e
+                p = ctypes.c_void_p()
+            self.peer.append(p.value)
+        # every rank must take the same transport: agree on success
+        if world > 1 and not _all_ranks_ok(err is None, group):
+            self.close()
+            raise PeerMappingError(f"CUDA IPC peer mapping failed on some rank ({err or 'peer'})")
 
     def slot(self, q: int, rows: int):
         """Rank q's slot (current set) for this rank's partial of block q (rows x d)."""
@@ -165,6 +174,18 @@ class PeerSlots:
         if self.own:
             _lib.call("hsk_ipc_free", self.own)
         self.peer, self.own = [], 0
+
+
+class PeerMappingError(RuntimeError):
+    """Some rank could not map a peer's receive buffer (collectively raised)."""
+
+
+def _all_ranks_ok(ok: bool, group) -> bool:
+    flag = torch.tensor([1 if ok else 0], dtype=torch.int32)
+    if dist.get_backend(group) == "nccl":
+        flag = flag.cuda()
+    dist.all_reduce(flag, op=dist.ReduceOp.MIN, group=group)
+    return bool(flag.item())
 
 
 _SLOTS: dict = {}
@@ -244,10 +265,16 @@ def sketch_row_sharded(A_shard, op, *, rank: int, world: int, n_rows: int,
     if op.n != n_rows:
         raise ValueError("S' = A^T R^T needs a square operator over the row space")
     sub = _restricted_cached(op, r0, r1)
-    if transport is None:
+    auto = transport is None
+    if auto:
         transport = "nccl" if (local_transposed is not None or deterministic) else "p2p"
     if transport == "p2p":
-        return S_local, _p2p_transposed(A_shard, sub, bounds, rank, world, group)
+        try:
+            return S_local, _p2p_transposed(A_shard, sub, bounds, rank, world, group)
+        except PeerMappingError:
+            if not auto:
+                raise
+            transport = "nccl"  # every rank got the same error: all fall back together
     if transport != "nccl":
         raise ValueError(f"unknown transport {transport!r}")
     local_transposed = local_transposed or _gpu_local_transposed_blocks

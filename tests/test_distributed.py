@@ -119,3 +119,31 @@ def test_transport_selection_and_validation():
     S, St = D.sketch_row_sharded(HostMat(A), op, rank=0, world=1, n_rows=n,
                                  local_right=_local_right, local_transposed=_local_transposed)
     np.testing.assert_allclose(St.numpy().T, O.apply_right_transposed(A, op), rtol=0, atol=1e-12)
+
+
+def _agree_worker(rank, world, port, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        # rank 1 "fails to map a peer": every rank must see the failure
+        q.put((rank, D._all_ranks_ok(rank != 1, None), D._all_ranks_ok(True, None)))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_peer_mapping_failure_is_agreed_by_all_ranks():
+    """The p2p S' transport falls back to NCCL only collectively: a peer
+    mapping failure on one rank is reported on every rank (no rank may take
+    the p2p path while another takes the reduce-scatter)."""
+    world, port = 2, _free_port()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_agree_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = sorted(q.get(timeout=120) for _ in range(world))
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    assert res == [(0, False, True), (1, False, True)]
