@@ -221,10 +221,11 @@ static Geom geom_dir(int64_t n, int d, int alpha, int trans, int64_t base, int p
         tk = wide && !trans ? tk_fit16(alpha, 128, 256, kStage2, g.ngroups, g.nw)
                             : tk_fit(alpha, 128, 128, kStage3, g.ngroups, g.nw);
     } else {
-        // (S on the narrower 20 x 13 / 24 x 11 warps prefers the deeper ring:
-        // C2 S 0.438 ms at TK 128 x 3 stages vs 0.447 at 208 x 2, r02)
-        tk = wide && (trans || g.nw == 16) ? tk_fit16(alpha, 64, 256, kStage2, g.ngroups, g.nw)
-                                           : tk_fit(alpha, 64, 128, kStage3, g.ngroups, g.nw);
+        // (S on the 20 x 13 warps: TK 128 x 3 stages measured faster in bursts,
+        // C2 0.439 vs 0.449 ms over 20 launches, but slower under the power cap,
+        // 0.514 vs 0.494 ms over 2000: two stages of TK 208 kept)
+        tk = wide ? tk_fit16(alpha, 64, 256, kStage2, g.ngroups, g.nw)
+                  : tk_fit(alpha, 64, 128, kStage3, g.ngroups, g.nw);
     }
     if (const int e = trans ? tuning().sjlt_tk_t : tuning().sjlt_tk; e > 0) tk = e;
     g.tm = 32 * g.rpt;
