@@ -155,6 +155,12 @@ HSK_API int hsk_gen_gauss_kernel(const double *pts, int64_t n, int32_t dim, doub
 HSK_API int hsk_gen_toeplitz_sin(int64_t n, int64_t row0, int64_t nrows, int64_t col0, int64_t ncols,
                          double *A, int64_t lda, void *stream);
 
+/* B = A^T: A rows x cols column-major (lda), B cols x rows column-major (ldb),
+ * both device.  The adaptive sketch keeps A^T once so every S' increment runs
+ * as S = A^T R^T on conflict-free tiles (adaptive.DeviceSketch). */
+HSK_API int hsk_transpose(const double *A, int64_t rows, int64_t cols, int64_t lda, double *B,
+                          int64_t ldb, void *stream);
+
 /* Streams `bytes` of scratch (device) to evict L2 between timed launches. */
 HSK_API int hsk_l2_flush(void *scratch, int64_t bytes, void *stream);
 

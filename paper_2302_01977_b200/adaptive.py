@@ -7,6 +7,14 @@ columns are never recomputed).  DeviceSketch keeps S = A R^T and
 S' = A^T R^T in HBM with capacity d_max columns; each increment launches the
 kernels once for the new block, writing straight into columns
 [d, d + dd) (hsk_*_apply `col0`).  Old columns are neither re-read nor moved.
+
+S' = A^T R^T of a TMA-landed A tile reads 8-byte column values whose
+16-row groups share 8 bank pairs (2-way conflicts), while
+S = A R^T reads contiguous rows conflict-free.  An adaptive run applies S' to
+the same A once per increment, so from the first extension on (when HBM holds
+a second copy) the sketch keeps A^T -- one transpose, 2 x bytes(A) of traffic
+-- and runs every later S' increment as S = A^T R^T (same entries, same
+per-bucket summation order over the input indices).
 """
 
 from __future__ import annotations
@@ -25,8 +33,11 @@ class DeviceSketch:
     overflow raises ValueError."""
 
     def __init__(self, A, n_cols_max: int, *, right: bool = True, transposed: bool = True,
-                 growable: bool = False):
+                 growable: bool = False, keep_transpose: bool | None = None):
         self.A = _sk.device_matrix_of(A)
+        # A^T for the S' increments: None = when it fits (the default), False = never
+        self.keep_transpose = keep_transpose
+        self.At = None
         self.capacity = int(n_cols_max)
         self.growable = growable
         self.d = 0
@@ -56,8 +67,23 @@ class DeviceSketch:
         if self.S is not None:
             _dev.apply_block(blk, self.A, False, self.S, self.d)
         if self.St is not None:
-            _dev.apply_block(blk, self.A, True, self.St, self.d)
+            if self.At is not None:     # S' = (A^T) R^T on the kept transpose
+                _dev.apply_block(blk, self.At, False, self.St, self.d)
+            else:
+                _dev.apply_block(blk, self.A, True, self.St, self.d)
         self.d += blk.rows
+
+    def _maybe_transpose(self):
+        """Keep A^T for the remaining S' increments if it fits in free HBM
+        (with a quarter of A as margin) -- or always / never when asked."""
+        if self.St is None or self.At is not None or self.keep_transpose is False:
+            return
+        if self.keep_transpose is None:
+            import torch
+            free, _ = torch.cuda.mem_get_info()
+            if free < 1.25 * 8 * self.A.rows * self.A.cols + (1 << 30):
+                return
+        self.At = self.A.transposed()
 
     def start(self, op) -> "DeviceSketch":
         """Sketch every block of a fresh operator (init_sketch)."""
@@ -66,6 +92,7 @@ class DeviceSketch:
         if self.St is not None and op.n != self.A.rows:
             raise ValueError("operator dimension does not match A's rows")
         self.d = 0
+        self.At = None   # a fresh schedule pays for its own transpose
         for blk in op.blocks:
             self._sketch_block(blk)
         self.op = op
@@ -77,6 +104,8 @@ class DeviceSketch:
         known = 0 if self.op is None else len(self.op.blocks)
         if self.op is not None and tuple(op.blocks[:known]) != tuple(self.op.blocks):
             raise ValueError("operator is not an extension of the sketched one")
+        if len(op.blocks) > known:
+            self._maybe_transpose()
         for blk in op.blocks[known:]:
             self._sketch_block(blk)
         self.op = op

@@ -283,6 +283,82 @@ extern "C" int hsk_gen_toeplitz_sin(int64_t n, int64_t row0, int64_t nrows, int6
     return HSK_OK;
 }
 
+// B = A^T through 64 x 64 shared tiles s[r][c] = A(r0 + r, c0 + c) with a
+// 65-double pitch.  Both directions move whole 128-byte lines: eight lanes
+// cover one 16-row run of a column as 16-byte pairs, a warp four such runs
+// (partial sectors would make every HBM write a read-modify-write); eight
+// pairs per thread in flight.  The shared stores and loads of a half-warp
+// (two columns / rows x eight pairs) hit 16 distinct bank pairs.  Partial
+// tiles and 8-byte-aligned operands take the scalar path.
+__global__ void __launch_bounds__(256) transpose_kernel(const double *__restrict__ A, int64_t rows,
+                                                        int64_t cols, int64_t lda,
+                                                        double *__restrict__ B, int64_t ldb, int vec) {
+    __shared__ double s[64 * 65];
+    const int l8 = threadIdx.x & 7, gi = threadIdx.x >> 3;  // 16-byte chunk of a run, run group
+    const int64_t r0 = (int64_t)blockIdx.x * 64;
+    for (int64_t c0 = (int64_t)blockIdx.y * 64; c0 < cols; c0 += (int64_t)gridDim.y * 64) {
+        const bool full = vec && r0 + 64 <= rows && c0 + 64 <= cols;
+        if (full) {
+            double2 v[8];
+#pragma unroll
+            for (int k = 0; k < 8; ++k) {  // run p: column p % 64, rows 16 (p / 64) + 2 l8
+                const int pr = gi + 32 * k, c = pr & 63, rb = pr >> 6;
+                v[k] = __ldcs(reinterpret_cast<const double2 *>(A + (c0 + c) * lda + r0 + 16 * rb + 2 * l8));
+            }
+#pragma unroll
+            for (int k = 0; k < 8; ++k) {
+                const int pr = gi + 32 * k, c = pr & 63, rb = pr >> 6;
+                s[(16 * rb + 2 * l8) * 65 + c] = v[k].x;
+                s[(16 * rb + 2 * l8 + 1) * 65 + c] = v[k].y;
+            }
+        } else {
+            for (int e = threadIdx.x; e < 64 * 64; e += 256) {
+                const int c = e >> 6, r = e & 63;
+                const int64_t gr = r0 + r, gc = c0 + c;
+                s[r * 65 + c] = (gr < rows && gc < cols) ? A[gc * lda + gr] : 0.0;
+            }
+        }
+        __syncthreads();
+        if (full) {
+#pragma unroll
+            for (int k = 0; k < 8; ++k) {  // run p: B column r0 + p % 64, entries 16 (p / 64) + 2 l8
+                const int pr = gi + 32 * k, r = pr & 63, cb = pr >> 6;
+                const int cc = 16 * cb + 2 * l8;
+                __stcs(reinterpret_cast<double2 *>(B + (r0 + r) * ldb + c0 + cc),
+                       make_double2(s[r * 65 + cc], s[r * 65 + cc + 1]));
+            }
+        } else {
+            for (int e = threadIdx.x; e < 64 * 64; e += 256) {
+                const int r = e >> 6, c = e & 63;
+                const int64_t gr = r0 + r, gc = c0 + c;
+                if (gr < rows && gc < cols) B[gr * ldb + gc] = s[r * 65 + c];
+            }
+        }
+        __syncthreads();
+    }
+}
+
+extern "C" int hsk_transpose(const double *A, int64_t rows, int64_t cols, int64_t lda, double *B,
+                             int64_t ldb, void *stream) {
+    HSK_REQUIRE(rows >= 0 && cols >= 0 && lda >= std::max<int64_t>(rows, 1) &&
+                    ldb >= std::max<int64_t>(cols, 1),
+                HSK_EINVAL, "transpose: bad shape rows=%lld cols=%lld lda=%lld ldb=%lld",
+                (long long)rows, (long long)cols, (long long)lda, (long long)ldb);
+    if (rows == 0 || cols == 0) return HSK_OK;
+    HSK_REQUIRE(A && B, HSK_EINVAL, "transpose: null pointer");
+    const int64_t gx = (rows + 63) / 64;
+    HSK_REQUIRE(gx < (1ll << 31), HSK_EINVAL, "transpose: too many rows");
+    const int vec = (lda % 2 == 0) && (ldb % 2 == 0) && ((reinterpret_cast<uintptr_t>(A) & 15) == 0) &&
+                    ((reinterpret_cast<uintptr_t>(B) & 15) == 0);
+    // ~8 column tiles per CTA: short CTAs balance the tail, enough of them
+    // amortise the start-up
+    const unsigned gy = (unsigned)std::min<int64_t>(std::max<int64_t>(1, (cols + 511) / 512), 65535);
+    transpose_kernel<<<dim3((unsigned)gx, gy, 1), 256, 0, as_stream(stream)>>>(A, rows, cols, lda, B,
+                                                                                 ldb, vec);
+    HSK_CHECK_LAUNCH("transpose_kernel");
+    return HSK_OK;
+}
+
 extern "C" int hsk_l2_flush(void *scratch, int64_t bytes, void *stream) {
     HSK_REQUIRE(scratch && bytes >= 32 && (reinterpret_cast<uintptr_t>(scratch) & 31) == 0,
                 HSK_EINVAL, "l2_flush: need a 32-byte aligned scratch buffer");

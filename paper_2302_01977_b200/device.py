@@ -129,6 +129,13 @@ class DeviceMatrix:
         host.copy_(self.t[col0:col0 + ncols, :self.rows])
         return host.numpy().T  # (rows, ncols) F-contiguous, owned by the caller
 
+    def transposed(self) -> "DeviceMatrix":
+        """A fresh device copy of this matrix's transpose (hsk_transpose)."""
+        out = DeviceMatrix(self.cols, self.rows)
+        _lib.call("hsk_transpose", self.ptr, self.rows, self.cols, self.ld, out.ptr, out.ld,
+                  current_stream_ptr())
+        return out
+
     def column_view(self, col0: int, ncols: int) -> "DeviceMatrix":
         sub = DeviceMatrix.__new__(DeviceMatrix)
         sub.rows, sub.cols, sub.ld = self.rows, ncols, self.ld

@@ -265,22 +265,36 @@ def test_fwht_gpu_known_answers(golden, cuda):
         sk.fwht(np.ones(6))
 
 
-def test_adaptive_append_matches_one_shot(cuda):
+@pytest.mark.parametrize("keep_t", [None, False])
+def test_adaptive_append_matches_one_shot(cuda, keep_t):
+    """Appended increments match the one-shot products; with keep_t None the
+    sketch keeps A^T from the first extension on and runs S' as A^T R^T."""
     rng = np.random.default_rng(21)
     n = 1500
     A = rng.standard_normal((n, n))
     for kind, kw in ((sk.SJLT, dict(alpha=8, construction=sk.BLOCK)), (sk.GAUSSIAN, {}),
                      (sk.SRHT, {})):
         op = sk.new_operator(kind, n, 128, seed=(0, 0), **kw)
-        ds = adaptive.DeviceSketch(sk.DenseAccessor(A), 128 + 5 * 64).start(op)
+        ds = adaptive.DeviceSketch(sk.DenseAccessor(A), 128 + 5 * 64, keep_transpose=keep_t).start(op)
         for r in range(1, 6):
             op = sk.append_columns(op, 64, seed=(0, r))
             ds.extend(op)
         assert ds.d == op.d
+        assert (ds.At is not None) == (keep_t is None)
         _close(ds.right(), O.apply_right(A, op), np.linalg.norm(A))
         _close(ds.transposed(), O.apply_right_transposed(A, op), np.linalg.norm(A))
         # the one-shot API gives the identical bytes (same kernels, same order)
         np.testing.assert_array_equal(ds.right(), sk.apply_right(A, op))
+
+
+@pytest.mark.parametrize("rows,cols,ld", [(1, 1, 2), (33, 70, 34), (257, 100, 258), (1000, 3001, 1000)])
+def test_device_transpose_exact(cuda, rows, cols, ld):
+    rng = np.random.default_rng(rows + cols)
+    B = rng.standard_normal((rows, cols))
+    dm = device.DeviceMatrix.from_host(B, ld=ld)
+    t = dm.transposed()
+    assert t.shape == (cols, rows)
+    np.testing.assert_array_equal(t.to_host(), B.T)
 
 
 def test_streamed_pinned_host_path_is_bit_identical(cuda, monkeypatch):
