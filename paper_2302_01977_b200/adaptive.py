@@ -14,7 +14,8 @@ S = A R^T reads contiguous rows conflict-free.  An adaptive run applies S' to
 the same A once per increment, so from the first extension on (when HBM holds
 a second copy) the sketch keeps A^T -- one transpose, 2 x bytes(A) of traffic
 -- and runs every later S' increment as S = A^T R^T (same entries, same
-per-bucket summation order over the input indices).
+per-bucket summation order over the input indices).  The copy is made at the
+second extension: a run that stops after one never pays for it.
 """
 
 from __future__ import annotations
@@ -38,6 +39,7 @@ class DeviceSketch:
         # A^T for the S' increments: None = when it fits (the default), False = never
         self.keep_transpose = keep_transpose
         self.At = None
+        self._extensions = 0
         self.capacity = int(n_cols_max)
         self.growable = growable
         self.d = 0
@@ -93,6 +95,7 @@ class DeviceSketch:
             raise ValueError("operator dimension does not match A's rows")
         self.d = 0
         self.At = None   # a fresh schedule pays for its own transpose
+        self._extensions = 0
         for blk in op.blocks:
             self._sketch_block(blk)
         self.op = op
@@ -104,7 +107,8 @@ class DeviceSketch:
         known = 0 if self.op is None else len(self.op.blocks)
         if self.op is not None and tuple(op.blocks[:known]) != tuple(self.op.blocks):
             raise ValueError("operator is not an extension of the sketched one")
-        if len(op.blocks) > known:
+        self._extensions += len(op.blocks) > known
+        if self._extensions >= 2:     # a run long enough to repay the copy
             self._maybe_transpose()
         for blk in op.blocks[known:]:
             self._sketch_block(blk)

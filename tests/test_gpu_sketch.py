@@ -268,7 +268,7 @@ def test_fwht_gpu_known_answers(golden, cuda):
 @pytest.mark.parametrize("keep_t", [None, False])
 def test_adaptive_append_matches_one_shot(cuda, keep_t):
     """Appended increments match the one-shot products; with keep_t None the
-    sketch keeps A^T from the first extension on and runs S' as A^T R^T."""
+    sketch keeps A^T from the second extension on and runs S' as A^T R^T."""
     rng = np.random.default_rng(21)
     n = 1500
     A = rng.standard_normal((n, n))
