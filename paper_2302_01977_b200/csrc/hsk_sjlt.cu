@@ -145,6 +145,18 @@ static inline void warp_shape(int rpt, int d, int trans, int &db, int &nw) {
     // bound by the shared-memory port, and more warps measured slower).
     // HSK_SJLT_W32 = 16 / 20 / 24 forces a shape (28: tuning builds).
     const int ws = tuning().sjlt_w32;
+    // 256 < d <= 384 (a light second slab): 128-bucket slabs (16 x 8) split
+    // the buckets evenly -- with stream-K the CTAs of a light slab idle while
+    // the full ones set the time.  Measured (n = 16384, S / S' ms): d = 300
+    // 0.517 / 0.824 vs 0.715 / 1.034 on 256-bucket slabs, d = 320 0.521 / 0.806
+    // vs 0.696 / 0.956, d = 384 0.536 / 0.678 vs 0.637 / 0.859; not for d in
+    // (512, 640]: 0.742 vs 0.712.  HSK_SJLT_W32 = 8 forces it, 16 / 20 / 24
+    // the wide shapes.
+    if (rpt == 2 && d > 128 && !w32 && (ws == 8 || (ws < 16 && d > 256 && d <= 384))) {
+        nw = 16;
+        db = 8;
+        return;
+    }
     if (rpt == 2 && d > 128 && !w32 && ws != 16 && (!trans || (HSK_TUNING && ws >= 20))) {
         const int pick = ws >= 20 ? ws : d > 512 ? 24 : 20;
         if (pick == 20) { nw = 20; db = 13; return; }
