@@ -156,7 +156,7 @@ HSK_API int hsk_gen_toeplitz_sin(int64_t n, int64_t row0, int64_t nrows, int64_t
                          double *A, int64_t lda, void *stream);
 
 /* B = A^T: A rows x cols column-major (lda), B cols x rows column-major (ldb),
- * both device.  The adaptive sketch keeps A^T once so every S' increment runs
+ * both device, not overlapping.  The adaptive sketch keeps A^T once so every S' increment runs
  * as S = A^T R^T on conflict-free tiles (adaptive.DeviceSketch). */
 HSK_API int hsk_transpose(const double *A, int64_t rows, int64_t cols, int64_t lda, double *B,
                           int64_t ldb, void *stream);
