@@ -34,6 +34,10 @@ import os
 import sys
 import time
 
+# every kernel of libhsk loaded at context creation: with lazy loading (the
+# CUDA 12 default) a row that first uses a kernel variant would pay its load
+os.environ.setdefault("CUDA_MODULE_LOADING", "EAGER")
+
 import numpy as np
 import torch
 
