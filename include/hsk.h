@@ -161,6 +161,11 @@ HSK_API int hsk_gen_toeplitz_sin(int64_t n, int64_t row0, int64_t nrows, int64_t
 HSK_API int hsk_transpose(const double *A, int64_t rows, int64_t cols, int64_t lda, double *B,
                           int64_t ldb, void *stream);
 
+/* *flag (one int32, DEVICE memory) = 1 if the n x n column-major A (lda) is not
+ * bitwise symmetric, else 0 (stream-ordered; read it after a sync).  An adaptive
+ * sketch of a symmetric A gets S' = A^T R^T = A R^T = S, bit for bit. */
+HSK_API int hsk_is_symmetric(const double *A, int64_t n, int64_t lda, int32_t *flag, void *stream);
+
 /* Streams `bytes` of scratch (device) to evict L2 between timed launches. */
 HSK_API int hsk_l2_flush(void *scratch, int64_t bytes, void *stream);
 

@@ -49,6 +49,7 @@ SIGNATURES = {
                                             _c_p]),
     "hsk_l2_flush": (ctypes.c_int, [_c_p, _c_i64, _c_p]),
     "hsk_transpose": (ctypes.c_int, [_c_p, _c_i64, _c_i64, _c_i64, _c_p, _c_i64, _c_p]),
+    "hsk_is_symmetric": (ctypes.c_int, [_c_p, _c_i64, _c_i64, _c_p, _c_p]),
     "hsk_ipc_alloc": (ctypes.c_int, [_c_i64, ctypes.POINTER(_c_p), _c_p]),
     "hsk_ipc_free": (ctypes.c_int, [_c_p]),
     "hsk_ipc_open": (ctypes.c_int, [_c_p, ctypes.POINTER(_c_p)]),

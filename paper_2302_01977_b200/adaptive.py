@@ -15,7 +15,10 @@ the same A once per increment, so from the first extension on (when HBM holds
 a second copy) the sketch keeps A^T -- one transpose, 2 x bytes(A) of traffic
 -- and runs every later S' increment as S = A^T R^T (same entries, same
 per-bucket summation order over the input indices).  The copy is made at the
-second extension: a run that stops after one never pays for it.
+second extension: a run that stops after one never pays for it.  A bitwise
+symmetric A (kernel and covariance matrices) needs no copy: A^T R^T = A R^T
+exactly, so from then on S' columns are the S columns just computed (one
+symmetry check, hsk_is_symmetric, instead of the transpose).
 """
 
 from __future__ import annotations
@@ -39,6 +42,7 @@ class DeviceSketch:
         # A^T for the S' increments: None = when it fits (the default), False = never
         self.keep_transpose = keep_transpose
         self.At = None
+        self.sym = False      # A == A^T bitwise: S' increments are copies of S
         self._extensions = 0
         self.capacity = int(n_cols_max)
         self.growable = growable
@@ -69,7 +73,10 @@ class DeviceSketch:
         if self.S is not None:
             _dev.apply_block(blk, self.A, False, self.S, self.d)
         if self.St is not None:
-            if self.At is not None:     # S' = (A^T) R^T on the kept transpose
+            if self.sym and self.S is not None:    # A^T R^T = A R^T, bit for bit
+                n = self.A.rows
+                self.St.t[self.d:self.d + blk.rows, :n].copy_(self.S.t[self.d:self.d + blk.rows, :n])
+            elif self.At is not None:     # S' = (A^T) R^T on the kept transpose
                 _dev.apply_block(blk, self.At, False, self.St, self.d)
             else:
                 _dev.apply_block(blk, self.A, True, self.St, self.d)
@@ -77,8 +84,12 @@ class DeviceSketch:
 
     def _maybe_transpose(self):
         """Keep A^T for the remaining S' increments if it fits in free HBM
-        (with a quarter of A as margin) -- or always / never when asked."""
-        if self.St is None or self.At is not None or self.keep_transpose is False:
+        (with a quarter of A as margin) -- or always / never when asked; a
+        symmetric A needs neither."""
+        if self.St is None or self.At is not None or self.sym or self.keep_transpose is False:
+            return
+        if self.S is not None and self.A.is_symmetric():
+            self.sym = True
             return
         if self.keep_transpose is None:
             import torch
@@ -94,7 +105,8 @@ class DeviceSketch:
         if self.St is not None and op.n != self.A.rows:
             raise ValueError("operator dimension does not match A's rows")
         self.d = 0
-        self.At = None   # a fresh schedule pays for its own transpose
+        self.At = None   # a fresh schedule pays for its own transpose / check
+        self.sym = False
         self._extensions = 0
         for blk in op.blocks:
             self._sketch_block(blk)

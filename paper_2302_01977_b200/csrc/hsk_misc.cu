@@ -359,6 +359,77 @@ extern "C" int hsk_transpose(const double *A, int64_t rows, int64_t cols, int64_
     return HSK_OK;
 }
 
+// Symmetry test of an n x n column-major A: CTA (bi, bj), bi <= bj, loads tile
+// (bi, bj) into shared memory with the transpose kernel's whole-line pattern,
+// then reads tile (bj, bi) the same way and compares each element bitwise with
+// its mirror; any mismatch sets *flag.  CTAs start by polling the flag, so a
+// nonsymmetric A costs about one wave.
+__global__ void __launch_bounds__(256) symmetric_kernel(const double *__restrict__ A, int64_t n,
+                                                        int64_t lda, int32_t *flag, int vec) {
+    __shared__ unsigned long long s[64 * 65];
+    __shared__ int bad;
+    const int64_t bi = blockIdx.x, bj = blockIdx.y;
+    if (bj < bi) return;
+    if (threadIdx.x == 0) bad = *reinterpret_cast<volatile int32_t *>(flag);
+    __syncthreads();
+    if (bad) return;
+    const unsigned long long *a = reinterpret_cast<const unsigned long long *>(A);
+    const int l8 = threadIdx.x & 7, gi = threadIdx.x >> 3;
+    const int64_t r0 = bi * 64, c0 = bj * 64;
+    const bool full = vec && r0 + 64 <= n && c0 + 64 <= n;
+    if (full) {
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {  // tile (bi, bj): s[r][c] = A(r0 + r, c0 + c)
+            const int pr = gi + 32 * k, c = pr & 63, rb = pr >> 6;
+            const ulonglong2 v =
+                *reinterpret_cast<const ulonglong2 *>(a + (c0 + c) * lda + r0 + 16 * rb + 2 * l8);
+            s[(16 * rb + 2 * l8) * 65 + c] = v.x;
+            s[(16 * rb + 2 * l8 + 1) * 65 + c] = v.y;
+        }
+    } else {
+        for (int e = threadIdx.x; e < 64 * 64; e += 256) {
+            const int c = e >> 6, r = e & 63;
+            const int64_t gr = r0 + r, gc = c0 + c;
+            s[r * 65 + c] = (gr < n && gc < n) ? a[gc * lda + gr] : 0ull;
+        }
+    }
+    __syncthreads();
+    int mism = 0;
+    if (full) {
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {  // tile (bj, bi): A(c0 + r', r0 + c') == s[c'][r']
+            const int pr = gi + 32 * k, cc = pr & 63, rb = pr >> 6;
+            const ulonglong2 v =
+                *reinterpret_cast<const ulonglong2 *>(a + (r0 + cc) * lda + c0 + 16 * rb + 2 * l8);
+            mism |= v.x != s[cc * 65 + 16 * rb + 2 * l8];
+            mism |= v.y != s[cc * 65 + 16 * rb + 2 * l8 + 1];
+        }
+    } else {
+        for (int e = threadIdx.x; e < 64 * 64; e += 256) {
+            const int cc = e >> 6, rr = e & 63;  // A(c0 + rr, r0 + cc) vs A(r0 + cc, c0 + rr)
+            const int64_t gr = c0 + rr, gc = r0 + cc;
+            if (gr < n && gc < n) mism |= a[gc * lda + gr] != s[cc * 65 + rr];
+        }
+    }
+    if (__syncthreads_or(mism) && threadIdx.x == 0) atomicExch(flag, 1);
+}
+
+extern "C" int hsk_is_symmetric(const double *A, int64_t n, int64_t lda, int32_t *flag, void *stream) {
+    HSK_REQUIRE(n >= 0 && lda >= std::max<int64_t>(n, 1) && flag, HSK_EINVAL,
+                "is_symmetric: bad arguments n=%lld lda=%lld", (long long)n, (long long)lda);
+    cudaError_t e = cudaMemsetAsync(flag, 0, sizeof(int32_t), as_stream(stream));
+    if (e != cudaSuccess) return cuda_status(e, "is_symmetric: memset");
+    if (n == 0) return HSK_OK;
+    HSK_REQUIRE(A, HSK_EINVAL, "is_symmetric: null matrix");
+    const int64_t nb = (n + 63) / 64;
+    HSK_REQUIRE(nb < 65536, HSK_EINVAL, "is_symmetric: n too large");
+    const int vec = (lda % 2 == 0) && ((reinterpret_cast<uintptr_t>(A) & 15) == 0);
+    symmetric_kernel<<<dim3((unsigned)nb, (unsigned)nb, 1), 256, 0, as_stream(stream)>>>(A, n, lda, flag,
+                                                                                           vec);
+    HSK_CHECK_LAUNCH("symmetric_kernel");
+    return HSK_OK;
+}
+
 extern "C" int hsk_l2_flush(void *scratch, int64_t bytes, void *stream) {
     HSK_REQUIRE(scratch && bytes >= 32 && (reinterpret_cast<uintptr_t>(scratch) & 31) == 0,
                 HSK_EINVAL, "l2_flush: need a 32-byte aligned scratch buffer");

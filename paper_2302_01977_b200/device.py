@@ -136,6 +136,16 @@ class DeviceMatrix:
                   current_stream_ptr())
         return out
 
+    def is_symmetric(self) -> bool:
+        """True if this square matrix equals its transpose bit for bit
+        (hsk_is_symmetric; one host sync)."""
+        if self.rows != self.cols:
+            return False
+        flag = torch.empty(1, dtype=torch.int32, device=self.t.device)
+        _lib.call("hsk_is_symmetric", self.ptr, self.rows, self.ld, flag.data_ptr(),
+                  current_stream_ptr())
+        return int(flag.item()) == 0
+
     def column_view(self, col0: int, ncols: int) -> "DeviceMatrix":
         sub = DeviceMatrix.__new__(DeviceMatrix)
         sub.rows, sub.cols, sub.ld = self.rows, ncols, self.ld

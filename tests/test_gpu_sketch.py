@@ -265,13 +265,16 @@ def test_fwht_gpu_known_answers(golden, cuda):
         sk.fwht(np.ones(6))
 
 
-@pytest.mark.parametrize("keep_t", [None, False])
-def test_adaptive_append_matches_one_shot(cuda, keep_t):
+@pytest.mark.parametrize("keep_t,sym", [(None, False), (False, False), (None, True)])
+def test_adaptive_append_matches_one_shot(cuda, keep_t, sym):
     """Appended increments match the one-shot products; with keep_t None the
-    sketch keeps A^T from the second extension on and runs S' as A^T R^T."""
+    sketch keeps A^T from the second extension on and runs S' as A^T R^T, or,
+    for a symmetric A, copies S' from S."""
     rng = np.random.default_rng(21)
     n = 1500
     A = rng.standard_normal((n, n))
+    if sym:
+        A = A + A.T
     for kind, kw in ((sk.SJLT, dict(alpha=8, construction=sk.BLOCK)), (sk.GAUSSIAN, {}),
                      (sk.SRHT, {})):
         op = sk.new_operator(kind, n, 128, seed=(0, 0), **kw)
@@ -280,7 +283,8 @@ def test_adaptive_append_matches_one_shot(cuda, keep_t):
             op = sk.append_columns(op, 64, seed=(0, r))
             ds.extend(op)
         assert ds.d == op.d
-        assert (ds.At is not None) == (keep_t is None)
+        assert (ds.At is not None) == (keep_t is None and not sym)
+        assert ds.sym == (keep_t is None and sym)
         _close(ds.right(), O.apply_right(A, op), np.linalg.norm(A))
         _close(ds.transposed(), O.apply_right_transposed(A, op), np.linalg.norm(A))
         # the one-shot API gives the identical bytes (same kernels, same order)
@@ -295,6 +299,19 @@ def test_device_transpose_exact(cuda, rows, cols, ld):
     t = dm.transposed()
     assert t.shape == (cols, rows)
     np.testing.assert_array_equal(t.to_host(), B.T)
+
+
+@pytest.mark.parametrize("n,ld", [(1, 2), (64, 64), (65, 66), (200, 201), (1000, 1000)])
+def test_device_symmetry_check(cuda, n, ld):
+    rng = np.random.default_rng(n)
+    B = rng.standard_normal((n, n))
+    S = B + B.T
+    assert device.DeviceMatrix.from_host(S, ld=ld).is_symmetric()
+    if n > 1:
+        S2 = S.copy()
+        S2[n - 1, 0] = np.nextafter(S2[n - 1, 0], np.inf)   # one ulp off the mirror
+        assert not device.DeviceMatrix.from_host(S2, ld=ld).is_symmetric()
+        assert not device.DeviceMatrix.from_host(B, ld=ld).is_symmetric()
 
 
 def test_streamed_pinned_host_path_is_bit_identical(cuda, monkeypatch):
