@@ -39,7 +39,9 @@ class DeviceSketch:
     def __init__(self, A, n_cols_max: int, *, right: bool = True, transposed: bool = True,
                  growable: bool = False, keep_transpose: bool | None = None):
         self.A = _sk.device_matrix_of(A)
-        # A^T for the S' increments: None = when it fits (the default), False = never
+        # A^T (or the symmetry shortcut) for the S' increments: None = for an A
+        # of at least MIN_BYTES that fits twice in HBM (the default), True =
+        # whenever it fits, False = never
         self.keep_transpose = keep_transpose
         self.At = None
         self.sym = False      # A == A^T bitwise: S' increments are copies of S
@@ -82,20 +84,26 @@ class DeviceSketch:
                 _dev.apply_block(blk, self.A, True, self.St, self.d)
         self.d += blk.rows
 
+    # below this size of A the adaptive S' shortcuts are not tried (measured:
+    # n = 8000, 3-18 blocks ran up to 2x slower with them; C3 at 34 GB and the
+    # covariance n = 27000 runs at 5.8 GB gain)
+    MIN_BYTES = 4 << 30
+
     def _maybe_transpose(self):
         """Keep A^T for the remaining S' increments if it fits in free HBM
-        (with a quarter of A as margin) -- or always / never when asked; a
-        symmetric A needs neither."""
+        (with a quarter of A as margin); a bitwise-symmetric A needs no copy.
+        keep_transpose None: only for an A of at least MIN_BYTES."""
         if self.St is None or self.At is not None or self.sym or self.keep_transpose is False:
             return
+        if self.keep_transpose is None and 8 * self.A.rows * self.A.cols < self.MIN_BYTES:
+            return  # small A: the check, the copy and its allocation cost more than they save
         if self.S is not None and self.A.is_symmetric():
             self.sym = True
             return
-        if self.keep_transpose is None:
-            import torch
-            free, _ = torch.cuda.mem_get_info()
-            if free < 1.25 * 8 * self.A.rows * self.A.cols + (1 << 30):
-                return
+        import torch
+        free, _ = torch.cuda.mem_get_info()
+        if free < 1.25 * 8 * self.A.rows * self.A.cols + (1 << 30):
+            return
         self.At = self.A.transposed()
 
     def start(self, op) -> "DeviceSketch":

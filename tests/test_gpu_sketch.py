@@ -265,11 +265,12 @@ def test_fwht_gpu_known_answers(golden, cuda):
         sk.fwht(np.ones(6))
 
 
-@pytest.mark.parametrize("keep_t,sym", [(None, False), (False, False), (None, True)])
+@pytest.mark.parametrize("keep_t,sym", [(True, False), (False, False), (True, True), (None, False)])
 def test_adaptive_append_matches_one_shot(cuda, keep_t, sym):
-    """Appended increments match the one-shot products; with keep_t None the
+    """Appended increments match the one-shot products; with keep_t True the
     sketch keeps A^T from the second extension on and runs S' as A^T R^T, or,
-    for a symmetric A, copies S' from S."""
+    for a symmetric A, copies S' from S (None: only for an A of at least
+    DeviceSketch.MIN_BYTES -- not this one)."""
     rng = np.random.default_rng(21)
     n = 1500
     A = rng.standard_normal((n, n))
@@ -283,8 +284,8 @@ def test_adaptive_append_matches_one_shot(cuda, keep_t, sym):
             op = sk.append_columns(op, 64, seed=(0, r))
             ds.extend(op)
         assert ds.d == op.d
-        assert (ds.At is not None) == (keep_t is None and not sym)
-        assert ds.sym == (keep_t is None and sym)
+        assert (ds.At is not None) == (keep_t is True and not sym)
+        assert ds.sym == (keep_t is True and sym)
         _close(ds.right(), O.apply_right(A, op), np.linalg.norm(A))
         _close(ds.transposed(), O.apply_right_transposed(A, op), np.linalg.norm(A))
         # the one-shot API gives the identical bytes (same kernels, same order)

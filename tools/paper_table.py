@@ -135,8 +135,11 @@ def sketch_phase(A, kind: str, final_d: int, seed: int = 0):
     torch.cuda.synchronize()
     wall_ms = (time.perf_counter() - w0) * 1e3
     assert ds.d == final_d + 64
+    # later S' increments: "kernel" (A^T R^T on A), "transpose" (S on the kept
+    # A^T) or "copy" (A bitwise symmetric: S' = S)
+    sp = "copy" if ds.sym else "transpose" if ds.At is not None else "kernel"
     return {"device_ms": e0.elapsed_time(e1), "wall_ms": wall_ms, "draw_ms": draw_ms,
-            "blocks": 1 + rounds, "cols": final_d + 64}
+            "blocks": 1 + rounds, "cols": final_d + 64, "s_prime_increments": sp}
 
 
 def full_construction(A, tree, kind: str, eps: float, seed: int = 0):
