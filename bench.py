@@ -619,7 +619,7 @@ def cfg_c3(args, peak):
            "gpu_launches": 5 * ds.launches_per_schedule(incs)}
     rec["roofline"]["note"] = ("achieved = algorithmic bytes of the schedule's passes over A "
                                "(A + the increment's S and S' columns per pass) / schedule time; "
-                               "from the second extension on S' runs as A^T R^T on a transposed "
+                               "from the fifth extension on S' runs as A^T R^T on a transposed "
                                "copy made once per schedule (its 2 x bytes(A) and time included)")
     rec["kept_transpose"] = ds.At is not None
     if not args.no_cpu:

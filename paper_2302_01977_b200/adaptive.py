@@ -11,11 +11,11 @@ kernels once for the new block, writing straight into columns
 S' = A^T R^T of a TMA-landed A tile reads 8-byte column values whose
 16-row groups share 8 bank pairs (2-way conflicts), while
 S = A R^T reads contiguous rows conflict-free.  An adaptive run applies S' to
-the same A once per increment, so from the first extension on (when HBM holds
-a second copy) the sketch keeps A^T -- one transpose, 2 x bytes(A) of traffic
+the same A once per increment, so in a long run (when HBM holds a second
+copy) the sketch keeps A^T -- one transpose, 2 x bytes(A) of traffic
 -- and runs every later S' increment as S = A^T R^T (same entries, same
 per-bucket summation order over the input indices).  The copy is made at the
-second extension: a run that stops after one never pays for it.  A bitwise
+fifth extension (AFTER_EXTENSIONS), so short runs never pay for it.  A bitwise
 symmetric A (kernel and covariance matrices) needs no copy: A^T R^T = A R^T
 exactly, so from then on S' columns are the S columns just computed (one
 symmetry check, hsk_is_symmetric, instead of the transpose).
@@ -88,6 +88,12 @@ class DeviceSketch:
     # n = 8000, 3-18 blocks ran up to 2x slower with them; C3 at 34 GB and the
     # covariance n = 27000 runs at 5.8 GB gain)
     MIN_BYTES = 4 << 30
+    # ... and only from this extension on: the copy costs ~9 increments' S'
+    # savings (2 x bytes(A) at 5.7 TB/s vs ~0.3 x bytes(A) saved per S'), so a
+    # rent-or-buy wait bounds the loss of short runs (Table 7.1's 4-extension
+    # covariance runs at n = 27000 were 10-20 % slower with the copy at the
+    # second extension) while long ones (C3: 15 extensions) still gain
+    AFTER_EXTENSIONS = 5
 
     def _maybe_transpose(self):
         """Keep A^T for the remaining S' increments if it fits in free HBM
@@ -128,7 +134,7 @@ class DeviceSketch:
         if self.op is not None and tuple(op.blocks[:known]) != tuple(self.op.blocks):
             raise ValueError("operator is not an extension of the sketched one")
         self._extensions += len(op.blocks) > known
-        if self._extensions >= 2:     # a run long enough to repay the copy
+        if self._extensions >= self.AFTER_EXTENSIONS:  # a run long enough to repay the copy
             self._maybe_transpose()
         for blk in op.blocks[known:]:
             self._sketch_block(blk)

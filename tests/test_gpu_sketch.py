@@ -268,7 +268,7 @@ def test_fwht_gpu_known_answers(golden, cuda):
 @pytest.mark.parametrize("keep_t,sym", [(True, False), (False, False), (True, True), (None, False)])
 def test_adaptive_append_matches_one_shot(cuda, keep_t, sym):
     """Appended increments match the one-shot products; with keep_t True the
-    sketch keeps A^T from the second extension on and runs S' as A^T R^T, or,
+    sketch keeps A^T from the fifth extension on and runs S' as A^T R^T, or,
     for a symmetric A, copies S' from S (None: only for an A of at least
     DeviceSketch.MIN_BYTES -- not this one)."""
     rng = np.random.default_rng(21)
@@ -279,8 +279,8 @@ def test_adaptive_append_matches_one_shot(cuda, keep_t, sym):
     for kind, kw in ((sk.SJLT, dict(alpha=8, construction=sk.BLOCK)), (sk.GAUSSIAN, {}),
                      (sk.SRHT, {})):
         op = sk.new_operator(kind, n, 128, seed=(0, 0), **kw)
-        ds = adaptive.DeviceSketch(sk.DenseAccessor(A), 128 + 5 * 64, keep_transpose=keep_t).start(op)
-        for r in range(1, 6):
+        ds = adaptive.DeviceSketch(sk.DenseAccessor(A), 128 + 6 * 64, keep_transpose=keep_t).start(op)
+        for r in range(1, 7):      # the shortcut starts at the fifth extension
             op = sk.append_columns(op, 64, seed=(0, r))
             ds.extend(op)
         assert ds.d == op.d
