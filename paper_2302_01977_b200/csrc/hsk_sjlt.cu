@@ -85,6 +85,8 @@ constexpr int64_t kMaxD = (1 << 19);    // bucket index fits 19 bits of the sort
 // 32-row tiles with 512-bucket slabs and TK = 256 (half the slab re-reads).
 struct Geom {
     int pair;          // paired plan (block construction, d/alpha = 8): below
+    int even;          // group lists start at even words (S' on 64-row tiles: the
+                       // walker fetches entry words in 8-byte pairs)
     int rpt;           // rows per lane (tile rows tm = 32 * rpt)
     int db, nw;        // buckets per consumer warp, consumer warps per CTA
     int64_t ngroups;   // warp groups of db buckets (nslabs * nw)
@@ -94,7 +96,9 @@ struct Geom {
     int tk;            // input indices per chunk
     int64_t nchunks;
     int64_t gstride;   // uint32 per group-start row (ngroups + 1, padded)
-    int64_t estride;   // words per chunk row (tk*alpha entries + ngroups terminators)
+    int64_t estride;   // words per chunk row (tk*alpha entries + group terminators;
+                       // even: every group list starts at an even word, so up to
+                       // 2 * ngroups + 1 words besides the entries)
     int64_t gptr_off;  // bytes from the plan base
     int64_t ent_off;   // bytes from the plan base
     int64_t end;       // bytes from the plan base (end of this sub-plan)
@@ -188,6 +192,7 @@ static Geom geom_dir(int64_t n, int d, int alpha, int trans, int64_t base, int p
     Geom g;
     int tk;
     g.pair = pair;
+    g.even = 0;
     if (pair) {
         constexpr int kStage3 = (226 * 1024 - 2048) / 3, kStage2 = (226 * 1024 - 2048) / 2;
         const int ae = alpha / 2;  // entries per input index
@@ -225,19 +230,23 @@ static Geom geom_dir(int64_t n, int d, int alpha, int trans, int64_t base, int p
     // d = 2048, alpha = 8)
     const bool wide = n >= 8192 && (trans || d <= 512);
     g.rpt = d <= 64 ? 4 : 2;
+    // (even-start entry rows: 2 * ngroups + 1 words besides the entries --
+    // passed to the TK fit as its group-word count)
     if (const int e = trans ? tuning().sjlt_rpt_t : tuning().sjlt_rpt; e == 2 || e == 4 || (HSK_TUNING && e == 1))
         g.rpt = e;
     warp_shape(g.rpt, d, trans, g.db, g.nw);
     g.ngroups = roundup(d, (int64_t)g.db * g.nw) / g.db;
+    g.even = trans && g.rpt == 2;
+    const int64_t gw = g.even ? 2 * g.ngroups + 1 : g.ngroups;
     if (d <= 64) {
-        tk = wide && !trans ? tk_fit16(alpha, 128, 256, kStage2, g.ngroups, g.nw)
-                            : tk_fit(alpha, 128, 128, kStage3, g.ngroups, g.nw);
+        tk = wide && !trans ? tk_fit16(alpha, 128, 256, kStage2, gw, g.nw)
+                            : tk_fit(alpha, 128, 128, kStage3, gw, g.nw);
     } else {
         // (S on the 20 x 13 warps: TK 128 x 3 stages measured faster in bursts,
         // C2 0.439 vs 0.449 ms over 20 launches, but slower under the power cap,
         // 0.514 vs 0.494 ms over 2000: two stages of TK 208 kept)
-        tk = wide ? tk_fit16(alpha, 64, 256, kStage2, g.ngroups, g.nw)
-                  : tk_fit(alpha, 64, 128, kStage3, g.ngroups, g.nw);
+        tk = wide ? tk_fit16(alpha, 64, 256, kStage2, gw, g.nw)
+                  : tk_fit(alpha, 64, 128, kStage3, gw, g.nw);
     }
     if (const int e = trans ? tuning().sjlt_tk_t : tuning().sjlt_tk; e > 0) tk = e;
     g.tm = 32 * g.rpt;
@@ -245,7 +254,7 @@ static Geom geom_dir(int64_t n, int d, int alpha, int trans, int64_t base, int p
     g.tk = tk;
     g.nchunks = (n + g.tk - 1) / g.tk;
     g.gstride = roundup(g.ngroups + 4, 4);  // a CTA copies nw + 1 starts, 16-byte rows
-    g.estride = roundup((int64_t)g.tk * alpha + g.ngroups, 4);  // 16-byte rows for the bulk copy
+    g.estride = roundup((int64_t)g.tk * alpha + gw, 4);  // 16-byte rows for the bulk copy
     g.gptr_off = base;
     g.ent_off = roundup(g.gptr_off + (g.nchunks + 1) * g.gstride * 4, 128);
     g.end = g.ent_off + roundup((g.nchunks + 1) * g.estride * 4, 128);
@@ -292,6 +301,10 @@ static bool geom_ok(const Geom &g, int alpha) {
 //   S' tiles (tm_t = -TM, transposed layout of 128-row tiles): kk*TM*8 | (kk%32)*8 --
 //                         lane address st + (e & 0xffff00) + ((e & 248) ^ 8*lane)
 // Group starts: gptr[c * gstride + g] = index of group g's first word.
+// Even plans (S' on 64-row tiles) start every group at an even word,
+// (lb(g) + 2g + 1) & ~1 with lb(g) = entries of the chunk in groups < g (a
+// list of cnt_g entries and its terminator ends at or before the next start),
+// so the walker fetches entry words in 8-byte pairs; the gaps stay null words.
 __host__ __device__ inline uint32_t entry_addr(uint32_t kk, int tm_t) {
     if (tm_t < 0) return kk * (uint32_t)(-tm_t) * 8u + ((kk & 31u) << 3);
     return tm_t ? (kk >> 4) * (uint32_t)tm_t * 128u + ((kk & 15u) << 3) : kk;
@@ -301,7 +314,7 @@ __host__ __device__ inline uint32_t entry_addr(uint32_t kk, int tm_t) {
 // bucket-tagged entry words, group terminators and group starts.
 __global__ void sjlt_plan_kernel(const int32_t *__restrict__ pos, const int8_t *__restrict__ sgn,
                                  int64_t n, int d, int alpha, int tk, int p2, int db, int64_t ngroups,
-                                 int64_t gstride, int64_t estride, int tm_t, int pair,
+                                 int64_t gstride, int64_t estride, int tm_t, int pair, int even,
                                  uint32_t *__restrict__ gptr, uint32_t *__restrict__ ent, int *err) {
     extern __shared__ uint32_t keys[];
     const int64_t c = blockIdx.x;
@@ -349,9 +362,21 @@ __global__ void sjlt_plan_kernel(const int32_t *__restrict__ pos, const int8_t *
         }
     }
     uint32_t *e_out = ent + c * estride;
-    // padding after the last terminator (the walk loads, never uses, one word
-    // past a terminator): null words
-    for (int64_t e = cnt + ngroups + threadIdx.x; e < estride; e += blockDim.x) e_out[e] = 0u;
+    // padding after the last terminator (the walk loads, never uses, up to two
+    // words past a terminator): null words (the host zero-fills the plan; the
+    // even rows' gaps stay null)
+    if (!even)
+        for (int64_t e = cnt + ngroups + threadIdx.x; e < estride; e += blockDim.x) e_out[e] = 0u;
+    // first key index of group g (keys sorted; unpaired plans)
+    auto lb_of = [&](int64_t g) {
+        const uint32_t target = (uint32_t)(g * db) << 12;
+        int lo = 0, hi = cnt;
+        while (lo < hi) {
+            const int mid = (lo + hi) >> 1;
+            if (keys[mid] < target) lo = mid + 1; else hi = mid;
+        }
+        return lo;
+    };
     // paired S' plans on TMA-landed tiles (tm_t > 0): within each (warp,
     // combo) run, entries of opposite input parity are emitted as adjacent
     // pairs (head word flagged, bit 29) ahead of the run's singles: the walker
@@ -373,8 +398,15 @@ __global__ void sjlt_plan_kernel(const int32_t *__restrict__ pos, const int8_t *
         }
         const uint32_t b = key >> 12;
         const int local = key & 4095;
-        e_out[e + b / (uint32_t)db] = (sgn[q0 + local] < 0 ? 0x80000000u : 0u) | ((b % (uint32_t)db) << 24) |
-                                      entry_addr((uint32_t)(local / alpha), tm_t);
+        const uint32_t grp = b / (uint32_t)db;
+        int64_t at = e + grp;
+        if (even) {
+            const int lb = lb_of(grp);
+            at = ((lb + 2 * (int64_t)grp + 1) & ~(int64_t)1) + (e - lb);
+        }
+        e_out[at] =
+            (sgn[q0 + local] < 0 ? 0x80000000u : 0u) | ((b % (uint32_t)db) << 24) |
+            entry_addr((uint32_t)(local / alpha), tm_t);
     }
     if (parity) {
         __syncthreads();
@@ -416,9 +448,18 @@ __global__ void sjlt_plan_kernel(const int32_t *__restrict__ pos, const int8_t *
             lb = lo;
         }
         const int64_t gg = g < ngroups ? g : ngroups;
-        g_out[g] = (uint32_t)(lb + gg);
-        // group g-1 ends where group g starts: its terminator
-        if (g >= 1 && g <= ngroups) e_out[lb + g - 1] = (uint32_t)(pair ? 16 : db) << 24;
+        if (!even) {
+            g_out[g] = (uint32_t)(lb + gg);
+            // group g-1 ends where group g starts: its terminator
+            if (g >= 1 && g <= ngroups) e_out[lb + g - 1] = (uint32_t)(pair ? 16 : db) << 24;
+        } else {
+            g_out[g] = (uint32_t)((lb + 2 * gg + 1) & ~(int64_t)1);
+            // group g's terminator after its entries
+            if (g < ngroups) {
+                const int64_t st = (lb + 2 * g + 1) & ~(int64_t)1;
+                e_out[st + (lb_of(g + 1) - lb)] = (uint32_t)db << 24;
+            }
+        }
     }
 }
 
@@ -979,10 +1020,14 @@ __global__ void __launch_bounds__((NW + (PROD ? (TRANS && RPT == 4 ? kXposeProdu
                 const uint32_t *gs = reinterpret_cast<const uint32_t *>(R.stage0 + (size_t)s * p.stage_bytes + p.gs_off);
                 const uint32_t *en = reinterpret_cast<const uint32_t *>(R.stage0 + (size_t)s * p.stage_bytes + p.en_off);
                 const uint32_t b0 = gs[warp], b1 = gs[warp + 1];
-                bool bad = b0 >= b1 || b1 > (uint32_t)p.estride || ((en[b1 - 1] >> 24) & 127u) != (uint32_t)DB;
-                for (uint32_t q = b0; !bad && q + 1 < b1; ++q)
-                    bad = ((en[q] >> 24) & 127u) >= (uint32_t)DB ||
+                // (unpaired lists start at even words: a null word may follow
+                // the terminator)
+                uint32_t q = b0;
+                bool bad = b0 >= b1 || b1 > (uint32_t)p.estride;
+                for (; !bad && q < b1 && ((en[q] >> 24) & 127u) != (uint32_t)DB; ++q)
+                    bad = ((en[q] >> 24) & 127u) > (uint32_t)DB ||
                           (q > b0 && ((en[q] >> 24) & 127u) < ((en[q - 1] >> 24) & 127u));
+                bad = bad || q >= b1 || (TRANS && RPT == 2 && !PAIR && (b0 & 1u));
                 if (bad) {
                     printf("sjlt dbg: cta %d warp %d chunk-iter %d bad list [%u, %u) estride %d\n",
                            (int)blockIdx.x, warp, ic, b0, b1, (int)p.estride);
@@ -1384,7 +1429,7 @@ extern "C" int hsk_sjlt_plan_build_ex(const int32_t *pos, const int8_t *sgn, int
             while (p2 < g->tk * (g->pair ? alpha / 2 : alpha)) p2 <<= 1;
             sjlt::sjlt_plan_kernel<<<(unsigned)g->nchunks, 256, 2 * p2 * sizeof(uint32_t), st>>>(
                 pos, sgn, n, d, alpha, g->tk, p2, g->db, g->ngroups, g->gstride, g->estride,
-                g == &pl.t ? (g->rpt == 4 ? -g->tm : g->tm) : 0, g->pair,
+                g == &pl.t ? (g->rpt == 4 ? -g->tm : g->tm) : 0, g->pair, g->even,
                 reinterpret_cast<uint32_t *>(base + g->gptr_off),
                 reinterpret_cast<uint32_t *>(base + g->ent_off), reinterpret_cast<int *>(base + 28));
             HSK_CHECK_LAUNCH("sjlt_plan_kernel");

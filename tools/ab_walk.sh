@@ -1,0 +1,14 @@
+# A/B of walker builds on one box: bash tools/ab_walk.sh <tag> <lib names...>
+# (libs under _exp/ab/libhsk_<name>.so; "new" = the in-tree build); parity of
+# the in-tree build first, then kbench and the 2000-launch sustain run per lib
+tag=$1; shift
+mkdir -p gpurun_out
+timeout 900 python -m pytest tests/test_gpu_sketch.py tests/test_gpu_configs.py -x -q > gpurun_out/pt_$tag.log 2>&1; tail -2 gpurun_out/pt_$tag.log
+for rep in 1 2; do
+for lib in "$@"; do
+  if [ $lib = new ]; then L=""; else L=_exp/ab/libhsk_$lib.so; fi
+  HSK_LIB=$L timeout 600 python tools/kbench.py --cases ${CASES:-c1,c2s,c5shard,c5shard_t} --reps 30 > gpurun_out/kb_${tag}_${lib}_$rep.json 2>&1
+  echo "== $lib ($rep)"; tail -1 gpurun_out/kb_${tag}_${lib}_$rep.json | python -c "import json,sys; d=json.loads(sys.stdin.read())['results']; print(' '.join(f'{k}={v[\"ms\"]:.4f}' for k,v in d.items()))"
+  if [ $rep = 1 ]; then HSK_LIB=$L timeout 300 python tools/sustain.py 2>&1 | grep reps; fi
+done
+done

@@ -150,6 +150,103 @@ def gen(rpt, db, trans, vote=None):
             f'                 : "memory");\n}}\n')
 
 
+def gen_tw(rpt, db, trans):
+    """S' walker of 64-row TMA tiles (REL_DOC): one-instruction bucket tests,
+    unrolled by two, entry words fetched in 8-byte pairs.
+
+    * The loop test of bucket jj is a LOP3 with a predicate output,
+          k = (E ^ jj << 24) & 0x7f000000,  q = k != 0,
+      instead of k = E & mask plus a compare.  k is the next word's bucket
+      relative to jj, so every bucket loop exits into its own chain, whose
+      links compare k with (b ^ jj) << 24 for b = jj + 1 .. DB - 1 and branch
+      into loop b on a match (the next bucket, the common case, first).
+    * Unrolled by two with the next-word register alternating between e0 and
+      e1: half A of loop jj holds the current entry at pe and the next word in
+      e0, half B the current entry at pe + 4 and the next word in e1; an exit
+      from A leaves the B state (its chain enters B halves), an exit from B the
+      A state.
+    * Group lists start at even words (plan kernel, Geom::even), so half A
+      (current entry at an even word) loads the next two words with one
+      ld.shared.v2 and half B loads none: one broadcast wavefront per two
+      entries.  The walk reads up to two words past its terminator.
+    Measured (same box, ms): C2 S' 0.611 -> 0.589, C1 S' 55.7 -> 53.4 us, C5
+    shard S' equal; on S the same walker is slower (C2 0.449 -> 0.454, C5
+    shard 8.7 -> 9.3: S is not bound by the word loads), so S keeps gen()."""
+    nacc = rpt * db
+    sh = log2(32 * rpt * 8)
+    L = []
+    a = L.append
+    sen, base = nacc, nacc + 1
+    lane8 = nacc + 2 if trans else None
+    sgs = nacc + (3 if trans else 2)
+    a(".reg .pred q, pz;")
+    a(".reg .b32 pe, t, ad, e, e0, e1, k, gh, zero, one;")
+    a(".reg .f64 " + ", ".join(f"u{r}" for r in range(rpt)) + ", g;")
+    a("mov.b32 zero, 0;")
+    a("mov.b32 one, 1072693248;")
+    a("setp.ne.u32 pz, zero, zero;")
+
+    def load_tile(e):
+        if trans:
+            out = [f"lop3.b32 ad, {e}, %{lane8}, 16777215, 0x28;", f"add.u32 ad, ad, %{base};"]
+            out += [f"ld.shared.f64 u{r}, [ad+{4096 * r}];" for r in range(rpt)]
+        else:
+            out = [f"shl.b32 t, {e}, {sh};", f"add.u32 ad, t, %{base};"]
+            out += [f"ld.shared.v2.f64 {{u{2 * h}, u{2 * h + 1}}}, [ad+{512 * h}];" for h in range(rpt // 2)]
+        out += [f"lop3.b32 gh, {e}, -2147483648, one, 0xEA;", "mov.b64 g, {zero, gh};"]
+        return out
+
+    def chain(jj, half):
+        rel = 0 if jj < 0 else jj
+        for b in range(jj + 1, db):
+            a(f"setp.eq.u32 q, k, {(b ^ rel) << 24};")
+            a("vote.sync.any.pred q, q, -1;")
+            a(f"@q bra.uni {half}{b};")
+        a("bra.uni DONE;")
+
+    def fma(jj):
+        for r in range(rpt):
+            acc = jj * rpt + r
+            a(f"fma.rn.f64 %{acc}, u{r}, g, %{acc};")
+
+    a(f"ld.shared.b32 t, [%{sgs}];")
+    a(f"mad.lo.u32 pe, t, 4, %{sen};")
+    a("ld.shared.v2.b32 {e, e0}, [pe];")
+    L.extend(load_tile("e"))
+    a("and.b32 k, e, 2130706432;")
+    chain(-1, "WA")
+    for jj in range(db):
+        a(f"WA{jj}:")
+        fma(jj)
+        L.extend(load_tile("e0"))
+        a(f"lop3.or.b32 k|q, e0, {jj << 24}, 2130706432, 0x28, pz;")
+        a("ld.shared.v2.b32 {e1, e0}, [pe+8];")
+        a("vote.sync.any.pred q, q, -1;")
+        a(f"@q bra.uni WX{jj};")
+        a(f"WB{jj}:")
+        fma(jj)
+        L.extend(load_tile("e1"))
+        a(f"lop3.or.b32 k|q, e1, {jj << 24}, 2130706432, 0x28, pz;")
+        a("add.u32 pe, pe, 8;")
+        a("vote.sync.any.pred q, !q, -1;")
+        a(f"@q bra.uni WA{jj};")
+        chain(jj, "WA")
+        a(f"WX{jj}:")
+        chain(jj, "WB")
+    a("DONE:")
+    txt = "\\n\\t".join(L)
+    outs = ", ".join(f'"+d"(acc[{k % rpt}][{k // rpt}])' for k in range(nacc))
+    ins = ['"r"(sen)', '"r"(base)'] + (['"r"(lanex)'] if trans else []) + ['"r"(sgs)']
+    name = f"pipe_{'t' if trans else 's'}_{rpt}x{db}"
+    sig = "uint32_t sen, uint32_t base, " + ("uint32_t lanex, " if trans else "")
+    return (f"__device__ __forceinline__ void {name}(double (&acc)[{rpt}][{db}], {sig}"
+            f"uint32_t sgs) {{\n"
+            f'    asm volatile("{{\\n\\t{txt}\\n\\t}}"\n'
+            f"                 : {outs}\n"
+            f"                 : {', '.join(ins)}\n"
+            f'                 : "memory");\n}}\n')
+
+
 def gen_pair(trans):
     """RPT = 2 rows per lane, 16 buckets = two chunks of 8 (see the docstring)."""
     rpt, nacc = 2, 20
@@ -337,7 +434,7 @@ def main():
     for rpt, db in S_CONFIGS:
         out.append(gen(rpt, db, False))
     for rpt, db in T_CONFIGS:
-        out.append(gen(rpt, db, True))
+        out.append(gen_tw(rpt, db, True) if rpt == 2 else gen(rpt, db, True))
     out.append(gen_pair(False))
     out.append(gen_pair_t())
     sys.stdout.write("\n".join(out))
