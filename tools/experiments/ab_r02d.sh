@@ -1,4 +1,4 @@
-# A/B of SJLT kernel builds on one box: bash tools/ab_r02d.sh <tag> <lib names...>
+# A/B of SJLT kernel builds on one box: bash tools/experiments/ab_r02d.sh <tag> <lib names...>
 # (libs under _exp/ab/libhsk_<name>.so; "new" = the in-tree build)
 tag=$1; shift
 mkdir -p gpurun_out

@@ -1,4 +1,4 @@
-# A/B of walker builds on one box: bash tools/ab_walk.sh <tag> <lib names...>
+# A/B of walker builds on one box: bash tools/experiments/ab_walk.sh <tag> <lib names...>
 # (libs under _exp/ab/libhsk_<name>.so; "new" = the in-tree build); parity of
 # the in-tree build first, then kbench and the 2000-launch sustain run per lib
 tag=$1; shift

@@ -3,7 +3,7 @@ copy, S' on A, and S on the kept A^T (the adaptive sketch's S' increments)."""
 import os, sys
 import numpy as np
 import torch
-sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__)))))
 from paper_2302_01977_b200 import device, matgen
 from paper_2302_01977_b200 import sketching as sk
 

@@ -2,7 +2,7 @@
 import os, sys, time
 import numpy as np
 import torch
-sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__)))))
 from paper_2302_01977_b200 import device, matgen
 from paper_2302_01977_b200 import sketching as sk
 

@@ -4,7 +4,7 @@ HSK_SJLT_W32 (16 / 20 / 24; unset = the default rule)."""
 import os, sys
 import numpy as np
 import torch
-sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__)))))
 from paper_2302_01977_b200 import device, matgen, _lib
 from paper_2302_01977_b200 import sketching as sk
 

@@ -1,5 +1,5 @@
 # TK / stages / L2-prefetch sweep of the SJLT kernels (one process per setting):
-#   CASES=c2s,c5shard bash tools/tk_sweep.sh <tag> "TK:STAGES:PF ..."
+#   CASES=c2s,c5shard bash tools/experiments/tk_sweep.sh <tag> "TK:STAGES:PF ..."
 tag=$1; shift
 mkdir -p gpurun_out
 for cfg in $1; do
