@@ -30,3 +30,14 @@ def test_reference_arm_other_ranks_exit_quietly():
                           "--gpus", "2", "--steps", "1"], capture_output=True, text=True,
                          timeout=300, env=env, cwd=ROOT)
     assert res.returncode == 0 and res.stdout.strip() == ""
+
+
+def test_committed_ncu_summary_feeds_roofline_traffic():
+    """bench.py's `roofline.traffic` is the headline kernel's per-launch DRAM
+    bytes from the committed ncu capture (profiles/ncu_summary.json): the key
+    must exist and sit near the algorithmic bytes (8 n^2 + 8 n d)."""
+    sys.path.insert(0, ROOT)
+    import bench
+    traffic = bench._traffic_from_profiles("sjlt_apply_S")
+    algorithmic = 8 * bench.N * bench.N + 8 * bench.N * bench.D
+    assert traffic is not None and 0.9 * algorithmic <= traffic <= 1.5 * algorithmic
