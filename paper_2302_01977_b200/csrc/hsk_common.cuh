@@ -34,7 +34,7 @@ int sm_count();
 // and A/B tools that change the environment in-process).  -1 = unset.
 struct Tuning {
     int sjlt_w32, sjlt_tk, sjlt_tk_t, sjlt_rpt, sjlt_rpt_t, sjlt_prod, sjlt_streamk, sjlt_mc,
-        sjlt_stages, sjlt_wait_ns, sjlt_dbg, sjlt_pf, sjlt_fused, gauss_splits;
+        sjlt_stages, sjlt_wait_ns, sjlt_dbg, sjlt_pf, sjlt_fused, sjlt_xp, sjlt_xp_gb, gauss_splits;
     char gauss_cfg[32];
 };
 const Tuning &tuning();

@@ -93,6 +93,8 @@ void tuning_load() {
     t.sjlt_dbg = env_int("HSK_SJLT_DBG");
     t.sjlt_pf = env_int("HSK_SJLT_PF");
     t.sjlt_fused = env_int("HSK_SJLT_FUSED");
+    t.sjlt_xp = env_int("HSK_SJLT_XP");
+    t.sjlt_xp_gb = env_int("HSK_SJLT_XP_GB");
     t.gauss_splits = env_int("HSK_GAUSS_SPLITS");
     const char *g = getenv("HSK_GAUSS_CFG");
     snprintf(t.gauss_cfg, sizeof(t.gauss_cfg), "%s", g ? g : "");

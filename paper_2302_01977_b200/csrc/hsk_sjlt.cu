@@ -60,6 +60,11 @@
 #define HSK_XPOSE_PRODUCERS 8
 #endif
 constexpr int kXposeProducers = HSK_XPOSE_PRODUCERS;
+// producer warps of the S' tiles transposed into the S layout (mode 5 / 6, below)
+#ifndef HSK_XP2_PRODUCERS
+#define HSK_XP2_PRODUCERS 4
+#endif
+constexpr int kXp2Producers = HSK_XP2_PRODUCERS;
 
 // TMA multicast across slab clusters (opt-in at build time and run time,
 // -DHSK_SJLT_MULTICAST=1 plus HSK_SJLT_MC=1): measured slower (see launch<>),
@@ -87,6 +92,8 @@ struct Geom {
     int pair;          // paired plan (block construction, d/alpha = 8): below
     int even;          // group lists start at even words (S' on 64-row tiles: the
                        // walker fetches entry words in 8-byte pairs)
+    int xp;            // S' on 64-row tiles transposed in shared memory into the S
+                       // layout and walked by the S walkers (xp_rule below)
     int rpt;           // rows per lane (tile rows tm = 32 * rpt)
     int db, nw;        // buckets per consumer warp, consumer warps per CTA
     int64_t ngroups;   // warp groups of db buckets (nslabs * nw)
@@ -188,11 +195,29 @@ static inline void warp_shape(int rpt, int d, int trans, int &db, int &nw) {
 // 16 (t1, t2) bucket combos per warp.
 constexpr int kPairSlab = 64;  // buckets per slab (4 chunk pairs)
 
+// S' tiles transposed in shared memory (modes 5 / 6).  In shared-memory passes
+// per staged element and slab CTA, with a = the element's entries in that slab:
+// a TMA-landed natural-layout tile costs 1 + 2a (its 8-byte column reads are
+// 2-way conflicted), a tile transposed into the S layout 3 + a (staging write,
+// the transposer's read and write, conflict-free 16-byte reads).  S' is bound
+// by that port, so the transposed tile wins from a = 4 on -- measured r02q,
+// n = 16384, S' ms natural / transposed: d = 128 alpha = 4 0.536 / 0.494,
+// d = 256 alpha = 8 1.062 / 0.757 (the 11 / 17 pass ratio); not the paired
+// plans (C3: 8.39 / 8.73 -- their walk is issue-bound and loses more to the
+// smaller chunk than the passes save) and not a <= 2 (C2, C5).
+// HSK_SJLT_XP = 0 / 1 forces the choice for every 64-row S' plan.
+static inline int xp_rule(int trans, int rpt, int a_per_slab, int pair) {
+    if (!trans || rpt != 2) return 0;
+    if (tuning().sjlt_xp >= 0) return tuning().sjlt_xp != 0;
+    return !pair && a_per_slab >= 4;
+}
+
 static Geom geom_dir(int64_t n, int d, int alpha, int trans, int64_t base, int pair = 0) {
     Geom g;
     int tk;
     g.pair = pair;
     g.even = 0;
+    g.xp = 0;
     if (pair) {
         constexpr int kStage3 = (226 * 1024 - 2048) / 3, kStage2 = (226 * 1024 - 2048) / 2;
         const int ae = alpha / 2;  // entries per input index
@@ -200,7 +225,10 @@ static Geom geom_dir(int64_t n, int d, int alpha, int trans, int64_t base, int p
         g.db = 16;
         g.nw = 16;
         g.ngroups = (int64_t)(d / kPairSlab) * g.nw;
-        tk = n >= 8192 ? tk_fit16(ae, 64, 256, kStage2, g.ngroups, g.nw)
+        g.xp = xp_rule(trans, g.rpt, ae, 1);
+        // (transposed S' tiles: two ring slots and the staging copy share the 226 KB)
+        tk = g.xp ? tk_fit16(ae, 64, 256, kStage3, g.ngroups, g.nw)
+           : n >= 8192 ? tk_fit16(ae, 64, 256, kStage2, g.ngroups, g.nw)
                        : tk_fit16(ae, 64, 128, kStage3, g.ngroups, g.nw);
         if (const int e = trans ? tuning().sjlt_tk_t : tuning().sjlt_tk; e > 0)
             tk = std::max(16, e / 16 * 16);
@@ -236,11 +264,14 @@ static Geom geom_dir(int64_t n, int d, int alpha, int trans, int64_t base, int p
         g.rpt = e;
     warp_shape(g.rpt, d, trans, g.db, g.nw);
     g.ngroups = roundup(d, (int64_t)g.db * g.nw) / g.db;
-    g.even = trans && g.rpt == 2;
+    g.xp = xp_rule(trans, g.rpt, alpha / (int)(g.ngroups / g.nw), 0);
+    g.even = trans && g.rpt == 2 && !g.xp;
     const int64_t gw = g.even ? 2 * g.ngroups + 1 : g.ngroups;
     if (d <= 64) {
         tk = wide && !trans ? tk_fit16(alpha, 128, 256, kStage2, gw, g.nw)
                             : tk_fit(alpha, 128, 128, kStage3, gw, g.nw);
+    } else if (g.xp) {
+        tk = tk_fit16(alpha, 64, 256, kStage3, gw, g.nw);
     } else {
         // (S on the 20 x 13 warps: TK 128 x 3 stages measured faster in bursts,
         // C2 0.439 vs 0.449 ms over 20 launches, but slower under the power cap,
@@ -536,6 +567,7 @@ struct ApplyArgs {
     int mc;
     int wait_ns;  // consumer full-barrier wait: try_wait suspend hint (ns)
     int pf;  // mode 0: chunks prefetched into L2 beyond the shared-memory ring
+    int nbox, gbox;  // mode 5: staging groups, boxes (16 input indices x TM rows) per group
     int64_t units;
     FastDiv div_slabs, div_ks;
     int32_t per;                   // whole-tile CTAs: chunks per k-split rank
@@ -634,7 +666,7 @@ __device__ __forceinline__ void issue_tma(const ApplyArgs &p, const CUtensorMap 
 }
 
 // cp.async producer of chunk j: threads [0, pnt) of the producer set
-template <int TM, bool TRANS, bool XPOSE, bool SK>
+template <int TM, bool TRANS, bool XPOSE, bool SK, bool XP2 = false>
 __device__ __forceinline__ void issue_coop(const ApplyArgs &p, const Ring &R, int j, int ptid, int pnt) {
     unsigned char *st = R.stage0 + (size_t)(j % R.stages) * p.stage_bytes;
     uint64_t *bar = &R.full[j % R.stages];
@@ -649,7 +681,21 @@ __device__ __forceinline__ void issue_coop(const ApplyArgs &p, const Ring &R, in
     }
     double *sx = reinterpret_cast<double *>(st);
     const int nel = p.tk * TM;
-    if (XPOSE) {
+    if (XP2) {
+        // mode 6 (unaligned A): (kk, rr) = A[k0+kk, r0+rr] -> sx[kk*TM + rr], the
+        // dense S layout; lanes along kk (coalesced reads; the strided writes
+        // conflict -- the rare odd-ld path)
+        const int tk = p.tk;
+        for (int kk = ptid; kk < tk; kk += pnt) {
+            const double *src = p.A + r0 * p.lda + k0 + kk;
+            double *dbase = sx + kk * TM;
+            const bool vk = kk < kc;
+            for (int rr = 0; rr < TM; ++rr, src += p.lda) {
+                const bool v = vk && (r0 + rr < p.m_out);
+                cp_async8(dbase + rr, v ? src : p.A, v);
+            }
+        }
+    } else if (XPOSE) {
         // (kk, rr) = A[k0+kk, r0+rr] -> sx[kk*TM + (rr ^ (kk%32))]; lanes
         // along kk: coalesced reads, conflict-free swizzled writes
         const int tk = p.tk;
@@ -713,15 +759,17 @@ __device__ __forceinline__ void ring_setup(const ApplyArgs &p, const CUtensorMap
         done[s] = 0;
     }
     mbar_init(R.empty + 7, ecount);  // sink of deferred releases (stages <= 7)
+    if (p.mode == 5)
+        for (int b = 0; b < p.nbox; ++b) mbar_init(R.full + 24 + b, 1);  // staging boxes
     fence_mbar_init();
-    if (p.mode == 0 || p.mode == 3 || p.mode == 4) prefetch_tmap(tmap);
+    if (p.mode == 0 || p.mode == 3 || p.mode == 4 || p.mode == 5) prefetch_tmap(tmap);
     if (p.mode == 4) mbar_init(R.full + 7, 1);  // staging buffer (stages <= 7 here)
 }
 
 // Dedicated producer warp(s): refill a slot as soon as every consumer warp
 // has released it (modes 0 / 3: one TMA-issuing lane; mode 4: TMA staging +
 // PW transposing warps; mode 1: PW warps of transposing cp.async copies).
-template <int TM, int PW, bool TRANS, bool XPOSE, bool SK>
+template <int TM, int PW, bool TRANS, bool XPOSE, bool SK, bool XP2 = false>
 __device__ __forceinline__ void producer_warps(const ApplyArgs &p, const CUtensorMap *tmap, const Ring R) {
     const int lane = threadIdx.x & 31;
     const int ptid = threadIdx.x - (blockDim.x - PW * 32);
@@ -732,6 +780,89 @@ __device__ __forceinline__ void producer_warps(const ApplyArgs &p, const CUtenso
             for (int j = 0; j < jn; ++j) {
                 if (j >= stages) mbar_wait(&R.empty[j % stages], (uint32_t)((j / stages) - 1) & 1u);
                 issue_tma<TM, TRANS, SK>(p, tmap, R, j);
+            }
+        }
+    } else if (XP2 && p.mode == 5) {
+        if constexpr (XP2) {
+            // S' tiles in the S layout (64-row tiles, aligned A).  One lane
+            // TMA-loads A's natural layout (boxes of 16 input indices x TM output
+            // rows, 128-byte swizzle) into a staging ring of p.nbox groups of
+            // p.gbox boxes that runs ahead of the slots: a group is refilled as
+            // soon as it has been read (its boxes issued back to back: gbox x
+            // 128 contiguous bytes per output row), so the loads in flight do
+            // not depend on the chunk size.  The PW warps copy group after group
+            // into the ring slot as [kk][row] with the rows contiguous, and the
+            // consumers run the S walkers (one conflict-free 16-byte load per
+            // entry).  Thread -> output row cc and index pairs q = ph + NPH i of
+            // a box: a quarter-warp's 16-byte loads hit eight different chunks
+            // of eight rows (conflict-free), a half-warp's 8-byte stores one
+            // 128-byte line.
+            constexpr int NPH = PW * 32 / TM;  // threads per output row
+            constexpr int NP = 8 / NPH;        // index pairs per thread and box
+            static_assert(PW * 32 % TM == 0 && 8 % NPH == 0, "xp2 transposer mapping");
+            constexpr int BOX = TM * 128;      // bytes per staging box
+            unsigned char *stg = R.stage0 + (size_t)stages * p.stage_bytes;  // 1024-aligned
+            uint64_t *grp_full = R.full + 24;  // p.nbox barriers (<= 16)
+            const int gb = p.gbox;             // boxes per group
+            const int gpc = p.tk / (16 * gb);  // groups per chunk
+            const int ngrp = p.nbox;
+            const int total = jn * gpc;        // groups of this CTA's chunks
+            // group g of the CTA's sequence -> chunk g / gpc, boxes (g % gpc) * gb ..
+            auto issue_group = [&](int g, int buf) {
+                const int j = g / gpc, q = g - j * gpc;
+                int64_t r0, c;
+                chunk_of<TM, SK>(p, R, j, r0, c);
+                mbar_arrive_expect_tx(&grp_full[buf], (uint32_t)(gb * BOX));
+                for (int i = 0; i < gb; ++i)
+                    tma_load_2d(stg + (size_t)(buf * gb + i) * BOX, tmap, (int)(c * p.tk + (q * gb + i) * 16),
+                                (int)r0, &grp_full[buf]);
+            };
+            if (ptid == 0)
+                for (int g = 0; g < ngrp && g < total; ++g) issue_group(g, g);
+            const int cc = ptid % TM, ph = ptid / TM;
+            uint32_t so[NP];
+#pragma unroll
+            for (int i = 0; i < NP; ++i) so[i] = (uint32_t)(cc * 128 + (((ph + NPH * i) ^ (cc & 7)) << 4));
+            int s = 0, buf = 0, g = 0;
+            uint32_t eph = 1u;  // parity of the slot's previous release (first round: none)
+            uint32_t bph = 0u;  // parity of the staging ring's current round
+            for (int j = 0; j < jn; ++j) {
+                unsigned char *st = R.stage0 + (size_t)s * p.stage_bytes;
+                if (j >= stages) mbar_wait(&R.empty[s], eph);
+                if (ptid == 0) {
+                    int64_t r0, c;
+                    chunk_of<TM, SK>(p, R, j, r0, c);
+                    mbar_arrive_expect_tx(&R.full[s], R.gs_bytes + R.en_bytes);
+                    bulk_g2s(st + p.gs_off, p.gptr + c * p.gstride + R.g0, R.gs_bytes, &R.full[s]);
+                    bulk_g2s(st + p.en_off, p.ent + c * p.estride, R.en_bytes, &R.full[s]);
+                }
+                double *dst = reinterpret_cast<double *>(st) + cc;
+                for (int q = 0; q < gpc; ++q, ++g) {
+                    mbar_wait(&grp_full[buf], bph);
+                    const unsigned char *src = stg + (size_t)buf * gb * BOX;
+#pragma unroll 2
+                    for (int b = 0; b < gb; ++b, src += BOX, dst += 16 * TM) {
+                        double2 v[NP];
+#pragma unroll
+                        for (int i = 0; i < NP; ++i) v[i] = *reinterpret_cast<const double2 *>(src + so[i]);
+#pragma unroll
+                        for (int i = 0; i < NP; ++i) {
+                            dst[(2 * (ph + NPH * i)) * TM] = v[i].x;
+                            dst[(2 * (ph + NPH * i) + 1) * TM] = v[i].y;
+                        }
+                    }
+                    asm volatile("bar.sync 2, %0;" ::"r"(PW * 32) : "memory");  // group read by every thread
+                    if (ptid == 0 && g + ngrp < total) issue_group(g + ngrp, buf);
+                    if (++buf == ngrp) {
+                        buf = 0;
+                        bph ^= 1u;
+                    }
+                }
+                mbar_arrive(&R.full[s]);  // this thread's stores of slot s are done
+                if (++s == stages) {
+                    s = 0;
+                    eph ^= 1u;
+                }
             }
         }
     } else if (XPOSE && p.mode == 4) {
@@ -780,7 +911,7 @@ __device__ __forceinline__ void producer_warps(const ApplyArgs &p, const CUtenso
     } else {
         for (int j = 0; j < jn; ++j) {
             if (j >= stages) mbar_wait(&R.empty[j % stages], (uint32_t)((j / stages) - 1) & 1u);
-            issue_coop<TM, TRANS, XPOSE, SK>(p, R, j, ptid, PW * 32);
+            issue_coop<TM, TRANS, XPOSE, SK, XP2>(p, R, j, ptid, PW * 32);
         }
     }
     __syncwarp();
@@ -810,17 +941,22 @@ __device__ __noinline__ void sk_post_flag(int *flag, int pub) {
 // producer warps (TMA issue, or transposing copies for 128-row S' tiles);
 // without them the consumers share the producer work (modes 1/2: every lane
 // issues its share of 8-byte cp.async for the chunk STAGES-1 ahead).
-template <int RPT, int DB, int NW, bool TRANS, bool PROD, bool SK, bool PAIR>
-__global__ void __launch_bounds__((NW + (PROD ? (TRANS && RPT == 4 ? kXposeProducers : 1) : 0)) * 32, 1)
+// XP2: S' whose tiles the producer warps transpose into the S layout (modes
+// 5 / 6): the producer side is S' (tensor map, chunk coordinates), the consumer
+// side -- walker, lane -> row mapping, epilogue -- is S's.
+template <int RPT, int DB, int NW, bool TRANS, bool PROD, bool SK, bool PAIR, bool XP2 = false>
+__global__ void __launch_bounds__((NW + (PROD ? (XP2 ? kXp2Producers : TRANS && RPT == 4 ? kXposeProducers : 1) : 0)) * 32, 1)
     sjlt_apply_kernel(const __grid_constant__ ApplyArgs p, const __grid_constant__ CUtensorMap tmap) {
+    static_assert(!XP2 || (TRANS && PROD && RPT == 2), "xp2 kernels: S' on 64-row tiles with producer warps");
     constexpr int TM = 32 * RPT;
     constexpr int SLAB = PAIR ? kPairSlab : NW * DB;
-    constexpr bool XPOSE = TRANS && RPT == 4;       // transposed S' tile layout
+    constexpr bool XPOSE = TRANS && RPT == 4 && !XP2;  // transposed S' tile layout (128-row tiles)
+    constexpr bool CT = TRANS && !XP2;                 // consumers read an S' tile layout
     // (paired plans: warp (p, h) = 4p + h holds t1 buckets 16p + 2h + {0, 1}
     // in acc[.][0..1] and, once the quarters are folded into h = 0, the t2
     // buckets 16p + 8 + c2 in acc[.][2 + c2]; partials published / reduced
     // across CTAs keep the per-warp layout of the unpaired kernels)
-    constexpr int PW = PROD ? (XPOSE ? kXposeProducers : 1) : 0;  // dedicated producer warps
+    constexpr int PW = PROD ? (XP2 ? kXp2Producers : XPOSE ? kXposeProducers : 1) : 0;  // dedicated producer warps
     constexpr int NT = NW * 32;
     constexpr int NJ = PAIR ? 10 : DB;  // accumulator columns in use
     // slot release: lane 0 of each consumer warp arrives (PROD: inline; the
@@ -831,9 +967,9 @@ __global__ void __launch_bounds__((NW + (PROD ? (TRANS && RPT == 4 ? kXposeProdu
     R.full = reinterpret_cast<uint64_t *>(smem);
     R.empty = R.full + 8;
     unsigned *done = reinterpret_cast<unsigned *>(R.full + 16);
-    // stage ring from the first 1024-byte boundary past the 256-byte header
+    // stage ring from the first 1024-byte boundary past the 512-byte header
     // (the S' tile layout relies on the TMA 128-byte swizzle pattern)
-    R.stage0 = smem + ((((smem_u32(smem) + 256u + 1023u) & ~1023u)) - smem_u32(smem));
+    R.stage0 = smem + ((((smem_u32(smem) + 512u + 1023u) & ~1023u)) - smem_u32(smem));
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int ks = p.ksplit;
@@ -911,7 +1047,7 @@ __global__ void __launch_bounds__((NW + (PROD ? (TRANS && RPT == 4 ? kXposeProdu
     if constexpr (PROD) {
         // (role test on a broadcast warp index: warp-uniform to ptxas)
         if (__shfl_sync(0xffffffffu, warp, 0) >= NW) {
-            producer_warps<TM, PW, TRANS, XPOSE, SK>(p, &tmap, R);
+            producer_warps<TM, PW, TRANS, XPOSE, SK, XP2>(p, &tmap, R);
             return;
         }
     }
@@ -936,7 +1072,7 @@ __global__ void __launch_bounds__((NW + (PROD ? (TRANS && RPT == 4 ? kXposeProdu
     // S' swizzle term of rows l + 32 r (TMA layout: 16-byte chunk; transposed: 8 bytes)
     const uint32_t lanex = XPOSE ? lane * 8u : (uint32_t)(lane & 7) << 4;
     // S: rows 2l, 2l+1 (+64) / l;  S': row l (TMA layout: 128 bytes per row)
-    const uint32_t lane_off = XPOSE ? 0u : TRANS ? lane * 128u : lane * 8u * (RPT == 1 ? 1u : 2u);
+    const uint32_t lane_off = XPOSE ? 0u : CT ? lane * 128u : lane * 8u * (RPT == 1 ? 1u : 2u);
 
     // Epilogue: one store per accumulator, every one executed: to S scaled
     // once (the reference's `out *= scale`) -- rows past m_out and buckets
@@ -953,7 +1089,7 @@ __global__ void __launch_bounds__((NW + (PROD ? (TRANS && RPT == 4 ? kXposeProdu
 #pragma unroll
             for (int r = 0; r < RPT; ++r) {
                 int64_t row;
-                if (TRANS) row = r0 + lane + 32 * r;             // lane owns rows lane + 32 r
+                if (CT) row = r0 + lane + 32 * r;                // lane owns rows lane + 32 r
                 else if (RPT == 1) row = r0 + lane;
                 else row = r0 + 64 * (r >> 1) + 2 * lane + (r & 1);  // rows 2l, 2l+1 (+64)
                 double *dst = pub ? pubw + ((warp * DB + jj) * RPT + r) * 32 + lane
@@ -1027,7 +1163,7 @@ __global__ void __launch_bounds__((NW + (PROD ? (TRANS && RPT == 4 ? kXposeProdu
                 for (; !bad && q < b1 && ((en[q] >> 24) & 127u) != (uint32_t)DB; ++q)
                     bad = ((en[q] >> 24) & 127u) > (uint32_t)DB ||
                           (q > b0 && ((en[q] >> 24) & 127u) < ((en[q - 1] >> 24) & 127u));
-                bad = bad || q >= b1 || (TRANS && RPT == 2 && !PAIR && (b0 & 1u));
+                bad = bad || q >= b1 || (CT && RPT == 2 && !PAIR && (b0 & 1u));
                 if (bad) {
                     printf("sjlt dbg: cta %d warp %d chunk-iter %d bad list [%u, %u) estride %d\n",
                            (int)blockIdx.x, warp, ic, b0, b1, (int)p.estride);
@@ -1036,11 +1172,11 @@ __global__ void __launch_bounds__((NW + (PROD ? (TRANS && RPT == 4 ? kXposeProdu
             }
 #endif
             if (DBG_IS(1)) {
-            } else if constexpr (PAIR && TRANS) {
+            } else if constexpr (PAIR && CT) {
                 pipe_t_pair(acc, sen, sx, lanex, sbw);
             } else if constexpr (PAIR) {
                 pipe_s_pair(acc, sen, sx, sbw);
-            } else if constexpr (TRANS) {
+            } else if constexpr (CT) {
                 if constexpr (RPT == 1 && DB == 16) pipe_t_1x16(acc, sen, sx, lanex, sbw);
                 else if constexpr (RPT == 1 && DB == 32) pipe_t_1x32(acc, sen, sx, lanex, sbw);
                 else if constexpr (RPT == 2 && DB == 4) pipe_t_2x4(acc, sen, sx, lanex, sbw);
@@ -1185,7 +1321,12 @@ static int launch(ApplyArgs a, const Geom &g, cudaStream_t st) {
     // 3: TMA S' tile (16 x TM boxes, 128-byte swizzle)
     constexpr bool XPOSE = RPT == 4;  // (for S') transposed tile, cp.async producer
     // 4: TMA S' staging + in-smem transpose into the transposed 128-row tile
-    a.mode = a.trans ? (aligned && a.tk % 16 == 0 ? (XPOSE ? 4 : 3) : 1) : (aligned ? 0 : 2);
+    // 5: TMA S' staging + in-smem copy into the S layout (64-row tiles, plans
+    // with g.xp); 6: the same tile written by 8-byte cp.async (unaligned A)
+    constexpr bool XP2_OK = RPT == 2 && NW == 16 && !SONLY;  // the shapes with xp2 kernels
+    const bool xp = a.trans && g.xp;
+    if (xp && !XP2_OK) return set_error(HSK_EINVAL, "sjlt apply: no transposed-tile S' kernel for rpt=%d db=%d nw=%d", RPT, DB, NW);
+    a.mode = a.trans ? (aligned && a.tk % 16 == 0 ? (xp ? 5 : XPOSE ? 4 : 3) : (xp ? 6 : 1)) : (aligned ? 0 : 2);
     a.log2tk = 0;
     while ((1 << a.log2tk) < a.tk) ++a.log2tk;
     // S' tiles occupy whole 16-index blocks (the layout's unit); ring slots
@@ -1215,8 +1356,8 @@ static int launch(ApplyArgs a, const Geom &g, cudaStream_t st) {
     // from the last consumer warp to release a slot instead
     bool prod = NW < 32;
     if (tuning().sjlt_prod >= 0) prod = tuning().sjlt_prod == 1;
-    const int pw = a.trans && XPOSE ? kXposeProducers : 1;
-    prod = prod && (a.mode == 0 || a.mode == 3 || ((a.mode == 1 || a.mode == 4) && XPOSE)) &&
+    const int pw = xp ? kXp2Producers : a.trans && XPOSE ? kXposeProducers : 1;
+    prod = (xp || prod) && (a.mode == 0 || a.mode == 3 || ((a.mode == 1 || a.mode == 4) && XPOSE) || xp) &&
            NW + pw <= 32;
     if (a.mode == 4 && !prod) a.mode = 1;  // the staging transpose needs the producer warps
     // persistent balanced schedule (stream-K) when whole-tile CTAs would
@@ -1255,15 +1396,31 @@ static int launch(ApplyArgs a, const Geom &g, cudaStream_t st) {
         int rc = make_tmap_f64_2d(&tmap, a.A, (uint64_t)a.m_out, (uint64_t)a.n, (uint64_t)a.lda,
                                   TM, (uint32_t)(a.tk / a.mc));
         if (rc) return rc;
-    } else if (a.mode == 3 || a.mode == 4) {  // A is n x m_out: inner dimension = input index
+    } else if (a.mode == 3 || a.mode == 4 || a.mode == 5) {  // A is n x m_out: inner dimension = input index
         int rc = make_tmap_f64_2d(&tmap, a.A, (uint64_t)a.n, (uint64_t)a.m_out, (uint64_t)a.lda,
                                   16, TM, true);
         if (rc) return rc;
     }
     const int nthreads = (NW + (prod ? pw : 0)) * 32;
     const int budget = 226 * 1024;
-    const int stg_bytes = a.mode == 4 ? a_bytes : 0;  // mode 4 staging buffer
-    const int stages_max = std::max(2, std::min(7, (budget - 2048 - stg_bytes) / a.stage_bytes));
+    // staging of the transposing producers: mode 4 one tile; mode 5 two ring
+    // slots and every 16-index box that fits beside them (2..16)
+    int stg_bytes = a.mode == 4 ? a_bytes : 0;
+    int stages_max = std::max(2, std::min(7, (budget - 2048 - stg_bytes) / a.stage_bytes));
+    a.nbox = a.gbox = 0;
+    if (a.mode == 5) {
+        stages_max = 2;
+        // groups of gbox boxes (default 4: 512 contiguous bytes per output row
+        // and TMA issue; the largest divisor of the chunk's boxes not above it)
+        const int nb = a.tk / 16;
+        int gb = tuning().sjlt_xp_gb > 0 ? tuning().sjlt_xp_gb : 4;
+        gb = std::max(1, std::min(gb, nb));
+        while (nb % gb) --gb;
+        a.gbox = gb;
+        a.nbox = std::min(16, (budget - 2048 - 2 * a.stage_bytes) / (gb * TM * 128));
+        HSK_REQUIRE(a.nbox >= 1, HSK_EINVAL, "sjlt: no room for the S' staging groups (TK %d)", a.tk);
+        stg_bytes = a.nbox * gb * TM * 128;
+    }
     if (a.streamk && a.mc > 1) {
         // every group is one cluster and groups wait on later groups: keep
         // the grid to the clusters that can be co-resident
@@ -1339,6 +1496,10 @@ static int launch(ApplyArgs a, const Geom &g, cudaStream_t st) {
                                      : sjlt_apply_kernel<RPT, DB, NW, true, true, false, PAIR>)
                         : (a.streamk ? sjlt_apply_kernel<RPT, DB, NW, true, false, true, PAIR>
                                      : sjlt_apply_kernel<RPT, DB, NW, true, false, false, PAIR>);
+    if constexpr (XP2_OK)
+        if (xp)
+            kern = a.streamk ? sjlt_apply_kernel<RPT, DB, NW, true, true, true, PAIR, true>
+                             : sjlt_apply_kernel<RPT, DB, NW, true, true, false, PAIR, true>;
     // L2 prefetch beyond the ring: off -- the duplicate requests cost power,
     // and sustained runs are power-capped (C2, 2000 launches: 0.505 ms
     // without, 0.540 ms with; no burst gain either).  HSK_SJLT_PF=<chunks>.
@@ -1429,7 +1590,7 @@ extern "C" int hsk_sjlt_plan_build_ex(const int32_t *pos, const int8_t *sgn, int
             while (p2 < g->tk * (g->pair ? alpha / 2 : alpha)) p2 <<= 1;
             sjlt::sjlt_plan_kernel<<<(unsigned)g->nchunks, 256, 2 * p2 * sizeof(uint32_t), st>>>(
                 pos, sgn, n, d, alpha, g->tk, p2, g->db, g->ngroups, g->gstride, g->estride,
-                g == &pl.t ? (g->rpt == 4 ? -g->tm : g->tm) : 0, g->pair, g->even,
+                g == &pl.t && !g->xp ? (g->rpt == 4 ? -g->tm : g->tm) : 0, g->pair, g->even,
                 reinterpret_cast<uint32_t *>(base + g->gptr_off),
                 reinterpret_cast<uint32_t *>(base + g->ent_off), reinterpret_cast<int *>(base + 28));
             HSK_CHECK_LAUNCH("sjlt_plan_kernel");

@@ -158,6 +158,39 @@ def test_sjlt_warp_shapes_vs_oracle(cuda, tune, ws):
                np.linalg.norm(B))
 
 
+@pytest.mark.parametrize("m,n,d,alpha", [
+    (5000, 3000, 128, 4),      # single slab, a = 4: transposed tile by default
+    (7000, 2000, 256, 8),      # a = 8
+    (6000, 1500, 64, 8),       # paired plan (default: natural layout)
+    (9000, 1100, 512, 4),      # two slabs, a = 2 (default: natural layout)
+    (300, 9000, 200, 5),       # few row tiles, long rows: k-split clusters
+])
+def test_sjlt_transposed_tile_paths_vs_oracle(cuda, tune, m, n, d, alpha):
+    """S' on 64-row tiles, both tile layouts (HSK_SJLT_XP = 0: the TMA-landed
+    natural layout, modes 3 / 1; = 1: transposed in shared memory into the S
+    layout, modes 5 / 6) under both schedules, for aligned (TMA) and odd-ld
+    (cp.async) operands; every variant is bitwise repeatable."""
+    rng = np.random.default_rng(m + d)
+    B = rng.standard_normal((n, m))
+    ref_t = None
+    for xp in ("0", "1"):
+        tune("HSK_SJLT_XP", xp)
+        # a fresh operator per setting: the device plan is cached per block
+        op = sk.new_operator(sk.SJLT, n, d, seed=(m, d), alpha=alpha, construction=sk.BLOCK)
+        b = op.blocks[0]
+        if ref_t is None:
+            ref_t = O.sjlt_right_t(B, b._pos, b._signs, d, b._scale)
+        for ld in (n + (n & 1), n + 1 - (n & 1)):       # even (TMA) / odd (cp.async)
+            dB = device.DeviceMatrix(n, m, ld=ld)
+            dB.upload(B)
+            for mode in ("0", "1"):
+                tune("HSK_SJLT_STREAMK", mode)
+                t1 = sk.apply_right_transposed_device(dB, op).to_host()
+                t2 = sk.apply_right_transposed_device(dB, op).to_host()
+                _close(t1, ref_t, np.linalg.norm(B))
+                np.testing.assert_array_equal(t1, t2)
+
+
 def test_odd_leading_dimension_and_column_offset(cuda):
     rng = np.random.default_rng(5)
     m, n, d = 77, 333, 96

@@ -86,6 +86,18 @@ def main():
                 byt = n * n * 8 + n * d * 8
                 out[f"{c}_{'St' if tr else 'S'}"] = {"ms": ms, "GBs": byt / ms / 1e6,
                                                      "frac": byt / ms / 1e6 / PEAK}
+        elif c.startswith("sj-"):  # sj-<n>-<d>-<alpha>: square Gaussian-kernel A, block construction
+            n, d, a = (int(x) for x in c.split("-")[1:4])
+            A = mat(n)
+            op = sk.new_operator(sk.SJLT, n, d, np.random.SeedSequence((0, 0)), alpha=a,
+                                 construction="block")
+            blk = op.blocks[0]
+            S = device.DeviceMatrix.empty(n, d)
+            for tr in (False, True):
+                ms = timeit(lambda: device.apply_block(blk, A, tr, S, 0), args.reps)
+                byt = n * n * 8 + n * d * 8
+                out[f"{c}_{'St' if tr else 'S'}"] = {"ms": ms, "GBs": byt / ms / 1e6,
+                                                     "frac": byt / ms / 1e6 / PEAK}
         elif c in ("c5shard", "c5shard_t"):
             # BASELINE configs[4] at 8 GPUs: the 16384 x 131072 row shard of the
             # n = 131072 kernel matrix; S = A_g R^T (d = 2048, alpha = 8) and the
