@@ -205,11 +205,16 @@ constexpr int kPairSlab = 64;  // buckets per slab (4 chunk pairs)
 // d = 256 alpha = 8 1.062 / 0.757 (the 11 / 17 pass ratio); not the paired
 // plans (C3: 8.39 / 8.73 -- their walk is issue-bound and loses more to the
 // smaller chunk than the passes save) and not a <= 2 (C2, C5).
-// HSK_SJLT_XP = 0 / 1 forces the choice for every 64-row S' plan.
+// 128-row tiles (d <= 64) always: their earlier producers (mode 4: one staging
+// tile, the transposed XOR layout read with 8-byte loads) measured 7-14 %
+// slower (n = 16384, S' ms: d = 64 alpha = 4 0.558 / 0.515, alpha = 2
+// 0.499 / 0.429, d = 32 alpha = 4 0.571 / 0.497; n = 65536 d = 64 alpha = 4
+// 8.09 / 7.48); mode 4 / 1 stay for HSK_SJLT_XP = 0.
+// HSK_SJLT_XP = 0 / 1 forces the choice for every S' plan.
 static inline int xp_rule(int trans, int rpt, int a_per_slab, int pair) {
-    if (!trans || rpt != 2) return 0;
+    if (!trans || (rpt != 2 && rpt != 4)) return 0;
     if (tuning().sjlt_xp >= 0) return tuning().sjlt_xp != 0;
-    return !pair && a_per_slab >= 4;
+    return rpt == 4 || (!pair && a_per_slab >= 4);
 }
 
 static Geom geom_dir(int64_t n, int d, int alpha, int trans, int64_t base, int pair = 0) {
@@ -947,7 +952,7 @@ __device__ __noinline__ void sk_post_flag(int *flag, int pub) {
 template <int RPT, int DB, int NW, bool TRANS, bool PROD, bool SK, bool PAIR, bool XP2 = false>
 __global__ void __launch_bounds__((NW + (PROD ? (XP2 ? kXp2Producers : TRANS && RPT == 4 ? kXposeProducers : 1) : 0)) * 32, 1)
     sjlt_apply_kernel(const __grid_constant__ ApplyArgs p, const __grid_constant__ CUtensorMap tmap) {
-    static_assert(!XP2 || (TRANS && PROD && RPT == 2), "xp2 kernels: S' on 64-row tiles with producer warps");
+    static_assert(!XP2 || (TRANS && PROD && (RPT == 2 || RPT == 4)), "xp2 kernels: S' on 64- / 128-row tiles with producer warps");
     constexpr int TM = 32 * RPT;
     constexpr int SLAB = PAIR ? kPairSlab : NW * DB;
     constexpr bool XPOSE = TRANS && RPT == 4 && !XP2;  // transposed S' tile layout (128-row tiles)
@@ -1323,7 +1328,7 @@ static int launch(ApplyArgs a, const Geom &g, cudaStream_t st) {
     // 4: TMA S' staging + in-smem transpose into the transposed 128-row tile
     // 5: TMA S' staging + in-smem copy into the S layout (64-row tiles, plans
     // with g.xp); 6: the same tile written by 8-byte cp.async (unaligned A)
-    constexpr bool XP2_OK = RPT == 2 && NW == 16 && !SONLY;  // the shapes with xp2 kernels
+    constexpr bool XP2_OK = (RPT == 2 || RPT == 4) && NW == 16 && !SONLY;  // the shapes with xp2 kernels
     const bool xp = a.trans && g.xp;
     if (xp && !XP2_OK) return set_error(HSK_EINVAL, "sjlt apply: no transposed-tile S' kernel for rpt=%d db=%d nw=%d", RPT, DB, NW);
     a.mode = a.trans ? (aligned && a.tk % 16 == 0 ? (xp ? 5 : XPOSE ? 4 : 3) : (xp ? 6 : 1)) : (aligned ? 0 : 2);
@@ -1410,10 +1415,11 @@ static int launch(ApplyArgs a, const Geom &g, cudaStream_t st) {
     a.nbox = a.gbox = 0;
     if (a.mode == 5) {
         stages_max = 2;
-        // groups of gbox boxes (default 4: 512 contiguous bytes per output row
-        // and TMA issue; the largest divisor of the chunk's boxes not above it)
+        // groups of gbox boxes (default 32 KB: 4 boxes of 64 rows, 512 contiguous
+        // bytes per output row and TMA issue; the largest divisor of the chunk's
+        // boxes not above it)
         const int nb = a.tk / 16;
-        int gb = tuning().sjlt_xp_gb > 0 ? tuning().sjlt_xp_gb : 4;
+        int gb = tuning().sjlt_xp_gb > 0 ? tuning().sjlt_xp_gb : 32768 / (TM * 128);
         gb = std::max(1, std::min(gb, nb));
         while (nb % gb) --gb;
         a.gbox = gb;

@@ -164,11 +164,14 @@ def test_sjlt_warp_shapes_vs_oracle(cuda, tune, ws):
     (6000, 1500, 64, 8),       # paired plan (default: natural layout)
     (9000, 1100, 512, 4),      # two slabs, a = 2 (default: natural layout)
     (300, 9000, 200, 5),       # few row tiles, long rows: k-split clusters
+    (8000, 1500, 64, 4),       # 128-row tiles (d <= 64): transposed tile by default
+    (4100, 2000, 32, 2),
 ])
 def test_sjlt_transposed_tile_paths_vs_oracle(cuda, tune, m, n, d, alpha):
-    """S' on 64-row tiles, both tile layouts (HSK_SJLT_XP = 0: the TMA-landed
-    natural layout, modes 3 / 1; = 1: transposed in shared memory into the S
-    layout, modes 5 / 6) under both schedules, for aligned (TMA) and odd-ld
+    """S' tiles in both layouts (HSK_SJLT_XP = 0: the TMA-landed natural layout
+    of 64-row tiles, modes 3 / 1, and the XOR-transposed 128-row tiles, modes
+    4 / 1; = 1: transposed in shared memory into the S layout, modes 5 / 6)
+    under both schedules, for aligned (TMA) and odd-ld
     (cp.async) operands; every variant is bitwise repeatable."""
     rng = np.random.default_rng(m + d)
     B = rng.standard_normal((n, m))
