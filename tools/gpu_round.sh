@@ -10,7 +10,7 @@ timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --lo
   python bench.py --steps 20 --warmup 5 --no-cpu > gpurun_out/ncu_l_$tag.log 2>&1; echo ncu_list=$?
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:sjlt_apply -s 5 -c 1 \
   -o gpurun_out/prof_bench_sjlt_$tag -f python bench.py --steps 2 --warmup 5 --no-configs --no-cpu > gpurun_out/ncu_f_$tag.log 2>&1; echo ncu_bench=$?
-for c in c5shard_S c5shard_St c2s_St; do
+for c in c5shard_S c5shard_St c2s_St xp8_St xp4_St c3a4_St; do
   timeout 600 ncu --set full --clock-control none --import-source on -k regex:sjlt_apply -s 1 -c 1 \
     -o gpurun_out/prof_${c}_$tag -f python tools/prof_once.py $c > gpurun_out/ncu_${c}_$tag.log 2>&1; echo ncu_$c=$?
 done

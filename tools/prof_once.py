@@ -17,6 +17,10 @@ CASES = {
     "c2g": ("gaussian", 16384, 512, None, None, "gauss"),
     "c3": ("sjlt", 65536, 64, 8, "block", "toep"),
     "c4": ("srht", 65536, 512, None, None, "gauss4"),
+    # S' on tiles transposed in shared memory (modes 5): a = 8 / a = 4 entries per element and slab
+    "xp8": ("sjlt", 16384, 256, 8, "block", "gauss"),
+    "xp4": ("sjlt", 16384, 128, 4, "block", "gauss"),
+    "c3a4": ("sjlt", 65536, 64, 4, "block", "toep"),
 }
 
 
