@@ -1409,7 +1409,7 @@ static int launch(ApplyArgs a, const Geom &g, cudaStream_t st) {
     const int nthreads = (NW + (prod ? pw : 0)) * 32;
     const int budget = 226 * 1024;
     // staging of the transposing producers: mode 4 one tile; mode 5 two ring
-    // slots and every 16-index box that fits beside them (2..16)
+    // slots and as many staging groups as fit beside them (<= 16)
     int stg_bytes = a.mode == 4 ? a_bytes : 0;
     int stages_max = std::max(2, std::min(7, (budget - 2048 - stg_bytes) / a.stage_bytes));
     a.nbox = a.gbox = 0;
