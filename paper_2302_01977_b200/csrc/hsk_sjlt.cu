@@ -1414,7 +1414,8 @@ static int launch(ApplyArgs a, const Geom &g, cudaStream_t st) {
     int stages_max = std::max(2, std::min(7, (budget - 2048 - stg_bytes) / a.stage_bytes));
     a.nbox = a.gbox = 0;
     if (a.mode == 5) {
-        stages_max = 2;
+        // two slots (HSK_SJLT_STAGES asks for more: they must leave room for a group)
+        stages_max = std::max(2, std::min(tuning().sjlt_stages, (budget - 2048 - 32768) / a.stage_bytes));
         // groups of gbox boxes (default 32 KB: 4 boxes of 64 rows, 512 contiguous
         // bytes per output row and TMA issue; the largest divisor of the chunk's
         // boxes not above it)
@@ -1423,7 +1424,7 @@ static int launch(ApplyArgs a, const Geom &g, cudaStream_t st) {
         gb = std::max(1, std::min(gb, nb));
         while (nb % gb) --gb;
         a.gbox = gb;
-        a.nbox = std::min(16, (budget - 2048 - 2 * a.stage_bytes) / (gb * TM * 128));
+        a.nbox = std::min(16, (budget - 2048 - stages_max * a.stage_bytes) / (gb * TM * 128));
         HSK_REQUIRE(a.nbox >= 1, HSK_EINVAL, "sjlt: no room for the S' staging groups (TK %d)", a.tk);
         stg_bytes = a.nbox * gb * TM * 128;
     }
