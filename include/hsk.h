@@ -61,6 +61,12 @@ HSK_API int hsk_abi_version(void);
  * counterpart. */
 HSK_API int hsk_tuning_reload(void);
 
+/* Number of hsk_tuning_reload() calls so far.  An SJLT plan's geometry (chunk
+ * size, tile layout) depends on the knobs, so a plan must be applied under the
+ * knobs it was built with: callers that cache plans rebuild them when this
+ * changes (device.block_state does).  No reference counterpart. */
+HSK_API int hsk_tuning_generation(void);
+
 /* Copies the calling thread's last error message into buf (NUL-terminated);
  * returns its full length. */
 HSK_API int hsk_last_error(char *buf, size_t len);

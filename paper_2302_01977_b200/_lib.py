@@ -26,6 +26,7 @@ _c_p = ctypes.c_void_p
 SIGNATURES = {
     "hsk_abi_version": (ctypes.c_int, []),
     "hsk_tuning_reload": (ctypes.c_int, []),
+    "hsk_tuning_generation": (ctypes.c_int, []),
     "hsk_last_error": (ctypes.c_int, [ctypes.c_char_p, ctypes.c_size_t]),
     "hsk_device_info": (ctypes.c_int, [ctypes.POINTER(ctypes.c_int), ctypes.POINTER(ctypes.c_int),
                                        ctypes.POINTER(ctypes.c_int), ctypes.POINTER(_c_i64)]),

@@ -71,6 +71,7 @@ int sm_count() {
 namespace {
 Tuning g_tuning;
 std::atomic<int> g_tuning_ready{0};
+std::atomic<int> g_tuning_gen{0};
 std::mutex g_tuning_mu;
 
 int env_int(const char *name) {
@@ -210,8 +211,11 @@ extern "C" int hsk_tuning_reload(void) {
     std::lock_guard<std::mutex> lk(g_tuning_mu);
     tuning_load();
     g_tuning_ready.store(1, std::memory_order_release);
+    g_tuning_gen.fetch_add(1, std::memory_order_relaxed);
     return HSK_OK;
 }
+
+extern "C" int hsk_tuning_generation(void) { return g_tuning_gen.load(std::memory_order_relaxed); }
 
 extern "C" int hsk_last_error(char *buf, size_t len) {
     const int n = (int)strlen(g_err);

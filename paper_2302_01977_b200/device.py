@@ -180,7 +180,7 @@ class RawMatrix:
 # --------------------------------------------------------------- R on device
 
 class _SjltState:
-    __slots__ = ("pos", "sgn", "plan", "n", "d", "alpha", "scale", "flags")
+    __slots__ = ("pos", "sgn", "plan", "n", "d", "alpha", "scale", "flags", "gen")
 
 
 HSK_SJLT_CHUNKED = 1  # include/hsk.h
@@ -224,7 +224,9 @@ def block_state(block):
     cache = block.__dict__.setdefault(_STATE_ATTR, {})
     key = _device_key()
     st = cache.get(key)
-    if st is not None:
+    # an SJLT plan is tied to the tuning knobs it was built under
+    gen = _lib.load().hsk_tuning_generation() if block.kind == "sjlt" else 0
+    if st is not None and getattr(st, "gen", 0) == gen:
         return st
     kind = block.kind
     dev = torch.device("cuda", key)
@@ -244,6 +246,7 @@ def block_state(block):
         st.scale = float(block._scale)
         chunked = sjlt_chunked(pos, d, alpha, getattr(block, "construction", None))
         st.flags = HSK_SJLT_CHUNKED if chunked else 0
+        st.gen = gen
         nbytes = _lib.load().hsk_sjlt_plan_bytes_ex(n, d, alpha, st.flags)
         _lib.check(nbytes, "hsk_sjlt_plan_bytes_ex")
         st.plan = torch.empty(int(nbytes), dtype=torch.uint8, device=dev)

@@ -175,14 +175,13 @@ def test_sjlt_transposed_tile_paths_vs_oracle(cuda, tune, m, n, d, alpha):
     (cp.async) operands; every variant is bitwise repeatable."""
     rng = np.random.default_rng(m + d)
     B = rng.standard_normal((n, m))
-    ref_t = None
+    # one operator for both settings: its cached device plan is rebuilt when the
+    # knobs change (hsk_tuning_generation, device.block_state)
+    op = sk.new_operator(sk.SJLT, n, d, seed=(m, d), alpha=alpha, construction=sk.BLOCK)
+    b = op.blocks[0]
+    ref_t = O.sjlt_right_t(B, b._pos, b._signs, d, b._scale)
     for xp in ("0", "1"):
         tune("HSK_SJLT_XP", xp)
-        # a fresh operator per setting: the device plan is cached per block
-        op = sk.new_operator(sk.SJLT, n, d, seed=(m, d), alpha=alpha, construction=sk.BLOCK)
-        b = op.blocks[0]
-        if ref_t is None:
-            ref_t = O.sjlt_right_t(B, b._pos, b._signs, d, b._scale)
         for ld in (n + (n & 1), n + 1 - (n & 1)):       # even (TMA) / odd (cp.async)
             dB = device.DeviceMatrix(n, m, ld=ld)
             dB.upload(B)
