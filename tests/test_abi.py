@@ -108,3 +108,39 @@ def test_chunked_flag_host_rule():
     assert not device.sjlt_chunked(bad, 64, 8, "graph")
     b2 = operators.new_operator("sjlt", 600, 512, seed=1, alpha=4, construction="block").blocks[0]
     assert not device.sjlt_chunked(np.asarray(b2._pos), 512, 4, "block")  # not a paired shape
+
+
+def test_plan_geometry_sweep_host_only():
+    """hsk_sjlt_plan_bytes_ex walks the chunk / tile-layout rules (geom_dir,
+    xp_rule, the TK fits) on the host: over a sweep of operator shapes --
+    including huge alpha, one-bucket operators and every HSK_SJLT_XP setting --
+    it returns a size that holds both directions' entry words and never less
+    than one 4-byte word per entry, and the tuning generation counts reloads."""
+    import os
+    lib = _lib.load()
+    gen0 = lib.hsk_tuning_generation()
+    shapes = [(n, d, a) for n in (1, 17, 4096, 8192, 70000)
+              for d in (1, 2, 64, 65, 128, 129, 256, 257, 384, 512, 513, 2048, 4096)
+              for a in (1, 2, 3, 4, 8, 64, 4096) if a <= d]
+    saved = os.environ.get("HSK_SJLT_XP")
+    try:
+        for xp in (None, "0", "1"):
+            if xp is None:
+                os.environ.pop("HSK_SJLT_XP", None)
+            else:
+                os.environ["HSK_SJLT_XP"] = xp
+            assert lib.hsk_tuning_reload() == 0
+            for n, d, a in shapes:
+                for flags in (0, 1):
+                    nbytes = lib.hsk_sjlt_plan_bytes_ex(n, d, a, flags)
+                    paired = flags and d % 64 == 0 and a * 8 == d
+                    per_dir = n * (a // 2 if paired else a) * 4
+                    assert nbytes >= 2 * per_dir, (xp, n, d, a, flags, nbytes)
+                    assert nbytes <= 2 * (8 * per_dir + 64 * (n + 4096) + (1 << 22)), (xp, n, d, a, flags, nbytes)
+    finally:
+        if saved is None:
+            os.environ.pop("HSK_SJLT_XP", None)
+        else:
+            os.environ["HSK_SJLT_XP"] = saved
+        lib.hsk_tuning_reload()
+    assert lib.hsk_tuning_generation() == gen0 + 4
