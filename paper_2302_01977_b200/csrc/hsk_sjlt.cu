@@ -65,6 +65,23 @@ constexpr int kXposeProducers = HSK_XPOSE_PRODUCERS;
 #define HSK_XP2_PRODUCERS 4
 #endif
 constexpr int kXp2Producers = HSK_XP2_PRODUCERS;
+// ... of 128-row tiles (their 4 x 4 accumulator blocks leave the registers for 24 warps)
+#ifndef HSK_XP2_WIDE_DB
+#define HSK_XP2_WIDE_DB 0
+#endif
+#ifndef HSK_XP2_PRODUCERS4
+#define HSK_XP2_PRODUCERS4 8
+#endif
+constexpr int kXp2Producers4 = HSK_XP2_PRODUCERS4;
+// (128-row tiles' 4 x 4 accumulator blocks leave the registers for 24 warps: eight producer
+// warps measured 4-7 % faster than four -- n = 16384 d = 64 alpha = 4 S' 0.517 -> 0.493 ms,
+// n = 65536 8.16 -> 7.65; 64-row tiles' 2 x 16 need the 96 registers of 20 warps, and 2 x 8
+// (HSK_XP2_WIDE_DB=8) gains under 2 % from eight)
+constexpr int xp2_pw(int rpt, int db) { return rpt == 4 || db <= HSK_XP2_WIDE_DB ? kXp2Producers4 : kXp2Producers; }
+// mode 6 copy mapping: consecutive inputs per warp instruction (x 32 / KQ rows)
+#ifndef HSK_XP6_KQ
+#define HSK_XP6_KQ 4
+#endif
 
 // TMA multicast across slab clusters (opt-in at build time and run time,
 // -DHSK_SJLT_MULTICAST=1 plus HSK_SJLT_MC=1): measured slower (see launch<>),
@@ -687,17 +704,31 @@ __device__ __forceinline__ void issue_coop(const ApplyArgs &p, const Ring &R, in
     double *sx = reinterpret_cast<double *>(st);
     const int nel = p.tk * TM;
     if (XP2) {
-        // mode 6 (unaligned A): (kk, rr) = A[k0+kk, r0+rr] -> sx[kk*TM + rr], the
-        // dense S layout; lanes along kk (coalesced reads; the strided writes
-        // conflict -- the rare odd-ld path)
+        // mode 6 (unaligned A):
+        // (kk, rr) = A[k0+kk, r0+rr] -> sx[kk*TM + rr], the dense S layout.  A warp copies 4 consecutive inputs x 8 consecutive rows
+        // per instruction: every 32-byte sector it reads is used whole, and its
+        // stores are four 64-byte runs (2-way conflicts; lanes along kk alone
+        // would put all 32 stores on one bank pair)
         const int tk = p.tk;
-        for (int kk = ptid; kk < tk; kk += pnt) {
-            const double *src = p.A + r0 * p.lda + k0 + kk;
-            double *dbase = sx + kk * TM;
-            const bool vk = kk < kc;
-            for (int rr = 0; rr < TM; ++rr, src += p.lda) {
-                const bool v = vk && (r0 + rr < p.m_out);
-                cp_async8(dbase + rr, v ? src : p.A, v);
+        constexpr int KQ = HSK_XP6_KQ, RQ = 32 / KQ;  // inputs x rows per warp instruction
+        const int kq = ptid % KQ, rq = (ptid / KQ) % RQ, pw = ptid >> 5, npw = pnt >> 5;
+        const int nkg = (tk + KQ - 1) / KQ;
+        const bool full_rows = r0 + TM <= p.m_out;
+        for (int kg = pw; kg < nkg; kg += npw) {
+            const int kk = kg * KQ + kq;
+            if (kk >= tk) continue;
+            const double *src = p.A + (r0 + rq) * p.lda + k0 + kk;
+            double *dst = sx + kk * TM + rq;
+            const int64_t step = (int64_t)RQ * p.lda;
+            if (kk < kc && full_rows) {
+#pragma unroll
+                for (int rg = 0; rg < TM / RQ; ++rg, src += step, dst += RQ) cp_async8(dst, src, true);
+            } else {
+                const bool vk = kk < kc;
+                for (int rg = 0; rg < TM / RQ; ++rg, src += step, dst += RQ) {
+                    const bool v = vk && (r0 + rq + rg * RQ < p.m_out);
+                    cp_async8(dst, v ? src : p.A, v);
+                }
             }
         }
     } else if (XPOSE) {
@@ -950,7 +981,7 @@ __device__ __noinline__ void sk_post_flag(int *flag, int pub) {
 // 5 / 6): the producer side is S' (tensor map, chunk coordinates), the consumer
 // side -- walker, lane -> row mapping, epilogue -- is S's.
 template <int RPT, int DB, int NW, bool TRANS, bool PROD, bool SK, bool PAIR, bool XP2 = false>
-__global__ void __launch_bounds__((NW + (PROD ? (XP2 ? kXp2Producers : TRANS && RPT == 4 ? kXposeProducers : 1) : 0)) * 32, 1)
+__global__ void __launch_bounds__((NW + (PROD ? (XP2 ? xp2_pw(RPT, DB) : TRANS && RPT == 4 ? kXposeProducers : 1) : 0)) * 32, 1)
     sjlt_apply_kernel(const __grid_constant__ ApplyArgs p, const __grid_constant__ CUtensorMap tmap) {
     static_assert(!XP2 || (TRANS && PROD && (RPT == 2 || RPT == 4)), "xp2 kernels: S' on 64- / 128-row tiles with producer warps");
     constexpr int TM = 32 * RPT;
@@ -961,7 +992,7 @@ __global__ void __launch_bounds__((NW + (PROD ? (XP2 ? kXp2Producers : TRANS && 
     // in acc[.][0..1] and, once the quarters are folded into h = 0, the t2
     // buckets 16p + 8 + c2 in acc[.][2 + c2]; partials published / reduced
     // across CTAs keep the per-warp layout of the unpaired kernels)
-    constexpr int PW = PROD ? (XP2 ? kXp2Producers : XPOSE ? kXposeProducers : 1) : 0;  // dedicated producer warps
+    constexpr int PW = PROD ? (XP2 ? xp2_pw(RPT, DB) : XPOSE ? kXposeProducers : 1) : 0;  // dedicated producer warps
     constexpr int NT = NW * 32;
     constexpr int NJ = PAIR ? 10 : DB;  // accumulator columns in use
     // slot release: lane 0 of each consumer warp arrives (PROD: inline; the
@@ -1063,7 +1094,7 @@ __global__ void __launch_bounds__((NW + (PROD ? (XP2 ? kXp2Producers : TRANS && 
                 for (; issued < nloc && issued < stages; ++issued) issue_tma<TM, TRANS, SK>(p, &tmap, R, issued);
         } else {
             for (; issued < nloc && issued < stages - 1; ++issued)
-                issue_coop<TM, TRANS, XPOSE, SK>(p, R, issued, threadIdx.x, NT);
+                issue_coop<TM, TRANS, XPOSE, SK, XP2>(p, R, issued, threadIdx.x, NT);
         }
     }
 
@@ -1144,7 +1175,7 @@ __global__ void __launch_bounds__((NW + (PROD ? (XP2 ? kXp2Producers : TRANS && 
                 if (!tma && issued < nloc) {
                     const int j = issued;
                     if (j >= stages) mbar_wait(&R.empty[j % stages], (uint32_t)((j / stages) - 1) & 1u);
-                    issue_coop<TM, TRANS, XPOSE, SK>(p, R, j, threadIdx.x, NT);
+                    issue_coop<TM, TRANS, XPOSE, SK, XP2>(p, R, j, threadIdx.x, NT);
                     ++issued;
                 }
             }
@@ -1361,7 +1392,12 @@ static int launch(ApplyArgs a, const Geom &g, cudaStream_t st) {
     // from the last consumer warp to release a slot instead
     bool prod = NW < 32;
     if (tuning().sjlt_prod >= 0) prod = tuning().sjlt_prod == 1;
-    const int pw = xp ? kXp2Producers : a.trans && XPOSE ? kXposeProducers : 1;
+    const int pw = xp ? xp2_pw(RPT, DB) : a.trans && XPOSE ? kXposeProducers : 1;
+    // (mode 6, the 8-byte copies of an unaligned operand, runs at ~1.5 ms on
+    // n = 16384 whoever issues them -- the four producer warps or all consumer
+    // warps, 2 to 32 inputs per warp instruction -- against 0.7-1.0 ms for the
+    // natural / XOR layouts of mode 1: the price of the dense layout on the rare
+    // odd-ld operand; DeviceMatrix pads every leading dimension to even)
     prod = (xp || prod) && (a.mode == 0 || a.mode == 3 || ((a.mode == 1 || a.mode == 4) && XPOSE) || xp) &&
            NW + pw <= 32;
     if (a.mode == 4 && !prod) a.mode = 1;  // the staging transpose needs the producer warps
