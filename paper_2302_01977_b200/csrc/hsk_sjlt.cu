@@ -221,7 +221,8 @@ constexpr int kPairSlab = 64;  // buckets per slab (4 chunk pairs)
 // n = 16384, S' ms natural / transposed: d = 128 alpha = 4 0.536 / 0.494,
 // d = 256 alpha = 8 1.062 / 0.757 (the 11 / 17 pass ratio); not the paired
 // plans (C3: 8.39 / 8.73 -- their walk is issue-bound and loses more to the
-// smaller chunk than the passes save) and not a <= 2 (C2, C5).
+// smaller chunk than the passes save) and not a <= 3 (d = 96 / 192 alpha = 3:
+// 0.418 / 0.443 and 0.436 / 0.466; d = 128 alpha = 2: 0.348 / 0.433; C2, C5).
 // 128-row tiles (d <= 64) always: their earlier producers (mode 4: one staging
 // tile, the transposed XOR layout read with 8-byte loads) measured 7-14 %
 // slower (n = 16384, S' ms: d = 64 alpha = 4 0.558 / 0.515, alpha = 2
